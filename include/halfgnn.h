@@ -1,0 +1,190 @@
+/*
+ * halfgnn.h -- C ABI of the B200 (sm_100a) half-precision GNN hot path.
+ *
+ * One shared library (libhalfgnn.so).  Every entry point:
+ *   - returns int: HG_OK (0), HG_EINVAL (1, bad argument; text in hg_last_error()),
+ *     HG_ECUDA (2, CUDA failure);
+ *   - takes only device pointers, POD sizes and a cudaStream_t (passed as void*);
+ *   - never allocates device memory: scratch is sized by the matching *_workspace
+ *     query and supplied by the caller;
+ *   - is stream-ordered and reentrant (no global mutable state besides the
+ *     thread-local error text).  Graph-construction calls (hg_build_csr,
+ *     hg_schedule_build) synchronise their stream once, because their output
+ *     size is data dependent; the compute calls never synchronise.
+ *
+ * Element types: "half" buffers hold IEEE binary16 bit patterns (uint16_t),
+ * "float" buffers IEEE binary32.  A `dtype` argument selects HG_F16 / HG_F32
+ * for the operators that exist in both precision modes of the reference
+ * (halfsparse DenseTensor modes "half" / "float32").
+ *
+ * Each function cites the reference operator (path:line under the halfsparse
+ * package, pkg/src/halfsparse/) whose behaviour it replaces.
+ */
+#ifndef HALFGNN_H
+#define HALFGNN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HG_ABI_VERSION 1
+
+enum { HG_OK = 0, HG_EINVAL = 1, HG_ECUDA = 2 };
+enum { HG_F16 = 0, HG_F32 = 1 };
+/* kernels.py:50 SCALINGS */
+enum { HG_SCALING_POST = 0, HG_SCALING_PRE = 1, HG_SCALING_DISCRETIZED = 2 };
+/* degree-factor kinds, kernels.py:118-140 ("left"/"right" use 1/d, "both" 1/sqrt(d)) */
+enum { HG_FACTOR_INV = 1, HG_FACTOR_INV_SQRT = 2 };
+
+/* Thread-local text of the last HG_EINVAL / HG_ECUDA. */
+const char* hg_last_error(void);
+int hg_abi_version(void);
+
+/* ---------------------------------------------------------------- graph build */
+
+/* CooGraph.from_edges + coo_to_csr (sparse.py:56-69, 97-101): canonicalise an
+ * unsorted int64 edge list (sort by (row, col), drop duplicates) and emit CSR.
+ * Errors (HG_EINVAL): "negative vertex id", "vertex id out of range".
+ * cols_out / rows_out need capacity num_edges_in; rows_out may be NULL.
+ * *num_edges_out (HOST pointer) receives the deduplicated edge count.
+ * Synchronises `stream`. */
+int hg_build_csr_workspace(int64_t num_edges_in, int64_t n, size_t* bytes);
+int hg_build_csr(const int64_t* rows_in, const int64_t* cols_in, int64_t num_edges_in,
+                 int64_t n, int64_t* offsets_out, int32_t* cols_out, int64_t* rows_out,
+                 int64_t* num_edges_out, void* ws, size_t ws_bytes, void* stream);
+
+/* transpose(g, return_perm=True) + col_degrees (sparse.py:109-125): CSC of a
+ * canonical CSR and the stable permutation perm[new] = old edge id
+ * (np.argsort(col*n+row, kind="stable")). */
+int hg_transpose_workspace(int64_t n, int64_t num_edges, size_t* bytes);
+int hg_transpose(const int64_t* offsets, const int32_t* cols, int64_t n, int64_t num_edges,
+                 int64_t* t_offsets, int32_t* t_cols, int32_t* perm, void* ws,
+                 size_t ws_bytes, void* stream);
+
+/* _degree_factors / _ref_factors (kernels.py:118-140, 583-600): per vertex
+ * rnd(fp32(1)/fp32(d)) or rnd(fp32(1)/sqrtf(fp32(d))), 0 for d == 0; degrees are
+ * offsets[v+1]-offsets[v] (pass CSR offsets for row degrees, CSC for column). */
+int hg_degree_factors(const int64_t* offsets, int64_t n, int kind, int dtype, void* out,
+                      void* stream);
+
+/* ------------------------------------------------------------------ scheduler */
+
+/* Degree-bucketed work units replacing simt.plan_edge_parallel /
+ * plan_vertex_grouped (simt.py:158-201) for the fp32-guarded kernels.
+ * Every row becomes max(1, ceil(deg/split_cap)) units {row, begin, end, slot}
+ * (int32 x4); slot = -1 for a whole row, else the row's fp32 carry slot.
+ * Units are ordered by descending length class floor(log2(len))+1, rows
+ * ascending inside a class (stable).  split_rows receives {row, first_slot,
+ * nparts, 0} for every row with nparts > 1, rows ascending.
+ * Capacities: max_units >= n + ceil(E/split_cap), max_split >= ceil(E/split_cap).
+ * counts_out (HOST int64[3]) = {num_units, num_split_rows, num_slots}.
+ * Synchronises `stream`. */
+int hg_schedule_workspace(int64_t n, int64_t num_edges, int32_t split_cap, size_t* bytes);
+int hg_schedule_build(const int64_t* offsets, int64_t n, int32_t split_cap, int32_t* units,
+                      int64_t max_units, int32_t* split_rows, int64_t max_split,
+                      int64_t* counts_out, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------- SpMM */
+
+/* fp32-guarded row-owned SpMM (the B200 hot kernel for spmm_v / spmm_ve,
+ * kernels.py:394-401; models.spmm_agg / spmm_weighted, models.py:274-314).
+ *   S[r] = sum_{e in row r} m_e * X'[cols[e]]   (fp32 accumulation),
+ *   X'   = rnd(X * in_scale[:, None])          (in_scale may be NULL),
+ *   m_e  = 1, or w[(w_index ? w_index[e] : e) * heads + head(f)] when w != NULL,
+ *   head(f) = f / (F / heads).
+ *   post:               y = rnd(rnd(S) * out_factor)   (keeps fp16 overflow of raw sums)
+ *   pre / discretized:  y = rnd(S * out_factor)        (one rounding)
+ *   out_factor NULL:    y = rnd(S)
+ * Rows are local (n_rows, offsets rebased to 0); cols index X's n_cols rows, so
+ * a row partition runs unchanged on all-gathered features.  Heavy rows are
+ * split into units with fp32 carry slots merged in slot order by a follow-up
+ * pass: no atomics, bitwise deterministic. */
+int hg_spmm_workspace(int64_t n_cols, int32_t F, int64_t num_slots, int has_in_scale,
+                      int dtype, size_t* bytes);
+int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_rows, int64_t n_cols,
+            int64_t num_edges, const int32_t* units, int64_t num_units,
+            const int32_t* split_rows, int64_t num_split_rows, int64_t num_slots,
+            const void* w, const int32_t* w_index, int32_t heads, const void* x, void* y,
+            int32_t F, int32_t scaling, const void* in_scale, const void* out_factor,
+            int dtype, void* ws, size_t ws_bytes, void* stream);
+
+/* Reference-order SpMM, bit-exact with halfsparse _spmm_edge_parallel
+ * (kernels.py:328-391; order spelled out in _ref_spmm_edge, kernels.py:603-688):
+ * warp w owns edges [w*warp_chunk, ...), CTA c owns warps [c*warps_per_cta, ...);
+ * per-segment fused folds (discretized batches of k = subwarp_layout(F).subwarps),
+ * adjacent-pair chain trees inside a CTA, one carry per CTA folded in CTA
+ * order by a follow-up pass, then post scaling.  staging_partials
+ * ([num_ctas*F], dtype) / staging_rows ([num_ctas] int64) receive the carry-out
+ * slots (StagingBuffer, kernels.py:70-87); both may be NULL. */
+int hg_spmm_edge_ref_workspace(int64_t n_cols, int64_t num_edges, int32_t F,
+                               int32_t warp_chunk, int32_t warps_per_cta, int has_in_scale,
+                               int dtype, size_t* bytes);
+int hg_spmm_edge_ref(const int64_t* offsets, const int32_t* cols, int64_t n_rows,
+                     int64_t n_cols, int64_t num_edges, int32_t warp_chunk,
+                     int32_t warps_per_cta, const void* w, const void* x, void* y, int32_t F,
+                     int32_t scaling, const void* in_scale, const void* out_factor,
+                     void* staging_partials, int64_t* staging_rows, int dtype, void* ws,
+                     size_t ws_bytes, void* stream);
+
+/* Vertex-grouped SpMMv, bit-exact with spmm_vertex_grouped (kernels.py:463-559):
+ * <=32-slot neighbour groups folded sequentially, discretized partial
+ * rnd(acc*f_r), ascending merge, post scaling.  If staging_partials != NULL,
+ * group_base[r] (int64, exclusive scan of the group counts of rows with more
+ * than one group) places row r's partials at staging_partials[group_base[r]+g]. */
+int hg_spmm_vertex_ref_workspace(int64_t n_cols, int32_t F, int has_in_scale, int dtype,
+                                 size_t* bytes);
+int hg_spmm_vertex_ref(const int64_t* offsets, const int32_t* cols, int64_t n_rows,
+                       int64_t n_cols, const void* x, void* y, int32_t F, int32_t scaling,
+                       const void* in_scale, const void* out_factor,
+                       const int64_t* group_base, void* staging_partials,
+                       int64_t* staging_rows, int dtype, void* ws, size_t ws_bytes,
+                       void* stream);
+
+/* --------------------------------------------------------------- SDDMM & GAT */
+
+/* sddmm (kernels.py:407-455), per head: out[e*heads+h] = tree-dot of
+ * X[row(e), h*fh:(h+1)*fh] and Y[cols[e], ...], fh = F/heads: products rounded
+ * one by one, adjacent pairs summed, adjacent-pair tree with pass-through.
+ * Bit-exact.  Uses the hg_schedule_build units (slots ignored). */
+int hg_sddmm(const int64_t* offsets, const int32_t* cols, int64_t n_rows, int64_t num_edges,
+             const int32_t* units, int64_t num_units, const void* x, const void* y,
+             void* out, int32_t F, int32_t heads, int dtype, void* stream);
+
+/* attention_scores + leaky_relu (models.py:317-326, 188-200), per head:
+ * e = rnd(s_l[row] + s_r[col]); out = e > 0 ? e : rnd(e * slope) (slope in fp64). */
+int hg_attn_scores(const int64_t* offsets, const int32_t* cols, int64_t n_rows,
+                   int64_t num_edges, const void* s_l, const void* s_r, int32_t heads,
+                   double slope, void* out, int dtype, void* stream);
+
+/* edge_softmax forward (models.py:382-402): per row and head, m = max,
+ * s = rnd(e-m), ex = rnd(exp(s)), den = adjacent-pair tree of ex in CSR order,
+ * alpha = rnd(ex/den).  Bit-exact. */
+int hg_edge_softmax_fwd(const int64_t* offsets, int64_t n_rows, int64_t num_edges,
+                        const void* e, void* alpha, int32_t heads, int dtype, void* stream);
+/* edge_softmax backward (models.py:403-410): prod = rnd(alpha*g),
+ * s = tree-sum(prod), de = rnd(alpha*rnd(g - s)).  Bit-exact. */
+int hg_edge_softmax_bwd(const int64_t* offsets, int64_t n_rows, int64_t num_edges,
+                        const void* alpha, const void* grad, void* de, int32_t heads,
+                        int dtype, void* stream);
+
+/* Row sums of per-edge values (attention_scores backward, models.py:329-337),
+ * fp32 accumulation, one rounding: out[r*heads+h] = rnd(sum_e v[idx(e)*heads+h]),
+ * idx(e) = perm ? perm[e] : e (perm turns a CSC walk into column sums). */
+int hg_edge_rowsum(const int64_t* offsets, int64_t n_rows, int64_t num_edges,
+                   const void* vals, const int32_t* perm, int32_t heads, void* out,
+                   int dtype, void* stream);
+
+/* ---------------------------------------------------------------- elementwise */
+
+/* out = rnd(x * s) with the product formed in fp64 (the reference multiplies
+ * fp16/fp32 values by Python floats in float64: leaky_relu slope,
+ * scale_combine lam, models.py:188-240). */
+int hg_scale_f64(const void* x, double s, void* out, int64_t count, int dtype, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HALFGNN_H */

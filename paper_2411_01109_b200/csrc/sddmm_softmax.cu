@@ -1,0 +1,457 @@
+// SDDMM, GAT attention scores and edge softmax (forward/backward) for sm_100a.
+// All of these reproduce the reference's rounding sequence bit for bit:
+//   sddmm           kernels.py:407-455 (products rounded, pair sums, adjacent-pair tree)
+//   attention       models.py:317-326 + leaky_relu 188-200
+//   edge softmax    models.py:382-412 (row max, rnd(exp), tree sum, rnd(ex/den))
+// The adjacent-pair tree with pass-through of a lone right-most element is the
+// implicit binary tree over power-of-two aligned index ranges; warps evaluate it
+// with predicated shuffle-down levels and combine 32-element block roots with a
+// binary-counter stack, so any row length reproduces the same tree.
+#include "hg_common.cuh"
+
+namespace hg {
+
+template <int BYTES> struct RawV;
+template <> struct RawV<16> { using type = uint4; };
+template <> struct RawV<4> { using type = uint32_t; };
+template <> struct RawV<8> { using type = uint2; };
+
+// ------------------------------------------------------------------- SDDMM
+
+// Tree value of one V-element chunk: per-pair sums v_i = rnd(rnd(x0*y0) + rnd(x1*y1)),
+// then the adjacent-pair tree over the V/2 sums (a power of two: all present).
+template <typename T, int V>
+__device__ __forceinline__ T chunk_dot(const typename RawV<V * sizeof(T)>::type& xr,
+                                       const typename RawV<V * sizeof(T)>::type& yr) {
+  using N = Num<T>;
+  const T* xa = reinterpret_cast<const T*>(&xr);
+  const T* ya = reinterpret_cast<const T*>(&yr);
+  T v[V / 2];
+#pragma unroll
+  for (int i = 0; i < V / 2; ++i)
+    v[i] = N::add(N::mul(xa[2 * i], ya[2 * i]), N::mul(xa[2 * i + 1], ya[2 * i + 1]));
+#pragma unroll
+  for (int s = 1; s < V / 2; s <<= 1)
+#pragma unroll
+    for (int i = 0; i + s < V / 2; i += 2 * s) v[i] = N::add(v[i], v[i + s]);
+  return v[0];
+}
+
+template <typename T>
+__device__ __forceinline__ T shfl_down_t(unsigned mask, T v, int s, int width) {
+  if constexpr (sizeof(T) == 2) {
+    unsigned short b = __half_as_ushort(v);
+    return __ushort_as_half((unsigned short)__shfl_down_sync(mask, (unsigned)b, s, width));
+  } else {
+    return __shfl_down_sync(mask, v, s, width);
+  }
+}
+
+// Team of TEAM lanes per unit (row slice); lane owns chunks c = tl + k*TEAM of V
+// elements; lph = chunks per head (fh / V).  Requires lph % 32 == 0 or 32 % lph == 0
+// when NCH > 1.
+template <typename T, int V, int TEAM, int NCH>
+__global__ void __launch_bounds__(256)
+k_sddmm(const int4* __restrict__ units, int64_t num_units, const int32_t* __restrict__ cols,
+        const T* __restrict__ x, const T* __restrict__ y, T* __restrict__ out, int F, int heads) {
+  using N = Num<T>;
+  using Raw = typename RawV<V * sizeof(T)>::type;
+  constexpr int EB = 4;
+  const int lane = threadIdx.x & 31;
+  const int tl = lane & (TEAM - 1);
+  const unsigned tmask =
+      TEAM == 32 ? 0xffffffffu : (((1u << TEAM) - 1u) << (lane & ~(TEAM - 1)));
+  const int64_t team = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TEAM;
+  if (team >= num_units) return;
+  const int4 un = units[team];
+  const int row = un.x, beg = un.y, end = un.z;
+  const int fh = F / heads, lph = fh / V, nvec = F / V;
+
+  Raw xr[NCH];
+  bool cval[NCH];
+  int q[NCH], hd[NCH];
+#pragma unroll
+  for (int k = 0; k < NCH; ++k) {
+    const int c = tl + k * TEAM;
+    cval[k] = c < nvec;
+    hd[k] = c / lph;
+    q[k] = c - hd[k] * lph;
+    if (cval[k]) xr[k] = *reinterpret_cast<const Raw*>(x + (int64_t)row * F + c * V);
+  }
+  for (int64_t base = beg; base < end; base += EB) {
+    int cj[EB];
+    Raw yr[EB][NCH];
+#pragma unroll
+    for (int j = 0; j < EB; ++j) {
+      const int64_t e = base + j;
+      cj[j] = e < end ? __ldg(cols + e) : 0;
+#pragma unroll
+      for (int k = 0; k < NCH; ++k)
+        if (e < end && cval[k])
+          yr[j][k] = __ldg(reinterpret_cast<const Raw*>(y + (int64_t)cj[j] * F + (tl + k * TEAM) * V));
+    }
+#pragma unroll
+    for (int j = 0; j < EB; ++j) {
+      const int64_t e = base + j;
+      if (e >= end) break;  // uniform across the team
+      T part[NCH];
+#pragma unroll
+      for (int k = 0; k < NCH; ++k) part[k] = cval[k] ? chunk_dot<T, V>(xr[k], yr[j][k]) : N::zero();
+      // shuffle levels inside each k-slice (q and q+s share the slice)
+#pragma unroll
+      for (int s = 1; s < TEAM; s <<= 1) {
+#pragma unroll
+        for (int k = 0; k < NCH; ++k) {
+          const T o = shfl_down_t(tmask, part[k], s, TEAM);
+          if ((q[k] & (2 * s - 1)) == 0 && q[k] + s < lph && (tl + s) < TEAM) part[k] = N::add(part[k], o);
+        }
+      }
+      // levels across k-slices (heads wider than one slice: lph multiple of TEAM)
+      if (NCH > 1 && lph > TEAM) {
+        const int spr = lph / TEAM;  // slices per head
+#pragma unroll
+        for (int s = 1; s < NCH; s <<= 1)
+#pragma unroll
+          for (int k = 0; k + s < NCH; k += 2 * s)
+            if ((k % spr) % (2 * s) == 0 && (k % spr) + s < spr) part[k] = N::add(part[k], part[k + s]);
+      }
+#pragma unroll
+      for (int k = 0; k < NCH; ++k)
+        if (cval[k] && q[k] == 0) out[e * heads + hd[k]] = part[k];
+    }
+  }
+}
+
+}  // namespace hg
+
+using namespace hg;
+
+template <typename T, int V, int TEAM, int NCH>
+static int launch_sddmm(const int4* units, int64_t nu, const int32_t* cols, const void* x,
+                        const void* y, void* out, int F, int heads, cudaStream_t st) {
+  constexpr int tpb = 256 / TEAM;
+  if (nu == 0) return HG_OK;
+  k_sddmm<T, V, TEAM, NCH><<<(unsigned)((nu + tpb - 1) / tpb), 256, 0, st>>>(
+      units, nu, cols, (const T*)x, (const T*)y, (T*)out, F, heads);
+  HG_LAUNCHED();
+  return HG_OK;
+}
+
+template <typename T, int V>
+static int dispatch_sddmm(const int4* units, int64_t nu, const int32_t* cols, const void* x,
+                          const void* y, void* out, int F, int heads, cudaStream_t st) {
+  const int nvec = F / V, lph = F / heads / V;
+#define HG_SD(TM, NC) return launch_sddmm<T, V, TM, NC>(units, nu, cols, x, y, out, F, heads, st)
+  if (nvec <= 1) HG_SD(1, 1);
+  if (nvec <= 2) HG_SD(2, 1);
+  if (nvec <= 4) HG_SD(4, 1);
+  if (nvec <= 8) HG_SD(8, 1);
+  if (nvec <= 16) HG_SD(16, 1);
+  if (nvec <= 32) HG_SD(32, 1);
+  HG_REQUIRE(lph % 32 == 0 || 32 % lph == 0,
+             "hg_sddmm: head width %d does not tile 32-lane slices", F / heads);
+  HG_REQUIRE(nvec % 32 == 0, "hg_sddmm: feature length %d unsupported", F);
+  if (nvec <= 64) HG_SD(32, 2);
+  if (nvec <= 128) HG_SD(32, 4);
+  if (nvec <= 256) HG_SD(32, 8);
+#undef HG_SD
+  HG_REQUIRE(false, "hg_sddmm: feature length %d too large", F);
+}
+
+extern "C" int hg_sddmm(const int64_t* offsets, const int32_t* cols, int64_t n_rows,
+                        int64_t num_edges, const int32_t* units, int64_t num_units,
+                        const void* x, const void* y, void* out, int32_t F, int32_t heads,
+                        int dtype, void* stream) {
+  (void)offsets; (void)n_rows; (void)num_edges;
+  HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
+  HG_REQUIRE(F > 0 && F % 2 == 0, "feature length %d must be even and positive", F);
+  HG_REQUIRE(heads >= 1 && F % heads == 0 && (F / heads) % 2 == 0,
+             "feature length %d does not split into %d even heads", F, heads);
+  cudaStream_t st = as_stream(stream);
+  const int fh = F / heads;
+  const int4* u = reinterpret_cast<const int4*>(units);
+  const bool aligned = reinterpret_cast<uintptr_t>(x) % 16 == 0 && reinterpret_cast<uintptr_t>(y) % 16 == 0;
+  if (dtype == HG_F16) {
+    if (aligned && fh % 8 == 0) return dispatch_sddmm<__half, 8>(u, num_units, cols, x, y, out, F, heads, st);
+    return dispatch_sddmm<__half, 2>(u, num_units, cols, x, y, out, F, heads, st);
+  }
+  if (aligned && fh % 4 == 0) return dispatch_sddmm<float, 4>(u, num_units, cols, x, y, out, F, heads, st);
+  return dispatch_sddmm<float, 2>(u, num_units, cols, x, y, out, F, heads, st);
+}
+
+// --------------------------------------------------------- attention scores
+
+namespace hg {
+
+// Edge-parallel: 256 consecutive edges per block, rows located by a block-local
+// binary search between the block's first and last rows.
+template <typename T>
+__global__ void k_attn_scores(const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
+                              int64_t n_rows, int64_t num_edges, const T* __restrict__ sl,
+                              const T* __restrict__ sr, int heads, double slope,
+                              T* __restrict__ out) {
+  using N = Num<T>;
+  __shared__ int64_t rng[2];
+  const int64_t e0 = (int64_t)blockIdx.x * blockDim.x;
+  if (e0 >= num_edges) return;
+  const int64_t elast = e0 + blockDim.x - 1 < num_edges ? e0 + blockDim.x - 1 : num_edges - 1;
+  if (threadIdx.x == 0) rng[0] = row_of_edge(offsets, n_rows, e0);
+  if (threadIdx.x == 1 || blockDim.x == 1) rng[1] = row_of_edge(offsets, n_rows, elast);
+  __syncthreads();
+  const int64_t e = e0 + threadIdx.x;
+  if (e >= num_edges) return;
+  int64_t lo = rng[0], hi = rng[1] + 1;  // answer in [lo, hi)
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (offsets[mid] <= e) lo = mid; else hi = mid;
+  }
+  const int64_t r = lo, c = cols[e];
+  for (int h = 0; h < heads; ++h) {
+    const T s = N::add(sl[r * heads + h], sr[c * heads + h]);
+    out[e * heads + h] = N::gt0(s) ? s : N::from_d(N::to_d(s) * slope);
+  }
+}
+
+// ------------------------------------------------------------ edge softmax
+
+// Adjacent-pair tree over a row's values, evaluated 32 at a time.
+template <typename T>
+struct RowTree {
+  T stk[40];
+  int64_t blocks = 0;
+  // v: lane's element of the block starting at `base`; valid iff base + lane < len.
+  __device__ __forceinline__ void push(T v, int64_t base, int64_t len, int lane) {
+    using N = Num<T>;
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+      const T o = shfl_down_t(0xffffffffu, v, s, 32);
+      if ((lane & (2 * s - 1)) == 0 && base + lane + s < len) v = N::add(v, o);
+    }
+    T cur = shfl_t(v);
+    int64_t t = blocks;
+    int lvl = 0;
+    while (t & 1) {
+      cur = N::add(stk[lvl], cur);
+      t >>= 1;
+      ++lvl;
+    }
+    stk[lvl] = cur;
+    ++blocks;
+  }
+  __device__ __forceinline__ T root() const {
+    using N = Num<T>;
+    T acc = N::zero();
+    bool have = false;
+    for (int lvl = 0; lvl < 40; ++lvl) {
+      if ((blocks >> lvl) & 1) {
+        acc = have ? N::add(stk[lvl], acc) : stk[lvl];
+        have = true;
+      }
+    }
+    return acc;
+  }
+  static __device__ __forceinline__ T shfl_t(T v) {
+    if constexpr (sizeof(T) == 2)
+      return __ushort_as_half((unsigned short)__shfl_sync(0xffffffffu, (unsigned)__half_as_ushort(v), 0));
+    else
+      return __shfl_sync(0xffffffffu, v, 0);
+  }
+};
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, s));
+  return v;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_softmax_fwd(const int64_t* __restrict__ offsets, int64_t n_rows, const T* __restrict__ e,
+              T* __restrict__ alpha, int heads) {
+  using N = Num<T>;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows;
+       r += nwarps) {
+    const int64_t beg = offsets[r], len = offsets[r + 1] - beg;
+    if (len == 0) continue;
+    for (int h = 0; h < heads; ++h) {
+      float m = -INFINITY;
+      bool nan = false;
+      for (int64_t i = lane; i < len; i += 32) {
+        const float v = N::to_f(e[(beg + i) * heads + h]);
+        nan |= v != v;
+        m = fmaxf(m, v);
+      }
+      m = warp_max(m);
+      nan = __any_sync(0xffffffffu, nan);
+      const T mt = nan ? N::from_f(NAN) : N::from_f(m);  // np.maximum propagates NaN
+      RowTree<T> tree;
+      for (int64_t b = 0; b < len; b += 32) {
+        const int64_t i = b + lane;
+        T ex = N::zero();
+        if (i < len) {
+          const T s = N::sub(e[(beg + i) * heads + h], mt);
+          ex = N::from_d(exp(N::to_d(s)));
+          alpha[(beg + i) * heads + h] = ex;
+        }
+        tree.push(ex, b, len, lane);
+      }
+      const double den = N::to_d(tree.root());
+      for (int64_t i = lane; i < len; i += 32) {
+        const int64_t k = (beg + i) * heads + h;
+        alpha[k] = N::from_d(N::to_d(alpha[k]) / den);
+      }
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_softmax_bwd(const int64_t* __restrict__ offsets, int64_t n_rows, const T* __restrict__ alpha,
+              const T* __restrict__ g, T* __restrict__ de, int heads) {
+  using N = Num<T>;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows;
+       r += nwarps) {
+    const int64_t beg = offsets[r], len = offsets[r + 1] - beg;
+    if (len == 0) continue;
+    for (int h = 0; h < heads; ++h) {
+      RowTree<T> tree;
+      for (int64_t b = 0; b < len; b += 32) {
+        const int64_t i = b + lane;
+        T p = N::zero();
+        if (i < len) {
+          const int64_t k = (beg + i) * heads + h;
+          p = N::mul(alpha[k], g[k]);
+        }
+        tree.push(p, b, len, lane);
+      }
+      const T s = tree.root();
+      for (int64_t i = lane; i < len; i += 32) {
+        const int64_t k = (beg + i) * heads + h;
+        de[k] = N::mul(alpha[k], N::sub(g[k], s));
+      }
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_edge_rowsum(const int64_t* __restrict__ offsets, int64_t n_rows, const T* __restrict__ v,
+              const int32_t* __restrict__ perm, int heads, T* __restrict__ out) {
+  using N = Num<T>;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows;
+       r += nwarps) {
+    const int64_t beg = offsets[r], end = offsets[r + 1];
+    for (int h = 0; h < heads; ++h) {
+      float s = 0.0f;
+      for (int64_t i = beg + lane; i < end; i += 32) {
+        const int64_t idx = perm ? (int64_t)perm[i] : i;
+        s += N::to_f(v[idx * heads + h]);
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) out[r * heads + h] = N::from_f(s);
+    }
+  }
+}
+
+template <typename T>
+__global__ void k_scale_f64(const T* __restrict__ x, double s, T* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = Num<T>::from_d(Num<T>::to_d(x[i]) * s);
+}
+
+}  // namespace hg
+
+extern "C" int hg_attn_scores(const int64_t* offsets, const int32_t* cols, int64_t n_rows,
+                              int64_t num_edges, const void* s_l, const void* s_r,
+                              int32_t heads, double slope, void* out, int dtype, void* stream) {
+  HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
+  HG_REQUIRE(heads >= 1, "heads must be positive");
+  if (num_edges == 0) return HG_OK;
+  cudaStream_t st = as_stream(stream);
+  const unsigned g = (unsigned)((num_edges + 255) / 256);
+  if (dtype == HG_F16)
+    k_attn_scores<__half><<<g, 256, 0, st>>>(offsets, cols, n_rows, num_edges, (const __half*)s_l,
+                                             (const __half*)s_r, heads, slope, (__half*)out);
+  else
+    k_attn_scores<float><<<g, 256, 0, st>>>(offsets, cols, n_rows, num_edges, (const float*)s_l,
+                                            (const float*)s_r, heads, slope, (float*)out);
+  HG_LAUNCHED();
+  return HG_OK;
+}
+
+extern "C" int hg_edge_softmax_fwd(const int64_t* offsets, int64_t n_rows, int64_t num_edges,
+                                   const void* e, void* alpha, int32_t heads, int dtype,
+                                   void* stream) {
+  (void)num_edges;
+  HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
+  HG_REQUIRE(heads >= 1, "heads must be positive");
+  if (n_rows == 0) return HG_OK;
+  cudaStream_t st = as_stream(stream);
+  const int g = grid_for(n_rows, 8, 148 * 64);
+  if (dtype == HG_F16)
+    k_softmax_fwd<__half><<<g, 256, 0, st>>>(offsets, n_rows, (const __half*)e, (__half*)alpha, heads);
+  else
+    k_softmax_fwd<float><<<g, 256, 0, st>>>(offsets, n_rows, (const float*)e, (float*)alpha, heads);
+  HG_LAUNCHED();
+  return HG_OK;
+}
+
+extern "C" int hg_edge_softmax_bwd(const int64_t* offsets, int64_t n_rows, int64_t num_edges,
+                                   const void* alpha, const void* grad, void* de, int32_t heads,
+                                   int dtype, void* stream) {
+  (void)num_edges;
+  HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
+  HG_REQUIRE(heads >= 1, "heads must be positive");
+  if (n_rows == 0) return HG_OK;
+  cudaStream_t st = as_stream(stream);
+  const int g = grid_for(n_rows, 8, 148 * 64);
+  if (dtype == HG_F16)
+    k_softmax_bwd<__half><<<g, 256, 0, st>>>(offsets, n_rows, (const __half*)alpha,
+                                             (const __half*)grad, (__half*)de, heads);
+  else
+    k_softmax_bwd<float><<<g, 256, 0, st>>>(offsets, n_rows, (const float*)alpha,
+                                            (const float*)grad, (float*)de, heads);
+  HG_LAUNCHED();
+  return HG_OK;
+}
+
+extern "C" int hg_edge_rowsum(const int64_t* offsets, int64_t n_rows, int64_t num_edges,
+                              const void* vals, const int32_t* perm, int32_t heads, void* out,
+                              int dtype, void* stream) {
+  (void)num_edges;
+  HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
+  HG_REQUIRE(heads >= 1, "heads must be positive");
+  if (n_rows == 0) return HG_OK;
+  cudaStream_t st = as_stream(stream);
+  const int g = grid_for(n_rows, 8, 148 * 64);
+  if (dtype == HG_F16)
+    k_edge_rowsum<__half><<<g, 256, 0, st>>>(offsets, n_rows, (const __half*)vals, perm, heads,
+                                             (__half*)out);
+  else
+    k_edge_rowsum<float><<<g, 256, 0, st>>>(offsets, n_rows, (const float*)vals, perm, heads,
+                                            (float*)out);
+  HG_LAUNCHED();
+  return HG_OK;
+}
+
+extern "C" int hg_scale_f64(const void* x, double s, void* out, int64_t count, int dtype,
+                            void* stream) {
+  HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
+  if (count == 0) return HG_OK;
+  cudaStream_t st = as_stream(stream);
+  const int g = grid_for(count, 256, 148 * 16);
+  if (dtype == HG_F16)
+    k_scale_f64<__half><<<g, 256, 0, st>>>((const __half*)x, s, (__half*)out, count);
+  else
+    k_scale_f64<float><<<g, 256, 0, st>>>((const float*)x, s, (float*)out, count);
+  HG_LAUNCHED();
+  return HG_OK;
+}

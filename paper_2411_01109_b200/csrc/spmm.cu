@@ -1,0 +1,693 @@
+// SpMM family for sm_100a.
+//
+//  * k_spmm_fast       fp32-guarded, row-owned: one lane team per work unit
+//                      (hg_schedule_build), 128-bit gathers of neighbour rows,
+//                      fp32 accumulation, one rounding at the row; heavy rows
+//                      split into units whose fp32 carries are merged by
+//                      k_spmm_fast_followup in slot order (no atomics).
+//  * k_spmm_edge_ref   bit-exact replica of halfsparse's edge-parallel order
+//                      (kernels.py:328-391 / _ref_spmm_edge 603-688).
+//  * k_spmm_vertex_ref bit-exact replica of spmm_vertex_grouped (463-559).
+#include "hg_common.cuh"
+
+namespace hg {
+
+template <int BYTES> struct RawVec;
+template <> struct RawVec<16> { using type = uint4; };
+template <> struct RawVec<8> { using type = uint2; };
+template <> struct RawVec<4> { using type = uint32_t; };
+
+// Convert a raw 16/8/4-byte vector of V elements of T to floats.
+template <typename T, int V>
+__device__ __forceinline__ void raw_to_float(const typename RawVec<V * sizeof(T)>::type& r,
+                                             float (&f)[V]) {
+  if constexpr (sizeof(T) == 2) {
+    const __half2* h = reinterpret_cast<const __half2*>(&r);
+#pragma unroll
+    for (int i = 0; i < V / 2; ++i) {
+      float2 t = __half22float2(h[i]);
+      f[2 * i] = t.x;
+      f[2 * i + 1] = t.y;
+    }
+  } else {
+    const float* p = reinterpret_cast<const float*>(&r);
+#pragma unroll
+    for (int i = 0; i < V; ++i) f[i] = p[i];
+  }
+}
+
+// fmode: 0 -> rnd(S); 1 -> post: rnd(rnd(S) * f) for f > 0; 2 -> rnd(S * f)
+template <typename T>
+__device__ __forceinline__ T finalize(float s, int fmode, T fo) {
+  if (fmode == 0) return Num<T>::from_f(s);
+  if (fmode == 1) {
+    T h = Num<T>::from_f(s);
+    return Num<T>::gt0(fo) ? Num<T>::mul(h, fo) : h;
+  }
+  return Num<T>::from_f(s * Num<T>::to_f(fo));
+}
+
+template <typename T, int V>
+__device__ __forceinline__ void store_out(T* dst, const float (&acc)[V], int fmode, T fo) {
+  using Raw = typename RawVec<V * sizeof(T)>::type;
+  Raw r;
+  T* p = reinterpret_cast<T*>(&r);
+#pragma unroll
+  for (int i = 0; i < V; ++i) p[i] = finalize<T>(acc[i], fmode, fo);
+  *reinterpret_cast<Raw*>(dst) = r;
+}
+
+template <int V>
+__device__ __forceinline__ void store_carry(float* dst, const float (&acc)[V]) {
+  if constexpr (V % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < V; i += 4)
+      *reinterpret_cast<float4*>(dst + i) = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+  } else if constexpr (V == 2) {
+    *reinterpret_cast<float2*>(dst) = make_float2(acc[0], acc[1]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; ++i) dst[i] = acc[i];
+  }
+}
+
+// Load CPL consecutive int32 starting at element index lo (possibly partially
+// outside [0, limit)); out-of-range entries become 0.
+template <int CPL>
+__device__ __forceinline__ void load_idx(const int32_t* __restrict__ base, int64_t lo, int64_t limit,
+                                         int (&out)[CPL]) {
+  if (lo >= 0 && lo + CPL <= limit) {
+    const int32_t* p = base + lo;
+    if constexpr (CPL == 1) {
+      out[0] = __ldcs(p);
+    } else if constexpr (CPL == 2) {
+      int2 v = __ldcs(reinterpret_cast<const int2*>(p));
+      out[0] = v.x; out[1] = v.y;
+    } else {
+#pragma unroll
+      for (int q = 0; q < CPL; q += 4) {
+        int4 v = __ldcs(reinterpret_cast<const int4*>(p + q));
+        out[q] = v.x; out[q + 1] = v.y; out[q + 2] = v.z; out[q + 3] = v.w;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      int64_t i = lo + q;
+      out[q] = (i >= 0 && i < limit) ? __ldcs(base + i) : 0;
+    }
+  }
+}
+
+// ------------------------------------------------------------- fast kernel
+
+template <typename T, int V, int TEAM, int NCH, bool WEIGHTED>
+__global__ void __launch_bounds__(256)
+k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __restrict__ cols,
+            int64_t num_edges, const T* __restrict__ w, const int32_t* __restrict__ widx,
+            int heads, int fh, const T* __restrict__ x, T* __restrict__ y,
+            float* __restrict__ carry, int F, int fmode, const T* __restrict__ fout) {
+  constexpr int EB = NCH >= 2 ? 4 : 8;                 // edges gathered per batch
+  constexpr int CPL = TEAM >= EB ? 1 : EB / TEAM;      // column ids loaded per lane
+  using Raw = typename RawVec<V * sizeof(T)>::type;
+
+  const int lane = threadIdx.x & 31;
+  const int tl = lane & (TEAM - 1);
+  const unsigned tmask =
+      TEAM == 32 ? 0xffffffffu : (((1u << TEAM) - 1u) << (lane & ~(TEAM - 1)));
+  const int64_t team = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TEAM;
+  if (team >= num_units) return;
+
+  const int4 un = units[team];
+  const int row = un.x, beg = un.y, end = un.z, slot = un.w;
+  const int nvec = F / V;
+
+  int coff[NCH];
+  bool cval[NCH];
+  int chead[NCH];
+#pragma unroll
+  for (int k = 0; k < NCH; ++k) {
+    int c = tl + k * TEAM;
+    cval[k] = c < nvec;
+    coff[k] = c * V;
+    chead[k] = WEIGHTED ? (c * V) / fh : 0;
+  }
+  float acc[NCH][V];
+#pragma unroll
+  for (int k = 0; k < NCH; ++k)
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc[k][i] = 0.0f;
+
+  // Align batches to the absolute address of cols so column ids come in as
+  // vector loads.
+  const int mis = (int)((reinterpret_cast<uintptr_t>(cols) >> 2) & (EB - 1));
+  int64_t base = (int64_t)beg - (((int64_t)beg + mis) & (EB - 1));
+  for (; base < end; base += EB) {
+    int myc[CPL] = {};
+    const int64_t lo = base + (int64_t)tl * CPL;
+    if (tl * CPL < EB) load_idx<CPL>(cols, lo, num_edges, myc);
+    int myw[CPL] = {};
+    if (WEIGHTED && widx != nullptr && tl * CPL < EB) load_idx<CPL>(widx, lo, num_edges, myw);
+
+    Raw raw[EB][NCH];
+    float wv[EB][NCH];
+    bool ok[EB];
+#pragma unroll
+    for (int j = 0; j < EB; ++j) {
+      const int64_t e = base + j;
+      ok[j] = e >= beg && e < end;
+      const int c = __shfl_sync(tmask, myc[j % CPL], j / CPL, TEAM);
+      int wi = (int)e;
+      if (WEIGHTED && widx != nullptr) wi = __shfl_sync(tmask, myw[j % CPL], j / CPL, TEAM);
+#pragma unroll
+      for (int k = 0; k < NCH; ++k) {
+        if (ok[j] && cval[k]) {
+          raw[j][k] = __ldg(reinterpret_cast<const Raw*>(x + (int64_t)c * F + coff[k]));
+          if (WEIGHTED) wv[j][k] = Num<T>::to_f(w[(int64_t)wi * heads + chead[k]]);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < EB; ++j) {
+#pragma unroll
+      for (int k = 0; k < NCH; ++k) {
+        if (ok[j] && cval[k]) {
+          float f[V];
+          raw_to_float<T, V>(raw[j][k], f);
+          if (WEIGHTED) {
+#pragma unroll
+            for (int i = 0; i < V; ++i) acc[k][i] = fmaf(wv[j][k], f[i], acc[k][i]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < V; ++i) acc[k][i] += f[i];
+          }
+        }
+      }
+    }
+  }
+
+  if (slot < 0) {
+    const T fo = fout ? fout[row] : Num<T>::zero();
+#pragma unroll
+    for (int k = 0; k < NCH; ++k)
+      if (cval[k]) store_out<T, V>(y + (int64_t)row * F + coff[k], acc[k], fmode, fo);
+  } else {
+#pragma unroll
+    for (int k = 0; k < NCH; ++k)
+      if (cval[k]) store_carry<V>(carry + (int64_t)slot * F + coff[k], acc[k]);
+  }
+}
+
+// One team per split row: fp32 carries folded in slot (edge) order.
+template <typename T, int V, int TEAM, int NCH>
+__global__ void __launch_bounds__(256)
+k_spmm_fast_followup(const int4* __restrict__ split_rows, int64_t num_split,
+                     const float* __restrict__ carry, T* __restrict__ y, int F, int fmode,
+                     const T* __restrict__ fout) {
+  const int lane = threadIdx.x & 31;
+  const int tl = lane & (TEAM - 1);
+  const int64_t team = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TEAM;
+  if (team >= num_split) return;
+  const int4 sr = split_rows[team];
+  const int nvec = F / V;
+  const T fo = fout ? fout[sr.x] : Num<T>::zero();
+#pragma unroll
+  for (int k = 0; k < NCH; ++k) {
+    const int c = tl + k * TEAM;
+    if (c >= nvec) continue;
+    float acc[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc[i] = 0.0f;
+    for (int p = 0; p < sr.z; ++p) {
+      const float* src = carry + (int64_t)(sr.y + p) * F + c * V;
+#pragma unroll
+      for (int i = 0; i < V; ++i) acc[i] += src[i];
+    }
+    store_out<T, V>(y + (int64_t)sr.x * F + c * V, acc, fmode, fo);
+  }
+}
+
+// X' = rnd(X * in_scale[:, None]) (kernels.py:358-361), one rounding per element.
+template <typename T>
+__global__ void k_scale_rows(const T* __restrict__ x, const T* __restrict__ s, int64_t rows,
+                             int F, T* __restrict__ out) {
+  const int64_t total = rows * (int64_t)F;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = Num<T>::mul(x[i], s[i / F]);
+}
+
+struct FastArgs {
+  const int64_t* offsets;
+  const int32_t* cols;
+  int64_t n_rows, n_cols, num_edges;
+  const int4* units;
+  int64_t num_units;
+  const int4* split_rows;
+  int64_t num_split;
+  const void* w;
+  const int32_t* widx;
+  int heads, fh;
+  const void* x;
+  void* y;
+  float* carry;
+  int F, fmode;
+  const void* fout;
+  cudaStream_t st;
+};
+
+template <typename T, int V, int TEAM, int NCH, bool WT>
+static int launch_fast(const FastArgs& a) {
+  constexpr int kThreads = 256;
+  constexpr int teams_per_block = kThreads / TEAM;
+  if (a.num_units > 0) {
+    int64_t blocks = (a.num_units + teams_per_block - 1) / teams_per_block;
+    k_spmm_fast<T, V, TEAM, NCH, WT><<<(unsigned)blocks, kThreads, 0, a.st>>>(
+        a.units, a.num_units, a.cols, a.num_edges, (const T*)a.w, a.widx, a.heads, a.fh,
+        (const T*)a.x, (T*)a.y, a.carry, a.F, a.fmode, (const T*)a.fout);
+    HG_LAUNCHED();
+  }
+  if (a.num_split > 0) {
+    int64_t blocks = (a.num_split + teams_per_block - 1) / teams_per_block;
+    k_spmm_fast_followup<T, V, TEAM, NCH><<<(unsigned)blocks, kThreads, 0, a.st>>>(
+        a.split_rows, a.num_split, a.carry, (T*)a.y, a.F, a.fmode, (const T*)a.fout);
+    HG_LAUNCHED();
+  }
+  return HG_OK;
+}
+
+template <typename T, int V, bool WT>
+static int dispatch_layout(const FastArgs& a) {
+  const int nvec = a.F / V;
+  if (nvec <= 1) return launch_fast<T, V, 1, 1, WT>(a);
+  if (nvec <= 2) return launch_fast<T, V, 2, 1, WT>(a);
+  if (nvec <= 4) return launch_fast<T, V, 4, 1, WT>(a);
+  if (nvec <= 8) return launch_fast<T, V, 8, 1, WT>(a);
+  if (nvec <= 16) return launch_fast<T, V, 16, 1, WT>(a);
+  if (nvec <= 32) return launch_fast<T, V, 32, 1, WT>(a);
+  if (nvec <= 64) return launch_fast<T, V, 32, 2, WT>(a);
+  if (nvec <= 128) return launch_fast<T, V, 32, 4, WT>(a);
+  if (nvec <= 256) return launch_fast<T, V, 32, 8, WT>(a);
+  HG_REQUIRE(false, "hg_spmm: feature length %d too large", a.F);
+}
+
+template <typename T>
+static int dispatch_fast(const FastArgs& a) {
+  constexpr int VB = 16 / sizeof(T);
+  const bool aligned = (reinterpret_cast<uintptr_t>(a.x) % 16 == 0) &&
+                       (reinterpret_cast<uintptr_t>(a.y) % 16 == 0);
+  const bool big = aligned && (a.fh % VB == 0);
+  if (a.w) return big ? dispatch_layout<T, VB, true>(a) : dispatch_layout<T, 2, true>(a);
+  return big ? dispatch_layout<T, VB, false>(a) : dispatch_layout<T, 2, false>(a);
+}
+
+static size_t elem_size(int dtype) { return dtype == HG_F16 ? 2 : 4; }
+
+static int scale_rows(const void* x, const void* s, int64_t rows, int F, void* out, int dtype,
+                      cudaStream_t st) {
+  int g = grid_for(rows * (int64_t)F, 256, 148 * 16);
+  if (dtype == HG_F16)
+    k_scale_rows<__half><<<g, 256, 0, st>>>((const __half*)x, (const __half*)s, rows, F,
+                                           (__half*)out);
+  else
+    k_scale_rows<float><<<g, 256, 0, st>>>((const float*)x, (const float*)s, rows, F,
+                                          (float*)out);
+  HG_LAUNCHED();
+  return HG_OK;
+}
+
+}  // namespace hg
+
+using namespace hg;
+
+extern "C" int hg_spmm_workspace(int64_t n_cols, int32_t F, int64_t num_slots, int has_in_scale,
+                                 int dtype, size_t* bytes) {
+  HG_REQUIRE(bytes && F > 0 && n_cols >= 0 && num_slots >= 0, "hg_spmm_workspace: bad arguments");
+  HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
+  Carver cv(nullptr, 0);
+  cv.take<float>((size_t)num_slots * F);
+  if (has_in_scale) cv.take<char>((size_t)n_cols * F * elem_size(dtype));
+  *bytes = cv.used;
+  return HG_OK;
+}
+
+extern "C" int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_rows,
+                       int64_t n_cols, int64_t num_edges, const int32_t* units, int64_t num_units,
+                       const int32_t* split_rows, int64_t num_split_rows, int64_t num_slots,
+                       const void* w, const int32_t* w_index, int32_t heads, const void* x,
+                       void* y, int32_t F, int32_t scaling, const void* in_scale,
+                       const void* out_factor, int dtype, void* ws, size_t ws_bytes,
+                       void* stream) {
+  HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
+  HG_REQUIRE(F > 0 && F % 2 == 0, "feature length %d must be even and positive", F);
+  HG_REQUIRE(heads >= 1 && F % heads == 0 && (F / heads) % 2 == 0,
+             "feature length %d does not split into %d even heads", F, heads);
+  HG_REQUIRE(scaling >= HG_SCALING_POST && scaling <= HG_SCALING_DISCRETIZED,
+             "unknown scaling %d", scaling);
+  HG_REQUIRE(n_rows >= 0 && n_cols >= 0 && num_edges >= 0, "hg_spmm: bad sizes");
+  HG_REQUIRE(num_edges <= (int64_t)INT32_MAX, "hg_spmm: edge count exceeds int32 units");
+  cudaStream_t st = as_stream(stream);
+  if (n_rows == 0) return HG_OK;
+  Carver cv(ws, ws_bytes);
+  float* carry = cv.take<float>((size_t)num_slots * F);
+  void* xs = in_scale ? cv.take<char>((size_t)n_cols * F * elem_size(dtype)) : nullptr;
+  HG_REQUIRE(cv.fits(), "hg_spmm: workspace too small (%zu < %zu)", ws_bytes, cv.used);
+  HG_REQUIRE(num_slots == 0 || carry != nullptr, "hg_spmm: carry workspace missing");
+  if (in_scale) {
+    int rc = scale_rows(x, in_scale, n_cols, F, xs, dtype, st);
+    if (rc) return rc;
+    x = xs;
+  }
+  FastArgs a;
+  a.offsets = offsets; a.cols = cols; a.n_rows = n_rows; a.n_cols = n_cols;
+  a.num_edges = num_edges;
+  a.units = reinterpret_cast<const int4*>(units); a.num_units = num_units;
+  a.split_rows = reinterpret_cast<const int4*>(split_rows); a.num_split = num_split_rows;
+  a.w = w; a.widx = w_index; a.heads = heads; a.fh = F / heads;
+  a.x = x; a.y = y; a.carry = carry; a.F = F;
+  a.fmode = out_factor == nullptr ? 0 : (scaling == HG_SCALING_POST ? 1 : 2);
+  a.fout = out_factor; a.st = st;
+  return dtype == HG_F16 ? dispatch_fast<__half>(a) : dispatch_fast<float>(a);
+}
+
+// ------------------------------------------------------ reference edge order
+
+namespace hg {
+
+// shared-memory header of k_spmm_edge_ref: brow int64[2W], nseg int[W], ent int[2W]
+__host__ __device__ inline size_t edge_ref_hdr(int W) { return ((size_t)28 * W + 15) / 16 * 16; }
+
+template <typename T, bool WEIGHTED>
+__global__ void k_spmm_edge_ref(const int64_t* __restrict__ offsets,
+                                const int32_t* __restrict__ cols, int64_t n_rows,
+                                int64_t num_edges, int C, int W, const T* __restrict__ w,
+                                const T* __restrict__ x, T* __restrict__ y, int F, int scaling,
+                                const T* __restrict__ fout, int kb, T* __restrict__ carry_vals,
+                                int64_t* __restrict__ carry_rows) {
+  using N = Num<T>;
+  using T2 = typename N::T2;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int P = F / 2;
+  int64_t* brow = reinterpret_cast<int64_t*>(smem_raw);   // [W][2]
+  int* nseg = reinterpret_cast<int*>(brow + 2 * W);       // [W]
+  int* ent = nseg + W;                                    // [2W] entry -> (warp*2+slot)
+  T2* bval = reinterpret_cast<T2*>(smem_raw + edge_ref_hdr(W));  // [W][2][P]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t cta = blockIdx.x;
+  const int64_t cta_e0 = cta * (int64_t)W * C;
+  const int64_t e0 = (cta * W + warp) * (int64_t)C;
+  const int64_t e1 = e0 + C < num_edges ? e0 + C : num_edges;
+  const bool post = scaling == HG_SCALING_POST;
+  const bool pre = scaling == HG_SCALING_PRE;
+  const bool disc = scaling == HG_SCALING_DISCRETIZED;
+  const T2* x2 = reinterpret_cast<const T2*>(x);
+  T2* y2 = reinterpret_cast<T2*>(y);
+  const T one = N::from_f(1.0f);
+
+  int ns = 0;
+  if (e0 < num_edges) {
+    int64_t r = row_of_edge(offsets, n_rows, e0);
+    int64_t e = e0;
+    while (e < e1) {
+      while (offsets[r + 1] <= e) ++r;
+      const int64_t s = e;
+      const int64_t t = offsets[r + 1] < e1 ? offsets[r + 1] : e1;
+      const bool is_first = ns == 0;
+      const bool is_last = t == e1;
+      const T fo = fout ? fout[r] : N::zero();
+      const T2 fo2 = N::bcast(fo);
+      for (int p = lane; p < P; p += 32) {
+        T2 acc = N::zero2();
+        if (disc) {
+          T2 raw = N::zero2();
+          int cnt = 0;
+          for (int64_t q = s; q < t; ++q) {
+            const T2 xv = x2[(int64_t)cols[q] * P + p];
+            raw = WEIGHTED ? N::fma2(N::bcast(w[q]), xv, raw) : N::add2(xv, raw);
+            if (++cnt == kb || q + 1 == t) {
+              acc = fout ? N::fma2(raw, fo2, acc) : N::add2(raw, acc);
+              raw = N::zero2();
+              cnt = 0;
+            }
+          }
+        } else {
+          for (int64_t q = s; q < t; ++q) {
+            const T2 xv = x2[(int64_t)cols[q] * P + p];
+            if (pre && fout) {
+              const T m = WEIGHTED ? N::mul(w[q], fo) : fo;
+              acc = N::fma2(N::bcast(m), xv, acc);
+            } else if (WEIGHTED) {
+              acc = N::fma2(N::bcast(w[q]), xv, acc);
+            } else {
+              acc = N::fma2(N::bcast(one), xv, acc);
+            }
+          }
+        }
+        if (is_first) {
+          bval[(warp * 2 + 0) * P + p] = acc;
+        } else if (is_last) {
+          bval[(warp * 2 + 1) * P + p] = acc;
+        } else {  // interior segment: a complete row that began in this warp
+          y2[r * P + p] = (post && fout && N::gt0(fo)) ? N::mul2(acc, fo2) : acc;
+        }
+      }
+      if (lane == 0) {
+        if (is_first) brow[warp * 2] = r;
+        else if (is_last) brow[warp * 2 + 1] = r;
+      }
+      ++ns;
+      e = t;
+    }
+  }
+  if (lane == 0) nseg[warp] = ns;
+  __syncthreads();
+  if (warp != 0) return;
+
+  // Boundary segments of the CTA in edge order; chains = runs of equal rows.
+  int total = 0;
+  for (int v = 0; v < W; ++v) {
+    const int k = nseg[v];
+    if (k >= 1) { if (lane == 0) ent[total] = v * 2; ++total; }
+    if (k >= 2) { if (lane == 0) ent[total] = v * 2 + 1; ++total; }
+  }
+  __syncwarp();
+  int i = 0;
+  while (i < total) {
+    const int64_t r = brow[ent[i]];
+    int j = i + 1;
+    while (j < total && brow[ent[j]] == r) ++j;
+    const int cnt = j - i;
+    const bool carry = j == total;
+    const T fo = fout ? fout[r] : N::zero();
+    const bool scale_now = !carry && post && fout && N::gt0(fo) && offsets[r] >= cta_e0;
+    for (int p = lane; p < P; p += 32) {
+      for (int stride = 1; stride < cnt; stride <<= 1)
+        for (int q = 0; q + stride < cnt; q += 2 * stride)
+          bval[ent[i + q] * P + p] = N::add2(bval[ent[i + q] * P + p], bval[ent[i + q + stride] * P + p]);
+      const T2 v = bval[ent[i] * P + p];
+      if (carry) reinterpret_cast<T2*>(carry_vals)[cta * P + p] = v;
+      else y2[r * P + p] = scale_now ? N::mul2(v, N::bcast(fo)) : v;
+    }
+    if (carry && lane == 0) carry_rows[cta] = r;
+    i = j;
+  }
+}
+
+// Fold each CTA's carry into its row in ascending CTA order, then post-scale.
+template <typename T>
+__global__ void k_spmm_edge_ref_followup(const typename Num<T>::T2* __restrict__ carry_vals,
+                                         const int64_t* __restrict__ carry_rows, int64_t num_ctas,
+                                         T* __restrict__ y, int F, int scaling,
+                                         const T* __restrict__ fout) {
+  using N = Num<T>;
+  using T2 = typename N::T2;
+  const int64_t c = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (c >= num_ctas) return;
+  const int64_t r = carry_rows[c];
+  if (c > 0 && carry_rows[c - 1] == r) return;  // not the leader of this row's run
+  const int P = F / 2;
+  T2* y2 = reinterpret_cast<T2*>(y);
+  const T fo = fout ? fout[r] : N::zero();
+  const bool scale = scaling == HG_SCALING_POST && fout && N::gt0(fo);
+  for (int p = lane; p < P; p += 32) {
+    T2 v = y2[r * P + p];
+    for (int64_t j = c; j < num_ctas && carry_rows[j] == r; ++j) v = N::add2(v, carry_vals[j * P + p]);
+    y2[r * P + p] = scale ? N::mul2(v, N::bcast(fo)) : v;
+  }
+}
+
+}  // namespace hg
+
+static size_t edge_ref_smem(int W, int F, int dtype) {
+  return hg::edge_ref_hdr(W) + (size_t)W * 2 * F * hg::elem_size(dtype);
+}
+
+extern "C" int hg_spmm_edge_ref_workspace(int64_t n_cols, int64_t num_edges, int32_t F,
+                                          int32_t warp_chunk, int32_t warps_per_cta,
+                                          int has_in_scale, int dtype, size_t* bytes) {
+  HG_REQUIRE(bytes && F > 0 && warp_chunk > 0 && warps_per_cta > 0,
+             "hg_spmm_edge_ref_workspace: bad arguments");
+  int64_t nw = (num_edges + warp_chunk - 1) / warp_chunk;
+  int64_t nc = (nw + warps_per_cta - 1) / warps_per_cta;
+  Carver cv(nullptr, 0);
+  cv.take<char>((size_t)nc * F * elem_size(dtype));
+  cv.take<int64_t>(nc);
+  if (has_in_scale) cv.take<char>((size_t)n_cols * F * elem_size(dtype));
+  *bytes = cv.used;
+  return HG_OK;
+}
+
+extern "C" int hg_spmm_edge_ref(const int64_t* offsets, const int32_t* cols, int64_t n_rows,
+                                int64_t n_cols, int64_t num_edges, int32_t C, int32_t W,
+                                const void* w, const void* x, void* y, int32_t F,
+                                int32_t scaling, const void* in_scale, const void* out_factor,
+                                void* staging_partials, int64_t* staging_rows, int dtype,
+                                void* ws, size_t ws_bytes, void* stream) {
+  HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
+  HG_REQUIRE(F > 0 && F % 2 == 0, "feature length %d must be even and positive", F);
+  HG_REQUIRE(C >= 64 && C % 2 == 0, "warp_chunk must be >= 64 and even, got %d", C);
+  HG_REQUIRE(W >= 1 && W <= 32, "warps_per_cta must be in [1, 32], got %d", W);
+  HG_REQUIRE(scaling >= HG_SCALING_POST && scaling <= HG_SCALING_DISCRETIZED,
+             "unknown scaling %d", scaling);
+  cudaStream_t st = as_stream(stream);
+  const size_t es = elem_size(dtype);
+  if (n_rows > 0) HG_CUDA(cudaMemsetAsync(y, 0, (size_t)n_rows * F * es, st));
+  if (num_edges == 0 || n_rows == 0) return HG_OK;
+  const int64_t nw = (num_edges + C - 1) / C;
+  const int64_t nc = (nw + W - 1) / W;
+  Carver cv(ws, ws_bytes);
+  void* cvals = cv.take<char>((size_t)nc * F * es);
+  int64_t* crows = cv.take<int64_t>(nc);
+  void* xs = in_scale ? cv.take<char>((size_t)n_cols * F * es) : nullptr;
+  HG_REQUIRE(cv.fits(), "hg_spmm_edge_ref: workspace too small");
+  if (staging_partials) cvals = staging_partials;
+  if (staging_rows) crows = staging_rows;
+  if (in_scale) {
+    int rc = scale_rows(x, in_scale, n_cols, F, xs, dtype, st);
+    if (rc) return rc;
+    x = xs;
+  }
+  // discretization batch k = simt.subwarp_layout(F).subwarps (simt.py:86-98)
+  const int kb = F > 64 ? 1 : 32 / (F / 2);
+  const size_t smem = edge_ref_smem(W, F, dtype);
+  HG_REQUIRE(smem <= 227 * 1024, "hg_spmm_edge_ref: F=%d too large for %d warps per CTA", F, W);
+  const dim3 grid((unsigned)nc), block(32 * W);
+  if (dtype == HG_F16) {
+    auto kfn = w ? k_spmm_edge_ref<__half, true> : k_spmm_edge_ref<__half, false>;
+    HG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kfn<<<grid, block, smem, st>>>(offsets, cols, n_rows, num_edges, C, W, (const __half*)w,
+                                   (const __half*)x, (__half*)y, F, scaling,
+                                   (const __half*)out_factor, kb, (__half*)cvals, crows);
+    HG_LAUNCHED();
+    k_spmm_edge_ref_followup<__half><<<grid_for(nc, 8), 256, 0, st>>>(
+        (const __half2*)cvals, crows, nc, (__half*)y, F, scaling, (const __half*)out_factor);
+  } else {
+    auto kfn = w ? k_spmm_edge_ref<float, true> : k_spmm_edge_ref<float, false>;
+    HG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kfn<<<grid, block, smem, st>>>(offsets, cols, n_rows, num_edges, C, W, (const float*)w,
+                                   (const float*)x, (float*)y, F, scaling,
+                                   (const float*)out_factor, kb, (float*)cvals, crows);
+    HG_LAUNCHED();
+    k_spmm_edge_ref_followup<float><<<grid_for(nc, 8), 256, 0, st>>>(
+        (const float2*)cvals, crows, nc, (float*)y, F, scaling, (const float*)out_factor);
+  }
+  HG_LAUNCHED();
+  return HG_OK;
+}
+
+// -------------------------------------------------- reference vertex groups
+
+namespace hg {
+
+template <typename T>
+__global__ void k_spmm_vertex_ref(const int64_t* __restrict__ offsets,
+                                  const int32_t* __restrict__ cols, int64_t n_rows,
+                                  const T* __restrict__ x, T* __restrict__ y, int F, int scaling,
+                                  const T* __restrict__ fout, const int64_t* __restrict__ gbase,
+                                  T* __restrict__ stage, int64_t* __restrict__ stage_rows) {
+  using N = Num<T>;
+  using T2 = typename N::T2;
+  const int lane = threadIdx.x & 31;
+  const int P = F / 2;
+  const T2* x2 = reinterpret_cast<const T2*>(x);
+  T2* y2 = reinterpret_cast<T2*>(y);
+  T2* s2 = reinterpret_cast<T2*>(stage);
+  const bool pre = scaling == HG_SCALING_PRE, disc = scaling == HG_SCALING_DISCRETIZED;
+  const bool post = scaling == HG_SCALING_POST;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows;
+       r += nwarps) {
+    const int64_t beg = offsets[r], end = offsets[r + 1];
+    const int64_t ng = (end - beg + 31) / 32;
+    const T fo = fout ? fout[r] : N::zero();
+    const T2 fo2 = N::bcast(fo);
+    const T2 m2 = (pre && fout) ? fo2 : N::bcast(N::from_f(1.0f));
+    if (stage && ng > 1 && lane < ng) {
+      for (int64_t g = lane; g < ng; g += 32) stage_rows[gbase[r] + g] = r;
+    }
+    for (int p = lane; p < P; p += 32) {
+      T2 yv = N::zero2();
+      for (int64_t g = 0; g < ng; ++g) {
+        const int64_t gb = beg + g * 32;
+        const int64_t ge = gb + 32 < end ? gb + 32 : end;
+        T2 acc = N::zero2();
+        for (int64_t q = gb; q < ge; ++q) acc = N::fma2(m2, x2[(int64_t)cols[q] * P + p], acc);
+        const T2 part = (disc && fout) ? N::mul2(acc, fo2) : acc;
+        if (stage && ng > 1) s2[(gbase[r] + g) * P + p] = part;
+        yv = g == 0 ? part : N::add2(yv, part);
+      }
+      if (post && fout && N::gt0(fo)) yv = N::mul2(yv, fo2);
+      y2[r * P + p] = yv;
+    }
+  }
+}
+
+}  // namespace hg
+
+extern "C" int hg_spmm_vertex_ref_workspace(int64_t n_cols, int32_t F, int has_in_scale,
+                                            int dtype, size_t* bytes) {
+  HG_REQUIRE(bytes && F > 0, "hg_spmm_vertex_ref_workspace: bad arguments");
+  Carver cv(nullptr, 0);
+  if (has_in_scale) cv.take<char>((size_t)n_cols * F * elem_size(dtype));
+  *bytes = cv.used;
+  return HG_OK;
+}
+
+extern "C" int hg_spmm_vertex_ref(const int64_t* offsets, const int32_t* cols, int64_t n_rows,
+                                  int64_t n_cols, const void* x, void* y, int32_t F,
+                                  int32_t scaling, const void* in_scale, const void* out_factor,
+                                  const int64_t* group_base, void* staging_partials,
+                                  int64_t* staging_rows, int dtype, void* ws, size_t ws_bytes,
+                                  void* stream) {
+  HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
+  HG_REQUIRE(F > 0 && F % 2 == 0, "feature length %d must be even and positive", F);
+  HG_REQUIRE(scaling >= HG_SCALING_POST && scaling <= HG_SCALING_DISCRETIZED,
+             "unknown scaling %d", scaling);
+  HG_REQUIRE(!staging_partials || (group_base && staging_rows),
+             "hg_spmm_vertex_ref: staging needs group_base and staging_rows");
+  cudaStream_t st = as_stream(stream);
+  if (n_rows == 0) return HG_OK;
+  Carver cv(ws, ws_bytes);
+  void* xs = in_scale ? cv.take<char>((size_t)n_cols * F * elem_size(dtype)) : nullptr;
+  HG_REQUIRE(cv.fits(), "hg_spmm_vertex_ref: workspace too small");
+  if (in_scale) {
+    int rc = scale_rows(x, in_scale, n_cols, F, xs, dtype, st);
+    if (rc) return rc;
+    x = xs;
+  }
+  const int g = grid_for(n_rows, 8, 148 * 64);
+  if (dtype == HG_F16)
+    k_spmm_vertex_ref<__half><<<g, 256, 0, st>>>(offsets, cols, n_rows, (const __half*)x,
+                                                 (__half*)y, F, scaling,
+                                                 (const __half*)out_factor, group_base,
+                                                 (__half*)staging_partials, staging_rows);
+  else
+    k_spmm_vertex_ref<float><<<g, 256, 0, st>>>(offsets, cols, n_rows, (const float*)x,
+                                                (float*)y, F, scaling, (const float*)out_factor,
+                                                group_base, (float*)staging_partials,
+                                                staging_rows);
+  HG_LAUNCHED();
+  return HG_OK;
+}

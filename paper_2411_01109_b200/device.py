@@ -1,0 +1,406 @@
+"""Device-resident graph and the torch-level entry points of the B200 kernels.
+
+Everything here takes CUDA tensors, launches on torch's current stream and
+returns CUDA tensors; nothing synchronises except graph construction (whose
+output sizes are data dependent).  torch provides device memory (the caching
+allocator backs every workspace) and streams; all arithmetic happens in
+libhalfgnn.so.
+
+HBM layout of a DeviceGraph (N vertices, E edges):
+    offsets   int64[N+1]   CSR row offsets          (sparse.py:72-94)
+    cols      int32[E]     CSR column ids, rows sorted by (row, col)
+    t_offsets int64[N+1]   CSC offsets (transposed CSR, sparse.py:109-120)
+    t_cols    int32[E]     CSC row ids
+    perm      int32[E]     CSC slot -> CSR edge id (stable, the reference's perm)
+    factor tables fp16/fp32[N] and degree-bucketed work units, built lazily.
+Features are row-major [rows, F] fp16 (or fp32 in float32 mode).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _native as nat
+
+DTYPE_CODE = {torch.float16: nat.HG_F16, torch.float32: nat.HG_F32}
+MIRROR = {"none": "none", "left": "right", "right": "left", "both": "both"}
+DEFAULT_SPLIT_CAP = 512
+
+
+def _p(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dtype_code(t):
+    try:
+        return DTYPE_CODE[t.dtype]
+    except KeyError:
+        raise ValueError(f"unsupported dtype {t.dtype}") from None
+
+
+_WS = {}
+
+
+def workspace(nbytes: int, device) -> torch.Tensor | None:
+    """Per-(device, stream) scratch from torch's caching allocator, grown on demand.
+    Kernels on one stream run in order, so one buffer per stream is safe."""
+    if nbytes <= 0:
+        return None
+    key = (torch.device(device), torch.cuda.current_stream(device).cuda_stream)
+    buf = _WS.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+        _WS[key] = buf
+    return buf
+
+
+def _require_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("halfgnn operators take CUDA tensors")
+
+
+# ── graph construction ───────────────────────────────────────────────────
+
+
+def build_csr(n: int, rows: torch.Tensor, cols: torch.Tensor, want_rows: bool = False):
+    """CooGraph.from_edges + coo_to_csr on the GPU (sort + dedup, bit-exact).
+    rows/cols: int64 CUDA tensors.  Returns (offsets, cols32, rows64|None)."""
+    _require_cuda(rows, cols)
+    rows = rows.to(torch.int64).contiguous()
+    cols = cols.to(torch.int64).contiguous()
+    m = rows.numel()
+    if cols.numel() != m:
+        raise ValueError("rows/cols must be matching 1-D arrays")
+    dev = rows.device
+    ws = workspace(nat.size_query("hg_build_csr_workspace", m, n), dev)
+    offsets = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    out_cols = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
+    out_rows = torch.empty(max(m, 1), dtype=torch.int64, device=dev) if want_rows else None
+    e = ctypes.c_int64(0)
+    nat.call("hg_build_csr", _p(rows), _p(cols), m, n, _p(offsets), _p(out_cols), _p(out_rows),
+             ctypes.byref(e), _p(ws), 0 if ws is None else ws.numel(), _stream())
+    e = int(e.value)
+    return offsets, out_cols[:e], (out_rows[:e] if want_rows else None)
+
+
+def transpose_csr(offsets: torch.Tensor, cols: torch.Tensor, n: int):
+    """transpose(g, return_perm=True) on the GPU.  Returns (t_offsets, t_cols, perm)."""
+    m = cols.numel()
+    dev = offsets.device
+    ws = workspace(nat.size_query("hg_transpose_workspace", n, m), dev)
+    t_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    t_cols = torch.empty(m, dtype=torch.int32, device=dev)
+    perm = torch.empty(m, dtype=torch.int32, device=dev)
+    nat.call("hg_transpose", _p(offsets), _p(cols), n, m, _p(t_off), _p(t_cols), _p(perm),
+             _p(ws), 0 if ws is None else ws.numel(), _stream())
+    return t_off, t_cols, perm
+
+
+def degree_factors(offsets: torch.Tensor, kind: str, dtype=torch.float16) -> torch.Tensor:
+    """kind 'inv' (left/right norms) or 'inv_sqrt' (both), from offsets' degrees."""
+    n = offsets.numel() - 1
+    out = torch.empty(n, dtype=dtype, device=offsets.device)
+    code = nat.FACTOR_INV if kind == "inv" else nat.FACTOR_INV_SQRT
+    nat.call("hg_degree_factors", _p(offsets), n, code, DTYPE_CODE[dtype], _p(out), _stream())
+    return out
+
+
+@dataclass
+class WorkSchedule:
+    """Degree-bucketed work units of one CSR (hg_schedule_build)."""
+
+    units: torch.Tensor       # int32 [U, 4] {row, begin, end, slot}
+    split_rows: torch.Tensor  # int32 [S, 4] {row, first_slot, nparts, 0}
+    num_slots: int
+    split_cap: int
+
+    @property
+    def num_units(self):
+        return self.units.shape[0]
+
+
+def build_schedule(offsets: torch.Tensor, split_cap: int = DEFAULT_SPLIT_CAP) -> WorkSchedule:
+    n = offsets.numel() - 1
+    m = int(offsets[-1].item())
+    dev = offsets.device
+    max_units = n + (m + split_cap - 1) // split_cap
+    max_split = max(1, (m + split_cap - 1) // split_cap)
+    units = torch.empty((max_units, 4), dtype=torch.int32, device=dev)
+    split = torch.empty((max_split, 4), dtype=torch.int32, device=dev)
+    ws = workspace(nat.size_query("hg_schedule_workspace", n, m, split_cap), dev)
+    counts = (ctypes.c_int64 * 3)()
+    nat.call("hg_schedule_build", _p(offsets), n, split_cap, _p(units), max_units, _p(split),
+             max_split, counts, _p(ws), 0 if ws is None else ws.numel(), _stream())
+    return WorkSchedule(units[: counts[0]], split[: counts[1]], int(counts[2]), split_cap)
+
+
+@dataclass
+class CsrView:
+    """One row-owned CSR operand: local rows, columns index a feature matrix of
+    n_cols rows (the full graph, or all-gathered rows of a partition)."""
+
+    offsets: torch.Tensor
+    cols: torch.Tensor
+    n_rows: int
+    n_cols: int
+    perm: torch.Tensor | None = None     # for a CSC view: slot -> forward edge id
+    _sched: dict = field(default_factory=dict, repr=False)
+
+    @property
+    def num_edges(self):
+        return self.cols.numel()
+
+    def schedule(self, split_cap: int = DEFAULT_SPLIT_CAP) -> WorkSchedule:
+        s = self._sched.get(split_cap)
+        if s is None:
+            s = build_schedule(self.offsets, split_cap)
+            self._sched[split_cap] = s
+        return s
+
+
+class DeviceGraph:
+    """Canonical graph resident in HBM: CSR, CSC + perm, factor tables, schedules."""
+
+    def __init__(self, n: int, offsets: torch.Tensor, cols: torch.Tensor,
+                 build_transpose: bool = True):
+        self.n = int(n)
+        self.offsets = offsets
+        self.cols = cols
+        self.device = offsets.device
+        self.fwd = CsrView(offsets, cols, self.n, self.n)
+        self.bwd = None
+        if build_transpose:
+            t_off, t_cols, perm = transpose_csr(offsets, cols, self.n)
+            self.bwd = CsrView(t_off, t_cols, self.n, self.n, perm=perm)
+        self._factors = {}
+        self._rows = None
+
+    @property
+    def num_edges(self):
+        return self.cols.numel()
+
+    @property
+    def perm(self):
+        return self.bwd.perm
+
+    @classmethod
+    def from_edges(cls, n, rows, cols, device="cuda", build_transpose=True):
+        """Canonicalise an arbitrary edge list (any order, duplicates allowed) on the GPU."""
+        rows = torch.as_tensor(rows, dtype=torch.int64).to(device)
+        cols = torch.as_tensor(cols, dtype=torch.int64).to(device)
+        offsets, c32, _ = build_csr(n, rows, cols)
+        return cls(n, offsets, c32, build_transpose)
+
+    def rows(self) -> torch.Tensor:
+        """int64 row id per CSR edge (csr_to_coo)."""
+        if self._rows is None:
+            deg = self.offsets[1:] - self.offsets[:-1]
+            self._rows = torch.repeat_interleave(
+                torch.arange(self.n, device=self.device, dtype=torch.int64), deg)
+        return self._rows
+
+    def factor(self, kind: str, side: str, dtype=torch.float16) -> torch.Tensor:
+        """Degree factor table; side 'row' uses CSR degrees, 'col' CSC degrees."""
+        key = (kind, side, dtype)
+        t = self._factors.get(key)
+        if t is None:
+            offs = self.offsets if side == "row" else self.bwd.offsets
+            t = degree_factors(offs, kind, dtype)
+            self._factors[key] = t
+        return t
+
+    def norm_tables(self, norm: str, transpose: bool, dtype):
+        """(in_scale, out_factor) of `norm` for the graph actually traversed
+        (the transpose when transpose=True), as kernels._degree_factors does."""
+        kind = "inv_sqrt" if norm == "both" else "inv"
+        row_side, col_side = ("col", "row") if transpose else ("row", "col")
+        fin = self.factor(kind, col_side, dtype) if norm in ("left", "both") else None
+        fout = self.factor(kind, row_side, dtype) if norm in ("right", "both") else None
+        return fin, fout
+
+    def view(self, transpose: bool = False) -> CsrView:
+        if transpose and self.bwd is None:
+            raise ValueError("graph was built without its transpose")
+        return self.bwd if transpose else self.fwd
+
+
+# ── SpMM ─────────────────────────────────────────────────────────────────
+
+
+def spmm_csr(view: CsrView, x: torch.Tensor, w=None, w_index=None, heads: int = 1,
+             scaling: str = "post", fin=None, fout=None, out=None,
+             split_cap: int = DEFAULT_SPLIT_CAP) -> torch.Tensor:
+    """fp32-guarded row-owned SpMM over one CSR view (hg_spmm)."""
+    _require_cuda(x)
+    x = x.contiguous()
+    if x.dim() != 2 or x.shape[0] != view.n_cols:
+        raise ValueError(f"feature tensor has {x.shape[0]} rows for {view.n_cols} columns")
+    f = x.shape[1]
+    dt = _dtype_code(x)
+    sched = view.schedule(split_cap)
+    if out is None:
+        out = torch.empty((view.n_rows, f), dtype=x.dtype, device=x.device)
+    nbytes = nat.size_query("hg_spmm_workspace", view.n_cols, f, sched.num_slots,
+                            int(fin is not None), dt)
+    ws = workspace(nbytes, x.device)
+    if w is not None:
+        w = w.contiguous()
+        if w.dtype != x.dtype:
+            raise ValueError("edge weights must match the feature dtype")
+    nat.call("hg_spmm", _p(view.offsets), _p(view.cols), view.n_rows, view.n_cols,
+             view.num_edges, _p(sched.units), sched.num_units, _p(sched.split_rows),
+             sched.split_rows.shape[0], sched.num_slots, _p(w), _p(w_index), heads, _p(x),
+             _p(out), f, nat.SCALING_CODES[scaling], _p(fin), _p(fout), dt, _p(ws),
+             0 if ws is None else ws.numel(), _stream())
+    return out
+
+
+def spmm(dg: DeviceGraph, x, w=None, scaling="post", norm="none", transpose=False, heads=1,
+         out=None, weight_via_perm=False):
+    """SpMMv / SpMMve on the graph (or its transpose), fp32-guarded.
+    weight_via_perm: w is indexed by forward edge id and read through perm
+    (spmm_weighted backward, models.py:309-311) without materialising w[perm]."""
+    view = dg.view(transpose)
+    fin, fout = dg.norm_tables(norm, transpose, x.dtype)
+    widx = view.perm if (w is not None and weight_via_perm) else None
+    return spmm_csr(view, x, w, widx, heads, scaling, fin, fout, out)
+
+
+def spmm_edge_ref(dg: DeviceGraph, x, w=None, scaling="post", norm="none", transpose=False,
+                  warp_chunk=128, warps_per_cta=4, staging=False):
+    """Reference-order SpMM (bit-exact with halfsparse.kernels.spmm_v / spmm_ve).
+    Returns y, or (y, staging_rows int64, staging_partials) when staging=True."""
+    view = dg.view(transpose)
+    _require_cuda(x)
+    x = x.contiguous()
+    f = x.shape[1]
+    dt = _dtype_code(x)
+    fin, fout = dg.norm_tables(norm, transpose, x.dtype)
+    y = torch.empty((view.n_rows, f), dtype=x.dtype, device=x.device)
+    m = view.num_edges
+    nw = (m + warp_chunk - 1) // warp_chunk
+    nc = (nw + warps_per_cta - 1) // warps_per_cta
+    st_rows = st_vals = None
+    if staging:
+        st_rows = torch.empty(max(nc, 1), dtype=torch.int64, device=x.device)
+        st_vals = torch.empty((max(nc, 1), f), dtype=x.dtype, device=x.device)
+    nbytes = nat.size_query("hg_spmm_edge_ref_workspace", view.n_cols, m, f, warp_chunk,
+                            warps_per_cta, int(fin is not None), dt)
+    ws = workspace(nbytes, x.device)
+    if w is not None:
+        w = w.contiguous()
+    nat.call("hg_spmm_edge_ref", _p(view.offsets), _p(view.cols), view.n_rows, view.n_cols, m,
+             warp_chunk, warps_per_cta, _p(w), _p(x), _p(y), f, nat.SCALING_CODES[scaling],
+             _p(fin), _p(fout), _p(st_vals), _p(st_rows), dt, _p(ws),
+             0 if ws is None else ws.numel(), _stream())
+    if staging:
+        return y, st_rows[:nc], st_vals[:nc]
+    return y
+
+
+def spmm_vertex_ref(dg: DeviceGraph, x, scaling="post", norm="none", staging=False):
+    """Vertex-grouped SpMMv, bit-exact with halfsparse.kernels.spmm_vertex_grouped."""
+    view = dg.fwd
+    _require_cuda(x)
+    x = x.contiguous()
+    f = x.shape[1]
+    dt = _dtype_code(x)
+    fin, fout = dg.norm_tables(norm, False, x.dtype)
+    y = torch.empty((view.n_rows, f), dtype=x.dtype, device=x.device)
+    gbase = st_rows = st_vals = None
+    total = 0
+    if staging:
+        deg = view.offsets[1:] - view.offsets[:-1]
+        ng = (deg + 31) // 32
+        ng = torch.where(ng > 1, ng, torch.zeros_like(ng))
+        csum = torch.cumsum(ng, 0)
+        total = int(csum[-1].item()) if csum.numel() else 0
+        gbase = (csum - ng).contiguous()
+        st_rows = torch.empty(max(total, 1), dtype=torch.int64, device=x.device)
+        st_vals = torch.empty((max(total, 1), f), dtype=x.dtype, device=x.device)
+    ws = workspace(nat.size_query("hg_spmm_vertex_ref_workspace", view.n_cols, f,
+                                  int(fin is not None), dt), x.device)
+    nat.call("hg_spmm_vertex_ref", _p(view.offsets), _p(view.cols), view.n_rows, view.n_cols,
+             _p(x), _p(y), f, nat.SCALING_CODES[scaling], _p(fin), _p(fout), _p(gbase),
+             _p(st_vals), _p(st_rows), dt, _p(ws), 0 if ws is None else ws.numel(), _stream())
+    if staging:
+        return y, st_rows[:total], st_vals[:total]
+    return y
+
+
+# ── SDDMM, attention, softmax ────────────────────────────────────────────
+
+
+def sddmm(dg: DeviceGraph, x, y, heads=1, transpose=False):
+    """Per-edge (per-head) tree dot products, bit-exact with kernels.sddmm.
+    Returns [E] for heads == 1, else [E, heads]."""
+    view = dg.view(transpose)
+    _require_cuda(x, y)
+    x, y = x.contiguous(), y.contiguous()
+    if x.dtype != y.dtype:
+        raise ValueError("operand modes differ")
+    if x.shape[1] != y.shape[1]:
+        raise ValueError("operand feature lengths differ")
+    f = x.shape[1]
+    sched = view.schedule()
+    out = torch.empty((view.num_edges, heads), dtype=x.dtype, device=x.device)
+    nat.call("hg_sddmm", _p(view.offsets), _p(view.cols), view.n_rows, view.num_edges,
+             _p(sched.units), sched.num_units, _p(x), _p(y), _p(out), f, heads,
+             _dtype_code(x), _stream())
+    return out[:, 0] if heads == 1 else out
+
+
+def attention_logits(dg: DeviceGraph, s_l, s_r, slope=0.2):
+    """leaky_relu(attention_scores(s_l, s_r)) per head: [E, H]."""
+    _require_cuda(s_l, s_r)
+    s_l, s_r = s_l.contiguous(), s_r.contiguous()
+    heads = s_l.shape[1] if s_l.dim() == 2 else 1
+    out = torch.empty((dg.num_edges, heads), dtype=s_l.dtype, device=s_l.device)
+    nat.call("hg_attn_scores", _p(dg.offsets), _p(dg.cols), dg.n, dg.num_edges, _p(s_l),
+             _p(s_r), heads, float(slope), _p(out), _dtype_code(s_l), _stream())
+    return out
+
+
+def edge_softmax_fwd(dg: DeviceGraph, e):
+    _require_cuda(e)
+    e = e.contiguous()
+    heads = e.shape[1] if e.dim() == 2 else 1
+    alpha = torch.empty_like(e)
+    nat.call("hg_edge_softmax_fwd", _p(dg.offsets), dg.n, dg.num_edges, _p(e), _p(alpha), heads,
+             _dtype_code(e), _stream())
+    return alpha
+
+
+def edge_softmax_bwd(dg: DeviceGraph, alpha, g):
+    alpha, g = alpha.contiguous(), g.contiguous()
+    heads = alpha.shape[1] if alpha.dim() == 2 else 1
+    de = torch.empty_like(alpha)
+    nat.call("hg_edge_softmax_bwd", _p(dg.offsets), dg.n, dg.num_edges, _p(alpha), _p(g),
+             _p(de), heads, _dtype_code(alpha), _stream())
+    return de
+
+
+def edge_rowsum(dg: DeviceGraph, v, transpose=False):
+    """Per-row (transpose=False) or per-column (True) sums of per-edge values."""
+    v = v.contiguous()
+    heads = v.shape[1] if v.dim() == 2 else 1
+    view = dg.view(transpose)
+    out = torch.empty((view.n_rows, heads), dtype=v.dtype, device=v.device)
+    nat.call("hg_edge_rowsum", _p(view.offsets), view.n_rows, view.num_edges, _p(v),
+             _p(view.perm if transpose else None), heads, _p(out), _dtype_code(v), _stream())
+    return out
+
+
+def scale_f64(x, s: float):
+    """rnd(x * s) with the product formed in float64."""
+    x = x.contiguous()
+    out = torch.empty_like(x)
+    nat.call("hg_scale_f64", _p(x), float(s), _p(out), x.numel(), _dtype_code(x), _stream())
+    return out

@@ -1,0 +1,364 @@
+"""GPU parity: every CUDA operator against the reference's golden vectors and
+the CPU oracle.  Bit-exact for graph construction, schedules, factor tables,
+reference-order SpMM, SDDMM and edge softmax; the fp32-guarded SpMM within the
+SURVEY Appendix A tolerance (|y - y_f64| <= 1e-2 * max(1, |y_f64|))."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from conftest import bits, golden_cases, load_golden
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-2  # SURVEY Appendix A, rule (1)
+
+
+def _dg(n, rows, cols, dev):
+    from paper_2411_01109_b200.device import DeviceGraph
+
+    return DeviceGraph.from_edges(n, np.asarray(rows), np.asarray(cols), device=dev)
+
+
+def _t(a, dev):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+
+# ── graph construction ───────────────────────────────────────────────────
+
+
+def test_build_csr_and_transpose_golden(cuda):
+    from paper_2411_01109_b200 import device as D
+
+    cases, _ = golden_cases("graph_build.npz")
+    for c in cases:
+        n = int(c["n"])
+        off, cols, rows = D.build_csr(n, _t(c["rows_in"], cuda), _t(c["cols_in"], cuda), True)
+        np.testing.assert_array_equal(off.cpu().numpy(), c["offsets"])
+        np.testing.assert_array_equal(cols.cpu().numpy(), c["cols"])
+        np.testing.assert_array_equal(rows.cpu().numpy(), c["rows"])
+        t_off, t_cols, perm = D.transpose_csr(off, cols, n)
+        np.testing.assert_array_equal(perm.cpu().numpy(), c["perm"])
+        np.testing.assert_array_equal(t_cols.cpu().numpy(), c["t_cols"])
+        np.testing.assert_array_equal(np.diff(t_off.cpu().numpy()), c["coldeg"])
+        # symmetrize / self loops = canonicalisation of the concatenation
+        r, cc = c["rows"], c["cols"]
+        off2, cols2, rows2 = D.build_csr(n, _t(np.r_[r, cc], cuda), _t(np.r_[cc, r], cuda), True)
+        np.testing.assert_array_equal(rows2.cpu().numpy(), c["sym_rows"])
+        np.testing.assert_array_equal(cols2.cpu().numpy(), c["sym_cols"])
+        v = np.arange(n)
+        off3, cols3, rows3 = D.build_csr(n, _t(np.r_[r, v], cuda), _t(np.r_[cc, v], cuda), True)
+        np.testing.assert_array_equal(rows3.cpu().numpy(), c["loop_rows"])
+        np.testing.assert_array_equal(cols3.cpu().numpy(), c["loop_cols"])
+
+
+def test_build_csr_errors(cuda):
+    from paper_2411_01109_b200 import device as D
+
+    with pytest.raises(ValueError, match="negative vertex id"):
+        D.build_csr(4, _t(np.array([0, -1]), cuda), _t(np.array([1, 2]), cuda))
+    with pytest.raises(ValueError, match="out of range"):
+        D.build_csr(4, _t(np.array([0, 4]), cuda), _t(np.array([1, 2]), cuda))
+
+
+def test_build_csr_large_random_vs_oracle(cuda):
+    from paper_2411_01109_b200 import device as D
+
+    rng = np.random.default_rng(7)
+    n, m = 200_000, 3_000_000
+    rows = rng.integers(0, n, m)
+    cols = (rows + rng.integers(-50, 50, m)) % n
+    off, c32, r64 = D.build_csr(n, _t(rows, cuda), _t(cols, cuda), True)
+    wr, wc = O.canonical_edges(n, rows, cols)
+    np.testing.assert_array_equal(r64.cpu().numpy(), wr)
+    np.testing.assert_array_equal(c32.cpu().numpy(), wc)
+    np.testing.assert_array_equal(off.cpu().numpy(), O.csr_offsets(n, wr))
+    _, _, perm = D.transpose_csr(off, c32, n)
+    np.testing.assert_array_equal(perm.cpu().numpy(), O.transpose_perm(n, wr, wc)[2])
+
+
+def test_factors_golden(cuda):
+    from paper_2411_01109_b200 import device as D
+
+    g = load_golden("factors.npz")
+    deg = g["deg"]
+    off = _t(np.r_[0, np.cumsum(deg)].astype(np.int64), cuda)
+    for dt, tag in ((torch.float16, "h"), (torch.float32, "f")):
+        inv = D.degree_factors(off, "inv", dt).cpu().numpy()
+        isq = D.degree_factors(off, "inv_sqrt", dt).cpu().numpy()
+        np.testing.assert_array_equal(bits(inv), bits(g[f"inv_{tag}"]))
+        np.testing.assert_array_equal(bits(isq), bits(g[f"isqrt_{tag}"]))
+
+
+@pytest.mark.parametrize("cap", [4, 32, 512])
+def test_schedule_matches_restatement(cuda, cap):
+    from paper_2411_01109_b200 import device as D
+
+    rng = np.random.default_rng(cap)
+    deg = np.concatenate([np.zeros(50, np.int64), rng.integers(0, 3 * cap, 3000),
+                          np.array([20 * cap + 3, 7 * cap])])
+    rng.shuffle(deg)
+    off = np.r_[0, np.cumsum(deg)].astype(np.int64)
+    s = D.build_schedule(_t(off, cuda), cap)
+    units, split_rows, slots = O.schedule_units(off, cap)
+    np.testing.assert_array_equal(s.units.cpu().numpy(), units)
+    np.testing.assert_array_equal(s.split_rows.cpu().numpy(), split_rows)
+    assert s.num_slots == slots
+
+
+# ── reference-order SpMM (bit-exact) ─────────────────────────────────────
+
+
+def test_spmm_edge_ref_golden(cuda):
+    from paper_2411_01109_b200 import device as D
+
+    cases, _ = golden_cases("spmm_edge.npz")
+    for i, c in enumerate(cases):
+        n = int(c["n"])
+        dg = _dg(n, c["rows"], c["cols"], cuda)
+        x = _t(c["x"], cuda)
+        w = _t(c["w"], cuda) if "w" in c else None
+        y, st_rows, st_vals = D.spmm_edge_ref(dg, x, w, str(c["scaling"]), str(c["norm"]),
+                                              warp_chunk=int(c["chunk"]),
+                                              warps_per_cta=int(c["wpc"]), staging=True)
+        np.testing.assert_array_equal(bits(y.cpu().numpy()), bits(c["y"]), err_msg=f"case {i}")
+        np.testing.assert_array_equal(st_rows.cpu().numpy(), c["st_rows"], err_msg=f"case {i}")
+        np.testing.assert_array_equal(bits(st_vals.cpu().numpy()), bits(c["st_vals"]),
+                                      err_msg=f"case {i}")
+
+
+def test_spmm_vertex_ref_golden(cuda):
+    from paper_2411_01109_b200 import device as D
+    from paper_2411_01109_b200.device import DeviceGraph
+
+    cases, _ = golden_cases("spmm_vertex.npz")
+    for i, c in enumerate(cases):
+        n = int(c["n"])
+        rows = O.rows_from_offsets(c["offsets"])
+        dg = DeviceGraph.from_edges(n, rows, c["cols"], device=cuda)
+        y, st_rows, st_vals = D.spmm_vertex_ref(dg, _t(c["x"], cuda), str(c["scaling"]),
+                                                str(c["norm"]), staging=True)
+        np.testing.assert_array_equal(bits(y.cpu().numpy()), bits(c["y"]), err_msg=f"case {i}")
+        np.testing.assert_array_equal(st_rows.cpu().numpy(), c["st_rows"])
+        np.testing.assert_array_equal(bits(st_vals.cpu().numpy()), bits(c["st_vals"]))
+
+
+@pytest.mark.parametrize("scaling,norm", [("post", "both"), ("discretized", "both"),
+                                          ("pre", "right"), ("post", "none")])
+@pytest.mark.parametrize("f", [16, 64, 256])
+def test_spmm_edge_ref_vs_oracle_powerlaw(cuda, scaling, norm, f):
+    from paper_2411_01109_b200 import device as D
+
+    rng = np.random.default_rng(f)
+    n = 3000
+    deg = np.minimum(rng.zipf(1.8, n), 2500)
+    rows = np.repeat(np.arange(n), deg)
+    cols = rng.integers(0, n, rows.size)
+    r, c = O.canonical_edges(n, rows, cols)
+    x = rng.normal(0, 1, (n, f)).astype(np.float16)
+    want, wrows, wvals = O.spmm_edge_parallel(n, r, c, x, None, 128, 4, scaling, norm)
+    dg = _dg(n, r, c, cuda)
+    y, srow, sval = D.spmm_edge_ref(dg, _t(x, cuda), None, scaling, norm, staging=True)
+    np.testing.assert_array_equal(bits(y.cpu().numpy()), bits(want))
+    np.testing.assert_array_equal(srow.cpu().numpy(), wrows)
+    np.testing.assert_array_equal(bits(sval.cpu().numpy()), bits(wvals))
+
+
+def test_hub_known_answers(cuda):
+    """test_acceptance.py:97-122: post -> INF in exactly the hub row, discretized 29904."""
+    from paper_2411_01109_b200 import device as D
+
+    n = 1025
+    dg = _dg(n, np.zeros(n - 1, np.int64), np.arange(1, n), cuda)
+    x = torch.full((n, 32), 30000.0, dtype=torch.float16, device=cuda)
+    y_post = D.spmm_edge_ref(dg, x, None, "post", "right").cpu().numpy()
+    assert np.isinf(y_post[0]).all() and np.isinf(y_post).sum() == 32
+    y_disc = D.spmm_edge_ref(dg, x, None, "discretized", "right").cpu().numpy()
+    assert np.isfinite(y_disc).all() and float(y_disc[0, 0]) == 29904.0
+    # the fp32-guarded kernel keeps the post-mode overflow of raw sums and is exact otherwise
+    yf = D.spmm(dg, x, None, "post", "right").cpu().numpy()
+    assert np.isinf(yf[0]).all() and np.isinf(yf).sum() == 32
+    yd = D.spmm(dg, x, None, "discretized", "right").cpu().numpy()
+    assert float(yd[0, 0]) == 30000.0
+
+
+# ── fp32-guarded SpMM (tolerance) ────────────────────────────────────────
+
+
+def _powerlaw(rng, n, alpha=1.7, cap=5000):
+    deg = np.minimum(rng.zipf(alpha, n), cap)
+    deg[rng.random(n) < 0.1] = 0
+    rows = np.repeat(np.arange(n), deg)
+    cols = rng.integers(0, n, rows.size)
+    return O.canonical_edges(n, rows, cols)
+
+
+def _check_tol(got, want, label):
+    err = np.abs(got.astype(np.float64) - want)
+    lim = TOL * np.maximum(1.0, np.abs(want))
+    bad = ~(err <= lim)
+    assert not bad.any(), f"{label}: {bad.sum()} entries outside tolerance, max err {err.max()}"
+
+
+@pytest.mark.parametrize("f", [2, 6, 8, 16, 42, 48, 64, 128, 256, 512, 1024])
+@pytest.mark.parametrize("scaling,norm", [("post", "none"), ("discretized", "both"),
+                                          ("pre", "left"), ("post", "right")])
+def test_spmm_fast_vs_f64(cuda, f, scaling, norm):
+    from paper_2411_01109_b200 import device as D
+
+    rng = np.random.default_rng(f * 7 + len(norm))
+    n = 4000
+    r, c = _powerlaw(rng, n)
+    x = rng.normal(0, 1, (n, f)).astype(np.float16)
+    dg = _dg(n, r, c, cuda)
+    fin, fout = O.norm_factors(n, r, c, norm, np.float16)
+    want = O.spmm_f64(n, r, c, x, None, fin, fout)
+    got = D.spmm(dg, _t(x, cuda), None, scaling, norm).cpu().numpy()
+    _check_tol(got, want, f"F={f} {scaling}/{norm}")
+    # rule (2): agreement with the reference order up to the reference's own error
+    ref = O.spmm_edge_parallel(n, r, c, x, None, 128, 4, scaling, norm)[0].astype(np.float64)
+    slack = TOL * np.maximum(1.0, np.abs(ref)) + np.abs(ref - want)
+    assert np.all(np.abs(got - ref) <= slack + 1e-12)
+
+
+@pytest.mark.parametrize("heads,fh", [(1, 16), (1, 64), (4, 16), (4, 64), (8, 8), (2, 6)])
+def test_spmm_fast_weighted_heads(cuda, heads, fh):
+    from paper_2411_01109_b200 import device as D
+
+    rng = np.random.default_rng(heads * 100 + fh)
+    n = 2000
+    r, c = _powerlaw(rng, n, cap=1500)
+    f = heads * fh
+    x = rng.normal(0, 1, (n, f)).astype(np.float16)
+    w = rng.uniform(0.5, 1.5, (r.size, heads)).astype(np.float16)
+    dg = _dg(n, r, c, cuda)
+    got = D.spmm(dg, _t(x, cuda), _t(w, cuda), heads=heads).cpu().numpy()
+    want = np.concatenate([O.spmm_f64(n, r, c, x[:, h * fh:(h + 1) * fh], w[:, h])
+                           for h in range(heads)], axis=1)
+    _check_tol(got, want, f"heads={heads} fh={fh}")
+    # transposed traversal with weights read through perm (spmm_weighted backward)
+    got_t = D.spmm(dg, _t(x, cuda), _t(w, cuda), heads=heads, transpose=True,
+                   weight_via_perm=True).cpu().numpy()
+    tr, tc, perm = O.transpose_perm(n, r, c)
+    want_t = np.concatenate([O.spmm_f64(n, tr, tc, x[:, h * fh:(h + 1) * fh], w[perm, h])
+                             for h in range(heads)], axis=1)
+    _check_tol(got_t, want_t, f"transposed heads={heads} fh={fh}")
+
+
+def test_spmm_fast_deterministic(cuda):
+    from paper_2411_01109_b200 import device as D
+
+    rng = np.random.default_rng(3)
+    n = 5000
+    r, c = _powerlaw(rng, n, alpha=1.5, cap=20000)
+    dg = _dg(n, r, c, cuda)
+    x = torch.randn(n, 64, device=cuda, dtype=torch.float16)
+    a = D.spmm(dg, x, None, "discretized", "both")
+    for _ in range(3):
+        assert torch.equal(a, D.spmm(dg, x, None, "discretized", "both"))
+
+
+def test_spmm_empty_and_isolated(cuda):
+    from paper_2411_01109_b200 import device as D
+    from paper_2411_01109_b200.device import DeviceGraph
+
+    dg = DeviceGraph.from_edges(4, np.zeros(0, np.int64), np.zeros(0, np.int64), device=cuda)
+    x = torch.ones(4, 8, dtype=torch.float16, device=cuda)
+    assert not D.spmm(dg, x).any()
+    assert not D.spmm_edge_ref(dg, x).any()
+    dg = DeviceGraph.from_edges(5, np.array([0]), np.array([1]), device=cuda)
+    x = torch.ones(5, 4, dtype=torch.float16, device=cuda)
+    y = D.spmm(dg, x, None, "post", "both").cpu().numpy()
+    assert y[0, 0] == 1.0 and not y[1:].any()
+
+
+# ── SDDMM / attention / softmax (bit-exact) ──────────────────────────────
+
+
+def test_sddmm_golden(cuda):
+    from paper_2411_01109_b200 import device as D
+
+    cases, _ = golden_cases("sddmm.npz")
+    for i, c in enumerate(cases):
+        dg = _dg(int(c["n"]), c["rows"], c["cols"], cuda)
+        out = D.sddmm(dg, _t(c["x"], cuda), _t(c["y"], cuda)).cpu().numpy()
+        np.testing.assert_array_equal(bits(out), bits(c["out"]), err_msg=f"case {i}")
+
+
+@pytest.mark.parametrize("heads,fh", [(1, 256), (1, 512), (4, 64), (2, 48), (8, 16), (4, 128)])
+def test_sddmm_heads_vs_oracle(cuda, heads, fh):
+    from paper_2411_01109_b200 import device as D
+
+    rng = np.random.default_rng(fh + heads)
+    n = 700
+    r, c = _powerlaw(rng, n, cap=600)
+    f = heads * fh
+    x = rng.normal(0, 1, (n, f)).astype(np.float16)
+    y = rng.normal(0, 1, (n, f)).astype(np.float16)
+    dg = _dg(n, r, c, cuda)
+    got = D.sddmm(dg, _t(x, cuda), _t(y, cuda), heads=heads).cpu().numpy()
+    want = O.sddmm(r, c, x, y, heads=heads)
+    np.testing.assert_array_equal(bits(got), bits(want))
+
+
+def test_attention_softmax_golden(cuda):
+    from paper_2411_01109_b200 import device as D
+
+    cases, d = golden_cases("attention.npz")
+    for i, c in enumerate(cases):
+        dg = _dg(int(c["n"]), c["rows"], c["cols"], cuda)
+        sl = _t(c["sl"][:, None], cuda)
+        sr = _t(c["sr"][:, None], cuda)
+        e2 = D.attention_logits(dg, sl, sr)[:, 0]
+        np.testing.assert_array_equal(bits(e2.cpu().numpy()), bits(c["e2"]), err_msg=f"case {i}")
+        alpha = D.edge_softmax_fwd(dg, e2)
+        np.testing.assert_array_equal(bits(alpha.cpu().numpy()), bits(c["alpha"]))
+        de = D.edge_softmax_bwd(dg, alpha, _t(c["seed"], cuda))
+        np.testing.assert_array_equal(bits(de.cpu().numpy()), bits(c["g_e2"]))
+
+
+def test_shadow_exp_exhaustive(cuda):
+    """Every non-positive half through the softmax exp path: row i holds
+    scores [v_i, 0] so ex = rnd(exp(v_i)) (test_acceptance.py:247-253)."""
+    from paper_2411_01109_b200 import device as D
+
+    vals = load_golden("attention.npz")["exp_in"]
+    n = vals.size
+    rows = np.repeat(np.arange(n), 2)
+    cols = np.stack([np.arange(n), (np.arange(n) + 1) % n], 1).reshape(-1)
+    r, c = O.canonical_edges(n, rows, cols)
+    dg = _dg(n, r, c, cuda)
+    e = np.zeros(r.size, np.float16)
+    diag = c == r
+    e[diag] = vals[r[diag]]
+    alpha = D.edge_softmax_fwd(dg, _t(e, cuda)).cpu().numpy()
+    want = O.edge_softmax_fwd(O.csr_offsets(n, r), e)
+    np.testing.assert_array_equal(bits(alpha), bits(want))
+
+
+def test_softmax_heads_long_rows_vs_oracle(cuda):
+    from paper_2411_01109_b200 import device as D
+
+    rng = np.random.default_rng(11)
+    n = 600
+    r, c = _powerlaw(rng, n, alpha=1.4, cap=590)
+    dg = _dg(n, r, c, cuda)
+    e = rng.uniform(-6, 6, (r.size, 4)).astype(np.float16)
+    g = rng.normal(size=(r.size, 4)).astype(np.float16)
+    off = O.csr_offsets(n, r)
+    alpha = D.edge_softmax_fwd(dg, _t(e, cuda))
+    np.testing.assert_array_equal(bits(alpha.cpu().numpy()), bits(O.edge_softmax_fwd(off, e)))
+    de = D.edge_softmax_bwd(dg, alpha, _t(g, cuda)).cpu().numpy()
+    np.testing.assert_array_equal(bits(de), bits(O.edge_softmax_bwd(off, alpha.cpu().numpy(), g)))
+
+
+def test_scale_f64_matches_numpy(cuda):
+    from paper_2411_01109_b200 import device as D
+
+    allv = np.arange(65536, dtype=np.uint16).view(np.float16)
+    allv = allv[np.isfinite(allv)]
+    got = D.scale_f64(_t(allv, cuda), 0.2).cpu().numpy()
+    want = (allv.astype(np.float64) * 0.2).astype(np.float16)
+    np.testing.assert_array_equal(bits(got), bits(want))
