@@ -1,0 +1,364 @@
+"""Benchmark: GCN training epoch on the Reddit-shaped graph (BASELINE config C3).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+A step is one full-batch training epoch -- forward, loss, backward, Adam -- of
+the paper's 2-layer GCN (hidden 64, fp16, discretized/both norm) on a
+synthetic Reddit-shaped graph (N=232,965, E=114,848,857, 602 features, 41
+classes).  value = ms/epoch with inputs resident in HBM (device-timed, max over
+ranks); e2e = the same through the public training loop with the features
+copied from pinned host memory every epoch and the loss read back.
+
+The dominant kernel is the fp32-guarded SpMM (k_spmm_fast); its roofline uses
+the gather-model algorithmic bytes of every hg_spmm launch in the timed region
+ over their CUDA-event durations, against MEASURED_PEAKS.json.
+The CPU baseline times the numpy restatement of the reference (oracle/) on a
+row-panel sample of the same workload and extrapolates the sparse part by E.
+Under torchrun (N > 1) the graph is row-partitioned and features are
+all-gathered over NCCL before every aggregation (partition.py).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "GCN/GAT ms/epoch at 1/2/4/8 B200; half2 SpMM GB/s vs HBM peak"
+N_FEAT, N_CLASSES, HIDDEN = 602, 41, 64
+
+
+def peaks():
+    try:
+        d = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return d["hbm_gbs"] * 1e9, "measured"
+    except Exception:
+        return 6.65e12, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during timing."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index=0):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in Path(self.path).read_text().splitlines():
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        except OSError:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def load_traffic_profile(f_key):
+    """ncu dram bytes per launch of k_spmm_fast from the committed profile summary."""
+    p = ROOT / "profiles" / "r01" / "ncu_spmm_summary.json"
+    try:
+        d = json.loads(p.read_text())
+        return d.get(str(f_key))
+    except Exception:
+        return None
+
+
+# ── CPU baseline (oracle restatement of the reference, row-panel sample) ──
+
+
+def cpu_baseline_gcn(offsets, cols, x16, labels, budget_edges, hidden=HIDDEN):
+    """Time one reference GCN epoch (oracle.train_epochs) on the first rows of the
+    graph holding ~budget_edges edges (all N vertices, all features), then
+    extrapolate: t = dense + sparse * E / E_sample.  Returns (ms, sample text, cores)."""
+    import numpy as np
+
+    import oracle as O
+
+    n = offsets.size - 1
+    e_total = int(offsets[-1])
+    r_end = int(np.searchsorted(offsets, budget_edges, side="left"))
+    r_end = max(1, min(r_end, n))
+    e_s = int(offsets[r_end])
+    rows = np.repeat(np.arange(r_end, dtype=np.int64), np.diff(offsets[: r_end + 1]))
+    g = O.OracleGraph(n, rows, cols[:e_s].astype(np.int64))
+    timer = O.Timer()
+    t0 = time.perf_counter()
+    O.train_epochs(g, x16.astype(np.float32), labels, kind="gcn", mode="half", epochs=1,
+                   hidden=hidden, timer=timer)
+    wall = time.perf_counter() - t0
+    other = max(0.0, wall - timer.dense - timer.sparse)
+    ms = (timer.dense + other + timer.sparse * e_total / max(e_s, 1)) * 1e3
+    sample = (f"rows [0,{r_end}) = {e_s:,} of {e_total:,} edges, all {n:,} vertices; "
+              f"sparse {timer.sparse:.2f}s x{e_total / max(e_s, 1):.1f} + dense {timer.dense:.2f}s"
+              f" + other {other:.2f}s")
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except AttributeError:
+        cores = os.cpu_count() or 1
+    return ms, sample, cores
+
+
+def reference_arm(args, ws, rank):
+    """--impl reference: the reference's CPU path (oracle port) on this host, rank 0 only."""
+    if rank != 0:
+        return
+    import numpy as np
+    import torch
+
+    from paper_2411_01109_b200 import graphgen
+
+    have_gpu = torch.cuda.is_available()
+    dev = "cuda" if have_gpu else "cpu"
+    if have_gpu:
+        dg = graphgen.reddit_like(args.seed)
+        offsets = dg.offsets.cpu().numpy()
+        cols = dg.cols.cpu().numpy()
+        x, labels = graphgen.planted_features(dg.n, N_FEAT, N_CLASSES, args.seed, dev)
+        x16, lab = x.cpu().numpy(), labels.cpu().numpy()
+    else:
+        raise SystemExit("reference arm needs the graph generator (GPU)")
+    steps = args.steps + args.warmup
+    budget = max(50_000, int(args.ref_budget_edges * 10 / max(steps, 1)))
+    vals = []
+    sample = cores = None
+    for i in range(steps):
+        ms, sample, cores = cpu_baseline_gcn(offsets, cols, x16, lab, budget)
+        if i >= args.warmup:
+            vals.append(ms)
+    v = statistics.median(vals) if vals else ms
+    line = {"metric": METRIC, "value": v, "unit": "ms/epoch", "impl": "reference",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": v,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f16", "data": "synthetic",
+            "config": workload_config(int(offsets.size - 1), int(offsets[-1])),
+            "cpu_baseline": {"value": v, "unit": "ms/epoch", "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "ms/epoch", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(n, e, parallelism="dp1"):
+    return {"workload": "GCN 2-layer train epoch, synthetic Reddit-shaped graph (C3)",
+            "nodes": n, "edges": e, "feat": N_FEAT, "hidden": HIDDEN, "classes": N_CLASSES,
+            "reduction": "discretized/both", "numerics": "fp32-guarded SpMM",
+            "l2": "inputs larger than L2 (column stream 459 MB, features 280 MB)",
+            "parallelism": parallelism}
+
+
+# ── B200 arm ─────────────────────────────────────────────────────────────
+
+
+def spmm_sweep(dg, peak, feats=(16, 32, 64, 128, 256, 512), reps=3):
+    import torch
+
+    from paper_2411_01109_b200 import device as D
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    out = {}
+    for f in feats:
+        x = torch.randn(dg.n, f, device="cuda", dtype=torch.float16)
+        D.spmm(dg, x, None, "discretized", "both")
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            D.spmm(dg, x, None, "discretized", "both")
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b) / 1e3)
+        t = statistics.median(ts)
+        byts = D.spmm_bytes(dg.n, dg.n, dg.num_edges, f)
+        out[str(f)] = {"ms": round(t * 1e3, 4), "GBps": round(byts / t / 1e9, 1),
+                       "frac": round(byts / t / peak, 4)}
+        del x
+    del flush
+    return out
+
+
+def b200_arm(args, ws, rank, local):
+    import numpy as np
+    import torch
+
+    from paper_2411_01109_b200 import device as D
+    from paper_2411_01109_b200 import graphgen
+    from paper_2411_01109_b200.models import GraphBundle, Trainer, TrainConfig
+
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peak, peak_kind = peaks()
+    t_setup = time.time()
+    dg = graphgen.reddit_like(args.seed)
+    x, labels = graphgen.planted_features(dg.n, N_FEAT, N_CLASSES, args.seed, "cuda")
+    cfg = TrainConfig(kind="gcn", mode="half", hidden=HIDDEN, seed=args.seed,
+                      scaling="discretized", norm="both", numerics="fast")
+    if ws > 1:
+        from paper_2411_01109_b200.partition import DistTrainer
+
+        tr = DistTrainer(dg, x, labels, cfg, dist)
+        parallelism = f"row-partition x{ws} (NCCL all-gather)"
+    else:
+        tr = Trainer(GraphBundle.build(dg, numerics="fast"), x, labels, cfg)
+        parallelism = "dp1"
+    for _ in range(args.warmup):
+        tr.step()
+    torch.cuda.synchronize()
+    setup_s = time.time() - t_setup
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    # ---- device-resident timing (value) ----
+    D.Probe.reset(timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for _ in range(args.steps):
+            loss, _ = tr.step()
+        ev1.record()
+        torch.cuda.synchronize()
+        barrier()
+    launches = D.Probe.launches
+    spmm_b, spmm_s, spmm_n = D.Probe.summary()
+    D.Probe.reset(timing=False)
+    t_ms = ev0.elapsed_time(ev1) / args.steps
+    if dist is not None:
+        tt = torch.tensor([t_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    final_loss = float(loss)
+
+    # ---- end to end through the public loop: host features in, loss out ----
+    host_x = x.cpu().pin_memory()
+    h2d = host_x.numel() * host_x.element_size() // (ws if ws > 1 else 1)
+    barrier()
+    torch.cuda.synchronize()
+    e0 = time.perf_counter()
+    for _ in range(args.steps):
+        tr.load_features(host_x, out=tr.x) if ws == 1 else tr.load_features(host_x)
+        loss, _ = tr.step()
+        float(loss)  # the reference loop's NaN check reads the loss every epoch
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = (time.perf_counter() - e0) * 1e3 / args.steps
+    if dist is not None:
+        tt = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+
+    result = None
+    if rank == 0:
+        achieved = spmm_b / spmm_s if spmm_s > 0 else 0.0
+        traffic = load_traffic_profile("gcn_epoch")
+        result = {
+            "metric": METRIC, "value": round(t_ms, 4), "unit": "ms/epoch", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_ms, 4),
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f16", "data": "synthetic (seeded Reddit-shaped graph, planted labels)",
+            "config": workload_config(dg.n, dg.num_edges, parallelism),
+            "clocks": clocks.summary(),
+            "e2e": {"value": round(e2e_ms, 4), "unit": "ms/epoch", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": 4},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "hbm", "achieved": round(achieved / 1e9, 1),
+                         "peak": round(peak / 1e9, 1), "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "kernel": "k_spmm_fast (hg_spmm)", "launches": spmm_n,
+                         "peak_source": peak_kind,
+                         "bytes_model": "4E+8(N+1)+2FE+2FN per SpMM launch, F = stored width"},
+            "final_loss": round(final_loss, 5),
+            "setup_s": round(setup_s, 1),
+        }
+    if not args.no_sweep and ws == 1:
+        result["spmm_sweep_reddit"] = spmm_sweep(dg, peak)
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        offsets = dg.offsets.cpu().numpy()
+        cols = dg.cols.cpu().numpy()
+        ms, sample, cores = cpu_baseline_gcn(offsets, cols, x.cpu().numpy(),
+                                             labels.cpu().numpy(), args.cpu_budget_edges)
+        result["cpu_baseline"] = {"value": round(ms, 1), "unit": "ms/epoch", "cores": cores,
+                                  "kind": "port", "sample": sample}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-edges", type=int, default=400_000)
+    ap.add_argument("--ref-budget-edges", type=int, default=400_000)
+    args = ap.parse_args()
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        reference_arm(args, ws, rank)
+        return
+    b200_arm(args, ws, rank, local)
+
+
+if __name__ == "__main__":
+    main()

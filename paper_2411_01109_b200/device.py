@@ -47,6 +47,36 @@ def _dtype_code(t):
 _WS = {}
 
 
+class Probe:
+    """Launch accounting for the bench: `launches` counts libhalfgnn kernels;
+    when `timing` is on, hg_spmm calls are bracketed by CUDA events on the
+    launching stream and logged with their algorithmic bytes."""
+
+    launches = 0
+    timing = False
+    records = []
+
+    @classmethod
+    def reset(cls, timing=False):
+        cls.launches = 0
+        cls.timing = timing
+        cls.records = []
+
+    @classmethod
+    def summary(cls):
+        """(total algorithmic bytes, total seconds, launches) of the timed spmm calls."""
+        torch.cuda.synchronize()
+        tb = sum(r[2] for r in cls.records)
+        ts = sum(r[0].elapsed_time(r[1]) for r in cls.records) / 1e3
+        return tb, ts, len(cls.records)
+
+
+def spmm_bytes(n_rows, n_cols, num_edges, f, heads=0, elem=2):
+    """Gather-model bytes of one SpMM: 4E + 8(N+1) + 2F*E + 2F*N (+2E*H)."""
+    return (4 * num_edges + 8 * (n_rows + 1) + elem * f * num_edges + elem * f * n_cols
+            + elem * num_edges * heads)
+
+
 def workspace(nbytes: int, device) -> torch.Tensor | None:
     """Per-(device, stream) scratch from torch's caching allocator, grown on demand.
     Kernels on one stream run in order, so one buffer per stream is safe."""
@@ -254,11 +284,22 @@ def spmm_csr(view: CsrView, x: torch.Tensor, w=None, w_index=None, heads: int = 
         w = w.contiguous()
         if w.dtype != x.dtype:
             raise ValueError("edge weights must match the feature dtype")
+    if Probe.timing:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
     nat.call("hg_spmm", _p(view.offsets), _p(view.cols), view.n_rows, view.n_cols,
              view.num_edges, _p(sched.units), sched.num_units, _p(sched.split_rows),
              sched.split_rows.shape[0], sched.num_slots, _p(w), _p(w_index), heads, _p(x),
              _p(out), f, nat.SCALING_CODES[scaling], _p(fin), _p(fout), dt, _p(ws),
              0 if ws is None else ws.numel(), _stream())
+    Probe.launches += int(sched.num_units > 0) + int(sched.split_rows.shape[0] > 0) + int(
+        fin is not None)
+    if Probe.timing:
+        ev1.record()
+        Probe.records.append((ev0, ev1, spmm_bytes(view.n_rows, view.n_cols, view.num_edges, f,
+                                                   heads if w is not None else 0,
+                                                   x.element_size())))
     return out
 
 
@@ -300,6 +341,7 @@ def spmm_edge_ref(dg: DeviceGraph, x, w=None, scaling="post", norm="none", trans
              warp_chunk, warps_per_cta, _p(w), _p(x), _p(y), f, nat.SCALING_CODES[scaling],
              _p(fin), _p(fout), _p(st_vals), _p(st_rows), dt, _p(ws),
              0 if ws is None else ws.numel(), _stream())
+    Probe.launches += 2 + int(fin is not None)
     if staging:
         return y, st_rows[:nc], st_vals[:nc]
     return y
@@ -354,6 +396,7 @@ def sddmm(dg: DeviceGraph, x, y, heads=1, transpose=False):
     nat.call("hg_sddmm", _p(view.offsets), _p(view.cols), view.n_rows, view.num_edges,
              _p(sched.units), sched.num_units, _p(x), _p(y), _p(out), f, heads,
              _dtype_code(x), _stream())
+    Probe.launches += 1
     return out[:, 0] if heads == 1 else out
 
 
@@ -365,6 +408,7 @@ def attention_logits(dg: DeviceGraph, s_l, s_r, slope=0.2):
     out = torch.empty((dg.num_edges, heads), dtype=s_l.dtype, device=s_l.device)
     nat.call("hg_attn_scores", _p(dg.offsets), _p(dg.cols), dg.n, dg.num_edges, _p(s_l),
              _p(s_r), heads, float(slope), _p(out), _dtype_code(s_l), _stream())
+    Probe.launches += 1
     return out
 
 
@@ -375,6 +419,7 @@ def edge_softmax_fwd(dg: DeviceGraph, e):
     alpha = torch.empty_like(e)
     nat.call("hg_edge_softmax_fwd", _p(dg.offsets), dg.n, dg.num_edges, _p(e), _p(alpha), heads,
              _dtype_code(e), _stream())
+    Probe.launches += 1
     return alpha
 
 
@@ -384,6 +429,7 @@ def edge_softmax_bwd(dg: DeviceGraph, alpha, g):
     de = torch.empty_like(alpha)
     nat.call("hg_edge_softmax_bwd", _p(dg.offsets), dg.n, dg.num_edges, _p(alpha), _p(g),
              _p(de), heads, _dtype_code(alpha), _stream())
+    Probe.launches += 1
     return de
 
 
@@ -395,6 +441,7 @@ def edge_rowsum(dg: DeviceGraph, v, transpose=False):
     out = torch.empty((view.n_rows, heads), dtype=v.dtype, device=v.device)
     nat.call("hg_edge_rowsum", _p(view.offsets), view.n_rows, view.num_edges, _p(v),
              _p(view.perm if transpose else None), heads, _p(out), _dtype_code(v), _stream())
+    Probe.launches += 1
     return out
 
 
@@ -403,4 +450,5 @@ def scale_f64(x, s: float):
     x = x.contiguous()
     out = torch.empty_like(x)
     nat.call("hg_scale_f64", _p(x), float(s), _p(out), x.numel(), _dtype_code(x), _stream())
+    Probe.launches += 1
     return out

@@ -1,0 +1,779 @@
+"""Mixed-precision GNN training on the B200 kernels (halfsparse/models.py API).
+
+torch autograd replaces the reference's tape (models.py:85-127); the sparse
+operators are torch.autograd.Functions over libhalfgnn:
+
+  spmm_agg        forward hg_spmm on the CSR, backward on the CSC with the
+                  norm mirrored (the exact adjoint, models.py:274-290)
+  spmm_weighted   forward weighted SpMM; backward SDDMM for dw and a
+                  transposed weighted SpMM reading w through perm (293-314)
+  attention       hg_attn_scores (+ leaky ReLU fused), backward row/column
+                  sums (317-340)
+  edge_softmax    hg_edge_softmax_fwd / _bwd, bit-exact (382-412)
+
+Dense GEMMs use cuBLAS on the tensor cores with fp32 accumulation and one
+rounding, like the reference's fp32-BLAS-then-round matmul (141-158).
+Parameters are fp32 masters published as fp16 leaves every step; only the
+logits cross to fp32, for the loss (203-217, 552-572).
+
+Numerics modes (GraphBundle.numerics): "fast" runs the fp32-guarded SpMM;
+"reference" runs the bit-exact reference-order SpMM for every aggregation.
+SDDMM, scores and softmax are bit-exact in both modes.
+"""
+from __future__ import annotations
+
+import csv
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import device as D
+from .kernels import Reduction
+from .sparse import CooGraph
+
+_DTYPES = {"half": torch.float16, "float32": torch.float32}
+_MIRROR = {"none": "none", "left": "right", "right": "left", "both": "both"}
+
+torch.backends.cuda.matmul.allow_fp16_reduced_precision_reduction = False
+torch.backends.cuda.matmul.allow_tf32 = False
+
+
+class NanLossError(RuntimeError):
+    """Training loss became non-finite; carries the epoch and overflow counters."""
+
+    def __init__(self, epoch, counters):
+        super().__init__(f"loss is NaN at epoch {epoch}")
+        self.epoch = epoch
+        self.counters = counters
+
+
+@dataclass
+class ConversionCounter:
+    forward: int = 0
+    backward: int = 0
+
+    @property
+    def total(self):
+        return self.forward + self.backward
+
+    def reset(self):
+        self.forward = 0
+        self.backward = 0
+
+
+class OverflowCounters:
+    """Non-finite output tallies per (layer, op) tag.  Counting runs on the
+    device; the host copy is taken lazily (one sync when read)."""
+
+    def __init__(self):
+        self._pending = []
+        self._inf = {}
+        self._nan = {}
+
+    def observe(self, tag, t):
+        if isinstance(t, np.ndarray):
+            t = torch.from_numpy(t)
+        self._pending.append((tag, torch.isinf(t).sum(), torch.isnan(t).sum()))
+
+    def _drain(self):
+        for tag, ni, nn in self._pending:
+            ni, nn = int(ni), int(nn)
+            if ni:
+                self._inf[tag] = self._inf.get(tag, 0) + ni
+            if nn:
+                self._nan[tag] = self._nan.get(tag, 0) + nn
+        self._pending.clear()
+
+    @property
+    def inf(self):
+        self._drain()
+        return self._inf
+
+    @property
+    def nan(self):
+        self._drain()
+        return self._nan
+
+    def totals(self):
+        return sum(self.inf.values()), sum(self.nan.values())
+
+    def reset(self):
+        self._pending.clear()
+        self._inf.clear()
+        self._nan.clear()
+
+
+# ── graph bundle ─────────────────────────────────────────────────────────
+
+
+class GraphBundle:
+    """Forward graph + transpose resident in HBM (models.py:246-264)."""
+
+    def __init__(self, dg: D.DeviceGraph, warp_chunk=128, warps_per_cta=4, numerics="fast",
+                 g: CooGraph | None = None):
+        if numerics not in ("fast", "reference"):
+            raise ValueError(f"unknown numerics {numerics!r}")
+        self.dg = dg
+        self.g = g
+        self.warp_chunk = warp_chunk
+        self.warps_per_cta = warps_per_cta
+        self.numerics = numerics
+        self._ones2 = {}
+
+    @classmethod
+    def build(cls, g, warp_chunk=128, warps_per_cta=4, numerics="fast"):
+        if isinstance(g, D.DeviceGraph):
+            return cls(g, warp_chunk, warps_per_cta, numerics)
+        return cls(g.device(), warp_chunk, warps_per_cta, numerics, g)
+
+    @property
+    def n(self):
+        return self.dg.n
+
+    @property
+    def num_edges(self):
+        return self.dg.num_edges
+
+    def spmm(self, x, w=None, scaling="post", norm="none", transpose=False, heads=1,
+             weight_via_perm=False):
+        if self.numerics == "fast":
+            return D.spmm(self.dg, x, w, scaling, norm, transpose, heads,
+                          weight_via_perm=weight_via_perm)
+        # reference order: one head at a time, weights materialised in CSC order
+        if w is not None and weight_via_perm:
+            w = w[self.dg.perm.long()]
+        if heads == 1:
+            w1 = None if w is None else w.reshape(-1)
+            return D.spmm_edge_ref(self.dg, x, w1, scaling, norm, transpose, self.warp_chunk,
+                                   self.warps_per_cta)
+        fh = x.shape[1] // heads
+        outs = [D.spmm_edge_ref(self.dg, x[:, h * fh:(h + 1) * fh].contiguous(),
+                                w[:, h].contiguous(), scaling, norm, transpose,
+                                self.warp_chunk, self.warps_per_cta) for h in range(heads)]
+        return torch.cat(outs, dim=1)
+
+    def edge_sums(self, v, transpose=False):
+        """Row (or column) sums of per-edge values [E, H] -> [N, H]
+        (attention_scores backward, models.py:329-337)."""
+        if self.numerics == "fast":
+            return D.edge_rowsum(self.dg, v, transpose)
+        v2 = v.reshape(v.shape[0], -1)
+        if transpose:
+            v2 = v2[self.dg.perm.long()]
+        ones = self._ones2.get(v.dtype)
+        if ones is None:
+            ones = torch.ones((self.n, 2), dtype=v.dtype, device=v.device)
+            self._ones2[v.dtype] = ones
+        cols = [D.spmm_edge_ref(self.dg, ones, v2[:, h].contiguous(), "post", "none", transpose,
+                                self.warp_chunk, self.warps_per_cta)[:, :1]
+                for h in range(v2.shape[1])]
+        return torch.cat(cols, dim=1)
+
+
+# ── sparse autograd ops ──────────────────────────────────────────────────
+
+
+class _AggFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, bundle, reduction):
+        ctx.bundle, ctx.reduction = bundle, reduction
+        return bundle.spmm(x, None, reduction.scaling, reduction.norm)
+
+    @staticmethod
+    def backward(ctx, g):
+        r = ctx.reduction
+        gx = ctx.bundle.spmm(g.contiguous(), None, r.scaling, _MIRROR[r.norm], transpose=True)
+        return gx, None, None
+
+
+def spmm_agg(bundle, x, reduction, width="half2", overflow=None, tag="agg"):
+    """Y = norm-scaled aggregation of X; the adjoint runs the transposed graph."""
+    y = _AggFn.apply(x, bundle, reduction)
+    if overflow is not None:
+        overflow.observe(tag, y.detach())
+    return y
+
+
+class _WeightedFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, w, x, bundle, heads):
+        ctx.bundle, ctx.heads = bundle, heads
+        ctx.save_for_backward(w, x)
+        return bundle.spmm(x, w, "post", "none", heads=heads)
+
+    @staticmethod
+    def backward(ctx, g):
+        w, x = ctx.saved_tensors
+        b, h = ctx.bundle, ctx.heads
+        g = g.contiguous()
+        gw = gx = None
+        if ctx.needs_input_grad[0]:
+            gw = D.sddmm(b.dg, g, x, heads=h).reshape(w.shape)
+        if ctx.needs_input_grad[1]:
+            gx = b.spmm(g, w, "post", "none", transpose=True, heads=h, weight_via_perm=True)
+        return gw, gx, None, None
+
+
+def spmm_weighted(bundle, w, x, width="half2", overflow=None, tag="agg"):
+    """Y[r] = sum over edges (r, c) of w[e] * X[c] (per head when w is [E, H])."""
+    heads = 1 if w.dim() == 1 else w.shape[1]
+    y = _WeightedFn.apply(w, x, bundle, heads)
+    if overflow is not None:
+        overflow.observe(tag, y.detach())
+    return y
+
+
+class _ScoresFn(torch.autograd.Function):
+    """e = rnd(s_l[row] + s_r[col]), then leaky ReLU (slope None: no activation)."""
+
+    @staticmethod
+    def forward(ctx, s_l, s_r, bundle, slope):
+        out = D.attention_logits(bundle.dg, s_l, s_r, 1.0 if slope is None else slope)
+        ctx.bundle, ctx.slope = bundle, slope
+        ctx.save_for_backward(out)
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        (out,) = ctx.saved_tensors
+        g = g.contiguous()
+        if ctx.slope is not None:
+            g = torch.where(out > 0, g, D.scale_f64(g, ctx.slope))
+        b = ctx.bundle
+        gl = b.edge_sums(g, transpose=False) if ctx.needs_input_grad[0] else None
+        gr = b.edge_sums(g, transpose=True) if ctx.needs_input_grad[1] else None
+        return gl, gr, None, None
+
+
+def attention_scores(bundle, s_l, s_r):
+    """Per-edge s_l[row] + s_r[col] (models.py:317-340); [E] for one head."""
+    one = s_l.dim() == 2 and s_l.shape[1] == 1
+    e = _ScoresFn.apply(s_l, s_r, bundle, None)
+    return e[:, 0] if one else e
+
+
+def attention_logits(bundle, s_l, s_r, slope=0.2):
+    """leaky_relu(attention_scores(s_l, s_r), slope), fused: [E, H]."""
+    return _ScoresFn.apply(s_l, s_r, bundle, slope)
+
+
+class _SoftmaxFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, e, bundle):
+        alpha = D.edge_softmax_fwd(bundle.dg, e)
+        ctx.bundle = bundle
+        ctx.save_for_backward(alpha)
+        return alpha
+
+    @staticmethod
+    def backward(ctx, g):
+        (alpha,) = ctx.saved_tensors
+        return D.edge_softmax_bwd(ctx.bundle.dg, alpha, g.contiguous()), None
+
+
+def edge_softmax(bundle, e, overflow=None, tag="softmax"):
+    """Row softmax over edge scores in the input precision, bit-exact."""
+    alpha = _SoftmaxFn.apply(e, bundle)
+    if overflow is not None:
+        overflow.observe(tag + "/exp", alpha.detach())
+        overflow.observe(tag + "/div", alpha.detach())
+    return alpha
+
+
+def shadow_exp(x, overflow=None, tag="exp"):
+    """exp on non-positive inputs, one rounding (models.py:360-371)."""
+    if bool((x > 0).any()):
+        raise ValueError("shadow_exp expects non-positive inputs")
+    y = torch.exp(x.double()).to(x.dtype)
+    if overflow is not None:
+        overflow.observe(tag, y)
+    return y
+
+
+def shadow_div(num, den, overflow=None, tag="div"):
+    y = (num.double() / den.double()).to(num.dtype)
+    if overflow is not None:
+        overflow.observe(tag, y)
+    return y
+
+
+# ── dense / elementwise ops ──────────────────────────────────────────────
+
+
+def matmul(a, b):
+    """Tensor-core GEMM, fp32 accumulation, one rounding to the input dtype."""
+    return a @ b
+
+
+def add_bias(x, b):
+    return x + b
+
+
+def relu(x):
+    return torch.relu(x)
+
+
+class _LeakyFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, slope):
+        ctx.slope = slope
+        ctx.save_for_backward(x)
+        return torch.where(x > 0, x, D.scale_f64(x, slope))
+
+    @staticmethod
+    def backward(ctx, g):
+        (x,) = ctx.saved_tensors
+        return torch.where(x > 0, g, D.scale_f64(g.contiguous(), ctx.slope)), None
+
+
+def leaky_relu(x, slope=0.2):
+    """where(x > 0, x, rnd(x * slope)), the product in fp64 (models.py:188-200)."""
+    return _LeakyFn.apply(x, slope)
+
+
+class _ConvertFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, dtype, counter):
+        ctx.src, ctx.counter = x.dtype, counter
+        if counter is not None:
+            counter.forward += 1
+        return x.to(dtype)
+
+    @staticmethod
+    def backward(ctx, g):
+        if ctx.counter is not None:
+            ctx.counter.backward += 1
+        return g.to(ctx.src), None, None
+
+
+def convert(x, mode, counter=None):
+    """Precision crossing as a graph op; the only place conversions count."""
+    return _ConvertFn.apply(x, _DTYPES[mode], counter)
+
+
+class _ScaleCombineFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, a, ope, lam):
+        ctx.lam = lam
+        ctx.save_for_backward(x, ope)
+        return x * ope + D.scale_f64(a, lam)
+
+    @staticmethod
+    def backward(ctx, g):
+        x, ope = ctx.saved_tensors
+        g = g.contiguous()
+        gx = g * ope if ctx.needs_input_grad[0] else None
+        ga = D.scale_f64(g, ctx.lam) if ctx.needs_input_grad[1] else None
+        gope = (x.double() * g.double()).sum().to(ope.dtype).reshape(ope.shape) \
+            if ctx.needs_input_grad[2] else None
+        return gx, ga, gope, None
+
+
+def scale_combine(x, a, one_plus_eps, lam):
+    """(1 + eps) * x + lam * a with per-term rounding (GIN combine, models.py:220-240)."""
+    return _ScaleCombineFn.apply(x, a, one_plus_eps, float(lam))
+
+
+# ── parameters and layers ────────────────────────────────────────────────
+
+
+class Param:
+    """fp32 master weight in HBM; publishes a compute-precision leaf each step."""
+
+    def __init__(self, value, device="cuda", store_shape=None):
+        v = torch.as_tensor(np.asarray(value, dtype=np.float32))
+        if store_shape is not None and tuple(store_shape) != tuple(v.shape):
+            padded = torch.zeros(store_shape, dtype=torch.float32)
+            padded[tuple(slice(0, s) for s in v.shape)] = v
+            v = padded
+        self.master = v.to(device)
+        self.published = None
+
+    def publish(self, mode):
+        data = self.master if mode == "float32" else self.master.to(torch.float16)
+        self.published = data.detach().requires_grad_(True)
+        return self.published
+
+    def grad32(self):
+        if self.published is None or self.published.grad is None:
+            return torch.zeros_like(self.master)
+        return self.published.grad.to(torch.float32)
+
+
+def _glorot(rng, fan_in, fan_out, shape=None):
+    """models._glorot (models.py:436-438): same draws, same RNG order."""
+    lim = np.sqrt(6.0 / (fan_in + fan_out))
+    return rng.uniform(-lim, lim, size=shape or (fan_in, fan_out)).astype(np.float32)
+
+
+def _round8(v):
+    return (v + 7) // 8 * 8
+
+
+def _placed(block, store_shape, in_rows=None):
+    """Embed a logical (fan_in, fan_out) block in zero storage; logical input
+    row i goes to storage row in_rows[i] (identity by default)."""
+    out = np.zeros(store_shape, np.float32)
+    rows = np.arange(block.shape[0]) if in_rows is None else np.asarray(in_rows)
+    out[rows, : block.shape[1]] = block
+    return out
+
+
+class Linear:
+    """x @ W (+ b).  Storage may be zero-padded beyond the logical (fan_in,
+    fan_out) so rows stay 16-byte aligned; padded entries stay exactly zero."""
+
+    def __init__(self, rng, fan_in, fan_out, bias=True, device="cuda", store_in=None,
+                 store_out=None, in_rows=None):
+        si, so = store_in or fan_in, store_out or fan_out
+        self.w = Param(_placed(_glorot(rng, fan_in, fan_out), (si, so), in_rows), device)
+        self.b = Param(np.zeros(fan_out, np.float32), device, (so,)) if bias else None
+
+    def params(self):
+        return [self.w] + ([self.b] if self.b is not None else [])
+
+    def __call__(self, x, mode):
+        out = matmul(x, self.w.publish(mode))
+        if self.b is not None:
+            out = add_bias(out, self.b.publish(mode))
+        return out
+
+
+class GCNLayer:
+    """norm-aggregate(X W + b) (models.py:456-468): bias before aggregation."""
+
+    def __init__(self, rng, fan_in, fan_out, reduction, device="cuda", store_in=None,
+                 store_out=None, in_rows=None):
+        self.lin = Linear(rng, fan_in, fan_out, True, device, store_in, store_out, in_rows)
+        self.reduction = reduction
+
+    def params(self):
+        return self.lin.params()
+
+    def __call__(self, bundle, x, mode, width, overflow, tag):
+        return spmm_agg(bundle, self.lin(x, mode), self.reduction, width, overflow, tag)
+
+
+class GINLayer:
+    """phi2(relu(phi1((1+eps) x + lam * mean-agg(x)))) (models.py:471-489)."""
+
+    def __init__(self, rng, fan_in, fan_out, lam=0.1, scaling="discretized", device="cuda",
+                 store_in=None, store_out=None, in_rows=None):
+        if not 0.0 < lam <= 1.0:
+            raise ValueError("lam must be in (0, 1]")
+        self.lam = float(lam)
+        self.reduction = Reduction(scaling, "right")
+        self.one_plus_eps = Param(np.float32(1.0), device)
+        self.phi1 = Linear(rng, fan_in, fan_out, True, device, store_in, store_out, in_rows)
+        self.phi2 = Linear(rng, fan_out, fan_out, True, device, store_out, store_out)
+
+    def params(self):
+        return [self.one_plus_eps] + self.phi1.params() + self.phi2.params()
+
+    def __call__(self, bundle, x, mode, width, overflow, tag):
+        agg = spmm_agg(bundle, x, self.reduction, width, overflow, tag)
+        mixed = scale_combine(x, agg, self.one_plus_eps.publish(mode), self.lam)
+        return self.phi2(relu(self.phi1(mixed, mode)), mode)
+
+
+class GATLayer:
+    """Multi-head graph attention.  heads=1 is the reference layer
+    (models.py:492-509); per-head parameters are drawn in head order exactly as
+    `heads` separate reference GATLayers would draw them.  Output [N, heads*fo]
+    (heads concatenated) or, with reduce="mean", the head mean [N, fo]."""
+
+    def __init__(self, rng, fan_in, fan_out, heads=1, device="cuda", store_in=None,
+                 store_out=None, reduce="concat", in_rows=None):
+        self.heads, self.fan_out, self.reduce = heads, fan_out, reduce
+        so = store_out or fan_out
+        si = store_in or fan_in
+        ws, al, ar = [], [], []
+        for _ in range(heads):
+            w = _placed(_glorot(rng, fan_in, fan_out), (si, so), in_rows)
+            a_l = np.zeros(so, np.float32)
+            a_l[:fan_out] = _glorot(rng, fan_out, 1)[:, 0]
+            a_r = np.zeros(so, np.float32)
+            a_r[:fan_out] = _glorot(rng, fan_out, 1)[:, 0]
+            ws.append(w), al.append(a_l), ar.append(a_r)
+        self.store_out = so
+        self.w = Param(np.concatenate(ws, axis=1), device)
+        self.a_l = Param(np.stack(al), device)
+        self.a_r = Param(np.stack(ar), device)
+
+    def params(self):
+        return [self.w, self.a_l, self.a_r]
+
+    def __call__(self, bundle, x, mode, width, overflow, tag):
+        h, so = self.heads, self.store_out
+        z = matmul(x, self.w.publish(mode))                       # [N, H*so]
+        zh = z.view(z.shape[0], h, so)
+        a_l, a_r = self.a_l.publish(mode), self.a_r.publish(mode)
+        # s = z_h . a_h with fp32 accumulation and one rounding (models.matmul)
+        s_l = torch.einsum("nhf,hf->nh", zh.float(), a_l.float()).to(z.dtype)
+        s_r = torch.einsum("nhf,hf->nh", zh.float(), a_r.float()).to(z.dtype)
+        e = attention_logits(bundle, s_l, s_r, 0.2)               # [E, H]
+        alpha = edge_softmax(bundle, e, overflow, tag + "/softmax")
+        out = spmm_weighted(bundle, alpha if h > 1 else alpha[:, 0], z, width, overflow, tag)
+        if self.reduce == "mean" and h > 1:
+            return _HeadMeanFn.apply(out, h)
+        return out
+
+
+class _HeadMeanFn(torch.autograd.Function):
+    """Mean over heads: fp64 sum / H, one rounding; backward rnd(g / H)."""
+
+    @staticmethod
+    def forward(ctx, y, heads):
+        ctx.heads = heads
+        n, f = y.shape
+        return (y.view(n, heads, f // heads).double().sum(1) / heads).to(y.dtype)
+
+    @staticmethod
+    def backward(ctx, g):
+        gg = (g.double() / ctx.heads).to(g.dtype)
+        return gg.repeat(1, ctx.heads), None
+
+
+_LAYER_KINDS = ("gcn", "gin", "gat")
+
+
+class Model:
+    """Stack of `layers` layers of one kind with ReLU between (models.py:515-546).
+    Defaults reproduce the reference (2 layers, 1 head).  Storage widths are
+    padded to multiples of 8 (zero, inert) for 128-bit feature rows."""
+
+    def __init__(self, kind, rng, dims, reduction=None, lam=0.1, heads=1, layers=2,
+                 device="cuda", in_store=None):
+        if kind not in _LAYER_KINDS:
+            raise ValueError(f"unknown model kind {kind!r}")
+        if layers < 1:
+            raise ValueError("need at least one layer")
+        self.kind, self.heads = kind, heads
+        fan_in, hidden, n_cls = dims
+        red = reduction or Reduction("discretized", "both")
+        self.n_cls = n_cls
+        self.out_store = _round8(n_cls)
+        fi, si = fan_in, in_store or fan_in
+        in_rows = None
+        self.layers = []
+        for li in range(layers):
+            last = li == layers - 1
+            fo = n_cls if last else hidden
+            so = self.out_store if last else _round8(hidden)
+            if kind == "gcn":
+                layer = GCNLayer(rng, fi, fo, red, device, si, so, in_rows)
+            elif kind == "gin":
+                layer = GINLayer(rng, fi, fo, lam, red.scaling, device, si, so, in_rows)
+            else:
+                layer = GATLayer(rng, fi, fo, heads, device, si, so,
+                                 reduce="mean" if last else "concat", in_rows=in_rows)
+            self.layers.append(layer)
+            if kind == "gat" and not last:
+                # concatenated heads: logical feature (h, j) lives at storage h*so + j
+                fi, si = fo * heads, so * heads
+                in_rows = (np.arange(heads)[:, None] * so + np.arange(fo)[None, :]).reshape(-1)
+            else:
+                fi, si, in_rows = fo, so, None
+
+    def params(self):
+        return [p for layer in self.layers for p in layer.params()]
+
+    def forward(self, bundle, x, mode, width="half2", overflow=None):
+        h = x
+        for i, layer in enumerate(self.layers):
+            h = layer(bundle, h, mode, width, overflow, f"{self.kind}{i}")
+            if i + 1 < len(self.layers):
+                h = relu(h)
+        return h
+
+
+# ── loss, optimiser, training loop ───────────────────────────────────────
+
+
+class _CrossEntropyFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, logits, labels, n_active):
+        z = logits[:, :n_active].double()
+        z = z - z.max(dim=1, keepdim=True).values
+        ez = torch.exp(z)
+        sumexp = ez.sum(dim=1)
+        p = ez / sumexp[:, None]
+        n = z.shape[0]
+        nll = torch.log(sumexp) - z.gather(1, labels[:, None])[:, 0]
+        ctx.save_for_backward(p, labels)
+        ctx.shape = logits.shape
+        return nll.mean().float()
+
+    @staticmethod
+    def backward(ctx, g):
+        p, labels = ctx.saved_tensors
+        n = p.shape[0]
+        grad = p.clone()
+        grad[torch.arange(n, device=p.device), labels] -= 1.0
+        full = torch.zeros(ctx.shape, dtype=torch.float32, device=p.device)
+        full[:, : p.shape[1]] = (grad / n * g.double()).float()
+        return full, None, None
+
+
+def cross_entropy(logits, labels, n_active=None):
+    """Mean CE over all nodes on fp32 logits (models.py:552-572); columns at or
+    beyond n_active (storage padding) take no part."""
+    if logits.dtype != torch.float32:
+        raise ValueError("cross-entropy expects float32 logits")
+    return _CrossEntropyFn.apply(logits, labels, n_active or logits.shape[1])
+
+
+class Adam:
+    """models.Adam (models.py:575-592) on device fp32 masters."""
+
+    def __init__(self, params, lr=1e-2, betas=(0.9, 0.999), eps=1e-8):
+        self.params = list(params)
+        self.lr, self.betas, self.eps = lr, betas, eps
+        self.m = [torch.zeros_like(p.master) for p in self.params]
+        self.v = [torch.zeros_like(p.master) for p in self.params]
+        self.t = 0
+
+    @torch.no_grad()
+    def step(self):
+        self.t += 1
+        b1, b2 = self.betas
+        c1, c2 = 1 - b1 ** self.t, 1 - b2 ** self.t
+        for p, m, v in zip(self.params, self.m, self.v):
+            g = p.grad32()
+            m.add_((1 - b1) * (g - m))
+            v.add_((1 - b2) * (g * g - v))
+            p.master.sub_(self.lr * (m / c1) / (torch.sqrt(v / c2) + self.eps))
+
+
+@dataclass
+class TrainConfig:
+    kind: str = "gcn"
+    mode: str = "half"
+    epochs: int = 200
+    hidden: int = 16
+    lr: float = 1e-2
+    seed: int = 0
+    width: str = "half2"
+    scaling: str = "discretized"
+    norm: str = "both"
+    lam: float = 0.1
+    val_fraction: float = 0.2
+    # builder extensions
+    numerics: str = "fast"
+    heads: int = 1
+    layers: int = 2
+    device: str = "cuda"
+
+
+@dataclass
+class TrainResult:
+    train_acc: float
+    val_acc: float
+    losses: list
+    trace: list
+    conversions: ConversionCounter
+    overflow: OverflowCounters
+    logits: torch.Tensor | None = field(default=None, repr=False)
+
+    def write_trace(self, path):
+        with open(path, "w", newline="") as fh:
+            w = csv.writer(fh)
+            w.writerow(["epoch", "loss", "train_acc", "val_acc", "inf_count", "nan_count"])
+            w.writerows(self.trace)
+
+
+def accuracy(logits, labels, mask, n_active=None):
+    if isinstance(logits, torch.Tensor):
+        if not bool(mask.any()):
+            return 0.0
+        pred = logits[mask][:, : n_active or logits.shape[1]].argmax(dim=1)
+        return float((pred == labels[mask]).float().mean())
+    if not mask.any():
+        return 0.0
+    pred = logits[mask][:, : n_active or logits.shape[1]].argmax(axis=1)
+    return float((pred == labels[mask]).mean())
+
+
+class Trainer:
+    """Full-batch node classification state (models.train, models.py:633-684):
+    model, optimiser, masks and device-resident inputs.  `step()` is one epoch
+    (forward, loss, backward, Adam) with no host synchronisation."""
+
+    def __init__(self, bundle: GraphBundle, features, labels, config: TrainConfig):
+        self.cfg = config
+        self.bundle = bundle
+        dev = config.device
+        rng = np.random.default_rng(config.seed)
+        feats = features if isinstance(features, torch.Tensor) else torch.from_numpy(
+            np.ascontiguousarray(features))
+        n, fan_in = feats.shape
+        labels_t = labels if isinstance(labels, torch.Tensor) else torch.from_numpy(
+            np.asarray(labels, dtype=np.int64))
+        c = int(labels_t.max()) + 1
+        self.n_cls = c + c % 2   # the reference harness pads odd class counts to even
+        self.in_store = _round8(fan_in)
+        red = Reduction(config.scaling, config.norm)
+        self.model = Model(config.kind, rng, (fan_in, config.hidden, self.n_cls), red,
+                           config.lam, config.heads, config.layers, dev, self.in_store)
+        self.opt = Adam(self.model.params(), lr=config.lr)
+        perm = rng.permutation(n)
+        val = np.zeros(n, dtype=bool)
+        val[perm[: int(n * config.val_fraction)]] = True
+        self.val_mask = torch.from_numpy(val).to(dev)
+        self.train_mask = ~self.val_mask
+        self.labels = labels_t.to(dev).long()
+        self.dtype = _DTYPES[config.mode]
+        self.x = self.load_features(feats)
+        self.conversions = ConversionCounter()
+
+    def load_features(self, feats, out=None):
+        """Round to the compute dtype (via fp32, as models.train does) and pad
+        columns to the 8-aligned storage width; `out` reuses a buffer."""
+        n, f = feats.shape
+        if out is None:
+            out = torch.zeros((n, self.in_store), dtype=self.dtype, device=self.cfg.device)
+        src = feats.to(self.cfg.device, non_blocking=True)
+        out[:, :f] = src.to(torch.float32).to(self.dtype) if src.dtype != self.dtype else src
+        return out
+
+    def step(self, overflow=None):
+        cfg = self.cfg
+        logits = self.model.forward(self.bundle, self.x, cfg.mode, cfg.width, overflow)
+        if cfg.mode == "half":
+            logits = convert(logits, "float32", self.conversions)
+        loss = cross_entropy(logits, self.labels, self.n_cls)
+        loss.backward()
+        self.opt.step()
+        return loss.detach(), logits.detach()
+
+
+def train(g, features, labels, config: TrainConfig) -> TrainResult:
+    """Full-batch node classification; raises NanLossError on a non-finite loss."""
+    bundle = g if isinstance(g, GraphBundle) else GraphBundle.build(g, numerics=config.numerics)
+    tr = Trainer(bundle, features, labels, config)
+    overflow = OverflowCounters()
+    trace, losses = [], []
+    train_acc = val_acc = 0.0
+    if config.epochs == 0:
+        with torch.no_grad():
+            logits = tr.model.forward(bundle, tr.x, config.mode, config.width, overflow)
+            if config.mode == "half":
+                logits = convert(logits, "float32", tr.conversions)
+        return TrainResult(accuracy(logits, tr.labels, tr.train_mask, tr.n_cls),
+                           accuracy(logits, tr.labels, tr.val_mask, tr.n_cls), [], [],
+                           tr.conversions, overflow, logits)
+    logits = None
+    for epoch in range(config.epochs):
+        overflow.reset()
+        loss, logits = tr.step(overflow)
+        lv = float(loss)
+        if not math.isfinite(lv):
+            raise NanLossError(epoch, overflow)
+        train_acc = accuracy(logits, tr.labels, tr.train_mask, tr.n_cls)
+        val_acc = accuracy(logits, tr.labels, tr.val_mask, tr.n_cls)
+        n_inf, n_nan = overflow.totals()
+        losses.append(lv)
+        trace.append([epoch, lv, train_acc, val_acc, n_inf, n_nan])
+    return TrainResult(train_acc, val_acc, losses, trace, tr.conversions, overflow, logits)

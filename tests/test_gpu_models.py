@@ -1,0 +1,371 @@
+"""GPU: the reference-facing API (kernels.*, sparse.*, models.*) on the B200.
+Mirrors the reference's own tests (pkg/tests/test_kernels.py, test_models.py,
+test_acceptance.py) -- same inputs, same expected values -- and compares
+training traces with the golden traces recorded from the reference."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from conftest import bits, load_golden
+
+pytestmark = pytest.mark.gpu
+
+REDUCTIONS = [("post", "none"), ("post", "left"), ("post", "right"), ("post", "both"),
+              ("pre", "left"), ("pre", "right"), ("pre", "both"),
+              ("discretized", "left"), ("discretized", "right"), ("discretized", "both")]
+
+
+def _random_graph(rng, n, density=0.2):
+    from paper_2411_01109_b200 import sparse as sp
+
+    mask = rng.random((n, n)) < density
+    np.fill_diagonal(mask, False)
+    return sp.CooGraph.from_edges(n, *np.nonzero(mask))
+
+
+def _feats(rng, n, f, dtype=np.float16):
+    from paper_2411_01109_b200 import sparse as sp
+
+    return sp.DenseTensor(rng.normal(0, 2, size=(n, f)).astype(dtype))
+
+
+# ── kernels API (test_kernels.py) ────────────────────────────────────────
+
+
+@pytest.mark.parametrize("red", REDUCTIONS, ids=lambda r: "-".join(r))
+@pytest.mark.parametrize("f", [4, 32])
+def test_spmm_v_matches_oracle_bits(cuda, red, f):
+    from paper_2411_01109_b200 import kernels as K, simt
+
+    rng = np.random.default_rng(f * 13 + 1)
+    g = _random_graph(rng, 48)
+    x = _feats(rng, 48, f)
+    sched = simt.plan_edge_parallel(g, warp_chunk=64, warps_per_cta=2)
+    got, _ = K.spmm_v(g, x, schedule=sched, reduction=K.Reduction(*red))
+    want = O.spmm_edge_parallel(g.n, g.rows, g.cols, x.data, None, 64, 2, *red)[0]
+    np.testing.assert_array_equal(bits(got.data), bits(want))
+
+
+def test_float32_mode_bit_exact(cuda):
+    from paper_2411_01109_b200 import kernels as K
+
+    rng = np.random.default_rng(17)
+    g = _random_graph(rng, 30)
+    x = _feats(rng, 30, 8, np.float32)
+    got, _ = K.spmm_v(g, x, reduction=K.Reduction("discretized", "both"))
+    want = O.spmm_edge_parallel(g.n, g.rows, g.cols, x.data, None, 128, 4, "discretized", "both")[0]
+    np.testing.assert_array_equal(bits(got.data), bits(want))
+
+
+def test_edge_metrics_hand_counted(cuda):
+    """test_kernels.py:210-243: 130 single-edge rows, chunk 128, F=32."""
+    from paper_2411_01109_b200 import kernels as K, simt, sparse as sp
+
+    rows = np.arange(130, dtype=np.int64)
+    g = sp.CooGraph(131, rows, rows + 1)
+    x = sp.DenseTensor(np.ones((131, 32), dtype=np.float16))
+    sched = simt.plan_edge_parallel(g, warp_chunk=128, warps_per_cta=4)
+    _, m = K.spmm_v(g, x, schedule=sched)
+    assert (m.load_transactions, m.load_bytes) == (70, 5 * 256 + 65 * 128)
+    assert (m.barrier_waits, m.intra_cta_rounds, m.staging_writes) == (2, 0, 1)
+    _, m = K.spmm_ve(g, np.ones(130, dtype=np.float16), x, schedule=sched)
+    assert (m.load_transactions, m.load_bytes) == (73, 9600 + 3 * 128)
+
+
+def test_intra_cta_chain_of_eight(cuda):
+    """test_kernels.py:256-273: one 512-edge row, chunk 64, 8 warps/CTA."""
+    from paper_2411_01109_b200 import kernels as K, simt, sparse as sp
+
+    g = sp.CooGraph(513, np.zeros(512, dtype=np.int64), np.arange(1, 513, dtype=np.int64))
+    x = sp.DenseTensor(np.ones((513, 4), dtype=np.float16))
+    sched = simt.plan_edge_parallel(g, warp_chunk=64, warps_per_cta=8)
+    y, m, st = K.spmm_v(g, x, schedule=sched, return_staging=True)
+    assert m.intra_cta_rounds == 3 and m.staging_writes == 1
+    assert st.capacity == 1 and st.rows.tolist() == [0]
+    assert float(st.partials[0, 0]) == 512.0 and float(y.data[0, 0]) == 512.0
+
+
+def test_vertex_conflict_writes(cuda):
+    """test_kernels.py:287-311: 70-edge row -> groups 32+32+6."""
+    from paper_2411_01109_b200 import kernels as K, sparse as sp
+
+    g = sp.CooGraph(80, np.zeros(70, dtype=np.int64), np.arange(1, 71, dtype=np.int64))
+    csr = sp.coo_to_csr(g)
+    x = sp.DenseTensor(np.ones((80, 4), dtype=np.float16))
+    y, m, st = K.spmm_vertex_grouped(csr, x, write_mode="staging", return_staging=True)
+    assert (m.staging_writes, m.atomic_writes, st.capacity) == (3, 0, 3)
+    assert st.rows.tolist() == [0, 0, 0] and float(y.data[0, 0]) == 70.0
+    _, m = K.spmm_vertex_grouped(csr, x, write_mode="atomic_model")
+    assert (m.atomic_writes, m.staging_writes) == (2, 0)
+
+
+def test_equivalences_and_padding(cuda):
+    from paper_2411_01109_b200 import kernels as K, sparse as sp
+
+    rng = np.random.default_rng(12)
+    g = _random_graph(rng, 50)
+    x = _feats(rng, 50, 16)
+    ones = np.ones(g.num_edges, dtype=np.float16)
+    for red in (K.Reduction("post", "both"), K.Reduction("discretized", "right")):
+        yv, _ = K.spmm_v(g, x, reduction=red)
+        yw, _ = K.spmm_ve(g, ones, x, reduction=red)
+        np.testing.assert_array_equal(bits(yv.data), bits(yw.data))
+    x6 = _feats(rng, 50, 6)
+    y, _ = K.spmm_v(g, x6, reduction=K.Reduction("post", "both"))
+    yp, _ = K.spmm_v(g, sp.pad_features(x6, 4), reduction=K.Reduction("post", "both"))
+    np.testing.assert_array_equal(bits(y.data), bits(yp.data)[:, :6])
+    a, b = _feats(rng, 50, 32), _feats(rng, 50, 32)
+    w2, m2 = K.sddmm(g, a, b, width="half2")
+    w8, m8 = K.sddmm(g, a, b, width="half8")
+    np.testing.assert_array_equal(bits(w2), bits(w8))
+    assert m2.shuffle_rounds == 4 * g.num_edges and m8.shuffle_rounds == 2 * g.num_edges
+
+
+def test_scaling_worked_example(cuda):
+    from paper_2411_01109_b200 import kernels as K, sparse as sp
+
+    g = sp.CooGraph(5, np.zeros(4, dtype=np.int64), np.arange(1, 5, dtype=np.int64))
+    x = sp.DenseTensor(np.full((5, 32), 30000.0, dtype=np.float16))
+    assert np.isinf(K.spmm_v(g, x, reduction=K.Reduction("post", "right"))[0].data[0]).all()
+    for scaling in ("pre", "discretized"):
+        for numerics in ("reference", "fast"):
+            y, _ = K.spmm_v(g, x, reduction=K.Reduction(scaling, "right"), numerics=numerics)
+            assert np.all(y.data[0] == 30000.0) and not y.data[1:].any()
+
+
+def test_validation_errors(cuda):
+    from paper_2411_01109_b200 import kernels as K, simt, sparse as sp
+
+    g = sp.CooGraph(3, np.array([0]), np.array([1]))
+    with pytest.raises(ValueError):
+        K.spmm_v(g, sp.DenseTensor(np.ones((3, 5), np.float16)))
+    with pytest.raises(ValueError):
+        K.spmm_v(g, sp.DenseTensor(np.ones((3, 4), np.float16)), width="half8")
+    with pytest.raises(ValueError, match="rows"):
+        K.spmm_v(g, sp.DenseTensor(np.ones((4, 4), np.float16)))
+    with pytest.raises(ValueError, match="CSR"):
+        K.spmm_vertex_grouped(g, sp.DenseTensor(np.ones((3, 4), np.float16)))
+    with pytest.raises(ValueError, match="modes"):
+        K.sddmm(g, sp.DenseTensor(np.ones((3, 4), np.float16)),
+                sp.DenseTensor(np.ones((3, 4), np.float32)))
+    csr = sp.coo_to_csr(g)
+    with pytest.raises(ValueError):
+        K.spmm_v(g, sp.DenseTensor(np.ones((3, 4), np.float16)),
+                 schedule=simt.plan_vertex_grouped(csr))
+    with pytest.raises(ValueError, match="negative"):
+        sp.CooGraph.from_edges(3, [0, -1], [1, 2])
+
+
+def test_sparse_api_matches_oracle(cuda):
+    from paper_2411_01109_b200 import sparse as sp
+
+    rng = np.random.default_rng(5)
+    n = 300
+    rows, cols = rng.integers(0, n, 4000), rng.integers(0, n, 4000)
+    g = sp.CooGraph.from_edges(n, rows, cols)
+    wr, wc = O.canonical_edges(n, rows, cols)
+    np.testing.assert_array_equal(g.rows, wr)
+    np.testing.assert_array_equal(g.cols, wc)
+    np.testing.assert_array_equal(sp.coo_to_csr(g).offsets, O.csr_offsets(n, wr))
+    gt, perm = sp.transpose(g, return_perm=True)
+    tr, tc, tp = O.transpose_perm(n, wr, wc)
+    np.testing.assert_array_equal(gt.rows, tr)
+    np.testing.assert_array_equal(gt.cols, tc)
+    np.testing.assert_array_equal(perm, tp)
+    np.testing.assert_array_equal(sp.col_degrees(g), np.bincount(wc, minlength=n))
+    s = sp.symmetrize(g)
+    np.testing.assert_array_equal(s.rows, O.symmetrize(n, wr, wc)[0])
+    lp = sp.add_self_loops(g)
+    np.testing.assert_array_equal(lp.cols, O.add_self_loops(n, wr, wc)[1])
+
+
+# ── autograd ops (test_models.py) ────────────────────────────────────────
+
+
+def _bundle(seed=0, n=24, density=0.25, numerics="reference"):
+    from paper_2411_01109_b200 import sparse as sp
+    from paper_2411_01109_b200.models import GraphBundle
+
+    rng = np.random.default_rng(seed)
+    mask = rng.random((n, n)) < density
+    np.fill_diagonal(mask, False)
+    g = sp.CooGraph.from_edges(n, *np.nonzero(mask))
+    return GraphBundle.build(g, numerics=numerics), g
+
+
+@pytest.mark.parametrize("numerics", ["reference", "fast"])
+def test_spmm_agg_backward_is_transposed(cuda, numerics):
+    from paper_2411_01109_b200 import models as M
+    from paper_2411_01109_b200.kernels import Reduction
+
+    bundle, g = _bundle(2, numerics=numerics)
+    rng = np.random.default_rng(3)
+    x = torch.tensor(rng.normal(size=(g.n, 4)).astype(np.float32), device=cuda,
+                     requires_grad=True)
+    y = M.spmm_agg(bundle, x, Reduction("post", "both"))
+    seed = rng.normal(size=(g.n, 4)).astype(np.float32)
+    y.backward(torch.tensor(seed, device=cuda))
+    deg_r = np.bincount(g.rows, minlength=g.n).astype(np.float64)
+    deg_c = np.bincount(g.cols, minlength=g.n).astype(np.float64)
+    fin = np.where(deg_r > 0, 1 / np.sqrt(np.maximum(deg_r, 1)), 0)
+    fout = np.where(deg_c > 0, 1 / np.sqrt(np.maximum(deg_c, 1)), 0)
+    tr, tc, _ = O.transpose_perm(g.n, g.rows, g.cols)
+    want = O.spmm_f64(g.n, tr, tc, seed, None, fin, fout)
+    np.testing.assert_allclose(x.grad.cpu().numpy(), want, rtol=1e-3, atol=1e-4)
+
+
+@pytest.mark.parametrize("numerics", ["reference", "fast"])
+def test_spmm_weighted_grads(cuda, numerics):
+    from paper_2411_01109_b200 import models as M
+
+    bundle, g = _bundle(5, numerics=numerics)
+    rng = np.random.default_rng(6)
+    w = torch.tensor(rng.normal(size=g.num_edges).astype(np.float32), device=cuda,
+                     requires_grad=True)
+    x = torch.tensor(rng.normal(size=(g.n, 4)).astype(np.float32), device=cuda,
+                     requires_grad=True)
+    y = M.spmm_weighted(bundle, w, x)
+    seed = rng.normal(size=(g.n, 4)).astype(np.float32)
+    y.backward(torch.tensor(seed, device=cuda))
+    want_w = np.einsum("ef,ef->e", seed.astype(np.float64)[g.rows],
+                       x.detach().cpu().numpy().astype(np.float64)[g.cols])
+    np.testing.assert_allclose(w.grad.cpu().numpy(), want_w, rtol=1e-3, atol=1e-4)
+    a = np.zeros((g.n, g.n))
+    a[g.rows, g.cols] = w.detach().cpu().numpy()
+    np.testing.assert_allclose(x.grad.cpu().numpy(), a.T @ seed, rtol=1e-3, atol=1e-4)
+
+
+def test_attention_backward_degree_sums(cuda):
+    from paper_2411_01109_b200 import models as M
+
+    for numerics in ("reference", "fast"):
+        bundle, g = _bundle(9, numerics=numerics)
+        s_l = torch.zeros((g.n, 1), dtype=torch.float16, device=cuda, requires_grad=True)
+        s_r = torch.zeros((g.n, 1), dtype=torch.float16, device=cuda, requires_grad=True)
+        e = M.attention_scores(bundle, s_l, s_r)
+        e.backward(torch.ones(g.num_edges, dtype=torch.float16, device=cuda))
+        np.testing.assert_array_equal(s_l.grad[:, 0].cpu().numpy(),
+                                      np.bincount(g.rows, minlength=g.n))
+        np.testing.assert_array_equal(s_r.grad[:, 0].cpu().numpy(),
+                                      np.bincount(g.cols, minlength=g.n))
+
+
+def test_attention_golden_through_models(cuda):
+    """attention_scores -> leaky_relu -> edge_softmax fwd+bwd against the
+    reference's own tape values, bit for bit (reference numerics)."""
+    from paper_2411_01109_b200 import models as M
+    from paper_2411_01109_b200 import sparse as sp
+    from conftest import golden_cases
+
+    cases, _ = golden_cases("attention.npz")
+    for i, c in enumerate(cases):
+        g = sp.CooGraph(int(c["n"]), c["rows"], c["cols"])
+        bundle = M.GraphBundle.build(g, numerics="reference")
+        dt = torch.float16 if c["sl"].dtype == np.float16 else torch.float32
+        s_l = torch.tensor(c["sl"][:, None], device=cuda, requires_grad=True)
+        s_r = torch.tensor(c["sr"][:, None], device=cuda, requires_grad=True)
+        e = M.attention_scores(bundle, s_l, s_r)
+        e2 = M.leaky_relu(e, 0.2)
+        alpha = M.edge_softmax(bundle, e2)
+        np.testing.assert_array_equal(bits(alpha.detach().cpu().numpy()), bits(c["alpha"]))
+        alpha.backward(torch.tensor(c["seed"], device=cuda, dtype=dt))
+        np.testing.assert_array_equal(bits(s_l.grad[:, 0].cpu().numpy()), bits(c["g_sl"]),
+                                      err_msg=f"case {i}")
+        np.testing.assert_array_equal(bits(s_r.grad[:, 0].cpu().numpy()), bits(c["g_sr"]),
+                                      err_msg=f"case {i}")
+
+
+def test_edge_softmax_uniform(cuda):
+    from paper_2411_01109_b200 import models as M, sparse as sp
+
+    g = sp.CooGraph(4, np.zeros(4, dtype=np.int64), np.arange(4, dtype=np.int64))
+    bundle = M.GraphBundle.build(g)
+    e = torch.zeros(4, dtype=torch.float16, device=cuda, requires_grad=True)
+    alpha = M.edge_softmax(bundle, e)
+    assert alpha.detach().cpu().tolist() == [0.25] * 4
+    alpha.backward(torch.ones(4, dtype=torch.float16, device=cuda))
+    assert not e.grad.any()
+
+
+# ── training (test_models.py TestTrain, test_acceptance.py C4) ───────────
+
+
+def _sbm_golden():
+    d = load_golden("training.npz")
+    from paper_2411_01109_b200 import sparse as sp
+
+    g = sp.CooGraph(60, d["sbm_rows"], d["sbm_cols"])
+    return g, d["sbm_x"], d["sbm_labels"], d
+
+
+@pytest.mark.parametrize("kind", ["gcn", "gin", "gat"])
+@pytest.mark.parametrize("mode", ["half", "float32"])
+def test_training_trace_matches_reference(cuda, kind, mode):
+    """5 epochs, reference numerics: losses within 2e-3 of the reference's."""
+    from paper_2411_01109_b200 import models as M
+
+    g, x, labels, d = _sbm_golden()
+    cfg = M.TrainConfig(kind=kind, mode=mode, epochs=5, seed=3, numerics="reference")
+    res = M.train(g, x, labels, cfg)
+    want = d[f"sbm_{kind}_{mode}_loss"]
+    np.testing.assert_allclose(res.losses, want, atol=2e-3)
+    cfg_fast = M.TrainConfig(kind=kind, mode=mode, epochs=5, seed=3, numerics="fast")
+    np.testing.assert_allclose(M.train(g, x, labels, cfg_fast).losses, want, atol=5e-3)
+
+
+def test_multihead_gat_trace(cuda):
+    from paper_2411_01109_b200 import models as M
+
+    g, x, labels, d = _sbm_golden()
+    cfg = M.TrainConfig(kind="gat", mode="half", epochs=4, seed=5, hidden=4, heads=4, layers=3,
+                        numerics="reference")
+    res = M.train(g, x, labels, cfg)
+    np.testing.assert_allclose(res.losses, d["sbm_gat4x3_half_loss"], atol=3e-3)
+
+
+def test_c1_gcn_accuracy_parity(cuda):
+    """C1 (Cora-shaped, 7 -> 8 classes) 200 epochs: final train/val accuracy
+    within 0.5 pt of the reference trainer's (north_star tolerance)."""
+    from paper_2411_01109_b200 import graphgen, models as M, sparse as sp
+
+    d = load_golden("training.npz")
+    rows, cols, feats, labels = graphgen.cora_like(0)
+    assert rows.size == int(d["c1_num_edges"])
+    g = sp.CooGraph(2708, rows, cols)
+    for numerics in ("fast", "reference"):
+        res = M.train(g, feats, labels, M.TrainConfig(kind="gcn", epochs=200, seed=0,
+                                                      numerics=numerics))
+        want_train, want_val = d["c1_gcn_half_acc"][-1]
+        assert abs(res.train_acc - want_train) <= 0.005, (numerics, res.train_acc, want_train)
+        assert abs(res.val_acc - want_val) <= 0.005, (numerics, res.val_acc, want_val)
+        assert all(row[5] == 0 for row in res.trace)
+
+
+def test_conversions_and_nan_abort(cuda):
+    from paper_2411_01109_b200 import graphgen, models as M, sparse as sp
+
+    g, x, labels, _ = _sbm_golden()
+    r = M.train(g, x, labels, M.TrainConfig(kind="gat", epochs=3))
+    assert (r.conversions.forward, r.conversions.backward) == (3, 3)
+    r = M.train(g, x, labels, M.TrainConfig(mode="float32", epochs=3))
+    assert r.conversions.total == 0
+    # test_models.py:337-350: GIN lam=1, x1000, post scaling overflows -> NaN at epoch 0
+    rows, cols, f8, lab = graphgen.synth_sbm(60, 2, 0.5, 0.1, 8, 3)
+    g2 = sp.CooGraph(60, rows, cols)
+    big = f8 * 1000.0
+    with pytest.raises(M.NanLossError) as err:
+        M.train(g2, big, lab, M.TrainConfig(kind="gin", epochs=5, lam=1.0, scaling="post",
+                                            norm="right"))
+    assert err.value.epoch == 0 and sum(err.value.counters.inf.values()) > 0
+    ok = M.train(g2, big, lab, M.TrainConfig(kind="gin", epochs=5, lam=1.0,
+                                             scaling="discretized", norm="right"))
+    assert all(row[4] == 0 and row[5] == 0 for row in ok.trace)
+
+
+def test_smoke_entry(cuda):
+    import __graft_entry__
+
+    __graft_entry__.smoke()
