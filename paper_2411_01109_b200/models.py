@@ -154,6 +154,18 @@ class GraphBundle:
                                 self.warp_chunk, self.warps_per_cta) for h in range(heads)]
         return torch.cat(outs, dim=1)
 
+    def sddmm(self, x, y, heads=1):
+        return D.sddmm(self.dg, x, y, heads=heads)
+
+    def attn_logits(self, s_l, s_r, slope):
+        return D.attention_logits(self.dg, s_l, s_r, slope)
+
+    def softmax_fwd(self, e):
+        return D.edge_softmax_fwd(self.dg, e)
+
+    def softmax_bwd(self, alpha, g):
+        return D.edge_softmax_bwd(self.dg, alpha, g)
+
     def edge_sums(self, v, transpose=False):
         """Row (or column) sums of per-edge values [E, H] -> [N, H]
         (attention_scores backward, models.py:329-337)."""
@@ -210,7 +222,7 @@ class _WeightedFn(torch.autograd.Function):
         g = g.contiguous()
         gw = gx = None
         if ctx.needs_input_grad[0]:
-            gw = D.sddmm(b.dg, g, x, heads=h).reshape(w.shape)
+            gw = b.sddmm(g, x, heads=h).reshape(w.shape)
         if ctx.needs_input_grad[1]:
             gx = b.spmm(g, w, "post", "none", transpose=True, heads=h, weight_via_perm=True)
         return gw, gx, None, None
@@ -230,7 +242,7 @@ class _ScoresFn(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, s_l, s_r, bundle, slope):
-        out = D.attention_logits(bundle.dg, s_l, s_r, 1.0 if slope is None else slope)
+        out = bundle.attn_logits(s_l, s_r, 1.0 if slope is None else slope)
         ctx.bundle, ctx.slope = bundle, slope
         ctx.save_for_backward(out)
         return out
@@ -262,7 +274,7 @@ def attention_logits(bundle, s_l, s_r, slope=0.2):
 class _SoftmaxFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, e, bundle):
-        alpha = D.edge_softmax_fwd(bundle.dg, e)
+        alpha = bundle.softmax_fwd(e)
         ctx.bundle = bundle
         ctx.save_for_backward(alpha)
         return alpha
@@ -270,7 +282,7 @@ class _SoftmaxFn(torch.autograd.Function):
     @staticmethod
     def backward(ctx, g):
         (alpha,) = ctx.saved_tensors
-        return D.edge_softmax_bwd(ctx.bundle.dg, alpha, g.contiguous()), None
+        return ctx.bundle.softmax_bwd(alpha, g.contiguous()), None
 
 
 def edge_softmax(bundle, e, overflow=None, tag="softmax"):
@@ -594,17 +606,16 @@ class Model:
 
 class _CrossEntropyFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, logits, labels, n_active):
+    def forward(ctx, logits, labels, n_active, denom):
         z = logits[:, :n_active].double()
         z = z - z.max(dim=1, keepdim=True).values
         ez = torch.exp(z)
         sumexp = ez.sum(dim=1)
         p = ez / sumexp[:, None]
-        n = z.shape[0]
         nll = torch.log(sumexp) - z.gather(1, labels[:, None])[:, 0]
         ctx.save_for_backward(p, labels)
-        ctx.shape = logits.shape
-        return nll.mean().float()
+        ctx.shape, ctx.denom = logits.shape, denom
+        return (nll.sum() / denom).float()
 
     @staticmethod
     def backward(ctx, g):
@@ -613,16 +624,18 @@ class _CrossEntropyFn(torch.autograd.Function):
         grad = p.clone()
         grad[torch.arange(n, device=p.device), labels] -= 1.0
         full = torch.zeros(ctx.shape, dtype=torch.float32, device=p.device)
-        full[:, : p.shape[1]] = (grad / n * g.double()).float()
-        return full, None, None
+        full[:, : p.shape[1]] = (grad / ctx.denom * g.double()).float()
+        return full, None, None, None
 
 
-def cross_entropy(logits, labels, n_active=None):
+def cross_entropy(logits, labels, n_active=None, denom=None):
     """Mean CE over all nodes on fp32 logits (models.py:552-572); columns at or
-    beyond n_active (storage padding) take no part."""
+    beyond n_active (storage padding) take no part.  denom: the global node
+    count when the rows are one partition of the graph."""
     if logits.dtype != torch.float32:
         raise ValueError("cross-entropy expects float32 logits")
-    return _CrossEntropyFn.apply(logits, labels, n_active or logits.shape[1])
+    return _CrossEntropyFn.apply(logits, labels, n_active or logits.shape[1],
+                                 denom or logits.shape[0])
 
 
 class Adam:
@@ -701,7 +714,7 @@ class Trainer:
     model, optimiser, masks and device-resident inputs.  `step()` is one epoch
     (forward, loss, backward, Adam) with no host synchronisation."""
 
-    def __init__(self, bundle: GraphBundle, features, labels, config: TrainConfig):
+    def __init__(self, bundle, features, labels, config: TrainConfig, row_slice=None):
         self.cfg = config
         self.bundle = bundle
         dev = config.device
@@ -721,11 +734,12 @@ class Trainer:
         perm = rng.permutation(n)
         val = np.zeros(n, dtype=bool)
         val[perm[: int(n * config.val_fraction)]] = True
-        self.val_mask = torch.from_numpy(val).to(dev)
+        lo, hi = row_slice or (0, n)
+        self.val_mask = torch.from_numpy(val[lo:hi]).to(dev)
         self.train_mask = ~self.val_mask
-        self.labels = labels_t.to(dev).long()
+        self.labels = labels_t[lo:hi].to(dev).long()
         self.dtype = _DTYPES[config.mode]
-        self.x = self.load_features(feats)
+        self.x = self.load_features(feats[lo:hi])
         self.conversions = ConversionCounter()
 
     def load_features(self, feats, out=None):

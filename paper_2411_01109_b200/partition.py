@@ -1,0 +1,297 @@
+"""Row-partitioned multi-GPU execution.
+
+One process per GPU.  Rank p owns the contiguous vertex range [s_p, s_{p+1})
+with s_p = searchsorted(offsets, (p*E)//P, 'left') (nnz-balanced, bit-exact
+with oracle.partition_splits): its CSR rows (global column ids), the CSC rows
+of the same vertices (for the backward pass), its feature rows and labels.
+
+Exchange: before each aggregation the rank's feature rows are all-gathered
+(NCCL over NVLink) into a [P * n_max, F] buffer -- rank q's rows at
+q*n_max.. -- and the local column ids are pre-remapped into that padded
+layout once, so the SpMM reads the gathered buffer in place (no compaction).
+Backward all-gathers the output gradient the same way and aggregates over the
+local CSC rows.  GAT additionally all-gathers per-edge values (alpha, d_e) in
+a padded per-rank edge layout for the column-owner side of its backward.
+Weight gradients and the loss are all-reduced (the data-parallel sum).
+Degree-factor tables are global (computed once from the full graph), which
+makes the concatenated rank outputs bit-identical to the 1-GPU result.
+
+The compute callbacks default to the CUDA kernels; `ops=` lets the CPU/gloo
+tests drive the same exchange logic with a host implementation.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import device as D
+from .device import CsrView
+
+
+def split_points(offsets, parts: int) -> np.ndarray:
+    """s_0 = 0, s_P = N, s_p = searchsorted(offsets, (p*E)//P, 'left')."""
+    off = offsets if isinstance(offsets, torch.Tensor) else torch.as_tensor(offsets)
+    n = off.numel() - 1
+    e = int(off[-1])
+    targets = torch.tensor([(p * e) // parts for p in range(1, parts)], dtype=off.dtype,
+                           device=off.device)
+    mid = torch.searchsorted(off, targets, right=False).cpu().numpy()
+    return np.concatenate([[0], mid, [n]]).astype(np.int64)
+
+
+def remap_to_padded(ids: torch.Tensor, splits: np.ndarray, stride: int) -> torch.Tensor:
+    """Global id -> q*stride + (id - splits[q]) where q owns id."""
+    bounds = torch.as_tensor(splits[1:-1], dtype=torch.int64, device=ids.device)
+    ids64 = ids.to(torch.int64)
+    q = torch.searchsorted(bounds, ids64, right=True)
+    base = torch.as_tensor(splits[:-1], dtype=torch.int64, device=ids.device)[q]
+    return (q * stride + (ids64 - base)).to(torch.int32)
+
+
+@dataclass
+class LocalPart:
+    rank: int
+    parts: int
+    splits: np.ndarray        # vertex split points [P+1]
+    edge_splits: np.ndarray   # CSR edge offsets of the split points [P+1]
+    n_max: int                # padded rows per rank in gathered feature buffers
+    e_max: int                # padded edges per rank in gathered edge buffers
+    fwd: CsrView              # local CSR rows, columns in the padded feature layout
+    bwd: CsrView              # local CSC rows, columns padded, perm -> padded edge layout
+
+    @property
+    def lo(self):
+        return int(self.splits[self.rank])
+
+    @property
+    def hi(self):
+        return int(self.splits[self.rank + 1])
+
+    @property
+    def n_local(self):
+        return self.hi - self.lo
+
+
+def make_local_part(offsets, cols, t_offsets, t_cols, perm, rank, parts) -> LocalPart:
+    """Slice rank `rank`'s CSR/CSC rows out of the global arrays and remap ids."""
+    splits = split_points(offsets, parts)
+    eoff = offsets[torch.as_tensor(splits, device=offsets.device)].cpu().numpy()
+    n_max = int(np.diff(splits).max())
+    e_max = int(np.diff(eoff).max()) if parts > 0 else 0
+    lo, hi = int(splits[rank]), int(splits[rank + 1])
+    f_off = (offsets[lo:hi + 1] - offsets[lo]).contiguous()
+    f_cols = remap_to_padded(cols[int(offsets[lo]):int(offsets[hi])], splits, n_max)
+    t_lo, t_hi = int(t_offsets[lo]), int(t_offsets[hi])
+    b_off = (t_offsets[lo:hi + 1] - t_offsets[lo]).contiguous()
+    b_cols = remap_to_padded(t_cols[t_lo:t_hi], splits, n_max)
+    b_perm = remap_to_padded(perm[t_lo:t_hi], eoff, e_max)
+    fwd = CsrView(f_off, f_cols, hi - lo, parts * n_max)
+    bwd = CsrView(b_off, b_cols, hi - lo, parts * n_max, perm=b_perm)
+    return LocalPart(rank, parts, splits, eoff, n_max, e_max, fwd, bwd)
+
+
+class Exchange:
+    """Padded all-gathers over a torch.distributed process group."""
+
+    def __init__(self, dist, part: LocalPart):
+        self.dist = dist
+        self.part = part
+
+    def gather_rows(self, x_local: torch.Tensor) -> torch.Tensor:
+        p = self.part
+        send = x_local
+        if x_local.shape[0] != p.n_max:
+            send = x_local.new_zeros((p.n_max,) + tuple(x_local.shape[1:]))
+            send[: x_local.shape[0]] = x_local
+        out = x_local.new_empty((p.parts * p.n_max,) + tuple(x_local.shape[1:]))
+        self.dist.all_gather_into_tensor(out, send.contiguous())
+        return out
+
+    def gather_edges(self, v_local: torch.Tensor) -> torch.Tensor:
+        p = self.part
+        send = v_local
+        if v_local.shape[0] != p.e_max:
+            send = v_local.new_zeros((p.e_max,) + tuple(v_local.shape[1:]))
+            send[: v_local.shape[0]] = v_local
+        out = v_local.new_empty((p.parts * p.e_max,) + tuple(v_local.shape[1:]))
+        self.dist.all_gather_into_tensor(out, send.contiguous())
+        return out
+
+    def all_reduce_(self, t: torch.Tensor) -> torch.Tensor:
+        self.dist.all_reduce(t)
+        return t
+
+
+class CudaOps:
+    """Compute callbacks on one rank's views (the B200 kernels)."""
+
+    @staticmethod
+    def spmm(view, x, w, w_index, heads, scaling, fin, fout):
+        return D.spmm_csr(view, x, w, w_index, heads, scaling, fin, fout)
+
+    @staticmethod
+    def sddmm(view, x_rows, y_cols, heads):
+        sched = view.schedule()
+        out = torch.empty((view.num_edges, heads), dtype=x_rows.dtype, device=x_rows.device)
+        D.nat.call("hg_sddmm", D._p(view.offsets), D._p(view.cols), view.n_rows,
+                   view.num_edges, D._p(sched.units), sched.num_units, D._p(x_rows),
+                   D._p(y_cols), D._p(out), x_rows.shape[1], heads, D._dtype_code(x_rows),
+                   D._stream())
+        return out
+
+    @staticmethod
+    def attn(view, s_l, s_r, slope):
+        heads = s_l.shape[1]
+        out = torch.empty((view.num_edges, heads), dtype=s_l.dtype, device=s_l.device)
+        D.nat.call("hg_attn_scores", D._p(view.offsets), D._p(view.cols), view.n_rows,
+                   view.num_edges, D._p(s_l), D._p(s_r), heads, float(slope), D._p(out),
+                   D._dtype_code(s_l), D._stream())
+        return out
+
+    @staticmethod
+    def softmax_fwd(view, e):
+        heads = e.shape[1] if e.dim() == 2 else 1
+        alpha = torch.empty_like(e)
+        D.nat.call("hg_edge_softmax_fwd", D._p(view.offsets), view.n_rows, view.num_edges,
+                   D._p(e), D._p(alpha), heads, D._dtype_code(e), D._stream())
+        return alpha
+
+    @staticmethod
+    def softmax_bwd(view, alpha, g):
+        heads = alpha.shape[1] if alpha.dim() == 2 else 1
+        de = torch.empty_like(alpha)
+        D.nat.call("hg_edge_softmax_bwd", D._p(view.offsets), view.n_rows, view.num_edges,
+                   D._p(alpha), D._p(g), D._p(de), heads, D._dtype_code(alpha), D._stream())
+        return de
+
+    @staticmethod
+    def edge_sums(view, v, perm):
+        heads = v.shape[1] if v.dim() == 2 else 1
+        out = torch.empty((view.n_rows, heads), dtype=v.dtype, device=v.device)
+        D.nat.call("hg_edge_rowsum", D._p(view.offsets), view.n_rows, view.num_edges, D._p(v),
+                   D._p(perm), heads, D._p(out), D._dtype_code(v), D._stream())
+        return out
+
+
+class DistBundle:
+    """GraphBundle interface over one rank's partition: inputs and outputs are
+    the rank's local rows (or local edges); exchanges happen inside."""
+
+    numerics = "fast"
+
+    def __init__(self, part: LocalPart, exchange: Exchange, tables, ops=CudaOps):
+        self.part = part
+        self.ex = exchange
+        self.ops = ops
+        self._tables = tables  # callable (kind, side, dtype) -> global table [N]
+        self._cache = {}
+
+    @property
+    def n(self):
+        return self.part.n_local
+
+    @property
+    def num_edges(self):
+        return self.part.fwd.num_edges
+
+    def _padded(self, table):
+        p = self.part
+        out = table.new_zeros(p.parts * p.n_max)
+        for q in range(p.parts):
+            a, b = int(p.splits[q]), int(p.splits[q + 1])
+            out[q * p.n_max: q * p.n_max + (b - a)] = table[a:b]
+        return out
+
+    def norm_tables(self, norm, transpose, dtype):
+        key = (norm, transpose, dtype)
+        t = self._cache.get(key)
+        if t is None:
+            kind = "inv_sqrt" if norm == "both" else "inv"
+            row_side, col_side = ("col", "row") if transpose else ("row", "col")
+            fin = self._padded(self._tables(kind, col_side, dtype)) \
+                if norm in ("left", "both") else None
+            fout = self._tables(kind, row_side, dtype)[self.part.lo:self.part.hi].contiguous() \
+                if norm in ("right", "both") else None
+            t = (fin, fout)
+            self._cache[key] = t
+        return t
+
+    def spmm(self, x, w=None, scaling="post", norm="none", transpose=False, heads=1,
+             weight_via_perm=False):
+        view = self.part.bwd if transpose else self.part.fwd
+        x_full = self.ex.gather_rows(x.contiguous())
+        fin, fout = self.norm_tables(norm, transpose, x.dtype)
+        widx = None
+        if w is not None and weight_via_perm:
+            w = self.ex.gather_edges(w.contiguous())
+            widx = view.perm
+        return self.ops.spmm(view, x_full, w, widx, heads, scaling, fin, fout)
+
+    def sddmm(self, x, y, heads=1):
+        out = self.ops.sddmm(self.part.fwd, x.contiguous(), self.ex.gather_rows(y.contiguous()),
+                             heads)
+        return out[:, 0] if heads == 1 else out
+
+    def attn_logits(self, s_l, s_r, slope):
+        return self.ops.attn(self.part.fwd, s_l.contiguous(),
+                             self.ex.gather_rows(s_r.contiguous()), slope)
+
+    def softmax_fwd(self, e):
+        return self.ops.softmax_fwd(self.part.fwd, e.contiguous())
+
+    def softmax_bwd(self, alpha, g):
+        return self.ops.softmax_bwd(self.part.fwd, alpha, g)
+
+    def edge_sums(self, v, transpose=False):
+        v = v.contiguous()
+        if not transpose:
+            return self.ops.edge_sums(self.part.fwd, v, None)
+        return self.ops.edge_sums(self.part.bwd, self.ex.gather_edges(v), self.part.bwd.perm)
+
+
+class DistTrainer:
+    """Trainer over a row partition: same model init, masks and optimiser as
+    the 1-GPU Trainer (identical RNG stream); the loss is the global mean, the
+    weight gradients are all-reduced before Adam."""
+
+    def __init__(self, dg: D.DeviceGraph, features, labels, config, dist, ops=CudaOps):
+        from .models import Trainer
+
+        self.dist = dist
+        rank, parts = dist.get_rank(), dist.get_world_size()
+        part = make_local_part(dg.offsets, dg.cols, dg.bwd.offsets, dg.bwd.cols, dg.bwd.perm,
+                               rank, parts)
+        self.part = part
+        self.bundle = DistBundle(part, Exchange(dist, part),
+                                 lambda k, side, dt: dg.factor(k, side, dt), ops)
+        self.inner = Trainer(self.bundle, features, labels, config, row_slice=(part.lo, part.hi))
+        self.n_total = dg.n
+
+    @property
+    def x(self):
+        return self.inner.x
+
+    def load_features(self, feats, out=None):
+        lo, hi = self.part.lo, self.part.hi
+        return self.inner.load_features(feats[lo:hi], out=self.inner.x)
+
+    def step(self, overflow=None):
+        from .models import convert, cross_entropy
+
+        tr = self.inner
+        cfg = tr.cfg
+        logits = tr.model.forward(self.bundle, tr.x, cfg.mode, cfg.width, overflow)
+        if cfg.mode == "half":
+            logits = convert(logits, "float32", tr.conversions)
+        loss = cross_entropy(logits, tr.labels, tr.n_cls, denom=self.n_total)
+        loss.backward()
+        for p in tr.opt.params:
+            g = p.grad32()
+            self.dist.all_reduce(g)
+            p.published.grad = g
+        tr.opt.step()
+        total = loss.detach().clone()
+        self.dist.all_reduce(total)
+        return total, logits.detach()

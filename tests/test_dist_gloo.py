@@ -1,0 +1,150 @@
+"""CPU, world_size 2 over gloo: the row-partitioned execution path
+(partition.py) -- split points, padded column remapping, feature / gradient /
+edge-value all-gathers, global loss and weight-gradient all-reduce -- gives the
+same training step as one process.  The CUDA kernels are swapped for a host
+implementation of the same row-owned semantics (HostOps below, test-only), so
+this checks the exchange logic, not the kernels (those are the -m gpu tests)."""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as O
+
+
+class HostOps:
+    """Row-owned host compute over one CsrView (fp64 accumulation, one rounding)."""
+
+    @staticmethod
+    def _rows(view):
+        deg = view.offsets[1:] - view.offsets[:-1]
+        return torch.repeat_interleave(torch.arange(view.n_rows), deg)
+
+    @staticmethod
+    def spmm(view, x, w, w_index, heads, scaling, fin, fout):
+        xs = x.double()
+        if fin is not None:
+            xs = (x * fin[:, None]).to(x.dtype).double()
+        rows = HostOps._rows(view)
+        contrib = xs[view.cols.long()]
+        if w is not None:
+            idx = torch.arange(view.num_edges) if w_index is None else w_index.long()
+            wt = w.reshape(w.shape[0], -1)[idx].double()
+            f = x.shape[1]
+            contrib = contrib * wt.repeat_interleave(f // heads, dim=1)
+        s = torch.zeros((view.n_rows, x.shape[1]), dtype=torch.float64)
+        s.index_add_(0, rows, contrib)
+        if fout is None:
+            return s.to(x.dtype)
+        if scaling == "post":
+            h = s.to(x.dtype)
+            return torch.where(fout[:, None] > 0, h * fout[:, None], h)
+        return (s * fout.double()[:, None]).to(x.dtype)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _graph():
+    rng = np.random.default_rng(21)
+    n = 120
+    deg = np.minimum(rng.zipf(1.6, n), 90)
+    rows = np.repeat(np.arange(n), deg)
+    cols = rng.integers(0, n, rows.size)
+    r, c = O.canonical_edges(n, rows, cols)
+    x = rng.normal(size=(n, 10)).astype(np.float32)
+    labels = (np.arange(n) * 3) // n
+    return n, r, c, x, labels
+
+
+class HostGraph:
+    """The slice of DeviceGraph that DistTrainer uses, built on the host."""
+
+    def __init__(self, n, r, c):
+        self.n = n
+        self.offsets = torch.from_numpy(O.csr_offsets(n, r))
+        self.cols = torch.from_numpy(c.astype(np.int32))
+        tr, tc, perm = O.transpose_perm(n, r, c)
+
+        class _B:
+            pass
+
+        self.bwd = _B()
+        self.bwd.offsets = torch.from_numpy(O.csr_offsets(n, tr))
+        self.bwd.cols = torch.from_numpy(tc.astype(np.int32))
+        self.bwd.perm = torch.from_numpy(perm.astype(np.int32))
+        self._deg = {"row": np.diff(O.csr_offsets(n, r)), "col": np.bincount(c, minlength=n)}
+
+    def factor(self, kind, side, dtype):
+        np_dt = np.float16 if dtype == torch.float16 else np.float32
+        f = O.degree_factor(self._deg[side], kind, np_dt).astype(np_dt)
+        return torch.from_numpy(f)
+
+
+def _run(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2411_01109_b200.models import TrainConfig
+        from paper_2411_01109_b200.partition import DistTrainer
+
+        n, r, c, x, labels = _graph()
+        g = HostGraph(n, r, c)
+        cfg = TrainConfig(kind="gcn", mode="float32", hidden=8, device="cpu", seed=1)
+        tr = DistTrainer(g, torch.from_numpy(x), labels, cfg, dist, ops=HostOps)
+        losses = []
+        first = None
+        for _ in range(3):
+            loss, logits = tr.step()
+            losses.append(float(loss))
+            first = logits.numpy() if first is None else first
+        parts = [None] * world
+        dist.all_gather_object(parts, (tr.part.lo, tr.part.hi, first, logits.numpy()))
+        if rank == 0:
+            out_q.put((losses, parts, [p.master.numpy() for p in tr.inner.opt.params]))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run_world(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_run, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return res
+
+
+@pytest.mark.timeout(400)
+def test_two_rank_gcn_step_matches_single_rank():
+    l1, parts1, w1 = _run_world(1)
+    l2, parts2, w2 = _run_world(2)
+    n = _graph()[0]
+    # nnz-balanced split points (bit-exact rule)
+    offsets = O.csr_offsets(n, _graph()[1])
+    s = O.partition_splits(offsets, 2)
+    assert [(p[0], p[1]) for p in parts2] == [(int(s[0]), int(s[1])), (int(s[1]), int(s[2]))]
+    # step 1 (same weights): row-owned aggregation + global tables give
+    # identical logits, rank by rank
+    np.testing.assert_array_equal(parts1[0][2], np.concatenate([p[2] for p in parts2], axis=0))
+    # later steps differ only through the all-reduce summation order of the grads
+    np.testing.assert_allclose(parts1[0][3], np.concatenate([p[3] for p in parts2], axis=0),
+                               rtol=1e-5, atol=1e-6)
+    # loss / weight gradients are all-reduced sums: equal up to summation order
+    np.testing.assert_allclose(l1, l2, rtol=1e-6, atol=1e-7)
+    for a, b in zip(w1, w2):
+        np.testing.assert_allclose(a, b, rtol=1e-5, atol=1e-6)
