@@ -101,8 +101,51 @@ __device__ __forceinline__ void load_idx(const int32_t* __restrict__ base, int64
 
 // ------------------------------------------------------------- fast kernel
 
+// acc[i] += x[i] (f16 or f32 element), one fp32 rounding.  For binary16 inputs
+// sm_100a fuses the widening into the add (FHADD / FHFMA: add.rn.f32.f16,
+// fma.rn.f32.f16), halving the ALU work of the gather loop.
+template <typename T, int V>
+__device__ __forceinline__ void acc_add(float (&acc)[V],
+                                        const typename RawVec<V * sizeof(T)>::type& r) {
+  if constexpr (sizeof(T) == 2) {
+    const unsigned short* h = reinterpret_cast<const unsigned short*>(&r);
+#pragma unroll
+    for (int i = 0; i < V; ++i)
+      asm("add.rn.f32.f16 %0, %1, %0;" : "+f"(acc[i]) : "h"(h[i]));
+  } else {
+    const float* p = reinterpret_cast<const float*>(&r);
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc[i] += p[i];
+  }
+}
+
+// acc[i] += w * x[i]; w in the element type.
+template <typename T, int V>
+__device__ __forceinline__ void acc_fma(float (&acc)[V], T w,
+                                        const typename RawVec<V * sizeof(T)>::type& r) {
+  if constexpr (sizeof(T) == 2) {
+    const unsigned short* h = reinterpret_cast<const unsigned short*>(&r);
+    const unsigned short wb = __half_as_ushort(w);
+#pragma unroll
+    for (int i = 0; i < V; ++i)
+      asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(acc[i]) : "h"(wb), "h"(h[i]));
+  } else {
+    const float* p = reinterpret_cast<const float*>(&r);
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc[i] = fmaf(w, p[i], acc[i]);
+  }
+}
+
+// Minimum resident blocks per SM: caps registers so that 256-thread blocks of
+// single-chunk teams run 3-4 deep (24-32 warps/SM) for memory-level
+// parallelism, without spilling (ptxas -v: 64 regs unweighted TEAM >= 8).
+template <int TEAM, int NCH, bool WT>
+struct FastOcc {
+  static constexpr int value = NCH == 1 ? ((!WT && TEAM >= 8) ? 4 : 3) : (NCH == 2 ? 2 : 1);
+};
+
 template <typename T, int V, int TEAM, int NCH, bool WEIGHTED>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, FastOcc<TEAM, NCH, WEIGHTED>::value)
 k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __restrict__ cols,
             int64_t num_edges, const T* __restrict__ w, const int32_t* __restrict__ widx,
             int heads, int fh, const T* __restrict__ x, T* __restrict__ y,
@@ -122,14 +165,14 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
   const int row = un.x, beg = un.y, end = un.z, slot = un.w;
   const int nvec = F / V;
 
-  int coff[NCH];
+  const T* xl[NCH];   // lane's column offset into every feature row
   bool cval[NCH];
   int chead[NCH];
 #pragma unroll
   for (int k = 0; k < NCH; ++k) {
-    int c = tl + k * TEAM;
+    const int c = tl + k * TEAM;
     cval[k] = c < nvec;
-    coff[k] = c * V;
+    xl[k] = x + c * V;
     chead[k] = WEIGHTED ? (c * V) / fh : 0;
   }
   float acc[NCH][V];
@@ -138,8 +181,8 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
 #pragma unroll
     for (int i = 0; i < V; ++i) acc[k][i] = 0.0f;
 
-  // Align batches to the absolute address of cols so column ids come in as
-  // vector loads.
+  // Batches aligned to the absolute address of cols so the column ids come in
+  // as vector loads; the first / last batch of a unit are partial.
   const int mis = (int)((reinterpret_cast<uintptr_t>(cols) >> 2) & (EB - 1));
   int64_t base = (int64_t)beg - (((int64_t)beg + mis) & (EB - 1));
   for (; base < end; base += EB) {
@@ -148,39 +191,35 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
     if (tl * CPL < EB) load_idx<CPL>(cols, lo, num_edges, myc);
     int myw[CPL] = {};
     if (WEIGHTED && widx != nullptr && tl * CPL < EB) load_idx<CPL>(widx, lo, num_edges, myw);
+    const bool full = base >= beg && base + EB <= end;
 
     Raw raw[EB][NCH];
-    float wv[EB][NCH];
-    bool ok[EB];
+    T wv[EB][NCH];
 #pragma unroll
     for (int j = 0; j < EB; ++j) {
       const int64_t e = base + j;
-      ok[j] = e >= beg && e < end;
+      const bool ok = full || (e >= beg && e < end);
       const int c = __shfl_sync(tmask, myc[j % CPL], j / CPL, TEAM);
       int wi = (int)e;
       if (WEIGHTED && widx != nullptr) wi = __shfl_sync(tmask, myw[j % CPL], j / CPL, TEAM);
+      const int64_t roff = (int64_t)c * F;
 #pragma unroll
       for (int k = 0; k < NCH; ++k) {
-        if (ok[j] && cval[k]) {
-          raw[j][k] = __ldg(reinterpret_cast<const Raw*>(x + (int64_t)c * F + coff[k]));
-          if (WEIGHTED) wv[j][k] = Num<T>::to_f(w[(int64_t)wi * heads + chead[k]]);
+        if (ok && cval[k]) {
+          raw[j][k] = __ldg(reinterpret_cast<const Raw*>(xl[k] + roff));
+          if (WEIGHTED) wv[j][k] = w[(int64_t)wi * heads + chead[k]];
         }
       }
     }
 #pragma unroll
     for (int j = 0; j < EB; ++j) {
+      const int64_t e = base + j;
+      const bool ok = full || (e >= beg && e < end);
 #pragma unroll
       for (int k = 0; k < NCH; ++k) {
-        if (ok[j] && cval[k]) {
-          float f[V];
-          raw_to_float<T, V>(raw[j][k], f);
-          if (WEIGHTED) {
-#pragma unroll
-            for (int i = 0; i < V; ++i) acc[k][i] = fmaf(wv[j][k], f[i], acc[k][i]);
-          } else {
-#pragma unroll
-            for (int i = 0; i < V; ++i) acc[k][i] += f[i];
-          }
+        if (ok && cval[k]) {
+          if (WEIGHTED) acc_fma<T, V>(acc[k], wv[j][k], raw[j][k]);
+          else acc_add<T, V>(acc[k], raw[j][k]);
         }
       }
     }
@@ -190,11 +229,11 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
     const T fo = fout ? fout[row] : Num<T>::zero();
 #pragma unroll
     for (int k = 0; k < NCH; ++k)
-      if (cval[k]) store_out<T, V>(y + (int64_t)row * F + coff[k], acc[k], fmode, fo);
+      if (cval[k]) store_out<T, V>(y + (int64_t)row * F + (xl[k] - x), acc[k], fmode, fo);
   } else {
 #pragma unroll
     for (int k = 0; k < NCH; ++k)
-      if (cval[k]) store_carry<V>(carry + (int64_t)slot * F + coff[k], acc[k]);
+      if (cval[k]) store_carry<V>(carry + (int64_t)slot * F + (xl[k] - x), acc[k]);
   }
 }
 
