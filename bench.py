@@ -226,6 +226,48 @@ def spmm_sweep(dg, peak, feats=(16, 32, 64, 128, 256, 512), reps=3):
     return out
 
 
+def small_configs(args, peak):
+    """C1 (Cora-shaped 2-layer GCN) and C2 (Pubmed-shaped 3-layer 4-head GAT):
+    device-timed ms/epoch, plus the oracle port's epoch on the same graph."""
+    import numpy as np
+    import torch
+
+    from paper_2411_01109_b200 import graphgen
+    from paper_2411_01109_b200.device import DeviceGraph
+    from paper_2411_01109_b200.models import GraphBundle, Trainer, TrainConfig
+
+    out = {}
+    specs = [("C1_gcn_cora", graphgen.cora_like, dict(kind="gcn", hidden=16)),
+             ("C2_gat_pubmed_3x4", graphgen.pubmed_like,
+              dict(kind="gat", hidden=16, heads=4, layers=3))]
+    for name, gen, kw in specs:
+        rows, cols, feats, labels = gen(0)
+        n = feats.shape[0]
+        dg = DeviceGraph.from_edges(n, rows, cols)
+        tr = Trainer(GraphBundle.build(dg), feats, labels, TrainConfig(**kw))
+        for _ in range(3):
+            tr.step()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        steps = 20
+        for _ in range(steps):
+            tr.step()
+        b.record()
+        torch.cuda.synchronize()
+        rec = {"ms_per_epoch": round(a.elapsed_time(b) / steps, 4), "nodes": n,
+               "edges": int(rows.size)}
+        if not args.no_cpu_baseline:
+            import oracle as O
+
+            g = O.OracleGraph(n, rows, cols)
+            t0 = time.perf_counter()
+            O.train_epochs(g, feats, labels, epochs=1, **kw)
+            rec["cpu_oracle_ms_per_epoch"] = round((time.perf_counter() - t0) * 1e3, 1)
+        out[name] = rec
+    return out
+
+
 def b200_arm(args, ws, rank, local):
     import numpy as np
     import torch
@@ -328,6 +370,8 @@ def b200_arm(args, ws, rank, local):
         }
     if not args.no_sweep and ws == 1:
         result["spmm_sweep_reddit"] = spmm_sweep(dg, peak)
+    if rank == 0 and ws == 1 and not args.no_small:
+        result["small_configs"] = small_configs(args, peak)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         offsets = dg.offsets.cpu().numpy()
         cols = dg.cols.cpu().numpy()
@@ -350,6 +394,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-small", action="store_true", help="skip the C1/C2 epoch timings")
     ap.add_argument("--cpu-budget-edges", type=int, default=400_000)
     ap.add_argument("--ref-budget-edges", type=int, default=400_000)
     args = ap.parse_args()

@@ -141,80 +141,72 @@ __device__ __forceinline__ void acc_fma(float (&acc)[V], T w,
 // parallelism, without spilling (ptxas -v: 64 regs unweighted TEAM >= 8).
 template <int TEAM, int NCH, bool WT>
 struct FastOcc {
-  static constexpr int value = NCH == 1 ? ((!WT && TEAM >= 8) ? 4 : 3) : (NCH == 2 ? 2 : 1);
+  static constexpr int value = NCH == 1 ? ((!WT && TEAM >= 8 && TEAM <= 16) ? 4 : 3) : (NCH == 2 ? 2 : 1);
 };
 
+// Column ids of one batch: lane tl holds ids [base + tl*CPL, +CPL).  FULL
+// batches lie inside [0, num_edges) and use unguarded vector loads.
+template <int CPL, bool FULL>
+__device__ __forceinline__ void load_batch_ids(const int32_t* __restrict__ base_ptr, int lo,
+                                               int limit, int (&out)[CPL]) {
+  if constexpr (FULL) {
+    const int32_t* p = base_ptr + lo;
+    if constexpr (CPL == 1) {
+      out[0] = __ldcs(p);
+    } else if constexpr (CPL == 2) {
+      int2 v = __ldcs(reinterpret_cast<const int2*>(p));
+      out[0] = v.x; out[1] = v.y;
+    } else {
+#pragma unroll
+      for (int q = 0; q < CPL; q += 4) {
+        int4 v = __ldcs(reinterpret_cast<const int4*>(p + q));
+        out[q] = v.x; out[q + 1] = v.y; out[q + 2] = v.z; out[q + 3] = v.w;
+      }
+    }
+  } else {
+    load_idx<CPL>(base_ptr, lo, limit, out);
+  }
+}
+
+// Per-team state of k_spmm_fast: lane column offsets, accumulators, unit range.
 template <typename T, int V, int TEAM, int NCH, bool WEIGHTED>
-__global__ void __launch_bounds__(256, FastOcc<TEAM, NCH, WEIGHTED>::value)
-k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __restrict__ cols,
-            int64_t num_edges, const T* __restrict__ w, const int32_t* __restrict__ widx,
-            int heads, int fh, const T* __restrict__ x, T* __restrict__ y,
-            float* __restrict__ carry, int F, int fmode, const T* __restrict__ fout) {
-  constexpr int EB = NCH >= 2 ? 4 : 8;                 // edges gathered per batch
-  constexpr int CPL = TEAM >= EB ? 1 : EB / TEAM;      // column ids loaded per lane
+struct FastTeam {
+  static constexpr int EB = NCH >= 2 ? 4 : 8;             // edges gathered per batch
+  static constexpr int CPL = TEAM >= EB ? 1 : EB / TEAM;  // column ids per loading lane
   using Raw = typename RawVec<V * sizeof(T)>::type;
 
-  const int lane = threadIdx.x & 31;
-  const int tl = lane & (TEAM - 1);
-  const unsigned tmask =
-      TEAM == 32 ? 0xffffffffu : (((1u << TEAM) - 1u) << (lane & ~(TEAM - 1)));
-  const int64_t team = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TEAM;
-  if (team >= num_units) return;
-
-  const int4 un = units[team];
-  const int row = un.x, beg = un.y, end = un.z, slot = un.w;
-  const int nvec = F / V;
-
-  const T* xl[NCH];   // lane's column offset into every feature row
+  const T* xl[NCH];
   bool cval[NCH];
   int chead[NCH];
-#pragma unroll
-  for (int k = 0; k < NCH; ++k) {
-    const int c = tl + k * TEAM;
-    cval[k] = c < nvec;
-    xl[k] = x + c * V;
-    chead[k] = WEIGHTED ? (c * V) / fh : 0;
-  }
   float acc[NCH][V];
-#pragma unroll
-  for (int k = 0; k < NCH; ++k)
-#pragma unroll
-    for (int i = 0; i < V; ++i) acc[k][i] = 0.0f;
+  unsigned tmask;
+  int beg, end, F, heads;
+  const T* w;
+  bool use_widx;
 
-  // Batches aligned to the absolute address of cols so the column ids come in
-  // as vector loads; the first / last batch of a unit are partial.
-  const int mis = (int)((reinterpret_cast<uintptr_t>(cols) >> 2) & (EB - 1));
-  int64_t base = (int64_t)beg - (((int64_t)beg + mis) & (EB - 1));
-  for (; base < end; base += EB) {
-    int myc[CPL] = {};
-    const int64_t lo = base + (int64_t)tl * CPL;
-    if (tl * CPL < EB) load_idx<CPL>(cols, lo, num_edges, myc);
-    int myw[CPL] = {};
-    if (WEIGHTED && widx != nullptr && tl * CPL < EB) load_idx<CPL>(widx, lo, num_edges, myw);
-    const bool full = base >= beg && base + EB <= end;
-
+  // One batch of EB edges [b, b+EB): issue every gather, then accumulate.
+  template <bool FULL>
+  __device__ __forceinline__ void batch(int b, const int (&ids)[CPL], const int (&wids)[CPL]) {
     Raw raw[EB][NCH];
     T wv[EB][NCH];
 #pragma unroll
     for (int j = 0; j < EB; ++j) {
-      const int64_t e = base + j;
-      const bool ok = full || (e >= beg && e < end);
-      const int c = __shfl_sync(tmask, myc[j % CPL], j / CPL, TEAM);
-      int wi = (int)e;
-      if (WEIGHTED && widx != nullptr) wi = __shfl_sync(tmask, myw[j % CPL], j / CPL, TEAM);
-      const int64_t roff = (int64_t)c * F;
+      const bool ok = FULL || (b + j >= beg && b + j < end);
+      const int c = __shfl_sync(tmask, ids[j % CPL], j / CPL, TEAM);
+      int wi = b + j;
+      if (WEIGHTED && use_widx) wi = __shfl_sync(tmask, wids[j % CPL], j / CPL, TEAM);
+      const size_t roff = (size_t)(unsigned)c * (unsigned)F;
 #pragma unroll
       for (int k = 0; k < NCH; ++k) {
         if (ok && cval[k]) {
           raw[j][k] = __ldg(reinterpret_cast<const Raw*>(xl[k] + roff));
-          if (WEIGHTED) wv[j][k] = w[(int64_t)wi * heads + chead[k]];
+          if (WEIGHTED) wv[j][k] = w[(size_t)(unsigned)wi * heads + chead[k]];
         }
       }
     }
 #pragma unroll
     for (int j = 0; j < EB; ++j) {
-      const int64_t e = base + j;
-      const bool ok = full || (e >= beg && e < end);
+      const bool ok = FULL || (b + j >= beg && b + j < end);
 #pragma unroll
       for (int k = 0; k < NCH; ++k) {
         if (ok && cval[k]) {
@@ -224,16 +216,91 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
       }
     }
   }
+};
+
+template <typename T, int V, int TEAM, int NCH, bool WEIGHTED>
+__global__ void __launch_bounds__(256, FastOcc<TEAM, NCH, WEIGHTED>::value)
+k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __restrict__ cols,
+            int64_t num_edges, const T* __restrict__ w, const int32_t* __restrict__ widx,
+            int heads, int fh, const T* __restrict__ x, T* __restrict__ y,
+            float* __restrict__ carry, int F, int fmode, const T* __restrict__ fout) {
+  using Team = FastTeam<T, V, TEAM, NCH, WEIGHTED>;
+  constexpr int EB = Team::EB;
+  constexpr int CPL = Team::CPL;
+
+  const int lane = threadIdx.x & 31;
+  const int tl = lane & (TEAM - 1);
+  const int64_t team_id = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TEAM;
+  if (team_id >= num_units) return;
+
+  const int4 un = units[team_id];
+  const int row = un.x, slot = un.w;
+  const int nvec = F / V;
+  const int limit = (int)num_edges;
+  const bool loader = tl * CPL < EB;  // lanes that fetch column ids
+
+  Team t;
+  t.tmask = TEAM == 32 ? 0xffffffffu : (((1u << TEAM) - 1u) << (lane & ~(TEAM - 1)));
+  t.beg = un.y;
+  t.end = un.z;
+  t.F = F;
+  t.heads = heads;
+  t.w = w;
+  t.use_widx = WEIGHTED && widx != nullptr;
+#pragma unroll
+  for (int k = 0; k < NCH; ++k) {
+    const int c = tl + k * TEAM;
+    t.cval[k] = c < nvec;
+    t.xl[k] = x + c * V;
+    t.chead[k] = WEIGHTED ? (c * V) / fh : 0;
+#pragma unroll
+    for (int i = 0; i < V; ++i) t.acc[k][i] = 0.0f;
+  }
+  const int beg = t.beg, end = t.end;
+
+  // Batches aligned to the absolute address of cols (vector id loads).
+  const int mis = (int)((reinterpret_cast<uintptr_t>(cols) >> 2) & (EB - 1));
+  int b = beg - ((beg + mis) & (EB - 1));
+  if (b < beg) {  // partial head batch
+    int ids[CPL] = {}, wids[CPL] = {};
+    if (loader) load_batch_ids<CPL, false>(cols, b + tl * CPL, limit, ids);
+    if (t.use_widx && loader) load_batch_ids<CPL, false>(widx, b + tl * CPL, limit, wids);
+    t.template batch<false>(b, ids, wids);
+    b += EB;
+  }
+  if (b + EB <= end) {  // full batches, column ids prefetched one batch ahead
+    int ids[CPL] = {}, wids[CPL] = {};
+    if (loader) load_batch_ids<CPL, true>(cols, b + tl * CPL, limit, ids);
+    if (t.use_widx && loader) load_batch_ids<CPL, true>(widx, b + tl * CPL, limit, wids);
+    for (;;) {
+      const int nb = b + EB;
+      const bool more = nb + EB <= end;
+      int nids[CPL] = {}, nwids[CPL] = {};
+      if (more && loader) load_batch_ids<CPL, true>(cols, nb + tl * CPL, limit, nids);
+      if (more && t.use_widx && loader) load_batch_ids<CPL, true>(widx, nb + tl * CPL, limit, nwids);
+      t.template batch<true>(b, ids, wids);
+      b = nb;
+      if (!more) break;
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) { ids[q] = nids[q]; wids[q] = nwids[q]; }
+    }
+  }
+  if (b < end) {  // partial tail batch
+    int ids[CPL] = {}, wids[CPL] = {};
+    if (loader) load_batch_ids<CPL, false>(cols, b + tl * CPL, limit, ids);
+    if (t.use_widx && loader) load_batch_ids<CPL, false>(widx, b + tl * CPL, limit, wids);
+    t.template batch<false>(b, ids, wids);
+  }
 
   if (slot < 0) {
     const T fo = fout ? fout[row] : Num<T>::zero();
 #pragma unroll
     for (int k = 0; k < NCH; ++k)
-      if (cval[k]) store_out<T, V>(y + (int64_t)row * F + (xl[k] - x), acc[k], fmode, fo);
+      if (t.cval[k]) store_out<T, V>(y + (int64_t)row * F + (t.xl[k] - x), t.acc[k], fmode, fo);
   } else {
 #pragma unroll
     for (int k = 0; k < NCH; ++k)
-      if (cval[k]) store_carry<V>(carry + (int64_t)slot * F + (xl[k] - x), acc[k]);
+      if (t.cval[k]) store_carry<V>(carry + (int64_t)slot * F + (t.xl[k] - x), t.acc[k]);
   }
 }
 

@@ -522,9 +522,11 @@ class GATLayer:
         z = matmul(x, self.w.publish(mode))                       # [N, H*so]
         zh = z.view(z.shape[0], h, so)
         a_l, a_r = self.a_l.publish(mode), self.a_r.publish(mode)
-        # s = z_h . a_h with fp32 accumulation and one rounding (models.matmul)
-        s_l = torch.einsum("nhf,hf->nh", zh.float(), a_l.float()).to(z.dtype)
-        s_r = torch.einsum("nhf,hf->nh", zh.float(), a_r.float()).to(z.dtype)
+        # s = z_h . a_h: one batched tensor-core GEMM per head pair [a_l | a_r],
+        # fp32 accumulation and one rounding (models.matmul semantics)
+        s = torch.matmul(zh.transpose(0, 1), torch.stack([a_l, a_r], dim=-1))  # [H, N, 2]
+        s_l = s[..., 0].t().contiguous()
+        s_r = s[..., 1].t().contiguous()
         e = attention_logits(bundle, s_l, s_r, 0.2)               # [E, H]
         alpha = edge_softmax(bundle, e, overflow, tag + "/softmax")
         out = spmm_weighted(bundle, alpha if h > 1 else alpha[:, 0], z, width, overflow, tag)
