@@ -641,20 +641,25 @@ def cross_entropy(logits, labels, n_active=None, denom=None):
 
 
 class Adam:
-    """models.Adam (models.py:575-592) on device fp32 masters."""
+    """models.Adam (models.py:575-592) on device fp32 masters.  The step count
+    lives on the device (fp64) so a step can be captured in a CUDA graph."""
 
     def __init__(self, params, lr=1e-2, betas=(0.9, 0.999), eps=1e-8):
         self.params = list(params)
         self.lr, self.betas, self.eps = lr, betas, eps
         self.m = [torch.zeros_like(p.master) for p in self.params]
         self.v = [torch.zeros_like(p.master) for p in self.params]
+        dev = self.params[0].master.device if self.params else "cpu"
+        self._t = torch.zeros((), dtype=torch.float64, device=dev)
         self.t = 0
 
     @torch.no_grad()
     def step(self):
         self.t += 1
         b1, b2 = self.betas
-        c1, c2 = 1 - b1 ** self.t, 1 - b2 ** self.t
+        self._t.add_(1.0)
+        c1 = (1.0 - torch.pow(b1, self._t)).float()
+        c2 = (1.0 - torch.pow(b2, self._t)).float()
         for p, m, v in zip(self.params, self.m, self.v):
             g = p.grad32()
             m.add_((1 - b1) * (g - m))
@@ -743,6 +748,8 @@ class Trainer:
         self.dtype = _DTYPES[config.mode]
         self.x = self.load_features(feats[lo:hi])
         self.conversions = ConversionCounter()
+        self._graph = None
+        self._graph_out = None
 
     def load_features(self, feats, out=None):
         """Round to the compute dtype (via fp32, as models.train does) and pad
@@ -755,6 +762,12 @@ class Trainer:
         return out
 
     def step(self, overflow=None):
+        if self._graph is not None and overflow is None:
+            self._graph.replay()
+            return self._graph_out
+        return self._step_eager(overflow)
+
+    def _step_eager(self, overflow=None):
         cfg = self.cfg
         logits = self.model.forward(self.bundle, self.x, cfg.mode, cfg.width, overflow)
         if cfg.mode == "half":
@@ -763,6 +776,24 @@ class Trainer:
         loss.backward()
         self.opt.step()
         return loss.detach(), logits.detach()
+
+    def capture(self, warmup=0):
+        """Record one training step (forward, backward, Adam) as a CUDA graph;
+        later step() calls replay it (one launch per epoch).  Call after at
+        least one eager step (schedules, workspaces and cuBLAS state exist);
+        capturing does not advance training, `warmup` extra side-stream steps
+        do.  Inputs stay at self.x (refresh with load_features(..., out=self.x))."""
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(warmup):
+                self._step_eager()
+        torch.cuda.current_stream().wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            out = self._step_eager()
+        self._graph, self._graph_out = graph, out
+        return graph
 
 
 def train(g, features, labels, config: TrainConfig) -> TrainResult:

@@ -369,3 +369,21 @@ def test_smoke_entry(cuda):
     import __graft_entry__
 
     __graft_entry__.smoke()
+
+
+def test_cuda_graph_step_matches_eager(cuda):
+    """A captured training step replays to the same losses as eager steps."""
+    from paper_2411_01109_b200 import graphgen, models as M
+    from paper_2411_01109_b200.device import DeviceGraph
+
+    rows, cols, feats, labels = graphgen.synth_sbm(300, 3, 0.05, 0.005, 12, 4)
+    dg = DeviceGraph.from_edges(300, rows, cols)
+    for kind, kw in (("gcn", {}), ("gat", {"heads": 2, "layers": 3}), ("gin", {})):
+        cfg = M.TrainConfig(kind=kind, hidden=8, **kw)
+        a = M.Trainer(M.GraphBundle.build(dg), feats, labels, cfg)
+        b = M.Trainer(M.GraphBundle.build(dg), feats, labels, cfg)
+        la = [float(a.step()[0]) for _ in range(6)]
+        lb = [float(b.step()[0])]
+        b.capture()
+        lb += [float(b.step()[0]) for _ in range(5)]
+        np.testing.assert_allclose(la, lb, rtol=0, atol=1e-6, err_msg=kind)
