@@ -245,18 +245,22 @@ def small_configs(args, peak):
         n = feats.shape[0]
         dg = DeviceGraph.from_edges(n, rows, cols)
         tr = Trainer(GraphBundle.build(dg), feats, labels, TrainConfig(**kw))
+        def timed(steps=20):
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(steps):
+                tr.step()
+            b.record()
+            torch.cuda.synchronize()
+            return round(a.elapsed_time(b) / steps, 4)
+
         for _ in range(3):
             tr.step()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        steps = 20
-        for _ in range(steps):
-            tr.step()
-        b.record()
-        torch.cuda.synchronize()
-        rec = {"ms_per_epoch": round(a.elapsed_time(b) / steps, 4), "nodes": n,
-               "edges": int(rows.size)}
+        eager = timed()
+        tr.capture()
+        rec = {"ms_per_epoch": timed(), "ms_per_epoch_eager": eager, "cuda_graph": True,
+               "nodes": n, "edges": int(rows.size)}
         if not args.no_cpu_baseline:
             import oracle as O
 
@@ -328,15 +332,20 @@ def b200_arm(args, ws, rank, local):
     final_loss = float(loss)
 
     # ---- end to end through the public loop: host features in, loss out ----
-    host_x = x.cpu().pin_memory()
-    h2d = host_x.numel() * host_x.element_size() // (ws if ws > 1 else 1)
+    inner = tr.inner if ws > 1 else tr
+    lo, hi = (tr.part.lo, tr.part.hi) if ws > 1 else (0, dg.n)
+    host_x = inner.host_features(x[lo:hi].cpu())
+    h2d = host_x.numel() * host_x.element_size()
     barrier()
     torch.cuda.synchronize()
     e0 = time.perf_counter()
-    for _ in range(args.steps):
-        tr.load_features(host_x, out=tr.x) if ws == 1 else tr.load_features(host_x)
-        loss, _ = tr.step()
-        float(loss)  # the reference loop's NaN check reads the loss every epoch
+    if ws > 1:
+        for _ in range(args.steps):
+            inner.x.copy_(host_x, non_blocking=True)
+            loss, _ = tr.step()
+            float(loss)
+    else:
+        tr.run_epochs(host_x, args.steps)
     torch.cuda.synchronize()
     barrier()
     e2e_ms = (time.perf_counter() - e0) * 1e3 / args.steps

@@ -777,6 +777,50 @@ class Trainer:
         self.opt.step()
         return loss.detach(), logits.detach()
 
+    def host_features(self, feats):
+        """Pinned host copy of the features in the device storage layout
+        (compute dtype, columns padded to the 8-aligned width)."""
+        f = feats if isinstance(feats, torch.Tensor) else torch.from_numpy(np.asarray(feats))
+        n, w = f.shape
+        host = torch.zeros((n, self.in_store), dtype=self.dtype).pin_memory()
+        host[:, :w] = f.to(torch.float32).to(self.dtype) if f.dtype != self.dtype else f
+        return host
+
+    def run_epochs(self, host_x, epochs, check_loss=True):
+        """Train `epochs` epochs feeding the inputs from pinned host memory every
+        epoch: the next epoch's host->device copy runs on a side stream while
+        the current epoch computes (double-buffered), and the loss is read back
+        and checked every epoch like models.train.  Returns the losses."""
+        cur_stream = torch.cuda.current_stream()
+        copy_stream = torch.cuda.Stream()
+        bufs = [self.x, torch.empty_like(self.x)]
+        copied = [torch.cuda.Event(), torch.cuda.Event()]
+        used = [torch.cuda.Event(), torch.cuda.Event()]
+        copy_stream.wait_stream(cur_stream)
+        with torch.cuda.stream(copy_stream):
+            bufs[0].copy_(host_x, non_blocking=True)
+            copied[0].record()
+        losses = []
+        for i in range(epochs):
+            cur, nxt = i % 2, 1 - i % 2
+            if i + 1 < epochs:
+                with torch.cuda.stream(copy_stream):
+                    if i >= 1:
+                        copy_stream.wait_event(used[nxt])
+                    bufs[nxt].copy_(host_x, non_blocking=True)
+                    copied[nxt].record()
+            cur_stream.wait_event(copied[cur])
+            self.x = bufs[cur]
+            loss, _ = self._step_eager()
+            used[cur].record()
+            if check_loss:
+                lv = float(loss)
+                if not math.isfinite(lv):
+                    raise NanLossError(i, OverflowCounters())
+                losses.append(lv)
+        self.x = bufs[0]
+        return losses
+
     def capture(self, warmup=0):
         """Record one training step (forward, backward, Adam) as a CUDA graph;
         later step() calls replay it (one launch per epoch).  Call after at

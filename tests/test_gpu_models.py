@@ -387,3 +387,18 @@ def test_cuda_graph_step_matches_eager(cuda):
         b.capture()
         lb += [float(b.step()[0]) for _ in range(5)]
         np.testing.assert_allclose(la, lb, rtol=0, atol=1e-6, err_msg=kind)
+
+
+def test_run_epochs_host_feed_matches_steps(cuda):
+    """Double-buffered host feeding (e2e path) trains exactly like step()."""
+    from paper_2411_01109_b200 import graphgen, models as M
+    from paper_2411_01109_b200.device import DeviceGraph
+
+    rows, cols, feats, labels = graphgen.synth_sbm(200, 2, 0.05, 0.005, 10, 2)
+    dg = DeviceGraph.from_edges(200, rows, cols)
+    cfg = M.TrainConfig(kind="gcn", hidden=8)
+    a = M.Trainer(M.GraphBundle.build(dg), feats, labels, cfg)
+    b = M.Trainer(M.GraphBundle.build(dg), feats, labels, cfg)
+    la = [float(a.step()[0]) for _ in range(5)]
+    lb = b.run_epochs(b.host_features(feats), 5)
+    assert la == lb
