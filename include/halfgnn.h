@@ -177,6 +177,31 @@ int hg_edge_rowsum(const int64_t* offsets, int64_t n_rows, int64_t num_edges,
                    const void* vals, const int32_t* perm, int32_t heads, void* out,
                    int dtype, void* stream);
 
+/* ------------------------------------------------------------------- loss */
+
+/* cross_entropy forward + backward in one pass (models.py:552-572), fp64 math:
+ * per row i, z = logits[i, :c_active] - max, nll[i] = log(sum exp z) - z[label],
+ * grad[i, j] = (softmax(z)_j - [j == label]) / denom for j < c_active, 0 for
+ * c_active <= j < ld (storage padding).  Loss = sum(nll) / denom. */
+int hg_softmax_xent(const float* logits, int64_t ld, const int64_t* labels, int64_t n,
+                    int32_t c_active, double denom, float* grad, double* nll, void* stream);
+
+/* GAT attention projections (models.py:503-506, s_l = z a_l, s_r = z a_r) for all
+ * heads at once: s_l[n*H+h] = rnd(sum_f z[n, h*fh+f] * a_l[h*fh+f]) (fp32
+ * accumulation of exact products, one rounding), same for s_r. */
+int hg_head_dots(const void* z, const void* a_l, const void* a_r, int64_t n, int32_t heads,
+                 int32_t fh, void* s_l, void* s_r, int dtype, void* stream);
+
+/* models.Adam step (models.py:583-592) over flat fp32 arrays, the reference's
+ * operation order with one fp32 rounding per op:
+ *   m += omb1*(g-m); v += omb2*(g*g-v); p -= lr*(m/c1) / (sqrt(v/c2) + eps),
+ *   c1 = fp32(1 - b1^t), c2 = fp32(1 - b2^t) with t = *step (device fp64).
+ * omb1/omb2 are fp32(1 - b1) / fp32(1 - b2) formed in double by the caller.
+ * g is read from `grad` (dtype) and widened. */
+int hg_adam_step(float* master, float* m, float* v, const void* grad, int grad_dtype,
+                 int64_t count, float lr, float omb1, float omb2, double b1, double b2,
+                 float eps, const double* step, void* stream);
+
 /* ---------------------------------------------------------------- elementwise */
 
 /* out = rnd(x * s) with the product formed in fp64 (the reference multiplies

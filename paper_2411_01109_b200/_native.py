@@ -8,7 +8,8 @@ HG_ECUDA -> RuntimeError.
 from __future__ import annotations
 
 import ctypes
-from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_int64, c_size_t, c_void_p
+from ctypes import (POINTER, c_char_p, c_double, c_float, c_int, c_int32, c_int64, c_size_t,
+                    c_void_p)
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().with_name("libhalfgnn.so")
@@ -50,6 +51,10 @@ SIGNATURES = {
     "hg_edge_softmax_bwd": [_P, _I64, _I64, _P, _P, _P, _I32, c_int, _P],
     "hg_edge_rowsum": [_P, _I64, _I64, _P, _P, _I32, _P, c_int, _P],
     "hg_scale_f64": [_P, c_double, _P, _I64, c_int, _P],
+    "hg_softmax_xent": [_P, _I64, _P, _I64, _I32, c_double, _P, _P, _P],
+    "hg_head_dots": [_P, _P, _P, _I64, _I32, _I32, _P, _P, c_int, _P],
+    "hg_adam_step": [_P, _P, _P, _P, c_int, _I64, c_float, c_float, c_float, c_double, c_double,
+                     c_float, _P, _P],
 }
 _RESTYPES = {"hg_last_error": c_char_p}
 

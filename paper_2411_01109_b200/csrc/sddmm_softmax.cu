@@ -56,7 +56,7 @@ k_sddmm(const int4* __restrict__ units, int64_t num_units, const int32_t* __rest
         const T* __restrict__ x, const T* __restrict__ y, T* __restrict__ out, int F, int heads) {
   using N = Num<T>;
   using Raw = typename RawV<V * sizeof(T)>::type;
-  constexpr int EB = 4;
+  constexpr int EB = NCH >= 2 ? 4 : 8;
   const int lane = threadIdx.x & 31;
   const int tl = lane & (TEAM - 1);
   const unsigned tmask =
@@ -78,16 +78,23 @@ k_sddmm(const int4* __restrict__ units, int64_t num_units, const int32_t* __rest
     q[k] = c - hd[k] * lph;
     if (cval[k]) xr[k] = *reinterpret_cast<const Raw*>(x + (int64_t)row * F + c * V);
   }
-  for (int64_t base = beg; base < end; base += EB) {
-    int cj[EB];
+  // column ids of the next batch are fetched while the current batch computes
+  int cj[EB];
+#pragma unroll
+  for (int j = 0; j < EB; ++j) cj[j] = beg + j < end ? __ldg(cols + beg + j) : 0;
+  for (int base = beg; base < end; base += EB) {
+    int nj[EB];
+#pragma unroll
+    for (int j = 0; j < EB; ++j) {
+      const int e = base + EB + j;
+      nj[j] = e < end ? __ldg(cols + e) : 0;
+    }
     Raw yr[EB][NCH];
 #pragma unroll
     for (int j = 0; j < EB; ++j) {
-      const int64_t e = base + j;
-      cj[j] = e < end ? __ldg(cols + e) : 0;
 #pragma unroll
       for (int k = 0; k < NCH; ++k)
-        if (e < end && cval[k])
+        if (base + j < end && cval[k])
           yr[j][k] = __ldg(reinterpret_cast<const Raw*>(y + (int64_t)cj[j] * F + (tl + k * TEAM) * V));
     }
 #pragma unroll
@@ -119,6 +126,8 @@ k_sddmm(const int4* __restrict__ units, int64_t num_units, const int32_t* __rest
       for (int k = 0; k < NCH; ++k)
         if (cval[k] && q[k] == 0) out[e * heads + hd[k]] = part[k];
     }
+#pragma unroll
+    for (int j = 0; j < EB; ++j) cj[j] = nj[j];
   }
 }
 
@@ -452,6 +461,174 @@ extern "C" int hg_scale_f64(const void* x, double s, void* out, int64_t count, i
     k_scale_f64<__half><<<g, 256, 0, st>>>((const __half*)x, s, (__half*)out, count);
   else
     k_scale_f64<float><<<g, 256, 0, st>>>((const float*)x, s, (float*)out, count);
+  HG_LAUNCHED();
+  return HG_OK;
+}
+
+// ------------------------------------------------------------ cross entropy
+
+namespace hg {
+
+// Warp per row; lanes stride the class columns.  fp64 like the reference.
+__global__ void __launch_bounds__(256)
+k_softmax_xent(const float* __restrict__ logits, int64_t ld, const int64_t* __restrict__ labels,
+               int64_t n, int c_active, double denom, float* __restrict__ grad,
+               double* __restrict__ nll) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n;
+       r += nwarps) {
+    const float* z = logits + r * ld;
+    double m = -INFINITY;
+    for (int j = lane; j < c_active; j += 32) m = fmax(m, (double)z[j]);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    double se = 0.0;
+    for (int j = lane; j < c_active; j += 32) se += exp((double)z[j] - m);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+    const int64_t lab = labels[r];
+    float* g = grad + r * ld;
+    for (int j = lane; j < ld; j += 32) {
+      float v = 0.0f;
+      if (j < c_active) {
+        const double p = exp((double)z[j] - m) / se;
+        v = (float)((p - (j == lab ? 1.0 : 0.0)) / denom);
+      }
+      g[j] = v;
+    }
+    if (lane == 0) nll[r] = log(se) - ((double)z[lab] - m);
+  }
+}
+
+}  // namespace hg
+
+extern "C" int hg_softmax_xent(const float* logits, int64_t ld, const int64_t* labels, int64_t n,
+                               int32_t c_active, double denom, float* grad, double* nll,
+                               void* stream) {
+  HG_REQUIRE(c_active >= 1 && c_active <= ld, "hg_softmax_xent: bad class counts");
+  if (n == 0) return HG_OK;
+  k_softmax_xent<<<grid_for(n, 8, 148 * 64), 256, 0, as_stream(stream)>>>(
+      logits, ld, labels, n, c_active, denom, grad, nll);
+  HG_LAUNCHED();
+  return HG_OK;
+}
+
+// --------------------------------------------------- GAT projections, Adam
+
+namespace hg {
+
+// Team of fh/V lanes per (node, head); lane chunk of V elements of z, a_l, a_r.
+template <typename T, int V, int TEAM>
+__global__ void __launch_bounds__(256)
+k_head_dots(const T* __restrict__ z, const T* __restrict__ al, const T* __restrict__ ar,
+            int64_t n, int heads, int fh, T* __restrict__ sl, T* __restrict__ sr) {
+  using Raw = typename RawV<V * sizeof(T)>::type;
+  const int lane = threadIdx.x & 31;
+  const int tl = lane & (TEAM - 1);
+  const unsigned tmask =
+      TEAM == 32 ? 0xffffffffu : (((1u << TEAM) - 1u) << (lane & ~(TEAM - 1)));
+  const int64_t item = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TEAM;
+  if (item >= n * heads) return;
+  const int64_t node = item / heads;
+  const int h = (int)(item - node * heads);
+  const int nchunk = fh / V;
+  float pl = 0.0f, pr = 0.0f;
+  for (int c = tl; c < nchunk; c += TEAM) {
+    const int f = h * fh + c * V;
+    const Raw zr = *reinterpret_cast<const Raw*>(z + node * (int64_t)heads * fh + f);
+    const Raw lr_ = *reinterpret_cast<const Raw*>(al + f);
+    const Raw rr_ = *reinterpret_cast<const Raw*>(ar + f);
+    const T* za = reinterpret_cast<const T*>(&zr);
+    const T* la = reinterpret_cast<const T*>(&lr_);
+    const T* ra = reinterpret_cast<const T*>(&rr_);
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const float zf = Num<T>::to_f(za[i]);
+      pl = fmaf(zf, Num<T>::to_f(la[i]), pl);
+      pr = fmaf(zf, Num<T>::to_f(ra[i]), pr);
+    }
+  }
+#pragma unroll
+  for (int o = TEAM / 2; o >= 1; o >>= 1) {
+    pl += __shfl_xor_sync(tmask, pl, o, TEAM);
+    pr += __shfl_xor_sync(tmask, pr, o, TEAM);
+  }
+  if (tl == 0) {
+    sl[item] = Num<T>::from_f(pl);
+    sr[item] = Num<T>::from_f(pr);
+  }
+}
+
+template <typename G>
+__global__ void k_adam(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
+                       const G* __restrict__ grad, int64_t count, float lr, float omb1,
+                       float omb2, double b1, double b2, float eps,
+                       const double* __restrict__ step) {
+  const double t = *step;
+  const float c1 = (float)(1.0 - pow(b1, t)), c2 = (float)(1.0 - pow(b2, t));
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float g = Num<G>::to_f(grad[i]);
+    float mi = m[i], vi = v[i];
+    mi = __fadd_rn(mi, __fmul_rn(omb1, __fsub_rn(g, mi)));
+    vi = __fadd_rn(vi, __fmul_rn(omb2, __fsub_rn(__fmul_rn(g, g), vi)));
+    m[i] = mi;
+    v[i] = vi;
+    const float num = __fmul_rn(lr, __fdiv_rn(mi, c1));
+    const float den = __fadd_rn(__fsqrt_rn(__fdiv_rn(vi, c2)), eps);
+    p[i] = __fsub_rn(p[i], __fdiv_rn(num, den));
+  }
+}
+
+}  // namespace hg
+
+extern "C" int hg_head_dots(const void* z, const void* a_l, const void* a_r, int64_t n,
+                            int32_t heads, int32_t fh, void* s_l, void* s_r, int dtype,
+                            void* stream) {
+  HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
+  HG_REQUIRE(heads >= 1 && fh >= 1, "hg_head_dots: bad shape");
+  if (n == 0) return HG_OK;
+  cudaStream_t st = as_stream(stream);
+  const int64_t items = n * heads;
+  const bool aligned = (reinterpret_cast<uintptr_t>(z) | reinterpret_cast<uintptr_t>(a_l) |
+                        reinterpret_cast<uintptr_t>(a_r)) % 16 == 0;
+#define HG_HD(TT, VV, TM)                                                                   \
+  k_head_dots<TT, VV, TM><<<(unsigned)((items * TM + 255) / 256), 256, 0, st>>>(            \
+      (const TT*)z, (const TT*)a_l, (const TT*)a_r, n, heads, fh, (TT*)s_l, (TT*)s_r)
+  if (dtype == HG_F16) {
+    if (aligned && fh % 8 == 0) {
+      const int nc = fh / 8;
+      if (nc <= 1) HG_HD(__half, 8, 1);
+      else if (nc <= 2) HG_HD(__half, 8, 2);
+      else if (nc <= 4) HG_HD(__half, 8, 4);
+      else if (nc <= 8) HG_HD(__half, 8, 8);
+      else HG_HD(__half, 8, 16);
+    } else {
+      HG_HD(__half, 2, 8);
+    }
+  } else {
+    if (aligned && fh % 4 == 0) HG_HD(float, 4, 8);
+    else HG_HD(float, 1, 8);
+  }
+#undef HG_HD
+  HG_LAUNCHED();
+  return HG_OK;
+}
+
+extern "C" int hg_adam_step(float* master, float* m, float* v, const void* grad, int grad_dtype,
+                            int64_t count, float lr, float omb1, float omb2, double b1, double b2,
+                            float eps, const double* step, void* stream) {
+  HG_REQUIRE(grad_dtype == HG_F16 || grad_dtype == HG_F32, "unknown dtype %d", grad_dtype);
+  if (count == 0) return HG_OK;
+  cudaStream_t st = as_stream(stream);
+  const int g = grid_for(count, 256, 148 * 8);
+  if (grad_dtype == HG_F16)
+    k_adam<__half><<<g, 256, 0, st>>>(master, m, v, (const __half*)grad, count, lr, omb1, omb2,
+                                      b1, b2, eps, step);
+  else
+    k_adam<float><<<g, 256, 0, st>>>(master, m, v, (const float*)grad, count, lr, omb1, omb2,
+                                     b1, b2, eps, step);
   HG_LAUNCHED();
   return HG_OK;
 }

@@ -171,7 +171,7 @@ __device__ __forceinline__ void load_batch_ids(const int32_t* __restrict__ base_
 // Per-team state of k_spmm_fast: lane column offsets, accumulators, unit range.
 template <typename T, int V, int TEAM, int NCH, bool WEIGHTED>
 struct FastTeam {
-  static constexpr int EB = NCH >= 2 ? 4 : 8;             // edges gathered per batch
+  static constexpr int EB = NCH >= 4 ? 4 : 8;             // edges gathered per batch
   static constexpr int CPL = TEAM >= EB ? 1 : EB / TEAM;  // column ids per loading lane
   using Raw = typename RawVec<V * sizeof(T)>::type;
 

@@ -452,3 +452,37 @@ def scale_f64(x, s: float):
     nat.call("hg_scale_f64", _p(x), float(s), _p(out), x.numel(), _dtype_code(x), _stream())
     Probe.launches += 1
     return out
+
+
+def softmax_xent(logits, labels, c_active, denom):
+    """Fused fp64 softmax cross-entropy: returns (nll [N] f64, grad [N, ld] f32)."""
+    logits = logits.contiguous()
+    n, ld = logits.shape
+    grad = torch.empty_like(logits)
+    nll = torch.empty(n, dtype=torch.float64, device=logits.device)
+    nat.call("hg_softmax_xent", _p(logits), ld, _p(labels), n, c_active, float(denom), _p(grad),
+             _p(nll), _stream())
+    Probe.launches += 1
+    return nll, grad
+
+
+def head_dots(z, a_l, a_r, heads):
+    """s_l[n, h] = z[n, h, :] . a_l[h, :], s_r likewise (fp32 accumulate, one rounding)."""
+    z = z.contiguous()
+    n = z.shape[0]
+    fh = z.shape[1] // heads
+    s_l = torch.empty((n, heads), dtype=z.dtype, device=z.device)
+    s_r = torch.empty_like(s_l)
+    nat.call("hg_head_dots", _p(z), _p(a_l.contiguous()), _p(a_r.contiguous()), n, heads, fh,
+             _p(s_l), _p(s_r), _dtype_code(z), _stream())
+    Probe.launches += 1
+    return s_l, s_r
+
+
+def adam_step(master, m, v, grad, lr, b1, b2, eps, step):
+    """One fused Adam update over flat fp32 arrays (hg_adam_step); `step` is the
+    device fp64 step count (already incremented)."""
+    nat.call("hg_adam_step", _p(master), _p(m), _p(v), _p(grad), _dtype_code(grad),
+             master.numel(), float(lr), float(1 - b1), float(1 - b2), float(b1), float(b2),
+             float(eps), _p(step), _stream())
+    Probe.launches += 1

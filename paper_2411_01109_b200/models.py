@@ -392,7 +392,9 @@ def scale_combine(x, a, one_plus_eps, lam):
 
 
 class Param:
-    """fp32 master weight in HBM; publishes a compute-precision leaf each step."""
+    """fp32 master weight in HBM; publishes a compute-precision leaf each step.
+    Inside a ParamGroup the master and the published leaf are views of the
+    group's flat buffers, and publish() returns the persistent leaf."""
 
     def __init__(self, value, device="cuda", store_shape=None):
         v = torch.as_tensor(np.asarray(value, dtype=np.float32))
@@ -402,8 +404,11 @@ class Param:
             v = padded
         self.master = v.to(device)
         self.published = None
+        self.group = None
 
     def publish(self, mode):
+        if self.group is not None and self.group.mode == mode:
+            return self.published
         data = self.master if mode == "float32" else self.master.to(torch.float16)
         self.published = data.detach().requires_grad_(True)
         return self.published
@@ -412,6 +417,46 @@ class Param:
         if self.published is None or self.published.grad is None:
             return torch.zeros_like(self.master)
         return self.published.grad.to(torch.float32)
+
+
+class ParamGroup:
+    """All parameters of a model in flat buffers: fp32 masters, the published
+    compute-precision copy (persistent autograd leaves viewing it) and their
+    gradients.  A training step is one cast (publish), the backward pass
+    accumulating straight into the flat gradient, and one fused Adam kernel."""
+
+    def __init__(self, params, mode):
+        self.params = list(params)
+        self.mode = mode
+        dev = self.params[0].master.device
+        self.dtype = _DTYPES[mode]
+        sizes = [p.master.numel() for p in self.params]
+        total = sum(sizes)
+        self.master = torch.empty(total, dtype=torch.float32, device=dev)
+        self.pub = torch.empty(total, dtype=self.dtype, device=dev)
+        self.grad = torch.zeros(total, dtype=self.dtype, device=dev)
+        off = 0
+        for p, sz in zip(self.params, sizes):
+            shape = p.master.shape
+            self.master[off:off + sz].copy_(p.master.reshape(-1))
+            p.master = self.master[off:off + sz].view(shape)
+            leaf = self.pub[off:off + sz].view(shape)
+            leaf.requires_grad_(True)
+            leaf.grad = self.grad[off:off + sz].view(shape)
+            p.published = leaf
+            p.group = self
+            off += sz
+        self._ptrs = [p.published.grad.data_ptr() for p in self.params]
+
+    @torch.no_grad()
+    def publish(self):
+        self.pub.copy_(self.master)
+        self.grad.zero_()
+
+    def check_grads(self):
+        """True if autograd accumulated in place into the flat gradient."""
+        return all(p.published.grad is not None and p.published.grad.data_ptr() == q
+                   for p, q in zip(self.params, self._ptrs))
 
 
 def _glorot(rng, fan_in, fan_out, shape=None):
@@ -522,17 +567,40 @@ class GATLayer:
         z = matmul(x, self.w.publish(mode))                       # [N, H*so]
         zh = z.view(z.shape[0], h, so)
         a_l, a_r = self.a_l.publish(mode), self.a_r.publish(mode)
-        # s = z_h . a_h: one batched tensor-core GEMM per head pair [a_l | a_r],
-        # fp32 accumulation and one rounding (models.matmul semantics)
-        s = torch.matmul(zh.transpose(0, 1), torch.stack([a_l, a_r], dim=-1))  # [H, N, 2]
-        s_l = s[..., 0].t().contiguous()
-        s_r = s[..., 1].t().contiguous()
+        # s = z_h . a_h for every head (models.matmul semantics: fp32
+        # accumulation of exact products, one rounding), one kernel
+        s_l, s_r = _HeadDotsFn.apply(z, a_l, a_r, h)
         e = attention_logits(bundle, s_l, s_r, 0.2)               # [E, H]
         alpha = edge_softmax(bundle, e, overflow, tag + "/softmax")
         out = spmm_weighted(bundle, alpha if h > 1 else alpha[:, 0], z, width, overflow, tag)
         if self.reduce == "mean" and h > 1:
             return _HeadMeanFn.apply(out, h)
         return out
+
+
+class _HeadDotsFn(torch.autograd.Function):
+    """(s_l, s_r)[n, h] = z[n, h, :] . (a_l, a_r)[h, :] (hg_head_dots).
+    Backward: dz = rnd(g_l a_l) + rnd(g_r a_r) (each an exact product rounded
+    once, as the reference's N x 1 by 1 x F matmul gradient), da = z_h^T g."""
+
+    @staticmethod
+    def forward(ctx, z, a_l, a_r, heads):
+        ctx.heads = heads
+        ctx.save_for_backward(z, a_l, a_r)
+        return D.head_dots(z, a_l, a_r, heads)
+
+    @staticmethod
+    def backward(ctx, g_l, g_r):
+        z, a_l, a_r = ctx.saved_tensors
+        h = ctx.heads
+        n = z.shape[0]
+        g_l, g_r = g_l.contiguous(), g_r.contiguous()
+        gz = ((g_l.float()[:, :, None] * a_l.float()[None]).to(z.dtype)
+              + (g_r.float()[:, :, None] * a_r.float()[None]).to(z.dtype)).reshape(n, -1)
+        zt = z.view(n, h, -1).permute(1, 2, 0)                      # [H, F, N]
+        ga_l = torch.matmul(zt, g_l.t()[:, :, None])[..., 0]        # [H, F]
+        ga_r = torch.matmul(zt, g_r.t()[:, :, None])[..., 0]
+        return gz, ga_l, ga_r, None
 
 
 class _HeadMeanFn(torch.autograd.Function):
@@ -607,64 +675,83 @@ class Model:
 
 
 class _CrossEntropyFn(torch.autograd.Function):
+    """Forward and backward of the softmax cross-entropy in one fused fp64 pass
+    (hg_softmax_xent); the saved gradient is scaled by the upstream grad."""
+
     @staticmethod
-    def forward(ctx, logits, labels, n_active, denom):
-        z = logits[:, :n_active].double()
-        z = z - z.max(dim=1, keepdim=True).values
-        ez = torch.exp(z)
-        sumexp = ez.sum(dim=1)
-        p = ez / sumexp[:, None]
-        nll = torch.log(sumexp) - z.gather(1, labels[:, None])[:, 0]
-        ctx.save_for_backward(p, labels)
-        ctx.shape, ctx.denom = logits.shape, denom
+    def forward(ctx, logits, labels, n_active, denom, impl):
+        nll, grad = impl(logits, labels, n_active, denom)
+        ctx.save_for_backward(grad)
         return (nll.sum() / denom).float()
 
     @staticmethod
     def backward(ctx, g):
-        p, labels = ctx.saved_tensors
-        n = p.shape[0]
-        grad = p.clone()
-        grad[torch.arange(n, device=p.device), labels] -= 1.0
-        full = torch.zeros(ctx.shape, dtype=torch.float32, device=p.device)
-        full[:, : p.shape[1]] = (grad / ctx.denom * g.double()).float()
-        return full, None, None, None
+        (grad,) = ctx.saved_tensors
+        return grad * g, None, None, None, None
 
 
-def cross_entropy(logits, labels, n_active=None, denom=None):
+def cross_entropy(logits, labels, n_active=None, denom=None, impl=None):
     """Mean CE over all nodes on fp32 logits (models.py:552-572); columns at or
     beyond n_active (storage padding) take no part.  denom: the global node
     count when the rows are one partition of the graph."""
     if logits.dtype != torch.float32:
         raise ValueError("cross-entropy expects float32 logits")
     return _CrossEntropyFn.apply(logits, labels, n_active or logits.shape[1],
-                                 denom or logits.shape[0])
+                                 denom or logits.shape[0], impl or D.softmax_xent)
 
 
 class Adam:
     """models.Adam (models.py:575-592) on device fp32 masters.  The step count
-    lives on the device (fp64) so a step can be captured in a CUDA graph."""
+    lives on the device (fp64) so a step can be captured in a CUDA graph; with
+    a ParamGroup the update is one fused kernel over the flat buffers."""
 
-    def __init__(self, params, lr=1e-2, betas=(0.9, 0.999), eps=1e-8):
+    def __init__(self, params, lr=1e-2, betas=(0.9, 0.999), eps=1e-8, group=None):
         self.params = list(params)
         self.lr, self.betas, self.eps = lr, betas, eps
-        self.m = [torch.zeros_like(p.master) for p in self.params]
-        self.v = [torch.zeros_like(p.master) for p in self.params]
+        self.group = group
+        if group is not None:
+            self.m = torch.zeros_like(group.master)
+            self.v = torch.zeros_like(group.master)
+        else:
+            self.m = [torch.zeros_like(p.master) for p in self.params]
+            self.v = [torch.zeros_like(p.master) for p in self.params]
         dev = self.params[0].master.device if self.params else "cpu"
         self._t = torch.zeros((), dtype=torch.float64, device=dev)
         self.t = 0
 
     @torch.no_grad()
-    def step(self):
+    def step(self, flat_grad=None):
+        """flat_grad: optional gradient for the whole group (e.g. all-reduced fp32)."""
         self.t += 1
         b1, b2 = self.betas
         self._t.add_(1.0)
+        g = self.group
+        if g is not None and g.master.is_cuda and (flat_grad is not None or g.check_grads()):
+            grad = g.grad if flat_grad is None else flat_grad
+            D.adam_step(g.master, self.m, self.v, grad, self.lr, b1, b2, self.eps, self._t)
+            return
+        if flat_grad is not None:
+            for o, p in zip(_offsets(self.params), self.params):
+                p.published.grad = flat_grad[o:o + p.master.numel()].view(p.master.shape)
         c1 = (1.0 - torch.pow(b1, self._t)).float()
         c2 = (1.0 - torch.pow(b2, self._t)).float()
-        for p, m, v in zip(self.params, self.m, self.v):
-            g = p.grad32()
-            m.add_((1 - b1) * (g - m))
-            v.add_((1 - b2) * (g * g - v))
-            p.master.sub_(self.lr * (m / c1) / (torch.sqrt(v / c2) + self.eps))
+        ms = self.m if g is None else [self.m[o:o + p.master.numel()]
+                                       for o, p in zip(_offsets(self.params), self.params)]
+        vs = self.v if g is None else [self.v[o:o + p.master.numel()]
+                                       for o, p in zip(_offsets(self.params), self.params)]
+        for p, m, v in zip(self.params, ms, vs):
+            grad = p.grad32().reshape(m.shape)
+            m.add_((1 - b1) * (grad - m))
+            v.add_((1 - b2) * (grad * grad - v))
+            p.master.sub_((self.lr * (m / c1) / (torch.sqrt(v / c2) + self.eps)).view(p.master.shape))
+
+
+def _offsets(params):
+    out, o = [], 0
+    for p in params:
+        out.append(o)
+        o += p.master.numel()
+    return out
 
 
 @dataclass
@@ -737,7 +824,8 @@ class Trainer:
         red = Reduction(config.scaling, config.norm)
         self.model = Model(config.kind, rng, (fan_in, config.hidden, self.n_cls), red,
                            config.lam, config.heads, config.layers, dev, self.in_store)
-        self.opt = Adam(self.model.params(), lr=config.lr)
+        self.group = ParamGroup(self.model.params(), config.mode)
+        self.opt = Adam(self.model.params(), lr=config.lr, group=self.group)
         perm = rng.permutation(n)
         val = np.zeros(n, dtype=bool)
         val[perm[: int(n * config.val_fraction)]] = True
@@ -769,6 +857,7 @@ class Trainer:
 
     def _step_eager(self, overflow=None):
         cfg = self.cfg
+        self.group.publish()
         logits = self.model.forward(self.bundle, self.x, cfg.mode, cfg.width, overflow)
         if cfg.mode == "half":
             logits = convert(logits, "float32", self.conversions)

@@ -167,6 +167,10 @@ class CudaOps:
         return de
 
     @staticmethod
+    def xent(logits, labels, n_active, denom):
+        return D.softmax_xent(logits, labels, n_active, denom)
+
+    @staticmethod
     def edge_sums(view, v, perm):
         heads = v.shape[1] if v.dim() == 2 else 1
         out = torch.empty((view.n_rows, heads), dtype=v.dtype, device=v.device)
@@ -282,16 +286,20 @@ class DistTrainer:
 
         tr = self.inner
         cfg = tr.cfg
+        tr.group.publish()
         logits = tr.model.forward(self.bundle, tr.x, cfg.mode, cfg.width, overflow)
         if cfg.mode == "half":
             logits = convert(logits, "float32", tr.conversions)
-        loss = cross_entropy(logits, tr.labels, tr.n_cls, denom=self.n_total)
+        loss = cross_entropy(logits, tr.labels, tr.n_cls, denom=self.n_total,
+                             impl=self.bundle.ops.xent)
         loss.backward()
-        for p in tr.opt.params:
-            g = p.grad32()
-            self.dist.all_reduce(g)
-            p.published.grad = g
-        tr.opt.step()
+        if not tr.group.check_grads():
+            raise RuntimeError("autograd did not accumulate into the flat gradient buffer")
+        # data-parallel sum of the weight gradients: one fp32 all-reduce of the
+        # group's flat gradient buffer
+        flat = tr.group.grad.to(torch.float32)
+        self.dist.all_reduce(flat)
+        tr.opt.step(flat_grad=flat)
         total = loss.detach().clone()
         self.dist.all_reduce(total)
         return total, logits.detach()

@@ -48,6 +48,22 @@ class HostOps:
         return (s * fout.double()[:, None]).to(x.dtype)
 
 
+def _host_xent(logits, labels, n_active, denom):
+    z = logits[:, :n_active].double()
+    z = z - z.max(dim=1, keepdim=True).values
+    ez = torch.exp(z)
+    se = ez.sum(dim=1)
+    nll = torch.log(se) - z.gather(1, labels[:, None])[:, 0]
+    g = ez / se[:, None]
+    g[torch.arange(z.shape[0]), labels] -= 1.0
+    grad = torch.zeros_like(logits)
+    grad[:, :n_active] = (g / denom).float()
+    return nll, grad
+
+
+HostOps.xent = staticmethod(_host_xent)
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
