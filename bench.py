@@ -115,7 +115,8 @@ def load_traffic_profile(f_key):
 # ── CPU baseline (oracle restatement of the reference, row-panel sample) ──
 
 
-def cpu_baseline_gcn(offsets, cols, x16, labels, budget_edges, hidden=HIDDEN):
+def cpu_baseline_gcn(offsets, cols, x16, labels, budget_edges, kind="gcn", hidden=HIDDEN,
+                     heads=1, layers=2):
     """Time one reference GCN epoch (oracle.train_epochs) on the first rows of the
     graph holding ~budget_edges edges (all N vertices, all features), then
     extrapolate: t = dense + sparse * E / E_sample.  Returns (ms, sample text, cores)."""
@@ -132,8 +133,8 @@ def cpu_baseline_gcn(offsets, cols, x16, labels, budget_edges, hidden=HIDDEN):
     g = O.OracleGraph(n, rows, cols[:e_s].astype(np.int64))
     timer = O.Timer()
     t0 = time.perf_counter()
-    O.train_epochs(g, x16.astype(np.float32), labels, kind="gcn", mode="half", epochs=1,
-                   hidden=hidden, timer=timer)
+    O.train_epochs(g, x16.astype(np.float32), labels, kind=kind, mode="half", epochs=1,
+                   hidden=hidden, heads=heads, layers=layers, timer=timer)
     wall = time.perf_counter() - t0
     other = max(0.0, wall - timer.dense - timer.sparse)
     ms = (timer.dense + other + timer.sparse * e_total / max(e_s, 1)) * 1e3
@@ -156,22 +157,20 @@ def reference_arm(args, ws, rank):
 
     from paper_2411_01109_b200 import graphgen
 
-    have_gpu = torch.cuda.is_available()
-    dev = "cuda" if have_gpu else "cpu"
-    if have_gpu:
-        dg = graphgen.reddit_like(args.seed)
-        offsets = dg.offsets.cpu().numpy()
-        cols = dg.cols.cpu().numpy()
-        x, labels = graphgen.planted_features(dg.n, N_FEAT, N_CLASSES, args.seed, dev)
-        x16, lab = x.cpu().numpy(), labels.cpu().numpy()
-    else:
+    if not torch.cuda.is_available():
         raise SystemExit("reference arm needs the graph generator (GPU)")
+    dg, x, labels = build_workload(args.workload, args.seed)
+    offsets = dg.offsets.cpu().numpy()
+    cols = dg.cols.cpu().numpy()
+    x16, lab = x.cpu().numpy(), labels.cpu().numpy()
+    del dg
     steps = args.steps + args.warmup
     budget = max(50_000, int(args.ref_budget_edges * 10 / max(steps, 1)))
     vals = []
     sample = cores = None
     for i in range(steps):
-        ms, sample, cores = cpu_baseline_gcn(offsets, cols, x16, lab, budget)
+        ms, sample, cores = cpu_baseline_gcn(offsets, cols, x16, lab, budget,
+                                             **WORKLOADS[args.workload]["cfg"])
         if i >= args.warmup:
             vals.append(ms)
     v = statistics.median(vals) if vals else ms
@@ -179,7 +178,8 @@ def reference_arm(args, ws, rank):
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": v,
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "f16", "data": "synthetic",
-            "config": workload_config(int(offsets.size - 1), int(offsets[-1])),
+            "config": workload_config(int(offsets.size - 1), int(offsets[-1]),
+                                      name=args.workload),
             "cpu_baseline": {"value": v, "unit": "ms/epoch", "cores": cores, "kind": "port",
                              "sample": sample},
             "e2e": {"value": v, "unit": "ms/epoch", "h2d_bytes_per_step": 0,
@@ -187,12 +187,52 @@ def reference_arm(args, ws, rank):
     print(json.dumps(line), flush=True)
 
 
-def workload_config(n, e, parallelism="dp1"):
-    return {"workload": "GCN 2-layer train epoch, synthetic Reddit-shaped graph (C3)",
-            "nodes": n, "edges": e, "feat": N_FEAT, "hidden": HIDDEN, "classes": N_CLASSES,
-            "reduction": "discretized/both", "numerics": "fp32-guarded SpMM",
-            "l2": "inputs larger than L2 (column stream 459 MB, features 280 MB)",
-            "parallelism": parallelism}
+# BASELINE.json configs as bench workloads (C3 is the headline default).
+WORKLOADS = {
+    "gcn-reddit": dict(desc="GCN 2-layer train epoch, synthetic Reddit-shaped graph (C3)",
+                       graph="reddit_like", feat=602, classes=41,
+                       cfg=dict(kind="gcn", hidden=64),
+                       l2="inputs larger than L2 (column stream 459 MB, features 280 MB)"),
+    "gin-products": dict(desc="GIN 2-layer train epoch, synthetic ogbn-products-shaped "
+                              "power-law graph (C4)",
+                         graph="products_like", feat=100, classes=47,
+                         cfg=dict(kind="gin", hidden=64),
+                         l2="inputs larger than L2 (column stream 495 MB, features 490 MB)"),
+    "gat-rmat": dict(desc="GAT 2-layer 4-head train epoch, synthetic RMAT scale-24 graph (C5)",
+                     graph="rmat", feat=128, classes=16,
+                     cfg=dict(kind="gat", hidden=32, heads=4),
+                     l2="inputs larger than L2 (column stream ~1 GB, features 4.3 GB)"),
+    "gat-pubmed": dict(desc="GAT 3-layer 4-head train epoch, synthetic Pubmed-shaped graph (C2)",
+                       graph="pubmed_like", feat=500, classes=3,
+                       cfg=dict(kind="gat", hidden=16, heads=4, layers=3),
+                       l2="inputs fit in L2; flushed between timed epochs is not applied"),
+}
+
+
+def workload_config(n, e, parallelism="dp1", name="gcn-reddit"):
+    w = WORKLOADS[name]
+    c = w["cfg"]
+    return {"workload": w["desc"], "nodes": n, "edges": e, "feat": w["feat"],
+            "hidden": c["hidden"], "heads": c.get("heads", 1), "layers": c.get("layers", 2),
+            "classes": w["classes"], "reduction": "discretized/both",
+            "numerics": "fp32-guarded SpMM", "l2": w["l2"], "parallelism": parallelism}
+
+
+def build_workload(name, seed, device="cuda"):
+    """(DeviceGraph, features [N, F] fp16 on device, labels) of a workload."""
+    import torch
+
+    from paper_2411_01109_b200 import graphgen
+    from paper_2411_01109_b200.device import DeviceGraph
+
+    w = WORKLOADS[name]
+    if w["graph"] == "pubmed_like":
+        rows, cols, feats, labels = graphgen.pubmed_like(seed)
+        dg = DeviceGraph.from_edges(feats.shape[0], rows, cols, device=device)
+        return dg, torch.from_numpy(feats).to(device).half(), torch.from_numpy(labels).to(device)
+    dg = getattr(graphgen, w["graph"])(seed=seed, device=device)
+    x, labels = graphgen.planted_features(dg.n, w["feat"], w["classes"], seed, device)
+    return dg, x, labels
 
 
 # ── B200 arm ─────────────────────────────────────────────────────────────
@@ -288,10 +328,9 @@ def b200_arm(args, ws, rank, local):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     peak, peak_kind = peaks()
     t_setup = time.time()
-    dg = graphgen.reddit_like(args.seed)
-    x, labels = graphgen.planted_features(dg.n, N_FEAT, N_CLASSES, args.seed, "cuda")
-    cfg = TrainConfig(kind="gcn", mode="half", hidden=HIDDEN, seed=args.seed,
-                      scaling="discretized", norm="both", numerics="fast")
+    dg, x, labels = build_workload(args.workload, args.seed)
+    cfg = TrainConfig(mode="half", seed=args.seed, scaling="discretized", norm="both",
+                      numerics="fast", **WORKLOADS[args.workload]["cfg"])
     if ws > 1:
         from paper_2411_01109_b200.partition import DistTrainer
 
@@ -363,7 +402,7 @@ def b200_arm(args, ws, rank, local):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_ms, 4),
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "f16", "data": "synthetic (seeded Reddit-shaped graph, planted labels)",
-            "config": workload_config(dg.n, dg.num_edges, parallelism),
+            "config": workload_config(dg.n, dg.num_edges, parallelism, args.workload),
             "clocks": clocks.summary(),
             "e2e": {"value": round(e2e_ms, 4), "unit": "ms/epoch", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": 4},
@@ -377,15 +416,16 @@ def b200_arm(args, ws, rank, local):
             "final_loss": round(final_loss, 5),
             "setup_s": round(setup_s, 1),
         }
-    if not args.no_sweep and ws == 1:
+    if not args.no_sweep and ws == 1 and args.workload == "gcn-reddit":
         result["spmm_sweep_reddit"] = spmm_sweep(dg, peak)
-    if rank == 0 and ws == 1 and not args.no_small:
+    if rank == 0 and ws == 1 and not args.no_small and args.workload == "gcn-reddit":
         result["small_configs"] = small_configs(args, peak)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         offsets = dg.offsets.cpu().numpy()
         cols = dg.cols.cpu().numpy()
         ms, sample, cores = cpu_baseline_gcn(offsets, cols, x.cpu().numpy(),
-                                             labels.cpu().numpy(), args.cpu_budget_edges)
+                                             labels.cpu().numpy(), args.cpu_budget_edges,
+                                             **WORKLOADS[args.workload]["cfg"])
         result["cpu_baseline"] = {"value": round(ms, 1), "unit": "ms/epoch", "cores": cores,
                                   "kind": "port", "sample": sample}
     if rank == 0:
@@ -401,6 +441,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="gcn-reddit")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-small", action="store_true", help="skip the C1/C2 epoch timings")

@@ -157,6 +157,14 @@ class GraphBundle:
     def sddmm(self, x, y, heads=1):
         return D.sddmm(self.dg, x, y, heads=heads)
 
+    @staticmethod
+    def head_dots(z, a_l, a_r, heads):
+        return D.head_dots(z, a_l, a_r, heads)
+
+    @staticmethod
+    def scale(x, s):
+        return D.scale_f64(x, s)
+
     def attn_logits(self, s_l, s_r, slope):
         return D.attention_logits(self.dg, s_l, s_r, slope)
 
@@ -251,9 +259,9 @@ class _ScoresFn(torch.autograd.Function):
     def backward(ctx, g):
         (out,) = ctx.saved_tensors
         g = g.contiguous()
-        if ctx.slope is not None:
-            g = torch.where(out > 0, g, D.scale_f64(g, ctx.slope))
         b = ctx.bundle
+        if ctx.slope is not None:
+            g = torch.where(out > 0, g, b.scale(g, ctx.slope))
         gl = b.edge_sums(g, transpose=False) if ctx.needs_input_grad[0] else None
         gr = b.edge_sums(g, transpose=True) if ctx.needs_input_grad[1] else None
         return gl, gr, None, None
@@ -569,7 +577,7 @@ class GATLayer:
         a_l, a_r = self.a_l.publish(mode), self.a_r.publish(mode)
         # s = z_h . a_h for every head (models.matmul semantics: fp32
         # accumulation of exact products, one rounding), one kernel
-        s_l, s_r = _HeadDotsFn.apply(z, a_l, a_r, h)
+        s_l, s_r = _HeadDotsFn.apply(z, a_l, a_r, h, bundle)
         e = attention_logits(bundle, s_l, s_r, 0.2)               # [E, H]
         alpha = edge_softmax(bundle, e, overflow, tag + "/softmax")
         out = spmm_weighted(bundle, alpha if h > 1 else alpha[:, 0], z, width, overflow, tag)
@@ -584,10 +592,10 @@ class _HeadDotsFn(torch.autograd.Function):
     once, as the reference's N x 1 by 1 x F matmul gradient), da = z_h^T g."""
 
     @staticmethod
-    def forward(ctx, z, a_l, a_r, heads):
+    def forward(ctx, z, a_l, a_r, heads, bundle):
         ctx.heads = heads
         ctx.save_for_backward(z, a_l, a_r)
-        return D.head_dots(z, a_l, a_r, heads)
+        return bundle.head_dots(z, a_l, a_r, heads)
 
     @staticmethod
     def backward(ctx, g_l, g_r):
@@ -600,7 +608,7 @@ class _HeadDotsFn(torch.autograd.Function):
         zt = z.view(n, h, -1).permute(1, 2, 0)                      # [H, F, N]
         ga_l = torch.matmul(zt, g_l.t()[:, :, None])[..., 0]        # [H, F]
         ga_r = torch.matmul(zt, g_r.t()[:, :, None])[..., 0]
-        return gz, ga_l, ga_r, None
+        return gz, ga_l, ga_r, None, None
 
 
 class _HeadMeanFn(torch.autograd.Function):

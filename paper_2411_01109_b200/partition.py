@@ -171,6 +171,14 @@ class CudaOps:
         return D.softmax_xent(logits, labels, n_active, denom)
 
     @staticmethod
+    def head_dots(z, a_l, a_r, heads):
+        return D.head_dots(z, a_l, a_r, heads)
+
+    @staticmethod
+    def scale(x, s):
+        return D.scale_f64(x, s)
+
+    @staticmethod
     def edge_sums(view, v, perm):
         heads = v.shape[1] if v.dim() == 2 else 1
         out = torch.empty((view.n_rows, heads), dtype=v.dtype, device=v.device)
@@ -241,6 +249,12 @@ class DistBundle:
     def attn_logits(self, s_l, s_r, slope):
         return self.ops.attn(self.part.fwd, s_l.contiguous(),
                              self.ex.gather_rows(s_r.contiguous()), slope)
+
+    def head_dots(self, z, a_l, a_r, heads):
+        return self.ops.head_dots(z, a_l, a_r, heads)
+
+    def scale(self, x, s):
+        return self.ops.scale(x, s)
 
     def softmax_fwd(self, e):
         return self.ops.softmax_fwd(self.part.fwd, e.contiguous())

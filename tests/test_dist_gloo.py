@@ -61,7 +61,55 @@ def _host_xent(logits, labels, n_active, denom):
     return nll, grad
 
 
+def _rows_of(view):
+    deg = (view.offsets[1:] - view.offsets[:-1]).numpy()
+    return np.repeat(np.arange(view.n_rows), deg)
+
+
+def _host_sddmm(view, x_rows, y_cols, heads):
+    out = O.sddmm(_rows_of(view), view.cols.numpy().astype(np.int64), x_rows.numpy(),
+                  y_cols.numpy(), heads=heads)
+    return torch.from_numpy(np.ascontiguousarray(out.reshape(view.num_edges, heads)))
+
+
+def _host_attn(view, s_l, s_r, slope):
+    rows, cols = _rows_of(view), view.cols.numpy().astype(np.int64)
+    sl, sr = s_l.numpy(), s_r.numpy()
+    e = np.stack([O.attention_scores(rows, cols, sl[:, h], sr[:, h]) for h in range(sl.shape[1])], 1)
+    return torch.from_numpy(np.ascontiguousarray(O.leaky_relu(e, slope)))
+
+
+def _host_softmax_fwd(view, e):
+    return torch.from_numpy(O.edge_softmax_fwd(view.offsets.numpy(), e.numpy()))
+
+
+def _host_softmax_bwd(view, alpha, g):
+    return torch.from_numpy(O.edge_softmax_bwd(view.offsets.numpy(), alpha.numpy(), g.numpy()))
+
+
+def _host_edge_sums(view, v, perm):
+    v2 = v.reshape(v.shape[0], -1).double()
+    if perm is not None:
+        v2 = v2[perm.long()]
+    out = torch.zeros((view.n_rows, v2.shape[1]), dtype=torch.float64)
+    out.index_add_(0, torch.from_numpy(_rows_of(view)), v2[: view.num_edges])
+    return out.to(v.dtype)
+
+
+def _host_head_dots(z, a_l, a_r, heads):
+    zh = z.view(z.shape[0], heads, -1).double()
+    return ((zh * a_l.double()[None]).sum(-1).to(z.dtype),
+            (zh * a_r.double()[None]).sum(-1).to(z.dtype))
+
+
 HostOps.xent = staticmethod(_host_xent)
+HostOps.sddmm = staticmethod(_host_sddmm)
+HostOps.attn = staticmethod(_host_attn)
+HostOps.softmax_fwd = staticmethod(_host_softmax_fwd)
+HostOps.softmax_bwd = staticmethod(_host_softmax_bwd)
+HostOps.edge_sums = staticmethod(_host_edge_sums)
+HostOps.head_dots = staticmethod(_host_head_dots)
+HostOps.scale = staticmethod(lambda x, s: (x.double() * s).to(x.dtype))
 
 
 def _free_port():
@@ -106,7 +154,7 @@ class HostGraph:
         return torch.from_numpy(f)
 
 
-def _run(rank, world, port, out_q):
+def _run(rank, world, port, out_q, kind="gcn"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -115,7 +163,8 @@ def _run(rank, world, port, out_q):
 
         n, r, c, x, labels = _graph()
         g = HostGraph(n, r, c)
-        cfg = TrainConfig(kind="gcn", mode="float32", hidden=8, device="cpu", seed=1)
+        extra = {"heads": 2} if kind == "gat" else {}
+        cfg = TrainConfig(kind=kind, mode="float32", hidden=8, device="cpu", seed=1, **extra)
         tr = DistTrainer(g, torch.from_numpy(x), labels, cfg, dist, ops=HostOps)
         losses = []
         first = None
@@ -131,11 +180,11 @@ def _run(rank, world, port, out_q):
         dist.destroy_process_group()
 
 
-def _run_world(world):
+def _run_world(world, kind="gcn"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_run, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_run, args=(r, world, port, q, kind)) for r in range(world)]
     for p in procs:
         p.start()
     res = q.get(timeout=240)
@@ -146,9 +195,10 @@ def _run_world(world):
 
 
 @pytest.mark.timeout(400)
-def test_two_rank_gcn_step_matches_single_rank():
-    l1, parts1, w1 = _run_world(1)
-    l2, parts2, w2 = _run_world(2)
+@pytest.mark.parametrize("kind", ["gcn", "gat"])
+def test_two_rank_step_matches_single_rank(kind):
+    l1, parts1, w1 = _run_world(1, kind)
+    l2, parts2, w2 = _run_world(2, kind)
     n = _graph()[0]
     # nnz-balanced split points (bit-exact rule)
     offsets = O.csr_offsets(n, _graph()[1])

@@ -402,3 +402,27 @@ def test_run_epochs_host_feed_matches_steps(cuda):
     la = [float(a.step()[0]) for _ in range(5)]
     lb = b.run_epochs(b.host_features(feats), 5)
     assert la == lb
+
+
+def test_synthetic_generators_shapes(cuda):
+    """C3/C4/C5 generators (small instances): exact edge counts, canonical CSR,
+    symmetry for the products-shaped graph, determinism for a seed."""
+    from paper_2411_01109_b200 import graphgen
+
+    g = graphgen.reddit_like(0, n=5000, e=200_000)
+    assert g.n == 5000 and g.num_edges == 200_000
+    off = g.offsets.cpu().numpy()
+    cols = g.cols.cpu().numpy()
+    rows = np.repeat(np.arange(g.n), np.diff(off))
+    assert np.all(np.diff(rows * g.n + cols) > 0)  # sorted, unique
+    p = graphgen.products_like(1, n=20000, undirected=100_000)
+    pr = np.repeat(np.arange(p.n), np.diff(p.offsets.cpu().numpy()))
+    pc = p.cols.cpu().numpy()
+    fwd = set(zip(pr.tolist(), pc.tolist()))
+    assert all((c, r) in fwd for r, c in list(fwd)[:5000])
+    r1 = graphgen.rmat(scale=12, edge_factor=8, seed=3)
+    r2 = graphgen.rmat(scale=12, edge_factor=8, seed=3)
+    assert r1.n == 4096 and 0 < r1.num_edges <= 8 * 4096
+    assert torch.equal(r1.cols, r2.cols) and torch.equal(r1.offsets, r2.offsets)
+    deg = np.diff(r1.offsets.cpu().numpy())
+    assert deg.max() > 20 * max(1, int(np.median(deg)))  # power-law skew
