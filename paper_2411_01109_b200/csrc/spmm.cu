@@ -8,8 +8,6 @@
 //  * k_spmm_edge_ref   bit-exact replica of halfsparse's edge-parallel order
 //                      (kernels.py:328-391 / _ref_spmm_edge 603-688).
 //  * k_spmm_vertex_ref bit-exact replica of spmm_vertex_grouped (463-559).
-#include <cstdlib>
-
 #include "hg_common.cuh"
 
 namespace hg {
@@ -306,124 +304,6 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
   }
 }
 
-// ----------------------------------------------- async-pipelined fast kernel
-//
-// Unweighted binary16 SpMM, one 16-byte chunk per lane per edge.  Gathers go
-// global -> shared with cp.async.cg (L1 bypass) into a per-lane ring of
-// DEPTH batches x EB edges laid out [stage][edge][thread] (conflict-free
-// 16-byte lanes), so (DEPTH-1)*EB gathers per lane stay in flight without
-// holding registers.  Edges outside the unit are zero-filled (src-size 0),
-// which is exact for the fp32 sums (acc starts at +0 and +0 is neutral), so
-// the consume loop has no predicates.
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
-               "r"(src_bytes));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-template <int TEAM, int DEPTH, int EB, int BLOCK>
-struct AsyncTeam {
-  static constexpr int CPL = TEAM >= EB ? 1 : EB / TEAM;
-  uint4* ring;
-  const __half* x;
-  const __half* xl;
-  unsigned tmask;
-  int beg, end, F, base0;
-  bool cval;
-
-  __device__ __forceinline__ void issue(int k, const int (&id)[CPL]) {
-    const int b = base0 + k * EB;
-    uint4* stage = ring + (size_t)(k % DEPTH) * EB * BLOCK + threadIdx.x;
-#pragma unroll
-    for (int j = 0; j < EB; ++j) {
-      const int c = __shfl_sync(tmask, id[j % CPL], j / CPL, TEAM);
-      const bool ok = cval && (b + j >= beg) && (b + j < end);
-      const __half* src = ok ? xl + (size_t)(unsigned)c * (unsigned)F : x;
-      cp_async16(stage + (size_t)j * BLOCK, src, ok ? 16 : 0);
-    }
-  }
-};
-
-template <int TEAM, int DEPTH, int EB, int BLOCK>
-__global__ void __launch_bounds__(BLOCK)
-k_spmm_async(const int4* __restrict__ units, int64_t num_units, const int32_t* __restrict__ cols,
-             int64_t num_edges, const __half* __restrict__ x, __half* __restrict__ y,
-             float* __restrict__ carry, int F, int fmode, const __half* __restrict__ fout) {
-  constexpr int V = 8;
-  using Team = AsyncTeam<TEAM, DEPTH, EB, BLOCK>;
-  constexpr int CPL = Team::CPL;
-  extern __shared__ __align__(16) uint4 ring_mem[];  // [DEPTH][EB][BLOCK]
-
-  const int lane = threadIdx.x & 31;
-  const int tl = lane & (TEAM - 1);
-  const int64_t team_id = ((int64_t)blockIdx.x * BLOCK + threadIdx.x) / TEAM;
-  if (team_id >= num_units) return;
-  const int4 un = units[team_id];
-  const int row = un.x, slot = un.w;
-  const int limit = (int)num_edges;
-  const bool loader = tl * CPL < EB;
-
-  Team t;
-  t.ring = ring_mem;
-  t.x = x;
-  t.xl = x + tl * V;
-  t.tmask = TEAM == 32 ? 0xffffffffu : (((1u << TEAM) - 1u) << (lane & ~(TEAM - 1)));
-  t.beg = un.y;
-  t.end = un.z;
-  t.F = F;
-  t.cval = tl < F / V;
-  const int mis = (int)((reinterpret_cast<uintptr_t>(cols) >> 2) & (EB - 1));
-  t.base0 = t.beg - ((t.beg + mis) & (EB - 1));
-  const int nb = (t.end - t.base0 + EB - 1) / EB;   // batches of this unit
-
-  float acc[V];
-#pragma unroll
-  for (int i = 0; i < V; ++i) acc[i] = 0.0f;
-
-  int ids[CPL] = {};  // column ids of the next batch to issue
-  if (nb > 0 && loader) load_idx<CPL>(cols, t.base0 + tl * CPL, limit, ids);
-
-#pragma unroll
-  for (int k = 0; k < DEPTH - 1; ++k) {  // prologue: DEPTH-1 batches in flight
-    if (k < nb) {
-      int nids[CPL] = {};
-      if (k + 1 < nb && loader) load_idx<CPL>(cols, t.base0 + (k + 1) * EB + tl * CPL, limit, nids);
-      t.issue(k, ids);
-#pragma unroll
-      for (int q = 0; q < CPL; ++q) ids[q] = nids[q];
-    }
-    cp_async_commit();
-  }
-  for (int k = 0; k < nb; ++k) {
-    const int kn = k + DEPTH - 1;
-    if (kn < nb) {
-      int nids[CPL] = {};
-      if (kn + 1 < nb && loader) load_idx<CPL>(cols, t.base0 + (kn + 1) * EB + tl * CPL, limit, nids);
-      t.issue(kn, ids);
-#pragma unroll
-      for (int q = 0; q < CPL; ++q) ids[q] = nids[q];
-    }
-    cp_async_commit();
-    cp_async_wait<DEPTH - 1>();
-    const uint4* stage = ring_mem + (size_t)(k % DEPTH) * EB * BLOCK + threadIdx.x;
-#pragma unroll
-    for (int j = 0; j < EB; ++j) acc_add<__half, V>(acc, stage[(size_t)j * BLOCK]);
-  }
-  cp_async_wait<0>();
-
-  if (!t.cval) return;
-  if (slot < 0) {
-    const __half fo = fout ? fout[row] : Num<__half>::zero();
-    store_out<__half, V>(y + (int64_t)row * F + tl * V, acc, fmode, fo);
-  } else {
-    store_carry<V>(carry + (int64_t)slot * F + tl * V, acc);
-  }
-}
-
 // One team per split row: fp32 carries folded in slot (edge) order.
 template <typename T, int V, int TEAM, int NCH>
 __global__ void __launch_bounds__(256)
@@ -517,77 +397,12 @@ static int dispatch_layout(const FastArgs& a) {
   HG_REQUIRE(false, "hg_spmm: feature length %d too large", a.F);
 }
 
-template <int TEAM, int DEPTH, int BLOCK>
-static int launch_async_cfg(const FastArgs& a) {
-  constexpr int EB = 8;
-  constexpr size_t smem = (size_t)DEPTH * EB * BLOCK * 16;
-  constexpr int teams_per_block = BLOCK / TEAM;
-  if (a.num_units > 0) {
-    auto kfn = k_spmm_async<TEAM, DEPTH, EB, BLOCK>;
-    HG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int64_t blocks = (a.num_units + teams_per_block - 1) / teams_per_block;
-    kfn<<<(unsigned)blocks, BLOCK, smem, a.st>>>(a.units, a.num_units, a.cols, a.num_edges,
-                                                 (const __half*)a.x, (__half*)a.y, a.carry, a.F,
-                                                 a.fmode, (const __half*)a.fout);
-    HG_LAUNCHED();
-  }
-  if (a.num_split > 0) {
-    constexpr int tpb = 256 / TEAM;
-    const int64_t blocks = (a.num_split + tpb - 1) / tpb;
-    k_spmm_fast_followup<__half, 8, TEAM, 1><<<(unsigned)blocks, 256, 0, a.st>>>(
-        a.split_rows, a.num_split, a.carry, (__half*)a.y, a.F, a.fmode, (const __half*)a.fout);
-    HG_LAUNCHED();
-  }
-  return HG_OK;
-}
-
-// Ring geometry (DEPTH x BLOCK); HG_SPMM_ASYNC_CFG selects alternatives for A/B runs.
-static int async_cfg() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("HG_SPMM_ASYNC_CFG");
-    v = e ? atoi(e) : 0;
-  }
-  return v;
-}
-
-template <int TEAM>
-static int launch_async(const FastArgs& a) {
-  switch (async_cfg()) {
-    case 1: return launch_async_cfg<TEAM, 3, 128>(a);
-    case 2: return launch_async_cfg<TEAM, 6, 64>(a);
-    case 3: return launch_async_cfg<TEAM, 8, 64>(a);
-    case 4: return launch_async_cfg<TEAM, 4, 64>(a);
-    default: return launch_async_cfg<TEAM, 4, 128>(a);
-  }
-}
-
-// HG_SPMM_ASYNC=0 in the environment selects the register-pipelined kernel
-// (kept for A/B measurements).
-static bool async_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("HG_SPMM_ASYNC");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
-}
-
 template <typename T>
 static int dispatch_fast(const FastArgs& a) {
   constexpr int VB = 16 / sizeof(T);
   const bool aligned = (reinterpret_cast<uintptr_t>(a.x) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(a.y) % 16 == 0);
   const bool big = aligned && (a.fh % VB == 0);
-  if constexpr (sizeof(T) == 2) {
-    const int nvec = a.F / VB;
-    if (big && !a.w && nvec >= 3 && nvec <= 32 && async_enabled()) {
-      if (nvec <= 4) return launch_async<4>(a);
-      if (nvec <= 8) return launch_async<8>(a);
-      if (nvec <= 16) return launch_async<16>(a);
-      return launch_async<32>(a);
-    }
-  }
   if (a.w) return big ? dispatch_layout<T, VB, true>(a) : dispatch_layout<T, 2, true>(a);
   return big ? dispatch_layout<T, VB, false>(a) : dispatch_layout<T, 2, false>(a);
 }
