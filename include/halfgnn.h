@@ -159,15 +159,21 @@ int hg_attn_scores(const int64_t* offsets, const int32_t* cols, int64_t n_rows,
                    int64_t num_edges, const void* s_l, const void* s_r, int32_t heads,
                    double slope, void* out, int dtype, void* stream);
 
+/* Rows longer than long_thresh (listed in long_rows, n_long of them; pass
+ * n_long = 0 to disable) are processed by one 1024-thread CTA each, with the
+ * identical reduction tree, so power-law hubs do not serialise on one warp. */
+
 /* edge_softmax forward (models.py:382-402): per row and head, m = max,
  * s = rnd(e-m), ex = rnd(exp(s)), den = adjacent-pair tree of ex in CSR order,
  * alpha = rnd(ex/den).  Bit-exact. */
 int hg_edge_softmax_fwd(const int64_t* offsets, int64_t n_rows, int64_t num_edges,
-                        const void* e, void* alpha, int32_t heads, int dtype, void* stream);
+                        const void* e, void* alpha, int32_t heads, const int32_t* long_rows,
+                        int64_t n_long, int64_t long_thresh, int dtype, void* stream);
 /* edge_softmax backward (models.py:403-410): prod = rnd(alpha*g),
  * s = tree-sum(prod), de = rnd(alpha*rnd(g - s)).  Bit-exact. */
 int hg_edge_softmax_bwd(const int64_t* offsets, int64_t n_rows, int64_t num_edges,
                         const void* alpha, const void* grad, void* de, int32_t heads,
+                        const int32_t* long_rows, int64_t n_long, int64_t long_thresh,
                         int dtype, void* stream);
 
 /* Row sums of per-edge values (attention_scores backward, models.py:329-337),
@@ -175,7 +181,8 @@ int hg_edge_softmax_bwd(const int64_t* offsets, int64_t n_rows, int64_t num_edge
  * idx(e) = perm ? perm[e] : e (perm turns a CSC walk into column sums). */
 int hg_edge_rowsum(const int64_t* offsets, int64_t n_rows, int64_t num_edges,
                    const void* vals, const int32_t* perm, int32_t heads, void* out,
-                   int dtype, void* stream);
+                   const int32_t* long_rows, int64_t n_long, int64_t long_thresh, int dtype,
+                   void* stream);
 
 /* ------------------------------------------------------------------- loss */
 
@@ -191,6 +198,15 @@ int hg_softmax_xent(const float* logits, int64_t ld, const int64_t* labels, int6
  * accumulation of exact products, one rounding), same for s_r. */
 int hg_head_dots(const void* z, const void* a_l, const void* a_r, int64_t n, int32_t heads,
                  int32_t fh, void* s_l, void* s_r, int dtype, void* stream);
+/* Its backward (the N x 1 by 1 x F matmul gradients of models.py:151-155):
+ * gz[n, h*fh+f] = rnd(rnd(g_l[n,h] a_l[h,f]) + rnd(g_r[n,h] a_r[h,f])) and
+ * ga_{l,r}[h, f] = rnd(sum_n z[n, h*fh+f] g_{l,r}[n, h]) with a deterministic
+ * two-pass fp32 reduction (workspace: hg_head_dots_bwd_workspace). */
+int hg_head_dots_bwd_workspace(int32_t heads, int32_t fh, size_t* bytes);
+int hg_head_dots_bwd(const void* z, const void* a_l, const void* a_r, const void* g_l,
+                     const void* g_r, int64_t n, int32_t heads, int32_t fh, void* gz,
+                     void* ga_l, void* ga_r, int dtype, void* ws, size_t ws_bytes,
+                     void* stream);
 
 /* models.Adam step (models.py:583-592) over flat fp32 arrays, the reference's
  * operation order with one fp32 rounding per op:

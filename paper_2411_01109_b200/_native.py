@@ -47,12 +47,15 @@ SIGNATURES = {
                            _P, c_size_t, _P],
     "hg_sddmm": [_P, _P, _I64, _I64, _P, _I64, _P, _P, _P, _I32, _I32, c_int, _P],
     "hg_attn_scores": [_P, _P, _I64, _I64, _P, _P, _I32, c_double, _P, c_int, _P],
-    "hg_edge_softmax_fwd": [_P, _I64, _I64, _P, _P, _I32, c_int, _P],
-    "hg_edge_softmax_bwd": [_P, _I64, _I64, _P, _P, _P, _I32, c_int, _P],
-    "hg_edge_rowsum": [_P, _I64, _I64, _P, _P, _I32, _P, c_int, _P],
+    "hg_edge_softmax_fwd": [_P, _I64, _I64, _P, _P, _I32, _P, _I64, _I64, c_int, _P],
+    "hg_edge_softmax_bwd": [_P, _I64, _I64, _P, _P, _P, _I32, _P, _I64, _I64, c_int, _P],
+    "hg_edge_rowsum": [_P, _I64, _I64, _P, _P, _I32, _P, _P, _I64, _I64, c_int, _P],
     "hg_scale_f64": [_P, c_double, _P, _I64, c_int, _P],
     "hg_softmax_xent": [_P, _I64, _P, _I64, _I32, c_double, _P, _P, _P],
     "hg_head_dots": [_P, _P, _P, _I64, _I32, _I32, _P, _P, c_int, _P],
+    "hg_head_dots_bwd_workspace": [_I32, _I32, _PSZ],
+    "hg_head_dots_bwd": [_P, _P, _P, _P, _P, _I64, _I32, _I32, _P, _P, _P, c_int, _P, c_size_t,
+                         _P],
     "hg_adam_step": [_P, _P, _P, _P, c_int, _I64, c_float, c_float, c_float, c_double, c_double,
                      c_float, _P, _P],
 }

@@ -247,6 +247,19 @@ struct RowTree {
     stk[lvl] = cur;
     ++blocks;
   }
+  // Push the root of the next aligned block (computed elsewhere).
+  __device__ __forceinline__ void push_root(T cur) {
+    using N = Num<T>;
+    int64_t t = blocks;
+    int lvl = 0;
+    while (t & 1) {
+      cur = N::add(stk[lvl], cur);
+      t >>= 1;
+      ++lvl;
+    }
+    stk[lvl] = cur;
+    ++blocks;
+  }
   __device__ __forceinline__ T root() const {
     using N = Num<T>;
     T acc = N::zero();
@@ -276,14 +289,14 @@ __device__ __forceinline__ float warp_max(float v) {
 template <typename T>
 __global__ void __launch_bounds__(256)
 k_softmax_fwd(const int64_t* __restrict__ offsets, int64_t n_rows, const T* __restrict__ e,
-              T* __restrict__ alpha, int heads) {
+              T* __restrict__ alpha, int heads, int64_t long_thresh) {
   using N = Num<T>;
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows;
        r += nwarps) {
     const int64_t beg = offsets[r], len = offsets[r + 1] - beg;
-    if (len == 0) continue;
+    if (len == 0 || len > long_thresh) continue;
     for (int h = 0; h < heads; ++h) {
       float m = -INFINITY;
       bool nan = false;
@@ -318,14 +331,14 @@ k_softmax_fwd(const int64_t* __restrict__ offsets, int64_t n_rows, const T* __re
 template <typename T>
 __global__ void __launch_bounds__(256)
 k_softmax_bwd(const int64_t* __restrict__ offsets, int64_t n_rows, const T* __restrict__ alpha,
-              const T* __restrict__ g, T* __restrict__ de, int heads) {
+              const T* __restrict__ g, T* __restrict__ de, int heads, int64_t long_thresh) {
   using N = Num<T>;
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows;
        r += nwarps) {
     const int64_t beg = offsets[r], len = offsets[r + 1] - beg;
-    if (len == 0) continue;
+    if (len == 0 || len > long_thresh) continue;
     for (int h = 0; h < heads; ++h) {
       RowTree<T> tree;
       for (int64_t b = 0; b < len; b += 32) {
@@ -349,13 +362,15 @@ k_softmax_bwd(const int64_t* __restrict__ offsets, int64_t n_rows, const T* __re
 template <typename T>
 __global__ void __launch_bounds__(256)
 k_edge_rowsum(const int64_t* __restrict__ offsets, int64_t n_rows, const T* __restrict__ v,
-              const int32_t* __restrict__ perm, int heads, T* __restrict__ out) {
+              const int32_t* __restrict__ perm, int heads, T* __restrict__ out,
+              int64_t long_thresh) {
   using N = Num<T>;
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows;
        r += nwarps) {
     const int64_t beg = offsets[r], end = offsets[r + 1];
+    if (end - beg > long_thresh) continue;
     for (int h = 0; h < heads; ++h) {
       float s = 0.0f;
       for (int64_t i = beg + lane; i < end; i += 32) {
@@ -366,6 +381,157 @@ k_edge_rowsum(const int64_t* __restrict__ offsets, int64_t n_rows, const T* __re
       for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       if (lane == 0) out[r * heads + h] = N::from_f(s);
     }
+  }
+}
+
+// ------------------------------------------------ long rows: one CTA per row
+// 1024 threads cover a 1024-element superblock per step: each warp reduces its
+// aligned 32-element block (predicated shuffles), warp 0 reduces the 32 block
+// roots the same way, and thread 0 pushes the superblock root onto the
+// binary-counter stack -- the same implicit aligned tree as the warp path.
+
+template <typename T>
+__device__ __forceinline__ T superblock_root(T v, int64_t sb, int64_t len, T* roots) {
+  using N = Num<T>;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t base = sb + (int64_t)warp * 32;
+#pragma unroll
+  for (int s = 1; s < 32; s <<= 1) {
+    const T o = shfl_down_t(0xffffffffu, v, s, 32);
+    if ((lane & (2 * s - 1)) == 0 && base + lane + s < len) v = N::add(v, o);
+  }
+  if (lane == 0) roots[warp] = v;
+  __syncthreads();
+  T r = N::zero();
+  if (warp == 0) {
+    r = roots[lane];
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+      const T o = shfl_down_t(0xffffffffu, r, s, 32);
+      if ((lane & (2 * s - 1)) == 0 && sb + 32 * (int64_t)(lane + s) < len) r = N::add(r, o);
+    }
+  }
+  __syncthreads();
+  return r;  // valid in thread 0
+}
+
+__device__ __forceinline__ float block_max(float v, float* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_max(v);
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    v = warp_max(red[lane]);
+    if (lane == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float r = red[0];
+  __syncthreads();
+  return r;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(1024)
+k_softmax_fwd_long(const int64_t* __restrict__ offsets, const int32_t* __restrict__ rows,
+                   const T* __restrict__ e, T* __restrict__ alpha, int heads) {
+  using N = Num<T>;
+  __shared__ T roots[32];
+  __shared__ float red[32];
+  __shared__ double den_s;
+  const int64_t r = rows[blockIdx.x];
+  const int64_t beg = offsets[r], len = offsets[r + 1] - beg;
+  for (int h = 0; h < heads; ++h) {
+    float m = -INFINITY, nanf_ = 0.0f;
+    for (int64_t i = threadIdx.x; i < len; i += 1024) {
+      const float v = N::to_f(e[(beg + i) * heads + h]);
+      if (v != v) nanf_ = 1.0f;
+      m = fmaxf(m, v);
+    }
+    m = block_max(m, red);
+    const bool nan = block_max(nanf_, red) > 0.0f;
+    const T mt = nan ? N::from_f(NAN) : N::from_f(m);
+    RowTree<T> tree;
+    for (int64_t sb = 0; sb < len; sb += 1024) {
+      const int64_t i = sb + threadIdx.x;
+      T ex = N::zero();
+      if (i < len) {
+        const T sv = N::sub(e[(beg + i) * heads + h], mt);
+        ex = N::from_d(exp(N::to_d(sv)));
+        alpha[(beg + i) * heads + h] = ex;
+      }
+      const T rt = superblock_root(ex, sb, len, roots);
+      if (threadIdx.x == 0) tree.push_root(rt);
+    }
+    if (threadIdx.x == 0) den_s = N::to_d(tree.root());
+    __syncthreads();
+    const double den = den_s;
+    for (int64_t i = threadIdx.x; i < len; i += 1024) {
+      const int64_t k = (beg + i) * heads + h;
+      alpha[k] = N::from_d(N::to_d(alpha[k]) / den);
+    }
+    __syncthreads();
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(1024)
+k_softmax_bwd_long(const int64_t* __restrict__ offsets, const int32_t* __restrict__ rows,
+                   const T* __restrict__ alpha, const T* __restrict__ g, T* __restrict__ de,
+                   int heads) {
+  using N = Num<T>;
+  __shared__ T roots[32];
+  __shared__ T s_s;
+  const int64_t r = rows[blockIdx.x];
+  const int64_t beg = offsets[r], len = offsets[r + 1] - beg;
+  for (int h = 0; h < heads; ++h) {
+    RowTree<T> tree;
+    for (int64_t sb = 0; sb < len; sb += 1024) {
+      const int64_t i = sb + threadIdx.x;
+      T p = N::zero();
+      if (i < len) {
+        const int64_t k = (beg + i) * heads + h;
+        p = N::mul(alpha[k], g[k]);
+      }
+      const T rt = superblock_root(p, sb, len, roots);
+      if (threadIdx.x == 0) tree.push_root(rt);
+    }
+    if (threadIdx.x == 0) s_s = tree.root();
+    __syncthreads();
+    const T sv = s_s;
+    for (int64_t i = threadIdx.x; i < len; i += 1024) {
+      const int64_t k = (beg + i) * heads + h;
+      de[k] = N::mul(alpha[k], N::sub(g[k], sv));
+    }
+    __syncthreads();
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(1024)
+k_edge_rowsum_long(const int64_t* __restrict__ offsets, const int32_t* __restrict__ rows,
+                   const T* __restrict__ v, const int32_t* __restrict__ perm, int heads,
+                   T* __restrict__ out) {
+  __shared__ float red[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r = rows[blockIdx.x];
+  const int64_t beg = offsets[r], end = offsets[r + 1];
+  for (int h = 0; h < heads; ++h) {
+    float s = 0.0f;
+    for (int64_t i = beg + threadIdx.x; i < end; i += 1024) {
+      const int64_t idx = perm ? (int64_t)perm[i] : i;
+      s += Num<T>::to_f(v[idx * heads + h]);
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) red[warp] = s;
+    __syncthreads();
+    if (warp == 0) {
+      s = red[lane];
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) out[r * heads + h] = Num<T>::from_f(s);
+    }
+    __syncthreads();
   }
 }
 
@@ -397,56 +563,88 @@ extern "C" int hg_attn_scores(const int64_t* offsets, const int32_t* cols, int64
 }
 
 extern "C" int hg_edge_softmax_fwd(const int64_t* offsets, int64_t n_rows, int64_t num_edges,
-                                   const void* e, void* alpha, int32_t heads, int dtype,
-                                   void* stream) {
+                                   const void* e, void* alpha, int32_t heads,
+                                   const int32_t* long_rows, int64_t n_long, int64_t long_thresh,
+                                   int dtype, void* stream) {
   (void)num_edges;
   HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
   HG_REQUIRE(heads >= 1, "heads must be positive");
+  HG_REQUIRE(n_long == 0 || long_rows, "long rows listed without an index array");
   if (n_rows == 0) return HG_OK;
+  if (n_long == 0) long_thresh = INT64_MAX;
   cudaStream_t st = as_stream(stream);
   const int g = grid_for(n_rows, 8, 148 * 64);
-  if (dtype == HG_F16)
-    k_softmax_fwd<__half><<<g, 256, 0, st>>>(offsets, n_rows, (const __half*)e, (__half*)alpha, heads);
-  else
-    k_softmax_fwd<float><<<g, 256, 0, st>>>(offsets, n_rows, (const float*)e, (float*)alpha, heads);
+  if (dtype == HG_F16) {
+    k_softmax_fwd<__half><<<g, 256, 0, st>>>(offsets, n_rows, (const __half*)e, (__half*)alpha,
+                                             heads, long_thresh);
+    if (n_long)
+      k_softmax_fwd_long<__half><<<(unsigned)n_long, 1024, 0, st>>>(
+          offsets, long_rows, (const __half*)e, (__half*)alpha, heads);
+  } else {
+    k_softmax_fwd<float><<<g, 256, 0, st>>>(offsets, n_rows, (const float*)e, (float*)alpha,
+                                            heads, long_thresh);
+    if (n_long)
+      k_softmax_fwd_long<float><<<(unsigned)n_long, 1024, 0, st>>>(
+          offsets, long_rows, (const float*)e, (float*)alpha, heads);
+  }
   HG_LAUNCHED();
   return HG_OK;
 }
 
 extern "C" int hg_edge_softmax_bwd(const int64_t* offsets, int64_t n_rows, int64_t num_edges,
                                    const void* alpha, const void* grad, void* de, int32_t heads,
+                                   const int32_t* long_rows, int64_t n_long, int64_t long_thresh,
                                    int dtype, void* stream) {
   (void)num_edges;
   HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
   HG_REQUIRE(heads >= 1, "heads must be positive");
+  HG_REQUIRE(n_long == 0 || long_rows, "long rows listed without an index array");
   if (n_rows == 0) return HG_OK;
+  if (n_long == 0) long_thresh = INT64_MAX;
   cudaStream_t st = as_stream(stream);
   const int g = grid_for(n_rows, 8, 148 * 64);
-  if (dtype == HG_F16)
+  if (dtype == HG_F16) {
     k_softmax_bwd<__half><<<g, 256, 0, st>>>(offsets, n_rows, (const __half*)alpha,
-                                             (const __half*)grad, (__half*)de, heads);
-  else
+                                             (const __half*)grad, (__half*)de, heads, long_thresh);
+    if (n_long)
+      k_softmax_bwd_long<__half><<<(unsigned)n_long, 1024, 0, st>>>(
+          offsets, long_rows, (const __half*)alpha, (const __half*)grad, (__half*)de, heads);
+  } else {
     k_softmax_bwd<float><<<g, 256, 0, st>>>(offsets, n_rows, (const float*)alpha,
-                                            (const float*)grad, (float*)de, heads);
+                                            (const float*)grad, (float*)de, heads, long_thresh);
+    if (n_long)
+      k_softmax_bwd_long<float><<<(unsigned)n_long, 1024, 0, st>>>(
+          offsets, long_rows, (const float*)alpha, (const float*)grad, (float*)de, heads);
+  }
   HG_LAUNCHED();
   return HG_OK;
 }
 
 extern "C" int hg_edge_rowsum(const int64_t* offsets, int64_t n_rows, int64_t num_edges,
                               const void* vals, const int32_t* perm, int32_t heads, void* out,
+                              const int32_t* long_rows, int64_t n_long, int64_t long_thresh,
                               int dtype, void* stream) {
   (void)num_edges;
   HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
   HG_REQUIRE(heads >= 1, "heads must be positive");
+  HG_REQUIRE(n_long == 0 || long_rows, "long rows listed without an index array");
   if (n_rows == 0) return HG_OK;
+  if (n_long == 0) long_thresh = INT64_MAX;
   cudaStream_t st = as_stream(stream);
   const int g = grid_for(n_rows, 8, 148 * 64);
-  if (dtype == HG_F16)
+  if (dtype == HG_F16) {
     k_edge_rowsum<__half><<<g, 256, 0, st>>>(offsets, n_rows, (const __half*)vals, perm, heads,
-                                             (__half*)out);
-  else
+                                             (__half*)out, long_thresh);
+    if (n_long)
+      k_edge_rowsum_long<__half><<<(unsigned)n_long, 1024, 0, st>>>(
+          offsets, long_rows, (const __half*)vals, perm, heads, (__half*)out);
+  } else {
     k_edge_rowsum<float><<<g, 256, 0, st>>>(offsets, n_rows, (const float*)vals, perm, heads,
-                                            (float*)out);
+                                            (float*)out, long_thresh);
+    if (n_long)
+      k_edge_rowsum_long<float><<<(unsigned)n_long, 1024, 0, st>>>(
+          offsets, long_rows, (const float*)vals, perm, heads, (float*)out);
+  }
   HG_LAUNCHED();
   return HG_OK;
 }
@@ -560,6 +758,67 @@ k_head_dots(const T* __restrict__ z, const T* __restrict__ al, const T* __restri
   }
 }
 
+// Head-dot backward, pass 1: blocks stride over rows; thread (rr, f) owns
+// column f of row slot rr; writes gz and fp32 partial column sums.
+constexpr int kHdbBlocks = 148 * 4;
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_head_dots_bwd(const T* __restrict__ z, const T* __restrict__ al, const T* __restrict__ ar,
+                const T* __restrict__ gl, const T* __restrict__ gr, int64_t n, int heads, int fh,
+                T* __restrict__ gz, float* __restrict__ part) {
+  using N = Num<T>;
+  const int F = heads * fh;
+  const int rpi = F >= 256 ? 1 : 256 / F;
+  const int rr = threadIdx.x / (F >= 256 ? 256 : F);
+  for (int f0 = 0; f0 < F; f0 += 256) {
+    const int f = f0 + (F >= 256 ? (int)threadIdx.x : (int)(threadIdx.x % F));
+    const bool act = f < F && rr < rpi;
+    const int h = act ? f / fh : 0;
+    const T a1 = act ? al[f] : N::zero(), a2 = act ? ar[f] : N::zero();
+    float sl = 0.0f, sr = 0.0f;
+    if (act) {
+      for (int64_t r = (int64_t)blockIdx.x * rpi + rr; r < n; r += (int64_t)gridDim.x * rpi) {
+        const T g1 = gl[r * heads + h], g2 = gr[r * heads + h];
+        const float zf = N::to_f(z[r * F + f]);
+        gz[r * F + f] = N::add(N::mul(g1, a1), N::mul(g2, a2));
+        sl = fmaf(zf, N::to_f(g1), sl);
+        sr = fmaf(zf, N::to_f(g2), sr);
+      }
+    }
+    // fold the rpi row slots of the block in slot order (deterministic)
+    __shared__ float bl[256], br[256];
+    bl[threadIdx.x] = sl;
+    br[threadIdx.x] = sr;
+    __syncthreads();
+    if (act && rr == 0) {
+      float tl = 0.0f, tr = 0.0f;
+      for (int q = 0; q < rpi; ++q) {
+        tl += bl[q * (F >= 256 ? 256 : F) + (threadIdx.x)];
+        tr += br[q * (F >= 256 ? 256 : F) + (threadIdx.x)];
+      }
+      part[((int64_t)blockIdx.x * 2 + 0) * F + f] = tl;
+      part[((int64_t)blockIdx.x * 2 + 1) * F + f] = tr;
+    }
+    __syncthreads();
+  }
+}
+
+// Pass 2: fold the per-block partials in block order, round once.
+template <typename T>
+__global__ void k_head_dots_bwd_fold(const float* __restrict__ part, int nblk, int F,
+                                     T* __restrict__ gal, T* __restrict__ gar) {
+  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x) {
+    float tl = 0.0f, tr = 0.0f;
+    for (int b = 0; b < nblk; ++b) {
+      tl += part[((int64_t)b * 2 + 0) * F + f];
+      tr += part[((int64_t)b * 2 + 1) * F + f];
+    }
+    gal[f] = Num<T>::from_f(tl);
+    gar[f] = Num<T>::from_f(tr);
+  }
+}
+
 template <typename G>
 __global__ void k_adam(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
                        const G* __restrict__ grad, int64_t count, float lr, float omb1,
@@ -629,6 +888,39 @@ extern "C" int hg_adam_step(float* master, float* m, float* v, const void* grad,
   else
     k_adam<float><<<g, 256, 0, st>>>(master, m, v, (const float*)grad, count, lr, omb1, omb2,
                                      b1, b2, eps, step);
+  HG_LAUNCHED();
+  return HG_OK;
+}
+
+extern "C" int hg_head_dots_bwd_workspace(int32_t heads, int32_t fh, size_t* bytes) {
+  HG_REQUIRE(bytes && heads >= 1 && fh >= 1, "hg_head_dots_bwd_workspace: bad arguments");
+  *bytes = (size_t)kHdbBlocks * 2 * heads * fh * sizeof(float);
+  return HG_OK;
+}
+
+extern "C" int hg_head_dots_bwd(const void* z, const void* a_l, const void* a_r, const void* g_l,
+                                const void* g_r, int64_t n, int32_t heads, int32_t fh, void* gz,
+                                void* ga_l, void* ga_r, int dtype, void* ws, size_t ws_bytes,
+                                void* stream) {
+  HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
+  HG_REQUIRE(heads >= 1 && fh >= 1, "hg_head_dots_bwd: bad shape");
+  const int F = heads * fh;
+  HG_REQUIRE(ws_bytes >= (size_t)kHdbBlocks * 2 * F * sizeof(float), "hg_head_dots_bwd: workspace too small");
+  cudaStream_t st = as_stream(stream);
+  float* part = (float*)ws;
+  if (dtype == HG_F16) {
+    k_head_dots_bwd<__half><<<kHdbBlocks, 256, 0, st>>>(
+        (const __half*)z, (const __half*)a_l, (const __half*)a_r, (const __half*)g_l,
+        (const __half*)g_r, n, heads, fh, (__half*)gz, part);
+    k_head_dots_bwd_fold<__half><<<(F + 255) / 256, 256, 0, st>>>(part, kHdbBlocks, F,
+                                                                (__half*)ga_l, (__half*)ga_r);
+  } else {
+    k_head_dots_bwd<float><<<kHdbBlocks, 256, 0, st>>>(
+        (const float*)z, (const float*)a_l, (const float*)a_r, (const float*)g_l,
+        (const float*)g_r, n, heads, fh, (float*)gz, part);
+    k_head_dots_bwd_fold<float><<<(F + 255) / 256, 256, 0, st>>>(part, kHdbBlocks, F,
+                                                               (float*)ga_l, (float*)ga_r);
+  }
   HG_LAUNCHED();
   return HG_OK;
 }

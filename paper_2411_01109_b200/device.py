@@ -27,6 +27,7 @@ from . import _native as nat
 DTYPE_CODE = {torch.float16: nat.HG_F16, torch.float32: nat.HG_F32}
 MIRROR = {"none": "none", "left": "right", "right": "left", "both": "both"}
 DEFAULT_SPLIT_CAP = 512
+LONG_ROW = 4096   # rows longer than this get a whole CTA in the row-owned softmax/sum kernels
 
 
 def _p(t):
@@ -193,6 +194,16 @@ class CsrView:
             s = build_schedule(self.offsets, split_cap)
             self._sched[split_cap] = s
         return s
+
+    def long_rows(self, thresh: int = LONG_ROW) -> torch.Tensor:
+        """int32 ids of rows with more than `thresh` edges (cached)."""
+        key = ("long", thresh)
+        t = self._sched.get(key)
+        if t is None:
+            deg = self.offsets[1:] - self.offsets[:-1]
+            t = torch.nonzero(deg > thresh).flatten().to(torch.int32)
+            self._sched[key] = t
+        return t
 
 
 class DeviceGraph:
@@ -412,37 +423,52 @@ def attention_logits(dg: DeviceGraph, s_l, s_r, slope=0.2):
     return out
 
 
-def edge_softmax_fwd(dg: DeviceGraph, e):
+def softmax_fwd_view(view: CsrView, e):
     _require_cuda(e)
     e = e.contiguous()
     heads = e.shape[1] if e.dim() == 2 else 1
     alpha = torch.empty_like(e)
-    nat.call("hg_edge_softmax_fwd", _p(dg.offsets), dg.n, dg.num_edges, _p(e), _p(alpha), heads,
-             _dtype_code(e), _stream())
-    Probe.launches += 1
+    lr = view.long_rows()
+    nat.call("hg_edge_softmax_fwd", _p(view.offsets), view.n_rows, view.num_edges, _p(e),
+             _p(alpha), heads, _p(lr), lr.numel(), LONG_ROW, _dtype_code(e), _stream())
+    Probe.launches += 1 + int(lr.numel() > 0)
     return alpha
 
 
-def edge_softmax_bwd(dg: DeviceGraph, alpha, g):
+def softmax_bwd_view(view: CsrView, alpha, g):
     alpha, g = alpha.contiguous(), g.contiguous()
     heads = alpha.shape[1] if alpha.dim() == 2 else 1
     de = torch.empty_like(alpha)
-    nat.call("hg_edge_softmax_bwd", _p(dg.offsets), dg.n, dg.num_edges, _p(alpha), _p(g),
-             _p(de), heads, _dtype_code(alpha), _stream())
-    Probe.launches += 1
+    lr = view.long_rows()
+    nat.call("hg_edge_softmax_bwd", _p(view.offsets), view.n_rows, view.num_edges, _p(alpha),
+             _p(g), _p(de), heads, _p(lr), lr.numel(), LONG_ROW, _dtype_code(alpha), _stream())
+    Probe.launches += 1 + int(lr.numel() > 0)
     return de
+
+
+def rowsum_view(view: CsrView, v, perm=None):
+    v = v.contiguous()
+    heads = v.shape[1] if v.dim() == 2 else 1
+    out = torch.empty((view.n_rows, heads), dtype=v.dtype, device=v.device)
+    lr = view.long_rows()
+    nat.call("hg_edge_rowsum", _p(view.offsets), view.n_rows, view.num_edges, _p(v), _p(perm),
+             heads, _p(out), _p(lr), lr.numel(), LONG_ROW, _dtype_code(v), _stream())
+    Probe.launches += 1 + int(lr.numel() > 0)
+    return out
+
+
+def edge_softmax_fwd(dg: DeviceGraph, e):
+    return softmax_fwd_view(dg.fwd, e)
+
+
+def edge_softmax_bwd(dg: DeviceGraph, alpha, g):
+    return softmax_bwd_view(dg.fwd, alpha, g)
 
 
 def edge_rowsum(dg: DeviceGraph, v, transpose=False):
     """Per-row (transpose=False) or per-column (True) sums of per-edge values."""
-    v = v.contiguous()
-    heads = v.shape[1] if v.dim() == 2 else 1
     view = dg.view(transpose)
-    out = torch.empty((view.n_rows, heads), dtype=v.dtype, device=v.device)
-    nat.call("hg_edge_rowsum", _p(view.offsets), view.n_rows, view.num_edges, _p(v),
-             _p(view.perm if transpose else None), heads, _p(out), _dtype_code(v), _stream())
-    Probe.launches += 1
-    return out
+    return rowsum_view(view, v, view.perm if transpose else None)
 
 
 def scale_f64(x, s: float):
@@ -486,3 +512,19 @@ def adam_step(master, m, v, grad, lr, b1, b2, eps, step):
              master.numel(), float(lr), float(1 - b1), float(1 - b2), float(b1), float(b2),
              float(eps), _p(step), _stream())
     Probe.launches += 1
+
+
+def head_dots_bwd(z, a_l, a_r, g_l, g_r, heads):
+    """Backward of head_dots: (gz, ga_l, ga_r), deterministic (hg_head_dots_bwd)."""
+    z = z.contiguous()
+    n = z.shape[0]
+    fh = z.shape[1] // heads
+    gz = torch.empty_like(z)
+    ga_l = torch.empty_like(a_l)
+    ga_r = torch.empty_like(a_r)
+    ws = workspace(nat.size_query("hg_head_dots_bwd_workspace", heads, fh), z.device)
+    nat.call("hg_head_dots_bwd", _p(z), _p(a_l.contiguous()), _p(a_r.contiguous()),
+             _p(g_l.contiguous()), _p(g_r.contiguous()), n, heads, fh, _p(gz), _p(ga_l),
+             _p(ga_r), _dtype_code(z), _p(ws), ws.numel(), _stream())
+    Probe.launches += 2
+    return gz, ga_l, ga_r

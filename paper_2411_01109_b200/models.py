@@ -165,6 +165,10 @@ class GraphBundle:
     def scale(x, s):
         return D.scale_f64(x, s)
 
+    @staticmethod
+    def head_dots_bwd(z, a_l, a_r, g_l, g_r, heads):
+        return D.head_dots_bwd(z, a_l, a_r, g_l, g_r, heads)
+
     def attn_logits(self, s_l, s_r, slope):
         return D.attention_logits(self.dg, s_l, s_r, slope)
 
@@ -593,21 +597,14 @@ class _HeadDotsFn(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, z, a_l, a_r, heads, bundle):
-        ctx.heads = heads
+        ctx.heads, ctx.bundle = heads, bundle
         ctx.save_for_backward(z, a_l, a_r)
         return bundle.head_dots(z, a_l, a_r, heads)
 
     @staticmethod
     def backward(ctx, g_l, g_r):
         z, a_l, a_r = ctx.saved_tensors
-        h = ctx.heads
-        n = z.shape[0]
-        g_l, g_r = g_l.contiguous(), g_r.contiguous()
-        gz = ((g_l.float()[:, :, None] * a_l.float()[None]).to(z.dtype)
-              + (g_r.float()[:, :, None] * a_r.float()[None]).to(z.dtype)).reshape(n, -1)
-        zt = z.view(n, h, -1).permute(1, 2, 0)                      # [H, F, N]
-        ga_l = torch.matmul(zt, g_l.t()[:, :, None])[..., 0]        # [H, F]
-        ga_r = torch.matmul(zt, g_r.t()[:, :, None])[..., 0]
+        gz, ga_l, ga_r = ctx.bundle.head_dots_bwd(z, a_l, a_r, g_l, g_r, ctx.heads)
         return gz, ga_l, ga_r, None, None
 
 

@@ -152,19 +152,11 @@ class CudaOps:
 
     @staticmethod
     def softmax_fwd(view, e):
-        heads = e.shape[1] if e.dim() == 2 else 1
-        alpha = torch.empty_like(e)
-        D.nat.call("hg_edge_softmax_fwd", D._p(view.offsets), view.n_rows, view.num_edges,
-                   D._p(e), D._p(alpha), heads, D._dtype_code(e), D._stream())
-        return alpha
+        return D.softmax_fwd_view(view, e)
 
     @staticmethod
     def softmax_bwd(view, alpha, g):
-        heads = alpha.shape[1] if alpha.dim() == 2 else 1
-        de = torch.empty_like(alpha)
-        D.nat.call("hg_edge_softmax_bwd", D._p(view.offsets), view.n_rows, view.num_edges,
-                   D._p(alpha), D._p(g), D._p(de), heads, D._dtype_code(alpha), D._stream())
-        return de
+        return D.softmax_bwd_view(view, alpha, g)
 
     @staticmethod
     def xent(logits, labels, n_active, denom):
@@ -180,11 +172,11 @@ class CudaOps:
 
     @staticmethod
     def edge_sums(view, v, perm):
-        heads = v.shape[1] if v.dim() == 2 else 1
-        out = torch.empty((view.n_rows, heads), dtype=v.dtype, device=v.device)
-        D.nat.call("hg_edge_rowsum", D._p(view.offsets), view.n_rows, view.num_edges, D._p(v),
-                   D._p(perm), heads, D._p(out), D._dtype_code(v), D._stream())
-        return out
+        return D.rowsum_view(view, v, perm)
+
+    @staticmethod
+    def head_dots_bwd(z, a_l, a_r, g_l, g_r, heads):
+        return D.head_dots_bwd(z, a_l, a_r, g_l, g_r, heads)
 
 
 class DistBundle:
@@ -255,6 +247,9 @@ class DistBundle:
 
     def scale(self, x, s):
         return self.ops.scale(x, s)
+
+    def head_dots_bwd(self, z, a_l, a_r, g_l, g_r, heads):
+        return self.ops.head_dots_bwd(z, a_l, a_r, g_l, g_r, heads)
 
     def softmax_fwd(self, e):
         return self.ops.softmax_fwd(self.part.fwd, e.contiguous())

@@ -102,6 +102,17 @@ def _host_head_dots(z, a_l, a_r, heads):
             (zh * a_r.double()[None]).sum(-1).to(z.dtype))
 
 
+def _host_head_dots_bwd(z, a_l, a_r, g_l, g_r, heads):
+    n = z.shape[0]
+    zh = z.view(n, heads, -1).double()
+    gz = ((g_l.double()[:, :, None] * a_l.double()[None]).to(z.dtype)
+          + (g_r.double()[:, :, None] * a_r.double()[None]).to(z.dtype)).reshape(n, -1)
+    ga_l = (zh * g_l.double()[:, :, None]).sum(0).to(z.dtype)
+    ga_r = (zh * g_r.double()[:, :, None]).sum(0).to(z.dtype)
+    return gz, ga_l, ga_r
+
+
+HostOps.head_dots_bwd = staticmethod(_host_head_dots_bwd)
 HostOps.xent = staticmethod(_host_xent)
 HostOps.sddmm = staticmethod(_host_sddmm)
 HostOps.attn = staticmethod(_host_attn)

@@ -362,3 +362,56 @@ def test_scale_f64_matches_numpy(cuda):
     got = D.scale_f64(_t(allv, cuda), 0.2).cpu().numpy()
     want = (allv.astype(np.float64) * 0.2).astype(np.float16)
     np.testing.assert_array_equal(bits(got), bits(want))
+
+
+def test_softmax_and_rowsum_long_rows(cuda):
+    """Rows above device.LONG_ROW take the one-CTA-per-row kernels; the tree
+    order (and so every bit) must not change."""
+    from paper_2411_01109_b200 import device as D
+
+    rng = np.random.default_rng(99)
+    n = 80_000
+    deg = rng.integers(0, 6, n)
+    deg[[3, 17, 500]] = [5000, 20_000, 70_001]
+    rows = np.repeat(np.arange(n), deg)
+    cols = rng.integers(0, n, rows.size)
+    r, c = O.canonical_edges(n, rows, cols)
+    dg = _dg(n, r, c, cuda)
+    assert dg.fwd.long_rows().numel() == 3
+    e = rng.uniform(-8, 8, (r.size, 2)).astype(np.float16)
+    g = rng.normal(size=(r.size, 2)).astype(np.float16)
+    off = O.csr_offsets(n, r)
+    alpha = D.edge_softmax_fwd(dg, _t(e, cuda))
+    np.testing.assert_array_equal(bits(alpha.cpu().numpy()), bits(O.edge_softmax_fwd(off, e)))
+    de = D.edge_softmax_bwd(dg, alpha, _t(g, cuda)).cpu().numpy()
+    np.testing.assert_array_equal(bits(de), bits(O.edge_softmax_bwd(off, alpha.cpu().numpy(), g)))
+    rs = D.edge_rowsum(dg, _t(g, cuda)).cpu().numpy().astype(np.float64)
+    want = np.zeros((n, 2))
+    np.add.at(want, r, g.astype(np.float64))
+    np.testing.assert_allclose(rs, want, rtol=2e-3, atol=2e-2)
+
+
+@pytest.mark.parametrize("heads,fh", [(1, 64), (4, 16), (4, 32), (3, 6), (2, 160)])
+def test_head_dots_fwd_bwd(cuda, heads, fh):
+    from paper_2411_01109_b200 import device as D
+
+    rng = np.random.default_rng(heads * fh)
+    n = 5000
+    z = rng.normal(size=(n, heads * fh)).astype(np.float16)
+    a_l = rng.normal(size=(heads, fh)).astype(np.float16)
+    a_r = rng.normal(size=(heads, fh)).astype(np.float16)
+    zt, alt, art = _t(z, cuda), _t(a_l, cuda), _t(a_r, cuda)
+    s_l, s_r = D.head_dots(zt, alt, art, heads)
+    zh = z.reshape(n, heads, fh).astype(np.float64)
+    want_l = (zh * a_l.astype(np.float64)[None]).sum(-1)
+    np.testing.assert_allclose(s_l.cpu().numpy().astype(np.float64), want_l, rtol=2e-3, atol=2e-2)
+    g_l = rng.normal(size=(n, heads)).astype(np.float16)
+    g_r = rng.normal(size=(n, heads)).astype(np.float16)
+    gz, ga_l, ga_r = D.head_dots_bwd(zt, alt, art, _t(g_l, cuda), _t(g_r, cuda), heads)
+    want_gz = ((g_l.astype(np.float64)[:, :, None] * a_l[None]).astype(np.float16).astype(np.float64)
+               + (g_r.astype(np.float64)[:, :, None] * a_r[None]).astype(np.float16)).astype(np.float16)
+    np.testing.assert_array_equal(bits(gz.cpu().numpy()), bits(want_gz.reshape(n, -1)))
+    want_ga = (zh * g_l.astype(np.float64)[:, :, None]).sum(0)
+    np.testing.assert_allclose(ga_l.cpu().numpy().astype(np.float64), want_ga, rtol=3e-3, atol=0.1)
+    a1 = D.head_dots_bwd(zt, alt, art, _t(g_l, cuda), _t(g_r, cuda), heads)
+    assert torch.equal(a1[1], ga_l) and torch.equal(a1[2], ga_r)  # deterministic
