@@ -128,21 +128,38 @@ def reddit_like(seed=0, device="cuda", n=REDDIT_N, e=REDDIT_E):
 
 
 def products_like(seed=0, device="cuda", n=PRODUCTS_N, undirected=PRODUCTS_UNDIRECTED_E,
-                  exponent=2.1):
-    """C4: Chung-Lu power-law graph with `undirected` edges, symmetrised."""
+                  exponent=2.1, max_degree=17_000):
+    """C4: Chung-Lu power-law graph with exactly `undirected` distinct undirected
+    edges (no self loops), symmetrised.  Expected degrees follow
+    rank^(-1/(exponent-1)) scaled to the target mean and clipped to
+    [1, max_degree] (ogbn-products' maximum degree is ~17K); endpoints are
+    drawn proportionally, duplicates are topped up until the count is exact."""
     gen = _gen(seed, device)
     ranks = torch.arange(1, n + 1, device=device, dtype=torch.float64)
-    weight = ranks.pow(-1.0 / (exponent - 1.0))
-    prob = weight / weight.sum()
-    src = torch.multinomial(prob.float(), undirected, replacement=True, generator=gen)
-    dst = torch.multinomial(prob.float(), undirected, replacement=True, generator=gen)
+    w = ranks.pow(-1.0 / (exponent - 1.0))
+    mean = 2.0 * undirected / n
+    for _ in range(20):  # rescale so the clipped weights keep the target mean
+        w = (w * (mean * n / w.clamp(1.0, max_degree).sum())).clamp(min=1e-9)
+    w = w.clamp(1.0, max_degree)
+    prob = (w / w.sum()).float()
     perm = torch.randperm(n, generator=gen, device=device)
-    src, dst = perm[src], perm[dst]
-    keep = src != dst
-    src, dst = src[keep], dst[keep]
-    rows = torch.cat([src, dst])
-    cols = torch.cat([dst, src])
-    offsets, c32, _ = build_csr(n, rows, cols)
+    keys = torch.empty(0, dtype=torch.int64, device=device)
+    need = undirected
+    for _ in range(16):
+        m = int(need * 1.15) + 1024
+        a = perm[torch.multinomial(prob, m, replacement=True, generator=gen)]
+        b = perm[torch.multinomial(prob, m, replacement=True, generator=gen)]
+        keep = a != b
+        lo, hi = torch.minimum(a, b)[keep], torch.maximum(a, b)[keep]
+        keys = torch.unique(torch.cat([keys, lo * n + hi]))
+        need = undirected - keys.numel()
+        if need <= 0:
+            break
+    if keys.numel() > undirected:  # drop a random surplus
+        pick = torch.randperm(keys.numel(), generator=gen, device=device)[:undirected]
+        keys = keys[pick]
+    src, dst = keys // n, keys % n
+    offsets, c32, _ = build_csr(n, torch.cat([src, dst]), torch.cat([dst, src]))
     return DeviceGraph(n, offsets, c32)
 
 
