@@ -384,6 +384,155 @@ k_edge_rowsum(const int64_t* __restrict__ offsets, int64_t n_rows, const T* __re
   }
 }
 
+// ------------------------------------ short rows, all heads per warp pass
+// Lane l works on edge (l / H) of the current 32/H-edge block and head l % H
+// (edge-major [E, H] storage: a warp reads 64 contiguous bytes).  Per-head
+// trees combine lanes at stride H; block roots are pushed on a per-lane
+// binary-counter stack (replicated across the lanes of a head).
+
+template <typename T, int H>
+struct HeadTree {
+  T stk[40];
+  int64_t blocks = 0;
+  static constexpr int EPB = 32 / H;  // edges per block
+  // v: this lane's element (edge base + lane/H, head lane%H); returns nothing,
+  // pushes the block root for this lane's head.
+  __device__ __forceinline__ void push(T v, int64_t base, int64_t len, int lane) {
+    using N = Num<T>;
+    const int j = lane / H;
+#pragma unroll
+    for (int s = 1; s < EPB; s <<= 1) {
+      const T o = shfl_down_t(0xffffffffu, v, s * H, 32);
+      if ((j & (2 * s - 1)) == 0 && base + j + s < len) v = N::add(v, o);
+    }
+    T cur;
+    if constexpr (sizeof(T) == 2)
+      cur = __ushort_as_half((unsigned short)__shfl_sync(0xffffffffu, (unsigned)__half_as_ushort(v), lane % H));
+    else
+      cur = __shfl_sync(0xffffffffu, v, lane % H);
+    int64_t t = blocks;
+    int lvl = 0;
+    while (t & 1) {
+      cur = N::add(stk[lvl], cur);
+      t >>= 1;
+      ++lvl;
+    }
+    stk[lvl] = cur;
+    ++blocks;
+  }
+  __device__ __forceinline__ T root() const {
+    using N = Num<T>;
+    T acc = N::zero();
+    bool have = false;
+    for (int lvl = 0; lvl < 40; ++lvl) {
+      if ((blocks >> lvl) & 1) {
+        acc = have ? N::add(stk[lvl], acc) : stk[lvl];
+        have = true;
+      }
+    }
+    return acc;
+  }
+};
+
+template <int H>
+__device__ __forceinline__ float head_max(float v) {
+#pragma unroll
+  for (int s = 16; s >= H; s >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, s));
+  return v;
+}
+
+template <typename T, int H>
+__global__ void __launch_bounds__(256)
+k_softmax_fwd_h(const int64_t* __restrict__ offsets, int64_t n_rows, const T* __restrict__ e,
+                T* __restrict__ alpha, int64_t long_thresh) {
+  using N = Num<T>;
+  constexpr int EPB = 32 / H;
+  const int lane = threadIdx.x & 31;
+  const int j = lane / H;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows;
+       r += nwarps) {
+    const int64_t beg = offsets[r], len = offsets[r + 1] - beg;
+    if (len == 0 || len > long_thresh) continue;
+    const T* er = e + beg * H;
+    T* ar = alpha + beg * H;
+    float m = -INFINITY;
+    bool nan = false;
+    for (int64_t i = lane; i < len * H; i += 32) {
+      const float v = N::to_f(er[i]);
+      nan |= v != v;
+      m = fmaxf(m, v);
+    }
+    m = head_max<H>(m);
+    nan = head_max<H>(nan ? 1.0f : 0.0f) > 0.0f;
+    const T mt = nan ? N::from_f(NAN) : N::from_f(m);
+    HeadTree<T, H> tree;
+    for (int64_t b = 0; b < len; b += EPB) {
+      const int64_t i = b + j;
+      T ex = N::zero();
+      if (i < len) {
+        ex = N::from_d(exp(N::to_d(N::sub(er[i * H + lane % H], mt))));
+        ar[i * H + lane % H] = ex;
+      }
+      tree.push(ex, b, len, lane);
+    }
+    const double den = N::to_d(tree.root());
+    for (int64_t i = lane; i < len * H; i += 32) ar[i] = N::from_d(N::to_d(ar[i]) / den);
+  }
+}
+
+template <typename T, int H>
+__global__ void __launch_bounds__(256)
+k_softmax_bwd_h(const int64_t* __restrict__ offsets, int64_t n_rows, const T* __restrict__ alpha,
+                const T* __restrict__ g, T* __restrict__ de, int64_t long_thresh) {
+  using N = Num<T>;
+  constexpr int EPB = 32 / H;
+  const int lane = threadIdx.x & 31;
+  const int j = lane / H;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows;
+       r += nwarps) {
+    const int64_t beg = offsets[r], len = offsets[r + 1] - beg;
+    if (len == 0 || len > long_thresh) continue;
+    const T* a = alpha + beg * H;
+    const T* gr = g + beg * H;
+    HeadTree<T, H> tree;
+    for (int64_t b = 0; b < len; b += EPB) {
+      const int64_t i = b + j;
+      T p = N::zero();
+      if (i < len) p = N::mul(a[i * H + lane % H], gr[i * H + lane % H]);
+      tree.push(p, b, len, lane);
+    }
+    const T sv = tree.root();  // this lane's head
+    // lanes of a head hold its root; element k = (edge, head) reads head k % H,
+    // which for the strided loop below is again lane % H (32 % H == 0)
+    for (int64_t k = lane; k < len * H; k += 32) de[beg * H + k] = N::mul(a[k], N::sub(gr[k], sv));
+  }
+}
+
+template <typename T, int H>
+__global__ void __launch_bounds__(256)
+k_edge_rowsum_h(const int64_t* __restrict__ offsets, int64_t n_rows, const T* __restrict__ v,
+                const int32_t* __restrict__ perm, T* __restrict__ out, int64_t long_thresh) {
+  const int lane = threadIdx.x & 31;
+  constexpr int EPB = 32 / H;
+  const int j = lane / H, h = lane % H;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows;
+       r += nwarps) {
+    const int64_t beg = offsets[r], end = offsets[r + 1];
+    if (end - beg > long_thresh) continue;
+    float s = 0.0f;
+    for (int64_t i = beg + j; i < end; i += EPB) {
+      const int64_t idx = perm ? (int64_t)perm[i] : i;
+      s += Num<T>::to_f(v[idx * H + h]);
+    }
+#pragma unroll
+    for (int o = 16; o >= H; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane < H) out[r * H + lane] = Num<T>::from_f(s);
+  }
+}
+
 // ------------------------------------------------ long rows: one CTA per row
 // 1024 threads cover a 1024-element superblock per step: each warp reduces its
 // aligned 32-element block (predicated shuffles), warp 0 reduces the 32 block
@@ -574,7 +723,26 @@ extern "C" int hg_edge_softmax_fwd(const int64_t* offsets, int64_t n_rows, int64
   if (n_long == 0) long_thresh = INT64_MAX;
   cudaStream_t st = as_stream(stream);
   const int g = grid_for(n_rows, 8, 148 * 64);
-  if (dtype == HG_F16) {
+  const bool pow2 = heads <= 16 && (heads & (heads - 1)) == 0;
+#define HG_SMF(TT)                                                                          \
+  switch (heads) {                                                                          \
+    case 1: k_softmax_fwd_h<TT, 1><<<g, 256, 0, st>>>(offsets, n_rows, (const TT*)e, (TT*)alpha, long_thresh); break; \
+    case 2: k_softmax_fwd_h<TT, 2><<<g, 256, 0, st>>>(offsets, n_rows, (const TT*)e, (TT*)alpha, long_thresh); break; \
+    case 4: k_softmax_fwd_h<TT, 4><<<g, 256, 0, st>>>(offsets, n_rows, (const TT*)e, (TT*)alpha, long_thresh); break; \
+    case 8: k_softmax_fwd_h<TT, 8><<<g, 256, 0, st>>>(offsets, n_rows, (const TT*)e, (TT*)alpha, long_thresh); break; \
+    default: k_softmax_fwd_h<TT, 16><<<g, 256, 0, st>>>(offsets, n_rows, (const TT*)e, (TT*)alpha, long_thresh); \
+  }
+  if (dtype == HG_F16 && pow2) {
+    HG_SMF(__half)
+    if (n_long)
+      k_softmax_fwd_long<__half><<<(unsigned)n_long, 1024, 0, st>>>(
+          offsets, long_rows, (const __half*)e, (__half*)alpha, heads);
+  } else if (dtype == HG_F32 && pow2) {
+    HG_SMF(float)
+    if (n_long)
+      k_softmax_fwd_long<float><<<(unsigned)n_long, 1024, 0, st>>>(
+          offsets, long_rows, (const float*)e, (float*)alpha, heads);
+  } else if (dtype == HG_F16) {
     k_softmax_fwd<__half><<<g, 256, 0, st>>>(offsets, n_rows, (const __half*)e, (__half*)alpha,
                                              heads, long_thresh);
     if (n_long)
@@ -603,7 +771,26 @@ extern "C" int hg_edge_softmax_bwd(const int64_t* offsets, int64_t n_rows, int64
   if (n_long == 0) long_thresh = INT64_MAX;
   cudaStream_t st = as_stream(stream);
   const int g = grid_for(n_rows, 8, 148 * 64);
-  if (dtype == HG_F16) {
+  const bool pow2 = heads <= 16 && (heads & (heads - 1)) == 0;
+#define HG_SMB(TT)                                                                          \
+  switch (heads) {                                                                          \
+    case 1: k_softmax_bwd_h<TT, 1><<<g, 256, 0, st>>>(offsets, n_rows, (const TT*)alpha, (const TT*)grad, (TT*)de, long_thresh); break; \
+    case 2: k_softmax_bwd_h<TT, 2><<<g, 256, 0, st>>>(offsets, n_rows, (const TT*)alpha, (const TT*)grad, (TT*)de, long_thresh); break; \
+    case 4: k_softmax_bwd_h<TT, 4><<<g, 256, 0, st>>>(offsets, n_rows, (const TT*)alpha, (const TT*)grad, (TT*)de, long_thresh); break; \
+    case 8: k_softmax_bwd_h<TT, 8><<<g, 256, 0, st>>>(offsets, n_rows, (const TT*)alpha, (const TT*)grad, (TT*)de, long_thresh); break; \
+    default: k_softmax_bwd_h<TT, 16><<<g, 256, 0, st>>>(offsets, n_rows, (const TT*)alpha, (const TT*)grad, (TT*)de, long_thresh); \
+  }
+  if (dtype == HG_F16 && pow2) {
+    HG_SMB(__half)
+    if (n_long)
+      k_softmax_bwd_long<__half><<<(unsigned)n_long, 1024, 0, st>>>(
+          offsets, long_rows, (const __half*)alpha, (const __half*)grad, (__half*)de, heads);
+  } else if (dtype == HG_F32 && pow2) {
+    HG_SMB(float)
+    if (n_long)
+      k_softmax_bwd_long<float><<<(unsigned)n_long, 1024, 0, st>>>(
+          offsets, long_rows, (const float*)alpha, (const float*)grad, (float*)de, heads);
+  } else if (dtype == HG_F16) {
     k_softmax_bwd<__half><<<g, 256, 0, st>>>(offsets, n_rows, (const __half*)alpha,
                                              (const __half*)grad, (__half*)de, heads, long_thresh);
     if (n_long)
@@ -632,7 +819,26 @@ extern "C" int hg_edge_rowsum(const int64_t* offsets, int64_t n_rows, int64_t nu
   if (n_long == 0) long_thresh = INT64_MAX;
   cudaStream_t st = as_stream(stream);
   const int g = grid_for(n_rows, 8, 148 * 64);
-  if (dtype == HG_F16) {
+  const bool pow2 = heads <= 16 && (heads & (heads - 1)) == 0;
+#define HG_RS(TT)                                                                           \
+  switch (heads) {                                                                          \
+    case 1: k_edge_rowsum_h<TT, 1><<<g, 256, 0, st>>>(offsets, n_rows, (const TT*)vals, perm, (TT*)out, long_thresh); break; \
+    case 2: k_edge_rowsum_h<TT, 2><<<g, 256, 0, st>>>(offsets, n_rows, (const TT*)vals, perm, (TT*)out, long_thresh); break; \
+    case 4: k_edge_rowsum_h<TT, 4><<<g, 256, 0, st>>>(offsets, n_rows, (const TT*)vals, perm, (TT*)out, long_thresh); break; \
+    case 8: k_edge_rowsum_h<TT, 8><<<g, 256, 0, st>>>(offsets, n_rows, (const TT*)vals, perm, (TT*)out, long_thresh); break; \
+    default: k_edge_rowsum_h<TT, 16><<<g, 256, 0, st>>>(offsets, n_rows, (const TT*)vals, perm, (TT*)out, long_thresh); \
+  }
+  if (dtype == HG_F16 && pow2) {
+    HG_RS(__half)
+    if (n_long)
+      k_edge_rowsum_long<__half><<<(unsigned)n_long, 1024, 0, st>>>(
+          offsets, long_rows, (const __half*)vals, perm, heads, (__half*)out);
+  } else if (dtype == HG_F32 && pow2) {
+    HG_RS(float)
+    if (n_long)
+      k_edge_rowsum_long<float><<<(unsigned)n_long, 1024, 0, st>>>(
+          offsets, long_rows, (const float*)vals, perm, heads, (float*)out);
+  } else if (dtype == HG_F16) {
     k_edge_rowsum<__half><<<g, 256, 0, st>>>(offsets, n_rows, (const __half*)vals, perm, heads,
                                              (__half*)out, long_thresh);
     if (n_long)
