@@ -26,6 +26,7 @@ NVCC_FLAGS = ARCH + [
     # numpy's float32 1/d and 1/sqrt(d) bit for bit (kernels.py:118-140).
     "-prec-div=true", "-prec-sqrt=true",
     f"-I{INCLUDE}",
+    f"-I{BUILD}",
 ]
 
 
@@ -47,8 +48,25 @@ def _stale(target: Path, deps) -> bool:
     return any(Path(d).stat().st_mtime > t for d in deps)
 
 
+def write_exp_table() -> Path:
+    """build/hg_exp16.inc: rnd_f16(exp(x)) for every binary16 input x, computed
+    with numpy's float64 exp and one RNE rounding -- the reference's shadow_exp
+    (models.py:360-371) -- so the device lookup is exact by construction."""
+    import numpy as np
+
+    out = BUILD / "hg_exp16.inc"
+    vals = np.arange(65536, dtype=np.uint16).view(np.float16).astype(np.float64)
+    with np.errstate(over="ignore", invalid="ignore"):
+        table = np.exp(vals).astype(np.float16).view(np.uint16)
+    text = ",".join(str(int(v)) for v in table)
+    if not out.exists() or out.read_text() != text:
+        out.write_text(text)
+    return out
+
+
 def build(verbose: bool = False, force: bool = False) -> Path:
     BUILD.mkdir(exist_ok=True)
+    write_exp_table()
     headers = list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h")) + [Path(__file__)]
     nvcc = _nvcc()
     jobs = []

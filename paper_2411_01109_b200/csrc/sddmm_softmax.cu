@@ -223,6 +223,26 @@ __global__ void k_attn_scores(const int64_t* __restrict__ offsets, const int32_t
 
 // ------------------------------------------------------------ edge softmax
 
+// rnd(exp(x)) for binary16 x: table of all 65536 inputs, generated at build
+// time from numpy's float64 exp (exact by construction); binary32 uses fp64 exp.
+__device__ const unsigned short kExp16[65536] = {
+#include "hg_exp16.inc"
+};
+
+template <typename T>
+__device__ __forceinline__ T exp_rnd(T x) {
+  if constexpr (sizeof(T) == 2) return __ushort_as_half(__ldg(&kExp16[__half_as_ushort(x)]));
+  else return Num<T>::from_d(exp(Num<T>::to_d(x)));
+}
+
+// rnd(a / b): for binary16 an fp32 IEEE quotient rounded once more is the
+// correctly rounded half quotient (24 >= 2*11 + 2); binary32 divides in fp64.
+template <typename T>
+__device__ __forceinline__ T div_rnd(T a, T b) {
+  if constexpr (sizeof(T) == 2) return __float2half_rn(__fdiv_rn(__half2float(a), __half2float(b)));
+  else return Num<T>::from_d(Num<T>::to_d(a) / Num<T>::to_d(b));
+}
+
 // Adjacent-pair tree over a row's values, evaluated 32 at a time.
 template <typename T>
 struct RowTree {
@@ -264,7 +284,7 @@ struct RowTree {
     using N = Num<T>;
     T acc = N::zero();
     bool have = false;
-    for (int lvl = 0; lvl < 40; ++lvl) {
+    for (int lvl = 0; (blocks >> lvl) != 0; ++lvl) {
       if ((blocks >> lvl) & 1) {
         acc = have ? N::add(stk[lvl], acc) : stk[lvl];
         have = true;
@@ -314,15 +334,15 @@ k_softmax_fwd(const int64_t* __restrict__ offsets, int64_t n_rows, const T* __re
         T ex = N::zero();
         if (i < len) {
           const T s = N::sub(e[(beg + i) * heads + h], mt);
-          ex = N::from_d(exp(N::to_d(s)));
+          ex = exp_rnd<T>(s);
           alpha[(beg + i) * heads + h] = ex;
         }
         tree.push(ex, b, len, lane);
       }
-      const double den = N::to_d(tree.root());
+      const T den = tree.root();
       for (int64_t i = lane; i < len; i += 32) {
         const int64_t k = (beg + i) * heads + h;
-        alpha[k] = N::from_d(N::to_d(alpha[k]) / den);
+        alpha[k] = div_rnd<T>(alpha[k], den);
       }
     }
   }
@@ -424,7 +444,7 @@ struct HeadTree {
     using N = Num<T>;
     T acc = N::zero();
     bool have = false;
-    for (int lvl = 0; lvl < 40; ++lvl) {
+    for (int lvl = 0; (blocks >> lvl) != 0; ++lvl) {
       if ((blocks >> lvl) & 1) {
         acc = have ? N::add(stk[lvl], acc) : stk[lvl];
         have = true;
@@ -471,13 +491,13 @@ k_softmax_fwd_h(const int64_t* __restrict__ offsets, int64_t n_rows, const T* __
       const int64_t i = b + j;
       T ex = N::zero();
       if (i < len) {
-        ex = N::from_d(exp(N::to_d(N::sub(er[i * H + lane % H], mt))));
+        ex = exp_rnd<T>(N::sub(er[i * H + lane % H], mt));
         ar[i * H + lane % H] = ex;
       }
       tree.push(ex, b, len, lane);
     }
-    const double den = N::to_d(tree.root());
-    for (int64_t i = lane; i < len * H; i += 32) ar[i] = N::from_d(N::to_d(ar[i]) / den);
+    const T den = tree.root();
+    for (int64_t i = lane; i < len * H; i += 32) ar[i] = div_rnd<T>(ar[i], den);
   }
 }
 
@@ -586,7 +606,7 @@ k_softmax_fwd_long(const int64_t* __restrict__ offsets, const int32_t* __restric
   using N = Num<T>;
   __shared__ T roots[32];
   __shared__ float red[32];
-  __shared__ double den_s;
+  __shared__ T den_s;
   const int64_t r = rows[blockIdx.x];
   const int64_t beg = offsets[r], len = offsets[r + 1] - beg;
   for (int h = 0; h < heads; ++h) {
@@ -605,18 +625,18 @@ k_softmax_fwd_long(const int64_t* __restrict__ offsets, const int32_t* __restric
       T ex = N::zero();
       if (i < len) {
         const T sv = N::sub(e[(beg + i) * heads + h], mt);
-        ex = N::from_d(exp(N::to_d(sv)));
+        ex = exp_rnd<T>(sv);
         alpha[(beg + i) * heads + h] = ex;
       }
       const T rt = superblock_root(ex, sb, len, roots);
       if (threadIdx.x == 0) tree.push_root(rt);
     }
-    if (threadIdx.x == 0) den_s = N::to_d(tree.root());
+    if (threadIdx.x == 0) den_s = tree.root();
     __syncthreads();
-    const double den = den_s;
+    const T den = den_s;
     for (int64_t i = threadIdx.x; i < len; i += 1024) {
       const int64_t k = (beg + i) * heads + h;
-      alpha[k] = N::from_d(N::to_d(alpha[k]) / den);
+      alpha[k] = div_rnd<T>(alpha[k], den);
     }
     __syncthreads();
   }
