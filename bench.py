@@ -348,26 +348,38 @@ def b200_arm(args, ws, rank, local):
         if dist is not None:
             dist.barrier()
 
-    # ---- device-resident timing (value) ----
-    D.Probe.reset(timing=True)
-    with ClockSampler(local) as clocks:
+    def timed_steps(k):
         barrier()
         torch.cuda.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
-        for _ in range(args.steps):
+        for _ in range(k):
             loss, _ = tr.step()
         ev1.record()
         torch.cuda.synchronize()
         barrier()
+        ms = ev0.elapsed_time(ev1) / k
+        if dist is not None:
+            tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = float(tt.item())
+        return ms, loss
+
+    # ---- eager pass: SpMM roofline (CUDA events around every hg_spmm) ----
+    D.Probe.reset(timing=True)
+    eager_ms, _ = timed_steps(args.steps)
     launches = D.Probe.launches
     spmm_b, spmm_s, spmm_n = D.Probe.summary()
     D.Probe.reset(timing=False)
-    t_ms = ev0.elapsed_time(ev1) / args.steps
-    if dist is not None:
-        tt = torch.tensor([t_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_ms = float(tt.item())
+
+    # ---- device-resident timing (value): the step replayed as a CUDA graph ----
+    graphed = ws == 1 and not args.no_graph
+    if graphed:
+        tr.capture()
+        tr.step()
+        torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        t_ms, loss = timed_steps(args.steps)
     final_loss = float(loss)
 
     # ---- end to end through the public loop: host features in, loss out ----
@@ -407,6 +419,7 @@ def b200_arm(args, ws, rank, local):
             "e2e": {"value": round(e2e_ms, 4), "unit": "ms/epoch", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": 4},
             "gpu_launches": int(launches),
+            "ms_per_step_eager": round(eager_ms, 4), "cuda_graph": graphed,
             "roofline": {"bound": "hbm", "achieved": round(achieved / 1e9, 1),
                          "peak": round(peak / 1e9, 1), "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
@@ -445,6 +458,7 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-small", action="store_true", help="skip the C1/C2 epoch timings")
+    ap.add_argument("--no-graph", action="store_true", help="time eager steps, no CUDA graph")
     ap.add_argument("--cpu-budget-edges", type=int, default=400_000)
     ap.add_argument("--ref-budget-edges", type=int, default=400_000)
     args = ap.parse_args()

@@ -871,6 +871,35 @@ class Trainer:
         self.opt.step()
         return loss.detach(), logits.detach()
 
+    def capture(self, warmup=0, double_buffer=True):
+        """Record one training step (forward, backward, Adam) as a CUDA graph;
+        later step() calls replay it (one launch per epoch).  Call after at
+        least one eager step (schedules, workspaces and cuBLAS state exist);
+        capturing does not advance training, `warmup` extra side-stream steps
+        do.  With double_buffer a second graph reads a second input buffer, so
+        run_epochs can copy the next epoch's features while one computes."""
+        if warmup:
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                for _ in range(warmup):
+                    self._step_eager()
+            torch.cuda.current_stream().wait_stream(side)
+        bufs = [self.x] + ([torch.empty_like(self.x)] if double_buffer else [])
+        graphs = []
+        pool = None
+        for b in bufs:
+            self.x = b
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, pool=pool):
+                out = self._step_eager()
+            pool = graph.pool()
+            graphs.append((graph, out, b))
+        self.x = bufs[0]
+        self._graphs = graphs
+        self._graph, self._graph_out = graphs[0][0], graphs[0][1]
+        return graphs[0][0]
+
     def host_features(self, feats):
         """Pinned host copy of the features in the device storage layout
         (compute dtype, columns padded to the 8-aligned width)."""
@@ -884,10 +913,16 @@ class Trainer:
         """Train `epochs` epochs feeding the inputs from pinned host memory every
         epoch: the next epoch's host->device copy runs on a side stream while
         the current epoch computes (double-buffered), and the loss is read back
-        and checked every epoch like models.train.  Returns the losses."""
+        and checked every epoch like models.train.  Uses the captured graphs
+        when capture(double_buffer=True) was called.  Returns the losses."""
         cur_stream = torch.cuda.current_stream()
         copy_stream = torch.cuda.Stream()
-        bufs = [self.x, torch.empty_like(self.x)]
+        graphs = getattr(self, "_graphs", None)
+        if graphs is not None and len(graphs) == 2:
+            bufs = [graphs[0][2], graphs[1][2]]
+        else:
+            graphs = None
+            bufs = [self.x, torch.empty_like(self.x)]
         copied = [torch.cuda.Event(), torch.cuda.Event()]
         used = [torch.cuda.Event(), torch.cuda.Event()]
         copy_stream.wait_stream(cur_stream)
@@ -904,8 +939,12 @@ class Trainer:
                     bufs[nxt].copy_(host_x, non_blocking=True)
                     copied[nxt].record()
             cur_stream.wait_event(copied[cur])
-            self.x = bufs[cur]
-            loss, _ = self._step_eager()
+            if graphs is not None:
+                graphs[cur][0].replay()
+                loss = graphs[cur][1][0]
+            else:
+                self.x = bufs[cur]
+                loss, _ = self._step_eager()
             used[cur].record()
             if check_loss:
                 lv = float(loss)
@@ -914,24 +953,6 @@ class Trainer:
                 losses.append(lv)
         self.x = bufs[0]
         return losses
-
-    def capture(self, warmup=0):
-        """Record one training step (forward, backward, Adam) as a CUDA graph;
-        later step() calls replay it (one launch per epoch).  Call after at
-        least one eager step (schedules, workspaces and cuBLAS state exist);
-        capturing does not advance training, `warmup` extra side-stream steps
-        do.  Inputs stay at self.x (refresh with load_features(..., out=self.x))."""
-        side = torch.cuda.Stream()
-        side.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(side):
-            for _ in range(warmup):
-                self._step_eager()
-        torch.cuda.current_stream().wait_stream(side)
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            out = self._step_eager()
-        self._graph, self._graph_out = graph, out
-        return graph
 
 
 def train(g, features, labels, config: TrainConfig) -> TrainResult:

@@ -426,3 +426,19 @@ def test_synthetic_generators_shapes(cuda):
     assert torch.equal(r1.cols, r2.cols) and torch.equal(r1.offsets, r2.offsets)
     deg = np.diff(r1.offsets.cpu().numpy())
     assert deg.max() > 20 * max(1, int(np.median(deg)))  # power-law skew
+
+
+def test_run_epochs_with_graphs_matches_eager(cuda):
+    from paper_2411_01109_b200 import graphgen, models as M
+    from paper_2411_01109_b200.device import DeviceGraph
+
+    rows, cols, feats, labels = graphgen.synth_sbm(200, 2, 0.05, 0.005, 10, 5)
+    dg = DeviceGraph.from_edges(200, rows, cols)
+    cfg = M.TrainConfig(kind="gat", hidden=8, heads=2)
+    a = M.Trainer(M.GraphBundle.build(dg), feats, labels, cfg)
+    b = M.Trainer(M.GraphBundle.build(dg), feats, labels, cfg)
+    la = [float(a.step()[0]) for _ in range(7)]
+    lb = [float(b.step()[0])]
+    b.capture()
+    lb += b.run_epochs(b.host_features(feats), 6)
+    np.testing.assert_allclose(la, lb, rtol=0, atol=1e-6)
