@@ -144,6 +144,20 @@ struct FastOcc {
   static constexpr int value = NCH == 1 ? ((!WT && TEAM >= 8 && TEAM <= 16) ? 4 : 3) : (NCH == 2 ? 2 : 1);
 };
 
+// Column ids of one batch for a non-power-of-two team: lane tl holds the ids
+// of edges base + tl + q*TEAM (q < CPL, within the batch of EB).
+template <int CPL, int TEAM, int EB, bool FULL>
+__device__ __forceinline__ void load_batch_ids_strided(const int32_t* __restrict__ base_ptr,
+                                                       int base, int tl, int limit,
+                                                       int (&out)[CPL]) {
+#pragma unroll
+  for (int q = 0; q < CPL; ++q) {
+    const int j = tl + q * TEAM;
+    const int e = base + j;
+    out[q] = (j < EB && (FULL || (e >= 0 && e < limit))) ? __ldcs(base_ptr + e) : 0;
+  }
+}
+
 // Column ids of one batch: lane tl holds ids [base + tl*CPL, +CPL).  FULL
 // batches lie inside [0, num_edges) and use unguarded vector loads.
 template <int CPL, bool FULL>
@@ -169,10 +183,21 @@ __device__ __forceinline__ void load_batch_ids(const int32_t* __restrict__ base_
 }
 
 // Per-team state of k_spmm_fast: lane column offsets, accumulators, unit range.
+// Teams of TEAM lanes; TEAM need not be a power of two (e.g. 6 lanes for F=48:
+// five teams per warp, 30 of 32 lanes busy).  Power-of-two teams load
+// column ids as vectors (lane tl holds edges tl*CPL+q); other teams load
+// scalars (lane tl holds edges tl + q*TEAM).
+template <int TEAM>
+struct TeamShape {
+  static constexpr bool P2 = (TEAM & (TEAM - 1)) == 0;
+  static constexpr int TPW = 32 / TEAM;  // teams per warp
+};
+
 template <typename T, int V, int TEAM, int NCH, bool WEIGHTED>
 struct FastTeam {
+  static constexpr bool P2 = TeamShape<TEAM>::P2;
   static constexpr int EB = NCH >= 4 ? 4 : 8;             // edges gathered per batch
-  static constexpr int CPL = TEAM >= EB ? 1 : EB / TEAM;  // column ids per loading lane
+  static constexpr int CPL = P2 ? (TEAM >= EB ? 1 : EB / TEAM) : (EB + TEAM - 1) / TEAM;
   using Raw = typename RawVec<V * sizeof(T)>::type;
 
   const T* xl[NCH];
@@ -180,9 +205,26 @@ struct FastTeam {
   int chead[NCH];
   float acc[NCH][V];
   unsigned tmask;
+  int tbase;  // lane id of the team's first lane
   int beg, end, F, heads;
   const T* w;
   bool use_widx;
+
+  // Fetch the ids of batch [base, base+EB) into this lane's slots.
+  template <bool FULL>
+  __device__ __forceinline__ void load_ids_impl(const int32_t* __restrict__ p, int base, int tl,
+                                                int limit, int (&out)[CPL]) const {
+    if constexpr (P2) {
+      if (tl * CPL < EB) load_batch_ids<CPL, FULL>(p, base + tl * CPL, limit, out);
+    } else {
+      load_batch_ids_strided<CPL, TEAM, EB, FULL>(p, base, tl, limit, out);
+    }
+  }
+
+  __device__ __forceinline__ int shfl_id(const int (&ids)[CPL], int j) const {
+    if constexpr (P2) return __shfl_sync(tmask, ids[j % CPL], j / CPL, TEAM);
+    else return __shfl_sync(tmask, ids[j / TEAM], tbase + j % TEAM);
+  }
 
   // One batch of EB edges [b, b+EB): issue every gather, then accumulate.
   template <bool FULL>
@@ -192,9 +234,9 @@ struct FastTeam {
 #pragma unroll
     for (int j = 0; j < EB; ++j) {
       const bool ok = FULL || (b + j >= beg && b + j < end);
-      const int c = __shfl_sync(tmask, ids[j % CPL], j / CPL, TEAM);
+      const int c = shfl_id(ids, j);
       int wi = b + j;
-      if (WEIGHTED && use_widx) wi = __shfl_sync(tmask, wids[j % CPL], j / CPL, TEAM);
+      if (WEIGHTED && use_widx) wi = shfl_id(wids, j);
       const size_t roff = (size_t)(unsigned)c * (unsigned)F;
 #pragma unroll
       for (int k = 0; k < NCH; ++k) {
@@ -227,20 +269,25 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
   using Team = FastTeam<T, V, TEAM, NCH, WEIGHTED>;
   constexpr int EB = Team::EB;
   constexpr int CPL = Team::CPL;
+  constexpr bool P2 = Team::P2;
+  constexpr int TPW = TeamShape<TEAM>::TPW;
 
   const int lane = threadIdx.x & 31;
-  const int tl = lane & (TEAM - 1);
-  const int64_t team_id = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TEAM;
+  const int tidx = lane / TEAM;
+  if (tidx >= TPW) return;  // spare lanes of a non-power-of-two split
+  const int tl = lane - tidx * TEAM;
+  const int64_t team_id = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * TPW + tidx;
   if (team_id >= num_units) return;
 
   const int4 un = units[team_id];
   const int row = un.x, slot = un.w;
   const int nvec = F / V;
   const int limit = (int)num_edges;
-  const bool loader = tl * CPL < EB;  // lanes that fetch column ids
+  const bool loader = P2 ? tl * CPL < EB : tl < EB;  // lanes that fetch column ids
 
   Team t;
-  t.tmask = TEAM == 32 ? 0xffffffffu : (((1u << TEAM) - 1u) << (lane & ~(TEAM - 1)));
+  t.tbase = tidx * TEAM;
+  t.tmask = TEAM == 32 ? 0xffffffffu : (((1u << TEAM) - 1u) << t.tbase);
   t.beg = un.y;
   t.end = un.z;
   t.F = F;
@@ -263,21 +310,21 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
   int b = beg - ((beg + mis) & (EB - 1));
   if (b < beg) {  // partial head batch
     int ids[CPL] = {}, wids[CPL] = {};
-    if (loader) load_batch_ids<CPL, false>(cols, b + tl * CPL, limit, ids);
-    if (t.use_widx && loader) load_batch_ids<CPL, false>(widx, b + tl * CPL, limit, wids);
+    if (loader) t.template load_ids_impl<false>(cols, b, tl, limit, ids);
+    if (t.use_widx && loader) t.template load_ids_impl<false>(widx, b, tl, limit, wids);
     t.template batch<false>(b, ids, wids);
     b += EB;
   }
   if (b + EB <= end) {  // full batches, column ids prefetched one batch ahead
     int ids[CPL] = {}, wids[CPL] = {};
-    if (loader) load_batch_ids<CPL, true>(cols, b + tl * CPL, limit, ids);
-    if (t.use_widx && loader) load_batch_ids<CPL, true>(widx, b + tl * CPL, limit, wids);
+    if (loader) t.template load_ids_impl<true>(cols, b, tl, limit, ids);
+    if (t.use_widx && loader) t.template load_ids_impl<true>(widx, b, tl, limit, wids);
     for (;;) {
       const int nb = b + EB;
       const bool more = nb + EB <= end;
       int nids[CPL] = {}, nwids[CPL] = {};
-      if (more && loader) load_batch_ids<CPL, true>(cols, nb + tl * CPL, limit, nids);
-      if (more && t.use_widx && loader) load_batch_ids<CPL, true>(widx, nb + tl * CPL, limit, nwids);
+      if (more && loader) t.template load_ids_impl<true>(cols, nb, tl, limit, nids);
+      if (more && t.use_widx && loader) t.template load_ids_impl<true>(widx, nb, tl, limit, nwids);
       t.template batch<true>(b, ids, wids);
       b = nb;
       if (!more) break;
@@ -287,8 +334,8 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
   }
   if (b < end) {  // partial tail batch
     int ids[CPL] = {}, wids[CPL] = {};
-    if (loader) load_batch_ids<CPL, false>(cols, b + tl * CPL, limit, ids);
-    if (t.use_widx && loader) load_batch_ids<CPL, false>(widx, b + tl * CPL, limit, wids);
+    if (loader) t.template load_ids_impl<false>(cols, b, tl, limit, ids);
+    if (t.use_widx && loader) t.template load_ids_impl<false>(widx, b, tl, limit, wids);
     t.template batch<false>(b, ids, wids);
   }
 
@@ -362,10 +409,14 @@ struct FastArgs {
   cudaStream_t st;
 };
 
+template <int X> struct Pow2Up { static constexpr int value = X <= 1 ? 1 : 2 * Pow2Up<(X + 1) / 2>::value; };
+template <> struct Pow2Up<1> { static constexpr int value = 1; };
+
 template <typename T, int V, int TEAM, int NCH, bool WT>
 static int launch_fast(const FastArgs& a) {
   constexpr int kThreads = 256;
-  constexpr int teams_per_block = kThreads / TEAM;
+  constexpr int teams_per_block = (kThreads / 32) * TeamShape<TEAM>::TPW;
+  constexpr int TEAMF = Pow2Up<TEAM>::value;  // follow-up pass: power-of-two teams
   if (a.num_units > 0) {
     int64_t blocks = (a.num_units + teams_per_block - 1) / teams_per_block;
     k_spmm_fast<T, V, TEAM, NCH, WT><<<(unsigned)blocks, kThreads, 0, a.st>>>(
@@ -374,8 +425,8 @@ static int launch_fast(const FastArgs& a) {
     HG_LAUNCHED();
   }
   if (a.num_split > 0) {
-    int64_t blocks = (a.num_split + teams_per_block - 1) / teams_per_block;
-    k_spmm_fast_followup<T, V, TEAM, NCH><<<(unsigned)blocks, kThreads, 0, a.st>>>(
+    int64_t blocks = (a.num_split + kThreads / TEAMF - 1) / (kThreads / TEAMF);
+    k_spmm_fast_followup<T, V, TEAMF, NCH><<<(unsigned)blocks, kThreads, 0, a.st>>>(
         a.split_rows, a.num_split, a.carry, (T*)a.y, a.F, a.fmode, (const T*)a.fout);
     HG_LAUNCHED();
   }
@@ -385,6 +436,17 @@ static int launch_fast(const FastArgs& a) {
 template <typename T, int V, bool WT>
 static int dispatch_layout(const FastArgs& a) {
   const int nvec = a.F / V;
+  if constexpr (V * sizeof(T) == 16) {  // exact-width teams for common odd chunk counts
+    switch (nvec) {
+      case 3: return launch_fast<T, V, 3, 1, WT>(a);
+      case 5: return launch_fast<T, V, 5, 1, WT>(a);
+      case 6: return launch_fast<T, V, 6, 1, WT>(a);
+      case 7: return launch_fast<T, V, 7, 1, WT>(a);
+      case 12: return launch_fast<T, V, 12, 1, WT>(a);
+      case 24: return launch_fast<T, V, 24, 1, WT>(a);
+      default: break;
+    }
+  }
   if (nvec <= 1) return launch_fast<T, V, 1, 1, WT>(a);
   if (nvec <= 2) return launch_fast<T, V, 2, 1, WT>(a);
   if (nvec <= 4) return launch_fast<T, V, 4, 1, WT>(a);

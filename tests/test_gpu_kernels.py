@@ -202,7 +202,7 @@ def _check_tol(got, want, label):
     assert not bad.any(), f"{label}: {bad.sum()} entries outside tolerance, max err {err.max()}"
 
 
-@pytest.mark.parametrize("f", [2, 6, 8, 16, 42, 48, 64, 128, 256, 512, 1024])
+@pytest.mark.parametrize("f", [2, 6, 8, 16, 24, 40, 42, 48, 56, 64, 96, 128, 192, 256, 512, 1024])
 @pytest.mark.parametrize("scaling,norm", [("post", "none"), ("discretized", "both"),
                                           ("pre", "left"), ("post", "right")])
 def test_spmm_fast_vs_f64(cuda, f, scaling, norm):
