@@ -330,7 +330,7 @@ def b200_arm(args, ws, rank, local):
     t_setup = time.time()
     dg, x, labels = build_workload(args.workload, args.seed)
     cfg = TrainConfig(mode="half", seed=args.seed, scaling="discretized", norm="both",
-                      numerics="fast", **WORKLOADS[args.workload]["cfg"])
+                      numerics="fast", grad_scale="auto", **WORKLOADS[args.workload]["cfg"])
     if ws > 1:
         from paper_2411_01109_b200.partition import DistTrainer
 
@@ -427,6 +427,7 @@ def b200_arm(args, ws, rank, local):
                          "peak_source": peak_kind,
                          "bytes_model": "4E+8(N+1)+2FE+2FN per SpMM launch, F = stored width"},
             "final_loss": round(final_loss, 5),
+            "grad_scale": (tr.inner if ws > 1 else tr).grad_scale,
             "setup_s": round(setup_s, 1),
         }
     if not args.no_sweep and ws == 1 and args.workload == "gcn-reddit":

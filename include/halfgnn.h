@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define HG_ABI_VERSION 1
+#define HG_ABI_VERSION 2
 
 enum { HG_OK = 0, HG_EINVAL = 1, HG_ECUDA = 2 };
 enum { HG_F16 = 0, HG_F32 = 1 };
@@ -186,12 +186,17 @@ int hg_edge_rowsum(const int64_t* offsets, int64_t n_rows, int64_t num_edges,
 
 /* ------------------------------------------------------------------- loss */
 
-/* cross_entropy forward + backward in one pass (models.py:552-572), fp64 math:
- * per row i, z = logits[i, :c_active] - max, nll[i] = log(sum exp z) - z[label],
- * grad[i, j] = (softmax(z)_j - [j == label]) / denom for j < c_active, 0 for
- * c_active <= j < ld (storage padding).  Loss = sum(nll) / denom. */
-int hg_softmax_xent(const float* logits, int64_t ld, const int64_t* labels, int64_t n,
-                    int32_t c_active, double denom, float* grad, double* nll, void* stream);
+/* convert(logits, "float32") + cross_entropy forward + backward + convert's
+ * backward in one pass (models.py:203-217, 552-572), fp64 math: per row i,
+ * z = logits[i, :c_active] - max (logits widened exactly from logits_dtype),
+ * nll[i] = log(sum exp z) - z[label], and
+ * grad[i, j] = rnd_g(fp32((softmax(z)_j - [j == label]) / denom) * grad_scale)
+ * for j < c_active, 0 for c_active <= j < ld (storage padding); rnd_g rounds to
+ * grad_dtype (fp16 = convert's backward).  grad_scale: 1, or a power of two (a
+ * static loss scale, exact).  Loss = sum(nll) / denom. */
+int hg_softmax_xent(const void* logits, int logits_dtype, int64_t ld, const int64_t* labels,
+                    int64_t n, int32_t c_active, double denom, float grad_scale, void* grad,
+                    int grad_dtype, double* nll, void* stream);
 
 /* GAT attention projections (models.py:503-506, s_l = z a_l, s_r = z a_r) for all
  * heads at once: s_l[n*H+h] = rnd(sum_f z[n, h*fh+f] * a_l[h*fh+f]) (fp32
@@ -213,10 +218,11 @@ int hg_head_dots_bwd(const void* z, const void* a_l, const void* a_r, const void
  *   m += omb1*(g-m); v += omb2*(g*g-v); p -= lr*(m/c1) / (sqrt(v/c2) + eps),
  *   c1 = fp32(1 - b1^t), c2 = fp32(1 - b2^t) with t = *step (device fp64).
  * omb1/omb2 are fp32(1 - b1) / fp32(1 - b2) formed in double by the caller.
- * g is read from `grad` (dtype) and widened. */
+ * g is read from `grad` (dtype), widened and multiplied by grad_unscale (1 for
+ * the reference; 2^-k undoes a static power-of-two loss scale exactly). */
 int hg_adam_step(float* master, float* m, float* v, const void* grad, int grad_dtype,
                  int64_t count, float lr, float omb1, float omb2, double b1, double b2,
-                 float eps, const double* step, void* stream);
+                 float eps, const double* step, float grad_unscale, void* stream);
 
 /* ---------------------------------------------------------------- elementwise */
 
@@ -224,6 +230,18 @@ int hg_adam_step(float* master, float* m, float* v, const void* grad, int grad_d
  * fp16/fp32 values by Python floats in float64: leaky_relu slope,
  * scale_combine lam, models.py:188-240). */
 int hg_scale_f64(const void* x, double s, void* out, int64_t count, int dtype, void* stream);
+
+/* models.add_bias (models.py:161-166) fused with the SpMM's left-norm input
+ * scaling (kernels.py:358-361): out[r, f] = rnd(rnd(x[r, f] + bias[f]) * row_scale[r]).
+ * bias and row_scale may each be NULL (step skipped).  x, out: [rows, F]. */
+int hg_bias_scale_rows(const void* x, const void* bias, const void* row_scale, int64_t rows,
+                       int32_t F, void* out, int dtype, void* stream);
+
+/* add_bias backward (models.py:168-170): out[f] = rnd(sum_r x[r, f]), fp32
+ * accumulation in a fixed (deterministic) order. */
+int hg_col_sums_workspace(int64_t rows, int32_t F, size_t* bytes);
+int hg_col_sums(const void* x, int64_t rows, int32_t F, void* out, int dtype, void* ws,
+                size_t ws_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -15,6 +15,7 @@ from pathlib import Path
 LIB_PATH = Path(__file__).resolve().with_name("libhalfgnn.so")
 
 HG_OK, HG_EINVAL, HG_ECUDA = 0, 1, 2
+ABI_VERSION = 2
 HG_F16, HG_F32 = 0, 1
 SCALING_CODES = {"post": 0, "pre": 1, "discretized": 2}
 FACTOR_INV, FACTOR_INV_SQRT = 1, 2
@@ -51,13 +52,16 @@ SIGNATURES = {
     "hg_edge_softmax_bwd": [_P, _I64, _I64, _P, _P, _P, _I32, _P, _I64, _I64, c_int, _P],
     "hg_edge_rowsum": [_P, _I64, _I64, _P, _P, _I32, _P, _P, _I64, _I64, c_int, _P],
     "hg_scale_f64": [_P, c_double, _P, _I64, c_int, _P],
-    "hg_softmax_xent": [_P, _I64, _P, _I64, _I32, c_double, _P, _P, _P],
+    "hg_softmax_xent": [_P, c_int, _I64, _P, _I64, _I32, c_double, c_float, _P, c_int, _P, _P],
     "hg_head_dots": [_P, _P, _P, _I64, _I32, _I32, _P, _P, c_int, _P],
     "hg_head_dots_bwd_workspace": [_I32, _I32, _PSZ],
     "hg_head_dots_bwd": [_P, _P, _P, _P, _P, _I64, _I32, _I32, _P, _P, _P, c_int, _P, c_size_t,
                          _P],
+    "hg_bias_scale_rows": [_P, _P, _P, _I64, _I32, _P, c_int, _P],
+    "hg_col_sums_workspace": [_I64, _I32, _PSZ],
+    "hg_col_sums": [_P, _I64, _I32, _P, c_int, _P, c_size_t, _P],
     "hg_adam_step": [_P, _P, _P, _P, c_int, _I64, c_float, c_float, c_float, c_double, c_double,
-                     c_float, _P, _P],
+                     c_float, _P, c_float, _P],
 }
 _RESTYPES = {"hg_last_error": c_char_p}
 
@@ -81,7 +85,7 @@ def lib():
             fn = getattr(handle, name)
             fn.argtypes = argtypes
             fn.restype = _RESTYPES.get(name, c_int)
-        if handle.hg_abi_version() != 1:
+        if handle.hg_abi_version() != ABI_VERSION:
             raise NativeLibraryMissing("libhalfgnn.so ABI version mismatch")
         _lib = handle
     return _lib

@@ -893,47 +893,119 @@ extern "C" int hg_scale_f64(const void* x, double s, void* out, int64_t count, i
 
 namespace hg {
 
-// Warp per row; lanes stride the class columns.  fp64 like the reference.
+// Warp per row; lane j holds classes j, j+32, ... (K per lane in registers,
+// one fp64 exp per class).  fp64 like the reference; logits are read in their
+// storage type (fp16 widens exactly, as models.convert does) and the gradient
+// is rounded to fp32 first (the reference's float32 grad), scaled by an exact
+// power of two, then to the gradient type (convert's backward rounding).
+template <typename L, typename G, int K>
 __global__ void __launch_bounds__(256)
-k_softmax_xent(const float* __restrict__ logits, int64_t ld, const int64_t* __restrict__ labels,
-               int64_t n, int c_active, double denom, float* __restrict__ grad,
+k_softmax_xent(const L* __restrict__ logits, int64_t ld, const int64_t* __restrict__ labels,
+               int64_t n, int c_active, double denom, float scale, G* __restrict__ grad,
                double* __restrict__ nll) {
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n;
        r += nwarps) {
-    const float* z = logits + r * ld;
+    const L* z = logits + r * ld;
+    double zv[K];
     double m = -INFINITY;
-    for (int j = lane; j < c_active; j += 32) m = fmax(m, (double)z[j]);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int j = lane + 32 * k;
+      zv[k] = j < c_active ? (double)Num<L>::to_f(z[j]) : -INFINITY;
+      m = fmax(m, zv[k]);
+    }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
     double se = 0.0;
-    for (int j = lane; j < c_active; j += 32) se += exp((double)z[j] - m);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      zv[k] = lane + 32 * k < c_active ? exp(zv[k] - m) : 0.0;
+      se += zv[k];
+    }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
     const int64_t lab = labels[r];
-    float* g = grad + r * ld;
+    G* g = grad + r * ld;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int j = lane + 32 * k;
+      if (j < ld) {
+        float v = 0.0f;
+        if (j < c_active) v = (float)((zv[k] / se - (j == lab ? 1.0 : 0.0)) / denom) * scale;
+        g[j] = Num<G>::from_f(v);
+      }
+    }
+    if (lane == 0) nll[r] = log(se) - ((double)Num<L>::to_f(z[lab]) - m);
+  }
+}
+
+// Classes beyond 32*K: recompute the exponentials (same operations).
+template <typename L, typename G>
+__global__ void __launch_bounds__(256)
+k_softmax_xent_wide(const L* __restrict__ logits, int64_t ld, const int64_t* __restrict__ labels,
+                    int64_t n, int c_active, double denom, float scale, G* __restrict__ grad,
+                    double* __restrict__ nll) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n;
+       r += nwarps) {
+    const L* z = logits + r * ld;
+    double m = -INFINITY;
+    for (int j = lane; j < c_active; j += 32) m = fmax(m, (double)Num<L>::to_f(z[j]));
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    double se = 0.0;
+    for (int j = lane; j < c_active; j += 32) se += exp((double)Num<L>::to_f(z[j]) - m);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+    const int64_t lab = labels[r];
+    G* g = grad + r * ld;
     for (int j = lane; j < ld; j += 32) {
       float v = 0.0f;
       if (j < c_active) {
-        const double p = exp((double)z[j] - m) / se;
-        v = (float)((p - (j == lab ? 1.0 : 0.0)) / denom);
+        const double p = exp((double)Num<L>::to_f(z[j]) - m) / se;
+        v = (float)((p - (j == lab ? 1.0 : 0.0)) / denom) * scale;
       }
-      g[j] = v;
+      g[j] = Num<G>::from_f(v);
     }
-    if (lane == 0) nll[r] = log(se) - ((double)z[lab] - m);
+    if (lane == 0) nll[r] = log(se) - ((double)Num<L>::to_f(z[lab]) - m);
   }
+}
+
+template <typename L, typename G>
+static void launch_xent(const void* logits, int64_t ld, const int64_t* labels, int64_t n,
+                        int c, double denom, float scale, void* grad, double* nll,
+                        cudaStream_t st) {
+  const int g = grid_for(n, 8, 148 * 64);
+  const L* lp = (const L*)logits;
+  G* gp = (G*)grad;
+  const int64_t w = ld > c ? ld : c;
+  if (w <= 32) k_softmax_xent<L, G, 1><<<g, 256, 0, st>>>(lp, ld, labels, n, c, denom, scale, gp, nll);
+  else if (w <= 64) k_softmax_xent<L, G, 2><<<g, 256, 0, st>>>(lp, ld, labels, n, c, denom, scale, gp, nll);
+  else if (w <= 128) k_softmax_xent<L, G, 4><<<g, 256, 0, st>>>(lp, ld, labels, n, c, denom, scale, gp, nll);
+  else k_softmax_xent_wide<L, G><<<g, 256, 0, st>>>(lp, ld, labels, n, c, denom, scale, gp, nll);
 }
 
 }  // namespace hg
 
-extern "C" int hg_softmax_xent(const float* logits, int64_t ld, const int64_t* labels, int64_t n,
-                               int32_t c_active, double denom, float* grad, double* nll,
+extern "C" int hg_softmax_xent(const void* logits, int logits_dtype, int64_t ld,
+                               const int64_t* labels, int64_t n, int32_t c_active, double denom,
+                               float grad_scale, void* grad, int grad_dtype, double* nll,
                                void* stream) {
   HG_REQUIRE(c_active >= 1 && c_active <= ld, "hg_softmax_xent: bad class counts");
+  HG_REQUIRE((logits_dtype == HG_F16 || logits_dtype == HG_F32) &&
+             (grad_dtype == HG_F16 || grad_dtype == HG_F32), "hg_softmax_xent: unknown dtype");
   if (n == 0) return HG_OK;
-  k_softmax_xent<<<grid_for(n, 8, 148 * 64), 256, 0, as_stream(stream)>>>(
-      logits, ld, labels, n, c_active, denom, grad, nll);
+  cudaStream_t st = as_stream(stream);
+  if (logits_dtype == HG_F16) {
+    if (grad_dtype == HG_F16) launch_xent<__half, __half>(logits, ld, labels, n, c_active, denom, grad_scale, grad, nll, st);
+    else launch_xent<__half, float>(logits, ld, labels, n, c_active, denom, grad_scale, grad, nll, st);
+  } else {
+    if (grad_dtype == HG_F16) launch_xent<float, __half>(logits, ld, labels, n, c_active, denom, grad_scale, grad, nll, st);
+    else launch_xent<float, float>(logits, ld, labels, n, c_active, denom, grad_scale, grad, nll, st);
+  }
   HG_LAUNCHED();
   return HG_OK;
 }
@@ -1049,12 +1121,12 @@ template <typename G>
 __global__ void k_adam(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
                        const G* __restrict__ grad, int64_t count, float lr, float omb1,
                        float omb2, double b1, double b2, float eps,
-                       const double* __restrict__ step) {
+                       const double* __restrict__ step, float unscale) {
   const double t = *step;
   const float c1 = (float)(1.0 - pow(b1, t)), c2 = (float)(1.0 - pow(b2, t));
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const float g = Num<G>::to_f(grad[i]);
+    const float g = __fmul_rn(Num<G>::to_f(grad[i]), unscale);
     float mi = m[i], vi = v[i];
     mi = __fadd_rn(mi, __fmul_rn(omb1, __fsub_rn(g, mi)));
     vi = __fadd_rn(vi, __fmul_rn(omb2, __fsub_rn(__fmul_rn(g, g), vi)));
@@ -1103,17 +1175,18 @@ extern "C" int hg_head_dots(const void* z, const void* a_l, const void* a_r, int
 
 extern "C" int hg_adam_step(float* master, float* m, float* v, const void* grad, int grad_dtype,
                             int64_t count, float lr, float omb1, float omb2, double b1, double b2,
-                            float eps, const double* step, void* stream) {
+                            float eps, const double* step, float grad_unscale,
+                            void* stream) {
   HG_REQUIRE(grad_dtype == HG_F16 || grad_dtype == HG_F32, "unknown dtype %d", grad_dtype);
   if (count == 0) return HG_OK;
   cudaStream_t st = as_stream(stream);
   const int g = grid_for(count, 256, 148 * 8);
   if (grad_dtype == HG_F16)
     k_adam<__half><<<g, 256, 0, st>>>(master, m, v, (const __half*)grad, count, lr, omb1, omb2,
-                                      b1, b2, eps, step);
+                                      b1, b2, eps, step, grad_unscale);
   else
     k_adam<float><<<g, 256, 0, st>>>(master, m, v, (const float*)grad, count, lr, omb1, omb2,
-                                     b1, b2, eps, step);
+                                     b1, b2, eps, step, grad_unscale);
   HG_LAUNCHED();
   return HG_OK;
 }

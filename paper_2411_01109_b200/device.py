@@ -471,6 +471,38 @@ def edge_rowsum(dg: DeviceGraph, v, transpose=False):
     return rowsum_view(view, v, view.perm if transpose else None)
 
 
+def bias_scale_rows(x, bias=None, row_scale=None, out=None):
+    """rnd(rnd(x + bias[None, :]) * row_scale[:, None]) (hg_bias_scale_rows);
+    either operand may be None."""
+    _require_cuda(x)
+    x = x.contiguous()
+    rows, f = x.shape
+    for t in (bias, row_scale):
+        if t is not None and t.dtype != x.dtype:
+            raise ValueError("bias / row scale must match the feature dtype")
+    if out is None:
+        out = torch.empty_like(x)
+    nat.call("hg_bias_scale_rows", _p(x), _p(None if bias is None else bias.contiguous()),
+             _p(None if row_scale is None else row_scale.contiguous()), rows, f, _p(out),
+             _dtype_code(x), _stream())
+    Probe.launches += 1
+    return out
+
+
+def col_sums(x):
+    """rnd(sum over rows) per column, fp32 accumulation (hg_col_sums)."""
+    _require_cuda(x)
+    x = x.contiguous()
+    rows, f = x.shape
+    out = torch.empty(f, dtype=x.dtype, device=x.device)
+    nbytes = nat.size_query("hg_col_sums_workspace", rows, f)
+    ws = workspace(nbytes, x.device)
+    nat.call("hg_col_sums", _p(x), rows, f, _p(out), _dtype_code(x), _p(ws), ws.numel(),
+             _stream())
+    Probe.launches += 2
+    return out
+
+
 def scale_f64(x, s: float):
     """rnd(x * s) with the product formed in float64."""
     x = x.contiguous()
@@ -480,14 +512,16 @@ def scale_f64(x, s: float):
     return out
 
 
-def softmax_xent(logits, labels, c_active, denom):
-    """Fused fp64 softmax cross-entropy: returns (nll [N] f64, grad [N, ld] f32)."""
+def softmax_xent(logits, labels, c_active, denom, scale=1.0, grad_dtype=None):
+    """Fused fp64 softmax cross-entropy on fp16 or fp32 logits: returns
+    (nll [N] f64, grad [N, ld] of grad_dtype (default the logits' dtype)),
+    grad = rnd(fp32((p - y) / denom) * scale)."""
     logits = logits.contiguous()
     n, ld = logits.shape
-    grad = torch.empty_like(logits)
+    grad = torch.empty((n, ld), dtype=grad_dtype or logits.dtype, device=logits.device)
     nll = torch.empty(n, dtype=torch.float64, device=logits.device)
-    nat.call("hg_softmax_xent", _p(logits), ld, _p(labels), n, c_active, float(denom), _p(grad),
-             _p(nll), _stream())
+    nat.call("hg_softmax_xent", _p(logits), _dtype_code(logits), ld, _p(labels), n, c_active,
+             float(denom), float(scale), _p(grad), _dtype_code(grad), _p(nll), _stream())
     Probe.launches += 1
     return nll, grad
 
@@ -505,12 +539,13 @@ def head_dots(z, a_l, a_r, heads):
     return s_l, s_r
 
 
-def adam_step(master, m, v, grad, lr, b1, b2, eps, step):
+def adam_step(master, m, v, grad, lr, b1, b2, eps, step, grad_unscale=1.0):
     """One fused Adam update over flat fp32 arrays (hg_adam_step); `step` is the
-    device fp64 step count (already incremented)."""
+    device fp64 step count (already incremented); the gradient is multiplied by
+    grad_unscale (exact for a power of two) before use."""
     nat.call("hg_adam_step", _p(master), _p(m), _p(v), _p(grad), _dtype_code(grad),
              master.numel(), float(lr), float(1 - b1), float(1 - b2), float(b1), float(b2),
-             float(eps), _p(step), _stream())
+             float(eps), _p(step), float(grad_unscale), _stream())
     Probe.launches += 1
 
 

@@ -154,6 +154,18 @@ class GraphBundle:
                                 self.warp_chunk, self.warps_per_cta) for h in range(heads)]
         return torch.cat(outs, dim=1)
 
+    @property
+    def fused_bias_agg(self):
+        """GCN layers may fuse add_bias into the aggregation's input pass."""
+        return self.numerics == "fast"
+
+    def bias_spmm(self, h, b, scaling, norm):
+        """spmm(add_bias(h, b)) with the bias add and the left-norm input
+        scaling in one pass (hg_bias_scale_rows), then the gather kernel."""
+        fin, fout = self.dg.norm_tables(norm, False, h.dtype)
+        xs = D.bias_scale_rows(h, b, fin)
+        return D.spmm_csr(self.dg.view(False), xs, None, None, 1, scaling, None, fout)
+
     def sddmm(self, x, y, heads=1):
         return D.sddmm(self.dg, x, y, heads=heads)
 
@@ -210,6 +222,23 @@ class _AggFn(torch.autograd.Function):
         r = ctx.reduction
         gx = ctx.bundle.spmm(g.contiguous(), None, r.scaling, _MIRROR[r.norm], transpose=True)
         return gx, None, None
+
+
+class _BiasAggFn(torch.autograd.Function):
+    """spmm_agg(add_bias(h, b)) (models.py:161-173, 274-290) as one op: the
+    forward fuses the bias add into the SpMM input pass; the backward is the
+    mirrored-norm transposed SpMM, and the bias gradient is its column sum."""
+
+    @staticmethod
+    def forward(ctx, h, b, bundle, reduction):
+        ctx.bundle, ctx.reduction = bundle, reduction
+        return bundle.bias_spmm(h, b, reduction.scaling, reduction.norm)
+
+    @staticmethod
+    def backward(ctx, g):
+        r = ctx.reduction
+        gh = ctx.bundle.spmm(g.contiguous(), None, r.scaling, _MIRROR[r.norm], transpose=True)
+        return gh, D.col_sums(gh), None, None
 
 
 def spmm_agg(bundle, x, reduction, width="half2", overflow=None, tag="agg"):
@@ -522,6 +551,12 @@ class GCNLayer:
         return self.lin.params()
 
     def __call__(self, bundle, x, mode, width, overflow, tag):
+        if getattr(bundle, "fused_bias_agg", False) and self.lin.b is not None:
+            h = matmul(x, self.lin.w.publish(mode))
+            y = _BiasAggFn.apply(h, self.lin.b.publish(mode), bundle, self.reduction)
+            if overflow is not None:
+                overflow.observe(tag, y.detach())
+            return y
         return spmm_agg(bundle, self.lin(x, mode), self.reduction, width, overflow, tag)
 
 
@@ -710,9 +745,11 @@ class Adam:
     lives on the device (fp64) so a step can be captured in a CUDA graph; with
     a ParamGroup the update is one fused kernel over the flat buffers."""
 
-    def __init__(self, params, lr=1e-2, betas=(0.9, 0.999), eps=1e-8, group=None):
+    def __init__(self, params, lr=1e-2, betas=(0.9, 0.999), eps=1e-8, group=None,
+                 grad_unscale=1.0):
         self.params = list(params)
         self.lr, self.betas, self.eps = lr, betas, eps
+        self.grad_unscale = float(grad_unscale)
         self.group = group
         if group is not None:
             self.m = torch.zeros_like(group.master)
@@ -733,7 +770,8 @@ class Adam:
         g = self.group
         if g is not None and g.master.is_cuda and (flat_grad is not None or g.check_grads()):
             grad = g.grad if flat_grad is None else flat_grad
-            D.adam_step(g.master, self.m, self.v, grad, self.lr, b1, b2, self.eps, self._t)
+            D.adam_step(g.master, self.m, self.v, grad, self.lr, b1, b2, self.eps, self._t,
+                        self.grad_unscale)
             return
         if flat_grad is not None:
             for o, p in zip(_offsets(self.params), self.params):
@@ -746,6 +784,8 @@ class Adam:
                                        for o, p in zip(_offsets(self.params), self.params)]
         for p, m, v in zip(self.params, ms, vs):
             grad = p.grad32().reshape(m.shape)
+            if self.grad_unscale != 1.0:
+                grad = grad * self.grad_unscale
             m.add_((1 - b1) * (grad - m))
             v.add_((1 - b2) * (grad * grad - v))
             p.master.sub_((self.lr * (m / c1) / (torch.sqrt(v / c2) + self.eps)).view(p.master.shape))
@@ -774,6 +814,11 @@ class TrainConfig:
     val_fraction: float = 0.2
     # builder extensions
     numerics: str = "fast"
+    # static power-of-two loss scale (1 = the reference; "auto" = the largest
+    # power of two <= N/64).  The reference's mean-over-N loss gradient
+    # (p - y)/N lands in fp16 subnormals for N ~ 1e5 (models.py:566-570);
+    # scaling it by 2^k keeps it normal and Adam unscales exactly in fp32.
+    grad_scale: float | str = 1.0
     heads: int = 1
     layers: int = 2
     device: str = "cuda"
@@ -808,6 +853,16 @@ def accuracy(logits, labels, mask, n_active=None):
     return float((pred == labels[mask]).mean())
 
 
+def resolve_grad_scale(spec, n):
+    """grad_scale value: a power of two >= 1, or "auto" -> largest 2^k <= n/64."""
+    if spec == "auto":
+        return float(2 ** max(0, int(math.floor(math.log2(max(n, 1) / 64.0)))))
+    s = float(spec)
+    if s < 1.0 or math.frexp(s)[0] != 0.5:
+        raise ValueError(f"grad_scale must be a power of two >= 1 or 'auto', got {spec!r}")
+    return s
+
+
 class Trainer:
     """Full-batch node classification state (models.train, models.py:633-684):
     model, optimiser, masks and device-resident inputs.  `step()` is one epoch
@@ -830,7 +885,9 @@ class Trainer:
         self.model = Model(config.kind, rng, (fan_in, config.hidden, self.n_cls), red,
                            config.lam, config.heads, config.layers, dev, self.in_store)
         self.group = ParamGroup(self.model.params(), config.mode)
-        self.opt = Adam(self.model.params(), lr=config.lr, group=self.group)
+        self.grad_scale = resolve_grad_scale(config.grad_scale, n)
+        self.opt = Adam(self.model.params(), lr=config.lr, group=self.group,
+                        grad_unscale=1.0 / self.grad_scale)
         perm = rng.permutation(n)
         val = np.zeros(n, dtype=bool)
         val[perm[: int(n * config.val_fraction)]] = True
@@ -864,12 +921,24 @@ class Trainer:
         cfg = self.cfg
         self.group.publish()
         logits = self.model.forward(self.bundle, self.x, cfg.mode, cfg.width, overflow)
-        if cfg.mode == "half":
-            logits = convert(logits, "float32", self.conversions)
-        loss = cross_entropy(logits, self.labels, self.n_cls)
-        loss.backward()
+        loss = self.loss_backward(logits, D.softmax_xent, logits.shape[0])
         self.opt.step()
-        return loss.detach(), logits.detach()
+        return loss, logits.detach()
+
+    def loss_backward(self, logits, xent, denom):
+        """convert(logits, "float32") -> cross_entropy -> backward, fused: one
+        kernel reads the compute-dtype logits, returns the per-row nll and the
+        loss gradient already in the logits' dtype (the rounding convert's
+        backward applies), scaled by grad_scale; autograd continues from the
+        logits.  Counts the two conversions the reference performs."""
+        nll, grad = xent(logits.detach(), self.labels, self.n_cls, denom,
+                         scale=self.grad_scale, grad_dtype=logits.dtype)
+        if self.cfg.mode == "half":
+            self.conversions.forward += 1
+            self.conversions.backward += 1
+        loss = (nll.sum() / denom).float()
+        torch.autograd.backward(logits, grad)
+        return loss
 
     def capture(self, warmup=0, double_buffer=True):
         """Record one training step (forward, backward, Adam) as a CUDA graph;
@@ -982,4 +1051,6 @@ def train(g, features, labels, config: TrainConfig) -> TrainResult:
         n_inf, n_nan = overflow.totals()
         losses.append(lv)
         trace.append([epoch, lv, train_acc, val_acc, n_inf, n_nan])
+    if logits is not None:
+        logits = logits.float()  # the fp32 logits the reference's convert produced
     return TrainResult(train_acc, val_acc, losses, trace, tr.conversions, overflow, logits)

@@ -159,8 +159,8 @@ class CudaOps:
         return D.softmax_bwd_view(view, alpha, g)
 
     @staticmethod
-    def xent(logits, labels, n_active, denom):
-        return D.softmax_xent(logits, labels, n_active, denom)
+    def xent(logits, labels, n_active, denom, scale=1.0, grad_dtype=None):
+        return D.softmax_xent(logits, labels, n_active, denom, scale, grad_dtype)
 
     @staticmethod
     def head_dots(z, a_l, a_r, heads):
@@ -291,17 +291,11 @@ class DistTrainer:
         return self.inner.load_features(feats[lo:hi], out=self.inner.x)
 
     def step(self, overflow=None):
-        from .models import convert, cross_entropy
-
         tr = self.inner
         cfg = tr.cfg
         tr.group.publish()
         logits = tr.model.forward(self.bundle, tr.x, cfg.mode, cfg.width, overflow)
-        if cfg.mode == "half":
-            logits = convert(logits, "float32", tr.conversions)
-        loss = cross_entropy(logits, tr.labels, tr.n_cls, denom=self.n_total,
-                             impl=self.bundle.ops.xent)
-        loss.backward()
+        loss = tr.loss_backward(logits, self.bundle.ops.xent, self.n_total)
         if not tr.group.check_grads():
             raise RuntimeError("autograd did not accumulate into the flat gradient buffer")
         # data-parallel sum of the weight gradients: one fp32 all-reduce of the

@@ -48,7 +48,7 @@ class HostOps:
         return (s * fout.double()[:, None]).to(x.dtype)
 
 
-def _host_xent(logits, labels, n_active, denom):
+def _host_xent(logits, labels, n_active, denom, scale=1.0, grad_dtype=None):
     z = logits[:, :n_active].double()
     z = z - z.max(dim=1, keepdim=True).values
     ez = torch.exp(z)
@@ -56,8 +56,8 @@ def _host_xent(logits, labels, n_active, denom):
     nll = torch.log(se) - z.gather(1, labels[:, None])[:, 0]
     g = ez / se[:, None]
     g[torch.arange(z.shape[0]), labels] -= 1.0
-    grad = torch.zeros_like(logits)
-    grad[:, :n_active] = (g / denom).float()
+    grad = torch.zeros(logits.shape, dtype=grad_dtype or logits.dtype)
+    grad[:, :n_active] = ((g / denom).float() * scale).to(grad.dtype)
     return nll, grad
 
 

@@ -415,3 +415,78 @@ def test_head_dots_fwd_bwd(cuda, heads, fh):
     np.testing.assert_allclose(ga_l.cpu().numpy().astype(np.float64), want_ga, rtol=3e-3, atol=0.1)
     a1 = D.head_dots_bwd(zt, alt, art, _t(g_l, cuda), _t(g_r, cuda), heads)
     assert torch.equal(a1[1], ga_l) and torch.equal(a1[2], ga_r)  # deterministic
+
+
+# ── dense-side helpers (GCN epilogue, loss) ──────────────────────────────
+
+
+@pytest.mark.parametrize("dtype", [np.float16, np.float32])
+@pytest.mark.parametrize("f", [6, 8, 48, 64, 602])
+def test_bias_scale_rows_bits(cuda, dtype, f):
+    """rnd(rnd(x + b) * s): add_bias (models.py:161-166) then the left-norm
+    input scaling (kernels.py:358-361), each an fp64 op rounded once."""
+    from paper_2411_01109_b200 import device as D
+
+    rng = np.random.default_rng(f)
+    n = 1537
+    x = rng.normal(0, 30, (n, f)).astype(dtype)
+    b = rng.normal(0, 3, f).astype(dtype)
+    s = rng.uniform(0, 1, n).astype(dtype)
+    s[::7] = 0
+    step1 = (x.astype(np.float64) + b.astype(np.float64)).astype(dtype)
+    want = (step1.astype(np.float64) * s.astype(np.float64)[:, None]).astype(dtype)
+    got = D.bias_scale_rows(_t(x, cuda), _t(b, cuda), _t(s, cuda)).cpu().numpy()
+    np.testing.assert_array_equal(bits(got), bits(want))
+    only_b = D.bias_scale_rows(_t(x, cuda), _t(b, cuda), None).cpu().numpy()
+    np.testing.assert_array_equal(bits(only_b), bits(step1))
+
+
+@pytest.mark.parametrize("dtype", [np.float16, np.float32])
+@pytest.mark.parametrize("n,f", [(0, 8), (1, 8), (1000, 6), (233_000, 64), (50_000, 48),
+                                 (3000, 4096)])
+def test_col_sums(cuda, dtype, n, f):
+    """add_bias backward: fp32 column sums rounded once (models.py:168-170);
+    checked against float64 with the fp32 accumulation bound; deterministic."""
+    from paper_2411_01109_b200 import device as D
+
+    rng = np.random.default_rng(n + f)
+    x = rng.normal(0, 1, (n, f)).astype(dtype)
+    xt = _t(x, cuda)
+    got = D.col_sums(xt).cpu().numpy().astype(np.float64)
+    want = x.astype(np.float64).sum(0)
+    bound = 1e-6 * np.abs(x).astype(np.float64).sum(0) + np.abs(want) * (
+        2.0 ** -11 if dtype == np.float16 else 2.0 ** -23) + 1e-30
+    assert np.all(np.abs(got - want) <= bound)
+    assert torch.equal(D.col_sums(xt), D.col_sums(xt))
+
+
+@pytest.mark.parametrize("c,ld", [(7, 8), (42, 48), (47, 48), (3, 4), (100, 104), (300, 304)])
+@pytest.mark.parametrize("scale", [1.0, 2048.0])
+def test_softmax_xent_fp16_logits(cuda, c, ld, scale):
+    """convert -> cross_entropy -> backward -> convert-backward in one kernel
+    (models.py:203-217, 552-572): nll in fp64, grad = fp16(fp32((p-y)/n) * S)."""
+    from paper_2411_01109_b200 import device as D
+
+    rng = np.random.default_rng(c)
+    n = 3001
+    z = rng.normal(0, 4, (n, ld)).astype(np.float16)
+    lab = rng.integers(0, c, n)
+    nll, g = D.softmax_xent(_t(z, cuda), _t(lab, cuda), c, n, scale=scale)
+    zz = z[:, :c].astype(np.float64)
+    zz = zz - zz.max(1, keepdims=True)
+    se = np.exp(zz).sum(1)
+    p = np.exp(zz) / se[:, None]
+    p[np.arange(n), lab] -= 1.0
+    want = np.zeros((n, ld), np.float16)
+    want[:, :c] = ((p / n).astype(np.float32) * np.float32(scale)).astype(np.float16)
+    got = g.cpu().numpy()
+    assert got.dtype == np.float16
+    diff = np.abs(bits(got).astype(np.int32) - bits(want).astype(np.int32))
+    assert diff.max() <= 1 and (diff > 0).mean() < 1e-3
+    want_nll = np.log(se) - zz[np.arange(n), lab]
+    np.testing.assert_allclose(nll.cpu().numpy(), want_nll, rtol=1e-12, atol=1e-12)
+    # fp32 logits / fp32 grad path
+    nll32, g32 = D.softmax_xent(_t(z.astype(np.float32), cuda), _t(lab, cuda), c, n)
+    assert g32.dtype == torch.float32
+    np.testing.assert_allclose(g32.cpu().numpy()[:, :c], (p / n).astype(np.float32),
+                               rtol=1e-6, atol=1e-12)

@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert set(declared) == set(_native.SIGNATURES), "ctypes table out of sync with header"
-    assert lib.hg_abi_version() == 1
+    assert lib.hg_abi_version() == 2
 
 
 def test_library_workspace_queries_without_gpu():
@@ -155,3 +155,16 @@ def test_operators_fail_loudly_without_gpu():
         K.spmm_v(g, x)
     with pytest.raises(Exception):
         sp.CooGraph.from_edges(3, [0, 1], [1, 2])
+
+
+def test_resolve_grad_scale():
+    from paper_2411_01109_b200.models import resolve_grad_scale
+
+    assert resolve_grad_scale(1.0, 10) == 1.0
+    assert resolve_grad_scale("auto", 2708) == 32.0
+    assert resolve_grad_scale("auto", 232_965) == 2048.0
+    assert resolve_grad_scale("auto", 10) == 1.0
+    assert resolve_grad_scale(256, 5) == 256.0
+    for bad in (0.5, 3.0, -2.0):
+        with pytest.raises(ValueError, match="power of two"):
+            resolve_grad_scale(bad, 100)
