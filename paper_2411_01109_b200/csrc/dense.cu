@@ -110,15 +110,19 @@ k_col_sums_part(const T* __restrict__ x, int64_t rows, int F, int64_t rpb,
   }
 }
 
-// Pass 2: out[f] = rnd(sum_k part[k, f]) in block order.
+// Pass 2: warp per column; lane l folds partials l, l+32, ... in order, then
+// a fixed xor-shuffle tree: out[f] = rnd(sum_k part[k, f]), deterministic.
 template <typename T>
 __global__ void k_col_sums_final(const float* __restrict__ part, int nb, int F,
                                  T* __restrict__ out) {
-  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  const int f = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   if (f >= F) return;
   float s = 0.0f;
-  for (int k = 0; k < nb; ++k) s = __fadd_rn(s, part[(int64_t)k * F + f]);
-  out[f] = Num<T>::from_f(s);
+  for (int k = lane; k < nb; k += 32) s = __fadd_rn(s, part[(int64_t)k * F + f]);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+  if (lane == 0) out[f] = Num<T>::from_f(s);
 }
 
 template <typename T>
@@ -146,7 +150,7 @@ static int launch_col_sums(const void* x, int64_t rows, int F, void* out, float*
     k_col_sums_part<T, 1><<<(unsigned)nb, 256, smem, st>>>((const T*)x, rows, F, rpb, part);
   }
   HG_LAUNCHED();
-  k_col_sums_final<T><<<(F + 255) / 256, 256, 0, st>>>(part, (int)nb, F, (T*)out);
+  k_col_sums_final<T><<<(F + 7) / 8, 256, 0, st>>>(part, (int)nb, F, (T*)out);
   HG_LAUNCHED();
   return HG_OK;
 }

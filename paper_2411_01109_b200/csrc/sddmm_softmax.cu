@@ -893,51 +893,53 @@ extern "C" int hg_scale_f64(const void* x, double s, void* out, int64_t count, i
 
 namespace hg {
 
-// Warp per row; lane j holds classes j, j+32, ... (K per lane in registers,
-// one fp64 exp per class).  fp64 like the reference; logits are read in their
-// storage type (fp16 widens exactly, as models.convert does) and the gradient
-// is rounded to fp32 first (the reference's float32 grad), scaled by an exact
-// power of two, then to the gradient type (convert's backward rounding).
-template <typename L, typename G, int K>
+// A team of TEAM lanes per row; lane t holds classes t, t+TEAM, ... (K per
+// lane in registers, one fp64 exp per class; several rows per warp keep the
+// fp64 latency chains overlapped).  fp64 like the reference; logits are read
+// in their storage type (fp16 widens exactly, as models.convert does) and the
+// gradient is rounded to fp32 first (the reference's float32 grad), scaled by
+// an exact power of two, then to the gradient type (convert's backward).
+template <typename L, typename G, int TEAM, int K>
 __global__ void __launch_bounds__(256)
 k_softmax_xent(const L* __restrict__ logits, int64_t ld, const int64_t* __restrict__ labels,
                int64_t n, int c_active, double denom, float scale, G* __restrict__ grad,
                double* __restrict__ nll) {
   const int lane = threadIdx.x & 31;
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n;
-       r += nwarps) {
+  const int tl = lane & (TEAM - 1);
+  const unsigned tmask = TEAM == 32 ? 0xffffffffu : (((1u << TEAM) - 1u) << (lane & ~(TEAM - 1)));
+  const int64_t teams = (int64_t)gridDim.x * (blockDim.x / TEAM);
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TEAM; r < n; r += teams) {
     const L* z = logits + r * ld;
     double zv[K];
     double m = -INFINITY;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      const int j = lane + 32 * k;
+      const int j = tl + TEAM * k;
       zv[k] = j < c_active ? (double)Num<L>::to_f(z[j]) : -INFINITY;
       m = fmax(m, zv[k]);
     }
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    for (int o = TEAM / 2; o >= 1; o >>= 1) m = fmax(m, __shfl_xor_sync(tmask, m, o, TEAM));
     double se = 0.0;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      zv[k] = lane + 32 * k < c_active ? exp(zv[k] - m) : 0.0;
+      zv[k] = tl + TEAM * k < c_active ? exp(zv[k] - m) : 0.0;
       se += zv[k];
     }
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+    for (int o = TEAM / 2; o >= 1; o >>= 1) se += __shfl_xor_sync(tmask, se, o, TEAM);
     const int64_t lab = labels[r];
     G* g = grad + r * ld;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      const int j = lane + 32 * k;
+      const int j = tl + TEAM * k;
       if (j < ld) {
         float v = 0.0f;
         if (j < c_active) v = (float)((zv[k] / se - (j == lab ? 1.0 : 0.0)) / denom) * scale;
         g[j] = Num<G>::from_f(v);
       }
     }
-    if (lane == 0) nll[r] = log(se) - ((double)Num<L>::to_f(z[lab]) - m);
+    if (tl == 0) nll[r] = log(se) - ((double)Num<L>::to_f(z[lab]) - m);
   }
 }
 
@@ -978,14 +980,20 @@ template <typename L, typename G>
 static void launch_xent(const void* logits, int64_t ld, const int64_t* labels, int64_t n,
                         int c, double denom, float scale, void* grad, double* nll,
                         cudaStream_t st) {
-  const int g = grid_for(n, 8, 148 * 64);
   const L* lp = (const L*)logits;
   G* gp = (G*)grad;
   const int64_t w = ld > c ? ld : c;
-  if (w <= 32) k_softmax_xent<L, G, 1><<<g, 256, 0, st>>>(lp, ld, labels, n, c, denom, scale, gp, nll);
-  else if (w <= 64) k_softmax_xent<L, G, 2><<<g, 256, 0, st>>>(lp, ld, labels, n, c, denom, scale, gp, nll);
-  else if (w <= 128) k_softmax_xent<L, G, 4><<<g, 256, 0, st>>>(lp, ld, labels, n, c, denom, scale, gp, nll);
-  else k_softmax_xent_wide<L, G><<<g, 256, 0, st>>>(lp, ld, labels, n, c, denom, scale, gp, nll);
+#define HG_XENT(TEAM, K)                                                             \
+  k_softmax_xent<L, G, TEAM, K><<<grid_for(n, 256 / TEAM, 148 * 32), 256, 0, st>>>( \
+      lp, ld, labels, n, c, denom, scale, gp, nll)
+  if (w <= 8) HG_XENT(8, 1);
+  else if (w <= 16) HG_XENT(8, 2);
+  else if (w <= 32) HG_XENT(8, 4);
+  else if (w <= 64) HG_XENT(8, 8);
+  else if (w <= 128) HG_XENT(16, 8);
+  else if (w <= 256) HG_XENT(32, 8);
+  else k_softmax_xent_wide<L, G><<<grid_for(n, 8, 148 * 64), 256, 0, st>>>(lp, ld, labels, n, c, denom, scale, gp, nll);
+#undef HG_XENT
 }
 
 }  // namespace hg

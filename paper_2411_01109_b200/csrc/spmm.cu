@@ -206,7 +206,7 @@ struct FastTeam {
   float acc[NCH][V];
   unsigned tmask;
   int tbase;  // lane id of the team's first lane
-  int beg, end, F, heads;
+  int beg, end, ldx, heads;
   const T* w;
   bool use_widx;
 
@@ -237,7 +237,7 @@ struct FastTeam {
       const int c = shfl_id(ids, j);
       int wi = b + j;
       if (WEIGHTED && use_widx) wi = shfl_id(wids, j);
-      const size_t roff = (size_t)(unsigned)c * (unsigned)F;
+      const size_t roff = (size_t)(unsigned)c * (unsigned)ldx;
 #pragma unroll
       for (int k = 0; k < NCH; ++k) {
         if (ok && cval[k]) {
@@ -265,7 +265,8 @@ __global__ void __launch_bounds__(256, FastOcc<TEAM, NCH, WEIGHTED>::value)
 k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __restrict__ cols,
             int64_t num_edges, const T* __restrict__ w, const int32_t* __restrict__ widx,
             int heads, int fh, const T* __restrict__ x, T* __restrict__ y,
-            float* __restrict__ carry, int F, int fmode, const T* __restrict__ fout) {
+            float* __restrict__ carry, int F, int ldx, int ldy, int fmode,
+            const T* __restrict__ fout) {
   using Team = FastTeam<T, V, TEAM, NCH, WEIGHTED>;
   constexpr int EB = Team::EB;
   constexpr int CPL = Team::CPL;
@@ -290,7 +291,7 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
   t.tmask = TEAM == 32 ? 0xffffffffu : (((1u << TEAM) - 1u) << t.tbase);
   t.beg = un.y;
   t.end = un.z;
-  t.F = F;
+  t.ldx = ldx;
   t.heads = heads;
   t.w = w;
   t.use_widx = WEIGHTED && widx != nullptr;
@@ -343,7 +344,7 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
     const T fo = fout ? fout[row] : Num<T>::zero();
 #pragma unroll
     for (int k = 0; k < NCH; ++k)
-      if (t.cval[k]) store_out<T, V>(y + (int64_t)row * F + (t.xl[k] - x), t.acc[k], fmode, fo);
+      if (t.cval[k]) store_out<T, V>(y + (int64_t)row * ldy + (t.xl[k] - x), t.acc[k], fmode, fo);
   } else {
 #pragma unroll
     for (int k = 0; k < NCH; ++k)
@@ -355,8 +356,8 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
 template <typename T, int V, int TEAM, int NCH>
 __global__ void __launch_bounds__(256)
 k_spmm_fast_followup(const int4* __restrict__ split_rows, int64_t num_split,
-                     const float* __restrict__ carry, T* __restrict__ y, int F, int fmode,
-                     const T* __restrict__ fout) {
+                     const float* __restrict__ carry, T* __restrict__ y, int F, int ldy,
+                     int fmode, const T* __restrict__ fout) {
   const int lane = threadIdx.x & 31;
   const int tl = lane & (TEAM - 1);
   const int64_t team = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TEAM;
@@ -376,18 +377,8 @@ k_spmm_fast_followup(const int4* __restrict__ split_rows, int64_t num_split,
 #pragma unroll
       for (int i = 0; i < V; ++i) acc[i] += src[i];
     }
-    store_out<T, V>(y + (int64_t)sr.x * F + c * V, acc, fmode, fo);
+    store_out<T, V>(y + (int64_t)sr.x * ldy + c * V, acc, fmode, fo);
   }
-}
-
-// X' = rnd(X * in_scale[:, None]) (kernels.py:358-361), one rounding per element.
-template <typename T>
-__global__ void k_scale_rows(const T* __restrict__ x, const T* __restrict__ s, int64_t rows,
-                             int F, T* __restrict__ out) {
-  const int64_t total = rows * (int64_t)F;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = Num<T>::mul(x[i], s[i / F]);
 }
 
 struct FastArgs {
@@ -404,7 +395,7 @@ struct FastArgs {
   const void* x;
   void* y;
   float* carry;
-  int F, fmode;
+  int F, ldx, ldy, fmode;
   const void* fout;
   cudaStream_t st;
 };
@@ -421,13 +412,13 @@ static int launch_fast(const FastArgs& a) {
     int64_t blocks = (a.num_units + teams_per_block - 1) / teams_per_block;
     k_spmm_fast<T, V, TEAM, NCH, WT><<<(unsigned)blocks, kThreads, 0, a.st>>>(
         a.units, a.num_units, a.cols, a.num_edges, (const T*)a.w, a.widx, a.heads, a.fh,
-        (const T*)a.x, (T*)a.y, a.carry, a.F, a.fmode, (const T*)a.fout);
+        (const T*)a.x, (T*)a.y, a.carry, a.F, a.ldx, a.ldy, a.fmode, (const T*)a.fout);
     HG_LAUNCHED();
   }
   if (a.num_split > 0) {
     int64_t blocks = (a.num_split + kThreads / TEAMF - 1) / (kThreads / TEAMF);
     k_spmm_fast_followup<T, V, TEAMF, NCH><<<(unsigned)blocks, kThreads, 0, a.st>>>(
-        a.split_rows, a.num_split, a.carry, (T*)a.y, a.F, a.fmode, (const T*)a.fout);
+        a.split_rows, a.num_split, a.carry, (T*)a.y, a.F, a.ldy, a.fmode, (const T*)a.fout);
     HG_LAUNCHED();
   }
   return HG_OK;
@@ -464,24 +455,17 @@ static int dispatch_fast(const FastArgs& a) {
   constexpr int VB = 16 / sizeof(T);
   const bool aligned = (reinterpret_cast<uintptr_t>(a.x) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(a.y) % 16 == 0);
-  const bool big = aligned && (a.fh % VB == 0);
+  const bool big = aligned && (a.fh % VB == 0) && a.ldx % VB == 0 && a.ldy % VB == 0;
   if (a.w) return big ? dispatch_layout<T, VB, true>(a) : dispatch_layout<T, 2, true>(a);
   return big ? dispatch_layout<T, VB, false>(a) : dispatch_layout<T, 2, false>(a);
 }
 
 static size_t elem_size(int dtype) { return dtype == HG_F16 ? 2 : 4; }
 
+// X' = rnd(X * s[:, None]): the vectorised row-scale pass of dense.cu.
 static int scale_rows(const void* x, const void* s, int64_t rows, int F, void* out, int dtype,
                       cudaStream_t st) {
-  int g = grid_for(rows * (int64_t)F, 256, 148 * 16);
-  if (dtype == HG_F16)
-    k_scale_rows<__half><<<g, 256, 0, st>>>((const __half*)x, (const __half*)s, rows, F,
-                                           (__half*)out);
-  else
-    k_scale_rows<float><<<g, 256, 0, st>>>((const float*)x, (const float*)s, rows, F,
-                                          (float*)out);
-  HG_LAUNCHED();
-  return HG_OK;
+  return hg_bias_scale_rows(x, nullptr, s, rows, F, out, dtype, st);
 }
 
 }  // namespace hg
@@ -503,9 +487,9 @@ extern "C" int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_ro
                        int64_t n_cols, int64_t num_edges, const int32_t* units, int64_t num_units,
                        const int32_t* split_rows, int64_t num_split_rows, int64_t num_slots,
                        const void* w, const int32_t* w_index, int32_t heads, const void* x,
-                       void* y, int32_t F, int32_t scaling, const void* in_scale,
-                       const void* out_factor, int dtype, void* ws, size_t ws_bytes,
-                       void* stream) {
+                       void* y, int32_t F, int64_t ldx, int64_t ldy, int32_t scaling,
+                       const void* in_scale, const void* out_factor, int dtype, void* ws,
+                       size_t ws_bytes, void* stream) {
   HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
   HG_REQUIRE(F > 0 && F % 2 == 0, "feature length %d must be even and positive", F);
   HG_REQUIRE(heads >= 1 && F % heads == 0 && (F / heads) % 2 == 0,
@@ -514,6 +498,11 @@ extern "C" int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_ro
              "unknown scaling %d", scaling);
   HG_REQUIRE(n_rows >= 0 && n_cols >= 0 && num_edges >= 0, "hg_spmm: bad sizes");
   HG_REQUIRE(num_edges <= (int64_t)INT32_MAX, "hg_spmm: edge count exceeds int32 units");
+  if (ldx == 0) ldx = F;
+  if (ldy == 0) ldy = F;
+  HG_REQUIRE(ldx >= F && ldy >= F && ldx <= INT32_MAX && ldy <= INT32_MAX,
+             "hg_spmm: row strides (%lld, %lld) must be >= F=%d", (long long)ldx, (long long)ldy, F);
+  HG_REQUIRE(!in_scale || ldx == F, "hg_spmm: in_scale needs a dense x (ldx == F)");
   cudaStream_t st = as_stream(stream);
   if (n_rows == 0) return HG_OK;
   Carver cv(ws, ws_bytes);
@@ -532,7 +521,7 @@ extern "C" int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_ro
   a.units = reinterpret_cast<const int4*>(units); a.num_units = num_units;
   a.split_rows = reinterpret_cast<const int4*>(split_rows); a.num_split = num_split_rows;
   a.w = w; a.widx = w_index; a.heads = heads; a.fh = F / heads;
-  a.x = x; a.y = y; a.carry = carry; a.F = F;
+  a.x = x; a.y = y; a.carry = carry; a.F = F; a.ldx = (int)ldx; a.ldy = (int)ldy;
   a.fmode = out_factor == nullptr ? 0 : (scaling == HG_SCALING_POST ? 1 : 2);
   a.fout = out_factor; a.st = st;
   return dtype == HG_F16 ? dispatch_fast<__half>(a) : dispatch_fast<float>(a);

@@ -275,12 +275,19 @@ class DeviceGraph:
 # ── SpMM ─────────────────────────────────────────────────────────────────
 
 
+def _row_strided(t):
+    """2-D tensor whose rows may be padded (unit column stride)."""
+    return t.dim() == 2 and t.stride(1) == 1 and t.stride(0) >= t.shape[1]
+
+
 def spmm_csr(view: CsrView, x: torch.Tensor, w=None, w_index=None, heads: int = 1,
              scaling: str = "post", fin=None, fout=None, out=None,
              split_cap: int = DEFAULT_SPLIT_CAP) -> torch.Tensor:
-    """fp32-guarded row-owned SpMM over one CSR view (hg_spmm)."""
+    """fp32-guarded row-owned SpMM over one CSR view (hg_spmm).  x and out may
+    be column slices of wider row-major storage (row strides passed through)."""
     _require_cuda(x)
-    x = x.contiguous()
+    if not _row_strided(x) or fin is not None:
+        x = x.contiguous()
     if x.dim() != 2 or x.shape[0] != view.n_cols:
         raise ValueError(f"feature tensor has {x.shape[0]} rows for {view.n_cols} columns")
     f = x.shape[1]
@@ -288,6 +295,8 @@ def spmm_csr(view: CsrView, x: torch.Tensor, w=None, w_index=None, heads: int = 
     sched = view.schedule(split_cap)
     if out is None:
         out = torch.empty((view.n_rows, f), dtype=x.dtype, device=x.device)
+    elif not _row_strided(out) or out.shape != (view.n_rows, f) or out.dtype != x.dtype:
+        raise ValueError("out must be [n_rows, F] with unit column stride")
     nbytes = nat.size_query("hg_spmm_workspace", view.n_cols, f, sched.num_slots,
                             int(fin is not None), dt)
     ws = workspace(nbytes, x.device)
@@ -302,7 +311,8 @@ def spmm_csr(view: CsrView, x: torch.Tensor, w=None, w_index=None, heads: int = 
     nat.call("hg_spmm", _p(view.offsets), _p(view.cols), view.n_rows, view.n_cols,
              view.num_edges, _p(sched.units), sched.num_units, _p(sched.split_rows),
              sched.split_rows.shape[0], sched.num_slots, _p(w), _p(w_index), heads, _p(x),
-             _p(out), f, nat.SCALING_CODES[scaling], _p(fin), _p(fout), dt, _p(ws),
+             _p(out), f, x.stride(0), out.stride(0), nat.SCALING_CODES[scaling], _p(fin),
+             _p(fout), dt, _p(ws),
              0 if ws is None else ws.numel(), _stream())
     Probe.launches += int(sched.num_units > 0) + int(sched.split_rows.shape[0] > 0) + int(
         fin is not None)

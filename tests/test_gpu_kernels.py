@@ -490,3 +490,28 @@ def test_softmax_xent_fp16_logits(cuda, c, ld, scale):
     assert g32.dtype == torch.float32
     np.testing.assert_allclose(g32.cpu().numpy()[:, :c], (p / n).astype(np.float32),
                                rtol=1e-6, atol=1e-12)
+
+
+@pytest.mark.parametrize("f,ld", [(48, 64), (24, 32), (6, 8), (40, 64), (64, 72)])
+def test_spmm_fast_row_strides(cuda, f, ld):
+    """x / y as column slices of wider rows (hg_spmm ldx / ldy): identical
+    values to the dense layout; padding columns of y untouched."""
+    from paper_2411_01109_b200 import device as D
+
+    rng = np.random.default_rng(f * ld)
+    n = 3000
+    deg = np.minimum(rng.zipf(1.6, n), 2500)
+    rows = np.repeat(np.arange(n), deg)
+    r, c = O.canonical_edges(n, rows, rng.integers(0, n, rows.size))
+    dg = _dg(n, r, c, cuda)
+    view = dg.view(False)
+    fin, fout = dg.norm_tables("both", False, torch.float16)
+    x = torch.randn(n, f, device=cuda, dtype=torch.float16)
+    wide = torch.randn(n, ld, device=cuda, dtype=torch.float16)
+    wide[:, :f] = x
+    want = D.spmm_csr(view, x, scaling="discretized", fout=fout)
+    ybuf = torch.full((n, ld), 7.0, device=cuda, dtype=torch.float16)
+    got = D.spmm_csr(view, wide[:, :f], scaling="discretized", fout=fout, out=ybuf[:, :f])
+    assert torch.equal(got, want)
+    assert torch.equal(ybuf[:, :f], want)
+    assert bool((ybuf[:, f:] == 7.0).all())
