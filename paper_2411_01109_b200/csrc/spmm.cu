@@ -427,17 +427,11 @@ static int launch_fast(const FastArgs& a) {
 template <typename T, int V, bool WT>
 static int dispatch_layout(const FastArgs& a) {
   const int nvec = a.F / V;
-  if constexpr (V * sizeof(T) == 16) {  // exact-width teams for common odd chunk counts
-    switch (nvec) {
-      case 3: return launch_fast<T, V, 3, 1, WT>(a);
-      case 5: return launch_fast<T, V, 5, 1, WT>(a);
-      case 6: return launch_fast<T, V, 6, 1, WT>(a);
-      case 7: return launch_fast<T, V, 7, 1, WT>(a);
-      case 12: return launch_fast<T, V, 12, 1, WT>(a);
-      case 24: return launch_fast<T, V, 24, 1, WT>(a);
-      default: break;
-    }
-  }
+  // Teams stay power-of-two lane groups even when some lanes idle (F=48: 6 of
+  // 8): a 16-byte-per-lane warp load is served in quarter-warp (8-lane)
+  // wavefronts, and a team straddling two quarters doubles the L1 data-pipe
+  // wavefronts (ncu, profiles/r01: 7-lane teams ran 27% slower than 8-lane
+  // teams at the same L2 sector count).
   if (nvec <= 1) return launch_fast<T, V, 1, 1, WT>(a);
   if (nvec <= 2) return launch_fast<T, V, 2, 1, WT>(a);
   if (nvec <= 4) return launch_fast<T, V, 4, 1, WT>(a);
