@@ -930,12 +930,15 @@ k_softmax_xent(const L* __restrict__ logits, int64_t ld, const int64_t* __restri
     for (int o = TEAM / 2; o >= 1; o >>= 1) se += __shfl_xor_sync(tmask, se, o, TEAM);
     const int64_t lab = labels[r];
     G* g = grad + r * ld;
+    // reciprocals instead of the reference's two divisions: the fp64 results
+    // differ in the last bit at most, below the fp32 rounding that follows
+    const double rse = 1.0 / se, rden = 1.0 / denom;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const int j = tl + TEAM * k;
       if (j < ld) {
         float v = 0.0f;
-        if (j < c_active) v = (float)((zv[k] / se - (j == lab ? 1.0 : 0.0)) / denom) * scale;
+        if (j < c_active) v = (float)((zv[k] * rse - (j == lab ? 1.0 : 0.0)) * rden) * scale;
         g[j] = Num<G>::from_f(v);
       }
     }
@@ -989,6 +992,7 @@ static void launch_xent(const void* logits, int64_t ld, const int64_t* labels, i
   if (w <= 8) HG_XENT(8, 1);
   else if (w <= 16) HG_XENT(8, 2);
   else if (w <= 32) HG_XENT(8, 4);
+  else if (w <= 48) HG_XENT(8, 6);
   else if (w <= 64) HG_XENT(8, 8);
   else if (w <= 128) HG_XENT(16, 8);
   else if (w <= 256) HG_XENT(32, 8);

@@ -372,10 +372,24 @@ k_spmm_fast_followup(const int4* __restrict__ split_rows, int64_t num_split,
     float acc[V];
 #pragma unroll
     for (int i = 0; i < V; ++i) acc[i] = 0.0f;
-    for (int p = 0; p < sr.z; ++p) {
-      const float* src = carry + (int64_t)(sr.y + p) * F + c * V;
+    // slots fetched 4 at a time (independent loads in flight), added in slot order
+    constexpr int PF = 4;
+    for (int p = 0; p < sr.z; p += PF) {
+      float buf[PF][V];
 #pragma unroll
-      for (int i = 0; i < V; ++i) acc[i] += src[i];
+      for (int q = 0; q < PF; ++q) {
+        if (p + q < sr.z) {
+          const float* src = carry + (int64_t)(sr.y + p + q) * F + c * V;
+#pragma unroll
+          for (int i = 0; i < V; ++i) buf[q][i] = src[i];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < PF; ++q)
+        if (p + q < sr.z) {
+#pragma unroll
+          for (int i = 0; i < V; ++i) acc[i] += buf[q][i];
+        }
     }
     store_out<T, V>(y + (int64_t)sr.x * ldy + c * V, acc, fmode, fo);
   }
