@@ -227,6 +227,47 @@ int hg_adam_step(float* master, float* m, float* v, const void* grad, int grad_d
                  int64_t count, float lr, float omb1, float omb2, double b1, double b2,
                  float eps, const double* step, float grad_unscale, void* stream);
 
+/* ------------------------------------------- fp32-guarded GAT ("fast" numerics) */
+
+/* Row classes for the row-owned fast kernels: rows with <= short_max edges run
+ * one thread per (row, head); medium_rows (int32 ids, short_max < deg <=
+ * long threshold) one warp per row; long_rows one 256-thread CTA per row.
+ * Every row must fall in exactly one class.  heads: power of two <= 16. */
+
+/* attention_scores + leaky_relu + edge_softmax (models.py:188-200, 317-326,
+ * 382-401) in one pass: alpha[e, h] = rnd(exp(l_e - m) / sum exp(l - m)) with
+ * l_e = leaky(s_l[r, h] + s_r[c, h]) in fp32 (slope), fp32 online max/sum. */
+int hg_gat_attention_fwd(const int64_t* offsets, const int32_t* cols, int64_t n_rows,
+                         const void* s_l, const void* s_r, int32_t heads, float slope,
+                         void* alpha, const int32_t* medium_rows, int64_t n_medium,
+                         const int32_t* long_rows, int64_t n_long, int32_t short_max,
+                         int dtype, void* stream);
+
+/* Backward of the above (models.py:188-200, 329-333, 403-410): per row,
+ * D = sum alpha*dalpha (fp32); de[e, h] = rnd(alpha (dalpha - D) * leaky'(l_e));
+ * ds_l[r, h] = rnd(sum_e of the unrounded de).  The column sums (ds_r) follow
+ * with hg_edge_sums_fast over the CSC and perm. */
+int hg_gat_attention_bwd(const int64_t* offsets, const int32_t* cols, int64_t n_rows,
+                         const void* s_l, const void* s_r, int32_t heads, float slope,
+                         const void* alpha, const void* dalpha, void* de, void* ds_l,
+                         const int32_t* medium_rows, int64_t n_medium,
+                         const int32_t* long_rows, int64_t n_long, int32_t short_max,
+                         int dtype, void* stream);
+
+/* out[r, h] = rnd(sum_{e in row r} vals[(perm ? perm[e] : e), h]) with fp32
+ * accumulation (row / column sums of per-edge values, models.py:329-337). */
+int hg_edge_sums_fast(const int64_t* offsets, int64_t n_rows, const void* vals,
+                      const int32_t* perm, int32_t heads, void* out,
+                      const int32_t* medium_rows, int64_t n_medium, const int32_t* long_rows,
+                      int64_t n_long, int32_t short_max, int dtype, void* stream);
+
+/* Mean over concatenated heads: out[n, f] = rnd(sum_h y[n, h*f + f'] / heads) in
+ * fp64 (exact sum); backward gin[n, h*f + f'] = rnd(g[n, f'] / heads). */
+int hg_head_mean(const void* y, int64_t n, int32_t heads, int32_t f, void* out, int dtype,
+                 void* stream);
+int hg_head_mean_bwd(const void* g, int64_t n, int32_t heads, int32_t f, void* gin, int dtype,
+                     void* stream);
+
 /* ---------------------------------------------------------------- elementwise */
 
 /* out = rnd(x * s) with the product formed in fp64 (the reference multiplies

@@ -57,6 +57,13 @@ SIGNATURES = {
     "hg_head_dots_bwd_workspace": [_I32, _I32, _PSZ],
     "hg_head_dots_bwd": [_P, _P, _P, _P, _P, _I64, _I32, _I32, _P, _P, _P, c_int, _P, c_size_t,
                          _P],
+    "hg_gat_attention_fwd": [_P, _P, _I64, _P, _P, _I32, c_float, _P, _P, _I64, _P, _I64, _I32,
+                             c_int, _P],
+    "hg_gat_attention_bwd": [_P, _P, _I64, _P, _P, _I32, c_float, _P, _P, _P, _P, _P, _I64, _P,
+                             _I64, _I32, c_int, _P],
+    "hg_edge_sums_fast": [_P, _I64, _P, _P, _I32, _P, _P, _I64, _P, _I64, _I32, c_int, _P],
+    "hg_head_mean": [_P, _I64, _I32, _I32, _P, c_int, _P],
+    "hg_head_mean_bwd": [_P, _I64, _I32, _I32, _P, c_int, _P],
     "hg_bias_scale_rows": [_P, _P, _P, _I64, _I32, _P, c_int, _P],
     "hg_col_sums_workspace": [_I64, _I32, _PSZ],
     "hg_col_sums": [_P, _I64, _I32, _P, c_int, _P, c_size_t, _P],

@@ -1,0 +1,485 @@
+// fp32-guarded GAT attention for numerics="fast" (the row-owned B200 path; the
+// bit-exact reference chain stays in sddmm_softmax.cu):
+//
+//  * k_gat_fwd_*   alpha[e, h] = rnd(softmax_r(leaky(s_l[r, h] + s_r[c, h])))
+//                  -- attention_scores + leaky_relu + edge_softmax
+//                  (models.py:188-200, 317-326, 382-401) in one pass: fp32
+//                  logits (never rounded), fp32 online max / sum (expf), one
+//                  rounding of alpha.  No E x H logits array is written.
+//  * k_gat_bwd_*   de'[e, h] = rnd(alpha (dalpha - sum_r alpha dalpha) *
+//                  leaky'(e)) and ds_l[r, h] = rnd(sum_r de') -- edge_softmax
+//                  backward (403-410), leaky backward and the row-sum half of
+//                  attention_scores backward (329-333) in one pass.
+//  * k_gat_sums_*  out[r, h] = rnd(sum_e v[idx(e), h]) with idx = perm (CSC
+//                  gather: the column-sum half of attention_scores backward,
+//                  335-337) or identity.
+//
+// Rows are split by length: <= short_max edges -> one thread per (row, head);
+// medium rows (listed) -> one warp per row, lanes over (edge, head); rows
+// longer than long_min (listed) -> one 256-thread CTA per row.  All sums are
+// fp32 in a fixed order per launch configuration: deterministic.
+#include "hg_common.cuh"
+
+namespace hg {
+
+__device__ __forceinline__ float leaky_f(float v, float slope) { return v > 0.0f ? v : v * slope; }
+
+// online softmax state (m, s): s = sum exp(v - m)
+__device__ __forceinline__ void ms_push(float& m, float& s, float v) {
+  if (v > m) {
+    s = s * expf(m - v) + 1.0f;
+    m = v;
+  } else {
+    s += expf(v - m);
+  }
+}
+
+__device__ __forceinline__ void ms_merge(float& m, float& s, float m2, float s2) {
+  const float mm = fmaxf(m, m2);
+  if (mm == -INFINITY) return;
+  s = (m == -INFINITY ? 0.0f : s * expf(m - mm)) + (m2 == -INFINITY ? 0.0f : s2 * expf(m2 - mm));
+  m = mm;
+}
+
+// combine (m, s) over lanes with the same lane % H
+template <int H>
+__device__ __forceinline__ void ms_warp(float& m, float& s) {
+#pragma unroll
+  for (int o = 16; o >= H; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+    const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    ms_merge(m, s, m2, s2);
+  }
+}
+
+template <int H>
+__device__ __forceinline__ float sum_warp(float v) {
+#pragma unroll
+  for (int o = 16; o >= H; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---------------------------------------------------------------- forward
+
+template <typename T, int H>
+__global__ void __launch_bounds__(256)
+k_gat_fwd_thread(const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
+                 int64_t n_rows, const T* __restrict__ sl, const T* __restrict__ sr, float slope,
+                 T* __restrict__ alpha, int short_max) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n_rows * H) return;
+  const int64_t r = t / H;
+  const int h = (int)(t - r * H);
+  const int64_t beg = offsets[r], end = offsets[r + 1];
+  if (end == beg || end - beg > short_max) return;
+  const float a = Num<T>::to_f(sl[t]);
+  float m = -INFINITY, s = 0.0f;
+  for (int64_t e = beg; e < end; ++e)
+    ms_push(m, s, leaky_f(a + Num<T>::to_f(sr[(int64_t)cols[e] * H + h]), slope));
+  const float inv = 1.0f / s;
+  for (int64_t e = beg; e < end; ++e) {
+    const float v = leaky_f(a + Num<T>::to_f(sr[(int64_t)cols[e] * H + h]), slope);
+    alpha[e * H + h] = Num<T>::from_f(expf(v - m) * inv);
+  }
+}
+
+template <typename T, int H>
+__global__ void __launch_bounds__(256)
+k_gat_fwd_warp(const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
+               const int32_t* __restrict__ rows, int64_t n_list, const T* __restrict__ sl,
+               const T* __restrict__ sr, float slope, T* __restrict__ alpha) {
+  constexpr int EPB = 32 / H;
+  const int lane = threadIdx.x & 31, j = lane / H, h = lane % H;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); w < n_list;
+       w += nwarps) {
+    const int64_t r = rows[w];
+    const int64_t beg = offsets[r], end = offsets[r + 1];
+    const float a = Num<T>::to_f(sl[r * H + h]);
+    float m = -INFINITY, s = 0.0f;
+    for (int64_t e = beg + j; e < end; e += EPB)
+      ms_push(m, s, leaky_f(a + Num<T>::to_f(sr[(int64_t)cols[e] * H + h]), slope));
+    ms_warp<H>(m, s);
+    const float inv = 1.0f / s;
+    for (int64_t e = beg + j; e < end; e += EPB) {
+      const float v = leaky_f(a + Num<T>::to_f(sr[(int64_t)cols[e] * H + h]), slope);
+      alpha[e * H + h] = Num<T>::from_f(expf(v - m) * inv);
+    }
+  }
+}
+
+template <typename T, int H>
+__global__ void __launch_bounds__(256)
+k_gat_fwd_cta(const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
+              const int32_t* __restrict__ rows, const T* __restrict__ sl,
+              const T* __restrict__ sr, float slope, T* __restrict__ alpha) {
+  constexpr int EPB = 256 / H;
+  __shared__ float sm[8][H], ss[8][H];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, j = tid / H, h = tid % H;
+  const int64_t r = rows[blockIdx.x];
+  const int64_t beg = offsets[r], end = offsets[r + 1];
+  const float a = Num<T>::to_f(sl[r * H + h]);
+  float m = -INFINITY, s = 0.0f;
+  for (int64_t e = beg + j; e < end; e += EPB)
+    ms_push(m, s, leaky_f(a + Num<T>::to_f(sr[(int64_t)cols[e] * H + h]), slope));
+  ms_warp<H>(m, s);
+  if (lane < H) { sm[warp][lane] = m; ss[warp][lane] = s; }
+  __syncthreads();
+  float mt = sm[0][h], st = ss[0][h];
+#pragma unroll
+  for (int k = 1; k < 8; ++k) ms_merge(mt, st, sm[k][h], ss[k][h]);
+  const float inv = 1.0f / st;
+  for (int64_t e = beg + j; e < end; e += EPB) {
+    const float v = leaky_f(a + Num<T>::to_f(sr[(int64_t)cols[e] * H + h]), slope);
+    alpha[e * H + h] = Num<T>::from_f(expf(v - mt) * inv);
+  }
+}
+
+// --------------------------------------------------------------- backward
+
+template <typename T, int H>
+__global__ void __launch_bounds__(256)
+k_gat_bwd_thread(const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
+                 int64_t n_rows, const T* __restrict__ sl, const T* __restrict__ sr, float slope,
+                 const T* __restrict__ alpha, const T* __restrict__ dalpha, T* __restrict__ de,
+                 T* __restrict__ dsl, int short_max) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n_rows * H) return;
+  const int64_t r = t / H;
+  const int h = (int)(t - r * H);
+  const int64_t beg = offsets[r], end = offsets[r + 1];
+  if (end - beg > short_max) return;
+  float d = 0.0f;
+  for (int64_t e = beg; e < end; ++e)
+    d = fmaf(Num<T>::to_f(alpha[e * H + h]), Num<T>::to_f(dalpha[e * H + h]), d);
+  const float a = Num<T>::to_f(sl[t]);
+  float acc = 0.0f;
+  for (int64_t e = beg; e < end; ++e) {
+    const float v = a + Num<T>::to_f(sr[(int64_t)cols[e] * H + h]);
+    float g = Num<T>::to_f(alpha[e * H + h]) * (Num<T>::to_f(dalpha[e * H + h]) - d);
+    g = v > 0.0f ? g : g * slope;
+    de[e * H + h] = Num<T>::from_f(g);
+    acc += g;
+  }
+  dsl[t] = Num<T>::from_f(acc);
+}
+
+template <typename T, int H>
+__global__ void __launch_bounds__(256)
+k_gat_bwd_warp(const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
+               const int32_t* __restrict__ rows, int64_t n_list, const T* __restrict__ sl,
+               const T* __restrict__ sr, float slope, const T* __restrict__ alpha,
+               const T* __restrict__ dalpha, T* __restrict__ de, T* __restrict__ dsl) {
+  constexpr int EPB = 32 / H;
+  const int lane = threadIdx.x & 31, j = lane / H, h = lane % H;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); w < n_list;
+       w += nwarps) {
+    const int64_t r = rows[w];
+    const int64_t beg = offsets[r], end = offsets[r + 1];
+    float d = 0.0f;
+    for (int64_t e = beg + j; e < end; e += EPB)
+      d = fmaf(Num<T>::to_f(alpha[e * H + h]), Num<T>::to_f(dalpha[e * H + h]), d);
+    d = sum_warp<H>(d);
+    const float a = Num<T>::to_f(sl[r * H + h]);
+    float acc = 0.0f;
+    for (int64_t e = beg + j; e < end; e += EPB) {
+      const float v = a + Num<T>::to_f(sr[(int64_t)cols[e] * H + h]);
+      float g = Num<T>::to_f(alpha[e * H + h]) * (Num<T>::to_f(dalpha[e * H + h]) - d);
+      g = v > 0.0f ? g : g * slope;
+      de[e * H + h] = Num<T>::from_f(g);
+      acc += g;
+    }
+    acc = sum_warp<H>(acc);
+    if (lane < H) dsl[r * H + lane] = Num<T>::from_f(acc);
+  }
+}
+
+template <int H>
+__device__ __forceinline__ float block_sum_h(float v, float (*red)[H]) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, h = tid % H;
+  v = sum_warp<H>(v);
+  if (lane < H) red[warp][lane] = v;
+  __syncthreads();
+  float t = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) t += red[k][h];
+  __syncthreads();
+  return t;
+}
+
+template <typename T, int H>
+__global__ void __launch_bounds__(256)
+k_gat_bwd_cta(const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
+              const int32_t* __restrict__ rows, const T* __restrict__ sl,
+              const T* __restrict__ sr, float slope, const T* __restrict__ alpha,
+              const T* __restrict__ dalpha, T* __restrict__ de, T* __restrict__ dsl) {
+  constexpr int EPB = 256 / H;
+  __shared__ float red[8][H];
+  const int tid = threadIdx.x, j = tid / H, h = tid % H;
+  const int64_t r = rows[blockIdx.x];
+  const int64_t beg = offsets[r], end = offsets[r + 1];
+  float d = 0.0f;
+  for (int64_t e = beg + j; e < end; e += EPB)
+    d = fmaf(Num<T>::to_f(alpha[e * H + h]), Num<T>::to_f(dalpha[e * H + h]), d);
+  d = block_sum_h<H>(d, red);
+  const float a = Num<T>::to_f(sl[r * H + h]);
+  float acc = 0.0f;
+  for (int64_t e = beg + j; e < end; e += EPB) {
+    const float v = a + Num<T>::to_f(sr[(int64_t)cols[e] * H + h]);
+    float g = Num<T>::to_f(alpha[e * H + h]) * (Num<T>::to_f(dalpha[e * H + h]) - d);
+    g = v > 0.0f ? g : g * slope;
+    de[e * H + h] = Num<T>::from_f(g);
+    acc += g;
+  }
+  acc = block_sum_h<H>(acc, red);
+  if (tid < H) dsl[r * H + tid] = Num<T>::from_f(acc);
+}
+
+// ------------------------------------------------------------- edge sums
+
+template <typename T, int H>
+__global__ void __launch_bounds__(256)
+k_gat_sums_thread(const int64_t* __restrict__ offsets, int64_t n_rows, const T* __restrict__ v,
+                  const int32_t* __restrict__ perm, T* __restrict__ out, int short_max) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n_rows * H) return;
+  const int64_t r = t / H;
+  const int h = (int)(t - r * H);
+  const int64_t beg = offsets[r], end = offsets[r + 1];
+  if (end - beg > short_max) return;
+  float acc = 0.0f;
+  for (int64_t e = beg; e < end; ++e) {
+    const int64_t i = perm ? (int64_t)perm[e] : e;
+    acc += Num<T>::to_f(v[i * H + h]);
+  }
+  out[t] = Num<T>::from_f(acc);
+}
+
+template <typename T, int H>
+__global__ void __launch_bounds__(256)
+k_gat_sums_warp(const int64_t* __restrict__ offsets, const int32_t* __restrict__ rows,
+                int64_t n_list, const T* __restrict__ v, const int32_t* __restrict__ perm,
+                T* __restrict__ out) {
+  constexpr int EPB = 32 / H;
+  const int lane = threadIdx.x & 31, j = lane / H, h = lane % H;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); w < n_list;
+       w += nwarps) {
+    const int64_t r = rows[w];
+    const int64_t beg = offsets[r], end = offsets[r + 1];
+    float acc = 0.0f;
+    for (int64_t e = beg + j; e < end; e += EPB) {
+      const int64_t i = perm ? (int64_t)perm[e] : e;
+      acc += Num<T>::to_f(v[i * H + h]);
+    }
+    acc = sum_warp<H>(acc);
+    if (lane < H) out[r * H + lane] = Num<T>::from_f(acc);
+  }
+}
+
+template <typename T, int H>
+__global__ void __launch_bounds__(256)
+k_gat_sums_cta(const int64_t* __restrict__ offsets, const int32_t* __restrict__ rows,
+               const T* __restrict__ v, const int32_t* __restrict__ perm, T* __restrict__ out) {
+  constexpr int EPB = 256 / H;
+  __shared__ float red[8][H];
+  const int tid = threadIdx.x, j = tid / H, h = tid % H;
+  const int64_t r = rows[blockIdx.x];
+  const int64_t beg = offsets[r], end = offsets[r + 1];
+  float acc = 0.0f;
+  for (int64_t e = beg + j; e < end; e += EPB) {
+    const int64_t i = perm ? (int64_t)perm[e] : e;
+    acc += Num<T>::to_f(v[i * H + h]);
+  }
+  acc = block_sum_h<H>(acc, red);
+  if (tid < H) out[r * H + tid] = Num<T>::from_f(acc);
+}
+
+// -------------------------------------------------------------- head mean
+
+// out[n, f] = rnd(sum_h y[n, h, f] / H): the H fp16 values sum exactly in fp64
+// (models.py mean of concatenated heads; _HeadMeanFn).  Backward:
+// g_in[n, h, f] = rnd(g[n, f] / H).
+template <typename T>
+__global__ void k_head_mean(const T* __restrict__ y, int64_t n, int heads, int f,
+                            T* __restrict__ out) {
+  const int64_t total = n * (int64_t)f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / f;
+    const int c = (int)(i - r * f);
+    double s = 0.0;
+    for (int h = 0; h < heads; ++h) s += Num<T>::to_d(y[(r * heads + h) * f + c]);
+    out[i] = Num<T>::from_d(s / heads);
+  }
+}
+
+template <typename T>
+__global__ void k_head_mean_bwd(const T* __restrict__ g, int64_t n, int heads, int f,
+                                T* __restrict__ gin) {
+  const int64_t total = n * (int64_t)f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / f;
+    const int c = (int)(i - r * f);
+    const T v = Num<T>::from_d(Num<T>::to_d(g[i]) / heads);
+    for (int h = 0; h < heads; ++h) gin[(r * heads + h) * f + c] = v;
+  }
+}
+
+struct GatRows {
+  const int64_t* offsets;
+  const int32_t* cols;
+  int64_t n_rows;
+  const int32_t* medium;
+  int64_t n_medium;
+  const int32_t* longr;
+  int64_t n_long;
+  int short_max;
+  cudaStream_t st;
+};
+
+template <typename T, int H>
+static void gat_fwd(const GatRows& g, const void* sl, const void* sr, float slope, void* alpha) {
+  const T* a = (const T*)sl;
+  const T* b = (const T*)sr;
+  T* out = (T*)alpha;
+  k_gat_fwd_thread<T, H><<<grid_for(g.n_rows * H, 256), 256, 0, g.st>>>(
+      g.offsets, g.cols, g.n_rows, a, b, slope, out, g.short_max);
+  if (g.n_medium)
+    k_gat_fwd_warp<T, H><<<grid_for(g.n_medium, 8, 148 * 32), 256, 0, g.st>>>(
+        g.offsets, g.cols, g.medium, g.n_medium, a, b, slope, out);
+  if (g.n_long)
+    k_gat_fwd_cta<T, H><<<(unsigned)g.n_long, 256, 0, g.st>>>(g.offsets, g.cols, g.longr, a, b,
+                                                              slope, out);
+}
+
+template <typename T, int H>
+static void gat_bwd(const GatRows& g, const void* sl, const void* sr, float slope,
+                    const void* alpha, const void* dalpha, void* de, void* dsl) {
+  const T *a = (const T*)sl, *b = (const T*)sr, *al = (const T*)alpha, *da = (const T*)dalpha;
+  T *o = (T*)de, *ds = (T*)dsl;
+  k_gat_bwd_thread<T, H><<<grid_for(g.n_rows * H, 256), 256, 0, g.st>>>(
+      g.offsets, g.cols, g.n_rows, a, b, slope, al, da, o, ds, g.short_max);
+  if (g.n_medium)
+    k_gat_bwd_warp<T, H><<<grid_for(g.n_medium, 8, 148 * 32), 256, 0, g.st>>>(
+        g.offsets, g.cols, g.medium, g.n_medium, a, b, slope, al, da, o, ds);
+  if (g.n_long)
+    k_gat_bwd_cta<T, H><<<(unsigned)g.n_long, 256, 0, g.st>>>(g.offsets, g.cols, g.longr, a, b,
+                                                              slope, al, da, o, ds);
+}
+
+template <typename T, int H>
+static void gat_sums(const GatRows& g, const void* v, const int32_t* perm, void* out) {
+  const T* vv = (const T*)v;
+  T* o = (T*)out;
+  k_gat_sums_thread<T, H><<<grid_for(g.n_rows * H, 256), 256, 0, g.st>>>(
+      g.offsets, g.n_rows, vv, perm, o, g.short_max);
+  if (g.n_medium)
+    k_gat_sums_warp<T, H><<<grid_for(g.n_medium, 8, 148 * 32), 256, 0, g.st>>>(
+        g.offsets, g.medium, g.n_medium, vv, perm, o);
+  if (g.n_long)
+    k_gat_sums_cta<T, H><<<(unsigned)g.n_long, 256, 0, g.st>>>(g.offsets, g.longr, vv, perm, o);
+}
+
+#define HG_GAT_HEADS(FN, T, ...)                  \
+  switch (heads) {                                \
+    case 1: FN<T, 1>(__VA_ARGS__); break;         \
+    case 2: FN<T, 2>(__VA_ARGS__); break;         \
+    case 4: FN<T, 4>(__VA_ARGS__); break;         \
+    case 8: FN<T, 8>(__VA_ARGS__); break;         \
+    default: FN<T, 16>(__VA_ARGS__); break;       \
+  }
+
+}  // namespace hg
+
+using namespace hg;
+
+static int gat_rows_check(int heads, int dtype, int64_t n_medium, const int32_t* medium,
+                          int64_t n_long, const int32_t* longr, int short_max) {
+  HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
+  HG_REQUIRE(heads >= 1 && heads <= 16 && (heads & (heads - 1)) == 0,
+             "heads must be a power of two <= 16, got %d", heads);
+  HG_REQUIRE((n_medium == 0 || medium) && (n_long == 0 || longr),
+             "row classes listed without index arrays");
+  HG_REQUIRE(short_max >= 0, "short_max must be >= 0");
+  return HG_OK;
+}
+
+extern "C" int hg_gat_attention_fwd(const int64_t* offsets, const int32_t* cols, int64_t n_rows,
+                                    const void* s_l, const void* s_r, int32_t heads, float slope,
+                                    void* alpha, const int32_t* medium_rows, int64_t n_medium,
+                                    const int32_t* long_rows, int64_t n_long, int32_t short_max,
+                                    int dtype, void* stream) {
+  int rc = gat_rows_check(heads, dtype, n_medium, medium_rows, n_long, long_rows, short_max);
+  if (rc) return rc;
+  if (n_rows == 0) return HG_OK;
+  GatRows g{offsets, cols, n_rows, medium_rows, n_medium, long_rows, n_long, short_max,
+            as_stream(stream)};
+  if (dtype == HG_F16) { HG_GAT_HEADS(gat_fwd, __half, g, s_l, s_r, slope, alpha) }
+  else { HG_GAT_HEADS(gat_fwd, float, g, s_l, s_r, slope, alpha) }
+  HG_LAUNCHED();
+  return HG_OK;
+}
+
+extern "C" int hg_gat_attention_bwd(const int64_t* offsets, const int32_t* cols, int64_t n_rows,
+                                    const void* s_l, const void* s_r, int32_t heads, float slope,
+                                    const void* alpha, const void* dalpha, void* de, void* ds_l,
+                                    const int32_t* medium_rows, int64_t n_medium,
+                                    const int32_t* long_rows, int64_t n_long, int32_t short_max,
+                                    int dtype, void* stream) {
+  int rc = gat_rows_check(heads, dtype, n_medium, medium_rows, n_long, long_rows, short_max);
+  if (rc) return rc;
+  if (n_rows == 0) return HG_OK;
+  GatRows g{offsets, cols, n_rows, medium_rows, n_medium, long_rows, n_long, short_max,
+            as_stream(stream)};
+  if (dtype == HG_F16) { HG_GAT_HEADS(gat_bwd, __half, g, s_l, s_r, slope, alpha, dalpha, de, ds_l) }
+  else { HG_GAT_HEADS(gat_bwd, float, g, s_l, s_r, slope, alpha, dalpha, de, ds_l) }
+  HG_LAUNCHED();
+  return HG_OK;
+}
+
+extern "C" int hg_edge_sums_fast(const int64_t* offsets, int64_t n_rows, const void* vals,
+                                 const int32_t* perm, int32_t heads, void* out,
+                                 const int32_t* medium_rows, int64_t n_medium,
+                                 const int32_t* long_rows, int64_t n_long, int32_t short_max,
+                                 int dtype, void* stream) {
+  int rc = gat_rows_check(heads, dtype, n_medium, medium_rows, n_long, long_rows, short_max);
+  if (rc) return rc;
+  if (n_rows == 0) return HG_OK;
+  GatRows g{offsets, nullptr, n_rows, medium_rows, n_medium, long_rows, n_long, short_max,
+            as_stream(stream)};
+  if (dtype == HG_F16) { HG_GAT_HEADS(gat_sums, __half, g, vals, perm, out) }
+  else { HG_GAT_HEADS(gat_sums, float, g, vals, perm, out) }
+  HG_LAUNCHED();
+  return HG_OK;
+}
+
+extern "C" int hg_head_mean(const void* y, int64_t n, int32_t heads, int32_t f, void* out,
+                            int dtype, void* stream) {
+  HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
+  HG_REQUIRE(heads >= 1 && f >= 1, "hg_head_mean: bad shape");
+  if (n == 0) return HG_OK;
+  const int g = grid_for(n * f, 256, 148 * 16);
+  if (dtype == HG_F16)
+    k_head_mean<__half><<<g, 256, 0, as_stream(stream)>>>((const __half*)y, n, heads, f, (__half*)out);
+  else
+    k_head_mean<float><<<g, 256, 0, as_stream(stream)>>>((const float*)y, n, heads, f, (float*)out);
+  HG_LAUNCHED();
+  return HG_OK;
+}
+
+extern "C" int hg_head_mean_bwd(const void* g, int64_t n, int32_t heads, int32_t f, void* gin,
+                                int dtype, void* stream) {
+  HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
+  HG_REQUIRE(heads >= 1 && f >= 1, "hg_head_mean_bwd: bad shape");
+  if (n == 0) return HG_OK;
+  const int gr = grid_for(n * f, 256, 148 * 16);
+  if (dtype == HG_F16)
+    k_head_mean_bwd<__half><<<gr, 256, 0, as_stream(stream)>>>((const __half*)g, n, heads, f, (__half*)gin);
+  else
+    k_head_mean_bwd<float><<<gr, 256, 0, as_stream(stream)>>>((const float*)g, n, heads, f, (float*)gin);
+  HG_LAUNCHED();
+  return HG_OK;
+}

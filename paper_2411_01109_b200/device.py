@@ -28,6 +28,7 @@ DTYPE_CODE = {torch.float16: nat.HG_F16, torch.float32: nat.HG_F32}
 MIRROR = {"none": "none", "left": "right", "right": "left", "both": "both"}
 DEFAULT_SPLIT_CAP = 512
 LONG_ROW = 4096   # rows longer than this get a whole CTA in the row-owned softmax/sum kernels
+SHORT_ROW = 32    # fast GAT kernels: rows up to this many edges get one thread per head
 
 
 def _p(t):
@@ -194,6 +195,18 @@ class CsrView:
             s = build_schedule(self.offsets, split_cap)
             self._sched[split_cap] = s
         return s
+
+    def row_classes(self, short_max: int = SHORT_ROW, long_min: int = LONG_ROW):
+        """(medium, long) int32 row ids: short_max < deg <= long_min, and
+        deg > long_min (cached); the rest run one thread per (row, head)."""
+        key = ("classes", short_max, long_min)
+        t = self._sched.get(key)
+        if t is None:
+            deg = self.offsets[1:] - self.offsets[:-1]
+            med = torch.nonzero((deg > short_max) & (deg <= long_min)).flatten().to(torch.int32)
+            t = (med, self.long_rows(long_min))
+            self._sched[key] = t
+        return t
 
     def long_rows(self, thresh: int = LONG_ROW) -> torch.Tensor:
         """int32 ids of rows with more than `thresh` edges (cached)."""
@@ -465,6 +478,70 @@ def rowsum_view(view: CsrView, v, perm=None):
              heads, _p(out), _p(lr), lr.numel(), LONG_ROW, _dtype_code(v), _stream())
     Probe.launches += 1 + int(lr.numel() > 0)
     return out
+
+
+def _heads_of(s):
+    return s.shape[1] if s.dim() == 2 else 1
+
+
+def gat_attention_fwd(view: CsrView, s_l, s_r, slope=0.2):
+    """Fused fp32-guarded leaky(s_l[r] + s_r[c]) -> edge softmax: alpha [E, H]."""
+    _require_cuda(s_l, s_r)
+    s_l, s_r = s_l.contiguous(), s_r.contiguous()
+    h = _heads_of(s_l)
+    alpha = torch.empty((view.num_edges, h), dtype=s_l.dtype, device=s_l.device)
+    med, lng = view.row_classes()
+    nat.call("hg_gat_attention_fwd", _p(view.offsets), _p(view.cols), view.n_rows, _p(s_l),
+             _p(s_r), h, float(slope), _p(alpha), _p(med), med.numel(), _p(lng), lng.numel(),
+             SHORT_ROW, _dtype_code(s_l), _stream())
+    Probe.launches += 1 + int(med.numel() > 0) + int(lng.numel() > 0)
+    return alpha
+
+
+def gat_attention_bwd(view: CsrView, s_l, s_r, alpha, dalpha, slope=0.2):
+    """(de [E, H], ds_l [N, H]) of gat_attention_fwd."""
+    s_l, s_r = s_l.contiguous(), s_r.contiguous()
+    alpha, dalpha = alpha.contiguous(), dalpha.contiguous().view(alpha.shape)
+    h = _heads_of(s_l)
+    de = torch.empty_like(alpha)
+    ds_l = torch.empty_like(s_l)
+    med, lng = view.row_classes()
+    nat.call("hg_gat_attention_bwd", _p(view.offsets), _p(view.cols), view.n_rows, _p(s_l),
+             _p(s_r), h, float(slope), _p(alpha), _p(dalpha), _p(de), _p(ds_l), _p(med),
+             med.numel(), _p(lng), lng.numel(), SHORT_ROW, _dtype_code(s_l), _stream())
+    Probe.launches += 1 + int(med.numel() > 0) + int(lng.numel() > 0)
+    return de, ds_l
+
+
+def edge_sums_fast(view: CsrView, v, perm=None):
+    """out[r, h] = rnd(sum over row r of v[perm[e] or e, h]), fp32 accumulation."""
+    v = v.contiguous()
+    h = _heads_of(v)
+    out = torch.empty((view.n_rows, h), dtype=v.dtype, device=v.device)
+    med, lng = view.row_classes()
+    nat.call("hg_edge_sums_fast", _p(view.offsets), view.n_rows, _p(v), _p(perm), h, _p(out),
+             _p(med), med.numel(), _p(lng), lng.numel(), SHORT_ROW, _dtype_code(v), _stream())
+    Probe.launches += 1 + int(med.numel() > 0) + int(lng.numel() > 0)
+    return out
+
+
+def head_mean(y, heads):
+    """Mean over concatenated heads, fp64 sum, one rounding: [N, H*f] -> [N, f]."""
+    y = y.contiguous()
+    n, hf = y.shape
+    out = torch.empty((n, hf // heads), dtype=y.dtype, device=y.device)
+    nat.call("hg_head_mean", _p(y), n, heads, hf // heads, _p(out), _dtype_code(y), _stream())
+    Probe.launches += 1
+    return out
+
+
+def head_mean_bwd(g, heads):
+    g = g.contiguous()
+    n, f = g.shape
+    gin = torch.empty((n, heads * f), dtype=g.dtype, device=g.device)
+    nat.call("hg_head_mean_bwd", _p(g), n, heads, f, _p(gin), _dtype_code(g), _stream())
+    Probe.launches += 1
+    return gin
 
 
 def edge_softmax_fwd(dg: DeviceGraph, e):

@@ -166,6 +166,20 @@ class GraphBundle:
         xs = D.bias_scale_rows(h, b, fin)
         return D.spmm_csr(self.dg.view(False), xs, None, None, 1, scaling, None, fout)
 
+    @property
+    def fused_gat(self):
+        """GAT layers may run scores + leaky + softmax as one fp32-guarded pass."""
+        return self.numerics == "fast"
+
+    def gat_attention(self, s_l, s_r, slope):
+        return D.gat_attention_fwd(self.dg.view(False), s_l, s_r, slope)
+
+    def gat_attention_bwd(self, s_l, s_r, alpha, g, slope):
+        """(ds_l, ds_r): row sums on the CSR, column sums through the CSC + perm."""
+        de, ds_l = D.gat_attention_bwd(self.dg.view(False), s_l, s_r, alpha, g, slope)
+        bwd = self.dg.view(True)
+        return ds_l, D.edge_sums_fast(bwd, de, bwd.perm)
+
     def sddmm(self, x, y, heads=1):
         return D.sddmm(self.dg, x, y, heads=heads)
 
@@ -298,6 +312,24 @@ class _ScoresFn(torch.autograd.Function):
         gl = b.edge_sums(g, transpose=False) if ctx.needs_input_grad[0] else None
         gr = b.edge_sums(g, transpose=True) if ctx.needs_input_grad[1] else None
         return gl, gr, None, None
+
+
+class _GatAttnFn(torch.autograd.Function):
+    """leaky(s_l[r] + s_r[c]) -> edge softmax in one fp32-guarded pass
+    (models.py:188-200, 317-340, 382-412; numerics="fast")."""
+
+    @staticmethod
+    def forward(ctx, s_l, s_r, bundle, slope):
+        ctx.bundle, ctx.slope = bundle, slope
+        alpha = bundle.gat_attention(s_l, s_r, slope)
+        ctx.save_for_backward(s_l, s_r, alpha)
+        return alpha
+
+    @staticmethod
+    def backward(ctx, g):
+        s_l, s_r, alpha = ctx.saved_tensors
+        ds_l, ds_r = ctx.bundle.gat_attention_bwd(s_l, s_r, alpha, g, ctx.slope)
+        return ds_l, ds_r, None, None
 
 
 def attention_scores(bundle, s_l, s_r):
@@ -617,8 +649,13 @@ class GATLayer:
         # s = z_h . a_h for every head (models.matmul semantics: fp32
         # accumulation of exact products, one rounding), one kernel
         s_l, s_r = _HeadDotsFn.apply(z, a_l, a_r, h, bundle)
-        e = attention_logits(bundle, s_l, s_r, 0.2)               # [E, H]
-        alpha = edge_softmax(bundle, e, overflow, tag + "/softmax")
+        if getattr(bundle, "fused_gat", False):
+            alpha = _GatAttnFn.apply(s_l, s_r, bundle, 0.2)       # [E, H]
+            if overflow is not None:
+                overflow.observe(tag + "/softmax", alpha.detach())
+        else:
+            e = attention_logits(bundle, s_l, s_r, 0.2)           # [E, H]
+            alpha = edge_softmax(bundle, e, overflow, tag + "/softmax")
         out = spmm_weighted(bundle, alpha if h > 1 else alpha[:, 0], z, width, overflow, tag)
         if self.reduce == "mean" and h > 1:
             return _HeadMeanFn.apply(out, h)
@@ -649,11 +686,15 @@ class _HeadMeanFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, y, heads):
         ctx.heads = heads
+        if y.is_cuda:
+            return D.head_mean(y, heads)
         n, f = y.shape
         return (y.view(n, heads, f // heads).double().sum(1) / heads).to(y.dtype)
 
     @staticmethod
     def backward(ctx, g):
+        if g.is_cuda:
+            return D.head_mean_bwd(g, ctx.heads), None
         gg = (g.double() / ctx.heads).to(g.dtype)
         return gg.repeat(1, ctx.heads), None
 

@@ -515,3 +515,82 @@ def test_spmm_fast_row_strides(cuda, f, ld):
     assert torch.equal(got, want)
     assert torch.equal(ybuf[:, :f], want)
     assert bool((ybuf[:, f:] == 7.0).all())
+
+
+# ── fp32-guarded GAT attention (numerics="fast") ─────────────────────────
+
+
+def _hub_graph(seed, n=6000):
+    """Degrees covering all three row classes: <= 32, (32, 4096], > 4096."""
+    rng = np.random.default_rng(seed)
+    deg = np.minimum(rng.zipf(1.8, n), 3000)
+    deg[:3] = [5000, 4097, 4096]
+    deg[3:6] = [33, 32, 0]
+    rows = np.repeat(np.arange(n), deg)
+    return O.canonical_edges(n, rows, rng.integers(0, n, rows.size))
+
+
+@pytest.mark.parametrize("heads", [1, 4, 8])
+def test_gat_attention_fast_vs_f64(cuda, heads):
+    from paper_2411_01109_b200 import device as D
+
+    n = 6000
+    r, c = _hub_graph(heads, n)
+    dg = _dg(n, r, c, cuda)
+    rng = np.random.default_rng(heads)
+    sl = rng.normal(0, 3, (n, heads)).astype(np.float16)
+    sr = rng.normal(0, 3, (n, heads)).astype(np.float16)
+    alpha = D.gat_attention_fwd(dg.view(False), _t(sl, cuda), _t(sr, cuda), 0.2).cpu().numpy()
+    # float64 reference
+    lg = sl.astype(np.float64)[r] + sr.astype(np.float64)[c]
+    lg = np.where(lg > 0, lg, 0.2 * lg)
+    off = O.csr_offsets(n, r)
+    want = np.zeros_like(lg)
+    for v in range(n):
+        s, e = off[v], off[v + 1]
+        if e > s:
+            z = np.exp(lg[s:e] - lg[s:e].max(0))
+            want[s:e] = z / z.sum(0)
+    a = alpha.astype(np.float64)
+    assert np.all(np.abs(a - want) <= 2.0 ** -10 * want + 1e-7)
+    # rows sum to 1 within fp16 rounding
+    rs = np.add.reduceat(a, off[:-1][np.diff(off) > 0], axis=0)
+    assert np.all(np.abs(rs - 1.0) <= 2e-3)
+
+    # backward: de = alpha (g - sum alpha g) leaky'(l); ds_l / ds_r row / col sums
+    g = rng.normal(0, 1, (r.size, heads)).astype(np.float16)
+    de, dsl = D.gat_attention_bwd(dg.view(False), _t(sl, cuda), _t(sr, cuda), _t(alpha, cuda),
+                                  _t(g, cuda), 0.2)
+    gg = g.astype(np.float64)
+    dd = np.zeros_like(gg)
+    for v in range(n):
+        s, e = off[v], off[v + 1]
+        if e > s:
+            dd[s:e] = a[s:e] * (gg[s:e] - (a[s:e] * gg[s:e]).sum(0))
+    raw = sl.astype(np.float64)[r] + sr.astype(np.float64)[c]
+    dd = np.where(raw > 0, dd, 0.2 * dd)
+    de = de.cpu().numpy().astype(np.float64)
+    assert np.all(np.abs(de - dd) <= 2.0 ** -10 * np.abs(dd) + 2e-4)
+    want_l = np.zeros((n, heads))
+    np.add.at(want_l, r, dd)
+    got_l = dsl.cpu().numpy().astype(np.float64)
+    assert np.all(np.abs(got_l - want_l) <= 2e-3 * np.maximum(1, np.abs(want_l)))
+    bwd = dg.view(True)
+    got_r = D.edge_sums_fast(bwd, _t(de.astype(np.float16), cuda), bwd.perm).cpu().numpy()
+    want_r = np.zeros((n, heads))
+    np.add.at(want_r, c, de)
+    assert np.all(np.abs(got_r.astype(np.float64) - want_r) <= 2e-3 * np.maximum(1, np.abs(want_r)))
+
+
+@pytest.mark.parametrize("heads,f", [(4, 16), (2, 3), (8, 8)])
+def test_head_mean_bits(cuda, heads, f):
+    from paper_2411_01109_b200 import device as D
+
+    rng = np.random.default_rng(f)
+    y = rng.normal(0, 100, (777, heads * f)).astype(np.float16)
+    got = D.head_mean(_t(y, cuda), heads).cpu().numpy()
+    want = (y.reshape(777, heads, f).astype(np.float64).sum(1) / heads).astype(np.float16)
+    np.testing.assert_array_equal(bits(got), bits(want))
+    g = rng.normal(0, 1, (777, f)).astype(np.float16)
+    gin = D.head_mean_bwd(_t(g, cuda), heads).cpu().numpy()
+    np.testing.assert_array_equal(bits(gin), bits(np.tile((g.astype(np.float64) / heads).astype(np.float16), (1, heads))))
