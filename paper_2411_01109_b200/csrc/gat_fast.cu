@@ -24,16 +24,7 @@ namespace hg {
 
 __device__ __forceinline__ float leaky_f(float v, float slope) { return v > 0.0f ? v : v * slope; }
 
-// online softmax state (m, s): s = sum exp(v - m)
-__device__ __forceinline__ void ms_push(float& m, float& s, float v) {
-  if (v > m) {
-    s = s * expf(m - v) + 1.0f;
-    m = v;
-  } else {
-    s += expf(v - m);
-  }
-}
-
+// merge two online-softmax states (m, s), s = sum exp(v - m)
 __device__ __forceinline__ void ms_merge(float& m, float& s, float m2, float s2) {
   const float mm = fmaxf(m, m2);
   if (mm == -INFINITY) return;
@@ -59,6 +50,127 @@ __device__ __forceinline__ float sum_warp(float v) {
   return v;
 }
 
+// All edge loops below visit edges e = first, first + step, ... in groups of
+// U (independent column-id loads, then independent gathers: the dependent
+// cols -> s_r chain is the latency that bounds these kernels).
+constexpr int U = 4;
+
+// online (max, sum) over the logits of the edges this thread visits
+template <typename T, int H>
+__device__ __forceinline__ void fwd_pass1(const int32_t* __restrict__ cols, const T* __restrict__ sr,
+                                          int64_t first, int64_t end, int64_t step, int h,
+                                          float a, float slope, float& m, float& s) {
+  for (int64_t e0 = first; e0 < end; e0 += step * U) {
+    int c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = e0 + u * step < end ? __ldg(cols + e0 + u * step) : -1;
+    float v[U];
+    float mu = -INFINITY;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      v[u] = c[u] >= 0 ? leaky_f(a + Num<T>::to_f(sr[(int64_t)c[u] * H + h]), slope) : -INFINITY;
+      mu = fmaxf(mu, v[u]);
+    }
+    if (mu > m) {
+      s = m == -INFINITY ? 0.0f : s * expf(m - mu);
+      m = mu;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (c[u] >= 0) s += expf(v[u] - m);
+  }
+}
+
+template <typename T, int H>
+__device__ __forceinline__ void fwd_pass2(const int32_t* __restrict__ cols, const T* __restrict__ sr,
+                                          int64_t first, int64_t end, int64_t step, int h,
+                                          float a, float slope, float m, float inv,
+                                          T* __restrict__ alpha) {
+  for (int64_t e0 = first; e0 < end; e0 += step * U) {
+    int c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = e0 + u * step < end ? __ldg(cols + e0 + u * step) : -1;
+    float v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      v[u] = c[u] >= 0 ? leaky_f(a + Num<T>::to_f(sr[(int64_t)c[u] * H + h]), slope) : 0.0f;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (c[u] >= 0) alpha[(e0 + u * step) * H + h] = Num<T>::from_f(expf(v[u] - m) * inv);
+  }
+}
+
+// D = sum alpha * dalpha over the visited edges
+template <typename T, int H>
+__device__ __forceinline__ float bwd_pass1(const T* __restrict__ alpha, const T* __restrict__ dalpha,
+                                           int64_t first, int64_t end, int64_t step, int h) {
+  float d = 0.0f;
+  for (int64_t e0 = first; e0 < end; e0 += step * U) {
+    float x[U], y[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + u * step;
+      x[u] = e < end ? Num<T>::to_f(alpha[e * H + h]) : 0.0f;
+      y[u] = e < end ? Num<T>::to_f(dalpha[e * H + h]) : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) d = fmaf(x[u], y[u], d);
+  }
+  return d;
+}
+
+// de = alpha (dalpha - D) leaky'(l); returns the thread's sum of de
+template <typename T, int H>
+__device__ __forceinline__ float bwd_pass2(const int32_t* __restrict__ cols, const T* __restrict__ sr,
+                                           const T* __restrict__ alpha, const T* __restrict__ dalpha,
+                                           int64_t first, int64_t end, int64_t step, int h, float a,
+                                           float slope, float d, T* __restrict__ de) {
+  float acc = 0.0f;
+  for (int64_t e0 = first; e0 < end; e0 += step * U) {
+    int c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = e0 + u * step < end ? __ldg(cols + e0 + u * step) : -1;
+    float sv[U], x[U], y[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + u * step;
+      sv[u] = c[u] >= 0 ? Num<T>::to_f(sr[(int64_t)c[u] * H + h]) : 0.0f;
+      x[u] = c[u] >= 0 ? Num<T>::to_f(alpha[e * H + h]) : 0.0f;
+      y[u] = c[u] >= 0 ? Num<T>::to_f(dalpha[e * H + h]) : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (c[u] >= 0) {
+        float g = x[u] * (y[u] - d);
+        g = a + sv[u] > 0.0f ? g : g * slope;
+        de[(e0 + u * step) * H + h] = Num<T>::from_f(g);
+        acc += g;
+      }
+    }
+  }
+  return acc;
+}
+
+template <typename T, int H>
+__device__ __forceinline__ float sums_pass(const T* __restrict__ v, const int32_t* __restrict__ perm,
+                                           int64_t first, int64_t end, int64_t step, int h) {
+  float acc = 0.0f;
+  for (int64_t e0 = first; e0 < end; e0 += step * U) {
+    int64_t idx[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + u * step;
+      idx[u] = e < end ? (perm ? (int64_t)__ldg(perm + e) : e) : -1;
+    }
+    float x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) x[u] = idx[u] >= 0 ? Num<T>::to_f(v[idx[u] * H + h]) : 0.0f;
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc += x[u];
+  }
+  return acc;
+}
+
 // ---------------------------------------------------------------- forward
 
 template <typename T, int H>
@@ -74,13 +186,8 @@ k_gat_fwd_thread(const int64_t* __restrict__ offsets, const int32_t* __restrict_
   if (end == beg || end - beg > short_max) return;
   const float a = Num<T>::to_f(sl[t]);
   float m = -INFINITY, s = 0.0f;
-  for (int64_t e = beg; e < end; ++e)
-    ms_push(m, s, leaky_f(a + Num<T>::to_f(sr[(int64_t)cols[e] * H + h]), slope));
-  const float inv = 1.0f / s;
-  for (int64_t e = beg; e < end; ++e) {
-    const float v = leaky_f(a + Num<T>::to_f(sr[(int64_t)cols[e] * H + h]), slope);
-    alpha[e * H + h] = Num<T>::from_f(expf(v - m) * inv);
-  }
+  fwd_pass1<T, H>(cols, sr, beg, end, 1, h, a, slope, m, s);
+  fwd_pass2<T, H>(cols, sr, beg, end, 1, h, a, slope, m, 1.0f / s, alpha);
 }
 
 template <typename T, int H>
@@ -97,14 +204,9 @@ k_gat_fwd_warp(const int64_t* __restrict__ offsets, const int32_t* __restrict__ 
     const int64_t beg = offsets[r], end = offsets[r + 1];
     const float a = Num<T>::to_f(sl[r * H + h]);
     float m = -INFINITY, s = 0.0f;
-    for (int64_t e = beg + j; e < end; e += EPB)
-      ms_push(m, s, leaky_f(a + Num<T>::to_f(sr[(int64_t)cols[e] * H + h]), slope));
+    fwd_pass1<T, H>(cols, sr, beg + j, end, EPB, h, a, slope, m, s);
     ms_warp<H>(m, s);
-    const float inv = 1.0f / s;
-    for (int64_t e = beg + j; e < end; e += EPB) {
-      const float v = leaky_f(a + Num<T>::to_f(sr[(int64_t)cols[e] * H + h]), slope);
-      alpha[e * H + h] = Num<T>::from_f(expf(v - m) * inv);
-    }
+    fwd_pass2<T, H>(cols, sr, beg + j, end, EPB, h, a, slope, m, 1.0f / s, alpha);
   }
 }
 
@@ -120,19 +222,14 @@ k_gat_fwd_cta(const int64_t* __restrict__ offsets, const int32_t* __restrict__ c
   const int64_t beg = offsets[r], end = offsets[r + 1];
   const float a = Num<T>::to_f(sl[r * H + h]);
   float m = -INFINITY, s = 0.0f;
-  for (int64_t e = beg + j; e < end; e += EPB)
-    ms_push(m, s, leaky_f(a + Num<T>::to_f(sr[(int64_t)cols[e] * H + h]), slope));
+  fwd_pass1<T, H>(cols, sr, beg + j, end, EPB, h, a, slope, m, s);
   ms_warp<H>(m, s);
   if (lane < H) { sm[warp][lane] = m; ss[warp][lane] = s; }
   __syncthreads();
   float mt = sm[0][h], st = ss[0][h];
 #pragma unroll
   for (int k = 1; k < 8; ++k) ms_merge(mt, st, sm[k][h], ss[k][h]);
-  const float inv = 1.0f / st;
-  for (int64_t e = beg + j; e < end; e += EPB) {
-    const float v = leaky_f(a + Num<T>::to_f(sr[(int64_t)cols[e] * H + h]), slope);
-    alpha[e * H + h] = Num<T>::from_f(expf(v - mt) * inv);
-  }
+  fwd_pass2<T, H>(cols, sr, beg + j, end, EPB, h, a, slope, mt, 1.0f / st, alpha);
 }
 
 // --------------------------------------------------------------- backward
@@ -149,19 +246,9 @@ k_gat_bwd_thread(const int64_t* __restrict__ offsets, const int32_t* __restrict_
   const int h = (int)(t - r * H);
   const int64_t beg = offsets[r], end = offsets[r + 1];
   if (end - beg > short_max) return;
-  float d = 0.0f;
-  for (int64_t e = beg; e < end; ++e)
-    d = fmaf(Num<T>::to_f(alpha[e * H + h]), Num<T>::to_f(dalpha[e * H + h]), d);
+  const float d = bwd_pass1<T, H>(alpha, dalpha, beg, end, 1, h);
   const float a = Num<T>::to_f(sl[t]);
-  float acc = 0.0f;
-  for (int64_t e = beg; e < end; ++e) {
-    const float v = a + Num<T>::to_f(sr[(int64_t)cols[e] * H + h]);
-    float g = Num<T>::to_f(alpha[e * H + h]) * (Num<T>::to_f(dalpha[e * H + h]) - d);
-    g = v > 0.0f ? g : g * slope;
-    de[e * H + h] = Num<T>::from_f(g);
-    acc += g;
-  }
-  dsl[t] = Num<T>::from_f(acc);
+  dsl[t] = Num<T>::from_f(bwd_pass2<T, H>(cols, sr, alpha, dalpha, beg, end, 1, h, a, slope, d, de));
 }
 
 template <typename T, int H>
@@ -177,20 +264,10 @@ k_gat_bwd_warp(const int64_t* __restrict__ offsets, const int32_t* __restrict__ 
        w += nwarps) {
     const int64_t r = rows[w];
     const int64_t beg = offsets[r], end = offsets[r + 1];
-    float d = 0.0f;
-    for (int64_t e = beg + j; e < end; e += EPB)
-      d = fmaf(Num<T>::to_f(alpha[e * H + h]), Num<T>::to_f(dalpha[e * H + h]), d);
-    d = sum_warp<H>(d);
+    const float d = sum_warp<H>(bwd_pass1<T, H>(alpha, dalpha, beg + j, end, EPB, h));
     const float a = Num<T>::to_f(sl[r * H + h]);
-    float acc = 0.0f;
-    for (int64_t e = beg + j; e < end; e += EPB) {
-      const float v = a + Num<T>::to_f(sr[(int64_t)cols[e] * H + h]);
-      float g = Num<T>::to_f(alpha[e * H + h]) * (Num<T>::to_f(dalpha[e * H + h]) - d);
-      g = v > 0.0f ? g : g * slope;
-      de[e * H + h] = Num<T>::from_f(g);
-      acc += g;
-    }
-    acc = sum_warp<H>(acc);
+    const float acc = sum_warp<H>(
+        bwd_pass2<T, H>(cols, sr, alpha, dalpha, beg + j, end, EPB, h, a, slope, d, de));
     if (lane < H) dsl[r * H + lane] = Num<T>::from_f(acc);
   }
 }
@@ -219,20 +296,10 @@ k_gat_bwd_cta(const int64_t* __restrict__ offsets, const int32_t* __restrict__ c
   const int tid = threadIdx.x, j = tid / H, h = tid % H;
   const int64_t r = rows[blockIdx.x];
   const int64_t beg = offsets[r], end = offsets[r + 1];
-  float d = 0.0f;
-  for (int64_t e = beg + j; e < end; e += EPB)
-    d = fmaf(Num<T>::to_f(alpha[e * H + h]), Num<T>::to_f(dalpha[e * H + h]), d);
-  d = block_sum_h<H>(d, red);
+  const float d = block_sum_h<H>(bwd_pass1<T, H>(alpha, dalpha, beg + j, end, EPB, h), red);
   const float a = Num<T>::to_f(sl[r * H + h]);
-  float acc = 0.0f;
-  for (int64_t e = beg + j; e < end; e += EPB) {
-    const float v = a + Num<T>::to_f(sr[(int64_t)cols[e] * H + h]);
-    float g = Num<T>::to_f(alpha[e * H + h]) * (Num<T>::to_f(dalpha[e * H + h]) - d);
-    g = v > 0.0f ? g : g * slope;
-    de[e * H + h] = Num<T>::from_f(g);
-    acc += g;
-  }
-  acc = block_sum_h<H>(acc, red);
+  const float acc = block_sum_h<H>(
+      bwd_pass2<T, H>(cols, sr, alpha, dalpha, beg + j, end, EPB, h, a, slope, d, de), red);
   if (tid < H) dsl[r * H + tid] = Num<T>::from_f(acc);
 }
 
@@ -248,12 +315,7 @@ k_gat_sums_thread(const int64_t* __restrict__ offsets, int64_t n_rows, const T* 
   const int h = (int)(t - r * H);
   const int64_t beg = offsets[r], end = offsets[r + 1];
   if (end - beg > short_max) return;
-  float acc = 0.0f;
-  for (int64_t e = beg; e < end; ++e) {
-    const int64_t i = perm ? (int64_t)perm[e] : e;
-    acc += Num<T>::to_f(v[i * H + h]);
-  }
-  out[t] = Num<T>::from_f(acc);
+  out[t] = Num<T>::from_f(sums_pass<T, H>(v, perm, beg, end, 1, h));
 }
 
 template <typename T, int H>
@@ -268,12 +330,7 @@ k_gat_sums_warp(const int64_t* __restrict__ offsets, const int32_t* __restrict__
        w += nwarps) {
     const int64_t r = rows[w];
     const int64_t beg = offsets[r], end = offsets[r + 1];
-    float acc = 0.0f;
-    for (int64_t e = beg + j; e < end; e += EPB) {
-      const int64_t i = perm ? (int64_t)perm[e] : e;
-      acc += Num<T>::to_f(v[i * H + h]);
-    }
-    acc = sum_warp<H>(acc);
+    const float acc = sum_warp<H>(sums_pass<T, H>(v, perm, beg + j, end, EPB, h));
     if (lane < H) out[r * H + lane] = Num<T>::from_f(acc);
   }
 }
@@ -287,12 +344,7 @@ k_gat_sums_cta(const int64_t* __restrict__ offsets, const int32_t* __restrict__ 
   const int tid = threadIdx.x, j = tid / H, h = tid % H;
   const int64_t r = rows[blockIdx.x];
   const int64_t beg = offsets[r], end = offsets[r + 1];
-  float acc = 0.0f;
-  for (int64_t e = beg + j; e < end; e += EPB) {
-    const int64_t i = perm ? (int64_t)perm[e] : e;
-    acc += Num<T>::to_f(v[i * H + h]);
-  }
-  acc = block_sum_h<H>(acc, red);
+  const float acc = block_sum_h<H>(sums_pass<T, H>(v, perm, beg + j, end, EPB, h), red);
   if (tid < H) out[r * H + tid] = Num<T>::from_f(acc);
 }
 
