@@ -227,6 +227,25 @@ int hg_adam_step(float* master, float* m, float* v, const void* grad, int grad_d
                  int64_t count, float lr, float omb1, float omb2, double b1, double b2,
                  float eps, const double* step, float grad_unscale, void* stream);
 
+/* ----------------------------------------------------------------- ingest */
+
+/* sparse.load_edge_list (sparse.py:143-177) on the GPU.  `text` is the file's
+ * bytes in device memory.  hg_count_lines -> *n_lines_out (HOST) = number of
+ * lines under Python universal newlines ('\n', '\r\n', lone '\r'); then
+ * hg_parse_edges writes the edge lines' (src, dst) in file order to rows_out /
+ * cols_out (capacity n_lines each) and result (HOST int64[4]) = {num_edges,
+ * max id (-1 if none), first bad line (1-based, 0 if none), code}: code 2 =
+ * "expected 'src dst'", 3 = "non-integer vertex id", 4 = "negative vertex id",
+ * 5 = id beyond int64 (reported after every line error, like the reference's
+ * np.asarray overflow).  Whitespace is ASCII (str.split on ' ', \t-\r,
+ * \x1c-\x1f); fields follow int() syntax ([+-]digits, single '_' between digits). */
+int hg_count_lines_workspace(int64_t nbytes, size_t* bytes);
+int hg_count_lines(const void* text, int64_t nbytes, int64_t* n_lines_out, void* ws,
+                   size_t ws_bytes, void* stream);
+int hg_parse_edges_workspace(int64_t nbytes, int64_t n_lines, size_t* bytes);
+int hg_parse_edges(const void* text, int64_t nbytes, int64_t n_lines, int64_t* rows_out,
+                   int64_t* cols_out, int64_t* result, void* ws, size_t ws_bytes, void* stream);
+
 /* ------------------------------------------- fp32-guarded GAT ("fast" numerics) */
 
 /* Row classes for the row-owned fast kernels: rows with <= short_max edges run

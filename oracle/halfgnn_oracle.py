@@ -44,6 +44,43 @@ def canonical_edges(n, rows, cols):
     return keys // n, keys % n
 
 
+def load_edge_list_text(text: bytes, num_vertices=None, symmetrize_edges=False, where="<path>"):
+    """sparse.load_edge_list (sparse.py:143-177) over the file's bytes: Python
+    universal-newline lines, str.strip / str.split fields, int() ids, the same
+    errors and messages.  Returns (n, rows, cols) canonical."""
+    import io
+
+    src, dst = [], []
+    for lineno, line in enumerate(io.TextIOWrapper(io.BytesIO(text), newline=None), start=1):
+        t = line.strip()
+        if not t or t[0] in "#%":
+            continue
+        parts = t.split()
+        if len(parts) < 2:
+            raise ValueError(f"{where}:{lineno}: expected 'src dst'")
+        try:
+            a, b = int(parts[0]), int(parts[1])
+        except ValueError as exc:
+            raise ValueError(f"{where}:{lineno}: non-integer vertex id") from exc
+        if a < 0 or b < 0:
+            raise ValueError(f"{where}:{lineno}: negative vertex id")
+        src.append(a)
+        dst.append(b)
+    rows = np.asarray(src, dtype=np.int64)
+    cols = np.asarray(dst, dtype=np.int64)
+    n = int(num_vertices) if num_vertices is not None else int(
+        max(rows.max(initial=-1), cols.max(initial=-1)) + 1)
+    if n <= 0:
+        raise ValueError(f"{where}: empty graph and no vertex count given")
+    if rows.size and max(rows.max(), cols.max()) >= n:
+        bad = np.argmax((rows >= n) | (cols >= n))
+        raise ValueError(f"{where}: vertex id out of range at edge {bad}")
+    r, c = canonical_edges(n, rows, cols)
+    if symmetrize_edges:
+        r, c = symmetrize(n, r, c)
+    return n, r, c
+
+
 def csr_offsets(n, rows):
     """coo_to_csr (sparse.py:97-101): offsets = [0, cumsum(bincount(rows))]."""
     off = np.zeros(n + 1, dtype=np.int64)

@@ -122,6 +122,52 @@ def build_csr(n: int, rows: torch.Tensor, cols: torch.Tensor, want_rows: bool = 
     return offsets, out_cols[:e], (out_rows[:e] if want_rows else None)
 
 
+_INGEST_ERRORS = {2: "expected 'src dst'", 3: "non-integer vertex id", 4: "negative vertex id"}
+
+
+def read_bytes_device(path, device="cuda") -> torch.Tensor:
+    """A file's bytes as a uint8 tensor in HBM (pinned staging, one copy)."""
+    import os
+
+    nbytes = os.path.getsize(path)
+    host = torch.empty(nbytes, dtype=torch.uint8).pin_memory() if nbytes else torch.empty(0, dtype=torch.uint8)
+    if nbytes:
+        with open(path, "rb") as fh:
+            got = fh.readinto(memoryview(host.numpy()))
+        if got != nbytes:
+            raise OSError(f"{path}: short read ({got} of {nbytes} bytes)")
+    return host.to(device, non_blocking=False)
+
+
+def parse_edge_text(text: torch.Tensor, where: str = "<text>"):
+    """GPU parse of edge-list text (hg_count_lines + hg_parse_edges): returns
+    (rows int64, cols int64, max_id) on the text's device, in file order.
+    Raises ValueError("{where}:{line}: ...") like sparse.load_edge_list."""
+    _require_cuda(text)
+    if text.dtype != torch.uint8 or text.dim() != 1:
+        raise ValueError("text must be a 1-D uint8 tensor")
+    dev = text.device
+    nbytes = text.numel()
+    n_lines = ctypes.c_int64(0)
+    ws = workspace(nat.size_query("hg_count_lines_workspace", nbytes), dev)
+    nat.call("hg_count_lines", _p(text), nbytes, ctypes.byref(n_lines), _p(ws),
+             0 if ws is None else ws.numel(), _stream())
+    lines = int(n_lines.value)
+    ws = workspace(nat.size_query("hg_parse_edges_workspace", nbytes, lines), dev)
+    rows = torch.empty(max(lines, 1), dtype=torch.int64, device=dev)
+    cols = torch.empty(max(lines, 1), dtype=torch.int64, device=dev)
+    res = (ctypes.c_int64 * 4)()
+    nat.call("hg_parse_edges", _p(text), nbytes, lines, _p(rows), _p(cols), res, _p(ws),
+             0 if ws is None else ws.numel(), _stream())
+    Probe.launches += 4
+    m, top, bad_line, code = (int(v) for v in res)
+    if code == 5:
+        raise OverflowError(f"{where}: vertex id does not fit in int64")
+    if code:
+        raise ValueError(f"{where}:{bad_line}: {_INGEST_ERRORS[code]}")
+    return rows[:m], cols[:m], top
+
+
 def transpose_csr(offsets: torch.Tensor, cols: torch.Tensor, n: int):
     """transpose(g, return_perm=True) on the GPU.  Returns (t_offsets, t_cols, perm)."""
     m = cols.numel()
@@ -243,6 +289,23 @@ class DeviceGraph:
     @property
     def perm(self):
         return self.bwd.perm
+
+    @classmethod
+    def from_edge_list(cls, path, num_vertices=None, symmetrize_edges=False, device="cuda",
+                       build_transpose=True):
+        """load_edge_list (sparse.py:143-177) entirely on the GPU: file bytes to
+        HBM, parse, validate, canonicalise; nothing but errors returns to the host."""
+        rows, cols, top = parse_edge_text(read_bytes_device(path, device), str(path))
+        n = int(num_vertices) if num_vertices is not None else top + 1
+        if n <= 0:
+            raise ValueError(f"{path}: empty graph and no vertex count given")
+        if rows.numel() and top >= n:
+            bad = int(torch.nonzero((rows >= n) | (cols >= n))[0, 0])
+            raise ValueError(f"{path}: vertex id out of range at edge {bad}")
+        if symmetrize_edges:
+            rows, cols = torch.cat([rows, cols]), torch.cat([cols, rows])
+        offsets, c32, _ = build_csr(n, rows, cols)
+        return cls(n, offsets, c32, build_transpose=build_transpose)
 
     @classmethod
     def from_edges(cls, n, rows, cols, device="cuda", build_transpose=True):

@@ -335,7 +335,81 @@ def gen_training():
     save("training.npz", **d)
 
 
+INGEST_CASES = [
+    # (text, num_vertices, symmetrize)
+    (b"# a comment\n0 1\n% another\n1 2\n\n2 0\n", None, False),    # test_sparse.py:127-131
+    (b"0 1\nnot an edge\n", None, False),                               # :133-137
+    (b"0\n", None, False),                                              # :139-143
+    (b"0 1\n", 10, False),                                              # :145-148
+    (b"0 1\n", None, True),                                             # :150-154
+    (b"0 1\r\n1 2\r\n2 x\r\n", None, False),
+    (b"0 1\r1 2\r3 -4\n", None, False),
+    (b"  0\t 1  extra\n\t2 3 4 5\n\n   \n", None, False),
+    (b"1_0 +2\n-0 003\n", None, False),
+    (b"1__0 2\n", None, False),
+    (b"_1 2\n", None, False),
+    (b"1_ 2\n", None, False),
+    (b"0 5\n", 3, False),
+    (b"", None, False),
+    (b"# only\n% comments\n", None, False),
+    (b"# only\n", 4, False),
+    (b"1 1\n0 1\n0 1\n", None, False),
+    (b"0 1\n1 2", None, False),
+    (b"0\x0b1\n2\x0c3\n4\x1f5\n", None, False),
+    (b"0 1 # trailing\n#c\n  # indented\n2 1", None, True),
+    (b"3 4\n1 2\n5 -1 x\n", None, False),
+    (b"3 4\nx\n5 -1\n", None, False),
+    (b"7 8\n+ 1\n", None, False),
+    (b"7 8\n- 1\n", None, False),
+    (b"0 99999999999999999999\n1 2\n", None, False),
+    (b"0 99999999999999999999\nbad line\n", None, False),
+    (b"-99999999999999999999 1\n", None, False),
+    (b"\r\n\r\n0 1\r\n\r", None, False),
+    (b"0 1\n2 3\n", 3, False),
+]
+
+
+def gen_ingest():
+    """sparse.load_edge_list on small texts (the loader tests plus whitespace,
+    newline, int() syntax, error-order and overflow cases) and one large
+    randomized file; errors recorded as '<Type>: <message>' with the path
+    replaced by '<path>'."""
+    import tempfile
+
+    rng = np.random.default_rng(11)
+    parts = []
+    for i in range(3000):
+        k = rng.integers(0, 20)
+        if k == 0:
+            parts.append(b"# comment line\n")
+        elif k == 1:
+            parts.append(b"\n")
+        else:
+            ws = [b" ", b"\t", b"  ", b" \t "][rng.integers(0, 4)]
+            parts.append(b"%d%s%d%s" % (rng.integers(0, 500), ws, rng.integers(0, 500),
+                                         [b"\n", b"\r\n", b" \n"][rng.integers(0, 3)]))
+    cases = INGEST_CASES + [(b"".join(parts), None, False), (b"".join(parts), 600, True)]
+    d = {"num_cases": np.int64(len(cases))}
+    with tempfile.TemporaryDirectory() as tmp:
+        for i, (text, nv, sym) in enumerate(cases):
+            p = Path(tmp) / f"c{i}.txt"
+            p.write_bytes(text)
+            d[f"c{i}_text"] = np.frombuffer(text, dtype=np.uint8).copy()
+            d[f"c{i}_nv"] = np.int64(-1 if nv is None else nv)
+            d[f"c{i}_sym"] = np.bool_(sym)
+            try:
+                g = sp.load_edge_list(p, num_vertices=nv, symmetrize_edges=sym)
+                d[f"c{i}_n"] = np.int64(g.n)
+                d[f"c{i}_rows"], d[f"c{i}_cols"] = g.rows, g.cols
+                d[f"c{i}_err"] = np.str_("")
+            except Exception as exc:  # record the reference's failure
+                d[f"c{i}_n"] = np.int64(-1)
+                d[f"c{i}_err"] = np.str_(f"{type(exc).__name__}: {str(exc).replace(str(p), '<path>')}")
+    save("ingest.npz", **d)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["graph", "factors", "spmm", "vertex", "sddmm", "attention", "training"]
+    which = sys.argv[1:] or ["graph", "factors", "spmm", "vertex", "sddmm", "attention", "training",
+                             "ingest"]
     for w in which:
         globals()[f"gen_{w}" if w != "graph" else "gen_graph_build"]()

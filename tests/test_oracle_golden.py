@@ -178,3 +178,21 @@ def test_schedule_units_cover_each_edge_once():
         cls = np.where(lens > 0, np.floor(np.log2(np.maximum(lens, 1))) + 1, 0)
         assert np.all(np.diff(cls) <= 0)  # long classes first
         assert slots == int(split_rows[:, 2].sum()) if split_rows.size else slots == 0
+
+
+def test_edge_list_loader_golden():
+    """oracle.load_edge_list_text == the reference's sparse.load_edge_list on
+    every recorded text (values and error type/message)."""
+    cases, _ = golden_cases("ingest.npz")
+    for i, c in enumerate(cases):
+        nv = None if int(c["nv"]) < 0 else int(c["nv"])
+        text = c["text"].tobytes()
+        if str(c["err"]):
+            with pytest.raises((ValueError, OverflowError)) as err:
+                O.load_edge_list_text(text, nv, bool(c["sym"]))
+            assert f"{type(err.value).__name__}: {err.value}" == str(c["err"]), i
+        else:
+            n, r, cc = O.load_edge_list_text(text, nv, bool(c["sym"]))
+            assert n == int(c["n"]), i
+            np.testing.assert_array_equal(r, c["rows"])
+            np.testing.assert_array_equal(cc, c["cols"])
