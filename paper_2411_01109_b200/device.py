@@ -139,6 +139,32 @@ def read_bytes_device(path, device="cuda") -> torch.Tensor:
     return host.to(device, non_blocking=False)
 
 
+def load_tensor_device(path, device="cuda") -> torch.Tensor:
+    """sparse.load_tensor (HSDT: 16-byte header magic, rows u32, cols u32, mode
+    u16, pad; little-endian payload; sparse.py:239-263) straight into HBM: the
+    header is checked on the host, the payload moves once through pinned memory."""
+    import os
+    import struct
+
+    with open(path, "rb") as fh:
+        head = fh.read(16)
+    if len(head) != 16 or head[:4] != b"HSDT":
+        raise ValueError(f"{path}: not a tensor file")
+    rows, cols, code = struct.unpack("<IIHxx", head[4:])
+    dt = {1: torch.float16, 2: torch.float32}.get(code)
+    if dt is None:
+        raise ValueError(f"{path}: unknown mode code {code}")
+    expect = rows * cols * (2 if code == 1 else 4)
+    payload = os.path.getsize(path) - 16
+    if payload != expect:
+        raise ValueError(f"{path}: payload is {payload} bytes, expected {expect}")
+    host = torch.empty(rows * cols, dtype=dt).pin_memory()
+    with open(path, "rb") as fh:
+        fh.seek(16)
+        fh.readinto(memoryview(host.numpy()).cast("B"))
+    return host.to(device).view(rows, cols)
+
+
 def parse_edge_text(text: torch.Tensor, where: str = "<text>"):
     """GPU parse of edge-list text (hg_count_lines + hg_parse_edges): returns
     (rows int64, cols int64, max_id) on the text's device, in file order.

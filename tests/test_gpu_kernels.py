@@ -654,3 +654,20 @@ def test_edge_list_ingest_large(cuda, tmp_path):
     assert dg.n == n
     np.testing.assert_array_equal(dg.offsets.cpu().numpy(), O.csr_offsets(n, r))
     np.testing.assert_array_equal(dg.cols.cpu().numpy(), c)
+
+
+def test_load_tensor_device_roundtrip(cuda, tmp_path):
+    """HSDT files (sparse.save_tensor) load straight into HBM bit for bit."""
+    from paper_2411_01109_b200 import sparse as sp
+    from paper_2411_01109_b200.device import load_tensor_device
+
+    rng = np.random.default_rng(0)
+    for dt in (np.float16, np.float32):
+        t = sp.DenseTensor(rng.normal(0, 5, (123, 37)).astype(dt))
+        p = tmp_path / f"t{np.dtype(dt).itemsize}.hsdt"
+        sp.save_tensor(t, p)
+        got = load_tensor_device(p).cpu().numpy()
+        np.testing.assert_array_equal(bits(got), bits(t.data))
+    p.write_bytes(p.read_bytes()[:-4])
+    with pytest.raises(ValueError, match="payload"):
+        load_tensor_device(p)
