@@ -96,10 +96,25 @@ class ClockSampler:
 
 
 def dist_env():
+    """(world size, rank, local device).  HG_DIST_SHARED_GPU=1 puts every rank
+    on cuda:0 (with HG_DIST_BACKEND=gloo: validating the N>1 path on one GPU;
+    never a measurement)."""
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("HG_DIST_SHARED_GPU") == "1":
+        local = 0
     return ws, rank, local
+
+
+def max_over_ranks(dist, v):
+    """Max of a host float over ranks (device tensor for NCCL, host for gloo)."""
+    import torch
+
+    dev = "cpu" if dist.get_backend() == "gloo" else "cuda"
+    tt = torch.tensor([v], device=dev, dtype=torch.float64)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    return float(tt.item())
 
 
 def load_traffic_profile(f_key):
@@ -325,7 +340,11 @@ def b200_arm(args, ws, rank, local):
     if ws > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("HG_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     peak, peak_kind = peaks()
     t_setup = time.time()
     dg, x, labels = build_workload(args.workload, args.seed)
@@ -360,9 +379,7 @@ def b200_arm(args, ws, rank, local):
         barrier()
         ms = ev0.elapsed_time(ev1) / k
         if dist is not None:
-            tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ms = float(tt.item())
+            ms = max_over_ranks(dist, ms)
         return ms, loss
 
     # ---- eager pass: SpMM roofline (CUDA events around every hg_spmm) ----
@@ -401,9 +418,7 @@ def b200_arm(args, ws, rank, local):
     barrier()
     e2e_ms = (time.perf_counter() - e0) * 1e3 / args.steps
     if dist is not None:
-        tt = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tt.item())
+        e2e_ms = max_over_ranks(dist, e2e_ms)
 
     result = None
     if rank == 0:
@@ -413,7 +428,8 @@ def b200_arm(args, ws, rank, local):
             "metric": METRIC, "value": round(t_ms, 4), "unit": "ms/epoch", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_ms, 4),
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f16", "data": "synthetic (seeded Reddit-shaped graph, planted labels)",
+            "dtype": "f16", "data": f"synthetic (seeded {WORKLOADS[args.workload]['graph']} graph, "
+                                    "planted labels)",
             "config": workload_config(dg.n, dg.num_edges, parallelism, args.workload),
             "clocks": clocks.summary(),
             "e2e": {"value": round(e2e_ms, 4), "unit": "ms/epoch", "h2d_bytes_per_step": int(h2d),

@@ -93,11 +93,22 @@ def make_local_part(offsets, cols, t_offsets, t_cols, perm, rank, parts) -> Loca
 
 
 class Exchange:
-    """Padded all-gathers over a torch.distributed process group."""
+    """Padded all-gathers over a torch.distributed process group.  NCCL moves
+    device tensors over NVLink; a gloo group (CPU tests, or several ranks
+    sharing one GPU for validation) stages device tensors through the host."""
 
     def __init__(self, dist, part: LocalPart):
         self.dist = dist
         self.part = part
+        self.staged = dist.get_backend() == "gloo"
+
+    def _all_gather(self, out, send):
+        if self.staged and out.is_cuda:
+            host = out.cpu()
+            self.dist.all_gather_into_tensor(host, send.cpu())
+            out.copy_(host)
+        else:
+            self.dist.all_gather_into_tensor(out, send)
 
     def gather_rows(self, x_local: torch.Tensor) -> torch.Tensor:
         p = self.part
@@ -106,7 +117,7 @@ class Exchange:
             send = x_local.new_zeros((p.n_max,) + tuple(x_local.shape[1:]))
             send[: x_local.shape[0]] = x_local
         out = x_local.new_empty((p.parts * p.n_max,) + tuple(x_local.shape[1:]))
-        self.dist.all_gather_into_tensor(out, send.contiguous())
+        self._all_gather(out, send.contiguous())
         return out
 
     def gather_edges(self, v_local: torch.Tensor) -> torch.Tensor:
@@ -116,11 +127,17 @@ class Exchange:
             send = v_local.new_zeros((p.e_max,) + tuple(v_local.shape[1:]))
             send[: v_local.shape[0]] = v_local
         out = v_local.new_empty((p.parts * p.e_max,) + tuple(v_local.shape[1:]))
-        self.dist.all_gather_into_tensor(out, send.contiguous())
+        self._all_gather(out, send.contiguous())
         return out
 
-    def all_reduce_(self, t: torch.Tensor) -> torch.Tensor:
-        self.dist.all_reduce(t)
+    def all_reduce_(self, t: torch.Tensor, op=None) -> torch.Tensor:
+        kw = {} if op is None else {"op": op}
+        if self.staged and t.is_cuda:
+            host = t.cpu()
+            self.dist.all_reduce(host, **kw)
+            t.copy_(host)
+        else:
+            self.dist.all_reduce(t, **kw)
         return t
 
 
@@ -301,8 +318,8 @@ class DistTrainer:
         # data-parallel sum of the weight gradients: one fp32 all-reduce of the
         # group's flat gradient buffer
         flat = tr.group.grad.to(torch.float32)
-        self.dist.all_reduce(flat)
+        self.bundle.ex.all_reduce_(flat)
         tr.opt.step(flat_grad=flat)
         total = loss.detach().clone()
-        self.dist.all_reduce(total)
+        self.bundle.ex.all_reduce_(total)
         return total, logits.detach()
