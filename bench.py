@@ -354,7 +354,7 @@ def b200_arm(args, ws, rank, local):
         from paper_2411_01109_b200.partition import DistTrainer
 
         tr = DistTrainer(dg, x, labels, cfg, dist)
-        parallelism = f"row-partition x{ws} (NCCL all-gather)"
+        parallelism = f"row-partition x{ws} ({dist.get_backend()} all-gather)"
     else:
         tr = Trainer(GraphBundle.build(dg, numerics="fast"), x, labels, cfg)
         parallelism = "dp1"

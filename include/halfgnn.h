@@ -201,6 +201,13 @@ int hg_softmax_xent(const void* logits, int logits_dtype, int64_t ld, const int6
                     int64_t n, int32_t c_active, double denom, float grad_scale, void* grad,
                     int grad_dtype, double* nll, void* stream);
 
+/* fp32-guarded SDDMM (numerics="fast"): out[e*heads+h] = rnd(sum over the head's
+ * fh features of X[row(e)] * Y[cols[e]]), exact f16 products accumulated in
+ * fp32, one rounding; same arguments as hg_sddmm. */
+int hg_sddmm_fast(const int64_t* offsets, const int32_t* cols, int64_t n_rows, int64_t num_edges,
+                  const int32_t* units, int64_t num_units, const void* x, const void* y,
+                  void* out, int32_t F, int32_t heads, int dtype, void* stream);
+
 /* GAT attention projections (models.py:503-506, s_l = z a_l, s_r = z a_r) for all
  * heads at once: s_l[n*H+h] = rnd(sum_f z[n, h*fh+f] * a_l[h*fh+f]) (fp32
  * accumulation of exact products, one rounding), same for s_r. */

@@ -4,8 +4,9 @@
 //  * k_gat_fwd_*   alpha[e, h] = rnd(softmax_r(leaky(s_l[r, h] + s_r[c, h])))
 //                  -- attention_scores + leaky_relu + edge_softmax
 //                  (models.py:188-200, 317-326, 382-401) in one pass: fp32
-//                  logits (never rounded), fp32 online max / sum (expf), one
-//                  rounding of alpha.  No E x H logits array is written.
+//                  logits (never rounded) kept in the log2 domain (leaky
+//                  commutes with the positive log2(e) scale), fp32 online
+//                  max / sum with exp2 (MUFU.EX2), one rounding of alpha.  No E x H logits array is written.
 //  * k_gat_bwd_*   de'[e, h] = rnd(alpha (dalpha - sum_r alpha dalpha) *
 //                  leaky'(e)) and ds_l[r, h] = rnd(sum_r de') -- edge_softmax
 //                  backward (403-410), leaky backward and the row-sum half of
@@ -24,11 +25,13 @@ namespace hg {
 
 __device__ __forceinline__ float leaky_f(float v, float slope) { return v > 0.0f ? v : v * slope; }
 
+constexpr float kLog2e = 1.4426950408889634f;
+
 // merge two online-softmax states (m, s), s = sum exp(v - m)
 __device__ __forceinline__ void ms_merge(float& m, float& s, float m2, float s2) {
   const float mm = fmaxf(m, m2);
   if (mm == -INFINITY) return;
-  s = (m == -INFINITY ? 0.0f : s * expf(m - mm)) + (m2 == -INFINITY ? 0.0f : s2 * expf(m2 - mm));
+  s = (m == -INFINITY ? 0.0f : s * exp2f(m - mm)) + (m2 == -INFINITY ? 0.0f : s2 * exp2f(m2 - mm));
   m = mm;
 }
 
@@ -68,16 +71,17 @@ __device__ __forceinline__ void fwd_pass1(const int32_t* __restrict__ cols, cons
     float mu = -INFINITY;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      v[u] = c[u] >= 0 ? leaky_f(a + Num<T>::to_f(sr[(int64_t)c[u] * H + h]), slope) : -INFINITY;
+      v[u] = c[u] >= 0 ? leaky_f(fmaf(Num<T>::to_f(sr[(size_t)(unsigned)c[u] * H + h]), kLog2e, a), slope)
+                       : -INFINITY;
       mu = fmaxf(mu, v[u]);
     }
     if (mu > m) {
-      s = m == -INFINITY ? 0.0f : s * expf(m - mu);
+      s = m == -INFINITY ? 0.0f : s * exp2f(m - mu);
       m = mu;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (c[u] >= 0) s += expf(v[u] - m);
+      if (c[u] >= 0) s += exp2f(v[u] - m);
   }
 }
 
@@ -93,10 +97,11 @@ __device__ __forceinline__ void fwd_pass2(const int32_t* __restrict__ cols, cons
     float v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      v[u] = c[u] >= 0 ? leaky_f(a + Num<T>::to_f(sr[(int64_t)c[u] * H + h]), slope) : 0.0f;
+      v[u] = c[u] >= 0 ? leaky_f(fmaf(Num<T>::to_f(sr[(size_t)(unsigned)c[u] * H + h]), kLog2e, a), slope)
+                       : 0.0f;
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (c[u] >= 0) alpha[(e0 + u * step) * H + h] = Num<T>::from_f(expf(v[u] - m) * inv);
+      if (c[u] >= 0) alpha[(e0 + u * step) * H + h] = Num<T>::from_f(exp2f(v[u] - m) * inv);
   }
 }
 
@@ -134,7 +139,7 @@ __device__ __forceinline__ float bwd_pass2(const int32_t* __restrict__ cols, con
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t e = e0 + u * step;
-      sv[u] = c[u] >= 0 ? Num<T>::to_f(sr[(int64_t)c[u] * H + h]) : 0.0f;
+      sv[u] = c[u] >= 0 ? Num<T>::to_f(sr[(size_t)(unsigned)c[u] * H + h]) : 0.0f;
       x[u] = c[u] >= 0 ? Num<T>::to_f(alpha[e * H + h]) : 0.0f;
       y[u] = c[u] >= 0 ? Num<T>::to_f(dalpha[e * H + h]) : 0.0f;
     }
@@ -184,7 +189,7 @@ k_gat_fwd_thread(const int64_t* __restrict__ offsets, const int32_t* __restrict_
   const int h = (int)(t - r * H);
   const int64_t beg = offsets[r], end = offsets[r + 1];
   if (end == beg || end - beg > short_max) return;
-  const float a = Num<T>::to_f(sl[t]);
+  const float a = Num<T>::to_f(sl[t]) * kLog2e;  // log2 domain
   float m = -INFINITY, s = 0.0f;
   fwd_pass1<T, H>(cols, sr, beg, end, 1, h, a, slope, m, s);
   fwd_pass2<T, H>(cols, sr, beg, end, 1, h, a, slope, m, 1.0f / s, alpha);
@@ -202,7 +207,7 @@ k_gat_fwd_warp(const int64_t* __restrict__ offsets, const int32_t* __restrict__ 
        w += nwarps) {
     const int64_t r = rows[w];
     const int64_t beg = offsets[r], end = offsets[r + 1];
-    const float a = Num<T>::to_f(sl[r * H + h]);
+    const float a = Num<T>::to_f(sl[r * H + h]) * kLog2e;
     float m = -INFINITY, s = 0.0f;
     fwd_pass1<T, H>(cols, sr, beg + j, end, EPB, h, a, slope, m, s);
     ms_warp<H>(m, s);
@@ -220,7 +225,7 @@ k_gat_fwd_cta(const int64_t* __restrict__ offsets, const int32_t* __restrict__ c
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, j = tid / H, h = tid % H;
   const int64_t r = rows[blockIdx.x];
   const int64_t beg = offsets[r], end = offsets[r + 1];
-  const float a = Num<T>::to_f(sl[r * H + h]);
+  const float a = Num<T>::to_f(sl[r * H + h]) * kLog2e;
   float m = -INFINITY, s = 0.0f;
   fwd_pass1<T, H>(cols, sr, beg + j, end, EPB, h, a, slope, m, s);
   ms_warp<H>(m, s);

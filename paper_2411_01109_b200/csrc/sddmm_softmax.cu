@@ -131,9 +131,145 @@ k_sddmm(const int4* __restrict__ units, int64_t num_units, const int32_t* __rest
   }
 }
 
+// fp32-guarded SDDMM (numerics="fast"): out[e, h] = rnd(sum_f x[r, hf] y[c, hf])
+// with exact f16 products accumulated in fp32 (fma.rn.f32.f16), one rounding.
+// Team of TEAM = F/V lanes per unit, G = fh/V lanes per head (power of two,
+// G <= TEAM).  The EB per-edge partial dots of a batch are reduced across the
+// G lanes of a head with a reduce-scatter butterfly: each level halves the
+// values a lane carries, so EB edges cost ~EB + log2(G) shuffles instead of
+// EB * log2(G).
+template <typename T, int V>
+__device__ __forceinline__ float chunk_dot_f32(const typename RawV<V * sizeof(T)>::type& xr,
+                                               const typename RawV<V * sizeof(T)>::type& yr) {
+  float acc = 0.0f;
+  if constexpr (sizeof(T) == 2) {
+    const unsigned short* xa = reinterpret_cast<const unsigned short*>(&xr);
+    const unsigned short* ya = reinterpret_cast<const unsigned short*>(&yr);
+#pragma unroll
+    for (int i = 0; i < V; ++i)
+      asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(acc) : "h"(xa[i]), "h"(ya[i]));
+  } else {
+    const float* xa = reinterpret_cast<const float*>(&xr);
+    const float* ya = reinterpret_cast<const float*>(&yr);
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc = fmaf(xa[i], ya[i], acc);
+  }
+  return acc;
+}
+
+template <typename T, int V, int TEAM, int G>
+__global__ void __launch_bounds__(256)
+k_sddmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __restrict__ cols,
+             const T* __restrict__ x, const T* __restrict__ y, T* __restrict__ out, int F,
+             int heads) {
+  using Raw = typename RawV<V * sizeof(T)>::type;
+  constexpr int EB = 8;
+  constexpr int LV = (G < EB ? G : EB);  // butterfly levels that halve the batch: log2(LV)
+  const int lane = threadIdx.x & 31;
+  const int tl = lane & (TEAM - 1);
+  const unsigned tmask =
+      TEAM == 32 ? 0xffffffffu : (((1u << TEAM) - 1u) << (lane & ~(TEAM - 1)));
+  const int64_t team = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TEAM;
+  if (team >= num_units) return;
+  const int4 un = units[team];
+  const int row = un.x, beg = un.y, end = un.z;
+  const int nvec = F / V;
+  const bool cval = tl < nvec;
+  const int hd = tl / G, gp = tl & (G - 1);  // head, position inside the head's lane group
+  Raw xr;
+  if (cval) xr = *reinterpret_cast<const Raw*>(x + (int64_t)row * F + tl * V);
+  int cj[EB];
+#pragma unroll
+  for (int j = 0; j < EB; ++j) cj[j] = beg + j < end ? __ldg(cols + beg + j) : 0;
+  for (int base = beg; base < end; base += EB) {
+    int nj[EB];
+#pragma unroll
+    for (int j = 0; j < EB; ++j) nj[j] = base + EB + j < end ? __ldg(cols + base + EB + j) : 0;
+    Raw yr[EB];
+#pragma unroll
+    for (int j = 0; j < EB; ++j)
+      if (base + j < end && cval) yr[j] = __ldg(reinterpret_cast<const Raw*>(y + (int64_t)cj[j] * F + tl * V));
+    float v[EB];
+#pragma unroll
+    for (int j = 0; j < EB; ++j) v[j] = (base + j < end && cval) ? chunk_dot_f32<T, V>(xr, yr[j]) : 0.0f;
+    // reduce-scatter over the G lanes of each head (xor partners stay in the group)
+    int eoff = 0;
+#pragma unroll
+    for (int s = G / 2, cnt = EB; s >= 1 && cnt > 1; s >>= 1, cnt >>= 1) {
+      const bool up = (gp & s) != 0;
+#pragma unroll
+      for (int i = 0; i < cnt / 2; ++i) {
+        const float send = up ? v[i] : v[i + cnt / 2];
+        const float keep = up ? v[i + cnt / 2] : v[i];
+        v[i] = keep + __shfl_xor_sync(tmask, send, s);
+      }
+      if (up) eoff += cnt / 2;
+    }
+    // heads wider than the batch: finish with plain xor sums (G > EB)
+#pragma unroll
+    for (int s = G / (2 * LV) > 0 ? (G / LV) / 2 : 0; s >= 1; s >>= 1)
+      v[0] += __shfl_xor_sync(tmask, v[0], s);
+    constexpr int KEEP = EB / LV;  // values per lane after the butterfly
+    const bool writer = G <= EB || (gp & (G / LV - 1)) == 0;
+    if (cval && writer) {
+#pragma unroll
+      for (int i = 0; i < KEEP; ++i) {
+        const int e = base + eoff + i;
+        if (e < end) out[(int64_t)e * heads + hd] = Num<T>::from_f(v[i]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < EB; ++j) cj[j] = nj[j];
+  }
+}
+
 }  // namespace hg
 
 using namespace hg;
+
+template <typename T, int V, int TEAM, int G>
+static int launch_sddmm_fast(const int4* units, int64_t nu, const int32_t* cols, const void* x,
+                             const void* y, void* out, int F, int heads, cudaStream_t st) {
+  constexpr int tpb = 256 / TEAM;
+  if (nu == 0) return HG_OK;
+  k_sddmm_fast<T, V, TEAM, G><<<(unsigned)((nu + tpb - 1) / tpb), 256, 0, st>>>(
+      units, nu, cols, (const T*)x, (const T*)y, (T*)out, F, heads);
+  HG_LAUNCHED();
+  return HG_OK;
+}
+
+template <typename T, int V, int TEAM>
+static int dispatch_sddmm_fast_g(const int4* units, int64_t nu, const int32_t* cols,
+                                 const void* x, const void* y, void* out, int F, int heads,
+                                 int g, cudaStream_t st) {
+  switch (g) {
+    case 1: return launch_sddmm_fast<T, V, TEAM, 1>(units, nu, cols, x, y, out, F, heads, st);
+    case 2: if constexpr (TEAM >= 2) return launch_sddmm_fast<T, V, TEAM, 2>(units, nu, cols, x, y, out, F, heads, st); break;
+    case 4: if constexpr (TEAM >= 4) return launch_sddmm_fast<T, V, TEAM, 4>(units, nu, cols, x, y, out, F, heads, st); break;
+    case 8: if constexpr (TEAM >= 8) return launch_sddmm_fast<T, V, TEAM, 8>(units, nu, cols, x, y, out, F, heads, st); break;
+    case 16: if constexpr (TEAM >= 16) return launch_sddmm_fast<T, V, TEAM, 16>(units, nu, cols, x, y, out, F, heads, st); break;
+    case 32: if constexpr (TEAM >= 32) return launch_sddmm_fast<T, V, TEAM, 32>(units, nu, cols, x, y, out, F, heads, st); break;
+    default: break;
+  }
+  HG_REQUIRE(false, "hg_sddmm_fast: head group %d unsupported", g);
+}
+
+// Returns -1 when the layout is not covered (caller falls back to the exact kernel).
+template <typename T, int V>
+static int dispatch_sddmm_fast(const int4* units, int64_t nu, const int32_t* cols, const void* x,
+                               const void* y, void* out, int F, int heads, cudaStream_t st) {
+  const int nvec = F / V, g = F / heads / V;
+  if (nvec > 32 || g < 1 || (g & (g - 1)) != 0 || nvec % g != 0) return -1;
+  const int team = nvec <= 1 ? 1 : nvec <= 2 ? 2 : nvec <= 4 ? 4 : nvec <= 8 ? 8 : nvec <= 16 ? 16 : 32;
+  switch (team) {
+    case 1: return dispatch_sddmm_fast_g<T, V, 1>(units, nu, cols, x, y, out, F, heads, g, st);
+    case 2: return dispatch_sddmm_fast_g<T, V, 2>(units, nu, cols, x, y, out, F, heads, g, st);
+    case 4: return dispatch_sddmm_fast_g<T, V, 4>(units, nu, cols, x, y, out, F, heads, g, st);
+    case 8: return dispatch_sddmm_fast_g<T, V, 8>(units, nu, cols, x, y, out, F, heads, g, st);
+    case 16: return dispatch_sddmm_fast_g<T, V, 16>(units, nu, cols, x, y, out, F, heads, g, st);
+    default: return dispatch_sddmm_fast_g<T, V, 32>(units, nu, cols, x, y, out, F, heads, g, st);
+  }
+}
 
 template <typename T, int V, int TEAM, int NCH>
 static int launch_sddmm(const int4* units, int64_t nu, const int32_t* cols, const void* x,
@@ -165,6 +301,34 @@ static int dispatch_sddmm(const int4* units, int64_t nu, const int32_t* cols, co
   if (nvec <= 256) HG_SD(32, 8);
 #undef HG_SD
   HG_REQUIRE(false, "hg_sddmm: feature length %d too large", F);
+}
+
+extern "C" int hg_sddmm_fast(const int64_t* offsets, const int32_t* cols, int64_t n_rows,
+                             int64_t num_edges, const int32_t* units, int64_t num_units,
+                             const void* x, const void* y, void* out, int32_t F, int32_t heads,
+                             int dtype, void* stream) {
+  HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
+  HG_REQUIRE(F > 0 && F % 2 == 0, "feature length %d must be even and positive", F);
+  HG_REQUIRE(heads >= 1 && F % heads == 0 && (F / heads) % 2 == 0,
+             "feature length %d does not split into %d even heads", F, heads);
+  cudaStream_t st = as_stream(stream);
+  const int fh = F / heads;
+  const int4* u = reinterpret_cast<const int4*>(units);
+  const bool aligned = reinterpret_cast<uintptr_t>(x) % 16 == 0 && reinterpret_cast<uintptr_t>(y) % 16 == 0;
+  int rc = -1;
+  if (dtype == HG_F16 && aligned && fh % 8 == 0)
+    rc = dispatch_sddmm_fast<__half, 8>(u, num_units, cols, x, y, out, F, heads, st);
+  else if (dtype == HG_F16)
+    rc = dispatch_sddmm_fast<__half, 2>(u, num_units, cols, x, y, out, F, heads, st);
+  else if (aligned && fh % 4 == 0)
+    rc = dispatch_sddmm_fast<float, 4>(u, num_units, cols, x, y, out, F, heads, st);
+  else
+    rc = dispatch_sddmm_fast<float, 2>(u, num_units, cols, x, y, out, F, heads, st);
+  if (rc >= 0) return rc;
+  // layouts outside the butterfly kernel (F/V > 32, non-power-of-two heads):
+  // the exact kernel (its result is within the fast tolerance by definition)
+  return hg_sddmm(offsets, cols, n_rows, num_edges, units, num_units, x, y, out, F, heads,
+                  dtype, stream);
 }
 
 extern "C" int hg_sddmm(const int64_t* offsets, const int32_t* cols, int64_t n_rows,

@@ -503,8 +503,9 @@ def spmm_vertex_ref(dg: DeviceGraph, x, scaling="post", norm="none", staging=Fal
 # ── SDDMM, attention, softmax ────────────────────────────────────────────
 
 
-def sddmm(dg: DeviceGraph, x, y, heads=1, transpose=False):
-    """Per-edge (per-head) tree dot products, bit-exact with kernels.sddmm.
+def sddmm(dg: DeviceGraph, x, y, heads=1, transpose=False, fast=False):
+    """Per-edge (per-head) tree dot products, bit-exact with kernels.sddmm
+    (fast=True: fp32 accumulation, one rounding -- hg_sddmm_fast).
     Returns [E] for heads == 1, else [E, heads]."""
     view = dg.view(transpose)
     _require_cuda(x, y)
@@ -516,9 +517,9 @@ def sddmm(dg: DeviceGraph, x, y, heads=1, transpose=False):
     f = x.shape[1]
     sched = view.schedule()
     out = torch.empty((view.num_edges, heads), dtype=x.dtype, device=x.device)
-    nat.call("hg_sddmm", _p(view.offsets), _p(view.cols), view.n_rows, view.num_edges,
-             _p(sched.units), sched.num_units, _p(x), _p(y), _p(out), f, heads,
-             _dtype_code(x), _stream())
+    nat.call("hg_sddmm_fast" if fast else "hg_sddmm", _p(view.offsets), _p(view.cols),
+             view.n_rows, view.num_edges, _p(sched.units), sched.num_units, _p(x), _p(y),
+             _p(out), f, heads, _dtype_code(x), _stream())
     Probe.launches += 1
     return out[:, 0] if heads == 1 else out
 

@@ -181,7 +181,7 @@ class GraphBundle:
         return ds_l, D.edge_sums_fast(bwd, de, bwd.perm)
 
     def sddmm(self, x, y, heads=1):
-        return D.sddmm(self.dg, x, y, heads=heads)
+        return D.sddmm(self.dg, x, y, heads=heads, fast=self.numerics == "fast")
 
     @staticmethod
     def head_dots(z, a_l, a_r, heads):

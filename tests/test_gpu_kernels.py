@@ -671,3 +671,28 @@ def test_load_tensor_device_roundtrip(cuda, tmp_path):
     p.write_bytes(p.read_bytes()[:-4])
     with pytest.raises(ValueError, match="payload"):
         load_tensor_device(p)
+
+
+@pytest.mark.parametrize("heads,fh", [(1, 8), (1, 16), (1, 64), (1, 256), (4, 32), (4, 8),
+                                      (2, 128), (8, 16), (2, 6), (1, 512)])
+def test_sddmm_fast_vs_f64(cuda, heads, fh):
+    """hg_sddmm_fast (fp32 accumulation + butterfly head reduction) within one
+    fp16 rounding of the float64 dot, on a power-law graph; layouts outside
+    the butterfly kernel fall back to the exact kernel."""
+    from paper_2411_01109_b200 import device as D
+
+    n = 3000
+    rng = np.random.default_rng(fh * heads)
+    deg = np.minimum(rng.zipf(1.7, n), 2000)
+    rows = np.repeat(np.arange(n), deg)
+    r, c = O.canonical_edges(n, rows, rng.integers(0, n, rows.size))
+    dg = _dg(n, r, c, cuda)
+    f = heads * fh
+    x = rng.normal(0, 1, (n, f)).astype(np.float16)
+    y = rng.normal(0, 1, (n, f)).astype(np.float16)
+    got = D.sddmm(dg, _t(x, cuda), _t(y, cuda), heads=heads, fast=True).cpu().numpy()
+    got = got.reshape(r.size, heads).astype(np.float64)
+    prod = x.astype(np.float64)[r] * y.astype(np.float64)[c]
+    want = prod.reshape(r.size, heads, fh).sum(-1)
+    bound = 2.0 ** -11 * np.abs(want) + 1e-6 * np.abs(prod).reshape(r.size, heads, fh).sum(-1) + 1e-7
+    assert np.all(np.abs(got - want) <= bound)

@@ -1,0 +1,35 @@
+"""Per-launch DRAM traffic of the dominant kernel from an ncu CSV taken with
+--metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum.
+Writes the JSON bench.py reads for roofline.traffic."""
+from __future__ import annotations
+
+import collections
+import csv
+import json
+import sys
+
+
+def main(path, out, pattern="k_spmm_fast<", last=4, source=""):
+    rows = list(csv.reader(open(path)))
+    h = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    hdr = rows[h]
+    ki, mi, vi, ii = (hdr.index(k) for k in ("Kernel Name", "Metric Name", "Metric Value", "ID"))
+    per = collections.defaultdict(dict)
+    names = {}
+    for r in rows[h + 1:]:
+        if len(r) <= vi:
+            continue
+        per[int(r[ii])][r[mi]] = float(r[vi].replace(",", ""))
+        names[int(r[ii])] = r[ki]
+    ids = [i for i in sorted(per) if pattern in names[i]][-last:]
+    bytes_ = [per[i]["dram__bytes_read.sum"] + per[i]["dram__bytes_write.sum"] for i in ids]
+    ns = [per[i]["gpu__time_duration.sum"] for i in ids]
+    d = {"gcn_epoch": sum(bytes_) / len(bytes_), "gcn_epoch_per_launch_bytes": bytes_,
+         "gcn_epoch_per_launch_ns": ns, "kernels": [names[i][:80] for i in ids],
+         "source": source}
+    json.dump(d, open(out, "w"), indent=1)
+    print(json.dumps(d))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], sys.argv[2], source=" ".join(sys.argv[3:]))
