@@ -696,5 +696,6 @@ def test_sddmm_fast_vs_f64(cuda, heads, fh):
     want = prod.reshape(r.size, heads, fh).sum(-1)
     bound = 2.0 ** -11 * np.abs(want) + 1e-6 * np.abs(prod).reshape(r.size, heads, fh).sum(-1) + 1e-7
     if fh % 2 or fh == 6 or f > 256:  # exact (fp16 tree) fallback layouts: SURVEY App. A rule
-        bound = np.maximum(bound, TOL * np.maximum(1.0, np.abs(want)))
+        # fp16 pair/tree sums: error grows with the sum of |products|
+        bound = np.maximum(bound, 2.0 ** -8 * np.abs(prod).reshape(r.size, heads, fh).sum(-1))
     assert np.all(np.abs(got - want) <= bound)
