@@ -234,6 +234,20 @@ int hg_adam_step(float* master, float* m, float* v, const void* grad, int grad_d
                  int64_t count, float lr, float omb1, float omb2, double b1, double b2,
                  float eps, const double* step, float grad_unscale, void* stream);
 
+/* ------------------------------------------------------ dense GEMM (tcgen05) */
+
+/* models.matmul -> add_bias -> left-norm input scaling (models.py:141-166,
+ * kernels.py:358-361) as one tensor-core GEMM with a fused epilogue:
+ *   out[m, n] = rnd(rnd(rnd(sum_k a[m, k] * bt[n, k]) + bias[n]) * row_scale[m])
+ * binary16 operands, fp32 accumulation in TMEM (tcgen05.mma kind::f16, M=128
+ * tiles, TMA-fed 4-stage ring), one rounding per step; bias / row_scale may be
+ * NULL.  a: [m, k] pitch lda; bt: [n, k] pitch ldb (B transposed, K-major);
+ * out: [m, n] pitch ldo.  n: multiple of 16 in [16, 256]; pitches multiples
+ * of 8 elements; 16-byte aligned pointers. */
+int hg_gemm_tc(const void* a, int64_t m, int64_t k, int64_t lda, const void* bt, int32_t n,
+               int64_t ldb, const void* bias, const void* row_scale, void* out, int64_t ldo,
+               void* stream);
+
 /* ----------------------------------------------------------------- ingest */
 
 /* sparse.load_edge_list (sparse.py:143-177) on the GPU.  `text` is the file's

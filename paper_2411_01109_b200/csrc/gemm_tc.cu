@@ -1,0 +1,283 @@
+// Dense per-layer feature GEMM on the 5th-generation tensor cores with the GCN
+// epilogue fused in:
+//
+//   out[m, n] = rnd(rnd(rnd(sum_k A[m, k] Bt[n, k]) + bias[n]) * row_scale[m])
+//
+// i.e. models.matmul (fp32 accumulation, one rounding, models.py:141-158) ->
+// add_bias (161-166) -> the aggregation's left-norm input scaling
+// (kernels.py:358-361), each rounding exactly where the reference rounds.
+//
+// One CTA per 128-row tile (128 threads):
+//   warp 0 / lane 0   TMA producer: 64-wide K slabs of A (128 x 64) and Bt
+//                     (N x 64) into a STAGES-deep shared-memory ring
+//                     (cp.async.bulk.tensor, SWIZZLE_128B, OOB -> zeros);
+//   warp 1 / lane 0   MMA issuer: 4 x tcgen05.mma.cta_group::1.kind::f16
+//                     (M=128, N, K=16) per slab into an fp32 accumulator in TMEM;
+//                     tcgen05.commit frees the slab / signals the epilogue;
+//   all 4 warps       epilogue: tcgen05.ld 32x32b (warp w owns TMEM lanes
+//                     32w..32w+31 = rows), fp16 rounding, bias, row scale,
+//                     16-byte stores.
+// Fed by TMA and drained from TMEM, the kernel is bound by reading A once
+// (HBM), which is what the GCN layer-1 GEMM (233K x 608 x 64) costs.
+#include <cuda.h>
+
+#include "hg_common.cuh"
+
+namespace hg {
+
+constexpr int kTcBM = 128;  // rows per tile (UMMA M)
+constexpr int kTcBK = 64;   // fp16 K elements per slab = one 128-byte swizzle row
+constexpr int kTcStages = 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// K-major operand in a 128-byte-swizzled tile: rows of 128 B, 8-row atoms 1024 B apart.
+__device__ __forceinline__ uint64_t sw128_kmajor_desc(const void* tile) {
+  const uint64_t addr = smem_u32(tile);
+  uint64_t d = (addr >> 4) & 0x3FFFull;  // start address
+  d |= 1ull << 16;                       // leading byte offset (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;      // stride byte offset: 8 rows x 128 B
+  d |= 1ull << 46;                       // descriptor version (sm_100)
+  d |= 2ull << 61;                       // SWIZZLE_128B
+  return d;
+}
+
+__device__ __forceinline__ void umma_f16_f32(uint32_t tmem_d, uint64_t da, uint64_t db,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(addr));
+}
+
+template <int N>
+__global__ void __launch_bounds__(128)
+k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+          int64_t m, int num_kb, const __half* __restrict__ bias,
+          const __half* __restrict__ row_scale, __half* __restrict__ out, int64_t ldo) {
+  constexpr uint32_t kABytes = kTcBM * kTcBK * 2;
+  constexpr uint32_t kBBytes = N * kTcBK * 2;
+  constexpr uint32_t kCols = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
+  // instruction descriptor: f16 x f16 -> f32, both K-major, M = 128, N
+  constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kTcBM >> 4) << 24);
+
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sa = base;                                 // [stages][128 x 128 B]
+  unsigned char* sb = base + kTcStages * kABytes;           // [stages][N x 128 B]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sb + kTcStages * kBBytes);
+  uint64_t* empty = full + kTcStages;
+  uint64_t* done = empty + kTcStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t m0 = (int64_t)blockIdx.x * kTcBM;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTcStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int s = kb % kTcStages;
+        if (kb >= kTcStages) mbar_wait(&empty[s], ((kb / kTcStages) + 1) & 1);
+        mbar_expect_tx(&full[s], kABytes + kBBytes);
+        tma_load_2d(sa + s * kABytes, &map_a, &full[s], kb * kTcBK, (int)m0);
+        tma_load_2d(sb + s * kBBytes, &map_b, &full[s], kb * kTcBK, 0);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int s = kb % kTcStages;
+        mbar_wait(&full[s], (kb / kTcStages) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint64_t da = sw128_kmajor_desc(sa + s * kABytes);
+        const uint64_t db = sw128_kmajor_desc(sb + s * kBBytes);
+#pragma unroll
+        for (int k = 0; k < kTcBK / 16; ++k)  // 16 fp16 = 32 B steps inside the swizzle row
+          umma_f16_f32(tmem, da + 2 * k, db + 2 * k, kIdesc, (kb | k) != 0);
+        umma_commit(&empty[s]);
+      }
+      umma_commit(done);
+    }
+    __syncwarp();
+  }
+
+  // epilogue: thread (warp w, lane l) owns row m0 + 32w + l = TMEM lane 32w + l
+  mbar_wait(done, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int64_t row = m0 + warp * 32 + lane;
+  const bool live = row < m;
+  const __half sv = (live && row_scale) ? row_scale[row] : __float2half_rn(1.0f);
+#pragma unroll
+  for (int c0 = 0; c0 < N; c0 += 16) {
+    uint32_t v[16];
+    tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (live) {
+      __align__(16) __half h[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        __half t = __float2half_rn(__uint_as_float(v[j]));
+        if (bias) t = __hadd_rn(t, bias[c0 + j]);
+        if (row_scale) t = __hmul_rn(t, sv);
+        h[j] = t;
+      }
+      uint4* dst = reinterpret_cast<uint4*>(out + row * ldo + c0);
+      dst[0] = *reinterpret_cast<const uint4*>(&h[0]);
+      dst[1] = *reinterpret_cast<const uint4*>(&h[8]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;  // process-wide driver entry point cache
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2-D fp16 tensor [rows, cols] with row pitch ld (elements), box {64 cols, box_rows}.
+static bool make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld,
+                     uint32_t box_rows) {
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {(cuuint32_t)kTcBK, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int N>
+static int launch_gemm_tc(const CUtensorMap& ma, const CUtensorMap& mb, int64_t m, int64_t k,
+                          const void* bias, const void* row_scale, void* out, int64_t ldo,
+                          cudaStream_t st) {
+  constexpr size_t smem = 1024 + kTcStages * (kTcBM + N) * kTcBK * 2 + (2 * kTcStages + 1) * 8 + 16;
+  HG_CUDA(cudaFuncSetAttribute(k_gemm_tc<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int num_kb = (int)((k + kTcBK - 1) / kTcBK);
+  k_gemm_tc<N><<<(unsigned)((m + kTcBM - 1) / kTcBM), 128, smem, st>>>(
+      ma, mb, m, num_kb, (const __half*)bias, (const __half*)row_scale, (__half*)out, ldo);
+  HG_LAUNCHED();
+  return HG_OK;
+}
+
+}  // namespace hg
+
+using namespace hg;
+
+extern "C" int hg_gemm_tc(const void* a, int64_t m, int64_t k, int64_t lda, const void* bt,
+                          int32_t n, int64_t ldb, const void* bias, const void* row_scale,
+                          void* out, int64_t ldo, void* stream) {
+  HG_REQUIRE(a && bt && out && m >= 0 && k > 0, "hg_gemm_tc: bad arguments");
+  HG_REQUIRE(n >= 16 && n <= 256 && n % 16 == 0, "hg_gemm_tc: N=%d must be a multiple of 16 in [16, 256]", n);
+  HG_REQUIRE(lda >= k && ldb >= k && ldo >= n && lda % 8 == 0 && ldb % 8 == 0 && ldo % 8 == 0,
+             "hg_gemm_tc: row pitches must cover K / N and be multiples of 8 elements");
+  HG_REQUIRE(((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(bt) |
+               reinterpret_cast<uintptr_t>(out)) & 15) == 0,
+             "hg_gemm_tc: operands must be 16-byte aligned");
+  if (m == 0) return HG_OK;
+  CUtensorMap ma, mb;
+  HG_REQUIRE(make_map(&ma, a, m, k, lda, kTcBM) && make_map(&mb, bt, n, k, ldb, (uint32_t)n),
+             "hg_gemm_tc: cuTensorMapEncodeTiled failed");
+  cudaStream_t st = as_stream(stream);
+  switch (n) {
+#define HG_TC(NN) case NN: return launch_gemm_tc<NN>(ma, mb, m, k, bias, row_scale, out, ldo, st);
+    HG_TC(16) HG_TC(32) HG_TC(48) HG_TC(64) HG_TC(80) HG_TC(96) HG_TC(112) HG_TC(128)
+    HG_TC(144) HG_TC(160) HG_TC(176) HG_TC(192) HG_TC(208) HG_TC(224) HG_TC(240) HG_TC(256)
+#undef HG_TC
+    default: break;
+  }
+  HG_REQUIRE(false, "hg_gemm_tc: unsupported N=%d", n);
+}

@@ -648,6 +648,27 @@ def edge_rowsum(dg: DeviceGraph, v, transpose=False):
     return rowsum_view(view, v, view.perm if transpose else None)
 
 
+def gemm_tc(a, bt, bias=None, row_scale=None, out=None):
+    """rnd(rnd(rnd(a @ bt.T) + bias) * row_scale[:, None]) on the tcgen05 tensor
+    cores (hg_gemm_tc): a [M, K] fp16, bt [N, K] fp16 (N % 16 == 0)."""
+    _require_cuda(a, bt)
+    if a.dtype != torch.float16 or bt.dtype != torch.float16:
+        raise ValueError("hg_gemm_tc takes binary16 operands")
+    a, bt = a.contiguous(), bt.contiguous()
+    m, k = a.shape
+    n, k2 = bt.shape
+    if k2 != k:
+        raise ValueError(f"inner dimensions differ: {k} vs {k2}")
+    if out is None:
+        out = torch.empty((m, n), dtype=torch.float16, device=a.device)
+    nat.call("hg_gemm_tc", _p(a), m, k, a.stride(0), _p(bt), n, bt.stride(0),
+             _p(None if bias is None else bias.contiguous()),
+             _p(None if row_scale is None else row_scale.contiguous()), _p(out), out.stride(0),
+             _stream())
+    Probe.launches += 1
+    return out
+
+
 def bias_scale_rows(x, bias=None, row_scale=None, out=None):
     """rnd(rnd(x + bias[None, :]) * row_scale[:, None]) (hg_bias_scale_rows);
     either operand may be None."""

@@ -699,3 +699,35 @@ def test_sddmm_fast_vs_f64(cuda, heads, fh):
         # fp16 pair/tree sums: error grows with the sum of |products|
         bound = np.maximum(bound, 2.0 ** -8 * np.abs(prod).reshape(r.size, heads, fh).sum(-1))
     assert np.all(np.abs(got - want) <= bound)
+
+
+# ── tcgen05 GEMM with the GCN epilogue (hg_gemm_tc) ──────────────────────
+
+
+@pytest.mark.parametrize("m,k,n", [(1000, 608, 64), (300, 64, 48), (4097, 1440, 16), (129, 16, 256),
+                                   (5000, 104, 128), (77, 200, 32)])
+@pytest.mark.parametrize("epi", ["none", "bias", "both"])
+def test_gemm_tc_vs_f64(cuda, m, k, n, epi):
+    """tcgen05 GEMM + fused epilogue against float64: the accumulation differs
+    from the reference only in fp32 summation order, so each output is within
+    one fp16 rounding step of rnd(rnd(rnd(A B) + b) * s) computed in float64."""
+    from paper_2411_01109_b200 import device as D
+
+    rng = np.random.default_rng(m + k + n)
+    a = rng.normal(0, 1, (m, k)).astype(np.float16)
+    w = rng.normal(0, 0.2, (k, n)).astype(np.float16)
+    b = rng.normal(0, 1, n).astype(np.float16) if epi != "none" else None
+    s = rng.uniform(0, 1, m).astype(np.float16) if epi == "both" else None
+    got = D.gemm_tc(_t(a, cuda), _t(np.ascontiguousarray(w.T), cuda),
+                    None if b is None else _t(b, cuda), None if s is None else _t(s, cuda))
+    got = got.cpu().numpy().astype(np.float64)
+    acc = a.astype(np.float64) @ w.astype(np.float64)
+    h = acc.astype(np.float16).astype(np.float64)
+    if b is not None:
+        h = (h + b.astype(np.float64)).astype(np.float16).astype(np.float64)
+    if s is not None:
+        h = (h * s.astype(np.float64)[:, None]).astype(np.float16).astype(np.float64)
+    mag = np.abs(a.astype(np.float64)) @ np.abs(w.astype(np.float64))
+    scale = 1.0 if s is None else s.astype(np.float64)[:, None]
+    bound = 2.0 ** -10 * np.abs(h) + (1e-6 * mag + 2.0 ** -24) * scale * 4
+    assert np.all(np.abs(got - h) <= bound)
