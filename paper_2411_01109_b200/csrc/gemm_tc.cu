@@ -7,16 +7,19 @@
 // add_bias (161-166) -> the aggregation's left-norm input scaling
 // (kernels.py:358-361), each rounding exactly where the reference rounds.
 //
-// One CTA per 128-row tile (128 threads):
+// Persistent, one CTA (192 threads) per SM over 128-row tiles:
 //   warp 0 / lane 0   TMA producer: 64-wide K slabs of A (128 x 64) and Bt
-//                     (N x 64) into a STAGES-deep shared-memory ring
-//                     (cp.async.bulk.tensor, SWIZZLE_128B, OOB -> zeros);
+//                     (N x 64) into a 3-8 deep shared-memory ring
+//                     (cp.async.bulk.tensor, SWIZZLE_128B, OOB -> zeros),
+//                     running ahead across tile boundaries;
 //   warp 1 / lane 0   MMA issuer: 4 x tcgen05.mma.cta_group::1.kind::f16
-//                     (M=128, N, K=16) per slab into an fp32 accumulator in TMEM;
-//                     tcgen05.commit frees the slab / signals the epilogue;
-//   all 4 warps       epilogue: tcgen05.ld 32x32b (warp w owns TMEM lanes
-//                     32w..32w+31 = rows), fp16 rounding, bias, row scale,
-//                     16-byte stores.
+//                     (M=128, N, K=16) per slab into one of two fp32 TMEM
+//                     accumulators; tcgen05.commit frees the slab / hands the
+//                     accumulator to the epilogue;
+//   warps 2-5         epilogue: tcgen05.ld 32x32b (warp w owns TMEM lanes
+//                     32(w%4)..+31 = rows), fp16 rounding, bias, row scale,
+//                     staged in shared memory, coalesced 16-byte stores; it
+//                     overlaps the next tile's MMAs.
 // Fed by TMA and drained from TMEM, the kernel is bound by reading A once
 // (HBM), which is what the GCN layer-1 GEMM (233K x 608 x 64) costs.
 #include <cuda.h>
@@ -27,7 +30,6 @@ namespace hg {
 
 constexpr int kTcBM = 128;  // rows per tile (UMMA M)
 constexpr int kTcBK = 64;   // fp16 K elements per slab = one 128-byte swizzle row
-constexpr int kTcStages = 4;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -104,36 +106,67 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
       : "r"(addr));
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
+__device__ __forceinline__ void epi_bar() {  // named barrier over the 4 epilogue warps
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+}
+
+// smem ring depth for a given N (the ring plus the output staging tile fit ~200 KB)
 template <int N>
-__global__ void __launch_bounds__(128)
+struct TcCfg {
+  static constexpr uint32_t kABytes = kTcBM * kTcBK * 2;
+  static constexpr uint32_t kBBytes = N * kTcBK * 2;
+  static constexpr uint32_t kPitch = N * 2 + 16;  // staging row pitch (bytes)
+  static constexpr uint32_t kStage = kTcBM * kPitch;
+  static constexpr int kStages0 = (int)((200u * 1024u - kStage) / (kABytes + kBBytes));
+  static constexpr int kStages = kStages0 > 8 ? 8 : kStages0;
+  static constexpr uint32_t kCols = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 2 * N <= 128 ? 128 : 2 * N <= 256 ? 256 : 512;
+  static constexpr size_t kSmem = 1024 + (size_t)kStages * (kABytes + kBBytes) + kStage +
+                                  (2 * kStages + 4) * 8 + 16;
+};
+
+// Persistent: one CTA per SM loops over 128-row tiles.  Warp 0 = TMA producer
+// (runs ahead across tile boundaries through the ring), warp 1 = MMA issuer,
+// warps 2-5 = epilogue.  Two TMEM accumulators: the epilogue of tile i
+// overlaps the MMAs of tile i+1.  The epilogue stages the fp16 tile in shared
+// memory and writes it back with coalesced 16-byte stores.
+template <int N>
+__global__ void __launch_bounds__(192, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
           int64_t m, int num_kb, const __half* __restrict__ bias,
           const __half* __restrict__ row_scale, __half* __restrict__ out, int64_t ldo) {
-  constexpr uint32_t kABytes = kTcBM * kTcBK * 2;
-  constexpr uint32_t kBBytes = N * kTcBK * 2;
-  constexpr uint32_t kCols = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
+  using C = TcCfg<N>;
+  constexpr int S = C::kStages;
   // instruction descriptor: f16 x f16 -> f32, both K-major, M = 128, N
   constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kTcBM >> 4) << 24);
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  unsigned char* sa = base;                                 // [stages][128 x 128 B]
-  unsigned char* sb = base + kTcStages * kABytes;           // [stages][N x 128 B]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sb + kTcStages * kBBytes);
-  uint64_t* empty = full + kTcStages;
-  uint64_t* done = empty + kTcStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  unsigned char* sa = base;                          // [S][128 x 128 B]
+  unsigned char* sb = base + S * C::kABytes;         // [S][N x 128 B]
+  unsigned char* stage = sb + S * C::kBBytes;        // [128][pitch] output tile
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage + C::kStage);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;                       // [2]
+  uint64_t* tempty = tfull + 2;                      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t m0 = (int64_t)blockIdx.x * kTcBM;
+  const int64_t num_tiles = (m + kTcBM - 1) / kTcBM;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kTcStages; ++s) {
+    for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(done, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
@@ -141,7 +174,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(kCols));
+                 "r"(C::kCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -151,62 +184,89 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
 
   if (warp == 0) {
     if (lane == 0) {  // TMA producer
-      for (int kb = 0; kb < num_kb; ++kb) {
-        const int s = kb % kTcStages;
-        if (kb >= kTcStages) mbar_wait(&empty[s], ((kb / kTcStages) + 1) & 1);
-        mbar_expect_tx(&full[s], kABytes + kBBytes);
-        tma_load_2d(sa + s * kABytes, &map_a, &full[s], kb * kTcBK, (int)m0);
-        tma_load_2d(sb + s * kBBytes, &map_b, &full[s], kb * kTcBK, 0);
+      uint32_t it = 0;
+      for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          const int s = it % S;
+          mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+          mbar_expect_tx(&full[s], C::kABytes + C::kBBytes);
+          tma_load_2d(sa + s * C::kABytes, &map_a, &full[s], kb * kTcBK, (int)(tile * kTcBM));
+          tma_load_2d(sb + s * C::kBBytes, &map_b, &full[s], kb * kTcBK, 0);
+        }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
-      for (int kb = 0; kb < num_kb; ++kb) {
-        const int s = kb % kTcStages;
-        mbar_wait(&full[s], (kb / kTcStages) & 1);
+      uint32_t it = 0, tc = 0;
+      for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tc) {
+        const uint32_t a = tc & 1;
+        mbar_wait(&tempty[a], ((tc >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint64_t da = sw128_kmajor_desc(sa + s * kABytes);
-        const uint64_t db = sw128_kmajor_desc(sb + s * kBBytes);
+        const uint32_t acc = tmem + a * N;
+        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          const int s = it % S;
+          mbar_wait(&full[s], (it / S) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t da = sw128_kmajor_desc(sa + s * C::kABytes);
+          const uint64_t db = sw128_kmajor_desc(sb + s * C::kBBytes);
 #pragma unroll
-        for (int k = 0; k < kTcBK / 16; ++k)  // 16 fp16 = 32 B steps inside the swizzle row
-          umma_f16_f32(tmem, da + 2 * k, db + 2 * k, kIdesc, (kb | k) != 0);
-        umma_commit(&empty[s]);
+          for (int k = 0; k < kTcBK / 16; ++k)  // 16 fp16 = 32 B steps inside the swizzle row
+            umma_f16_f32(acc, da + 2 * k, db + 2 * k, kIdesc, (kb | k) != 0);
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&tfull[a]);
       }
-      umma_commit(done);
     }
     __syncwarp();
-  }
-
-  // epilogue: thread (warp w, lane l) owns row m0 + 32w + l = TMEM lane 32w + l
-  mbar_wait(done, 0);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const int64_t row = m0 + warp * 32 + lane;
-  const bool live = row < m;
-  const __half sv = (live && row_scale) ? row_scale[row] : __float2half_rn(1.0f);
+  } else {  // epilogue warps 2..5: TMEM lane quarter = warp % 4
+    const int q = warp & 3;
+    const int r = q * 32 + lane;  // tile row = TMEM lane
+    const int et = threadIdx.x - 64;  // 0..127
+    uint32_t tc = 0;
+    for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tc) {
+      const uint32_t a = tc & 1;
+      const int64_t m0 = tile * kTcBM;
+      const int64_t row = m0 + r;
+      const bool live = row < m;
+      const __half sv = (live && row_scale) ? row_scale[row] : __float2half_rn(1.0f);
+      mbar_wait(&tfull[a], (tc >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      unsigned char* srow = stage + r * C::kPitch;
 #pragma unroll
-  for (int c0 = 0; c0 < N; c0 += 16) {
-    uint32_t v[16];
-    tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    if (live) {
-      __align__(16) __half h[16];
+      for (int c0 = 0; c0 < N; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + a * N + c0, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        __align__(16) __half h[16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        __half t = __float2half_rn(__uint_as_float(v[j]));
-        if (bias) t = __hadd_rn(t, bias[c0 + j]);
-        if (row_scale) t = __hmul_rn(t, sv);
-        h[j] = t;
+        for (int j = 0; j < 16; ++j) {
+          __half t = __float2half_rn(__uint_as_float(v[j]));
+          if (bias) t = __hadd_rn(t, bias[c0 + j]);
+          if (row_scale) t = __hmul_rn(t, sv);
+          h[j] = t;
+        }
+        reinterpret_cast<uint4*>(srow + c0 * 2)[0] = *reinterpret_cast<const uint4*>(&h[0]);
+        reinterpret_cast<uint4*>(srow + c0 * 2)[1] = *reinterpret_cast<const uint4*>(&h[8]);
       }
-      uint4* dst = reinterpret_cast<uint4*>(out + row * ldo + c0);
-      dst[0] = *reinterpret_cast<const uint4*>(&h[0]);
-      dst[1] = *reinterpret_cast<const uint4*>(&h[8]);
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&tempty[a]);  // accumulator drained: the MMA warp may reuse it
+      epi_bar();
+      // coalesced write-back of the live rows: 16-byte chunks, row-major
+      const int rows = (int)((m - m0) < kTcBM ? (m - m0) : kTcBM);
+      constexpr int CPR = N / 8;
+      for (int ch = et; ch < rows * CPR; ch += 128) {
+        const int rr = ch / CPR, c8 = ch - rr * CPR;
+        *reinterpret_cast<uint4*>(out + (m0 + rr) * ldo + c8 * 8) =
+            *reinterpret_cast<const uint4*>(stage + rr * C::kPitch + c8 * 16);
+      }
+      epi_bar();
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::kCols));
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -244,10 +304,17 @@ template <int N>
 static int launch_gemm_tc(const CUtensorMap& ma, const CUtensorMap& mb, int64_t m, int64_t k,
                           const void* bias, const void* row_scale, void* out, int64_t ldo,
                           cudaStream_t st) {
-  constexpr size_t smem = 1024 + kTcStages * (kTcBM + N) * kTcBK * 2 + (2 * kTcStages + 1) * 8 + 16;
+  constexpr size_t smem = TcCfg<N>::kSmem;
+  static_assert(smem <= 227 * 1024, "gemm_tc shared memory budget");
   HG_CUDA(cudaFuncSetAttribute(k_gemm_tc<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int num_kb = (int)((k + kTcBK - 1) / kTcBK);
-  k_gemm_tc<N><<<(unsigned)((m + kTcBM - 1) / kTcBM), 128, smem, st>>>(
+  const int64_t tiles = (m + kTcBM - 1) / kTcBM;
+  int sms = 148;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = (unsigned)(tiles < sms ? tiles : sms);
+  k_gemm_tc<N><<<grid, 192, smem, st>>>(
       ma, mb, m, num_kb, (const __half*)bias, (const __half*)row_scale, (__half*)out, ldo);
   HG_LAUNCHED();
   return HG_OK;
