@@ -255,6 +255,30 @@ class _BiasAggFn(torch.autograd.Function):
         return gh, D.col_sums(gh), None, None
 
 
+class _GCNLayerFn(torch.autograd.Function):
+    """GCNLayer (models.py:456-468) = spmm_agg(add_bias(matmul(x, W), b)) with
+    the GEMM, the bias add and the aggregation's left-norm input scale in one
+    tcgen05 kernel (hg_gemm_tc), then the gather SpMM.  Backward: transposed
+    SpMM, bias gradient = its column sums, dW = x^T dh and dx = dh W^T on
+    cuBLAS (fp32 accumulation, one rounding: matmul's backward, 150-155)."""
+
+    @staticmethod
+    def forward(ctx, x, w, b, bundle, reduction):
+        ctx.bundle, ctx.reduction = bundle, reduction
+        ctx.save_for_backward(x, w)
+        fin, fout = bundle.dg.norm_tables(reduction.norm, False, x.dtype)
+        xs = D.gemm_tc(x, w.t().contiguous(), b, fin)
+        return D.spmm_csr(bundle.dg.view(False), xs, None, None, 1, reduction.scaling, None, fout)
+
+    @staticmethod
+    def backward(ctx, g):
+        x, w = ctx.saved_tensors
+        r = ctx.reduction
+        gh = ctx.bundle.spmm(g.contiguous(), None, r.scaling, _MIRROR[r.norm], transpose=True)
+        gx = gh @ w.t() if ctx.needs_input_grad[0] else None
+        return gx, x.t() @ gh, D.col_sums(gh), None, None
+
+
 def spmm_agg(bundle, x, reduction, width="half2", overflow=None, tag="agg"):
     """Y = norm-scaled aggregation of X; the adjoint runs the transposed graph."""
     y = _AggFn.apply(x, bundle, reduction)
@@ -584,8 +608,12 @@ class GCNLayer:
 
     def __call__(self, bundle, x, mode, width, overflow, tag):
         if getattr(bundle, "fused_bias_agg", False) and self.lin.b is not None:
-            h = matmul(x, self.lin.w.publish(mode))
-            y = _BiasAggFn.apply(h, self.lin.b.publish(mode), bundle, self.reduction)
+            w, b = self.lin.w.publish(mode), self.lin.b.publish(mode)
+            if mode == "half" and w.shape[1] % 16 == 0 and x.shape[1] % 8 == 0:
+                # tensor-core GEMM with the bias / input-scale epilogue fused
+                y = _GCNLayerFn.apply(x, w, b, bundle, self.reduction)
+            else:
+                y = _BiasAggFn.apply(matmul(x, w), b, bundle, self.reduction)
             if overflow is not None:
                 overflow.observe(tag, y.detach())
             return y
