@@ -470,6 +470,30 @@ static int dispatch_fast(const FastArgs& a) {
 
 static size_t elem_size(int dtype) { return dtype == HG_F16 ? 2 : 4; }
 
+// Half the device's L2 (per-device attribute cache), the working-set budget of
+// one aggregation pass's gathered feature slab.
+static size_t l2_budget() {
+  static size_t cache[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return (size_t)48 << 20;
+  if (!cache[dev]) {
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    cache[dev] = l2 > 0 ? (size_t)l2 / 2 : (size_t)48 << 20;
+  }
+  return cache[dev];
+}
+
+// Slab width (columns) for hg_spmm: F itself unless X exceeds the L2 budget and
+// a multiple of 32 columns >= 32 fits it.
+static int slab_width(int64_t n_cols, int F, size_t es, bool sliceable) {
+  if (!sliceable || n_cols <= 0) return F;
+  const size_t budget = l2_budget();
+  if ((size_t)F * n_cols * es <= budget) return F;
+  const int64_t cand = (int64_t)(budget / ((size_t)n_cols * es)) / 32 * 32;
+  return (cand >= 32 && cand < F) ? (int)cand : F;
+}
+
 // X' = rnd(X * s[:, None]): the vectorised row-scale pass of dense.cu.
 static int scale_rows(const void* x, const void* s, int64_t rows, int F, void* out, int dtype,
                       cudaStream_t st) {
@@ -532,7 +556,20 @@ extern "C" int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_ro
   a.x = x; a.y = y; a.carry = carry; a.F = F; a.ldx = (int)ldx; a.ldy = (int)ldy;
   a.fmode = out_factor == nullptr ? 0 : (scaling == HG_SCALING_POST ? 1 : 2);
   a.fout = out_factor; a.st = st;
-  return dtype == HG_F16 ? dispatch_fast<__half>(a) : dispatch_fast<float>(a);
+  // Column slabs: when X (n_cols x F) overflows the L2 budget but a slab of
+  // >= 32 columns fits, aggregate slab by slab so the random row gathers of
+  // each pass hit L2 (the column stream is re-read once per slab, sequentially).
+  const int W = slab_width(n_cols, F, elem_size(dtype), w == nullptr || heads == 1);
+  for (int j = 0; j < F; j += W) {
+    FastArgs s = a;
+    s.F = F - j < W ? F - j : W;
+    if (heads == 1) s.fh = s.F;
+    s.x = static_cast<const char*>(x) + (size_t)j * elem_size(dtype);
+    s.y = static_cast<char*>(y) + (size_t)j * elem_size(dtype);
+    const int rc = dtype == HG_F16 ? dispatch_fast<__half>(s) : dispatch_fast<float>(s);
+    if (rc) return rc;
+  }
+  return HG_OK;
 }
 
 // ------------------------------------------------------ reference edge order

@@ -734,3 +734,30 @@ def test_gemm_tc_vs_f64(cuda, m, k, n, epi):
         h = (h * sc).astype(np.float16).astype(np.float64)
         slack = slack * sc + 2.0 ** -10 * np.abs(h)
     assert np.all(np.abs(got - h) <= slack + 2.0 ** -24)
+
+
+@pytest.mark.parametrize("f", [256, 520])
+def test_spmm_column_slabs_vs_f64(cuda, f):
+    """X larger than half the L2 makes hg_spmm aggregate in column slabs (each
+    pass's gathers stay L2-resident): same tolerance as the one-pass kernel,
+    checked on sampled rows (incl. split heavy rows)."""
+    from paper_2411_01109_b200 import device as D, graphgen
+
+    dg = graphgen.reddit_like(9, n=200_000, e=3_000_000)
+    assert 2 * f * dg.n > 63 * 2**20  # above the slab threshold on B200
+    x = torch.randn(dg.n, f, device=cuda, dtype=torch.float16)
+    y = D.spmm(dg, x, None, "discretized", "both")
+    assert torch.equal(y, D.spmm(dg, x, None, "discretized", "both"))
+    off = dg.offsets.cpu().numpy()
+    cols = dg.cols.cpu().numpy()
+    deg = np.diff(off)
+    rng = np.random.default_rng(f)
+    rows = np.concatenate([np.argsort(deg)[-5:], rng.integers(0, dg.n, 300)])
+    fin, fout = dg.norm_tables("both", False, torch.float16)
+    fin, fout = fin.cpu().numpy().astype(np.float64), fout.cpu().numpy().astype(np.float64)
+    xs = (x.cpu().numpy().astype(np.float64) * fin[:, None]).astype(np.float16).astype(np.float64)
+    yh = y.cpu().numpy().astype(np.float64)
+    for r in rows:
+        c = cols[off[r]:off[r + 1]]
+        want = xs[c].sum(0) * fout[r]
+        assert np.all(np.abs(yh[r] - want) <= TOL * np.maximum(1.0, np.abs(want))), r
