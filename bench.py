@@ -76,6 +76,18 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
 
+    def wait_first_sample(self, timeout=3.0):
+        """Block until nvidia-smi has written its first sample (its start-up
+        latency would otherwise leave a short timed region unsampled)."""
+        t0 = time.time()
+        while self.proc is not None and time.time() - t0 < timeout:
+            try:
+                if Path(self.path).read_text().strip():
+                    return
+            except OSError:
+                pass
+            time.sleep(0.02)
+
     def summary(self):
         rows = []
         try:
@@ -382,6 +394,10 @@ def b200_arm(args, ws, rank, local):
             ms = max_over_ranks(dist, ms)
         return ms, loss
 
+    # clocks are sampled from before the first timed step to after the last
+    clocks = ClockSampler(local).__enter__()
+    clocks.wait_first_sample()
+
     # ---- eager pass: SpMM roofline (CUDA events around every hg_spmm) ----
     D.Probe.reset(timing=True)
     eager_ms, _ = timed_steps(args.steps)
@@ -395,8 +411,8 @@ def b200_arm(args, ws, rank, local):
         tr.capture()
         tr.step()
         torch.cuda.synchronize()
-    with ClockSampler(local) as clocks:
-        t_ms, loss = timed_steps(args.steps)
+    t_ms, loss = timed_steps(args.steps)
+    clocks.__exit__(None, None, None)
     final_loss = float(loss)
 
     # ---- end to end through the public loop: host features in, loss out ----
