@@ -238,15 +238,16 @@ int hg_adam_step(float* master, float* m, float* v, const void* grad, int grad_d
 
 /* models.matmul -> add_bias -> left-norm input scaling (models.py:141-166,
  * kernels.py:358-361) as one tensor-core GEMM with a fused epilogue:
- *   out[m, n] = rnd(rnd(rnd(sum_k a[m, k] * bt[n, k]) + bias[n]) * row_scale[m])
+ *   out[m, n] = rnd(rnd(rnd(sum_k a[m, k] * bt[n, k]) + bias[n]) * row_scale[m]),
+ * then max(out, 0) when relu != 0 (models.relu, 176-185)
  * binary16 operands, fp32 accumulation in TMEM (tcgen05.mma kind::f16, M=128
  * tiles, TMA-fed 4-stage ring), one rounding per step; bias / row_scale may be
  * NULL.  a: [m, k] pitch lda; bt: [n, k] pitch ldb (B transposed, K-major);
  * out: [m, n] pitch ldo.  n: multiple of 16 in [16, 256]; pitches multiples
  * of 8 elements; 16-byte aligned pointers. */
 int hg_gemm_tc(const void* a, int64_t m, int64_t k, int64_t lda, const void* bt, int32_t n,
-               int64_t ldb, const void* bias, const void* row_scale, void* out, int64_t ldo,
-               void* stream);
+               int64_t ldb, const void* bias, const void* row_scale, int32_t relu, void* out,
+               int64_t ldo, void* stream);
 
 /* ----------------------------------------------------------------- ingest */
 
@@ -320,6 +321,18 @@ int hg_scale_f64(const void* x, double s, void* out, int64_t count, int dtype, v
  * bias and row_scale may each be NULL (step skipped).  x, out: [rows, F]. */
 int hg_bias_scale_rows(const void* x, const void* bias, const void* row_scale, int64_t rows,
                        int32_t F, void* out, int dtype, void* stream);
+
+/* GIN combine, scale_combine (models.py:220-240):
+ *   out = rnd(rnd(x * one_plus_eps) + rnd(a * lam)) (products in fp64);
+ * backward: gx = rnd(g * one_plus_eps), ga = rnd(g * lam), and
+ * gope = rnd(sum x * g) with an fp64, fixed-order sum.  gx / ga / gope may be
+ * NULL (not needed); one_plus_eps / gope are device scalars. */
+int hg_scale_combine(const void* x, const void* a, const void* one_plus_eps, double lam,
+                     int64_t count, void* out, int dtype, void* stream);
+int hg_scale_combine_bwd_workspace(size_t* bytes);
+int hg_scale_combine_bwd(const void* x, const void* g, const void* one_plus_eps, double lam,
+                         int64_t count, void* gx, void* ga, void* gope, int dtype, void* ws,
+                         size_t ws_bytes, void* stream);
 
 /* add_bias backward (models.py:168-170): out[f] = rnd(sum_r x[r, f]), fp32
  * accumulation in a fixed (deterministic) order. */

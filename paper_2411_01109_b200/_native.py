@@ -58,7 +58,7 @@ SIGNATURES = {
     "hg_head_dots_bwd_workspace": [_I32, _I32, _PSZ],
     "hg_head_dots_bwd": [_P, _P, _P, _P, _P, _I64, _I32, _I32, _P, _P, _P, c_int, _P, c_size_t,
                          _P],
-    "hg_gemm_tc": [_P, _I64, _I64, _I64, _P, _I32, _I64, _P, _P, _P, _I64, _P],
+    "hg_gemm_tc": [_P, _I64, _I64, _I64, _P, _I32, _I64, _P, _P, _I32, _P, _I64, _P],
     "hg_count_lines_workspace": [_I64, _PSZ],
     "hg_count_lines": [_P, _I64, _PI64, _P, c_size_t, _P],
     "hg_parse_edges_workspace": [_I64, _I64, _PSZ],
@@ -70,6 +70,9 @@ SIGNATURES = {
     "hg_edge_sums_fast": [_P, _I64, _P, _P, _I32, _P, _P, _I64, _P, _I64, _I32, c_int, _P],
     "hg_head_mean": [_P, _I64, _I32, _I32, _P, c_int, _P],
     "hg_head_mean_bwd": [_P, _I64, _I32, _I32, _P, c_int, _P],
+    "hg_scale_combine": [_P, _P, _P, c_double, _I64, _P, c_int, _P],
+    "hg_scale_combine_bwd_workspace": [_PSZ],
+    "hg_scale_combine_bwd": [_P, _P, _P, c_double, _I64, _P, _P, _P, c_int, _P, c_size_t, _P],
     "hg_bias_scale_rows": [_P, _P, _P, _I64, _I32, _P, c_int, _P],
     "hg_col_sums_workspace": [_I64, _I32, _PSZ],
     "hg_col_sums": [_P, _I64, _I32, _P, c_int, _P, c_size_t, _P],

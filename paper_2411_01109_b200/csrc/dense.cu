@@ -155,9 +155,168 @@ static int launch_col_sums(const void* x, int64_t rows, int F, void* out, float*
   return HG_OK;
 }
 
+// GIN combine (models.py:220-240): out = rnd(rnd(x * ope) + rnd(a * lam)), the
+// products formed in fp64 (lam is a Python float; x * ope of two fp16 values is
+// exact in fp32 already).  Backward: gx = rnd(g * ope), ga = rnd(g * lam) and
+// the (1 + eps) gradient rnd(sum x * g) with an fp64 sum (per-block partials,
+// fixed-order final fold: deterministic).
+template <typename T, int V>
+__global__ void __launch_bounds__(256)
+k_scale_combine(const T* __restrict__ x, const T* __restrict__ a, const T* __restrict__ ope,
+                double lam, int64_t count, T* __restrict__ out) {
+  using Raw = typename Vec<T, V>::raw;
+  const double o = Num<T>::to_d(*ope);
+  const int64_t nv = count / V;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    Raw xv = reinterpret_cast<const Raw*>(x)[i];
+    const Raw av = reinterpret_cast<const Raw*>(a)[i];
+    T* xe = reinterpret_cast<T*>(&xv);
+    const T* ae = reinterpret_cast<const T*>(&av);
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      const T u = Num<T>::from_d(Num<T>::to_d(xe[k]) * o);
+      const T v = Num<T>::from_d(Num<T>::to_d(ae[k]) * lam);
+      xe[k] = Num<T>::add(u, v);
+    }
+    reinterpret_cast<Raw*>(out)[i] = xv;
+  }
+}
+
+constexpr int kCombBlocks = 148 * 8;
+
+template <typename T, int V>
+__global__ void __launch_bounds__(256)
+k_scale_combine_bwd(const T* __restrict__ x, const T* __restrict__ g, const T* __restrict__ ope,
+                    double lam, int64_t count, T* __restrict__ gx, T* __restrict__ ga,
+                    double* __restrict__ part) {
+  using Raw = typename Vec<T, V>::raw;
+  __shared__ double red[8];
+  const double o = Num<T>::to_d(*ope);
+  const int64_t nv = count / V;
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const Raw gv = reinterpret_cast<const Raw*>(g)[i];
+    const T* ge = reinterpret_cast<const T*>(&gv);
+    if (part) {
+      const Raw xv = reinterpret_cast<const Raw*>(x)[i];
+      const T* xe = reinterpret_cast<const T*>(&xv);
+#pragma unroll
+      for (int k = 0; k < V; ++k) acc = fma(Num<T>::to_d(xe[k]), Num<T>::to_d(ge[k]), acc);
+    }
+    if (gx) {
+      Raw r;
+      T* re = reinterpret_cast<T*>(&r);
+#pragma unroll
+      for (int k = 0; k < V; ++k) re[k] = Num<T>::from_d(Num<T>::to_d(ge[k]) * o);
+      reinterpret_cast<Raw*>(gx)[i] = r;
+    }
+    if (ga) {
+      Raw r;
+      T* re = reinterpret_cast<T*>(&r);
+#pragma unroll
+      for (int k = 0; k < V; ++k) re[k] = Num<T>::from_d(Num<T>::to_d(ge[k]) * lam);
+      reinterpret_cast<Raw*>(ga)[i] = r;
+    }
+  }
+  if (!part) return;
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    part[blockIdx.x] = t;
+  }
+}
+
+template <typename T>
+__global__ void k_scale_combine_fold(const double* __restrict__ part, int nb, T* __restrict__ gope) {
+  __shared__ double red[32];
+  double t = 0.0;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) t += part[i];
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) t += __shfl_xor_sync(0xffffffffu, t, s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double u = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) u += red[w];
+    *gope = Num<T>::from_d(u);
+  }
+}
+
 }  // namespace hg
 
 using namespace hg;
+
+extern "C" int hg_scale_combine(const void* x, const void* a, const void* one_plus_eps,
+                                double lam, int64_t count, void* out, int dtype, void* stream) {
+  HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
+  HG_REQUIRE(count >= 0 && one_plus_eps, "hg_scale_combine: bad arguments");
+  if (count == 0) return HG_OK;
+  cudaStream_t st = as_stream(stream);
+  const bool vec = count % 8 == 0 && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(a) |
+                                       reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+  if (dtype == HG_F16) {
+    if (vec) k_scale_combine<__half, 8><<<grid_for(count / 8, 256, 148 * 16), 256, 0, st>>>(
+        (const __half*)x, (const __half*)a, (const __half*)one_plus_eps, lam, count, (__half*)out);
+    else k_scale_combine<__half, 1><<<grid_for(count, 256, 148 * 16), 256, 0, st>>>(
+        (const __half*)x, (const __half*)a, (const __half*)one_plus_eps, lam, count, (__half*)out);
+  } else {
+    if (vec) k_scale_combine<float, 4><<<grid_for(count / 4, 256, 148 * 16), 256, 0, st>>>(
+        (const float*)x, (const float*)a, (const float*)one_plus_eps, lam, count, (float*)out);
+    else k_scale_combine<float, 1><<<grid_for(count, 256, 148 * 16), 256, 0, st>>>(
+        (const float*)x, (const float*)a, (const float*)one_plus_eps, lam, count, (float*)out);
+  }
+  HG_LAUNCHED();
+  return HG_OK;
+}
+
+extern "C" int hg_scale_combine_bwd_workspace(size_t* bytes) {
+  HG_REQUIRE(bytes, "hg_scale_combine_bwd_workspace: bad arguments");
+  *bytes = (size_t)kCombBlocks * sizeof(double);
+  return HG_OK;
+}
+
+extern "C" int hg_scale_combine_bwd(const void* x, const void* g, const void* one_plus_eps,
+                                    double lam, int64_t count, void* gx, void* ga, void* gope,
+                                    int dtype, void* ws, size_t ws_bytes, void* stream) {
+  HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
+  HG_REQUIRE(count >= 0 && one_plus_eps && g, "hg_scale_combine_bwd: bad arguments");
+  HG_REQUIRE(!gope || (x && ws && ws_bytes >= (size_t)kCombBlocks * sizeof(double)),
+             "hg_scale_combine_bwd: the (1+eps) gradient needs x and a workspace");
+  cudaStream_t st = as_stream(stream);
+  double* part = gope ? (double*)ws : nullptr;
+  const int64_t V = dtype == HG_F16 ? 8 : 4;
+  const bool vec = count % V == 0 && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(g) |
+                                       reinterpret_cast<uintptr_t>(gx) | reinterpret_cast<uintptr_t>(ga)) & 15) == 0;
+  const int nb = grid_for(vec ? count / V : count, 256, kCombBlocks);
+  if (dtype == HG_F16) {
+    if (vec) k_scale_combine_bwd<__half, 8><<<nb, 256, 0, st>>>(
+        (const __half*)x, (const __half*)g, (const __half*)one_plus_eps, lam, count, (__half*)gx,
+        (__half*)ga, part);
+    else k_scale_combine_bwd<__half, 1><<<nb, 256, 0, st>>>(
+        (const __half*)x, (const __half*)g, (const __half*)one_plus_eps, lam, count, (__half*)gx,
+        (__half*)ga, part);
+  } else {
+    if (vec) k_scale_combine_bwd<float, 4><<<nb, 256, 0, st>>>(
+        (const float*)x, (const float*)g, (const float*)one_plus_eps, lam, count, (float*)gx,
+        (float*)ga, part);
+    else k_scale_combine_bwd<float, 1><<<nb, 256, 0, st>>>(
+        (const float*)x, (const float*)g, (const float*)one_plus_eps, lam, count, (float*)gx,
+        (float*)ga, part);
+  }
+  HG_LAUNCHED();
+  if (gope) {
+    if (dtype == HG_F16) k_scale_combine_fold<__half><<<1, 1024, 0, st>>>(part, nb, (__half*)gope);
+    else k_scale_combine_fold<float><<<1, 1024, 0, st>>>(part, nb, (float*)gope);
+    HG_LAUNCHED();
+  }
+  return HG_OK;
+}
 
 extern "C" int hg_bias_scale_rows(const void* x, const void* bias, const void* row_scale,
                                   int64_t rows, int32_t F, void* out, int dtype, void* stream) {

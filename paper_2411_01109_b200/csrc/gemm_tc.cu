@@ -137,7 +137,7 @@ template <int N>
 __global__ void __launch_bounds__(192, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
           int64_t m, int num_kb, const __half* __restrict__ bias,
-          const __half* __restrict__ row_scale, __half* __restrict__ out, int64_t ldo) {
+          const __half* __restrict__ row_scale, __half* __restrict__ out, int64_t ldo, int relu) {
   using C = TcCfg<N>;
   constexpr int S = C::kStages;
   // instruction descriptor: f16 x f16 -> f32, both K-major, M = 128, N
@@ -244,6 +244,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
           __half t = __float2half_rn(__uint_as_float(v[j]));
           if (bias) t = __hadd_rn(t, bias[c0 + j]);
           if (row_scale) t = __hmul_rn(t, sv);
+          if (relu && !(__hgt(t, __float2half_rn(0.0f)))) t = __float2half_rn(0.0f);
           h[j] = t;
         }
         reinterpret_cast<uint4*>(srow + c0 * 2)[0] = *reinterpret_cast<const uint4*>(&h[0]);
@@ -303,7 +304,7 @@ static bool make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t co
 template <int N>
 static int launch_gemm_tc(const CUtensorMap& ma, const CUtensorMap& mb, int64_t m, int64_t k,
                           const void* bias, const void* row_scale, void* out, int64_t ldo,
-                          cudaStream_t st) {
+                          int relu, cudaStream_t st) {
   constexpr size_t smem = TcCfg<N>::kSmem;
   static_assert(smem <= 227 * 1024, "gemm_tc shared memory budget");
   HG_CUDA(cudaFuncSetAttribute(k_gemm_tc<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -315,7 +316,7 @@ static int launch_gemm_tc(const CUtensorMap& ma, const CUtensorMap& mb, int64_t 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const unsigned grid = (unsigned)(tiles < sms ? tiles : sms);
   k_gemm_tc<N><<<grid, 192, smem, st>>>(
-      ma, mb, m, num_kb, (const __half*)bias, (const __half*)row_scale, (__half*)out, ldo);
+      ma, mb, m, num_kb, (const __half*)bias, (const __half*)row_scale, (__half*)out, ldo, relu);
   HG_LAUNCHED();
   return HG_OK;
 }
@@ -326,7 +327,7 @@ using namespace hg;
 
 extern "C" int hg_gemm_tc(const void* a, int64_t m, int64_t k, int64_t lda, const void* bt,
                           int32_t n, int64_t ldb, const void* bias, const void* row_scale,
-                          void* out, int64_t ldo, void* stream) {
+                          int32_t relu, void* out, int64_t ldo, void* stream) {
   HG_REQUIRE(a && bt && out && m >= 0 && k > 0, "hg_gemm_tc: bad arguments");
   HG_REQUIRE(n >= 16 && n <= 256 && n % 16 == 0, "hg_gemm_tc: N=%d must be a multiple of 16 in [16, 256]", n);
   HG_REQUIRE(lda >= k && ldb >= k && ldo >= n && lda % 8 == 0 && ldb % 8 == 0 && ldo % 8 == 0,
@@ -340,7 +341,7 @@ extern "C" int hg_gemm_tc(const void* a, int64_t m, int64_t k, int64_t lda, cons
              "hg_gemm_tc: cuTensorMapEncodeTiled failed");
   cudaStream_t st = as_stream(stream);
   switch (n) {
-#define HG_TC(NN) case NN: return launch_gemm_tc<NN>(ma, mb, m, k, bias, row_scale, out, ldo, st);
+#define HG_TC(NN) case NN: return launch_gemm_tc<NN>(ma, mb, m, k, bias, row_scale, out, ldo, relu, st);
     HG_TC(16) HG_TC(32) HG_TC(48) HG_TC(64) HG_TC(80) HG_TC(96) HG_TC(112) HG_TC(128)
     HG_TC(144) HG_TC(160) HG_TC(176) HG_TC(192) HG_TC(208) HG_TC(224) HG_TC(240) HG_TC(256)
 #undef HG_TC

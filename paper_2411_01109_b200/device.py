@@ -648,9 +648,10 @@ def edge_rowsum(dg: DeviceGraph, v, transpose=False):
     return rowsum_view(view, v, view.perm if transpose else None)
 
 
-def gemm_tc(a, bt, bias=None, row_scale=None, out=None):
-    """rnd(rnd(rnd(a @ bt.T) + bias) * row_scale[:, None]) on the tcgen05 tensor
-    cores (hg_gemm_tc): a [M, K] fp16, bt [N, K] fp16 (N % 16 == 0)."""
+def gemm_tc(a, bt, bias=None, row_scale=None, out=None, relu=False):
+    """rnd(rnd(rnd(a @ bt.T) + bias) * row_scale[:, None]) (then max(., 0) with
+    relu) on the tcgen05 tensor cores (hg_gemm_tc): a [M, K] fp16, bt [N, K]
+    fp16 (N % 16 == 0)."""
     _require_cuda(a, bt)
     if a.dtype != torch.float16 or bt.dtype != torch.float16:
         raise ValueError("hg_gemm_tc takes binary16 operands")
@@ -663,8 +664,8 @@ def gemm_tc(a, bt, bias=None, row_scale=None, out=None):
         out = torch.empty((m, n), dtype=torch.float16, device=a.device)
     nat.call("hg_gemm_tc", _p(a), m, k, a.stride(0), _p(bt), n, bt.stride(0),
              _p(None if bias is None else bias.contiguous()),
-             _p(None if row_scale is None else row_scale.contiguous()), _p(out), out.stride(0),
-             _stream())
+             _p(None if row_scale is None else row_scale.contiguous()), int(relu), _p(out),
+             out.stride(0), _stream())
     Probe.launches += 1
     return out
 
@@ -685,6 +686,32 @@ def bias_scale_rows(x, bias=None, row_scale=None, out=None):
              _dtype_code(x), _stream())
     Probe.launches += 1
     return out
+
+
+def scale_combine(x, a, one_plus_eps, lam):
+    """GIN combine rnd(rnd(x * ope) + rnd(a * lam)) in one pass (hg_scale_combine)."""
+    _require_cuda(x, a)
+    x, a = x.contiguous(), a.contiguous()
+    out = torch.empty_like(x)
+    nat.call("hg_scale_combine", _p(x), _p(a), _p(one_plus_eps.contiguous()), float(lam),
+             x.numel(), _p(out), _dtype_code(x), _stream())
+    Probe.launches += 1
+    return out
+
+
+def scale_combine_bwd(x, g, one_plus_eps, lam, need_gx=True, need_ga=True, need_gope=True):
+    """(gx, ga, gope) of scale_combine; entries not needed are None."""
+    g = g.contiguous()
+    x = x.contiguous()
+    gx = torch.empty_like(g) if need_gx else None
+    ga = torch.empty_like(g) if need_ga else None
+    gope = torch.empty_like(one_plus_eps) if need_gope else None
+    ws = workspace(nat.size_query("hg_scale_combine_bwd_workspace"), g.device) if need_gope else None
+    nat.call("hg_scale_combine_bwd", _p(x), _p(g), _p(one_plus_eps.contiguous()), float(lam),
+             g.numel(), _p(gx), _p(ga), _p(gope), _dtype_code(g), _p(ws),
+             0 if ws is None else ws.numel(), _stream())
+    Probe.launches += 1 + int(need_gope)
+    return gx, ga, gope
 
 
 def col_sums(x):

@@ -467,12 +467,17 @@ class _ScaleCombineFn(torch.autograd.Function):
     def forward(ctx, x, a, ope, lam):
         ctx.lam = lam
         ctx.save_for_backward(x, ope)
+        if x.is_cuda:
+            return D.scale_combine(x, a, ope, lam)
         return x * ope + D.scale_f64(a, lam)
 
     @staticmethod
     def backward(ctx, g):
         x, ope = ctx.saved_tensors
         g = g.contiguous()
+        if g.is_cuda:
+            gx, ga, gope = D.scale_combine_bwd(x, g, ope, ctx.lam, *ctx.needs_input_grad[:3])
+            return gx, ga, gope, None
         gx = g * ope if ctx.needs_input_grad[0] else None
         ga = D.scale_f64(g, ctx.lam) if ctx.needs_input_grad[1] else None
         gope = (x.double() * g.double()).sum().to(ope.dtype).reshape(ope.shape) \
@@ -588,11 +593,39 @@ class Linear:
     def params(self):
         return [self.w] + ([self.b] if self.b is not None else [])
 
-    def __call__(self, x, mode):
-        out = matmul(x, self.w.publish(mode))
+    def __call__(self, x, mode, tc=False, relu_out=False):
+        """tc: run on the tcgen05 GEMM with the bias (and, with relu_out, the
+        following ReLU) fused into its epilogue when the shapes allow."""
+        w = self.w.publish(mode)
+        if (tc and mode == "half" and x.is_cuda and self.b is not None and w.shape[1] % 16 == 0
+                and x.shape[1] % 8 == 0):
+            return _LinearTCFn.apply(x, w, self.b.publish(mode), relu_out)
+        out = matmul(x, w)
         if self.b is not None:
             out = add_bias(out, self.b.publish(mode))
-        return out
+        return relu(out) if relu_out else out
+
+
+class _LinearTCFn(torch.autograd.Function):
+    """[relu](add_bias(matmul(x, W), b)) (models.py:141-185) as one tcgen05 GEMM
+    with the epilogue fused; backward on cuBLAS (fp32 accumulation, one
+    rounding), the ReLU mask taken from the output (y > 0 iff pre-activation > 0)."""
+
+    @staticmethod
+    def forward(ctx, x, w, b, relu_out):
+        y = D.gemm_tc(x, w.t().contiguous(), b, None, relu=relu_out)
+        ctx.relu_out = relu_out
+        ctx.save_for_backward(x, w, y if relu_out else None)
+        return y
+
+    @staticmethod
+    def backward(ctx, g):
+        x, w, y = ctx.saved_tensors
+        g = g.contiguous()
+        if ctx.relu_out:
+            g = torch.where(y > 0, g, torch.zeros((), dtype=g.dtype, device=g.device))
+        gx = g @ w.t() if ctx.needs_input_grad[0] else None
+        return gx, x.t() @ g, D.col_sums(g), None
 
 
 class GCNLayer:
@@ -639,7 +672,8 @@ class GINLayer:
     def __call__(self, bundle, x, mode, width, overflow, tag):
         agg = spmm_agg(bundle, x, self.reduction, width, overflow, tag)
         mixed = scale_combine(x, agg, self.one_plus_eps.publish(mode), self.lam)
-        return self.phi2(relu(self.phi1(mixed, mode)), mode)
+        tc = getattr(bundle, "fused_bias_agg", False)
+        return self.phi2(self.phi1(mixed, mode, tc=tc, relu_out=True), mode, tc=tc)
 
 
 class GATLayer:

@@ -706,7 +706,7 @@ def test_sddmm_fast_vs_f64(cuda, heads, fh):
 
 @pytest.mark.parametrize("m,k,n", [(1000, 608, 64), (300, 64, 48), (4097, 1440, 16), (129, 16, 256),
                                    (5000, 104, 128), (77, 200, 32)])
-@pytest.mark.parametrize("epi", ["none", "bias", "both"])
+@pytest.mark.parametrize("epi", ["none", "bias", "both", "relu"])
 def test_gemm_tc_vs_f64(cuda, m, k, n, epi):
     """tcgen05 GEMM + fused epilogue against float64: the accumulation differs
     from the reference only in fp32 summation order, so each output is within
@@ -719,7 +719,8 @@ def test_gemm_tc_vs_f64(cuda, m, k, n, epi):
     b = rng.normal(0, 1, n).astype(np.float16) if epi != "none" else None
     s = rng.uniform(0, 1, m).astype(np.float16) if epi == "both" else None
     got = D.gemm_tc(_t(a, cuda), _t(np.ascontiguousarray(w.T), cuda),
-                    None if b is None else _t(b, cuda), None if s is None else _t(s, cuda))
+                    None if b is None else _t(b, cuda), None if s is None else _t(s, cuda),
+                    relu=epi == "relu")
     got = got.cpu().numpy().astype(np.float64)
     acc = a.astype(np.float64) @ w.astype(np.float64)
     h = acc.astype(np.float16).astype(np.float64)
@@ -733,6 +734,8 @@ def test_gemm_tc_vs_f64(cuda, m, k, n, epi):
         sc = s.astype(np.float64)[:, None]
         h = (h * sc).astype(np.float16).astype(np.float64)
         slack = slack * sc + 2.0 ** -10 * np.abs(h)
+    if epi == "relu":
+        h = np.maximum(h, 0.0)
     assert np.all(np.abs(got - h) <= slack + 2.0 ** -24)
 
 
@@ -761,3 +764,30 @@ def test_spmm_column_slabs_vs_f64(cuda, f):
         c = cols[off[r]:off[r + 1]]
         want = xs[c].sum(0) * fout[r]
         assert np.all(np.abs(yh[r] - want) <= TOL * np.maximum(1.0, np.abs(want))), r
+
+
+@pytest.mark.parametrize("count", [8, 1000, 999, 2_449_029 * 104 // 64])
+def test_scale_combine_bits(cuda, count):
+    """GIN combine (models.py:220-240) forward bit-exact; backward gx / ga
+    bit-exact, the (1+eps) gradient an fp64 sum within one fp16 rounding."""
+    from paper_2411_01109_b200 import device as D
+
+    rng = np.random.default_rng(count)
+    x = rng.normal(0, 3, count).astype(np.float16)
+    a = rng.normal(0, 30, count).astype(np.float16)
+    g = rng.normal(0, 1, count).astype(np.float16)
+    ope = np.array(1.0009765625, dtype=np.float16)
+    lam = 0.1
+    got = D.scale_combine(_t(x, cuda), _t(a, cuda), _t(ope, cuda), lam).cpu().numpy()
+    u = (x.astype(np.float64) * float(ope)).astype(np.float16).astype(np.float64)
+    v = (a.astype(np.float64) * lam).astype(np.float16).astype(np.float64)
+    np.testing.assert_array_equal(bits(got), bits((u + v).astype(np.float16)))
+    gx, ga, gope = D.scale_combine_bwd(_t(x, cuda), _t(g, cuda), _t(ope, cuda), lam)
+    np.testing.assert_array_equal(bits(gx.cpu().numpy()),
+                                  bits((g.astype(np.float64) * float(ope)).astype(np.float16)))
+    np.testing.assert_array_equal(bits(ga.cpu().numpy()),
+                                  bits((g.astype(np.float64) * lam).astype(np.float16)))
+    want = np.float64((x.astype(np.float64) * g.astype(np.float64)).sum())
+    assert abs(float(gope.cpu()) - want) <= 2.0 ** -10 * abs(want) + 1e-3
+    _, _, only = D.scale_combine_bwd(_t(x, cuda), _t(g, cuda), _t(ope, cuda), lam, False, False)
+    assert torch.equal(only, gope)
