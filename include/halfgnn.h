@@ -334,6 +334,9 @@ int hg_scale_combine_bwd(const void* x, const void* g, const void* one_plus_eps,
                          int64_t count, void* gx, void* ga, void* gope, int dtype, void* ws,
                          size_t ws_bytes, void* stream);
 
+/* relu backward (models.py:176-185) from the ReLU output y: out = y > 0 ? g : 0. */
+int hg_relu_grad(const void* y, const void* g, int64_t count, void* out, int dtype, void* stream);
+
 /* add_bias backward (models.py:168-170): out[f] = rnd(sum_r x[r, f]), fp32
  * accumulation in a fixed (deterministic) order. */
 int hg_col_sums_workspace(int64_t rows, int32_t F, size_t* bytes);

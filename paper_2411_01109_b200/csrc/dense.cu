@@ -318,6 +318,50 @@ extern "C" int hg_scale_combine_bwd(const void* x, const void* g, const void* on
   return HG_OK;
 }
 
+namespace hg {
+// relu backward (models.py:176-185) from the ReLU's output: g where y > 0, else 0.
+template <typename T, int V>
+__global__ void k_relu_grad(const T* __restrict__ y, const T* __restrict__ g, int64_t count,
+                            T* __restrict__ out) {
+  using Raw = typename Vec<T, V>::raw;
+  const int64_t nv = count / V;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const Raw yv = reinterpret_cast<const Raw*>(y)[i];
+    Raw gv = reinterpret_cast<const Raw*>(g)[i];
+    const T* ye = reinterpret_cast<const T*>(&yv);
+    T* ge = reinterpret_cast<T*>(&gv);
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+      if (!Num<T>::gt0(ye[k])) ge[k] = Num<T>::zero();
+    reinterpret_cast<Raw*>(out)[i] = gv;
+  }
+}
+}  // namespace hg
+
+extern "C" int hg_relu_grad(const void* y, const void* g, int64_t count, void* out, int dtype,
+                            void* stream) {
+  HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
+  if (count == 0) return HG_OK;
+  cudaStream_t st = as_stream(stream);
+  const int64_t V = dtype == HG_F16 ? 8 : 4;
+  const bool vec = count % V == 0 && ((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(g) |
+                                       reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+  if (dtype == HG_F16) {
+    if (vec) k_relu_grad<__half, 8><<<grid_for(count / 8, 256, 148 * 16), 256, 0, st>>>(
+        (const __half*)y, (const __half*)g, count, (__half*)out);
+    else k_relu_grad<__half, 1><<<grid_for(count, 256, 148 * 16), 256, 0, st>>>(
+        (const __half*)y, (const __half*)g, count, (__half*)out);
+  } else {
+    if (vec) k_relu_grad<float, 4><<<grid_for(count / 4, 256, 148 * 16), 256, 0, st>>>(
+        (const float*)y, (const float*)g, count, (float*)out);
+    else k_relu_grad<float, 1><<<grid_for(count, 256, 148 * 16), 256, 0, st>>>(
+        (const float*)y, (const float*)g, count, (float*)out);
+  }
+  HG_LAUNCHED();
+  return HG_OK;
+}
+
 extern "C" int hg_bias_scale_rows(const void* x, const void* bias, const void* row_scale,
                                   int64_t rows, int32_t F, void* out, int dtype, void* stream) {
   HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);

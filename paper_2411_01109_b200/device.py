@@ -714,6 +714,15 @@ def scale_combine_bwd(x, g, one_plus_eps, lam, need_gx=True, need_ga=True, need_
     return gx, ga, gope
 
 
+def relu_grad(y, g):
+    """g where y > 0 else 0 (y = the ReLU's output), one pass (hg_relu_grad)."""
+    y, g = y.contiguous(), g.contiguous()
+    out = torch.empty_like(g)
+    nat.call("hg_relu_grad", _p(y), _p(g), g.numel(), _p(out), _dtype_code(g), _stream())
+    Probe.launches += 1
+    return out
+
+
 def col_sums(x):
     """rnd(sum over rows) per column, fp32 accumulation (hg_col_sums)."""
     _require_cuda(x)

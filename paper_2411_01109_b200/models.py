@@ -623,8 +623,11 @@ class _LinearTCFn(torch.autograd.Function):
         x, w, y = ctx.saved_tensors
         g = g.contiguous()
         if ctx.relu_out:
-            g = torch.where(y > 0, g, torch.zeros((), dtype=g.dtype, device=g.device))
-        gx = g @ w.t() if ctx.needs_input_grad[0] else None
+            g = D.relu_grad(y, g)
+        gx = None
+        if ctx.needs_input_grad[0]:
+            # dx = g W^T: W is already the [K, N] "B transposed" operand of hg_gemm_tc
+            gx = D.gemm_tc(g, w) if w.shape[0] % 16 == 0 else g @ w.t()
         return gx, x.t() @ g, D.col_sums(g), None
 
 
@@ -669,11 +672,14 @@ class GINLayer:
     def params(self):
         return [self.one_plus_eps] + self.phi1.params() + self.phi2.params()
 
-    def __call__(self, bundle, x, mode, width, overflow, tag):
+    fuses_relu_out = True
+
+    def __call__(self, bundle, x, mode, width, overflow, tag, relu_out=False):
         agg = spmm_agg(bundle, x, self.reduction, width, overflow, tag)
         mixed = scale_combine(x, agg, self.one_plus_eps.publish(mode), self.lam)
         tc = getattr(bundle, "fused_bias_agg", False)
-        return self.phi2(self.phi1(mixed, mode, tc=tc, relu_out=True), mode, tc=tc)
+        return self.phi2(self.phi1(mixed, mode, tc=tc, relu_out=True), mode, tc=tc,
+                         relu_out=relu_out)
 
 
 class GATLayer:
@@ -808,8 +814,13 @@ class Model:
     def forward(self, bundle, x, mode, width="half2", overflow=None):
         h = x
         for i, layer in enumerate(self.layers):
+            inner = i + 1 < len(self.layers)
+            if inner and getattr(layer, "fuses_relu_out", False):
+                # the layer applies the inter-layer ReLU in its own epilogue
+                h = layer(bundle, h, mode, width, overflow, f"{self.kind}{i}", relu_out=True)
+                continue
             h = layer(bundle, h, mode, width, overflow, f"{self.kind}{i}")
-            if i + 1 < len(self.layers):
+            if inner:
                 h = relu(h)
         return h
 

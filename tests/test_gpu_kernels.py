@@ -791,3 +791,14 @@ def test_scale_combine_bits(cuda, count):
     assert abs(float(gope.cpu()) - want) <= 2.0 ** -10 * abs(want) + 1e-3
     _, _, only = D.scale_combine_bwd(_t(x, cuda), _t(g, cuda), _t(ope, cuda), lam, False, False)
     assert torch.equal(only, gope)
+
+
+def test_relu_grad(cuda):
+    from paper_2411_01109_b200 import device as D
+
+    rng = np.random.default_rng(1)
+    pre = rng.normal(0, 1, 4099).astype(np.float16)
+    y = np.maximum(pre, 0).astype(np.float16)
+    g = rng.normal(0, 1, 4099).astype(np.float16)
+    got = D.relu_grad(_t(y, cuda), _t(g, cuda)).cpu().numpy()
+    np.testing.assert_array_equal(bits(got), bits(np.where(pre > 0, g, np.float16(0))))
