@@ -656,6 +656,10 @@ def gemm_tc(a, bt, bias=None, row_scale=None, out=None, relu=False):
     if a.dtype != torch.float16 or bt.dtype != torch.float16:
         raise ValueError("hg_gemm_tc takes binary16 operands")
     a, bt = a.contiguous(), bt.contiguous()
+    if a.data_ptr() % 16:
+        a = a.clone()
+    if bt.data_ptr() % 16:
+        bt = bt.clone()
     m, k = a.shape
     n, k2 = bt.shape
     if k2 != k:

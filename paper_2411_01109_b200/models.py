@@ -533,12 +533,14 @@ class ParamGroup:
         dev = self.params[0].master.device
         self.dtype = _DTYPES[mode]
         sizes = [p.master.numel() for p in self.params]
-        total = sum(sizes)
-        self.master = torch.empty(total, dtype=torch.float32, device=dev)
+        offs = _offsets(self.params)
+        total = offs[-1] + sizes[-1] if sizes else 0
+        # parameters start on 8-element boundaries (16-byte aligned fp16 views for
+        # the vectorised / TMA kernels); the gaps stay zero and take no updates
+        self.master = torch.zeros(total, dtype=torch.float32, device=dev)
         self.pub = torch.empty(total, dtype=self.dtype, device=dev)
         self.grad = torch.zeros(total, dtype=self.dtype, device=dev)
-        off = 0
-        for p, sz in zip(self.params, sizes):
+        for p, sz, off in zip(self.params, sizes, offs):
             shape = p.master.shape
             self.master[off:off + sz].copy_(p.master.reshape(-1))
             p.master = self.master[off:off + sz].view(shape)
@@ -547,7 +549,6 @@ class ParamGroup:
             leaf.grad = self.grad[off:off + sz].view(shape)
             p.published = leaf
             p.group = self
-            off += sz
         self._ptrs = [p.published.grad.data_ptr() for p in self.params]
 
     @torch.no_grad()
@@ -906,10 +907,11 @@ class Adam:
 
 
 def _offsets(params):
+    """Start of each parameter in a ParamGroup's flat buffers (8-element aligned)."""
     out, o = [], 0
     for p in params:
         out.append(o)
-        o += p.master.numel()
+        o += (p.master.numel() + 7) // 8 * 8
     return out
 
 
