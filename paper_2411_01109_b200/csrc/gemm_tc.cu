@@ -288,17 +288,24 @@ static EncodeTiledFn encode_tiled() {
 }
 
 // 2-D fp16 tensor [rows, cols] with row pitch ld (elements), box {64 cols, box_rows}.
+static int g_tma_err = 0;
 static bool make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld,
                      uint32_t box_rows) {
   EncodeTiledFn fn = encode_tiled();
-  if (!fn) return false;
+  if (!fn) {
+    g_tma_err = -1;
+    return false;
+  }
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
   cuuint32_t box[2] = {(cuuint32_t)kTcBK, box_rows};
   cuuint32_t estr[2] = {1, 1};
-  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
-            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptr), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  g_tma_err = (int)r;
+  return r == CUDA_SUCCESS;
 }
 
 template <int N>
@@ -336,9 +343,18 @@ extern "C" int hg_gemm_tc(const void* a, int64_t m, int64_t k, int64_t lda, cons
                reinterpret_cast<uintptr_t>(out)) & 15) == 0,
              "hg_gemm_tc: operands must be 16-byte aligned");
   if (m == 0) return HG_OK;
+  // the tensor-map encoder is a driver call: bind the runtime's primary context
+  // to this thread first (autograd runs backward on its own worker threads)
+  int dev = 0;
+  HG_CUDA(cudaGetDevice(&dev));
+  HG_CUDA(cudaSetDevice(dev));
   CUtensorMap ma, mb;
-  HG_REQUIRE(make_map(&ma, a, m, k, lda, kTcBM) && make_map(&mb, bt, n, k, ldb, (uint32_t)n),
-             "hg_gemm_tc: cuTensorMapEncodeTiled failed");
+  HG_REQUIRE(make_map(&ma, a, m, k, lda, kTcBM),
+             "hg_gemm_tc: cuTensorMapEncodeTiled(A [%lld x %lld], pitch %lld, ptr %p) failed: %d",
+             (long long)m, (long long)k, (long long)lda, a, g_tma_err);
+  HG_REQUIRE(make_map(&mb, bt, n, k, ldb, (uint32_t)n),
+             "hg_gemm_tc: cuTensorMapEncodeTiled(Bt [%d x %lld], pitch %lld, ptr %p) failed: %d",
+             n, (long long)k, (long long)ldb, bt, g_tma_err);
   cudaStream_t st = as_stream(stream);
   switch (n) {
 #define HG_TC(NN) case NN: return launch_gemm_tc<NN>(ma, mb, m, k, bias, row_scale, out, ldo, relu, st);

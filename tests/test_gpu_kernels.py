@@ -802,3 +802,19 @@ def test_relu_grad(cuda):
     g = rng.normal(0, 1, 4099).astype(np.float16)
     got = D.relu_grad(_t(y, cuda), _t(g, cuda)).cpu().numpy()
     np.testing.assert_array_equal(bits(got), bits(np.where(pre > 0, g, np.float16(0))))
+
+
+def test_gemm_tc_from_autograd_worker_thread(cuda):
+    """hg_gemm_tc encodes its TMA descriptors through the driver API; it must
+    work from autograd's backward worker thread (no context bound there)."""
+    from paper_2411_01109_b200 import models as M
+
+    x = torch.randn(3000, 64, device=cuda, dtype=torch.float16, requires_grad=True)
+    w = (torch.randn(64, 48, device=cuda, dtype=torch.float16) * 0.1).requires_grad_(True)
+    b = torch.zeros(48, device=cuda, dtype=torch.float16, requires_grad=True)
+    y = M._LinearTCFn.apply(x, w, b, True)
+    y.float().sum().backward()
+    ref = torch.relu(x.detach().float() @ w.detach().float() + b.detach().float())
+    assert torch.allclose(y.float(), ref, atol=2e-2, rtol=1e-2)
+    g = (ref > 0).float()
+    assert torch.allclose(x.grad.float(), g @ w.detach().float().t(), atol=2e-2, rtol=1e-2)
