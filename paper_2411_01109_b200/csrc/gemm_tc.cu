@@ -119,8 +119,12 @@ template <int N>
 struct TcCfg {
   static constexpr uint32_t kABytes = kTcBM * kTcBK * 2;
   static constexpr uint32_t kBBytes = N * kTcBK * 2;
-  static constexpr uint32_t kPitch = N * 2 + 16;  // staging row pitch (bytes)
-  static constexpr uint32_t kStage = kTcBM * kPitch;
+  // N % 64 == 0: two 128-byte-swizzled staging tiles written back by TMA
+  // stores (double-buffered); otherwise one padded tile + coalesced stores
+  static constexpr bool kTmaStore = N % 64 == 0;
+  static constexpr uint32_t kPitch = N * 2 + 16;  // padded staging row pitch (bytes)
+  static constexpr uint32_t kBufs = (kTmaStore && N <= 128) ? 2 : 1;
+  static constexpr uint32_t kStage = kTmaStore ? kBufs * kTcBM * N * 2 : kTcBM * kPitch;
   static constexpr int kStages0 = (int)((200u * 1024u - kStage) / (kABytes + kBBytes));
   static constexpr int kStages = kStages0 > 8 ? 8 : kStages0;
   static constexpr uint32_t kCols = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 2 * N <= 128 ? 128 : 2 * N <= 256 ? 256 : 512;
@@ -133,10 +137,17 @@ struct TcCfg {
 // warps 2-5 = epilogue.  Two TMEM accumulators: the epilogue of tile i
 // overlaps the MMAs of tile i+1.  The epilogue stages the fp16 tile in shared
 // memory and writes it back with coalesced 16-byte stores.
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+
 template <int N>
 __global__ void __launch_bounds__(192, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-          int64_t m, int num_kb, const __half* __restrict__ bias,
+          const __grid_constant__ CUtensorMap map_o, int64_t m, int num_kb, const __half* __restrict__ bias,
           const __half* __restrict__ row_scale, __half* __restrict__ out, int64_t ldo, int relu) {
   using C = TcCfg<N>;
   constexpr int S = C::kStages;
@@ -232,7 +243,16 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
       const __half sv = (live && row_scale) ? row_scale[row] : __float2half_rn(1.0f);
       mbar_wait(&tfull[a], (tc >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      unsigned char* srow = stage + r * C::kPitch;
+      unsigned char* sbuf = stage + (C::kTmaStore ? (tc % C::kBufs) * (kTcBM * N * 2) : 0);
+      if constexpr (C::kTmaStore) {
+        // the TMA store issued from this buffer kBufs tiles ago has read it
+        if (et == 0) {
+          if constexpr (C::kBufs == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+        epi_bar();
+      }
+      unsigned char* srow = sbuf + r * (C::kTmaStore ? 128 : C::kPitch);
 #pragma unroll
       for (int c0 = 0; c0 < N; c0 += 16) {
         uint32_t v[16];
@@ -247,22 +267,44 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
           if (relu && !(__hgt(t, __float2half_rn(0.0f)))) t = __float2half_rn(0.0f);
           h[j] = t;
         }
-        reinterpret_cast<uint4*>(srow + c0 * 2)[0] = *reinterpret_cast<const uint4*>(&h[0]);
-        reinterpret_cast<uint4*>(srow + c0 * 2)[1] = *reinterpret_cast<const uint4*>(&h[8]);
+        if constexpr (C::kTmaStore) {
+          // 64-column boxes of 128 rows x 128 B, 16-byte chunk c of row r at c ^ (r & 7)
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int c = c0 / 8 + hh;
+            unsigned char* dst = sbuf + (c / 8) * (kTcBM * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4);
+            *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(&h[8 * hh]);
+          }
+        } else {
+          reinterpret_cast<uint4*>(srow + c0 * 2)[0] = *reinterpret_cast<const uint4*>(&h[0]);
+          reinterpret_cast<uint4*>(srow + c0 * 2)[1] = *reinterpret_cast<const uint4*>(&h[8]);
+        }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&tempty[a]);  // accumulator drained: the MMA warp may reuse it
-      epi_bar();
-      // coalesced write-back of the live rows: 16-byte chunks, row-major
-      const int rows = (int)((m - m0) < kTcBM ? (m - m0) : kTcBM);
-      constexpr int CPR = N / 8;
-      for (int ch = et; ch < rows * CPR; ch += 128) {
-        const int rr = ch / CPR, c8 = ch - rr * CPR;
-        *reinterpret_cast<uint4*>(out + (m0 + rr) * ldo + c8 * 8) =
-            *reinterpret_cast<const uint4*>(stage + rr * C::kPitch + c8 * 16);
+      if constexpr (C::kTmaStore) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> TMA
+        epi_bar();
+        if (et == 0) {
+#pragma unroll
+          for (int bx = 0; bx < N / 64; ++bx)
+            tma_store_2d(&map_o, sbuf + bx * (kTcBM * 128), bx * 64, (int)m0);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      } else {
+        epi_bar();
+        // coalesced write-back of the live rows: 16-byte chunks, row-major
+        const int rows = (int)((m - m0) < kTcBM ? (m - m0) : kTcBM);
+        constexpr int CPR = N / 8;
+        for (int ch = et; ch < rows * CPR; ch += 128) {
+          const int rr = ch / CPR, c8 = ch - rr * CPR;
+          *reinterpret_cast<uint4*>(out + (m0 + rr) * ldo + c8 * 8) =
+              *reinterpret_cast<const uint4*>(sbuf + rr * C::kPitch + c8 * 16);
+        }
+        epi_bar();
       }
-      epi_bar();
     }
+    if (C::kTmaStore && et == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -309,7 +351,8 @@ static bool make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t co
 }
 
 template <int N>
-static int launch_gemm_tc(const CUtensorMap& ma, const CUtensorMap& mb, int64_t m, int64_t k,
+static int launch_gemm_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
+                          int64_t m, int64_t k,
                           const void* bias, const void* row_scale, void* out, int64_t ldo,
                           int relu, cudaStream_t st) {
   constexpr size_t smem = TcCfg<N>::kSmem;
@@ -323,7 +366,7 @@ static int launch_gemm_tc(const CUtensorMap& ma, const CUtensorMap& mb, int64_t 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const unsigned grid = (unsigned)(tiles < sms ? tiles : sms);
   k_gemm_tc<N><<<grid, 192, smem, st>>>(
-      ma, mb, m, num_kb, (const __half*)bias, (const __half*)row_scale, (__half*)out, ldo, relu);
+      ma, mb, mo, m, num_kb, (const __half*)bias, (const __half*)row_scale, (__half*)out, ldo, relu);
   HG_LAUNCHED();
   return HG_OK;
 }
@@ -355,9 +398,14 @@ extern "C" int hg_gemm_tc(const void* a, int64_t m, int64_t k, int64_t lda, cons
   HG_REQUIRE(make_map(&mb, bt, n, k, ldb, (uint32_t)n),
              "hg_gemm_tc: cuTensorMapEncodeTiled(Bt [%d x %lld], pitch %lld, ptr %p) failed: %d",
              n, (long long)k, (long long)ldb, bt, g_tma_err);
+  CUtensorMap mo = ma;  // TMA-store epilogue (N % 64 == 0): 64-column boxes of the output
+  if (n % 64 == 0)
+    HG_REQUIRE(make_map(&mo, out, m, n, ldo, kTcBM),
+               "hg_gemm_tc: cuTensorMapEncodeTiled(out [%lld x %d], pitch %lld) failed: %d",
+               (long long)m, n, (long long)ldo, g_tma_err);
   cudaStream_t st = as_stream(stream);
   switch (n) {
-#define HG_TC(NN) case NN: return launch_gemm_tc<NN>(ma, mb, m, k, bias, row_scale, out, ldo, relu, st);
+#define HG_TC(NN) case NN: return launch_gemm_tc<NN>(ma, mb, mo, m, k, bias, row_scale, out, ldo, relu, st);
     HG_TC(16) HG_TC(32) HG_TC(48) HG_TC(64) HG_TC(80) HG_TC(96) HG_TC(112) HG_TC(128)
     HG_TC(144) HG_TC(160) HG_TC(176) HG_TC(192) HG_TC(208) HG_TC(224) HG_TC(240) HG_TC(256)
 #undef HG_TC
