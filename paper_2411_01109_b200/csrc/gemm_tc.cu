@@ -115,21 +115,26 @@ __device__ __forceinline__ void epi_bar() {  // named barrier over the 4 epilogu
 }
 
 // smem ring depth for a given N (the ring plus the output staging tile fit ~200 KB)
-template <int N>
+template <int N, bool RESB>
 struct TcCfg {
   static constexpr uint32_t kABytes = kTcBM * kTcBK * 2;
   static constexpr uint32_t kBBytes = N * kTcBK * 2;
+  // RESB: all of Bt (<= kMaxResKb slabs) stays resident in shared memory for
+  // the CTA's lifetime; the ring then streams A only
+  static constexpr int kMaxResKb = RESB ? (int)((96u * 1024u) / kBBytes) : 0;
+  static constexpr uint32_t kRes = (uint32_t)kMaxResKb * kBBytes;
+  static constexpr uint32_t kSlot = kABytes + (RESB ? 0 : kBBytes);  // ring bytes per stage
   // N % 64 == 0: two 128-byte-swizzled staging tiles written back by TMA
   // stores (double-buffered); otherwise one padded tile + coalesced stores
   static constexpr bool kTmaStore = N % 64 == 0;
   static constexpr uint32_t kPitch = N * 2 + 16;  // padded staging row pitch (bytes)
   static constexpr uint32_t kBufs = (kTmaStore && N <= 128) ? 2 : 1;
   static constexpr uint32_t kStage = kTmaStore ? kBufs * kTcBM * N * 2 : kTcBM * kPitch;
-  static constexpr int kStages0 = (int)((200u * 1024u - kStage) / (kABytes + kBBytes));
+  static constexpr int kStages0 = (int)((200u * 1024u - kStage - kRes) / kSlot);
   static constexpr int kStages = kStages0 > 8 ? 8 : kStages0;
   static constexpr uint32_t kCols = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 2 * N <= 128 ? 128 : 2 * N <= 256 ? 256 : 512;
-  static constexpr size_t kSmem = 1024 + (size_t)kStages * (kABytes + kBBytes) + kStage +
-                                  (2 * kStages + 4) * 8 + 16;
+  static constexpr size_t kSmem = 1024 + (size_t)kStages * kSlot + kRes + kStage +
+                                  (2 * kStages + 5) * 8 + 16;
 };
 
 // Persistent: one CTA per SM loops over 128-row tiles.  Warp 0 = TMA producer
@@ -144,12 +149,12 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
                : "memory");
 }
 
-template <int N>
+template <int N, bool RESB>
 __global__ void __launch_bounds__(192, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
           const __grid_constant__ CUtensorMap map_o, int64_t m, int num_kb, const __half* __restrict__ bias,
           const __half* __restrict__ row_scale, __half* __restrict__ out, int64_t ldo, int relu) {
-  using C = TcCfg<N>;
+  using C = TcCfg<N, RESB>;
   constexpr int S = C::kStages;
   // instruction descriptor: f16 x f16 -> f32, both K-major, M = 128, N
   constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kTcBM >> 4) << 24);
@@ -158,13 +163,14 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
   unsigned char* base = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* sa = base;                          // [S][128 x 128 B]
-  unsigned char* sb = base + S * C::kABytes;         // [S][N x 128 B]
-  unsigned char* stage = sb + S * C::kBBytes;        // [128][pitch] output tile
+  unsigned char* sb = base + S * C::kABytes;         // ring: [S][N x 128 B]; RESB: [kb][N x 128 B]
+  unsigned char* stage = sb + (RESB ? C::kRes : S * C::kBBytes);  // output staging
   uint64_t* full = reinterpret_cast<uint64_t*>(stage + C::kStage);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;                       // [2]
   uint64_t* tempty = tfull + 2;                      // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* bfull = tempty + 2;                      // resident B landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t num_tiles = (m + kTcBM - 1) / kTcBM;
@@ -178,6 +184,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 128);
     }
+    mbar_init(bfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
@@ -195,20 +202,26 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
 
   if (warp == 0) {
     if (lane == 0) {  // TMA producer
+      if (RESB) {
+        mbar_expect_tx(bfull, (uint32_t)num_kb * C::kBBytes);
+        for (int kb = 0; kb < num_kb; ++kb)
+          tma_load_2d(sb + kb * C::kBBytes, &map_b, bfull, kb * kTcBK, 0);
+      }
       uint32_t it = 0;
       for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         for (int kb = 0; kb < num_kb; ++kb, ++it) {
           const int s = it % S;
           mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
-          mbar_expect_tx(&full[s], C::kABytes + C::kBBytes);
+          mbar_expect_tx(&full[s], RESB ? C::kABytes : C::kABytes + C::kBBytes);
           tma_load_2d(sa + s * C::kABytes, &map_a, &full[s], kb * kTcBK, (int)(tile * kTcBM));
-          tma_load_2d(sb + s * C::kBBytes, &map_b, &full[s], kb * kTcBK, 0);
+          if (!RESB) tma_load_2d(sb + s * C::kBBytes, &map_b, &full[s], kb * kTcBK, 0);
         }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
+      if (RESB) mbar_wait(bfull, 0);
       uint32_t it = 0, tc = 0;
       for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tc) {
         const uint32_t a = tc & 1;
@@ -220,7 +233,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
           mbar_wait(&full[s], (it / S) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint64_t da = sw128_kmajor_desc(sa + s * C::kABytes);
-          const uint64_t db = sw128_kmajor_desc(sb + s * C::kBBytes);
+          const uint64_t db = sw128_kmajor_desc(sb + (RESB ? kb : s) * C::kBBytes);
 #pragma unroll
           for (int k = 0; k < kTcBK / 16; ++k)  // 16 fp16 = 32 B steps inside the swizzle row
             umma_f16_f32(acc, da + 2 * k, db + 2 * k, kIdesc, (kb | k) != 0);
@@ -350,25 +363,34 @@ static bool make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t co
   return r == CUDA_SUCCESS;
 }
 
-template <int N>
-static int launch_gemm_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
-                          int64_t m, int64_t k,
-                          const void* bias, const void* row_scale, void* out, int64_t ldo,
-                          int relu, cudaStream_t st) {
-  constexpr size_t smem = TcCfg<N>::kSmem;
+template <int N, bool RESB>
+static int launch_gemm_tc_v(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
+                            int64_t m, int num_kb, const void* bias, const void* row_scale,
+                            void* out, int64_t ldo, int relu, cudaStream_t st) {
+  constexpr size_t smem = TcCfg<N, RESB>::kSmem;
   static_assert(smem <= 227 * 1024, "gemm_tc shared memory budget");
-  HG_CUDA(cudaFuncSetAttribute(k_gemm_tc<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int num_kb = (int)((k + kTcBK - 1) / kTcBK);
+  static_assert(TcCfg<N, RESB>::kStages >= 2, "gemm_tc ring too shallow");
+  HG_CUDA(cudaFuncSetAttribute(k_gemm_tc<N, RESB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t tiles = (m + kTcBM - 1) / kTcBM;
   int sms = 148;
   int dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const unsigned grid = (unsigned)(tiles < sms ? tiles : sms);
-  k_gemm_tc<N><<<grid, 192, smem, st>>>(
+  k_gemm_tc<N, RESB><<<grid, 192, smem, st>>>(
       ma, mb, mo, m, num_kb, (const __half*)bias, (const __half*)row_scale, (__half*)out, ldo, relu);
   HG_LAUNCHED();
   return HG_OK;
+}
+
+template <int N>
+static int launch_gemm_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
+                          int64_t m, int64_t k, const void* bias, const void* row_scale, void* out,
+                          int64_t ldo, int relu, cudaStream_t st) {
+  const int num_kb = (int)((k + kTcBK - 1) / kTcBK);
+  if (num_kb <= TcCfg<N, true>::kMaxResKb)
+    return launch_gemm_tc_v<N, true>(ma, mb, mo, m, num_kb, bias, row_scale, out, ldo, relu, st);
+  return launch_gemm_tc_v<N, false>(ma, mb, mo, m, num_kb, bias, row_scale, out, ldo, relu, st);
 }
 
 }  // namespace hg
