@@ -121,7 +121,7 @@ struct TcCfg {
   static constexpr uint32_t kBBytes = N * kTcBK * 2;
   // RESB: all of Bt (<= kMaxResKb slabs) stays resident in shared memory for
   // the CTA's lifetime; the ring then streams A only
-  static constexpr int kMaxResKb = RESB ? (int)((96u * 1024u) / kBBytes) : 0;
+  static constexpr int kMaxResKb = RESB ? (int)((32u * 1024u) / kBBytes) : 0;
   static constexpr uint32_t kRes = (uint32_t)kMaxResKb * kBBytes;
   static constexpr uint32_t kSlot = kABytes + (RESB ? 0 : kBBytes);  // ring bytes per stage
   // N % 64 == 0: two 128-byte-swizzled staging tiles written back by TMA
@@ -266,11 +266,19 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
         epi_bar();
       }
       unsigned char* srow = sbuf + r * (C::kTmaStore ? 128 : C::kPitch);
+      // TMEM loads batched 32 columns per wait (two x16 loads in flight)
+      constexpr int kLdB = N % 32 == 0 ? 32 : 16;
 #pragma unroll
-      for (int c0 = 0; c0 < N; c0 += 16) {
-        uint32_t v[16];
-        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + a * N + c0, v);
+      for (int cb = 0; cb < N; cb += kLdB) {
+        uint32_t vv[kLdB];
+#pragma unroll
+        for (int u = 0; u < kLdB / 16; ++u)
+          tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + a * N + cb + 16 * u,
+                    *reinterpret_cast<uint32_t(*)[16]>(&vv[16 * u]));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int c0 = cb; c0 < cb + kLdB; c0 += 16) {
+        const uint32_t* v = &vv[c0 - cb];
         __align__(16) __half h[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
@@ -292,6 +300,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
           reinterpret_cast<uint4*>(srow + c0 * 2)[0] = *reinterpret_cast<const uint4*>(&h[0]);
           reinterpret_cast<uint4*>(srow + c0 * 2)[1] = *reinterpret_cast<const uint4*>(&h[8]);
         }
+      }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&tempty[a]);  // accumulator drained: the MMA warp may reuse it
