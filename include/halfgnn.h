@@ -334,6 +334,11 @@ int hg_scale_combine_bwd(const void* x, const void* g, const void* one_plus_eps,
                          int64_t count, void* gx, void* ga, void* gope, int dtype, void* ws,
                          size_t ws_bytes, void* stream);
 
+/* dst[i, :] = src[idx[i], :] for rows of row_bytes bytes (e.g. per-edge values
+ * [E, H] re-ordered into CSC order through perm, w[perm] of models.py:309). */
+int hg_gather_rows(const void* src, const int32_t* idx, int64_t rows, int32_t row_bytes,
+                   void* dst, void* stream);
+
 /* relu backward (models.py:176-185) from the ReLU output y: out = y > 0 ? g : 0. */
 int hg_relu_grad(const void* y, const void* g, int64_t count, void* out, int dtype, void* stream);
 

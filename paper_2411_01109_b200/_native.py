@@ -74,6 +74,7 @@ SIGNATURES = {
     "hg_scale_combine_bwd_workspace": [_PSZ],
     "hg_scale_combine_bwd": [_P, _P, _P, c_double, _I64, _P, _P, _P, c_int, _P, c_size_t, _P],
     "hg_relu_grad": [_P, _P, _I64, _P, c_int, _P],
+    "hg_gather_rows": [_P, _P, _I64, _I32, _P, _P],
     "hg_bias_scale_rows": [_P, _P, _P, _I64, _I32, _P, c_int, _P],
     "hg_col_sums_workspace": [_I64, _I32, _PSZ],
     "hg_col_sums": [_P, _I64, _I32, _P, c_int, _P, c_size_t, _P],

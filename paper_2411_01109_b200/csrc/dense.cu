@@ -362,6 +362,45 @@ extern "C" int hg_relu_grad(const void* y, const void* g, int64_t count, void* o
   return HG_OK;
 }
 
+namespace hg {
+// dst[i, :] = src[idx[i], :] for rows of `width` bytes (a multiple of 4).
+template <typename W>
+__global__ void k_gather_rows_bytes(const W* __restrict__ src, const int32_t* __restrict__ idx,
+                                    int64_t rows, int wpr, W* __restrict__ dst) {
+  const int64_t total = rows * (int64_t)wpr;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / wpr;
+    const int c = (int)(i - r * wpr);
+    dst[i] = src[(int64_t)__ldg(idx + r) * wpr + c];
+  }
+}
+}  // namespace hg
+
+extern "C" int hg_gather_rows(const void* src, const int32_t* idx, int64_t rows,
+                              int32_t row_bytes, void* dst, void* stream) {
+  HG_REQUIRE(rows >= 0 && row_bytes > 0 && row_bytes % 2 == 0, "hg_gather_rows: bad shape");
+  if (rows == 0) return HG_OK;
+  cudaStream_t st = as_stream(stream);
+  const bool a8 = row_bytes % 8 == 0 && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 7) == 0;
+  const bool a4 = row_bytes % 4 == 0 && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 3) == 0;
+  if (a8) {
+    const int wpr = row_bytes / 8;
+    k_gather_rows_bytes<uint2><<<grid_for(rows * wpr, 256, 148 * 32), 256, 0, st>>>(
+        (const uint2*)src, idx, rows, wpr, (uint2*)dst);
+  } else if (a4) {
+    const int wpr = row_bytes / 4;
+    k_gather_rows_bytes<uint32_t><<<grid_for(rows * wpr, 256, 148 * 32), 256, 0, st>>>(
+        (const uint32_t*)src, idx, rows, wpr, (uint32_t*)dst);
+  } else {
+    const int wpr = row_bytes / 2;
+    k_gather_rows_bytes<uint16_t><<<grid_for(rows * wpr, 256, 148 * 32), 256, 0, st>>>(
+        (const uint16_t*)src, idx, rows, wpr, (uint16_t*)dst);
+  }
+  HG_LAUNCHED();
+  return HG_OK;
+}
+
 extern "C" int hg_bias_scale_rows(const void* x, const void* bias, const void* row_scale,
                                   int64_t rows, int32_t F, void* out, int dtype, void* stream) {
   HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);

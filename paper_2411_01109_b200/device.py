@@ -718,6 +718,18 @@ def scale_combine_bwd(x, g, one_plus_eps, lam, need_gx=True, need_ga=True, need_
     return gx, ga, gope
 
 
+def gather_rows(src, idx):
+    """src[idx] along dim 0 (int32 idx), one pass (hg_gather_rows)."""
+    src = src.contiguous()
+    rows = idx.numel()
+    out = torch.empty((rows,) + tuple(src.shape[1:]), dtype=src.dtype, device=src.device)
+    row_bytes = src[0].numel() * src.element_size() if src.shape[0] else 0
+    if rows and row_bytes:
+        nat.call("hg_gather_rows", _p(src), _p(idx), rows, row_bytes, _p(out), _stream())
+        Probe.launches += 1
+    return out
+
+
 def relu_grad(y, g):
     """g where y > 0 else 0 (y = the ReLU's output), one pass (hg_relu_grad)."""
     y, g = y.contiguous(), g.contiguous()

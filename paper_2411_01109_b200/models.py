@@ -303,7 +303,13 @@ class _WeightedFn(torch.autograd.Function):
         if ctx.needs_input_grad[0]:
             gw = b.sddmm(g, x, heads=h).reshape(w.shape)
         if ctx.needs_input_grad[1]:
-            gx = b.spmm(g, w, "post", "none", transpose=True, heads=h, weight_via_perm=True)
+            if getattr(b, "numerics", None) == "fast":
+                # w re-ordered into CSC order once (one gather pass), so the
+                # transposed SpMM reads its weights contiguously
+                wt = D.gather_rows(w, b.dg.perm)
+                gx = b.spmm(g, wt, "post", "none", transpose=True, heads=h)
+            else:
+                gx = b.spmm(g, w, "post", "none", transpose=True, heads=h, weight_via_perm=True)
         return gw, gx, None, None
 
 

@@ -818,3 +818,14 @@ def test_gemm_tc_from_autograd_worker_thread(cuda):
     assert torch.allclose(y.float(), ref, atol=2e-2, rtol=1e-2)
     g = (ref > 0).float()
     assert torch.allclose(x.grad.float(), g @ w.detach().float().t(), atol=2e-2, rtol=1e-2)
+
+
+@pytest.mark.parametrize("shape", [(1000,), (1000, 4), (999, 3), (500, 8)])
+def test_gather_rows(cuda, shape):
+    from paper_2411_01109_b200 import device as D
+
+    rng = np.random.default_rng(len(shape))
+    src = rng.normal(0, 1, shape).astype(np.float16)
+    idx = rng.permutation(shape[0]).astype(np.int32)
+    got = D.gather_rows(_t(src, cuda), _t(idx, cuda)).cpu().numpy()
+    np.testing.assert_array_equal(bits(got), bits(src[idx]))
