@@ -303,7 +303,7 @@ class _WeightedFn(torch.autograd.Function):
         if ctx.needs_input_grad[0]:
             gw = b.sddmm(g, x, heads=h).reshape(w.shape)
         if ctx.needs_input_grad[1]:
-            if getattr(b, "numerics", None) == "fast":
+            if isinstance(b, GraphBundle) and b.numerics == "fast":
                 # w re-ordered into CSC order once (one gather pass), so the
                 # transposed SpMM reads its weights contiguously
                 wt = D.gather_rows(w, b.dg.perm)
