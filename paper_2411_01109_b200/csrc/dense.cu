@@ -363,16 +363,35 @@ extern "C" int hg_relu_grad(const void* y, const void* g, int64_t count, void* o
 }
 
 namespace hg {
-// dst[i, :] = src[idx[i], :] for rows of `width` bytes (a multiple of 4).
+// dst[i, :] = src[idx[i], :] in words W (wpr words per row).  Each thread keeps
+// 8 independent gathers in flight (the idx -> src chain is latency-bound).
 template <typename W>
-__global__ void k_gather_rows_bytes(const W* __restrict__ src, const int32_t* __restrict__ idx,
-                                    int64_t rows, int wpr, W* __restrict__ dst) {
+__global__ void __launch_bounds__(256)
+k_gather_rows_bytes(const W* __restrict__ src, const int32_t* __restrict__ idx, int64_t rows,
+                    int wpr, W* __restrict__ dst) {
+  constexpr int U = 8;
   const int64_t total = rows * (int64_t)wpr;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / wpr;
-    const int c = (int)(i - r * wpr);
-    dst[i] = src[(int64_t)__ldg(idx + r) * wpr + c];
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x * U; base < total;
+       base += (int64_t)gridDim.x * blockDim.x * U) {
+    int64_t pos[U];
+    W v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + (int64_t)u * blockDim.x + threadIdx.x;
+      pos[u] = -1;
+      if (i < total) {
+        const int64_t r = i / wpr;
+        pos[u] = (int64_t)__ldg(idx + r) * wpr + (i - r * wpr);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (pos[u] >= 0) v[u] = __ldg(src + pos[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + (int64_t)u * blockDim.x + threadIdx.x;
+      if (i < total) dst[i] = v[u];
+    }
   }
 }
 }  // namespace hg
@@ -386,15 +405,15 @@ extern "C" int hg_gather_rows(const void* src, const int32_t* idx, int64_t rows,
   const bool a4 = row_bytes % 4 == 0 && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 3) == 0;
   if (a8) {
     const int wpr = row_bytes / 8;
-    k_gather_rows_bytes<uint2><<<grid_for(rows * wpr, 256, 148 * 32), 256, 0, st>>>(
+    k_gather_rows_bytes<uint2><<<grid_for(rows * wpr, 256 * 8, 148 * 16), 256, 0, st>>>(
         (const uint2*)src, idx, rows, wpr, (uint2*)dst);
   } else if (a4) {
     const int wpr = row_bytes / 4;
-    k_gather_rows_bytes<uint32_t><<<grid_for(rows * wpr, 256, 148 * 32), 256, 0, st>>>(
+    k_gather_rows_bytes<uint32_t><<<grid_for(rows * wpr, 256 * 8, 148 * 16), 256, 0, st>>>(
         (const uint32_t*)src, idx, rows, wpr, (uint32_t*)dst);
   } else {
     const int wpr = row_bytes / 2;
-    k_gather_rows_bytes<uint16_t><<<grid_for(rows * wpr, 256, 148 * 32), 256, 0, st>>>(
+    k_gather_rows_bytes<uint16_t><<<grid_for(rows * wpr, 256 * 8, 148 * 16), 256, 0, st>>>(
         (const uint16_t*)src, idx, rows, wpr, (uint16_t*)dst);
   }
   HG_LAUNCHED();
