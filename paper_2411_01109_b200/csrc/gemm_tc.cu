@@ -409,7 +409,9 @@ using namespace hg;
 extern "C" int hg_gemm_tc(const void* a, int64_t m, int64_t k, int64_t lda, const void* bt,
                           int32_t n, int64_t ldb, const void* bias, const void* row_scale,
                           int32_t relu, void* out, int64_t ldo, void* stream) {
-  HG_REQUIRE(a && bt && out && m >= 0 && k > 0, "hg_gemm_tc: bad arguments");
+  HG_REQUIRE(m >= 0 && k > 0, "hg_gemm_tc: bad arguments");
+  if (m == 0) return HG_OK;
+  HG_REQUIRE(a && bt && out, "hg_gemm_tc: null operand");
   HG_REQUIRE(n >= 16 && n <= 256 && n % 16 == 0, "hg_gemm_tc: N=%d must be a multiple of 16 in [16, 256]", n);
   HG_REQUIRE(lda >= k && ldb >= k && ldo >= n && lda % 8 == 0 && ldb % 8 == 0 && ldo % 8 == 0,
              "hg_gemm_tc: row pitches must cover K / N and be multiples of 8 elements");
