@@ -285,7 +285,12 @@ extern "C" int hg_scale_combine_bwd(const void* x, const void* g, const void* on
                                     double lam, int64_t count, void* gx, void* ga, void* gope,
                                     int dtype, void* ws, size_t ws_bytes, void* stream) {
   HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
-  HG_REQUIRE(count >= 0 && one_plus_eps && g, "hg_scale_combine_bwd: bad arguments");
+  HG_REQUIRE(count >= 0 && one_plus_eps, "hg_scale_combine_bwd: bad arguments");
+  if (count == 0) {
+    if (gope) HG_CUDA(cudaMemsetAsync(gope, 0, dtype == HG_F16 ? 2 : 4, as_stream(stream)));
+    return HG_OK;
+  }
+  HG_REQUIRE(g, "hg_scale_combine_bwd: null gradient");
   HG_REQUIRE(!gope || (x && ws && ws_bytes >= (size_t)kCombBlocks * sizeof(double)),
              "hg_scale_combine_bwd: the (1+eps) gradient needs x and a workspace");
   cudaStream_t st = as_stream(stream);
