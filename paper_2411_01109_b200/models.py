@@ -159,6 +159,13 @@ class GraphBundle:
         """GCN layers may fuse add_bias into the aggregation's input pass."""
         return self.numerics == "fast"
 
+    def gcn_agg_tc(self, x, w, b, reduction):
+        """GCN layer forward: tcgen05 GEMM with bias + input scale fused, then
+        the gather SpMM."""
+        fin, fout = self.dg.norm_tables(reduction.norm, False, x.dtype)
+        xs = D.gemm_tc(x, w.t().contiguous(), b, fin)
+        return D.spmm_csr(self.dg.view(False), xs, None, None, 1, reduction.scaling, None, fout)
+
     def bias_spmm(self, h, b, scaling, norm):
         """spmm(add_bias(h, b)) with the bias add and the left-norm input
         scaling in one pass (hg_bias_scale_rows), then the gather kernel."""
@@ -266,9 +273,7 @@ class _GCNLayerFn(torch.autograd.Function):
     def forward(ctx, x, w, b, bundle, reduction):
         ctx.bundle, ctx.reduction = bundle, reduction
         ctx.save_for_backward(x, w)
-        fin, fout = bundle.dg.norm_tables(reduction.norm, False, x.dtype)
-        xs = D.gemm_tc(x, w.t().contiguous(), b, fin)
-        return D.spmm_csr(bundle.dg.view(False), xs, None, None, 1, reduction.scaling, None, fout)
+        return bundle.gcn_agg_tc(x, w, b, reduction)
 
     @staticmethod
     def backward(ctx, g):

@@ -176,6 +176,10 @@ class CudaOps:
         return D.softmax_bwd_view(view, alpha, g)
 
     @staticmethod
+    def row_scale(x, s):
+        return D.bias_scale_rows(x, None, s)
+
+    @staticmethod
     def xent(logits, labels, n_active, denom, scale=1.0, grad_dtype=None):
         return D.softmax_xent(logits, labels, n_active, denom, scale, grad_dtype)
 
@@ -239,9 +243,58 @@ class DistBundle:
             self._cache[key] = t
         return t
 
+    def local_in_scale(self, norm, transpose, dtype):
+        """The left-norm input scale of this rank's own rows (global table)."""
+        if norm not in ("left", "both"):
+            return None
+        key = ("fin_local", norm, transpose, dtype)
+        t = self._cache.get(key)
+        if t is None:
+            kind = "inv_sqrt" if norm == "both" else "inv"
+            side = "row" if transpose else "col"
+            t = self._tables(kind, side, dtype)[self.part.lo:self.part.hi].contiguous()
+            self._cache[key] = t
+        return t
+
+    @property
+    def fused_bias_agg(self):
+        """GCN layers run the tcgen05 GEMM + epilogue on local rows (CUDA ops only)."""
+        return self.ops is CudaOps
+
+    def _gather_scaled(self, xs, scaling, norm, transpose, heads=1, w=None, widx=None):
+        view = self.part.bwd if transpose else self.part.fwd
+        _, fout = self.norm_tables(norm, transpose, xs.dtype)
+        return self.ops.spmm(view, self.ex.gather_rows(xs.contiguous()), w, widx, heads,
+                             scaling, None, fout)
+
+    def bias_spmm(self, h, b, scaling, norm):
+        """spmm(add_bias(h, b)): bias and input scale applied to the local rows
+        before the all-gather (hg_bias_scale_rows), then the gathered SpMM."""
+        xs = D.bias_scale_rows(h, b, self.local_in_scale(norm, False, h.dtype))
+        return self._gather_scaled(xs, scaling, norm, False)
+
+    def gcn_agg_tc(self, x, w, b, reduction):
+        """GCN layer forward: tcgen05 GEMM + bias + input scale on the local rows,
+        all-gather of the scaled rows, SpMM over the local CSR rows."""
+        fin = self.local_in_scale(reduction.norm, False, x.dtype)
+        xs = D.gemm_tc(x, w.t().contiguous(), b, fin)
+        return self._gather_scaled(xs, reduction.scaling, reduction.norm, False)
+
     def spmm(self, x, w=None, scaling="post", norm="none", transpose=False, heads=1,
              weight_via_perm=False):
         view = self.part.bwd if transpose else self.part.fwd
+        fin_local = self.local_in_scale(norm, transpose, x.dtype)
+        row_scale = getattr(self.ops, "row_scale", None)
+        if fin_local is not None and row_scale is not None:
+            # X' = rnd(X * in_scale) on the local rows before the gather (the
+            # same elementwise rounding hg_spmm applies, done once per row
+            # instead of on every rank's gathered copy)
+            widx = None
+            if w is not None and weight_via_perm:
+                w = self.ex.gather_edges(w.contiguous())
+                widx = view.perm
+            return self._gather_scaled(row_scale(x.contiguous(), fin_local), scaling, norm,
+                                       transpose, heads, w, widx)
         x_full = self.ex.gather_rows(x.contiguous())
         fin, fout = self.norm_tables(norm, transpose, x.dtype)
         widx = None

@@ -121,6 +121,7 @@ HostOps.softmax_bwd = staticmethod(_host_softmax_bwd)
 HostOps.edge_sums = staticmethod(_host_edge_sums)
 HostOps.head_dots = staticmethod(_host_head_dots)
 HostOps.scale = staticmethod(lambda x, s: (x.double() * s).to(x.dtype))
+HostOps.row_scale = staticmethod(lambda x, s: (x.double() * s.double()[:, None]).to(x.dtype))
 
 
 def _free_port():
