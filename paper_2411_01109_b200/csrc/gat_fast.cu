@@ -179,11 +179,11 @@ __device__ __forceinline__ float sums_pass(const T* __restrict__ v, const int32_
 // ---------------------------------------------------------------- forward
 
 template <typename T, int H>
-__global__ void __launch_bounds__(256)
-k_gat_fwd_thread(const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
+__device__ __forceinline__ void
+d_gat_fwd_thread(int64_t blk, int64_t nblk, const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
                  int64_t n_rows, const T* __restrict__ sl, const T* __restrict__ sr, float slope,
                  T* __restrict__ alpha, int short_max) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t t = blk * (int64_t)blockDim.x + threadIdx.x;
   if (t >= n_rows * H) return;
   const int64_t r = t / H;
   const int h = (int)(t - r * H);
@@ -196,14 +196,14 @@ k_gat_fwd_thread(const int64_t* __restrict__ offsets, const int32_t* __restrict_
 }
 
 template <typename T, int H>
-__global__ void __launch_bounds__(256)
-k_gat_fwd_warp(const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
+__device__ __forceinline__ void
+d_gat_fwd_warp(int64_t blk, int64_t nblk, const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
                const int32_t* __restrict__ rows, int64_t n_list, const T* __restrict__ sl,
                const T* __restrict__ sr, float slope, T* __restrict__ alpha) {
   constexpr int EPB = 32 / H;
   const int lane = threadIdx.x & 31, j = lane / H, h = lane % H;
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); w < n_list;
+  const int64_t nwarps = (int64_t)nblk * (blockDim.x >> 5);
+  for (int64_t w = blk * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); w < n_list;
        w += nwarps) {
     const int64_t r = rows[w];
     const int64_t beg = offsets[r], end = offsets[r + 1];
@@ -216,14 +216,14 @@ k_gat_fwd_warp(const int64_t* __restrict__ offsets, const int32_t* __restrict__ 
 }
 
 template <typename T, int H>
-__global__ void __launch_bounds__(256)
-k_gat_fwd_cta(const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
+__device__ __forceinline__ void
+d_gat_fwd_cta(int64_t blk, int64_t nblk, const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
               const int32_t* __restrict__ rows, const T* __restrict__ sl,
               const T* __restrict__ sr, float slope, T* __restrict__ alpha) {
   constexpr int EPB = 256 / H;
   __shared__ float sm[8][H], ss[8][H];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, j = tid / H, h = tid % H;
-  const int64_t r = rows[blockIdx.x];
+  const int64_t r = rows[blk];
   const int64_t beg = offsets[r], end = offsets[r + 1];
   const float a = Num<T>::to_f(sl[r * H + h]) * kLog2e;
   float m = -INFINITY, s = 0.0f;
@@ -240,12 +240,12 @@ k_gat_fwd_cta(const int64_t* __restrict__ offsets, const int32_t* __restrict__ c
 // --------------------------------------------------------------- backward
 
 template <typename T, int H>
-__global__ void __launch_bounds__(256)
-k_gat_bwd_thread(const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
+__device__ __forceinline__ void
+d_gat_bwd_thread(int64_t blk, int64_t nblk, const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
                  int64_t n_rows, const T* __restrict__ sl, const T* __restrict__ sr, float slope,
                  const T* __restrict__ alpha, const T* __restrict__ dalpha, T* __restrict__ de,
                  T* __restrict__ dsl, int short_max) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t t = blk * (int64_t)blockDim.x + threadIdx.x;
   if (t >= n_rows * H) return;
   const int64_t r = t / H;
   const int h = (int)(t - r * H);
@@ -257,15 +257,15 @@ k_gat_bwd_thread(const int64_t* __restrict__ offsets, const int32_t* __restrict_
 }
 
 template <typename T, int H>
-__global__ void __launch_bounds__(256)
-k_gat_bwd_warp(const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
+__device__ __forceinline__ void
+d_gat_bwd_warp(int64_t blk, int64_t nblk, const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
                const int32_t* __restrict__ rows, int64_t n_list, const T* __restrict__ sl,
                const T* __restrict__ sr, float slope, const T* __restrict__ alpha,
                const T* __restrict__ dalpha, T* __restrict__ de, T* __restrict__ dsl) {
   constexpr int EPB = 32 / H;
   const int lane = threadIdx.x & 31, j = lane / H, h = lane % H;
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); w < n_list;
+  const int64_t nwarps = (int64_t)nblk * (blockDim.x >> 5);
+  for (int64_t w = blk * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); w < n_list;
        w += nwarps) {
     const int64_t r = rows[w];
     const int64_t beg = offsets[r], end = offsets[r + 1];
@@ -291,15 +291,15 @@ __device__ __forceinline__ float block_sum_h(float v, float (*red)[H]) {
 }
 
 template <typename T, int H>
-__global__ void __launch_bounds__(256)
-k_gat_bwd_cta(const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
+__device__ __forceinline__ void
+d_gat_bwd_cta(int64_t blk, int64_t nblk, const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
               const int32_t* __restrict__ rows, const T* __restrict__ sl,
               const T* __restrict__ sr, float slope, const T* __restrict__ alpha,
               const T* __restrict__ dalpha, T* __restrict__ de, T* __restrict__ dsl) {
   constexpr int EPB = 256 / H;
   __shared__ float red[8][H];
   const int tid = threadIdx.x, j = tid / H, h = tid % H;
-  const int64_t r = rows[blockIdx.x];
+  const int64_t r = rows[blk];
   const int64_t beg = offsets[r], end = offsets[r + 1];
   const float d = block_sum_h<H>(bwd_pass1<T, H>(alpha, dalpha, beg + j, end, EPB, h), red);
   const float a = Num<T>::to_f(sl[r * H + h]);
@@ -311,10 +311,10 @@ k_gat_bwd_cta(const int64_t* __restrict__ offsets, const int32_t* __restrict__ c
 // ------------------------------------------------------------- edge sums
 
 template <typename T, int H>
-__global__ void __launch_bounds__(256)
-k_gat_sums_thread(const int64_t* __restrict__ offsets, int64_t n_rows, const T* __restrict__ v,
+__device__ __forceinline__ void
+d_gat_sums_thread(int64_t blk, int64_t nblk, const int64_t* __restrict__ offsets, int64_t n_rows, const T* __restrict__ v,
                   const int32_t* __restrict__ perm, T* __restrict__ out, int short_max) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t t = blk * (int64_t)blockDim.x + threadIdx.x;
   if (t >= n_rows * H) return;
   const int64_t r = t / H;
   const int h = (int)(t - r * H);
@@ -324,14 +324,14 @@ k_gat_sums_thread(const int64_t* __restrict__ offsets, int64_t n_rows, const T* 
 }
 
 template <typename T, int H>
-__global__ void __launch_bounds__(256)
-k_gat_sums_warp(const int64_t* __restrict__ offsets, const int32_t* __restrict__ rows,
+__device__ __forceinline__ void
+d_gat_sums_warp(int64_t blk, int64_t nblk, const int64_t* __restrict__ offsets, const int32_t* __restrict__ rows,
                 int64_t n_list, const T* __restrict__ v, const int32_t* __restrict__ perm,
                 T* __restrict__ out) {
   constexpr int EPB = 32 / H;
   const int lane = threadIdx.x & 31, j = lane / H, h = lane % H;
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); w < n_list;
+  const int64_t nwarps = (int64_t)nblk * (blockDim.x >> 5);
+  for (int64_t w = blk * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); w < n_list;
        w += nwarps) {
     const int64_t r = rows[w];
     const int64_t beg = offsets[r], end = offsets[r + 1];
@@ -341,16 +341,72 @@ k_gat_sums_warp(const int64_t* __restrict__ offsets, const int32_t* __restrict__
 }
 
 template <typename T, int H>
-__global__ void __launch_bounds__(256)
-k_gat_sums_cta(const int64_t* __restrict__ offsets, const int32_t* __restrict__ rows,
+__device__ __forceinline__ void
+d_gat_sums_cta(int64_t blk, int64_t nblk, const int64_t* __restrict__ offsets, const int32_t* __restrict__ rows,
                const T* __restrict__ v, const int32_t* __restrict__ perm, T* __restrict__ out) {
   constexpr int EPB = 256 / H;
   __shared__ float red[8][H];
   const int tid = threadIdx.x, j = tid / H, h = tid % H;
-  const int64_t r = rows[blockIdx.x];
+  const int64_t r = rows[blk];
   const int64_t beg = offsets[r], end = offsets[r + 1];
   const float acc = block_sum_h<H>(sums_pass<T, H>(v, perm, beg + j, end, EPB, h), red);
   if (tid < H) out[r * H + tid] = Num<T>::from_f(acc);
+}
+
+
+// One launch per operation: blocks [0, n_long) take the long rows (one CTA each,
+// dispatched first so the hub rows start early and overlap everything else),
+// the next b_med blocks the medium rows (warp per row), the rest one thread per
+// (row, head) for the short rows.
+template <typename T, int H>
+__global__ void __launch_bounds__(256)
+k_gat_fwd_all(const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
+              int64_t n_rows, const int32_t* __restrict__ medium, int64_t n_medium,
+              const int32_t* __restrict__ longr, int64_t n_long, int64_t b_med,
+              const T* __restrict__ sl, const T* __restrict__ sr, float slope,
+              T* __restrict__ alpha, int short_max) {
+  int64_t b = blockIdx.x;
+  if (b < n_long) return d_gat_fwd_cta<T, H>(b, n_long, offsets, cols, longr, sl, sr, slope, alpha);
+  b -= n_long;
+  if (b < b_med)
+    return d_gat_fwd_warp<T, H>(b, b_med, offsets, cols, medium, n_medium, sl, sr, slope, alpha);
+  b -= b_med;
+  d_gat_fwd_thread<T, H>(b, 0, offsets, cols, n_rows, sl, sr, slope, alpha, short_max);
+}
+
+template <typename T, int H>
+__global__ void __launch_bounds__(256)
+k_gat_bwd_all(const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
+              int64_t n_rows, const int32_t* __restrict__ medium, int64_t n_medium,
+              const int32_t* __restrict__ longr, int64_t n_long, int64_t b_med,
+              const T* __restrict__ sl, const T* __restrict__ sr, float slope,
+              const T* __restrict__ alpha, const T* __restrict__ dalpha, T* __restrict__ de,
+              T* __restrict__ dsl, int short_max) {
+  int64_t b = blockIdx.x;
+  if (b < n_long)
+    return d_gat_bwd_cta<T, H>(b, n_long, offsets, cols, longr, sl, sr, slope, alpha, dalpha, de, dsl);
+  b -= n_long;
+  if (b < b_med)
+    return d_gat_bwd_warp<T, H>(b, b_med, offsets, cols, medium, n_medium, sl, sr, slope, alpha,
+                                dalpha, de, dsl);
+  b -= b_med;
+  d_gat_bwd_thread<T, H>(b, 0, offsets, cols, n_rows, sl, sr, slope, alpha, dalpha, de, dsl,
+                         short_max);
+}
+
+template <typename T, int H>
+__global__ void __launch_bounds__(256)
+k_gat_sums_all(const int64_t* __restrict__ offsets, int64_t n_rows,
+               const int32_t* __restrict__ medium, int64_t n_medium,
+               const int32_t* __restrict__ longr, int64_t n_long, int64_t b_med,
+               const T* __restrict__ v, const int32_t* __restrict__ perm, T* __restrict__ out,
+               int short_max) {
+  int64_t b = blockIdx.x;
+  if (b < n_long) return d_gat_sums_cta<T, H>(b, n_long, offsets, longr, v, perm, out);
+  b -= n_long;
+  if (b < b_med) return d_gat_sums_warp<T, H>(b, b_med, offsets, medium, n_medium, v, perm, out);
+  b -= b_med;
+  d_gat_sums_thread<T, H>(b, 0, offsets, n_rows, v, perm, out, short_max);
 }
 
 // -------------------------------------------------------------- head mean
@@ -397,47 +453,35 @@ struct GatRows {
   cudaStream_t st;
 };
 
+static inline int64_t med_blocks(const GatRows& g) {
+  return g.n_medium ? grid_for(g.n_medium, 8, 148 * 32) : 0;
+}
+
+static inline unsigned all_blocks(const GatRows& g, int H) {
+  return (unsigned)(g.n_long + med_blocks(g) + grid_for(g.n_rows * H, 256));
+}
+
 template <typename T, int H>
 static void gat_fwd(const GatRows& g, const void* sl, const void* sr, float slope, void* alpha) {
-  const T* a = (const T*)sl;
-  const T* b = (const T*)sr;
-  T* out = (T*)alpha;
-  k_gat_fwd_thread<T, H><<<grid_for(g.n_rows * H, 256), 256, 0, g.st>>>(
-      g.offsets, g.cols, g.n_rows, a, b, slope, out, g.short_max);
-  if (g.n_medium)
-    k_gat_fwd_warp<T, H><<<grid_for(g.n_medium, 8, 148 * 32), 256, 0, g.st>>>(
-        g.offsets, g.cols, g.medium, g.n_medium, a, b, slope, out);
-  if (g.n_long)
-    k_gat_fwd_cta<T, H><<<(unsigned)g.n_long, 256, 0, g.st>>>(g.offsets, g.cols, g.longr, a, b,
-                                                              slope, out);
+  k_gat_fwd_all<T, H><<<all_blocks(g, H), 256, 0, g.st>>>(
+      g.offsets, g.cols, g.n_rows, g.medium, g.n_medium, g.longr, g.n_long, med_blocks(g),
+      (const T*)sl, (const T*)sr, slope, (T*)alpha, g.short_max);
 }
 
 template <typename T, int H>
 static void gat_bwd(const GatRows& g, const void* sl, const void* sr, float slope,
                     const void* alpha, const void* dalpha, void* de, void* dsl) {
-  const T *a = (const T*)sl, *b = (const T*)sr, *al = (const T*)alpha, *da = (const T*)dalpha;
-  T *o = (T*)de, *ds = (T*)dsl;
-  k_gat_bwd_thread<T, H><<<grid_for(g.n_rows * H, 256), 256, 0, g.st>>>(
-      g.offsets, g.cols, g.n_rows, a, b, slope, al, da, o, ds, g.short_max);
-  if (g.n_medium)
-    k_gat_bwd_warp<T, H><<<grid_for(g.n_medium, 8, 148 * 32), 256, 0, g.st>>>(
-        g.offsets, g.cols, g.medium, g.n_medium, a, b, slope, al, da, o, ds);
-  if (g.n_long)
-    k_gat_bwd_cta<T, H><<<(unsigned)g.n_long, 256, 0, g.st>>>(g.offsets, g.cols, g.longr, a, b,
-                                                              slope, al, da, o, ds);
+  k_gat_bwd_all<T, H><<<all_blocks(g, H), 256, 0, g.st>>>(
+      g.offsets, g.cols, g.n_rows, g.medium, g.n_medium, g.longr, g.n_long, med_blocks(g),
+      (const T*)sl, (const T*)sr, slope, (const T*)alpha, (const T*)dalpha, (T*)de, (T*)dsl,
+      g.short_max);
 }
 
 template <typename T, int H>
 static void gat_sums(const GatRows& g, const void* v, const int32_t* perm, void* out) {
-  const T* vv = (const T*)v;
-  T* o = (T*)out;
-  k_gat_sums_thread<T, H><<<grid_for(g.n_rows * H, 256), 256, 0, g.st>>>(
-      g.offsets, g.n_rows, vv, perm, o, g.short_max);
-  if (g.n_medium)
-    k_gat_sums_warp<T, H><<<grid_for(g.n_medium, 8, 148 * 32), 256, 0, g.st>>>(
-        g.offsets, g.medium, g.n_medium, vv, perm, o);
-  if (g.n_long)
-    k_gat_sums_cta<T, H><<<(unsigned)g.n_long, 256, 0, g.st>>>(g.offsets, g.longr, vv, perm, o);
+  k_gat_sums_all<T, H><<<all_blocks(g, H), 256, 0, g.st>>>(
+      g.offsets, g.n_rows, g.medium, g.n_medium, g.longr, g.n_long, med_blocks(g),
+      (const T*)v, perm, (T*)out, g.short_max);
 }
 
 #define HG_GAT_HEADS(FN, T, ...)                  \
