@@ -1200,35 +1200,56 @@ k_head_dots(const T* __restrict__ z, const T* __restrict__ al, const T* __restri
   const int tl = lane & (TEAM - 1);
   const unsigned tmask =
       TEAM == 32 ? 0xffffffffu : (((1u << TEAM) - 1u) << (lane & ~(TEAM - 1)));
-  const int64_t item = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TEAM;
-  if (item >= n * heads) return;
-  const int64_t node = item / heads;
-  const int h = (int)(item - node * heads);
+  const int64_t items = n * heads;
+  const int64_t stride = (int64_t)gridDim.x * (blockDim.x / TEAM);
   const int nchunk = fh / V;
-  float pl = 0.0f, pr = 0.0f;
-  for (int c = tl; c < nchunk; c += TEAM) {
-    const int f = h * fh + c * V;
-    const Raw zr = *reinterpret_cast<const Raw*>(z + node * (int64_t)heads * fh + f);
-    const Raw lr_ = *reinterpret_cast<const Raw*>(al + f);
-    const Raw rr_ = *reinterpret_cast<const Raw*>(ar + f);
-    const T* za = reinterpret_cast<const T*>(&zr);
-    const T* la = reinterpret_cast<const T*>(&lr_);
-    const T* ra = reinterpret_cast<const T*>(&rr_);
+  // grid-stride, two (node, head) items in flight per team
+  for (int64_t it0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TEAM; it0 < items;
+       it0 += 2 * stride) {
+    float pl[2] = {0.0f, 0.0f}, pr[2] = {0.0f, 0.0f};
+    for (int c = tl; c < nchunk; c += TEAM) {
+      Raw zr[2];
 #pragma unroll
-    for (int i = 0; i < V; ++i) {
-      const float zf = Num<T>::to_f(za[i]);
-      pl = fmaf(zf, Num<T>::to_f(la[i]), pl);
-      pr = fmaf(zf, Num<T>::to_f(ra[i]), pr);
+      for (int u = 0; u < 2; ++u) {
+        const int64_t item = it0 + u * stride;
+        if (item < items) {
+          const int64_t node = item / heads;
+          const int h = (int)(item - node * heads);
+          zr[u] = *reinterpret_cast<const Raw*>(z + node * (int64_t)heads * fh + h * fh + c * V);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int64_t item = it0 + u * stride;
+        if (item >= items) continue;
+        const int h = (int)(item % heads);
+        const int f = h * fh + c * V;
+        const Raw lr_ = *reinterpret_cast<const Raw*>(al + f);
+        const Raw rr_ = *reinterpret_cast<const Raw*>(ar + f);
+        const T* za = reinterpret_cast<const T*>(&zr[u]);
+        const T* la = reinterpret_cast<const T*>(&lr_);
+        const T* ra = reinterpret_cast<const T*>(&rr_);
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+          const float zf = Num<T>::to_f(za[i]);
+          pl[u] = fmaf(zf, Num<T>::to_f(la[i]), pl[u]);
+          pr[u] = fmaf(zf, Num<T>::to_f(ra[i]), pr[u]);
+        }
+      }
     }
-  }
 #pragma unroll
-  for (int o = TEAM / 2; o >= 1; o >>= 1) {
-    pl += __shfl_xor_sync(tmask, pl, o, TEAM);
-    pr += __shfl_xor_sync(tmask, pr, o, TEAM);
-  }
-  if (tl == 0) {
-    sl[item] = Num<T>::from_f(pl);
-    sr[item] = Num<T>::from_f(pr);
+    for (int u = 0; u < 2; ++u) {
+#pragma unroll
+      for (int o = TEAM / 2; o >= 1; o >>= 1) {
+        pl[u] += __shfl_xor_sync(tmask, pl[u], o, TEAM);
+        pr[u] += __shfl_xor_sync(tmask, pr[u], o, TEAM);
+      }
+      const int64_t item = it0 + u * stride;
+      if (tl == 0 && item < items) {
+        sl[item] = Num<T>::from_f(pl[u]);
+        sr[item] = Num<T>::from_f(pr[u]);
+      }
+    }
   }
 }
 
@@ -1275,6 +1296,64 @@ k_head_dots_bwd(const T* __restrict__ z, const T* __restrict__ al, const T* __re
       part[((int64_t)blockIdx.x * 2 + 1) * F + f] = tr;
     }
     __syncthreads();
+  }
+}
+
+// Vectorised pass 1 for binary16 with fh % 8 == 0: thread (rr, c) owns the
+// 8-feature chunk c of row slot rr (one head), 16-byte loads / stores, fp32
+// partials per feature folded over the row slots in slot order.
+__global__ void __launch_bounds__(256)
+k_head_dots_bwd_v8(const __half* __restrict__ z, const __half* __restrict__ al,
+                   const __half* __restrict__ ar, const __half* __restrict__ gl,
+                   const __half* __restrict__ gr, int64_t n, int heads, int fh,
+                   __half* __restrict__ gz, float* __restrict__ part) {
+  extern __shared__ float hdb_sh[];  // [2][rpi][F]
+  const int F = heads * fh, C = F / 8;
+  const int rpi = 256 / C;
+  const int rr = threadIdx.x / C, c = threadIdx.x - (threadIdx.x / C) * C;
+  const bool act = rr < rpi;
+  const int h = (c * 8) / fh;
+  __align__(16) __half a1[8], a2[8];
+  float sl[8], sr[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) sl[i] = sr[i] = 0.0f;
+  if (act) {
+    *reinterpret_cast<uint4*>(a1) = *reinterpret_cast<const uint4*>(al + c * 8);
+    *reinterpret_cast<uint4*>(a2) = *reinterpret_cast<const uint4*>(ar + c * 8);
+    for (int64_t r = (int64_t)blockIdx.x * rpi + rr; r < n; r += (int64_t)gridDim.x * rpi) {
+      const __half g1 = gl[r * heads + h], g2 = gr[r * heads + h];
+      const float g1f = __half2float(g1), g2f = __half2float(g2);
+      const uint4 zv = *reinterpret_cast<const uint4*>(z + r * F + c * 8);
+      const __half* ze = reinterpret_cast<const __half*>(&zv);
+      __align__(16) __half o[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        o[i] = __hadd_rn(__hmul_rn(g1, a1[i]), __hmul_rn(g2, a2[i]));
+        const float zf = __half2float(ze[i]);
+        sl[i] = fmaf(zf, g1f, sl[i]);
+        sr[i] = fmaf(zf, g2f, sr[i]);
+      }
+      *reinterpret_cast<uint4*>(gz + r * F + c * 8) = *reinterpret_cast<const uint4*>(o);
+    }
+  }
+  float* bl = hdb_sh;
+  float* br = hdb_sh + rpi * F;
+  if (act) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      bl[rr * F + c * 8 + i] = sl[i];
+      br[rr * F + c * 8 + i] = sr[i];
+    }
+  }
+  __syncthreads();
+  for (int f = threadIdx.x; f < F; f += blockDim.x) {
+    float tl = 0.0f, tr = 0.0f;
+    for (int q = 0; q < rpi; ++q) {
+      tl += bl[q * F + f];
+      tr += br[q * F + f];
+    }
+    part[((int64_t)blockIdx.x * 2 + 0) * F + f] = tl;
+    part[((int64_t)blockIdx.x * 2 + 1) * F + f] = tr;
   }
 }
 
@@ -1327,7 +1406,7 @@ extern "C" int hg_head_dots(const void* z, const void* a_l, const void* a_r, int
   const bool aligned = (reinterpret_cast<uintptr_t>(z) | reinterpret_cast<uintptr_t>(a_l) |
                         reinterpret_cast<uintptr_t>(a_r)) % 16 == 0;
 #define HG_HD(TT, VV, TM)                                                                   \
-  k_head_dots<TT, VV, TM><<<(unsigned)((items * TM + 255) / 256), 256, 0, st>>>(            \
+  k_head_dots<TT, VV, TM><<<grid_for(items * TM, 256, 148 * 16), 256, 0, st>>>(            \
       (const TT*)z, (const TT*)a_l, (const TT*)a_r, n, heads, fh, (TT*)s_l, (TT*)s_r)
   if (dtype == HG_F16) {
     if (aligned && fh % 8 == 0) {
@@ -1384,9 +1463,21 @@ extern "C" int hg_head_dots_bwd(const void* z, const void* a_l, const void* a_r,
   cudaStream_t st = as_stream(stream);
   float* part = (float*)ws;
   if (dtype == HG_F16) {
-    k_head_dots_bwd<__half><<<kHdbBlocks, 256, 0, st>>>(
-        (const __half*)z, (const __half*)a_l, (const __half*)a_r, (const __half*)g_l,
-        (const __half*)g_r, n, heads, fh, (__half*)gz, part);
+    const bool vec = fh % 8 == 0 && F / 8 <= 256 &&
+                     ((reinterpret_cast<uintptr_t>(z) | reinterpret_cast<uintptr_t>(a_l) |
+                       reinterpret_cast<uintptr_t>(a_r) | reinterpret_cast<uintptr_t>(gz)) & 15) == 0;
+    if (vec) {
+      const size_t sh = (size_t)2 * (256 / (F / 8)) * F * sizeof(float);
+      if (sh > 48 * 1024)
+        HG_CUDA(cudaFuncSetAttribute(k_head_dots_bwd_v8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+      k_head_dots_bwd_v8<<<kHdbBlocks, 256, sh, st>>>(
+          (const __half*)z, (const __half*)a_l, (const __half*)a_r, (const __half*)g_l,
+          (const __half*)g_r, n, heads, fh, (__half*)gz, part);
+    } else {
+      k_head_dots_bwd<__half><<<kHdbBlocks, 256, 0, st>>>(
+          (const __half*)z, (const __half*)a_l, (const __half*)a_r, (const __half*)g_l,
+          (const __half*)g_r, n, heads, fh, (__half*)gz, part);
+    }
     k_head_dots_bwd_fold<__half><<<(F + 255) / 256, 256, 0, st>>>(part, kHdbBlocks, F,
                                                                 (__half*)ga_l, (__half*)ga_r);
   } else {
