@@ -441,6 +441,49 @@ __global__ void k_head_mean_bwd(const T* __restrict__ g, int64_t n, int heads, i
   }
 }
 
+// 8-column vector versions (binary16, f % 8 == 0, 16-byte aligned).
+__global__ void k_head_mean_v8(const __half* __restrict__ y, int64_t n, int heads, int f,
+                               __half* __restrict__ out) {
+  const int C = f / 8;
+  const int64_t total = n * (int64_t)C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / C;
+    const int c = (int)(i - r * C);
+    double s[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s[k] = 0.0;
+    for (int h = 0; h < heads; ++h) {
+      const uint4 v = *reinterpret_cast<const uint4*>(y + (r * heads + h) * f + c * 8);
+      const __half* e = reinterpret_cast<const __half*>(&v);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s[k] += (double)__half2float(e[k]);
+    }
+    __align__(16) __half o[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = __double2half(s[k] / heads);
+    *reinterpret_cast<uint4*>(out + r * f + c * 8) = *reinterpret_cast<const uint4*>(o);
+  }
+}
+
+__global__ void k_head_mean_bwd_v8(const __half* __restrict__ g, int64_t n, int heads, int f,
+                                   __half* __restrict__ gin) {
+  const int C = f / 8;
+  const int64_t total = n * (int64_t)C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / C;
+    const int c = (int)(i - r * C);
+    const uint4 v = *reinterpret_cast<const uint4*>(g + r * f + c * 8);
+    const __half* e = reinterpret_cast<const __half*>(&v);
+    __align__(16) __half o[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = __double2half((double)__half2float(e[k]) / heads);
+    for (int h = 0; h < heads; ++h)
+      *reinterpret_cast<uint4*>(gin + (r * heads + h) * f + c * 8) = *reinterpret_cast<const uint4*>(o);
+  }
+}
+
 struct GatRows {
   const int64_t* offsets;
   const int32_t* cols;
@@ -563,7 +606,12 @@ extern "C" int hg_head_mean(const void* y, int64_t n, int32_t heads, int32_t f, 
   HG_REQUIRE(heads >= 1 && f >= 1, "hg_head_mean: bad shape");
   if (n == 0) return HG_OK;
   const int g = grid_for(n * f, 256, 148 * 16);
-  if (dtype == HG_F16)
+  const bool v8 = dtype == HG_F16 && f % 8 == 0 &&
+                  ((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+  if (v8)
+    k_head_mean_v8<<<grid_for(n * (f / 8), 256, 148 * 16), 256, 0, as_stream(stream)>>>(
+        (const __half*)y, n, heads, f, (__half*)out);
+  else if (dtype == HG_F16)
     k_head_mean<__half><<<g, 256, 0, as_stream(stream)>>>((const __half*)y, n, heads, f, (__half*)out);
   else
     k_head_mean<float><<<g, 256, 0, as_stream(stream)>>>((const float*)y, n, heads, f, (float*)out);
@@ -577,7 +625,12 @@ extern "C" int hg_head_mean_bwd(const void* g, int64_t n, int32_t heads, int32_t
   HG_REQUIRE(heads >= 1 && f >= 1, "hg_head_mean_bwd: bad shape");
   if (n == 0) return HG_OK;
   const int gr = grid_for(n * f, 256, 148 * 16);
-  if (dtype == HG_F16)
+  const bool v8 = dtype == HG_F16 && f % 8 == 0 &&
+                  ((reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(gin)) & 15) == 0;
+  if (v8)
+    k_head_mean_bwd_v8<<<grid_for(n * (f / 8), 256, 148 * 16), 256, 0, as_stream(stream)>>>(
+        (const __half*)g, n, heads, f, (__half*)gin);
+  else if (dtype == HG_F16)
     k_head_mean_bwd<__half><<<gr, 256, 0, as_stream(stream)>>>((const __half*)g, n, heads, f, (__half*)gin);
   else
     k_head_mean_bwd<float><<<gr, 256, 0, as_stream(stream)>>>((const float*)g, n, heads, f, (float*)gin);

@@ -582,7 +582,7 @@ def test_gat_attention_fast_vs_f64(cuda, heads):
     assert np.all(np.abs(got_r.astype(np.float64) - want_r) <= 2e-3 * np.maximum(1, np.abs(want_r)))
 
 
-@pytest.mark.parametrize("heads,f", [(4, 16), (2, 3), (8, 8)])
+@pytest.mark.parametrize("heads,f", [(4, 16), (2, 3), (8, 8), (4, 24), (3, 40)])
 def test_head_mean_bits(cuda, heads, f):
     from paper_2411_01109_b200 import device as D
 
