@@ -104,15 +104,17 @@ int hg_schedule_build(const int64_t* offsets, int64_t n, int32_t split_cap, int3
  * pass: no atomics, bitwise deterministic.  x / y rows are ldx / ldy elements
  * apart (0 = F): a narrower F can run over wider (padded) storage, e.g. 48
  * classes in 64-wide rows whose 128-byte lines never straddle; in_scale needs
- * ldx == F. */
+ * ldx == F.  relu != 0 applies models.relu to each output (the next layer's
+ * activation fused into the aggregation's epilogue). */
 int hg_spmm_workspace(int64_t n_cols, int32_t F, int64_t num_slots, int has_in_scale,
                       int dtype, size_t* bytes);
 int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_rows, int64_t n_cols,
             int64_t num_edges, const int32_t* units, int64_t num_units,
             const int32_t* split_rows, int64_t num_split_rows, int64_t num_slots,
             const void* w, const int32_t* w_index, int32_t heads, const void* x, void* y,
-            int32_t F, int64_t ldx, int64_t ldy, int32_t scaling, const void* in_scale,
-            const void* out_factor, int dtype, void* ws, size_t ws_bytes, void* stream);
+            int32_t F, int64_t ldx, int64_t ldy, int32_t scaling, int32_t relu,
+            const void* in_scale, const void* out_factor, int dtype, void* ws, size_t ws_bytes,
+            void* stream);
 
 /* Reference-order SpMM, bit-exact with halfsparse _spmm_edge_parallel
  * (kernels.py:328-391; order spelled out in _ref_spmm_edge, kernels.py:603-688):

@@ -36,15 +36,22 @@ __device__ __forceinline__ void raw_to_float(const typename RawVec<V * sizeof(T)
   }
 }
 
-// fmode: 0 -> rnd(S); 1 -> post: rnd(rnd(S) * f) for f > 0; 2 -> rnd(S * f)
+// fmode & 3: 0 -> rnd(S); 1 -> post: rnd(rnd(S) * f) for f > 0; 2 -> rnd(S * f);
+// fmode & 4: then ReLU (models.relu: x > 0 ? x : 0, models.py:176-185).
 template <typename T>
-__device__ __forceinline__ T finalize(float s, int fmode, T fo) {
-  if (fmode == 0) return Num<T>::from_f(s);
-  if (fmode == 1) {
+__device__ __forceinline__ T finalize_mode(float s, int fmode, T fo) {
+  if ((fmode & 3) == 0) return Num<T>::from_f(s);
+  if ((fmode & 3) == 1) {
     T h = Num<T>::from_f(s);
     return Num<T>::gt0(fo) ? Num<T>::mul(h, fo) : h;
   }
   return Num<T>::from_f(s * Num<T>::to_f(fo));
+}
+
+template <typename T>
+__device__ __forceinline__ T finalize(float s, int fmode, T fo) {
+  const T h = finalize_mode<T>(s, fmode, fo);
+  return (fmode & 4) && !Num<T>::gt0(h) ? Num<T>::zero() : h;
 }
 
 template <typename T, int V>
@@ -520,8 +527,8 @@ extern "C" int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_ro
                        const int32_t* split_rows, int64_t num_split_rows, int64_t num_slots,
                        const void* w, const int32_t* w_index, int32_t heads, const void* x,
                        void* y, int32_t F, int64_t ldx, int64_t ldy, int32_t scaling,
-                       const void* in_scale, const void* out_factor, int dtype, void* ws,
-                       size_t ws_bytes, void* stream) {
+                       int32_t relu, const void* in_scale, const void* out_factor, int dtype,
+                       void* ws, size_t ws_bytes, void* stream) {
   HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
   HG_REQUIRE(F > 0 && F % 2 == 0, "feature length %d must be even and positive", F);
   HG_REQUIRE(heads >= 1 && F % heads == 0 && (F / heads) % 2 == 0,
@@ -554,7 +561,7 @@ extern "C" int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_ro
   a.split_rows = reinterpret_cast<const int4*>(split_rows); a.num_split = num_split_rows;
   a.w = w; a.widx = w_index; a.heads = heads; a.fh = F / heads;
   a.x = x; a.y = y; a.carry = carry; a.F = F; a.ldx = (int)ldx; a.ldy = (int)ldy;
-  a.fmode = out_factor == nullptr ? 0 : (scaling == HG_SCALING_POST ? 1 : 2);
+  a.fmode = (out_factor == nullptr ? 0 : (scaling == HG_SCALING_POST ? 1 : 2)) | (relu ? 4 : 0);
   a.fout = out_factor; a.st = st;
   // Column slabs: when X (n_cols x F) overflows the L2 budget but a slab of
   // >= 32 columns fits, aggregate slab by slab so the random row gathers of

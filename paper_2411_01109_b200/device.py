@@ -384,7 +384,7 @@ def _row_strided(t):
 
 def spmm_csr(view: CsrView, x: torch.Tensor, w=None, w_index=None, heads: int = 1,
              scaling: str = "post", fin=None, fout=None, out=None,
-             split_cap: int = DEFAULT_SPLIT_CAP) -> torch.Tensor:
+             split_cap: int = DEFAULT_SPLIT_CAP, relu: bool = False) -> torch.Tensor:
     """fp32-guarded row-owned SpMM over one CSR view (hg_spmm).  x and out may
     be column slices of wider row-major storage (row strides passed through)."""
     _require_cuda(x)
@@ -413,8 +413,8 @@ def spmm_csr(view: CsrView, x: torch.Tensor, w=None, w_index=None, heads: int = 
     nat.call("hg_spmm", _p(view.offsets), _p(view.cols), view.n_rows, view.n_cols,
              view.num_edges, _p(sched.units), sched.num_units, _p(sched.split_rows),
              sched.split_rows.shape[0], sched.num_slots, _p(w), _p(w_index), heads, _p(x),
-             _p(out), f, x.stride(0), out.stride(0), nat.SCALING_CODES[scaling], _p(fin),
-             _p(fout), dt, _p(ws),
+             _p(out), f, x.stride(0), out.stride(0), nat.SCALING_CODES[scaling], int(relu),
+             _p(fin), _p(fout), dt, _p(ws),
              0 if ws is None else ws.numel(), _stream())
     Probe.launches += int(sched.num_units > 0) + int(sched.split_rows.shape[0] > 0) + int(
         fin is not None)
@@ -427,14 +427,14 @@ def spmm_csr(view: CsrView, x: torch.Tensor, w=None, w_index=None, heads: int = 
 
 
 def spmm(dg: DeviceGraph, x, w=None, scaling="post", norm="none", transpose=False, heads=1,
-         out=None, weight_via_perm=False):
+         out=None, weight_via_perm=False, relu=False):
     """SpMMv / SpMMve on the graph (or its transpose), fp32-guarded.
     weight_via_perm: w is indexed by forward edge id and read through perm
     (spmm_weighted backward, models.py:309-311) without materialising w[perm]."""
     view = dg.view(transpose)
     fin, fout = dg.norm_tables(norm, transpose, x.dtype)
     widx = view.perm if (w is not None and weight_via_perm) else None
-    return spmm_csr(view, x, w, widx, heads, scaling, fin, fout, out)
+    return spmm_csr(view, x, w, widx, heads, scaling, fin, fout, out, relu=relu)
 
 
 def spmm_edge_ref(dg: DeviceGraph, x, w=None, scaling="post", norm="none", transpose=False,

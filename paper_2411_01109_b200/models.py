@@ -136,11 +136,18 @@ class GraphBundle:
     def num_edges(self):
         return self.dg.num_edges
 
+    @property
+    def fused_relu(self):
+        """Aggregations may apply the following ReLU in their epilogue."""
+        return self.numerics == "fast"
+
     def spmm(self, x, w=None, scaling="post", norm="none", transpose=False, heads=1,
-             weight_via_perm=False):
+             weight_via_perm=False, relu=False):
         if self.numerics == "fast":
             return D.spmm(self.dg, x, w, scaling, norm, transpose, heads,
-                          weight_via_perm=weight_via_perm)
+                          weight_via_perm=weight_via_perm, relu=relu)
+        if relu:
+            raise ValueError("fused ReLU needs numerics='fast'")
         # reference order: one head at a time, weights materialised in CSC order
         if w is not None and weight_via_perm:
             w = w[self.dg.perm.long()]
@@ -159,19 +166,20 @@ class GraphBundle:
         """GCN layers may fuse add_bias into the aggregation's input pass."""
         return self.numerics == "fast"
 
-    def gcn_agg_tc(self, x, w, b, reduction):
+    def gcn_agg_tc(self, x, w, b, reduction, relu=False):
         """GCN layer forward: tcgen05 GEMM with bias + input scale fused, then
-        the gather SpMM."""
+        the gather SpMM (optionally with the next ReLU in its epilogue)."""
         fin, fout = self.dg.norm_tables(reduction.norm, False, x.dtype)
         xs = D.gemm_tc(x, w.t().contiguous(), b, fin)
-        return D.spmm_csr(self.dg.view(False), xs, None, None, 1, reduction.scaling, None, fout)
+        return D.spmm_csr(self.dg.view(False), xs, None, None, 1, reduction.scaling, None, fout,
+                          relu=relu)
 
-    def bias_spmm(self, h, b, scaling, norm):
+    def bias_spmm(self, h, b, scaling, norm, relu=False):
         """spmm(add_bias(h, b)) with the bias add and the left-norm input
         scaling in one pass (hg_bias_scale_rows), then the gather kernel."""
         fin, fout = self.dg.norm_tables(norm, False, h.dtype)
         xs = D.bias_scale_rows(h, b, fin)
-        return D.spmm_csr(self.dg.view(False), xs, None, None, 1, scaling, None, fout)
+        return D.spmm_csr(self.dg.view(False), xs, None, None, 1, scaling, None, fout, relu=relu)
 
     @property
     def fused_gat(self):
@@ -251,15 +259,22 @@ class _BiasAggFn(torch.autograd.Function):
     mirrored-norm transposed SpMM, and the bias gradient is its column sum."""
 
     @staticmethod
-    def forward(ctx, h, b, bundle, reduction):
-        ctx.bundle, ctx.reduction = bundle, reduction
+    def forward(ctx, h, b, bundle, reduction, relu=False):
+        ctx.bundle, ctx.reduction, ctx.relu = bundle, reduction, relu
+        if relu:
+            y = bundle.bias_spmm(h, b, reduction.scaling, reduction.norm, relu=True)
+            ctx.save_for_backward(y)
+            return y
         return bundle.bias_spmm(h, b, reduction.scaling, reduction.norm)
 
     @staticmethod
     def backward(ctx, g):
         r = ctx.reduction
-        gh = ctx.bundle.spmm(g.contiguous(), None, r.scaling, _MIRROR[r.norm], transpose=True)
-        return gh, D.col_sums(gh), None, None
+        g = g.contiguous()
+        if ctx.relu:
+            g = D.relu_grad(ctx.saved_tensors[0], g)
+        gh = ctx.bundle.spmm(g, None, r.scaling, _MIRROR[r.norm], transpose=True)
+        return gh, D.col_sums(gh), None, None, None
 
 
 class _GCNLayerFn(torch.autograd.Function):
@@ -270,18 +285,23 @@ class _GCNLayerFn(torch.autograd.Function):
     cuBLAS (fp32 accumulation, one rounding: matmul's backward, 150-155)."""
 
     @staticmethod
-    def forward(ctx, x, w, b, bundle, reduction):
-        ctx.bundle, ctx.reduction = bundle, reduction
-        ctx.save_for_backward(x, w)
-        return bundle.gcn_agg_tc(x, w, b, reduction)
+    def forward(ctx, x, w, b, bundle, reduction, relu=False):
+        ctx.bundle, ctx.reduction, ctx.relu = bundle, reduction, relu
+        y = bundle.gcn_agg_tc(x, w, b, reduction, relu=True) if relu else \
+            bundle.gcn_agg_tc(x, w, b, reduction)
+        ctx.save_for_backward(x, w, y if relu else None)
+        return y
 
     @staticmethod
     def backward(ctx, g):
-        x, w = ctx.saved_tensors
+        x, w, y = ctx.saved_tensors
         r = ctx.reduction
-        gh = ctx.bundle.spmm(g.contiguous(), None, r.scaling, _MIRROR[r.norm], transpose=True)
+        g = g.contiguous()
+        if ctx.relu:
+            g = D.relu_grad(y, g)
+        gh = ctx.bundle.spmm(g, None, r.scaling, _MIRROR[r.norm], transpose=True)
         gx = gh @ w.t() if ctx.needs_input_grad[0] else None
-        return gx, x.t() @ gh, D.col_sums(gh), None, None
+        return gx, x.t() @ gh, D.col_sums(gh), None, None, None
 
 
 def spmm_agg(bundle, x, reduction, width="half2", overflow=None, tag="agg"):
@@ -294,16 +314,22 @@ def spmm_agg(bundle, x, reduction, width="half2", overflow=None, tag="agg"):
 
 class _WeightedFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, w, x, bundle, heads):
-        ctx.bundle, ctx.heads = bundle, heads
-        ctx.save_for_backward(w, x)
+    def forward(ctx, w, x, bundle, heads, relu=False):
+        ctx.bundle, ctx.heads, ctx.relu = bundle, heads, relu
+        if relu:
+            y = bundle.spmm(x, w, "post", "none", heads=heads, relu=True)
+            ctx.save_for_backward(w, x, y)
+            return y
+        ctx.save_for_backward(w, x, None)
         return bundle.spmm(x, w, "post", "none", heads=heads)
 
     @staticmethod
     def backward(ctx, g):
-        w, x = ctx.saved_tensors
+        w, x, y = ctx.saved_tensors
         b, h = ctx.bundle, ctx.heads
         g = g.contiguous()
+        if ctx.relu:
+            g = D.relu_grad(y, g)
         gw = gx = None
         if ctx.needs_input_grad[0]:
             gw = b.sddmm(g, x, heads=h).reshape(w.shape)
@@ -312,13 +338,14 @@ class _WeightedFn(torch.autograd.Function):
             # (hg_gather_rows) costs the same random reads (measured: 5.5 ms
             # gather vs 4.4-5.3 ms saved in the SpMM on RMAT-24)
             gx = b.spmm(g, w, "post", "none", transpose=True, heads=h, weight_via_perm=True)
-        return gw, gx, None, None
+        return gw, gx, None, None, None
 
 
-def spmm_weighted(bundle, w, x, width="half2", overflow=None, tag="agg"):
-    """Y[r] = sum over edges (r, c) of w[e] * X[c] (per head when w is [E, H])."""
+def spmm_weighted(bundle, w, x, width="half2", overflow=None, tag="agg", relu=False):
+    """Y[r] = sum over edges (r, c) of w[e] * X[c] (per head when w is [E, H]);
+    relu=True (bundles with fused_relu) applies the next ReLU in the epilogue."""
     heads = 1 if w.dim() == 1 else w.shape[1]
-    y = _WeightedFn.apply(w, x, bundle, heads)
+    y = _WeightedFn.apply(w, x, bundle, heads, relu)
     if overflow is not None:
         overflow.observe(tag, y.detach())
     return y
@@ -651,18 +678,25 @@ class GCNLayer:
     def params(self):
         return self.lin.params()
 
-    def __call__(self, bundle, x, mode, width, overflow, tag):
+    fuses_relu_out = True
+
+    def __call__(self, bundle, x, mode, width, overflow, tag, relu_out=False):
+        # fused ReLU only when no overflow counters watch the pre-activation
+        fuse = relu_out and overflow is None and getattr(bundle, "fused_relu", False)
         if getattr(bundle, "fused_bias_agg", False) and self.lin.b is not None:
             w, b = self.lin.w.publish(mode), self.lin.b.publish(mode)
             if mode == "half" and w.shape[1] % 16 == 0 and x.shape[1] % 8 == 0:
                 # tensor-core GEMM with the bias / input-scale epilogue fused
-                y = _GCNLayerFn.apply(x, w, b, bundle, self.reduction)
+                y = _GCNLayerFn.apply(x, w, b, bundle, self.reduction, fuse)
             else:
-                y = _BiasAggFn.apply(matmul(x, w), b, bundle, self.reduction)
+                y = _BiasAggFn.apply(matmul(x, w), b, bundle, self.reduction, fuse)
             if overflow is not None:
                 overflow.observe(tag, y.detach())
+            if relu_out and not fuse:
+                y = relu(y)
             return y
-        return spmm_agg(bundle, self.lin(x, mode), self.reduction, width, overflow, tag)
+        y = spmm_agg(bundle, self.lin(x, mode), self.reduction, width, overflow, tag)
+        return relu(y) if relu_out else y
 
 
 class GINLayer:
@@ -718,7 +752,9 @@ class GATLayer:
     def params(self):
         return [self.w, self.a_l, self.a_r]
 
-    def __call__(self, bundle, x, mode, width, overflow, tag):
+    fuses_relu_out = True
+
+    def __call__(self, bundle, x, mode, width, overflow, tag, relu_out=False):
         h, so = self.heads, self.store_out
         z = matmul(x, self.w.publish(mode))                       # [N, H*so]
         zh = z.view(z.shape[0], h, so)
@@ -733,10 +769,13 @@ class GATLayer:
         else:
             e = attention_logits(bundle, s_l, s_r, 0.2)           # [E, H]
             alpha = edge_softmax(bundle, e, overflow, tag + "/softmax")
-        out = spmm_weighted(bundle, alpha if h > 1 else alpha[:, 0], z, width, overflow, tag)
+        fuse = (relu_out and overflow is None and not (self.reduce == "mean" and h > 1)
+                and getattr(bundle, "fused_relu", False))
+        out = spmm_weighted(bundle, alpha if h > 1 else alpha[:, 0], z, width, overflow, tag,
+                            relu=fuse)
         if self.reduce == "mean" and h > 1:
-            return _HeadMeanFn.apply(out, h)
-        return out
+            out = _HeadMeanFn.apply(out, h)
+        return relu(out) if relu_out and not fuse else out
 
 
 class _HeadDotsFn(torch.autograd.Function):
