@@ -218,12 +218,14 @@ int hg_head_dots(const void* z, const void* a_l, const void* a_r, int64_t n, int
 /* Its backward (the N x 1 by 1 x F matmul gradients of models.py:151-155):
  * gz[n, h*fh+f] = rnd(rnd(g_l[n,h] a_l[h,f]) + rnd(g_r[n,h] a_r[h,f])) and
  * ga_{l,r}[h, f] = rnd(sum_n z[n, h*fh+f] g_{l,r}[n, h]) with a deterministic
- * two-pass fp32 reduction (workspace: hg_head_dots_bwd_workspace). */
+ * two-pass fp32 reduction (workspace: hg_head_dots_bwd_workspace).  With gz_in
+ * (may alias gz) the result is accumulated: gz = rnd(gz_in + that value) -- the
+ * two gradient contributions z receives in a GAT layer, summed in one pass. */
 int hg_head_dots_bwd_workspace(int32_t heads, int32_t fh, size_t* bytes);
 int hg_head_dots_bwd(const void* z, const void* a_l, const void* a_r, const void* g_l,
                      const void* g_r, int64_t n, int32_t heads, int32_t fh, void* gz,
-                     void* ga_l, void* ga_r, int dtype, void* ws, size_t ws_bytes,
-                     void* stream);
+                     void* ga_l, void* ga_r, const void* gz_in, int dtype, void* ws,
+                     size_t ws_bytes, void* stream);
 
 /* models.Adam step (models.py:583-592) over flat fp32 arrays, the reference's
  * operation order with one fp32 rounding per op:

@@ -56,7 +56,7 @@ SIGNATURES = {
     "hg_softmax_xent": [_P, c_int, _I64, _P, _I64, _I32, c_double, c_float, _P, c_int, _P, _P],
     "hg_head_dots": [_P, _P, _P, _I64, _I32, _I32, _P, _P, c_int, _P],
     "hg_head_dots_bwd_workspace": [_I32, _I32, _PSZ],
-    "hg_head_dots_bwd": [_P, _P, _P, _P, _P, _I64, _I32, _I32, _P, _P, _P, c_int, _P, c_size_t,
+    "hg_head_dots_bwd": [_P, _P, _P, _P, _P, _I64, _I32, _I32, _P, _P, _P, _P, c_int, _P, c_size_t,
                          _P],
     "hg_gemm_tc": [_P, _I64, _I64, _I64, _P, _I32, _I64, _P, _P, _I32, _P, _I64, _P],
     "hg_count_lines_workspace": [_I64, _PSZ],

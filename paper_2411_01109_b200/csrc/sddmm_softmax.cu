@@ -1261,7 +1261,7 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 k_head_dots_bwd(const T* __restrict__ z, const T* __restrict__ al, const T* __restrict__ ar,
                 const T* __restrict__ gl, const T* __restrict__ gr, int64_t n, int heads, int fh,
-                T* __restrict__ gz, float* __restrict__ part) {
+                T* gz, const T* gz_in, float* __restrict__ part) {
   using N = Num<T>;
   const int F = heads * fh;
   const int rpi = F >= 256 ? 1 : 256 / F;
@@ -1276,7 +1276,8 @@ k_head_dots_bwd(const T* __restrict__ z, const T* __restrict__ al, const T* __re
       for (int64_t r = (int64_t)blockIdx.x * rpi + rr; r < n; r += (int64_t)gridDim.x * rpi) {
         const T g1 = gl[r * heads + h], g2 = gr[r * heads + h];
         const float zf = N::to_f(z[r * F + f]);
-        gz[r * F + f] = N::add(N::mul(g1, a1), N::mul(g2, a2));
+        const T v = N::add(N::mul(g1, a1), N::mul(g2, a2));
+        gz[r * F + f] = gz_in ? N::add(gz_in[r * F + f], v) : v;
         sl = fmaf(zf, N::to_f(g1), sl);
         sr = fmaf(zf, N::to_f(g2), sr);
       }
@@ -1306,7 +1307,7 @@ __global__ void __launch_bounds__(256)
 k_head_dots_bwd_v8(const __half* __restrict__ z, const __half* __restrict__ al,
                    const __half* __restrict__ ar, const __half* __restrict__ gl,
                    const __half* __restrict__ gr, int64_t n, int heads, int fh,
-                   __half* __restrict__ gz, float* __restrict__ part) {
+                   __half* gz, const __half* gz_in, float* __restrict__ part) {
   extern __shared__ float hdb_sh[];  // [2][rpi][F]
   const int F = heads * fh, C = F / 8;
   const int rpi = 256 / C;
@@ -1326,9 +1327,13 @@ k_head_dots_bwd_v8(const __half* __restrict__ z, const __half* __restrict__ al,
       const uint4 zv = *reinterpret_cast<const uint4*>(z + r * F + c * 8);
       const __half* ze = reinterpret_cast<const __half*>(&zv);
       __align__(16) __half o[8];
+      uint4 prev = make_uint4(0, 0, 0, 0);
+      if (gz_in) prev = *reinterpret_cast<const uint4*>(gz_in + r * F + c * 8);
+      const __half* pe = reinterpret_cast<const __half*>(&prev);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         o[i] = __hadd_rn(__hmul_rn(g1, a1[i]), __hmul_rn(g2, a2[i]));
+        if (gz_in) o[i] = __hadd_rn(pe[i], o[i]);
         const float zf = __half2float(ze[i]);
         sl[i] = fmaf(zf, g1f, sl[i]);
         sr[i] = fmaf(zf, g2f, sr[i]);
@@ -1454,8 +1459,8 @@ extern "C" int hg_head_dots_bwd_workspace(int32_t heads, int32_t fh, size_t* byt
 
 extern "C" int hg_head_dots_bwd(const void* z, const void* a_l, const void* a_r, const void* g_l,
                                 const void* g_r, int64_t n, int32_t heads, int32_t fh, void* gz,
-                                void* ga_l, void* ga_r, int dtype, void* ws, size_t ws_bytes,
-                                void* stream) {
+                                void* ga_l, void* ga_r, const void* gz_in, int dtype, void* ws,
+                                size_t ws_bytes, void* stream) {
   HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
   HG_REQUIRE(heads >= 1 && fh >= 1, "hg_head_dots_bwd: bad shape");
   const int F = heads * fh;
@@ -1472,18 +1477,18 @@ extern "C" int hg_head_dots_bwd(const void* z, const void* a_l, const void* a_r,
         HG_CUDA(cudaFuncSetAttribute(k_head_dots_bwd_v8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
       k_head_dots_bwd_v8<<<kHdbBlocks, 256, sh, st>>>(
           (const __half*)z, (const __half*)a_l, (const __half*)a_r, (const __half*)g_l,
-          (const __half*)g_r, n, heads, fh, (__half*)gz, part);
+          (const __half*)g_r, n, heads, fh, (__half*)gz, (const __half*)gz_in, part);
     } else {
       k_head_dots_bwd<__half><<<kHdbBlocks, 256, 0, st>>>(
           (const __half*)z, (const __half*)a_l, (const __half*)a_r, (const __half*)g_l,
-          (const __half*)g_r, n, heads, fh, (__half*)gz, part);
+          (const __half*)g_r, n, heads, fh, (__half*)gz, (const __half*)gz_in, part);
     }
     k_head_dots_bwd_fold<__half><<<(F + 255) / 256, 256, 0, st>>>(part, kHdbBlocks, F,
                                                                 (__half*)ga_l, (__half*)ga_r);
   } else {
     k_head_dots_bwd<float><<<kHdbBlocks, 256, 0, st>>>(
         (const float*)z, (const float*)a_l, (const float*)a_r, (const float*)g_l,
-        (const float*)g_r, n, heads, fh, (float*)gz, part);
+        (const float*)g_r, n, heads, fh, (float*)gz, (const float*)gz_in, part);
     k_head_dots_bwd_fold<float><<<(F + 255) / 256, 256, 0, st>>>(part, kHdbBlocks, F,
                                                                (float*)ga_l, (float*)ga_r);
   }

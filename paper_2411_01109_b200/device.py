@@ -799,17 +799,18 @@ def adam_step(master, m, v, grad, lr, b1, b2, eps, step, grad_unscale=1.0):
     Probe.launches += 1
 
 
-def head_dots_bwd(z, a_l, a_r, g_l, g_r, heads):
-    """Backward of head_dots: (gz, ga_l, ga_r), deterministic (hg_head_dots_bwd)."""
+def head_dots_bwd(z, a_l, a_r, g_l, g_r, heads, gz_acc=None):
+    """Backward of head_dots: (gz, ga_l, ga_r), deterministic (hg_head_dots_bwd).
+    gz_acc: an existing gradient of z to accumulate into (in place)."""
     z = z.contiguous()
     n = z.shape[0]
     fh = z.shape[1] // heads
-    gz = torch.empty_like(z)
+    gz = torch.empty_like(z) if gz_acc is None else gz_acc
     ga_l = torch.empty_like(a_l)
     ga_r = torch.empty_like(a_r)
     ws = workspace(nat.size_query("hg_head_dots_bwd_workspace", heads, fh), z.device)
     nat.call("hg_head_dots_bwd", _p(z), _p(a_l.contiguous()), _p(a_r.contiguous()),
              _p(g_l.contiguous()), _p(g_r.contiguous()), n, heads, fh, _p(gz), _p(ga_l),
-             _p(ga_r), _dtype_code(z), _p(ws), ws.numel(), _stream())
+             _p(ga_r), _p(gz_acc), _dtype_code(z), _p(ws), ws.numel(), _stream())
     Probe.launches += 2
     return gz, ga_l, ga_r

@@ -757,8 +757,14 @@ class GATLayer:
     def __call__(self, bundle, x, mode, width, overflow, tag, relu_out=False):
         h, so = self.heads, self.store_out
         z = matmul(x, self.w.publish(mode))                       # [N, H*so]
-        zh = z.view(z.shape[0], h, so)
         a_l, a_r = self.a_l.publish(mode), self.a_r.publish(mode)
+        mean = self.reduce == "mean" and h > 1
+        if (overflow is None and isinstance(bundle, GraphBundle) and bundle.fused_gat):
+            fuse = relu_out and not mean
+            out = _GATCoreFn.apply(z, a_l, a_r, bundle, h, fuse)
+            if mean:
+                out = _HeadMeanFn.apply(out, h)
+            return relu(out) if relu_out and not fuse else out
         # s = z_h . a_h for every head (models.matmul semantics: fp32
         # accumulation of exact products, one rounding), one kernel
         s_l, s_r = _HeadDotsFn.apply(z, a_l, a_r, h, bundle)
@@ -776,6 +782,40 @@ class GATLayer:
         if self.reduce == "mean" and h > 1:
             out = _HeadMeanFn.apply(out, h)
         return relu(out) if relu_out and not fuse else out
+
+
+class _GATCoreFn(torch.autograd.Function):
+    """The multi-head GAT layer core (models.py:492-509) after z = x W as one
+    autograd node, for single-GPU fast numerics: head dots s = z a -> fused
+    attention (scores + leaky + softmax, fp32-guarded) -> weighted aggregation
+    [-> the next ReLU].  Backward: SDDMM for d alpha, transposed weighted SpMM
+    for dz, attention backward with row/column sums, then the head-dot
+    backward accumulates its dz contribution into the SpMM's in the same pass
+    (no separate add of the two N x H*F gradients)."""
+
+    @staticmethod
+    def forward(ctx, z, a_l, a_r, bundle, heads, relu):
+        s_l, s_r = bundle.head_dots(z, a_l, a_r, heads)
+        alpha = bundle.gat_attention(s_l, s_r, 0.2)
+        w = alpha if heads > 1 else alpha[:, 0]
+        out = bundle.spmm(z, w, "post", "none", heads=heads, relu=relu)
+        ctx.bundle, ctx.heads, ctx.relu = bundle, heads, relu
+        ctx.save_for_backward(z, a_l, a_r, s_l, s_r, alpha, out if relu else None)
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        z, a_l, a_r, s_l, s_r, alpha, y = ctx.saved_tensors
+        b, h = ctx.bundle, ctx.heads
+        g = g.contiguous()
+        if ctx.relu:
+            g = D.relu_grad(y, g)
+        w = alpha if h > 1 else alpha[:, 0]
+        dalpha = b.sddmm(g, z, heads=h).reshape(alpha.shape)
+        gz = b.spmm(g, w, "post", "none", transpose=True, heads=h, weight_via_perm=True)
+        ds_l, ds_r = b.gat_attention_bwd(s_l, s_r, alpha, dalpha, 0.2)
+        gz, ga_l, ga_r = D.head_dots_bwd(z, a_l, a_r, ds_l, ds_r, h, gz_acc=gz.contiguous())
+        return gz, ga_l, ga_r, None, None, None
 
 
 class _HeadDotsFn(torch.autograd.Function):
