@@ -494,3 +494,29 @@ def test_gcn_large_graph_tracks_torch_fp32_with_grad_scale(cuda):
     l1 = [float(t1.step()[0]) for _ in range(2)]
     assert l1[0] == got[0]
     assert abs(l1[1] - want[1]) > abs(got[1] - want[1])
+
+
+def test_gat_core_fused_matches_composed(cuda):
+    """The single-node GAT core (_GATCoreFn, ReLU fused) against the composed
+    ops (taken when overflow counters watch): same outputs and gradients up to
+    fp16 rounding order."""
+    from paper_2411_01109_b200 import graphgen, models as M
+    from paper_2411_01109_b200.device import DeviceGraph
+
+    rows, cols, feats, labels = graphgen.synth_sbm(400, 3, 0.05, 0.005, 24, 7)
+    dg = DeviceGraph.from_edges(400, rows, cols)
+    b = M.GraphBundle.build(dg)
+    rng = np.random.default_rng(0)
+    layer = M.GATLayer(rng, 24, 8, heads=4, store_in=24, store_out=8)
+    x = torch.from_numpy(feats).cuda().half()
+    outs, grads = [], []
+    for ov in (None, M.OverflowCounters()):
+        for p in layer.params():
+            p.published = None
+        y = layer(b, x, "half", "half2", ov, "gat", relu_out=True)
+        (y.float() * torch.linspace(-1, 1, y.numel(), device=cuda).view_as(y)).sum().backward()
+        outs.append(y.detach().float())
+        grads.append([p.published.grad.float().clone() for p in layer.params()])
+    assert torch.allclose(outs[0], outs[1], atol=2e-3, rtol=2e-3)
+    for g0, g1 in zip(*grads):
+        assert torch.allclose(g0, g1, atol=2e-2, rtol=2e-2)
