@@ -349,8 +349,15 @@ def b200_arm(args, ws, rank, local):
 
     torch.cuda.set_device(local)
     dist = None
-    if ws > 1:
+    # HG_FORCE_DIST=1: the partitioned trainer even at N=1 (a one-rank NCCL group:
+    # validates the N>1 code path, graph capture of its collectives included)
+    use_dist = ws > 1 or os.environ.get("HG_FORCE_DIST") == "1"
+    if use_dist:
         import torch.distributed as dist
+
+        for k, v in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29531"), ("RANK", "0"),
+                     ("WORLD_SIZE", "1")):
+            os.environ.setdefault(k, v)
 
         backend = os.environ.get("HG_DIST_BACKEND", "nccl")
         if backend == "nccl":
@@ -362,7 +369,7 @@ def b200_arm(args, ws, rank, local):
     dg, x, labels = build_workload(args.workload, args.seed)
     cfg = TrainConfig(mode="half", seed=args.seed, scaling="discretized", norm="both",
                       numerics="fast", grad_scale="auto", **WORKLOADS[args.workload]["cfg"])
-    if ws > 1:
+    if use_dist:
         from paper_2411_01109_b200.partition import DistTrainer
 
         tr = DistTrainer(dg, x, labels, cfg, dist)
@@ -406,24 +413,30 @@ def b200_arm(args, ws, rank, local):
     D.Probe.reset(timing=False)
 
     # ---- device-resident timing (value): the step replayed as a CUDA graph ----
-    graphed = ws == 1 and not args.no_graph
+    graphed = not args.no_graph and (not use_dist or dist.get_backend() == "nccl")
     if graphed:
-        tr.capture()
-        tr.step()
-        torch.cuda.synchronize()
+        try:
+            tr.capture()
+            tr.step()
+            torch.cuda.synchronize()
+        except Exception as exc:  # a capture failure must not lose the measurement
+            print(f"[bench] CUDA graph capture failed, timing eager steps: {exc}",
+                  file=sys.stderr, flush=True)
+            tr._graph = None
+            graphed = False
     t_ms, loss = timed_steps(args.steps)
     clocks.__exit__(None, None, None)
     final_loss = float(loss)
 
     # ---- end to end through the public loop: host features in, loss out ----
-    inner = tr.inner if ws > 1 else tr
-    lo, hi = (tr.part.lo, tr.part.hi) if ws > 1 else (0, dg.n)
+    inner = tr.inner if use_dist else tr
+    lo, hi = (tr.part.lo, tr.part.hi) if use_dist else (0, dg.n)
     host_x = inner.host_features(x[lo:hi].cpu())
     h2d = host_x.numel() * host_x.element_size()
     barrier()
     torch.cuda.synchronize()
     e0 = time.perf_counter()
-    if ws > 1:
+    if use_dist:
         for _ in range(args.steps):
             inner.x.copy_(host_x, non_blocking=True)
             loss, _ = tr.step()
@@ -459,7 +472,7 @@ def b200_arm(args, ws, rank, local):
                          "peak_source": peak_kind,
                          "bytes_model": "4E+8(N+1)+2FE+2FN per SpMM launch, F = stored width"},
             "final_loss": round(final_loss, 5),
-            "grad_scale": (tr.inner if ws > 1 else tr).grad_scale,
+            "grad_scale": (tr.inner if use_dist else tr).grad_scale,
             "setup_s": round(setup_s, 1),
         }
     if not args.no_sweep and ws == 1 and args.workload == "gcn-reddit":

@@ -351,6 +351,8 @@ class DistTrainer:
                                  lambda k, side, dt: dg.factor(k, side, dt), ops)
         self.inner = Trainer(self.bundle, features, labels, config, row_slice=(part.lo, part.hi))
         self.n_total = dg.n
+        self._graph = None
+        self._graph_out = None
 
     @property
     def x(self):
@@ -361,6 +363,24 @@ class DistTrainer:
         return self.inner.load_features(feats[lo:hi], out=self.inner.x)
 
     def step(self, overflow=None):
+        if self._graph is not None and overflow is None:
+            self._graph.replay()
+            return self._graph_out
+        return self._step_eager(overflow)
+
+    def capture(self):
+        """Record one step -- exchanges (NCCL all-gathers / all-reduces) included
+        -- as a CUDA graph; later step() calls replay it.  Call after an eager
+        step.  Needs an NCCL group (gloo's host staging cannot be captured)."""
+        if self.dist.get_backend() != "nccl":
+            raise RuntimeError("graph capture of the partitioned step needs the NCCL backend")
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            out = self._step_eager()
+        self._graph, self._graph_out = graph, out
+        return graph
+
+    def _step_eager(self, overflow=None):
         tr = self.inner
         cfg = tr.cfg
         tr.group.publish()
