@@ -82,3 +82,46 @@ def test_partitioned_cuda_step_matches_one_rank(cuda, kind):
         np.testing.assert_allclose(p1[0][3], np.concatenate([p[3] for p in pw]), rtol=0,
                                    atol=5e-3, err_msg=kind)
         np.testing.assert_allclose(l1, lw, rtol=1e-4, err_msg=kind)
+
+
+def _run_nccl_graph(port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        from paper_2411_01109_b200 import graphgen
+        from paper_2411_01109_b200.models import TrainConfig
+        from paper_2411_01109_b200.partition import DistTrainer
+
+        dg = graphgen.reddit_like(5, n=4000, e=300_000)
+        x, labels = graphgen.planted_features(dg.n, 40, 5, 5, "cuda")
+        res = {}
+        for kind in ("gcn", "gat", "gin"):
+            extra = {"heads": 2} if kind == "gat" else {}
+            cfg = TrainConfig(kind=kind, mode="half", hidden=16, seed=3, grad_scale="auto", **extra)
+            a = DistTrainer(dg, x, labels, cfg, dist)
+            b = DistTrainer(dg, x, labels, cfg, dist)
+            la = [float(a.step()[0]) for _ in range(5)]
+            lb = [float(b.step()[0])]
+            b.capture()
+            lb += [float(b.step()[0]) for _ in range(4)]
+            res[kind] = (la, lb)
+        out_q.put(res)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+def test_partitioned_step_cuda_graph_with_nccl(cuda):
+    """The partitioned step (NCCL all-gathers / all-reduces inside) captured as
+    a CUDA graph replays to the same losses as eager steps (one-rank NCCL
+    group: the capture path bench.py takes at N > 1)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_run_nccl_graph, args=(_free_port(), q))
+    p.start()
+    res = q.get(timeout=500)
+    p.join(timeout=120)
+    assert p.exitcode == 0
+    for kind, (la, lb) in res.items():
+        np.testing.assert_allclose(la, lb, rtol=0, atol=1e-6, err_msg=kind)
