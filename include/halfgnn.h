@@ -105,16 +105,21 @@ int hg_schedule_build(const int64_t* offsets, int64_t n, int32_t split_cap, int3
  * apart (0 = F): a narrower F can run over wider (padded) storage, e.g. 48
  * classes in 64-wide rows whose 128-byte lines never straddle; in_scale needs
  * ldx == F.  relu != 0 applies models.relu to each output (the next layer's
- * activation fused into the aggregation's epilogue). */
+ * activation fused into the aggregation's epilogue).  Edge e's weights are
+ * w[idx(e) * w_ld + head] (w_ld 0 = heads).  out2 != NULL additionally writes
+ * out2[r, h] = rnd(sum_e w[idx(e) * w_ld + w2_off + h]) (fp32 sum, same row
+ * ownership): the GAT backward's column sums of d_e read from the same
+ * interleaved (alpha, d_e) rows as the transposed aggregation's weights
+ * (models.py:309-311, 335-337); needs F/8 <= 32 lanes of whole-vector heads. */
 int hg_spmm_workspace(int64_t n_cols, int32_t F, int64_t num_slots, int has_in_scale,
-                      int dtype, size_t* bytes);
+                      int32_t sum_heads, int dtype, size_t* bytes);
 int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_rows, int64_t n_cols,
             int64_t num_edges, const int32_t* units, int64_t num_units,
             const int32_t* split_rows, int64_t num_split_rows, int64_t num_slots,
             const void* w, const int32_t* w_index, int32_t heads, const void* x, void* y,
             int32_t F, int64_t ldx, int64_t ldy, int32_t scaling, int32_t relu,
-            const void* in_scale, const void* out_factor, int dtype, void* ws, size_t ws_bytes,
-            void* stream);
+            const void* in_scale, const void* out_factor, int64_t w_ld, int32_t w2_off,
+            void* out2, int dtype, void* ws, size_t ws_bytes, void* stream);
 
 /* Reference-order SpMM, bit-exact with halfsparse _spmm_edge_parallel
  * (kernels.py:328-391; order spelled out in _ref_spmm_edge, kernels.py:603-688):
@@ -281,21 +286,24 @@ int hg_parse_edges(const void* text, int64_t nbytes, int64_t n_lines, int64_t* r
 
 /* attention_scores + leaky_relu + edge_softmax (models.py:188-200, 317-326,
  * 382-401) in one pass: alpha[e, h] = rnd(exp(l_e - m) / sum exp(l - m)) with
- * l_e = leaky(s_l[r, h] + s_r[c, h]) in fp32 (slope), fp32 online max/sum. */
+ * l_e = leaky(s_l[r, h] + s_r[c, h]) in fp32 (slope), fp32 online max/sum.
+ * alpha rows are alpha_ld elements apart (0 = heads; 2*heads for interleaved
+ * (alpha | d_e) rows that the fused transposed aggregation reads). */
 int hg_gat_attention_fwd(const int64_t* offsets, const int32_t* cols, int64_t n_rows,
                          const void* s_l, const void* s_r, int32_t heads, float slope,
-                         void* alpha, const int32_t* medium_rows, int64_t n_medium,
-                         const int32_t* long_rows, int64_t n_long, int32_t short_max,
-                         int dtype, void* stream);
+                         void* alpha, int64_t alpha_ld, const int32_t* medium_rows,
+                         int64_t n_medium, const int32_t* long_rows, int64_t n_long,
+                         int32_t short_max, int dtype, void* stream);
 
 /* Backward of the above (models.py:188-200, 329-333, 403-410): per row,
  * D = sum alpha*dalpha (fp32); de[e, h] = rnd(alpha (dalpha - D) * leaky'(l_e));
- * ds_l[r, h] = rnd(sum_e of the unrounded de).  The column sums (ds_r) follow
- * with hg_edge_sums_fast over the CSC and perm. */
+ * ds_l[r, h] = rnd(sum_e of the unrounded de).  alpha and de rows are ae_ld
+ * elements apart (0 = heads), dalpha is dense.  The column sums (ds_r) follow
+ * with hg_edge_sums_fast over the CSC and perm, or inside hg_spmm (out2). */
 int hg_gat_attention_bwd(const int64_t* offsets, const int32_t* cols, int64_t n_rows,
                          const void* s_l, const void* s_r, int32_t heads, float slope,
-                         const void* alpha, const void* dalpha, void* de, void* ds_l,
-                         const int32_t* medium_rows, int64_t n_medium,
+                         const void* alpha, const void* dalpha, void* de, int64_t ae_ld,
+                         void* ds_l, const int32_t* medium_rows, int64_t n_medium,
                          const int32_t* long_rows, int64_t n_long, int32_t short_max,
                          int dtype, void* stream);
 

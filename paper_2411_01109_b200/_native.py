@@ -37,9 +37,9 @@ SIGNATURES = {
     "hg_degree_factors": [_P, _I64, c_int, c_int, _P, _P],
     "hg_schedule_workspace": [_I64, _I64, _I32, _PSZ],
     "hg_schedule_build": [_P, _I64, _I32, _P, _I64, _P, _I64, _PI64, _P, c_size_t, _P],
-    "hg_spmm_workspace": [_I64, _I32, _I64, c_int, c_int, _PSZ],
+    "hg_spmm_workspace": [_I64, _I32, _I64, c_int, _I32, c_int, _PSZ],
     "hg_spmm": [_P, _P, _I64, _I64, _I64, _P, _I64, _P, _I64, _I64, _P, _P, _I32, _P, _P,
-                _I32, _I64, _I64, _I32, _I32, _P, _P, c_int, _P, c_size_t, _P],
+                _I32, _I64, _I64, _I32, _I32, _P, _P, _I64, _I32, _P, c_int, _P, c_size_t, _P],
     "hg_spmm_edge_ref_workspace": [_I64, _I64, _I32, _I32, _I32, c_int, c_int, _PSZ],
     "hg_spmm_edge_ref": [_P, _P, _I64, _I64, _I64, _I32, _I32, _P, _P, _P, _I32, _I32, _P, _P,
                          _P, _P, c_int, _P, c_size_t, _P],
@@ -63,10 +63,10 @@ SIGNATURES = {
     "hg_count_lines": [_P, _I64, _PI64, _P, c_size_t, _P],
     "hg_parse_edges_workspace": [_I64, _I64, _PSZ],
     "hg_parse_edges": [_P, _I64, _I64, _P, _P, _PI64, _P, c_size_t, _P],
-    "hg_gat_attention_fwd": [_P, _P, _I64, _P, _P, _I32, c_float, _P, _P, _I64, _P, _I64, _I32,
-                             c_int, _P],
-    "hg_gat_attention_bwd": [_P, _P, _I64, _P, _P, _I32, c_float, _P, _P, _P, _P, _P, _I64, _P,
-                             _I64, _I32, c_int, _P],
+    "hg_gat_attention_fwd": [_P, _P, _I64, _P, _P, _I32, c_float, _P, _I64, _P, _I64, _P, _I64,
+                             _I32, c_int, _P],
+    "hg_gat_attention_bwd": [_P, _P, _I64, _P, _P, _I32, c_float, _P, _P, _P, _I64, _P, _P, _I64,
+                             _P, _I64, _I32, c_int, _P],
     "hg_edge_sums_fast": [_P, _I64, _P, _P, _I32, _P, _P, _I64, _P, _I64, _I32, c_int, _P],
     "hg_head_mean": [_P, _I64, _I32, _I32, _P, c_int, _P],
     "hg_head_mean_bwd": [_P, _I64, _I32, _I32, _P, c_int, _P],

@@ -89,7 +89,7 @@ template <typename T, int H>
 __device__ __forceinline__ void fwd_pass2(const int32_t* __restrict__ cols, const T* __restrict__ sr,
                                           int64_t first, int64_t end, int64_t step, int h,
                                           float a, float slope, float m, float inv,
-                                          T* __restrict__ alpha) {
+                                          T* __restrict__ alpha, int ald) {
   for (int64_t e0 = first; e0 < end; e0 += step * U) {
     int c[U];
 #pragma unroll
@@ -101,21 +101,21 @@ __device__ __forceinline__ void fwd_pass2(const int32_t* __restrict__ cols, cons
                        : 0.0f;
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (c[u] >= 0) alpha[(e0 + u * step) * H + h] = Num<T>::from_f(exp2f(v[u] - m) * inv);
+      if (c[u] >= 0) alpha[(e0 + u * step) * ald + h] = Num<T>::from_f(exp2f(v[u] - m) * inv);
   }
 }
 
 // D = sum alpha * dalpha over the visited edges
 template <typename T, int H>
 __device__ __forceinline__ float bwd_pass1(const T* __restrict__ alpha, const T* __restrict__ dalpha,
-                                           int64_t first, int64_t end, int64_t step, int h) {
+                                           int64_t first, int64_t end, int64_t step, int h, int ald) {
   float d = 0.0f;
   for (int64_t e0 = first; e0 < end; e0 += step * U) {
     float x[U], y[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t e = e0 + u * step;
-      x[u] = e < end ? Num<T>::to_f(alpha[e * H + h]) : 0.0f;
+      x[u] = e < end ? Num<T>::to_f(alpha[e * ald + h]) : 0.0f;
       y[u] = e < end ? Num<T>::to_f(dalpha[e * H + h]) : 0.0f;
     }
 #pragma unroll
@@ -129,7 +129,7 @@ template <typename T, int H>
 __device__ __forceinline__ float bwd_pass2(const int32_t* __restrict__ cols, const T* __restrict__ sr,
                                            const T* __restrict__ alpha, const T* __restrict__ dalpha,
                                            int64_t first, int64_t end, int64_t step, int h, float a,
-                                           float slope, float d, T* __restrict__ de) {
+                                           float slope, float d, T* __restrict__ de, int ald) {
   float acc = 0.0f;
   for (int64_t e0 = first; e0 < end; e0 += step * U) {
     int c[U];
@@ -140,7 +140,7 @@ __device__ __forceinline__ float bwd_pass2(const int32_t* __restrict__ cols, con
     for (int u = 0; u < U; ++u) {
       const int64_t e = e0 + u * step;
       sv[u] = c[u] >= 0 ? Num<T>::to_f(sr[(size_t)(unsigned)c[u] * H + h]) : 0.0f;
-      x[u] = c[u] >= 0 ? Num<T>::to_f(alpha[e * H + h]) : 0.0f;
+      x[u] = c[u] >= 0 ? Num<T>::to_f(alpha[e * ald + h]) : 0.0f;
       y[u] = c[u] >= 0 ? Num<T>::to_f(dalpha[e * H + h]) : 0.0f;
     }
 #pragma unroll
@@ -148,7 +148,7 @@ __device__ __forceinline__ float bwd_pass2(const int32_t* __restrict__ cols, con
       if (c[u] >= 0) {
         float g = x[u] * (y[u] - d);
         g = a + sv[u] > 0.0f ? g : g * slope;
-        de[(e0 + u * step) * H + h] = Num<T>::from_f(g);
+        de[(e0 + u * step) * ald + h] = Num<T>::from_f(g);
         acc += g;
       }
     }
@@ -182,7 +182,7 @@ template <typename T, int H>
 __device__ __forceinline__ void
 d_gat_fwd_thread(int64_t blk, int64_t nblk, const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
                  int64_t n_rows, const T* __restrict__ sl, const T* __restrict__ sr, float slope,
-                 T* __restrict__ alpha, int short_max) {
+                 T* __restrict__ alpha, int short_max, int ald) {
   const int64_t t = blk * (int64_t)blockDim.x + threadIdx.x;
   if (t >= n_rows * H) return;
   const int64_t r = t / H;
@@ -192,14 +192,14 @@ d_gat_fwd_thread(int64_t blk, int64_t nblk, const int64_t* __restrict__ offsets,
   const float a = Num<T>::to_f(sl[t]) * kLog2e;  // log2 domain
   float m = -INFINITY, s = 0.0f;
   fwd_pass1<T, H>(cols, sr, beg, end, 1, h, a, slope, m, s);
-  fwd_pass2<T, H>(cols, sr, beg, end, 1, h, a, slope, m, 1.0f / s, alpha);
+  fwd_pass2<T, H>(cols, sr, beg, end, 1, h, a, slope, m, 1.0f / s, alpha, ald);
 }
 
 template <typename T, int H>
 __device__ __forceinline__ void
 d_gat_fwd_warp(int64_t blk, int64_t nblk, const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
                const int32_t* __restrict__ rows, int64_t n_list, const T* __restrict__ sl,
-               const T* __restrict__ sr, float slope, T* __restrict__ alpha) {
+               const T* __restrict__ sr, float slope, T* __restrict__ alpha, int ald) {
   constexpr int EPB = 32 / H;
   const int lane = threadIdx.x & 31, j = lane / H, h = lane % H;
   const int64_t nwarps = (int64_t)nblk * (blockDim.x >> 5);
@@ -211,7 +211,7 @@ d_gat_fwd_warp(int64_t blk, int64_t nblk, const int64_t* __restrict__ offsets, c
     float m = -INFINITY, s = 0.0f;
     fwd_pass1<T, H>(cols, sr, beg + j, end, EPB, h, a, slope, m, s);
     ms_warp<H>(m, s);
-    fwd_pass2<T, H>(cols, sr, beg + j, end, EPB, h, a, slope, m, 1.0f / s, alpha);
+    fwd_pass2<T, H>(cols, sr, beg + j, end, EPB, h, a, slope, m, 1.0f / s, alpha, ald);
   }
 }
 
@@ -219,7 +219,7 @@ template <typename T, int H>
 __device__ __forceinline__ void
 d_gat_fwd_cta(int64_t blk, int64_t nblk, const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
               const int32_t* __restrict__ rows, const T* __restrict__ sl,
-              const T* __restrict__ sr, float slope, T* __restrict__ alpha) {
+              const T* __restrict__ sr, float slope, T* __restrict__ alpha, int ald) {
   constexpr int EPB = 256 / H;
   __shared__ float sm[8][H], ss[8][H];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, j = tid / H, h = tid % H;
@@ -234,7 +234,7 @@ d_gat_fwd_cta(int64_t blk, int64_t nblk, const int64_t* __restrict__ offsets, co
   float mt = sm[0][h], st = ss[0][h];
 #pragma unroll
   for (int k = 1; k < 8; ++k) ms_merge(mt, st, sm[k][h], ss[k][h]);
-  fwd_pass2<T, H>(cols, sr, beg + j, end, EPB, h, a, slope, mt, 1.0f / st, alpha);
+  fwd_pass2<T, H>(cols, sr, beg + j, end, EPB, h, a, slope, mt, 1.0f / st, alpha, ald);
 }
 
 // --------------------------------------------------------------- backward
@@ -244,16 +244,16 @@ __device__ __forceinline__ void
 d_gat_bwd_thread(int64_t blk, int64_t nblk, const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
                  int64_t n_rows, const T* __restrict__ sl, const T* __restrict__ sr, float slope,
                  const T* __restrict__ alpha, const T* __restrict__ dalpha, T* __restrict__ de,
-                 T* __restrict__ dsl, int short_max) {
+                 T* __restrict__ dsl, int short_max, int ald) {
   const int64_t t = blk * (int64_t)blockDim.x + threadIdx.x;
   if (t >= n_rows * H) return;
   const int64_t r = t / H;
   const int h = (int)(t - r * H);
   const int64_t beg = offsets[r], end = offsets[r + 1];
   if (end - beg > short_max) return;
-  const float d = bwd_pass1<T, H>(alpha, dalpha, beg, end, 1, h);
+  const float d = bwd_pass1<T, H>(alpha, dalpha, beg, end, 1, h, ald);
   const float a = Num<T>::to_f(sl[t]);
-  dsl[t] = Num<T>::from_f(bwd_pass2<T, H>(cols, sr, alpha, dalpha, beg, end, 1, h, a, slope, d, de));
+  dsl[t] = Num<T>::from_f(bwd_pass2<T, H>(cols, sr, alpha, dalpha, beg, end, 1, h, a, slope, d, de, ald));
 }
 
 template <typename T, int H>
@@ -261,7 +261,7 @@ __device__ __forceinline__ void
 d_gat_bwd_warp(int64_t blk, int64_t nblk, const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
                const int32_t* __restrict__ rows, int64_t n_list, const T* __restrict__ sl,
                const T* __restrict__ sr, float slope, const T* __restrict__ alpha,
-               const T* __restrict__ dalpha, T* __restrict__ de, T* __restrict__ dsl) {
+               const T* __restrict__ dalpha, T* __restrict__ de, T* __restrict__ dsl, int ald) {
   constexpr int EPB = 32 / H;
   const int lane = threadIdx.x & 31, j = lane / H, h = lane % H;
   const int64_t nwarps = (int64_t)nblk * (blockDim.x >> 5);
@@ -269,10 +269,10 @@ d_gat_bwd_warp(int64_t blk, int64_t nblk, const int64_t* __restrict__ offsets, c
        w += nwarps) {
     const int64_t r = rows[w];
     const int64_t beg = offsets[r], end = offsets[r + 1];
-    const float d = sum_warp<H>(bwd_pass1<T, H>(alpha, dalpha, beg + j, end, EPB, h));
+    const float d = sum_warp<H>(bwd_pass1<T, H>(alpha, dalpha, beg + j, end, EPB, h, ald));
     const float a = Num<T>::to_f(sl[r * H + h]);
     const float acc = sum_warp<H>(
-        bwd_pass2<T, H>(cols, sr, alpha, dalpha, beg + j, end, EPB, h, a, slope, d, de));
+        bwd_pass2<T, H>(cols, sr, alpha, dalpha, beg + j, end, EPB, h, a, slope, d, de, ald));
     if (lane < H) dsl[r * H + lane] = Num<T>::from_f(acc);
   }
 }
@@ -295,16 +295,16 @@ __device__ __forceinline__ void
 d_gat_bwd_cta(int64_t blk, int64_t nblk, const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
               const int32_t* __restrict__ rows, const T* __restrict__ sl,
               const T* __restrict__ sr, float slope, const T* __restrict__ alpha,
-              const T* __restrict__ dalpha, T* __restrict__ de, T* __restrict__ dsl) {
+              const T* __restrict__ dalpha, T* __restrict__ de, T* __restrict__ dsl, int ald) {
   constexpr int EPB = 256 / H;
   __shared__ float red[8][H];
   const int tid = threadIdx.x, j = tid / H, h = tid % H;
   const int64_t r = rows[blk];
   const int64_t beg = offsets[r], end = offsets[r + 1];
-  const float d = block_sum_h<H>(bwd_pass1<T, H>(alpha, dalpha, beg + j, end, EPB, h), red);
+  const float d = block_sum_h<H>(bwd_pass1<T, H>(alpha, dalpha, beg + j, end, EPB, h, ald), red);
   const float a = Num<T>::to_f(sl[r * H + h]);
   const float acc = block_sum_h<H>(
-      bwd_pass2<T, H>(cols, sr, alpha, dalpha, beg + j, end, EPB, h, a, slope, d, de), red);
+      bwd_pass2<T, H>(cols, sr, alpha, dalpha, beg + j, end, EPB, h, a, slope, d, de, ald), red);
   if (tid < H) dsl[r * H + tid] = Num<T>::from_f(acc);
 }
 
@@ -364,14 +364,16 @@ k_gat_fwd_all(const int64_t* __restrict__ offsets, const int32_t* __restrict__ c
               int64_t n_rows, const int32_t* __restrict__ medium, int64_t n_medium,
               const int32_t* __restrict__ longr, int64_t n_long, int64_t b_med,
               const T* __restrict__ sl, const T* __restrict__ sr, float slope,
-              T* __restrict__ alpha, int short_max) {
+              T* __restrict__ alpha, int short_max, int ald) {
   int64_t b = blockIdx.x;
-  if (b < n_long) return d_gat_fwd_cta<T, H>(b, n_long, offsets, cols, longr, sl, sr, slope, alpha);
+  if (b < n_long)
+    return d_gat_fwd_cta<T, H>(b, n_long, offsets, cols, longr, sl, sr, slope, alpha, ald);
   b -= n_long;
   if (b < b_med)
-    return d_gat_fwd_warp<T, H>(b, b_med, offsets, cols, medium, n_medium, sl, sr, slope, alpha);
+    return d_gat_fwd_warp<T, H>(b, b_med, offsets, cols, medium, n_medium, sl, sr, slope, alpha,
+                                ald);
   b -= b_med;
-  d_gat_fwd_thread<T, H>(b, 0, offsets, cols, n_rows, sl, sr, slope, alpha, short_max);
+  d_gat_fwd_thread<T, H>(b, 0, offsets, cols, n_rows, sl, sr, slope, alpha, short_max, ald);
 }
 
 template <typename T, int H>
@@ -381,17 +383,18 @@ k_gat_bwd_all(const int64_t* __restrict__ offsets, const int32_t* __restrict__ c
               const int32_t* __restrict__ longr, int64_t n_long, int64_t b_med,
               const T* __restrict__ sl, const T* __restrict__ sr, float slope,
               const T* __restrict__ alpha, const T* __restrict__ dalpha, T* __restrict__ de,
-              T* __restrict__ dsl, int short_max) {
+              T* __restrict__ dsl, int short_max, int ald) {
   int64_t b = blockIdx.x;
   if (b < n_long)
-    return d_gat_bwd_cta<T, H>(b, n_long, offsets, cols, longr, sl, sr, slope, alpha, dalpha, de, dsl);
+    return d_gat_bwd_cta<T, H>(b, n_long, offsets, cols, longr, sl, sr, slope, alpha, dalpha, de,
+                               dsl, ald);
   b -= n_long;
   if (b < b_med)
     return d_gat_bwd_warp<T, H>(b, b_med, offsets, cols, medium, n_medium, sl, sr, slope, alpha,
-                                dalpha, de, dsl);
+                                dalpha, de, dsl, ald);
   b -= b_med;
   d_gat_bwd_thread<T, H>(b, 0, offsets, cols, n_rows, sl, sr, slope, alpha, dalpha, de, dsl,
-                         short_max);
+                         short_max, ald);
 }
 
 template <typename T, int H>
@@ -494,6 +497,7 @@ struct GatRows {
   int64_t n_long;
   int short_max;
   cudaStream_t st;
+  int ald;  // row stride (elements) of alpha and d_e: H, or 2H for interleaved rows
 };
 
 static inline int64_t med_blocks(const GatRows& g) {
@@ -508,7 +512,7 @@ template <typename T, int H>
 static void gat_fwd(const GatRows& g, const void* sl, const void* sr, float slope, void* alpha) {
   k_gat_fwd_all<T, H><<<all_blocks(g, H), 256, 0, g.st>>>(
       g.offsets, g.cols, g.n_rows, g.medium, g.n_medium, g.longr, g.n_long, med_blocks(g),
-      (const T*)sl, (const T*)sr, slope, (T*)alpha, g.short_max);
+      (const T*)sl, (const T*)sr, slope, (T*)alpha, g.short_max, g.ald);
 }
 
 template <typename T, int H>
@@ -517,7 +521,7 @@ static void gat_bwd(const GatRows& g, const void* sl, const void* sr, float slop
   k_gat_bwd_all<T, H><<<all_blocks(g, H), 256, 0, g.st>>>(
       g.offsets, g.cols, g.n_rows, g.medium, g.n_medium, g.longr, g.n_long, med_blocks(g),
       (const T*)sl, (const T*)sr, slope, (const T*)alpha, (const T*)dalpha, (T*)de, (T*)dsl,
-      g.short_max);
+      g.short_max, g.ald);
 }
 
 template <typename T, int H>
@@ -553,14 +557,15 @@ static int gat_rows_check(int heads, int dtype, int64_t n_medium, const int32_t*
 
 extern "C" int hg_gat_attention_fwd(const int64_t* offsets, const int32_t* cols, int64_t n_rows,
                                     const void* s_l, const void* s_r, int32_t heads, float slope,
-                                    void* alpha, const int32_t* medium_rows, int64_t n_medium,
-                                    const int32_t* long_rows, int64_t n_long, int32_t short_max,
-                                    int dtype, void* stream) {
+                                    void* alpha, int64_t alpha_ld, const int32_t* medium_rows,
+                                    int64_t n_medium, const int32_t* long_rows, int64_t n_long,
+                                    int32_t short_max, int dtype, void* stream) {
   int rc = gat_rows_check(heads, dtype, n_medium, medium_rows, n_long, long_rows, short_max);
   if (rc) return rc;
+  HG_REQUIRE(alpha_ld == 0 || (alpha_ld >= heads && alpha_ld <= INT32_MAX), "bad alpha row stride");
   if (n_rows == 0) return HG_OK;
   GatRows g{offsets, cols, n_rows, medium_rows, n_medium, long_rows, n_long, short_max,
-            as_stream(stream)};
+            as_stream(stream), (int)(alpha_ld ? alpha_ld : heads)};
   if (dtype == HG_F16) { HG_GAT_HEADS(gat_fwd, __half, g, s_l, s_r, slope, alpha) }
   else { HG_GAT_HEADS(gat_fwd, float, g, s_l, s_r, slope, alpha) }
   HG_LAUNCHED();
@@ -569,15 +574,16 @@ extern "C" int hg_gat_attention_fwd(const int64_t* offsets, const int32_t* cols,
 
 extern "C" int hg_gat_attention_bwd(const int64_t* offsets, const int32_t* cols, int64_t n_rows,
                                     const void* s_l, const void* s_r, int32_t heads, float slope,
-                                    const void* alpha, const void* dalpha, void* de, void* ds_l,
-                                    const int32_t* medium_rows, int64_t n_medium,
+                                    const void* alpha, const void* dalpha, void* de, int64_t ae_ld,
+                                    void* ds_l, const int32_t* medium_rows, int64_t n_medium,
                                     const int32_t* long_rows, int64_t n_long, int32_t short_max,
                                     int dtype, void* stream) {
   int rc = gat_rows_check(heads, dtype, n_medium, medium_rows, n_long, long_rows, short_max);
   if (rc) return rc;
+  HG_REQUIRE(ae_ld == 0 || (ae_ld >= heads && ae_ld <= INT32_MAX), "bad alpha / d_e row stride");
   if (n_rows == 0) return HG_OK;
   GatRows g{offsets, cols, n_rows, medium_rows, n_medium, long_rows, n_long, short_max,
-            as_stream(stream)};
+            as_stream(stream), (int)(ae_ld ? ae_ld : heads)};
   if (dtype == HG_F16) { HG_GAT_HEADS(gat_bwd, __half, g, s_l, s_r, slope, alpha, dalpha, de, ds_l) }
   else { HG_GAT_HEADS(gat_bwd, float, g, s_l, s_r, slope, alpha, dalpha, de, ds_l) }
   HG_LAUNCHED();
@@ -593,7 +599,7 @@ extern "C" int hg_edge_sums_fast(const int64_t* offsets, int64_t n_rows, const v
   if (rc) return rc;
   if (n_rows == 0) return HG_OK;
   GatRows g{offsets, nullptr, n_rows, medium_rows, n_medium, long_rows, n_long, short_max,
-            as_stream(stream)};
+            as_stream(stream), heads};
   if (dtype == HG_F16) { HG_GAT_HEADS(gat_sums, __half, g, vals, perm, out) }
   else { HG_GAT_HEADS(gat_sums, float, g, vals, perm, out) }
   HG_LAUNCHED();

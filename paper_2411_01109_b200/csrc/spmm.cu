@@ -200,7 +200,7 @@ struct TeamShape {
   static constexpr int TPW = 32 / TEAM;  // teams per warp
 };
 
-template <typename T, int V, int TEAM, int NCH, bool WEIGHTED>
+template <typename T, int V, int TEAM, int NCH, bool WEIGHTED, bool SUMW = false>
 struct FastTeam {
   static constexpr bool P2 = TeamShape<TEAM>::P2;
   static constexpr int EB = NCH >= 4 ? 4 : 8;             // edges gathered per batch
@@ -216,6 +216,8 @@ struct FastTeam {
   int beg, end, ldx, heads;
   const T* w;
   bool use_widx;
+  int wld, w2off;   // weight row stride; SUMW: offset of the summed second value block
+  float acc2;       // SUMW: this lane's head sum of w[idx(e), w2off + head]
 
   // Fetch the ids of batch [base, base+EB) into this lane's slots.
   template <bool FULL>
@@ -238,6 +240,7 @@ struct FastTeam {
   __device__ __forceinline__ void batch(int b, const int (&ids)[CPL], const int (&wids)[CPL]) {
     Raw raw[EB][NCH];
     T wv[EB][NCH];
+    T w2v[EB];
 #pragma unroll
     for (int j = 0; j < EB; ++j) {
       const bool ok = FULL || (b + j >= beg && b + j < end);
@@ -249,9 +252,14 @@ struct FastTeam {
       for (int k = 0; k < NCH; ++k) {
         if (ok && cval[k]) {
           raw[j][k] = __ldg(reinterpret_cast<const Raw*>(xl[k] + roff));
-          if (WEIGHTED) wv[j][k] = w[(size_t)(unsigned)wi * heads + chead[k]];
+          if (WEIGHTED) wv[j][k] = w[(size_t)(unsigned)wi * wld + chead[k]];
         }
       }
+      if (SUMW) w2v[j] = (ok && cval[0]) ? w[(size_t)(unsigned)wi * wld + w2off + chead[0]] : Num<T>::zero();
+    }
+    if (SUMW) {
+#pragma unroll
+      for (int j = 0; j < EB; ++j) acc2 += Num<T>::to_f(w2v[j]);
     }
 #pragma unroll
     for (int j = 0; j < EB; ++j) {
@@ -267,14 +275,15 @@ struct FastTeam {
   }
 };
 
-template <typename T, int V, int TEAM, int NCH, bool WEIGHTED>
+template <typename T, int V, int TEAM, int NCH, bool WEIGHTED, bool SUMW = false>
 __global__ void __launch_bounds__(256, FastOcc<TEAM, NCH, WEIGHTED>::value)
 k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __restrict__ cols,
             int64_t num_edges, const T* __restrict__ w, const int32_t* __restrict__ widx,
             int heads, int fh, const T* __restrict__ x, T* __restrict__ y,
             float* __restrict__ carry, int F, int ldx, int ldy, int fmode,
-            const T* __restrict__ fout) {
-  using Team = FastTeam<T, V, TEAM, NCH, WEIGHTED>;
+            const T* __restrict__ fout, int wld, int w2off, T* __restrict__ out2,
+            float* __restrict__ carry2) {
+  using Team = FastTeam<T, V, TEAM, NCH, WEIGHTED, SUMW>;
   constexpr int EB = Team::EB;
   constexpr int CPL = Team::CPL;
   constexpr bool P2 = Team::P2;
@@ -302,6 +311,9 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
   t.heads = heads;
   t.w = w;
   t.use_widx = WEIGHTED && widx != nullptr;
+  t.wld = wld;
+  t.w2off = w2off;
+  t.acc2 = 0.0f;
 #pragma unroll
   for (int k = 0; k < NCH; ++k) {
     const int c = tl + k * TEAM;
@@ -357,6 +369,10 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
     for (int k = 0; k < NCH; ++k)
       if (t.cval[k]) store_carry<V>(carry + (int64_t)slot * F + (t.xl[k] - x), t.acc[k]);
   }
+  if (SUMW && t.cval[0] && (tl * V) % fh == 0) {  // first lane of each head
+    if (slot < 0) out2[(int64_t)row * heads + t.chead[0]] = Num<T>::from_f(t.acc2);
+    else carry2[(int64_t)slot * heads + t.chead[0]] = t.acc2;
+  }
 }
 
 // One team per split row: fp32 carries folded in slot (edge) order.
@@ -364,12 +380,20 @@ template <typename T, int V, int TEAM, int NCH>
 __global__ void __launch_bounds__(256)
 k_spmm_fast_followup(const int4* __restrict__ split_rows, int64_t num_split,
                      const float* __restrict__ carry, T* __restrict__ y, int F, int ldy,
-                     int fmode, const T* __restrict__ fout) {
+                     int fmode, const T* __restrict__ fout, int heads2,
+                     const float* __restrict__ carry2, T* __restrict__ out2) {
   const int lane = threadIdx.x & 31;
   const int tl = lane & (TEAM - 1);
   const int64_t team = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TEAM;
   if (team >= num_split) return;
   const int4 sr = split_rows[team];
+  if (out2) {  // second-value head sums of the split row, folded in slot order
+    for (int hh = tl; hh < heads2; hh += TEAM) {
+      float s = 0.0f;
+      for (int p = 0; p < sr.z; ++p) s += carry2[(int64_t)(sr.y + p) * heads2 + hh];
+      out2[(int64_t)sr.x * heads2 + hh] = Num<T>::from_f(s);
+    }
+  }
   const int nvec = F / V;
   const T fo = fout ? fout[sr.x] : Num<T>::zero();
 #pragma unroll
@@ -418,31 +442,50 @@ struct FastArgs {
   float* carry;
   int F, ldx, ldy, fmode;
   const void* fout;
+  int wld, w2off;
+  void* out2;
+  float* carry2;
   cudaStream_t st;
 };
 
 template <int X> struct Pow2Up { static constexpr int value = X <= 1 ? 1 : 2 * Pow2Up<(X + 1) / 2>::value; };
 template <> struct Pow2Up<1> { static constexpr int value = 1; };
 
-template <typename T, int V, int TEAM, int NCH, bool WT>
+template <typename T, int V, int TEAM, int NCH, bool WT, bool SUMW = false>
 static int launch_fast(const FastArgs& a) {
   constexpr int kThreads = 256;
   constexpr int teams_per_block = (kThreads / 32) * TeamShape<TEAM>::TPW;
   constexpr int TEAMF = Pow2Up<TEAM>::value;  // follow-up pass: power-of-two teams
   if (a.num_units > 0) {
     int64_t blocks = (a.num_units + teams_per_block - 1) / teams_per_block;
-    k_spmm_fast<T, V, TEAM, NCH, WT><<<(unsigned)blocks, kThreads, 0, a.st>>>(
+    k_spmm_fast<T, V, TEAM, NCH, WT, SUMW><<<(unsigned)blocks, kThreads, 0, a.st>>>(
         a.units, a.num_units, a.cols, a.num_edges, (const T*)a.w, a.widx, a.heads, a.fh,
-        (const T*)a.x, (T*)a.y, a.carry, a.F, a.ldx, a.ldy, a.fmode, (const T*)a.fout);
+        (const T*)a.x, (T*)a.y, a.carry, a.F, a.ldx, a.ldy, a.fmode, (const T*)a.fout,
+        a.wld, a.w2off, (T*)a.out2, a.carry2);
     HG_LAUNCHED();
   }
   if (a.num_split > 0) {
     int64_t blocks = (a.num_split + kThreads / TEAMF - 1) / (kThreads / TEAMF);
     k_spmm_fast_followup<T, V, TEAMF, NCH><<<(unsigned)blocks, kThreads, 0, a.st>>>(
-        a.split_rows, a.num_split, a.carry, (T*)a.y, a.F, a.ldy, a.fmode, (const T*)a.fout);
+        a.split_rows, a.num_split, a.carry, (T*)a.y, a.F, a.ldy, a.fmode, (const T*)a.fout,
+        SUMW ? a.heads : 0, a.carry2, SUMW ? (T*)a.out2 : nullptr);
     HG_LAUNCHED();
   }
   return HG_OK;
+}
+
+// Weighted aggregation that also sums a second per-edge value block (w2off)
+// per head: one team size per power-of-two chunk count, single chunk per lane.
+template <typename T, int V>
+static int dispatch_sumw(const FastArgs& a) {
+  const int nvec = a.F / V;
+  HG_REQUIRE(nvec <= 32 && a.fh % V == 0, "hg_spmm: summed weights need F/V <= 32 and heads of whole vectors");
+  if (nvec <= 1) return launch_fast<T, V, 1, 1, true, true>(a);
+  if (nvec <= 2) return launch_fast<T, V, 2, 1, true, true>(a);
+  if (nvec <= 4) return launch_fast<T, V, 4, 1, true, true>(a);
+  if (nvec <= 8) return launch_fast<T, V, 8, 1, true, true>(a);
+  if (nvec <= 16) return launch_fast<T, V, 16, 1, true, true>(a);
+  return launch_fast<T, V, 32, 1, true, true>(a);
 }
 
 template <typename T, int V, bool WT>
@@ -471,6 +514,7 @@ static int dispatch_fast(const FastArgs& a) {
   const bool aligned = (reinterpret_cast<uintptr_t>(a.x) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(a.y) % 16 == 0);
   const bool big = aligned && (a.fh % VB == 0) && a.ldx % VB == 0 && a.ldy % VB == 0;
+  if (a.out2) return big ? dispatch_sumw<T, VB>(a) : dispatch_sumw<T, 2>(a);
   if (a.w) return big ? dispatch_layout<T, VB, true>(a) : dispatch_layout<T, 2, true>(a);
   return big ? dispatch_layout<T, VB, false>(a) : dispatch_layout<T, 2, false>(a);
 }
@@ -512,12 +556,14 @@ static int scale_rows(const void* x, const void* s, int64_t rows, int F, void* o
 using namespace hg;
 
 extern "C" int hg_spmm_workspace(int64_t n_cols, int32_t F, int64_t num_slots, int has_in_scale,
-                                 int dtype, size_t* bytes) {
-  HG_REQUIRE(bytes && F > 0 && n_cols >= 0 && num_slots >= 0, "hg_spmm_workspace: bad arguments");
+                                 int32_t sum_heads, int dtype, size_t* bytes) {
+  HG_REQUIRE(bytes && F > 0 && n_cols >= 0 && num_slots >= 0 && sum_heads >= 0,
+             "hg_spmm_workspace: bad arguments");
   HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
   Carver cv(nullptr, 0);
   cv.take<float>((size_t)num_slots * F);
   if (has_in_scale) cv.take<char>((size_t)n_cols * F * elem_size(dtype));
+  if (sum_heads) cv.take<float>((size_t)num_slots * sum_heads);
   *bytes = cv.used;
   return HG_OK;
 }
@@ -527,8 +573,9 @@ extern "C" int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_ro
                        const int32_t* split_rows, int64_t num_split_rows, int64_t num_slots,
                        const void* w, const int32_t* w_index, int32_t heads, const void* x,
                        void* y, int32_t F, int64_t ldx, int64_t ldy, int32_t scaling,
-                       int32_t relu, const void* in_scale, const void* out_factor, int dtype,
-                       void* ws, size_t ws_bytes, void* stream) {
+                       int32_t relu, const void* in_scale, const void* out_factor,
+                       int64_t w_ld, int32_t w2_off, void* out2, int dtype, void* ws,
+                       size_t ws_bytes, void* stream) {
   HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
   HG_REQUIRE(F > 0 && F % 2 == 0, "feature length %d must be even and positive", F);
   HG_REQUIRE(heads >= 1 && F % heads == 0 && (F / heads) % 2 == 0,
@@ -542,11 +589,17 @@ extern "C" int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_ro
   HG_REQUIRE(ldx >= F && ldy >= F && ldx <= INT32_MAX && ldy <= INT32_MAX,
              "hg_spmm: row strides (%lld, %lld) must be >= F=%d", (long long)ldx, (long long)ldy, F);
   HG_REQUIRE(!in_scale || ldx == F, "hg_spmm: in_scale needs a dense x (ldx == F)");
+  if (w_ld == 0) w_ld = heads;
+  HG_REQUIRE(!w || (w_ld >= heads && w_ld <= INT32_MAX), "hg_spmm: weight row stride %lld < heads %d",
+             (long long)w_ld, heads);
+  HG_REQUIRE(!out2 || (w && w2_off >= heads && w2_off + heads <= w_ld),
+             "hg_spmm: summed second weight block needs w and heads <= w2_off <= w_ld - heads");
   cudaStream_t st = as_stream(stream);
   if (n_rows == 0) return HG_OK;
   Carver cv(ws, ws_bytes);
   float* carry = cv.take<float>((size_t)num_slots * F);
   void* xs = in_scale ? cv.take<char>((size_t)n_cols * F * elem_size(dtype)) : nullptr;
+  float* carry2 = out2 ? cv.take<float>((size_t)num_slots * heads) : nullptr;
   HG_REQUIRE(cv.fits(), "hg_spmm: workspace too small (%zu < %zu)", ws_bytes, cv.used);
   HG_REQUIRE(num_slots == 0 || carry != nullptr, "hg_spmm: carry workspace missing");
   if (in_scale) {
@@ -563,10 +616,11 @@ extern "C" int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_ro
   a.x = x; a.y = y; a.carry = carry; a.F = F; a.ldx = (int)ldx; a.ldy = (int)ldy;
   a.fmode = (out_factor == nullptr ? 0 : (scaling == HG_SCALING_POST ? 1 : 2)) | (relu ? 4 : 0);
   a.fout = out_factor; a.st = st;
+  a.wld = (int)w_ld; a.w2off = w2_off; a.out2 = out2; a.carry2 = carry2;
   // Column slabs: when X (n_cols x F) overflows the L2 budget but a slab of
   // >= 32 columns fits, aggregate slab by slab so the random row gathers of
   // each pass hit L2 (the column stream is re-read once per slab, sequentially).
-  const int W = slab_width(n_cols, F, elem_size(dtype), w == nullptr || heads == 1);
+  const int W = out2 ? F : slab_width(n_cols, F, elem_size(dtype), w == nullptr || heads == 1);
   for (int j = 0; j < F; j += W) {
     FastArgs s = a;
     s.F = F - j < W ? F - j : W;

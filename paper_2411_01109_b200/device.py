@@ -384,7 +384,8 @@ def _row_strided(t):
 
 def spmm_csr(view: CsrView, x: torch.Tensor, w=None, w_index=None, heads: int = 1,
              scaling: str = "post", fin=None, fout=None, out=None,
-             split_cap: int = DEFAULT_SPLIT_CAP, relu: bool = False) -> torch.Tensor:
+             split_cap: int = DEFAULT_SPLIT_CAP, relu: bool = False, w2_off: int = 0,
+             out2=None) -> torch.Tensor:
     """fp32-guarded row-owned SpMM over one CSR view (hg_spmm).  x and out may
     be column slices of wider row-major storage (row strides passed through)."""
     _require_cuda(x)
@@ -400,10 +401,14 @@ def spmm_csr(view: CsrView, x: torch.Tensor, w=None, w_index=None, heads: int = 
     elif not _row_strided(out) or out.shape != (view.n_rows, f) or out.dtype != x.dtype:
         raise ValueError("out must be [n_rows, F] with unit column stride")
     nbytes = nat.size_query("hg_spmm_workspace", view.n_cols, f, sched.num_slots,
-                            int(fin is not None), dt)
+                            int(fin is not None), heads if out2 is not None else 0, dt)
     ws = workspace(nbytes, x.device)
+    w_ld = 0
     if w is not None:
-        w = w.contiguous()
+        if w.dim() == 2 and w.stride(1) == 1:
+            w_ld = w.stride(0)  # row-strided weights (e.g. interleaved alpha | d_e rows)
+        else:
+            w = w.contiguous()
         if w.dtype != x.dtype:
             raise ValueError("edge weights must match the feature dtype")
     if Probe.timing:
@@ -414,7 +419,7 @@ def spmm_csr(view: CsrView, x: torch.Tensor, w=None, w_index=None, heads: int = 
              view.num_edges, _p(sched.units), sched.num_units, _p(sched.split_rows),
              sched.split_rows.shape[0], sched.num_slots, _p(w), _p(w_index), heads, _p(x),
              _p(out), f, x.stride(0), out.stride(0), nat.SCALING_CODES[scaling], int(relu),
-             _p(fin), _p(fout), dt, _p(ws),
+             _p(fin), _p(fout), w_ld, int(w2_off), _p(out2), dt, _p(ws),
              0 if ws is None else ws.numel(), _stream())
     Probe.launches += int(sched.num_units > 0) + int(sched.split_rows.shape[0] > 0) + int(
         fin is not None)
@@ -574,31 +579,43 @@ def _heads_of(s):
     return s.shape[1] if s.dim() == 2 else 1
 
 
-def gat_attention_fwd(view: CsrView, s_l, s_r, slope=0.2):
-    """Fused fp32-guarded leaky(s_l[r] + s_r[c]) -> edge softmax: alpha [E, H]."""
+def gat_attention_fwd(view: CsrView, s_l, s_r, slope=0.2, out=None):
+    """Fused fp32-guarded leaky(s_l[r] + s_r[c]) -> edge softmax: alpha [E, H]
+    (out: an [E, H] view with unit column stride, e.g. the alpha half of
+    interleaved [E, 2H] rows)."""
     _require_cuda(s_l, s_r)
     s_l, s_r = s_l.contiguous(), s_r.contiguous()
     h = _heads_of(s_l)
-    alpha = torch.empty((view.num_edges, h), dtype=s_l.dtype, device=s_l.device)
+    alpha = out if out is not None else torch.empty((view.num_edges, h), dtype=s_l.dtype,
+                                                    device=s_l.device)
     med, lng = view.row_classes()
     nat.call("hg_gat_attention_fwd", _p(view.offsets), _p(view.cols), view.n_rows, _p(s_l),
-             _p(s_r), h, float(slope), _p(alpha), _p(med), med.numel(), _p(lng), lng.numel(),
-             SHORT_ROW, _dtype_code(s_l), _stream())
+             _p(s_r), h, float(slope), _p(alpha), alpha.stride(0), _p(med), med.numel(), _p(lng),
+             lng.numel(), SHORT_ROW, _dtype_code(s_l), _stream())
     Probe.launches += 1
     return alpha
 
 
-def gat_attention_bwd(view: CsrView, s_l, s_r, alpha, dalpha, slope=0.2):
-    """(de [E, H], ds_l [N, H]) of gat_attention_fwd."""
+def gat_attention_bwd(view: CsrView, s_l, s_r, alpha, dalpha, slope=0.2, de_out=None):
+    """(de [E, H], ds_l [N, H]) of gat_attention_fwd.  With de_out (the d_e half
+    of interleaved [E, 2H] rows, alpha its other half) the two share one row
+    stride."""
     s_l, s_r = s_l.contiguous(), s_r.contiguous()
-    alpha, dalpha = alpha.contiguous(), dalpha.contiguous().view(alpha.shape)
     h = _heads_of(s_l)
-    de = torch.empty_like(alpha)
+    dalpha = dalpha.contiguous().view(alpha.shape[0], h)
+    if de_out is None:
+        alpha = alpha.contiguous()
+        de = torch.empty_like(alpha)
+    else:
+        de = de_out
+        if alpha.stride(0) != de.stride(0):
+            raise ValueError("alpha and d_e must share a row stride")
     ds_l = torch.empty_like(s_l)
     med, lng = view.row_classes()
     nat.call("hg_gat_attention_bwd", _p(view.offsets), _p(view.cols), view.n_rows, _p(s_l),
-             _p(s_r), h, float(slope), _p(alpha), _p(dalpha), _p(de), _p(ds_l), _p(med),
-             med.numel(), _p(lng), lng.numel(), SHORT_ROW, _dtype_code(s_l), _stream())
+             _p(s_r), h, float(slope), _p(alpha), _p(dalpha), _p(de), alpha.stride(0),
+             _p(ds_l), _p(med), med.numel(), _p(lng), lng.numel(), SHORT_ROW,
+             _dtype_code(s_l), _stream())
     Probe.launches += 1
     return de, ds_l
 

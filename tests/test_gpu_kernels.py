@@ -829,3 +829,25 @@ def test_gather_rows(cuda, shape):
     idx = rng.permutation(shape[0]).astype(np.int32)
     got = D.gather_rows(_t(src, cuda), _t(idx, cuda)).cpu().numpy()
     np.testing.assert_array_equal(bits(got), bits(src[idx]))
+
+
+@pytest.mark.parametrize("heads,fh", [(4, 32), (4, 16), (2, 64), (1, 128), (8, 8)])
+def test_spmm_interleaved_weights_and_second_sums(cuda, heads, fh):
+    """hg_spmm over interleaved [E, 2H] (w | w2) rows read through perm: the
+    aggregation equals the one with dense weights, and out2 equals the column
+    sums of w2 (hg_edge_sums_fast) -- incl. split heavy rows."""
+    from paper_2411_01109_b200 import device as D
+
+    n = 5000
+    r, c = _hub_graph(heads + fh, n)
+    dg = _dg(n, r, c, cuda)
+    bwd = dg.view(True)
+    e = r.size
+    ae = torch.randn(e, 2 * heads, device=cuda, dtype=torch.float16)
+    g = torch.randn(n, heads * fh, device=cuda, dtype=torch.float16)
+    s2 = torch.empty(n, heads, device=cuda, dtype=torch.float16)
+    got = D.spmm_csr(bwd, g, ae[:, :heads], bwd.perm, heads, "post", w2_off=heads, out2=s2)
+    want = D.spmm_csr(bwd, g, ae[:, :heads].contiguous(), bwd.perm, heads, "post")
+    assert torch.equal(got, want)
+    want2 = D.edge_sums_fast(bwd, ae[:, heads:].contiguous(), bwd.perm)
+    assert torch.allclose(s2.float(), want2.float(), atol=2e-2, rtol=2e-3)
