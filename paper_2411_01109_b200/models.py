@@ -796,35 +796,28 @@ class _GATCoreFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, z, a_l, a_r, bundle, heads, relu):
         s_l, s_r = bundle.head_dots(z, a_l, a_r, heads)
-        # alpha and (in backward) d_e share interleaved [E, 2H] rows, so the
-        # transposed aggregation reads both through perm from one sector
-        ae = torch.empty((bundle.num_edges, 2 * heads), dtype=z.dtype, device=z.device)
-        alpha = D.gat_attention_fwd(bundle.dg.view(False), s_l, s_r, 0.2, out=ae[:, :heads])
+        alpha = D.gat_attention_fwd(bundle.dg.view(False), s_l, s_r, 0.2)
         out = D.spmm_csr(bundle.dg.view(False), z, alpha, None, heads, "post", relu=relu)
         ctx.bundle, ctx.heads, ctx.relu = bundle, heads, relu
-        ctx.save_for_backward(z, a_l, a_r, s_l, s_r, ae, out if relu else None)
+        ctx.save_for_backward(z, a_l, a_r, s_l, s_r, alpha, out if relu else None)
         return out
 
     @staticmethod
     def backward(ctx, g):
-        z, a_l, a_r, s_l, s_r, ae, y = ctx.saved_tensors
+        z, a_l, a_r, s_l, s_r, alpha, y = ctx.saved_tensors
         b, h = ctx.bundle, ctx.heads
         g = g.contiguous()
         if ctx.relu:
             g = D.relu_grad(y, g)
-        alpha, de = ae[:, :h], ae[:, h:]
         dalpha = b.sddmm(g, z, heads=h).reshape(-1, h)
-        ds_l = D.gat_attention_bwd(b.dg.view(False), s_l, s_r, alpha, dalpha, 0.2,
-                                   de_out=de)[1]
         bwd = b.dg.view(True)
-        f = g.shape[1]
-        if f % 8 == 0 and (f // h) % 8 == 0 and f // 8 <= 32:
-            # transposed aggregation + the column sums of d_e in one pass
-            ds_r = torch.empty_like(s_l)
-            gz = D.spmm_csr(bwd, g, alpha, bwd.perm, h, "post", w2_off=h, out2=ds_r)
-        else:
-            gz = D.spmm_csr(bwd, g, alpha, bwd.perm, h, "post")
-            ds_r = D.edge_sums_fast(bwd, de, bwd.perm)
+        gz = D.spmm_csr(bwd, g, alpha, bwd.perm, h, "post")
+        de, ds_l = D.gat_attention_bwd(b.dg.view(False), s_l, s_r, alpha, dalpha, 0.2)
+        # (fusing these column sums into the transposed aggregation through
+        # interleaved (alpha | d_e) rows -- hg_spmm out2 -- measured slower on
+        # RMAT-24: +14.7 ms in the aggregation and +3 ms in the strided
+        # attention kernels against the 10.6 ms sum pass it replaces)
+        ds_r = D.edge_sums_fast(bwd, de, bwd.perm)
         gz, ga_l, ga_r = D.head_dots_bwd(z, a_l, a_r, ds_l, ds_r, h, gz_acc=gz)
         return gz, ga_l, ga_r, None, None, None
 
