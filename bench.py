@@ -167,7 +167,8 @@ def cpu_baseline_gcn(offsets, cols, x16, labels, budget_edges, kind="gcn", hidde
     ms = (timer.dense + other + timer.sparse * e_total / max(e_s, 1)) * 1e3
     sample = (f"rows [0,{r_end}) = {e_s:,} of {e_total:,} edges, all {n:,} vertices; "
               f"sparse {timer.sparse:.2f}s x{e_total / max(e_s, 1):.1f} + dense {timer.dense:.2f}s"
-              f" + other {other:.2f}s")
+              f" + other {other:.2f}s (numpy oracle: sparse kernels single-threaded, dense "
+              f"BLAS on all cores)")
     try:
         cores = len(os.sched_getaffinity(0))
     except AttributeError:
