@@ -267,6 +267,26 @@ class DistBundle:
         return self.ops.spmm(view, self.ex.gather_rows(xs.contiguous()), w, widx, heads,
                              scaling, None, fout)
 
+    @property
+    def fused_gat(self):
+        """GAT layers use the fp32-guarded fused attention (CUDA ops only)."""
+        return self.ops is CudaOps
+
+    def gat_attention(self, s_l, s_r, slope):
+        """Row-owned fused attention over the local rows; the column scores s_r
+        are all-gathered (N x H, small)."""
+        return D.gat_attention_fwd(self.part.fwd, s_l.contiguous(),
+                                   self.ex.gather_rows(s_r.contiguous()), slope)
+
+    def gat_attention_bwd(self, s_l, s_r, alpha, g, slope):
+        """(ds_l, ds_r): row sums locally; the column owner sums d_e over its CSC
+        rows after the padded all-gather of every rank's edge values."""
+        de, ds_l = D.gat_attention_bwd(self.part.fwd, s_l.contiguous(),
+                                       self.ex.gather_rows(s_r.contiguous()), alpha, g, slope)
+        bwd = self.part.bwd
+        ds_r = D.edge_sums_fast(bwd, self.ex.gather_edges(de), bwd.perm)
+        return ds_l, ds_r
+
     def bias_spmm(self, h, b, scaling, norm):
         """spmm(add_bias(h, b)): bias and input scale applied to the local rows
         before the all-gather (hg_bias_scale_rows), then the gathered SpMM."""
