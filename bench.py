@@ -415,6 +415,7 @@ def b200_arm(args, ws, rank, local):
     eager_ms, _ = timed_steps(args.steps)
     launches = D.Probe.launches
     spmm_b, spmm_s, spmm_n = D.Probe.summary()
+    compulsory = D.Probe.compulsory_per_launch()
     D.Probe.reset(timing=False)
 
     # ---- device-resident timing (value): the step replayed as a CUDA graph ----
@@ -475,7 +476,11 @@ def b200_arm(args, ws, rank, local):
                          "frac": round(achieved / peak, 4), "traffic": traffic,
                          "kernel": "k_spmm_fast (hg_spmm)", "launches": spmm_n,
                          "peak_source": peak_kind,
-                         "bytes_model": "4E+8(N+1)+2FE+2FN per SpMM launch, F = stored width"},
+                         "bytes_model": "4E+8(N+1)+2FE+2FN per SpMM launch, F = stored width",
+                         "compulsory_bytes": round(compulsory),
+                         "traffic_over_compulsory": (round(traffic / compulsory, 3)
+                                                     if traffic and compulsory else None),
+                         "compulsory_model": "4E+8(N+1)+2F(N_cols+N_rows): ids, X once, Y once"},
             "final_loss": round(final_loss, 5),
             "grad_scale": (tr.inner if use_dist else tr).grad_scale,
             "setup_s": round(setup_s, 1),

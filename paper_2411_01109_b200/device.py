@@ -72,6 +72,18 @@ class Probe:
         ts = sum(r[0].elapsed_time(r[1]) for r in cls.records) / 1e3
         return tb, ts, len(cls.records)
 
+    @classmethod
+    def compulsory_per_launch(cls):
+        """Mean compulsory DRAM bytes per timed spmm call."""
+        return sum(r[3] for r in cls.records) / max(len(cls.records), 1)
+
+
+def compulsory_bytes(n_rows, n_cols, num_edges, f, heads=0, elem=2):
+    """Bytes an SpMM must move from/to DRAM at least: the column ids and offsets,
+    X read once, Y written once (+ the edge weights): 4E + 8(N+1) + e(F n_cols
+    + F n_rows) (+ e E H)."""
+    return 4 * num_edges + 8 * (n_rows + 1) + elem * f * (n_cols + n_rows) + elem * num_edges * heads
+
 
 def spmm_bytes(n_rows, n_cols, num_edges, f, heads=0, elem=2):
     """Gather-model bytes of one SpMM: 4E + 8(N+1) + 2F*E + 2F*N (+2E*H)."""
@@ -427,7 +439,10 @@ def spmm_csr(view: CsrView, x: torch.Tensor, w=None, w_index=None, heads: int = 
         ev1.record()
         Probe.records.append((ev0, ev1, spmm_bytes(view.n_rows, view.n_cols, view.num_edges, f,
                                                    heads if w is not None else 0,
-                                                   x.element_size())))
+                                                   x.element_size()),
+                              compulsory_bytes(view.n_rows, view.n_cols, view.num_edges, f,
+                                               heads if w is not None else 0,
+                                               x.element_size())))
     return out
 
 
