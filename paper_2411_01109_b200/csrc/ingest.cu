@@ -12,6 +12,8 @@
 //   3. edge lines compacted in file order (cub::DeviceSelect::Flagged), max id
 //      reduced -- the (rows, cols) arrays the reference hands to from_edges.
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
 #include "hg_common.cuh"
 
@@ -129,7 +131,7 @@ static int plan_ingest(Carver& cv, int64_t nbytes, int64_t n_lines, IngestPlan& 
   p.max_id = cv.take<int64_t>(1);
   p.first_err = cv.take<unsigned long long>(1);
   size_t b1 = 0, b2 = 0, b3 = 0;
-  cub::CountingInputIterator<int64_t> it(0);
+  thrust::counting_iterator<int64_t> it(0);
   HG_CUDA(cub::DeviceSelect::If(nullptr, b1, it, (int64_t*)nullptr, (int64_t*)nullptr,
                                 nbytes > 0 ? nbytes : 1, IsTerminator{nullptr, 0}));
   HG_CUDA(cub::DeviceSelect::Flagged(nullptr, b2, (int64_t*)nullptr, (uint8_t*)nullptr,
@@ -148,10 +150,9 @@ using namespace hg;
 extern "C" int hg_count_lines_workspace(int64_t nbytes, size_t* bytes) {
   HG_REQUIRE(bytes && nbytes >= 0, "hg_count_lines_workspace: bad arguments");
   size_t b = 0;
-  HG_CUDA(cub::DeviceReduce::Sum(nullptr, b, cub::TransformInputIterator<int64_t, IsTerminator,
-                                                                          cub::CountingInputIterator<int64_t>>(
-                                                 cub::CountingInputIterator<int64_t>(0),
-                                                 IsTerminator{nullptr, 0}),
+  using It = thrust::transform_iterator<IsTerminator, thrust::counting_iterator<int64_t>, int64_t>;
+  HG_CUDA(cub::DeviceReduce::Sum(nullptr, b, It(thrust::counting_iterator<int64_t>(0),
+                                                IsTerminator{nullptr, 0}),
                                  (int64_t*)nullptr, nbytes > 0 ? nbytes : 1));
   *bytes = align_up(b) + 256;
   return HG_OK;
@@ -168,8 +169,8 @@ extern "C" int hg_count_lines(const void* text, int64_t nbytes, int64_t* n_lines
   Carver cv(ws, ws_bytes);
   int64_t* cnt = cv.take<int64_t>(1);
   size_t b = 0;
-  using It = cub::TransformInputIterator<int64_t, IsTerminator, cub::CountingInputIterator<int64_t>>;
-  It it(cub::CountingInputIterator<int64_t>(0), IsTerminator{(const unsigned char*)text, nbytes});
+  using It = thrust::transform_iterator<IsTerminator, thrust::counting_iterator<int64_t>, int64_t>;
+  It it(thrust::counting_iterator<int64_t>(0), IsTerminator{(const unsigned char*)text, nbytes});
   HG_CUDA(cub::DeviceReduce::Sum(nullptr, b, it, cnt, nbytes));
   void* tmp = cv.take<char>(b);
   HG_REQUIRE(cv.fits(), "hg_count_lines: workspace too small");
@@ -212,7 +213,7 @@ extern "C" int hg_parse_edges(const void* text, int64_t nbytes, int64_t n_lines,
   HG_REQUIRE(cv.fits(), "hg_parse_edges: workspace too small (%zu < %zu)", ws_bytes, cv.used);
   const unsigned char* t = (const unsigned char*)text;
   size_t tb = p.cub_bytes;
-  HG_CUDA(cub::DeviceSelect::If(p.cub_tmp, tb, cub::CountingInputIterator<int64_t>(0), p.terms,
+  HG_CUDA(cub::DeviceSelect::If(p.cub_tmp, tb, thrust::counting_iterator<int64_t>(0), p.terms,
                                 p.n_sel, nbytes, IsTerminator{t, nbytes}, st));
   int64_t n_terms = 0;
   HG_CUDA(cudaMemcpyAsync(&n_terms, p.n_sel, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
