@@ -3,7 +3,7 @@
 //
 //   1. line terminators: '\n', or '\r' not followed by '\n' (Python universal
 //      newlines, so line numbers match the reference's enumerate(fh, 1));
-//      positions selected with cub::DeviceSelect::If over a counting iterator.
+//      found with 16-byte loads, per-block counts, a scan, and a write pass.
 //   2. one thread per line: str.strip/str.split semantics on ASCII whitespace
 //      (' ', \t, \n, \r, \v, \f, \x1c-\x1f); empty and '#'/'%' lines skipped;
 //      fewer than two fields -> "expected 'src dst'"; int() syntax ([+-]digits
@@ -12,8 +12,6 @@
 //   3. edge lines compacted in file order (cub::DeviceSelect::Flagged), max id
 //      reduced -- the (rows, cols) arrays the reference hands to from_edges.
 #include <cub/cub.cuh>
-#include <thrust/iterator/counting_iterator.h>
-#include <thrust/iterator/transform_iterator.h>
 
 #include "hg_common.cuh"
 
@@ -21,14 +19,65 @@ namespace hg {
 
 enum : uint32_t { kLineSkip = 0, kLineEdge = 1, kErrFields = 2, kErrInt = 3, kErrNeg = 4, kErrBig = 5 };
 
-struct IsTerminator {
-  const unsigned char* text;
-  int64_t n;
-  __device__ __forceinline__ bool operator()(int64_t i) const {
-    const unsigned char ch = text[i];
-    return ch == '\n' || (ch == '\r' && (i + 1 == n || text[i + 1] != '\n'));
+
+// Line terminators in one pass over the text: block b owns bytes
+// [b*kTermChunk, (b+1)*kTermChunk), thread t a 64-byte run of it read as four
+// 16-byte vectors (the byte after a '\r' decides whether it ends a line).
+// Pass 1 counts per block; pass 2 re-reads, block-scans the per-thread counts
+// and writes the terminator positions in file order.
+constexpr int kTermThreads = 256;
+constexpr int kTermPerThread = 64;
+constexpr int64_t kTermChunk = (int64_t)kTermThreads * kTermPerThread;
+
+__device__ __forceinline__ unsigned term_mask64(const unsigned char* __restrict__ t, int64_t n,
+                                                int64_t p0, uint64_t& mask) {
+  __align__(16) unsigned char b[kTermPerThread + 1];
+  if (p0 + kTermPerThread < n && ((reinterpret_cast<uintptr_t>(t) & 15) == 0)) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      *reinterpret_cast<uint4*>(b + 16 * q) = *reinterpret_cast<const uint4*>(t + p0 + 16 * q);
+    b[kTermPerThread] = t[p0 + kTermPerThread];
+  } else {
+    for (int i = 0; i <= kTermPerThread; ++i) b[i] = p0 + i < n ? t[p0 + i] : 0;
   }
-};
+  mask = 0;
+#pragma unroll
+  for (int i = 0; i < kTermPerThread; ++i) {
+    const bool in = p0 + i < n;
+    const bool term = b[i] == '\n' || (b[i] == '\r' && (p0 + i + 1 == n || b[i + 1] != '\n'));
+    if (in && term) mask |= 1ull << i;
+  }
+  return __popcll(mask);
+}
+
+__global__ void __launch_bounds__(kTermThreads)
+k_count_terms(const unsigned char* __restrict__ t, int64_t n, int64_t* __restrict__ counts) {
+  using BR = cub::BlockReduce<unsigned, kTermThreads>;
+  __shared__ typename BR::TempStorage tmp;
+  uint64_t mask;
+  const int64_t p0 = (int64_t)blockIdx.x * kTermChunk + (int64_t)threadIdx.x * kTermPerThread;
+  const unsigned c = p0 < n ? term_mask64(t, n, p0, mask) : 0u;
+  const unsigned total = BR(tmp).Sum(c);
+  if (threadIdx.x == 0) counts[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(kTermThreads)
+k_write_terms(const unsigned char* __restrict__ t, int64_t n, const int64_t* __restrict__ base,
+              int64_t* __restrict__ terms) {
+  using BS = cub::BlockScan<unsigned, kTermThreads>;
+  __shared__ typename BS::TempStorage tmp;
+  uint64_t mask = 0;
+  const int64_t p0 = (int64_t)blockIdx.x * kTermChunk + (int64_t)threadIdx.x * kTermPerThread;
+  const unsigned c = p0 < n ? term_mask64(t, n, p0, mask) : 0u;
+  unsigned off;
+  BS(tmp).ExclusiveSum(c, off);
+  int64_t o = base[blockIdx.x] + off;
+  while (mask) {
+    const int i = __ffsll((long long)mask) - 1;
+    terms[o++] = p0 + i;
+    mask &= mask - 1;
+  }
+}
 
 __device__ __forceinline__ bool is_ws(unsigned char c) {
   return c == ' ' || (c >= 9 && c <= 13) || (c >= 0x1c && c <= 0x1f);
@@ -116,6 +165,9 @@ struct IngestPlan {
   int64_t* line_max;
   int64_t* max_id;
   unsigned long long* first_err;
+  int64_t nblk;
+  int64_t* blk;   // per-block terminator counts (+ a zero)
+  int64_t* blkx;  // their exclusive scan: first terminator slot per block, total last
   void* cub_tmp;
   size_t cub_bytes;
 };
@@ -130,10 +182,12 @@ static int plan_ingest(Carver& cv, int64_t nbytes, int64_t n_lines, IngestPlan& 
   p.line_max = cv.take<int64_t>(L);
   p.max_id = cv.take<int64_t>(1);
   p.first_err = cv.take<unsigned long long>(1);
+  p.nblk = (nbytes + kTermChunk - 1) / kTermChunk;
+  p.blk = cv.take<int64_t>(p.nblk + 1);
+  p.blkx = cv.take<int64_t>(p.nblk + 1);
   size_t b1 = 0, b2 = 0, b3 = 0;
-  thrust::counting_iterator<int64_t> it(0);
-  HG_CUDA(cub::DeviceSelect::If(nullptr, b1, it, (int64_t*)nullptr, (int64_t*)nullptr,
-                                nbytes > 0 ? nbytes : 1, IsTerminator{nullptr, 0}));
+  HG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b1, (int64_t*)nullptr, (int64_t*)nullptr,
+                                        p.nblk + 1));
   HG_CUDA(cub::DeviceSelect::Flagged(nullptr, b2, (int64_t*)nullptr, (uint8_t*)nullptr,
                                      (int64_t*)nullptr, (int64_t*)nullptr, L));
   HG_CUDA(cub::DeviceReduce::Max(nullptr, b3, (int64_t*)nullptr, (int64_t*)nullptr, L));
@@ -149,12 +203,15 @@ using namespace hg;
 
 extern "C" int hg_count_lines_workspace(int64_t nbytes, size_t* bytes) {
   HG_REQUIRE(bytes && nbytes >= 0, "hg_count_lines_workspace: bad arguments");
+  const int64_t nblk = (nbytes + kTermChunk - 1) / kTermChunk;
   size_t b = 0;
-  using It = thrust::transform_iterator<IsTerminator, thrust::counting_iterator<int64_t>, int64_t>;
-  HG_CUDA(cub::DeviceReduce::Sum(nullptr, b, It(thrust::counting_iterator<int64_t>(0),
-                                                IsTerminator{nullptr, 0}),
-                                 (int64_t*)nullptr, nbytes > 0 ? nbytes : 1));
-  *bytes = align_up(b) + 256;
+  HG_CUDA(cub::DeviceReduce::Sum(nullptr, b, (int64_t*)nullptr, (int64_t*)nullptr,
+                                 nblk > 0 ? nblk : 1));
+  Carver cv(nullptr, 0);
+  cv.take<int64_t>(nblk > 0 ? nblk : 1);
+  cv.take<int64_t>(1);
+  cv.take<char>(b);
+  *bytes = cv.used;
   return HG_OK;
 }
 
@@ -166,15 +223,18 @@ extern "C" int hg_count_lines(const void* text, int64_t nbytes, int64_t* n_lines
     return HG_OK;
   }
   cudaStream_t st = as_stream(stream);
+  const int64_t nblk = (nbytes + kTermChunk - 1) / kTermChunk;
   Carver cv(ws, ws_bytes);
+  int64_t* counts = cv.take<int64_t>(nblk);
   int64_t* cnt = cv.take<int64_t>(1);
   size_t b = 0;
-  using It = thrust::transform_iterator<IsTerminator, thrust::counting_iterator<int64_t>, int64_t>;
-  It it(thrust::counting_iterator<int64_t>(0), IsTerminator{(const unsigned char*)text, nbytes});
-  HG_CUDA(cub::DeviceReduce::Sum(nullptr, b, it, cnt, nbytes));
+  HG_CUDA(cub::DeviceReduce::Sum(nullptr, b, counts, cnt, nblk));
   void* tmp = cv.take<char>(b);
   HG_REQUIRE(cv.fits(), "hg_count_lines: workspace too small");
-  HG_CUDA(cub::DeviceReduce::Sum(tmp, b, it, cnt, nbytes, st));
+  k_count_terms<<<(unsigned)nblk, kTermThreads, 0, st>>>((const unsigned char*)text, nbytes,
+                                                        counts);
+  HG_LAUNCHED();
+  HG_CUDA(cub::DeviceReduce::Sum(tmp, b, counts, cnt, nblk, st));
   int64_t terms = 0;
   unsigned char last = 0;
   HG_CUDA(cudaMemcpyAsync(&terms, cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -213,10 +273,14 @@ extern "C" int hg_parse_edges(const void* text, int64_t nbytes, int64_t n_lines,
   HG_REQUIRE(cv.fits(), "hg_parse_edges: workspace too small (%zu < %zu)", ws_bytes, cv.used);
   const unsigned char* t = (const unsigned char*)text;
   size_t tb = p.cub_bytes;
-  HG_CUDA(cub::DeviceSelect::If(p.cub_tmp, tb, thrust::counting_iterator<int64_t>(0), p.terms,
-                                p.n_sel, nbytes, IsTerminator{t, nbytes}, st));
+  HG_CUDA(cudaMemsetAsync(p.blk + p.nblk, 0, sizeof(int64_t), st));
+  k_count_terms<<<(unsigned)p.nblk, kTermThreads, 0, st>>>(t, nbytes, p.blk);
+  HG_LAUNCHED();
+  HG_CUDA(cub::DeviceScan::ExclusiveSum(p.cub_tmp, tb, p.blk, p.blkx, p.nblk + 1, st));
+  k_write_terms<<<(unsigned)p.nblk, kTermThreads, 0, st>>>(t, nbytes, p.blkx, p.terms);
+  HG_LAUNCHED();
   int64_t n_terms = 0;
-  HG_CUDA(cudaMemcpyAsync(&n_terms, p.n_sel, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  HG_CUDA(cudaMemcpyAsync(&n_terms, p.blkx + p.nblk, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   HG_CUDA(cudaStreamSynchronize(st));
   HG_REQUIRE(n_terms <= n_lines && n_lines <= n_terms + 1,
              "hg_parse_edges: n_lines %lld does not match the text (%lld terminators)",
