@@ -10,8 +10,9 @@ Exchange: before each aggregation the rank's feature rows are all-gathered
 q*n_max.. -- and the local column ids are pre-remapped into that padded
 layout once, so the SpMM reads the gathered buffer in place (no compaction).
 Backward all-gathers the output gradient the same way and aggregates over the
-local CSC rows.  GAT additionally all-gathers per-edge values (alpha, d_e) in
-a padded per-rank edge layout for the column-owner side of its backward.
+local CSC rows.  GAT additionally sends per-edge values (alpha, d_e) to the
+owner of each edge's column with one all-to-all (each edge travels once,
+E/P per rank instead of the E an all-gather would deliver).
 Weight gradients and the loss are all-reduced (the data-parallel sum).
 Degree-factor tables are global (computed once from the full graph), which
 makes the concatenated rank outputs bit-identical to the 1-GPU result.
@@ -57,9 +58,12 @@ class LocalPart:
     splits: np.ndarray        # vertex split points [P+1]
     edge_splits: np.ndarray   # CSR edge offsets of the split points [P+1]
     n_max: int                # padded rows per rank in gathered feature buffers
-    e_max: int                # padded edges per rank in gathered edge buffers
+    e_max: int                # largest per-rank edge count
     fwd: CsrView              # local CSR rows, columns in the padded feature layout
-    bwd: CsrView              # local CSC rows, columns padded, perm -> padded edge layout
+    bwd: CsrView              # local CSC rows, columns padded, perm -> received edge buffer
+    send_index: torch.Tensor  # local CSR edges grouped by the rank owning their column
+    send_counts: list         # edges sent to each rank
+    recv_counts: list         # edges received from each rank (this rank's CSC edges)
 
     @property
     def lo(self):
@@ -86,10 +90,28 @@ def make_local_part(offsets, cols, t_offsets, t_cols, perm, rank, parts) -> Loca
     t_lo, t_hi = int(t_offsets[lo]), int(t_offsets[hi])
     b_off = (t_offsets[lo:hi + 1] - t_offsets[lo]).contiguous()
     b_cols = remap_to_padded(t_cols[t_lo:t_hi], splits, n_max)
-    b_perm = remap_to_padded(perm[t_lo:t_hi], eoff, e_max)
+    # Edge values for the column owner travel by all-to-all (SURVEY 8(e)
+    # option A): rank q sends rank p the values of its edges whose column p
+    # owns, in ascending global edge id; concatenated over q that is p's CSC
+    # edges sorted by global edge id, and recv_pos maps each CSC slot into it.
+    dev = offsets.device
+    g_ids = perm[t_lo:t_hi].to(torch.int64)
+    order = torch.argsort(g_ids, stable=True)
+    sorted_g = g_ids[order]
+    eoff_t = torch.as_tensor(eoff, dtype=torch.int64, device=dev)
+    bounds = torch.searchsorted(sorted_g, eoff_t, right=False)
+    recv_counts = (bounds[1:] - bounds[:-1]).cpu().tolist()
+    recv_pos = torch.empty_like(order)
+    recv_pos[order] = torch.arange(order.numel(), device=dev)
+    my_cols = cols[int(offsets[lo]):int(offsets[hi])].to(torch.int64)
+    owner = torch.searchsorted(torch.as_tensor(splits[1:-1], dtype=torch.int64, device=dev),
+                               my_cols, right=True)
+    send_index = torch.argsort(owner, stable=True)
+    send_counts = torch.bincount(owner, minlength=parts).cpu().tolist()
     fwd = CsrView(f_off, f_cols, hi - lo, parts * n_max)
-    bwd = CsrView(b_off, b_cols, hi - lo, parts * n_max, perm=b_perm)
-    return LocalPart(rank, parts, splits, eoff, n_max, e_max, fwd, bwd)
+    bwd = CsrView(b_off, b_cols, hi - lo, parts * n_max, perm=recv_pos.to(torch.int32))
+    return LocalPart(rank, parts, splits, eoff, n_max, e_max, fwd, bwd, send_index,
+                     send_counts, recv_counts)
 
 
 class Exchange:
@@ -121,13 +143,18 @@ class Exchange:
         return out
 
     def gather_edges(self, v_local: torch.Tensor) -> torch.Tensor:
+        """Per-edge values ([E_local, ...], CSR order) -> the values of this
+        rank's CSC edges in received order (index with part.bwd.perm): one
+        all-to-all, each edge sent once to its column's owner."""
         p = self.part
-        send = v_local
-        if v_local.shape[0] != p.e_max:
-            send = v_local.new_zeros((p.e_max,) + tuple(v_local.shape[1:]))
-            send[: v_local.shape[0]] = v_local
-        out = v_local.new_empty((p.parts * p.e_max,) + tuple(v_local.shape[1:]))
-        self._all_gather(out, send.contiguous())
+        send = v_local.index_select(0, p.send_index).contiguous()
+        out = v_local.new_empty((sum(p.recv_counts),) + tuple(v_local.shape[1:]))
+        if self.staged and out.is_cuda:
+            host = out.cpu()
+            self.dist.all_to_all_single(host, send.cpu(), p.recv_counts, p.send_counts)
+            out.copy_(host)
+        else:
+            self.dist.all_to_all_single(out, send, p.recv_counts, p.send_counts)
         return out
 
     def all_reduce_(self, t: torch.Tensor, op=None) -> torch.Tensor:

@@ -1,6 +1,6 @@
 """CPU, world_size 2 over gloo: the row-partitioned execution path
 (partition.py) -- split points, padded column remapping, feature / gradient /
-edge-value all-gathers, global loss and weight-gradient all-reduce -- gives the
+edge-value all-to-alls, global loss and weight-gradient all-reduce -- gives the
 same training step as one process.  The CUDA kernels are swapped for a host
 implementation of the same row-owned semantics (HostOps below, test-only), so
 this checks the exchange logic, not the kernels (those are the -m gpu tests)."""

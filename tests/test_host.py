@@ -35,9 +35,9 @@ def test_library_workspace_queries_without_gpu():
     from paper_2411_01109_b200 import _native
 
     # (the CUB-backed sizing queries need a device; these are pure arithmetic)
-    assert _native.size_query("hg_spmm_workspace", 100, 64, 10, 1, 0) >= 100 * 64 * 2
+    assert _native.size_query("hg_spmm_workspace", 100, 64, 10, 1, 1, 0) >= 100 * 64 * 2
     with pytest.raises(ValueError):
-        _native.size_query("hg_spmm_workspace", 100, 0, 10, 1, 0)
+        _native.size_query("hg_spmm_workspace", 100, 0, 10, 1, 1, 0)
 
 
 def test_library_is_sm100a():
