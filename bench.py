@@ -129,12 +129,13 @@ def max_over_ranks(dist, v):
     return float(tt.item())
 
 
-def load_traffic_profile(f_key):
-    """ncu dram bytes per launch of k_spmm_fast from the committed profile summary."""
+def load_traffic_profile(workload):
+    """ncu dram bytes per k_spmm_fast launch of this workload's epoch, from the
+    committed profile summary (None when that workload was not captured)."""
     p = ROOT / "profiles" / "r01" / "ncu_spmm_summary.json"
     try:
-        d = json.loads(p.read_text())
-        return d.get(str(f_key))
+        d = json.loads(p.read_text()).get(workload)
+        return d["bytes_per_launch"] if d else None
     except Exception:
         return None
 
@@ -416,6 +417,15 @@ def b200_arm(args, ws, rank, local):
     launches = D.Probe.launches
     spmm_b, spmm_s, spmm_n = D.Probe.summary()
     compulsory = D.Probe.compulsory_per_launch()
+    # one more eager step holding its SpMM operands: the same gathers with the
+    # arithmetic removed (hg_gather_probe) give the floor those launches could reach
+    ceiling_s = None
+    D.Probe.reset(timing=True, keep=True)
+    timed_steps(1)
+    _, probe_s, _ = D.Probe.summary()
+    ceil = D.Probe.gather_ceiling()
+    if ceil:
+        ceiling_s = (ceil, probe_s)
     D.Probe.reset(timing=False)
 
     # ---- device-resident timing (value): the step replayed as a CUDA graph ----
@@ -458,7 +468,7 @@ def b200_arm(args, ws, rank, local):
     result = None
     if rank == 0:
         achieved = spmm_b / spmm_s if spmm_s > 0 else 0.0
-        traffic = load_traffic_profile("gcn_epoch")
+        traffic = load_traffic_profile(args.workload)
         result = {
             "metric": METRIC, "value": round(t_ms, 4), "unit": "ms/epoch", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_ms, 4),
@@ -480,7 +490,14 @@ def b200_arm(args, ws, rank, local):
                          "compulsory_bytes": round(compulsory),
                          "traffic_over_compulsory": (round(traffic / compulsory, 3)
                                                      if traffic and compulsory else None),
-                         "compulsory_model": "4E+8(N+1)+2F(N_cols+N_rows): ids, X once, Y once"},
+                         "compulsory_model": "4E+8(N+1)+2F(N_cols+N_rows): ids, X once, Y once",
+                         "gather_ceiling": (None if ceiling_s is None else {
+                             "spmm_ms_per_step": round(ceiling_s[1] * 1e3, 4),
+                             "probe_ms_per_step": round(ceiling_s[0] * 1e3, 4),
+                             "frac": round(ceiling_s[0] / ceiling_s[1], 4),
+                             "what": "hg_gather_probe: the same column ids, feature buffers and "
+                                     "widths as the step's hg_spmm calls, loads only (X warm in "
+                                     "L2); frac = probe time / hg_spmm time"})},
             "final_loss": round(final_loss, 5),
             "grad_scale": (tr.inner if use_dist else tr).grad_scale,
             "setup_s": round(setup_s, 1),

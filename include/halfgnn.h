@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define HG_ABI_VERSION 2
+#define HG_ABI_VERSION 3
 
 enum { HG_OK = 0, HG_EINVAL = 1, HG_ECUDA = 2 };
 enum { HG_F16 = 0, HG_F32 = 1 };
@@ -79,12 +79,20 @@ int hg_degree_factors(const int64_t* offsets, int64_t n, int kind, int dtype, vo
  * Units are ordered by descending length class floor(log2(len))+1, rows
  * ascending inside a class (stable).  split_rows receives {row, first_slot,
  * nparts, 0} for every row with nparts > 1, rows ascending.
- * Capacities: max_units >= n + ceil(E/split_cap), max_split >= ceil(E/split_cap).
- * counts_out (HOST int64[3]) = {num_units, num_split_rows, num_slots}.
+ * Packing (pack_rows > 0: a power of two in [2, 16], pack_rows * pack_deg <=
+ * split_cap): every aligned block of pack_rows rows [k*pack_rows, ...) whose
+ * rows all have degree <= pack_deg becomes one pack {first_row, begin, end,
+ * rows} (int32 x4, rows ascending) instead of per-row units -- short rows
+ * walked as one edge stream by hg_spmm, so a run of near-empty rows costs one
+ * team, not one dependent load chain per row.  pack_rows = 0: no packs.
+ * Capacities: max_units >= n + ceil(E/split_cap), max_split >= ceil(E/split_cap),
+ * max_packs >= ceil(n/pack_rows).
+ * counts_out (HOST int64[4]) = {num_units, num_split_rows, num_slots, num_packs}.
  * Synchronises `stream`. */
 int hg_schedule_workspace(int64_t n, int64_t num_edges, int32_t split_cap, size_t* bytes);
-int hg_schedule_build(const int64_t* offsets, int64_t n, int32_t split_cap, int32_t* units,
-                      int64_t max_units, int32_t* split_rows, int64_t max_split,
+int hg_schedule_build(const int64_t* offsets, int64_t n, int32_t split_cap, int32_t pack_rows,
+                      int32_t pack_deg, int32_t* units, int64_t max_units, int32_t* split_rows,
+                      int64_t max_split, int32_t* packs, int64_t max_packs,
                       int64_t* counts_out, void* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------- SpMM */
@@ -110,12 +118,17 @@ int hg_schedule_build(const int64_t* offsets, int64_t n, int32_t split_cap, int3
  * out2[r, h] = rnd(sum_e w[idx(e) * w_ld + w2_off + h]) (fp32 sum, same row
  * ownership): the GAT backward's column sums of d_e read from the same
  * interleaved (alpha, d_e) rows as the transposed aggregation's weights
- * (models.py:309-311, 335-337); needs F/8 <= 32 lanes of whole-vector heads. */
+ * (models.py:309-311, 335-337); needs F/8 <= 32 lanes of whole-vector heads.
+ * packs / num_packs: the hg_schedule_build packs of the same CSR (NULL / 0 when
+ * the schedule was built without packing), pack_rowid: int32 row id per edge
+ * (needed with packs); a packed row's result is bitwise the one it gets as its
+ * own unit. */
 int hg_spmm_workspace(int64_t n_cols, int32_t F, int64_t num_slots, int has_in_scale,
                       int32_t sum_heads, int dtype, size_t* bytes);
 int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_rows, int64_t n_cols,
             int64_t num_edges, const int32_t* units, int64_t num_units,
             const int32_t* split_rows, int64_t num_split_rows, int64_t num_slots,
+            const int32_t* packs, int64_t num_packs, const int32_t* pack_rowid,
             const void* w, const int32_t* w_index, int32_t heads, const void* x, void* y,
             int32_t F, int64_t ldx, int64_t ldy, int32_t scaling, int32_t relu,
             const void* in_scale, const void* out_factor, int64_t w_ld, int32_t w2_off,
@@ -152,6 +165,15 @@ int hg_spmm_vertex_ref(const int64_t* offsets, const int32_t* cols, int64_t n_ro
                        const int64_t* group_base, void* staging_partials,
                        int64_t* staging_rows, int dtype, void* ws, size_t ws_bytes,
                        void* stream);
+
+/* Measurement only (no reference counterpart): the gather pattern of one SpMM
+ * with the arithmetic removed -- cols[0..num_edges) streamed once and, per
+ * edge, row_bytes (multiple of 16, <= 512) of x at cols[e] * ld_bytes fetched
+ * with the k_spmm_fast team shape.  Its time is the floor of any gather SpMM of
+ * that graph and width; bench.py reports hg_spmm against it.  *out is written
+ * only on a hash collision (keeps the loads live). */
+int hg_gather_probe(const int32_t* cols, int64_t num_edges, const void* x, int32_t row_bytes,
+                    int64_t ld_bytes, uint32_t* out, void* stream);
 
 /* --------------------------------------------------------------- SDDMM & GAT */
 

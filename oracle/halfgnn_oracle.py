@@ -412,15 +412,27 @@ def edge_softmax_bwd(offsets, alpha, g):
 # ── scheduler and partitioner restatements (build-specified integer maps) ─
 
 
-def schedule_units(offsets, cap):
+def schedule_units(offsets, cap, pack_rows=0, pack_deg=0):
     """Restatement of hg_schedule_build (include/halfgnn.h): the degree-bucketed
     work units that replace simt.plan_edge_parallel / plan_vertex_grouped
     (simt.py:158-201) for the fp32-guarded kernels.  Returns (units (U,4) int32,
-    split_rows (S,4) int32, num_slots)."""
+    split_rows (S,4) int32, num_slots), plus packs (P,4) int32 {first_row,
+    begin, end, rows} when pack_rows > 0 (aligned blocks of pack_rows rows all
+    of degree <= pack_deg; their rows get no units)."""
     offsets = np.asarray(offsets, np.int64)
     n = offsets.size - 1
     deg = np.diff(offsets)
     nparts = np.where(deg == 0, 1, -(-deg // cap))
+    packs = np.zeros((0, 4), np.int32)
+    if pack_rows:
+        nb = -(-n // pack_rows)
+        short = np.ones(nb * pack_rows, bool)
+        short[:n] = deg <= pack_deg
+        blk = short.reshape(nb, pack_rows).all(axis=1)
+        nparts = np.where(np.repeat(blk, pack_rows)[:n], 0, nparts)
+        r0 = np.flatnonzero(blk) * pack_rows
+        cnt = np.minimum(pack_rows, n - r0)
+        packs = np.stack([r0, offsets[r0], offsets[r0 + cnt], cnt], axis=1).astype(np.int32)
     ubase = np.cumsum(nparts) - nparts
     row = np.repeat(np.arange(n, dtype=np.int64), nparts)
     part = np.arange(row.size) - ubase[row]
@@ -439,6 +451,8 @@ def schedule_units(offsets, cap):
     srows = np.flatnonzero(split)
     split_rows = np.stack([srows, sbase[srows], nparts[srows], np.zeros_like(srows)],
                           axis=1).astype(np.int32)
+    if pack_rows:
+        return units, split_rows.reshape(-1, 4), int(sparts.sum()), packs.reshape(-1, 4)
     return units, split_rows.reshape(-1, 4), int(sparts.sum())
 
 

@@ -15,7 +15,7 @@ from pathlib import Path
 LIB_PATH = Path(__file__).resolve().with_name("libhalfgnn.so")
 
 HG_OK, HG_EINVAL, HG_ECUDA = 0, 1, 2
-ABI_VERSION = 2
+ABI_VERSION = 3
 HG_F16, HG_F32 = 0, 1
 SCALING_CODES = {"post": 0, "pre": 1, "discretized": 2}
 FACTOR_INV, FACTOR_INV_SQRT = 1, 2
@@ -36,9 +36,11 @@ SIGNATURES = {
     "hg_transpose": [_P, _P, _I64, _I64, _P, _P, _P, _P, c_size_t, _P],
     "hg_degree_factors": [_P, _I64, c_int, c_int, _P, _P],
     "hg_schedule_workspace": [_I64, _I64, _I32, _PSZ],
-    "hg_schedule_build": [_P, _I64, _I32, _P, _I64, _P, _I64, _PI64, _P, c_size_t, _P],
+    "hg_schedule_build": [_P, _I64, _I32, _I32, _I32, _P, _I64, _P, _I64, _P, _I64, _PI64, _P,
+                          c_size_t, _P],
     "hg_spmm_workspace": [_I64, _I32, _I64, c_int, _I32, c_int, _PSZ],
-    "hg_spmm": [_P, _P, _I64, _I64, _I64, _P, _I64, _P, _I64, _I64, _P, _P, _I32, _P, _P,
+    "hg_spmm": [_P, _P, _I64, _I64, _I64, _P, _I64, _P, _I64, _I64, _P, _I64, _P, _P, _P, _I32,
+                _P, _P,
                 _I32, _I64, _I64, _I32, _I32, _P, _P, _I64, _I32, _P, c_int, _P, c_size_t, _P],
     "hg_spmm_edge_ref_workspace": [_I64, _I64, _I32, _I32, _I32, c_int, c_int, _PSZ],
     "hg_spmm_edge_ref": [_P, _P, _I64, _I64, _I64, _I32, _I32, _P, _P, _P, _I32, _I32, _P, _P,
@@ -46,6 +48,7 @@ SIGNATURES = {
     "hg_spmm_vertex_ref_workspace": [_I64, _I32, c_int, c_int, _PSZ],
     "hg_spmm_vertex_ref": [_P, _P, _I64, _I64, _P, _P, _I32, _I32, _P, _P, _P, _P, _P, c_int,
                            _P, c_size_t, _P],
+    "hg_gather_probe": [_P, _I64, _P, _I32, _I64, _P, _P],
     "hg_sddmm": [_P, _P, _I64, _I64, _P, _I64, _P, _P, _P, _I32, _I32, c_int, _P],
     "hg_sddmm_fast": [_P, _P, _I64, _I64, _P, _I64, _P, _P, _P, _I32, _I32, c_int, _P],
     "hg_attn_scores": [_P, _P, _I64, _I64, _P, _P, _I32, c_double, _P, c_int, _P],

@@ -297,16 +297,34 @@ namespace hg {
 
 static constexpr int kNumClasses = 33;  // len 0 -> class 0, else floor(log2(len)) + 1
 
+// Per row: unit count, carry slots, split flag; with packing (pack_rows > 0, a
+// power of two <= 32) a row inside an aligned block of pack_rows rows that all
+// have degree <= pack_deg gets no unit -- the block becomes one pack, flagged
+// at its first row.  Blocks are whole half/quarter warps (blockDim % 32 == 0).
 __global__ void k_unit_counts(const int64_t* __restrict__ offsets, int64_t n, int64_t cap,
+                              int pack_rows, int64_t pack_deg,
                               int64_t* __restrict__ nparts, int64_t* __restrict__ split_parts,
-                              int64_t* __restrict__ split_flag) {
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
-       r += (int64_t)gridDim.x * blockDim.x) {
-    int64_t d = offsets[r + 1] - offsets[r];
-    int64_t p = d == 0 ? 1 : (d + cap - 1) / cap;
-    nparts[r] = p;
-    split_parts[r] = p > 1 ? p : 0;
-    split_flag[r] = p > 1 ? 1 : 0;
+                              int64_t* __restrict__ split_flag, int64_t* __restrict__ pack_flag) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = base + threadIdx.x;
+    const bool in = r < n;
+    const int64_t d = in ? offsets[r + 1] - offsets[r] : 0;
+    bool packed = false;
+    if (pack_rows > 0) {
+      const unsigned bal = __ballot_sync(0xffffffffu, !in || d <= pack_deg);
+      const unsigned grp = (pack_rows == 32 ? 0xffffffffu : ((1u << pack_rows) - 1u))
+                           << (lane & ~(pack_rows - 1));
+      packed = (bal & grp) == grp;
+    }
+    if (in) {
+      const int64_t p = packed ? 0 : (d == 0 ? 1 : (d + cap - 1) / cap);
+      nparts[r] = p;
+      split_parts[r] = p > 1 ? p : 0;
+      split_flag[r] = p > 1 ? 1 : 0;
+      pack_flag[r] = packed && (r & (pack_rows - 1)) == 0 ? 1 : 0;
+    }
   }
 }
 
@@ -316,10 +334,16 @@ __global__ void k_emit_units(const int64_t* __restrict__ offsets, int64_t n, int
                              const int64_t* __restrict__ slot_base,
                              const int64_t* __restrict__ split_idx, int4* __restrict__ units,
                              uint32_t* __restrict__ keys, int32_t* __restrict__ iota,
-                             int4* __restrict__ split_rows) {
+                             int4* __restrict__ split_rows, int pack_rows,
+                             const int64_t* __restrict__ pack_flag,
+                             const int64_t* __restrict__ pack_idx, int4* __restrict__ packs) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
        r += (int64_t)gridDim.x * blockDim.x) {
     int64_t beg = offsets[r], end = offsets[r + 1];
+    if (pack_rows > 0 && pack_flag[r]) {
+      const int64_t cnt = n - r < pack_rows ? n - r : pack_rows;
+      packs[pack_idx[r]] = make_int4((int)r, (int)beg, (int)offsets[r + cnt], (int)cnt);
+    }
     int64_t p = nparts[r];
     int64_t ub = unit_base[r];
     for (int64_t j = 0; j < p; ++j) {
@@ -344,6 +368,7 @@ __global__ void k_gather_units(const int4* __restrict__ src, const int32_t* __re
 
 struct SchedPlan {
   int64_t *nparts, *split_parts, *split_flag, *unit_base, *slot_base, *split_idx;
+  int64_t *pack_flag, *pack_idx;
   int4* units_tmp;
   uint32_t *keys, *keys_alt;
   int32_t *iota, *order;
@@ -361,6 +386,8 @@ static int plan_schedule(Carver& cv, int64_t n, int64_t max_units, SchedPlan& p)
   p.unit_base = cv.take<int64_t>(n + 1);
   p.slot_base = cv.take<int64_t>(n + 1);
   p.split_idx = cv.take<int64_t>(n + 1);
+  p.pack_flag = cv.take<int64_t>(n);
+  p.pack_idx = cv.take<int64_t>(n + 1);
   p.units_tmp = cv.take<int4>(max_units);
   p.keys = cv.take<uint32_t>(max_units);
   p.keys_alt = cv.take<uint32_t>(max_units);
@@ -390,10 +417,19 @@ extern "C" int hg_schedule_workspace(int64_t n, int64_t m, int32_t cap, size_t* 
   return HG_OK;
 }
 
-extern "C" int hg_schedule_build(const int64_t* offsets, int64_t n, int32_t cap, int32_t* units,
+extern "C" int hg_schedule_build(const int64_t* offsets, int64_t n, int32_t cap,
+                                 int32_t pack_rows, int32_t pack_deg, int32_t* units,
                                  int64_t max_units, int32_t* split_rows, int64_t max_split,
-                                 int64_t* counts_out, void* ws, size_t ws_bytes, void* stream) {
+                                 int32_t* packs, int64_t max_packs, int64_t* counts_out, void* ws,
+                                 size_t ws_bytes, void* stream) {
   HG_REQUIRE(n > 0 && cap > 0 && counts_out, "hg_schedule_build: bad arguments");
+  HG_REQUIRE(pack_rows == 0 || (pack_rows >= 2 && pack_rows <= kPackRows &&
+                                (pack_rows & (pack_rows - 1)) == 0 && pack_deg >= 0 &&
+                                (int64_t)pack_rows * pack_deg <= cap && packs &&
+                                max_packs >= (n + pack_rows - 1) / pack_rows),
+             "hg_schedule_build: pack_rows must be a power of two in [2, %d] with "
+             "pack_rows * pack_deg <= split_cap and room for ceil(n / pack_rows) packs",
+             kPackRows);
   HG_REQUIRE(n <= (int64_t)INT32_MAX, "hg_schedule_build: too many rows");
   cudaStream_t st = as_stream(stream);
   int64_t m = 0;
@@ -411,7 +447,8 @@ extern "C" int hg_schedule_build(const int64_t* offsets, int64_t n, int32_t cap,
   HG_REQUIRE(cv.fits(), "hg_schedule_build: workspace too small");
 
   int g = grid_for(n, 256, 148 * 16);
-  k_unit_counts<<<g, 256, 0, st>>>(offsets, n, cap, p.nparts, p.split_parts, p.split_flag);
+  k_unit_counts<<<g, 256, 0, st>>>(offsets, n, cap, pack_rows, pack_deg, p.nparts,
+                                   p.split_parts, p.split_flag, p.pack_flag);
   HG_LAUNCHED();
   // exclusive scans as inclusive scans shifted by one slot (base[0] = 0)
   HG_CUDA(cudaMemsetAsync(p.unit_base, 0, sizeof(int64_t), st));
@@ -425,12 +462,22 @@ extern "C" int hg_schedule_build(const int64_t* offsets, int64_t n, int32_t cap,
   tb = p.cub_bytes;
   HG_CUDA(cub::DeviceScan::InclusiveSum(p.cub_tmp, tb, p.split_flag, p.split_idx + 1, (int64_t)n,
                                         st));
-  int64_t totals[3];
+  HG_CUDA(cudaMemsetAsync(p.pack_idx, 0, sizeof(int64_t), st));
+  if (pack_rows > 0) {
+    tb = p.cub_bytes;
+    HG_CUDA(cub::DeviceScan::InclusiveSum(p.cub_tmp, tb, p.pack_flag, p.pack_idx + 1, (int64_t)n,
+                                          st));
+  }
+  int64_t totals[4] = {0, 0, 0, 0};
   HG_CUDA(cudaMemcpyAsync(&totals[0], p.unit_base + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   HG_CUDA(cudaMemcpyAsync(&totals[1], p.split_idx + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   HG_CUDA(cudaMemcpyAsync(&totals[2], p.slot_base + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  if (pack_rows > 0)
+    HG_CUDA(cudaMemcpyAsync(&totals[3], p.pack_idx + n, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                            st));
   k_emit_units<<<g, 256, 0, st>>>(offsets, n, cap, p.nparts, p.unit_base, p.slot_base,
-                                  p.split_idx, p.units_tmp, p.keys, p.iota, (int4*)split_rows);
+                                  p.split_idx, p.units_tmp, p.keys, p.iota, (int4*)split_rows,
+                                  pack_rows, p.pack_flag, p.pack_idx, (int4*)packs);
   HG_LAUNCHED();
   HG_CUDA(cudaStreamSynchronize(st));
   int64_t nu = totals[0];
@@ -444,5 +491,6 @@ extern "C" int hg_schedule_build(const int64_t* offsets, int64_t n, int32_t cap,
   counts_out[0] = totals[0];
   counts_out[1] = totals[1];
   counts_out[2] = totals[2];
+  counts_out[3] = totals[3];
   return HG_OK;
 }

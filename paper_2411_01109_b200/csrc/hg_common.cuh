@@ -13,6 +13,10 @@
 
 namespace hg {
 
+// Rows per packed work unit (hg_schedule_build pack_rows upper bound; the
+// SpMM team keeps one end offset per packed row in its lanes' registers).
+constexpr int kPackRows = 16;
+
 void set_error(const char* fmt, ...);
 
 #define HG_REQUIRE(cond, ...)          \

@@ -219,6 +219,43 @@ struct FastTeam {
   int wld, w2off;   // weight row stride; SUMW: offset of the summed second value block
   float acc2;       // SUMW: this lane's head sum of w[idx(e), w2off + head]
 
+  // Packed unit (an aligned run of short rows walked as one edge stream):
+  // each edge's row id comes with its column id; when it changes, the
+  // finished row is stored and the accumulators cleared.  Each lane still
+  // accumulates a row's edges one by one in edge order, so a packed row rounds
+  // exactly like the same row processed as its own unit.  Empty rows of the
+  // pack are written before the stream (write_empty_rows).
+  int prow;      // row being accumulated (-1 before the first edge)
+  T pfo;         // its output factor
+  const T* px;
+  T* py;
+  const T* pfout;
+  T* pout2;
+  int pldy, pfmode;
+  bool plead;
+
+  __device__ __forceinline__ void store_row() {
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) {
+      if (cval[k]) store_out<T, V>(py + (int64_t)prow * pldy + (xl[k] - px), acc[k], pfmode, pfo);
+#pragma unroll
+      for (int i = 0; i < V; ++i) acc[k][i] = 0.0f;
+    }
+    if (SUMW) {
+      if (plead) pout2[(int64_t)prow * heads + chead[0]] = Num<T>::from_f(acc2);
+      acc2 = 0.0f;
+    }
+  }
+
+  // Edge of row r arrives: close the previous row if r starts a new one.
+  __device__ __forceinline__ void enter_row(int r) {
+    if (r != prow) {
+      if (prow >= 0) store_row();
+      prow = r;
+      pfo = pfout ? pfout[r] : Num<T>::zero();
+    }
+  }
+
   // Fetch the ids of batch [base, base+EB) into this lane's slots.
   template <bool FULL>
   __device__ __forceinline__ void load_ids_impl(const int32_t* __restrict__ p, int base, int tl,
@@ -236,8 +273,9 @@ struct FastTeam {
   }
 
   // One batch of EB edges [b, b+EB): issue every gather, then accumulate.
-  template <bool FULL>
-  __device__ __forceinline__ void batch(int b, const int (&ids)[CPL], const int (&wids)[CPL]) {
+  template <bool FULL, bool PACKED = false>
+  __device__ __forceinline__ void batch(int b, const int (&ids)[CPL], const int (&wids)[CPL],
+                                        const int (&rids)[CPL]) {
     Raw raw[EB][NCH];
     T wv[EB][NCH];
     T w2v[EB];
@@ -257,6 +295,39 @@ struct FastTeam {
       }
       if (SUMW) w2v[j] = (ok && cval[0]) ? w[(size_t)(unsigned)wi * wld + w2off + chead[0]] : Num<T>::zero();
     }
+    if constexpr (PACKED) {
+      // Rolled over the batch (one copy of the row-store path, so the kernel
+      // stays inside the instruction cache): edge j is always in slot 0 and
+      // the batch registers shift down one slot per step.
+      int rj[EB];
+#pragma unroll
+      for (int j = 0; j < EB; ++j) rj[j] = shfl_id(rids, j);
+#pragma unroll 1
+      for (int j = 0; j < EB; ++j) {
+        if (b + j >= beg && b + j < end) {
+          enter_row(rj[0]);
+          if (SUMW) acc2 += Num<T>::to_f(w2v[0]);
+#pragma unroll
+          for (int k = 0; k < NCH; ++k) {
+            if (cval[k]) {
+              if (WEIGHTED) acc_fma<T, V>(acc[k], wv[0][k], raw[0][k]);
+              else acc_add<T, V>(acc[k], raw[0][k]);
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q + 1 < EB; ++q) {
+          rj[q] = rj[q + 1];
+          if (SUMW) w2v[q] = w2v[q + 1];
+#pragma unroll
+          for (int k = 0; k < NCH; ++k) {
+            raw[q][k] = raw[q + 1][k];
+            if (WEIGHTED) wv[q][k] = wv[q + 1][k];
+          }
+        }
+      }
+      return;
+    }
     if (SUMW) {
 #pragma unroll
       for (int j = 0; j < EB; ++j) acc2 += Num<T>::to_f(w2v[j]);
@@ -275,14 +346,21 @@ struct FastTeam {
   }
 };
 
-template <typename T, int V, int TEAM, int NCH, bool WEIGHTED, bool SUMW = false>
-__global__ void __launch_bounds__(256, FastOcc<TEAM, NCH, WEIGHTED>::value)
+// PACKED = false: units {row, begin, end, slot} (slot -1 = whole row, else the
+// row's fp32 carry slot).  PACKED = true: packs {first_row, begin, end, rows}
+// of consecutive short rows (hg_schedule_build), each row stored as the edge
+// stream crosses its end.
+template <typename T, int V, int TEAM, int NCH, bool WEIGHTED, bool SUMW = false,
+          bool PACKED = false>
+__global__ void __launch_bounds__(256, PACKED ? FastOcc<TEAM, NCH, true>::value
+                                             : FastOcc<TEAM, NCH, WEIGHTED>::value)
 k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __restrict__ cols,
             int64_t num_edges, const T* __restrict__ w, const int32_t* __restrict__ widx,
             int heads, int fh, const T* __restrict__ x, T* __restrict__ y,
             float* __restrict__ carry, int F, int ldx, int ldy, int fmode,
             const T* __restrict__ fout, int wld, int w2off, T* __restrict__ out2,
-            float* __restrict__ carry2) {
+            float* __restrict__ carry2, const int64_t* __restrict__ offsets,
+            const int32_t* __restrict__ rowid) {
   using Team = FastTeam<T, V, TEAM, NCH, WEIGHTED, SUMW>;
   constexpr int EB = Team::EB;
   constexpr int CPL = Team::CPL;
@@ -323,20 +401,71 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
 #pragma unroll
     for (int i = 0; i < V; ++i) t.acc[k][i] = 0.0f;
   }
+  const bool lead = t.cval[0] && (tl * V) % fh == 0;  // SUMW: first lane of its head
+  if constexpr (PACKED) {
+    t.prow = -1;
+    t.pfo = Num<T>::zero();
+    t.px = x;
+    t.py = y;
+    t.pfout = fout;
+    t.pout2 = out2;
+    t.pldy = ldy;
+    t.pfmode = fmode;
+    t.plead = lead;
+    // empty rows of the pack (degrees read lane-parallel): finalize(0) with the
+    // row's factor, as their own units would store
+    constexpr unsigned kTeamBits = TEAM == 32 ? 0xffffffffu : ((1u << TEAM) - 1u);
+    unsigned empty = 0;
+#pragma unroll
+    for (int q = 0; q < (kPackRows + TEAM - 1) / TEAM; ++q) {
+      const int i = q * TEAM + tl;
+      const bool e = i < slot && __ldg(offsets + row + i) == __ldg(offsets + row + i + 1);
+      empty |= ((__ballot_sync(t.tmask, e) >> t.tbase) & kTeamBits) << (q * TEAM);
+    }
+    while (empty) {
+      const int i = __ffs(empty) - 1;
+      empty &= empty - 1;
+      t.prow = row + i;
+      t.pfo = fout ? fout[row + i] : Num<T>::zero();
+      t.store_row();
+    }
+    t.prow = -1;
+  }
   const int beg = t.beg, end = t.end;
 
   // Batches aligned to the absolute address of cols (vector id loads).
   const int mis = (int)((reinterpret_cast<uintptr_t>(cols) >> 2) & (EB - 1));
   int b = beg - ((beg + mis) & (EB - 1));
+  if constexpr (PACKED) {  // one (guarded) batch site, ids prefetched one batch ahead
+    int ids[CPL] = {}, wids[CPL] = {}, rids[CPL] = {};
+    if (b < end && loader) {
+      t.template load_ids_impl<false>(cols, b, tl, limit, ids);
+      if (t.use_widx) t.template load_ids_impl<false>(widx, b, tl, limit, wids);
+      t.template load_ids_impl<false>(rowid, b, tl, limit, rids);
+    }
+    for (; b < end; b += EB) {
+      int nids[CPL] = {}, nwids[CPL] = {}, nrids[CPL] = {};
+      if (b + EB < end && loader) {
+        t.template load_ids_impl<false>(cols, b + EB, tl, limit, nids);
+        if (t.use_widx) t.template load_ids_impl<false>(widx, b + EB, tl, limit, nwids);
+        t.template load_ids_impl<false>(rowid, b + EB, tl, limit, nrids);
+      }
+      t.template batch<false, true>(b, ids, wids, rids);
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) { ids[q] = nids[q]; wids[q] = nwids[q]; rids[q] = nrids[q]; }
+    }
+    if (t.prow >= 0) t.store_row();  // the pack's last non-empty row
+    return;
+  }
   if (b < beg) {  // partial head batch
-    int ids[CPL] = {}, wids[CPL] = {};
+    int ids[CPL] = {}, wids[CPL] = {}, rids[CPL] = {};
     if (loader) t.template load_ids_impl<false>(cols, b, tl, limit, ids);
     if (t.use_widx && loader) t.template load_ids_impl<false>(widx, b, tl, limit, wids);
-    t.template batch<false>(b, ids, wids);
+    t.template batch<false>(b, ids, wids, rids);
     b += EB;
   }
   if (b + EB <= end) {  // full batches, column ids prefetched one batch ahead
-    int ids[CPL] = {}, wids[CPL] = {};
+    int ids[CPL] = {}, wids[CPL] = {}, rids[CPL] = {};
     if (loader) t.template load_ids_impl<true>(cols, b, tl, limit, ids);
     if (t.use_widx && loader) t.template load_ids_impl<true>(widx, b, tl, limit, wids);
     for (;;) {
@@ -345,7 +474,7 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
       int nids[CPL] = {}, nwids[CPL] = {};
       if (more && loader) t.template load_ids_impl<true>(cols, nb, tl, limit, nids);
       if (more && t.use_widx && loader) t.template load_ids_impl<true>(widx, nb, tl, limit, nwids);
-      t.template batch<true>(b, ids, wids);
+      t.template batch<true>(b, ids, wids, rids);
       b = nb;
       if (!more) break;
 #pragma unroll
@@ -353,10 +482,10 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
     }
   }
   if (b < end) {  // partial tail batch
-    int ids[CPL] = {}, wids[CPL] = {};
+    int ids[CPL] = {}, wids[CPL] = {}, rids[CPL] = {};
     if (loader) t.template load_ids_impl<false>(cols, b, tl, limit, ids);
     if (t.use_widx && loader) t.template load_ids_impl<false>(widx, b, tl, limit, wids);
-    t.template batch<false>(b, ids, wids);
+    t.template batch<false>(b, ids, wids, rids);
   }
 
   if (slot < 0) {
@@ -369,7 +498,7 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
     for (int k = 0; k < NCH; ++k)
       if (t.cval[k]) store_carry<V>(carry + (int64_t)slot * F + (t.xl[k] - x), t.acc[k]);
   }
-  if (SUMW && t.cval[0] && (tl * V) % fh == 0) {  // first lane of each head
+  if (SUMW && lead) {  // first lane of each head
     if (slot < 0) out2[(int64_t)row * heads + t.chead[0]] = Num<T>::from_f(t.acc2);
     else carry2[(int64_t)slot * heads + t.chead[0]] = t.acc2;
   }
@@ -434,6 +563,9 @@ struct FastArgs {
   int64_t num_units;
   const int4* split_rows;
   int64_t num_split;
+  const int4* packs;
+  int64_t num_packs;
+  const int32_t* rowid;
   const void* w;
   const int32_t* widx;
   int heads, fh;
@@ -461,7 +593,15 @@ static int launch_fast(const FastArgs& a) {
     k_spmm_fast<T, V, TEAM, NCH, WT, SUMW><<<(unsigned)blocks, kThreads, 0, a.st>>>(
         a.units, a.num_units, a.cols, a.num_edges, (const T*)a.w, a.widx, a.heads, a.fh,
         (const T*)a.x, (T*)a.y, a.carry, a.F, a.ldx, a.ldy, a.fmode, (const T*)a.fout,
-        a.wld, a.w2off, (T*)a.out2, a.carry2);
+        a.wld, a.w2off, (T*)a.out2, a.carry2, a.offsets, nullptr);
+    HG_LAUNCHED();
+  }
+  if (a.num_packs > 0) {
+    int64_t blocks = (a.num_packs + teams_per_block - 1) / teams_per_block;
+    k_spmm_fast<T, V, TEAM, NCH, WT, SUMW, true><<<(unsigned)blocks, kThreads, 0, a.st>>>(
+        a.packs, a.num_packs, a.cols, a.num_edges, (const T*)a.w, a.widx, a.heads, a.fh,
+        (const T*)a.x, (T*)a.y, nullptr, a.F, a.ldx, a.ldy, a.fmode, (const T*)a.fout,
+        a.wld, a.w2off, (T*)a.out2, nullptr, a.offsets, a.rowid);
     HG_LAUNCHED();
   }
   if (a.num_split > 0) {
@@ -571,6 +711,7 @@ extern "C" int hg_spmm_workspace(int64_t n_cols, int32_t F, int64_t num_slots, i
 extern "C" int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_rows,
                        int64_t n_cols, int64_t num_edges, const int32_t* units, int64_t num_units,
                        const int32_t* split_rows, int64_t num_split_rows, int64_t num_slots,
+                       const int32_t* packs, int64_t num_packs, const int32_t* pack_rowid,
                        const void* w, const int32_t* w_index, int32_t heads, const void* x,
                        void* y, int32_t F, int64_t ldx, int64_t ldy, int32_t scaling,
                        int32_t relu, const void* in_scale, const void* out_factor,
@@ -612,6 +753,9 @@ extern "C" int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_ro
   a.num_edges = num_edges;
   a.units = reinterpret_cast<const int4*>(units); a.num_units = num_units;
   a.split_rows = reinterpret_cast<const int4*>(split_rows); a.num_split = num_split_rows;
+  a.packs = reinterpret_cast<const int4*>(packs); a.num_packs = packs ? num_packs : 0;
+  a.rowid = pack_rowid;
+  HG_REQUIRE(a.num_packs == 0 || num_edges == 0 || pack_rowid, "hg_spmm: packs need pack_rowid");
   a.w = w; a.widx = w_index; a.heads = heads; a.fh = F / heads;
   a.x = x; a.y = y; a.carry = carry; a.F = F; a.ldx = (int)ldx; a.ldy = (int)ldy;
   a.fmode = (out_factor == nullptr ? 0 : (scaling == HG_SCALING_POST ? 1 : 2)) | (relu ? 4 : 0);
@@ -951,6 +1095,67 @@ extern "C" int hg_spmm_vertex_ref(const int64_t* offsets, const int32_t* cols, i
                                                 (float*)y, F, scaling, (const float*)out_factor,
                                                 group_base, (float*)staging_partials,
                                                 staging_rows);
+  HG_LAUNCHED();
+  return HG_OK;
+}
+
+// ── Gather ceiling probe (measurement only) ───────────────────────────────────
+// The memory access of one SpMM with all arithmetic, scheduling and output
+// removed: the column ids streamed once in edge order, and for every edge the
+// row_bytes of X at its column fetched with 16-byte loads by a power-of-two lane
+// team (the k_spmm_fast team shape).  Its time is the floor any gather SpMM on
+// that graph and width can reach; bench.py reports hg_spmm's time against it.
+namespace hg {
+template <int TEAM>
+__global__ void __launch_bounds__(256) k_gather_probe(const int* __restrict__ cols, int64_t E,
+                                                      const int4* __restrict__ x, int64_t ldv,
+                                                      int lanes, unsigned* __restrict__ out) {
+  constexpr int RPL = 32 / TEAM;  // rows fetched per warp load
+  const int lane = threadIdx.x & 31;
+  const int sub = lane % TEAM, slot = lane / TEAM;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned acc = 0;
+  for (int64_t base = warp * 32; base < E; base += nwarps * 32) {
+    const int c = base + lane < E ? __ldg(cols + base + lane) : -1;
+    int4 v[TEAM];
+#pragma unroll
+    for (int k = 0; k < TEAM; ++k) {
+      const int r = __shfl_sync(0xffffffffu, c, k * RPL + slot);
+      v[k] = (r >= 0 && sub < lanes) ? __ldg(x + (int64_t)r * ldv + sub) : make_int4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < TEAM; ++k) acc ^= (unsigned)(v[k].x ^ v[k].y ^ v[k].z ^ v[k].w);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc ^= __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0 && acc == 0x9e3779b9u) atomicXor(out, acc);  // keeps the loads live
+}
+}  // namespace hg
+
+extern "C" int hg_gather_probe(const int32_t* cols, int64_t num_edges, const void* x,
+                               int32_t row_bytes, int64_t ld_bytes, uint32_t* out, void* stream) {
+  HG_REQUIRE(row_bytes > 0 && row_bytes % 16 == 0 && row_bytes <= 512,
+             "hg_gather_probe: row_bytes %d must be a multiple of 16 in [16, 512]", row_bytes);
+  HG_REQUIRE(ld_bytes % 16 == 0 && ld_bytes >= row_bytes && num_edges >= 0,
+             "hg_gather_probe: bad row stride");
+  HG_REQUIRE(reinterpret_cast<uintptr_t>(x) % 16 == 0, "hg_gather_probe: x must be 16-byte aligned");
+  if (num_edges == 0) return HG_OK;
+  cudaStream_t st = as_stream(stream);
+  const int lanes = row_bytes / 16;
+  const int64_t ldv = ld_bytes / 16;
+  int sms = 148;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned g = (unsigned)sms * 8;
+  const int4* xv = (const int4*)x;
+  unsigned* o = (unsigned*)out;
+  if (lanes <= 1) k_gather_probe<1><<<g, 256, 0, st>>>(cols, num_edges, xv, ldv, lanes, o);
+  else if (lanes <= 2) k_gather_probe<2><<<g, 256, 0, st>>>(cols, num_edges, xv, ldv, lanes, o);
+  else if (lanes <= 4) k_gather_probe<4><<<g, 256, 0, st>>>(cols, num_edges, xv, ldv, lanes, o);
+  else if (lanes <= 8) k_gather_probe<8><<<g, 256, 0, st>>>(cols, num_edges, xv, ldv, lanes, o);
+  else if (lanes <= 16) k_gather_probe<16><<<g, 256, 0, st>>>(cols, num_edges, xv, ldv, lanes, o);
+  else k_gather_probe<32><<<g, 256, 0, st>>>(cols, num_edges, xv, ldv, lanes, o);
   HG_LAUNCHED();
   return HG_OK;
 }

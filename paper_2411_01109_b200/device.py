@@ -18,6 +18,7 @@ Features are row-major [rows, F] fp16 (or fp32 in float32 mode).
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 
 import torch
@@ -27,6 +28,14 @@ from . import _native as nat
 DTYPE_CODE = {torch.float16: nat.HG_F16, torch.float32: nat.HG_F32}
 MIRROR = {"none": "none", "left": "right", "right": "left", "both": "both"}
 DEFAULT_SPLIT_CAP = 512
+# hg_spmm packs: aligned blocks of PACK_ROWS rows of degree <= PACK_DEG walked
+# by one team as one edge stream (hg_schedule_build)
+PACK_ROWS = 16
+PACKING = os.environ.get("HG_SPMM_PACKS", "1") != "0"  # A/B switch for measurement
+# row-degree bound of a pack by output row width: wide rows (>= 256 bytes, lane
+# teams of 16+) pack short rows; narrower teams pack only all-empty blocks
+PACK_DEG_WIDE = int(os.environ.get("HG_PACK_DEG_WIDE", "32"))
+PACK_DEG_NARROW = int(os.environ.get("HG_PACK_DEG_NARROW", "0"))
 LONG_ROW = 4096   # rows longer than this get a whole CTA in the row-owned softmax/sum kernels
 SHORT_ROW = 32    # fast GAT kernels: rows up to this many edges get one thread per head
 
@@ -56,12 +65,15 @@ class Probe:
 
     launches = 0
     timing = False
+    keep = False
     records = []
 
     @classmethod
-    def reset(cls, timing=False):
+    def reset(cls, timing=False, keep=False):
+        """keep: also hold each call's (cols, edges, x, F) for gather_ceiling."""
         cls.launches = 0
         cls.timing = timing
+        cls.keep = keep
         cls.records = []
 
     @classmethod
@@ -76,6 +88,37 @@ class Probe:
     def compulsory_per_launch(cls):
         """Mean compulsory DRAM bytes per timed spmm call."""
         return sum(r[3] for r in cls.records) / max(len(cls.records), 1)
+
+    @classmethod
+    def gather_ceiling(cls, reps=3):
+        """Seconds the timed spmm calls' gathers alone take (hg_gather_probe on
+        the same column ids, feature buffer and width, X warm in L2 as after
+        the producing kernel): the floor those calls could reach.  None when a
+        call's row exceeds the probe's 512 bytes."""
+        total = 0.0
+        for r in cls.records:
+            cols, ne, x, f = r[4]
+            row_bytes = -(-f * x.element_size() // 16) * 16
+            ld = x.stride(0) * x.element_size()
+            if row_bytes > 512 or ld < row_bytes or ld % 16 or x.data_ptr() % 16:
+                return None
+            gather_probe(cols, ne, x, row_bytes)
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            for _ in range(reps):
+                gather_probe(cols, ne, x, row_bytes)
+            ev1.record()
+            torch.cuda.synchronize()
+            total += ev0.elapsed_time(ev1) / 1e3 / reps
+        return total
+
+
+def gather_probe(cols, num_edges, x, row_bytes):
+    """hg_gather_probe over cols[:num_edges] into x's rows (measurement only)."""
+    sink = workspace(16, x.device)
+    nat.call("hg_gather_probe", _p(cols), int(num_edges), _p(x), int(row_bytes),
+             x.stride(0) * x.element_size(), _p(sink), _stream())
 
 
 def compulsory_bytes(n_rows, n_cols, num_edges, f, heads=0, elem=2):
@@ -236,13 +279,21 @@ class WorkSchedule:
     split_rows: torch.Tensor  # int32 [S, 4] {row, first_slot, nparts, 0}
     num_slots: int
     split_cap: int
+    packs: torch.Tensor | None = None  # int32 [P, 4] {first_row, begin, end, rows}
+
+    @property
+    def num_packs(self):
+        return 0 if self.packs is None else self.packs.shape[0]
 
     @property
     def num_units(self):
         return self.units.shape[0]
 
 
-def build_schedule(offsets: torch.Tensor, split_cap: int = DEFAULT_SPLIT_CAP) -> WorkSchedule:
+def build_schedule(offsets: torch.Tensor, split_cap: int = DEFAULT_SPLIT_CAP,
+                   pack_rows: int = 0, pack_deg: int = 0) -> WorkSchedule:
+    """pack_rows > 0: aligned blocks of pack_rows rows of degree <= pack_deg
+    become packs (hg_spmm only; the other unit consumers take pack_rows = 0)."""
     n = offsets.numel() - 1
     m = int(offsets[-1].item())
     dev = offsets.device
@@ -250,11 +301,15 @@ def build_schedule(offsets: torch.Tensor, split_cap: int = DEFAULT_SPLIT_CAP) ->
     max_split = max(1, (m + split_cap - 1) // split_cap)
     units = torch.empty((max_units, 4), dtype=torch.int32, device=dev)
     split = torch.empty((max_split, 4), dtype=torch.int32, device=dev)
+    max_packs = -(-n // pack_rows) if pack_rows else 0
+    packs = torch.empty((max(max_packs, 1), 4), dtype=torch.int32, device=dev)
     ws = workspace(nat.size_query("hg_schedule_workspace", n, m, split_cap), dev)
-    counts = (ctypes.c_int64 * 3)()
-    nat.call("hg_schedule_build", _p(offsets), n, split_cap, _p(units), max_units, _p(split),
-             max_split, counts, _p(ws), 0 if ws is None else ws.numel(), _stream())
-    return WorkSchedule(units[: counts[0]], split[: counts[1]], int(counts[2]), split_cap)
+    counts = (ctypes.c_int64 * 4)()
+    nat.call("hg_schedule_build", _p(offsets), n, split_cap, pack_rows, pack_deg, _p(units),
+             max_units, _p(split), max_split, _p(packs), max_packs, counts, _p(ws),
+             0 if ws is None else ws.numel(), _stream())
+    return WorkSchedule(units[: counts[0]], split[: counts[1]], int(counts[2]), split_cap,
+                        packs[: counts[3]] if pack_rows else None)
 
 
 @dataclass
@@ -273,12 +328,29 @@ class CsrView:
     def num_edges(self):
         return self.cols.numel()
 
-    def schedule(self, split_cap: int = DEFAULT_SPLIT_CAP) -> WorkSchedule:
-        s = self._sched.get(split_cap)
+    def schedule(self, split_cap: int = DEFAULT_SPLIT_CAP, pack_deg: int = -1) -> WorkSchedule:
+        """Work units (cached); pack_deg >= 0: aligned blocks of PACK_ROWS rows
+        of degree <= pack_deg become packs (hg_spmm only)."""
+        key = (split_cap, pack_deg)
+        s = self._sched.get(key)
         if s is None:
-            s = build_schedule(self.offsets, split_cap)
-            self._sched[split_cap] = s
+            if pack_deg >= 0:
+                s = build_schedule(self.offsets, split_cap, PACK_ROWS,
+                                   min(pack_deg, split_cap // PACK_ROWS))
+            else:
+                s = build_schedule(self.offsets, split_cap)
+            self._sched[key] = s
         return s
+
+    def row_ids(self) -> torch.Tensor:
+        """int32 local row id per edge (cached; the packed SpMM's row stream)."""
+        t = self._sched.get("row_ids")
+        if t is None:
+            deg = self.offsets[1:] - self.offsets[:-1]
+            t = torch.repeat_interleave(
+                torch.arange(self.n_rows, device=self.offsets.device, dtype=torch.int32), deg)
+            self._sched["row_ids"] = t
+        return t
 
     def row_classes(self, short_max: int = SHORT_ROW, long_min: int = LONG_ROW):
         """(medium, long) int32 row ids: short_max < deg <= long_min, and
@@ -407,7 +479,10 @@ def spmm_csr(view: CsrView, x: torch.Tensor, w=None, w_index=None, heads: int = 
         raise ValueError(f"feature tensor has {x.shape[0]} rows for {view.n_cols} columns")
     f = x.shape[1]
     dt = _dtype_code(x)
-    sched = view.schedule(split_cap)
+    pack_deg = -1
+    if PACKING:
+        pack_deg = PACK_DEG_WIDE if f * x.element_size() >= 256 else PACK_DEG_NARROW
+    sched = view.schedule(split_cap, pack_deg)
     if out is None:
         out = torch.empty((view.n_rows, f), dtype=x.dtype, device=x.device)
     elif not _row_strided(out) or out.shape != (view.n_rows, f) or out.dtype != x.dtype:
@@ -429,11 +504,13 @@ def spmm_csr(view: CsrView, x: torch.Tensor, w=None, w_index=None, heads: int = 
         ev0.record()
     nat.call("hg_spmm", _p(view.offsets), _p(view.cols), view.n_rows, view.n_cols,
              view.num_edges, _p(sched.units), sched.num_units, _p(sched.split_rows),
-             sched.split_rows.shape[0], sched.num_slots, _p(w), _p(w_index), heads, _p(x),
+             sched.split_rows.shape[0], sched.num_slots, _p(sched.packs), sched.num_packs,
+             _p(view.row_ids() if sched.num_packs else None), _p(w), _p(w_index), heads, _p(x),
              _p(out), f, x.stride(0), out.stride(0), nat.SCALING_CODES[scaling], int(relu),
              _p(fin), _p(fout), w_ld, int(w2_off), _p(out2), dt, _p(ws),
              0 if ws is None else ws.numel(), _stream())
-    Probe.launches += int(sched.num_units > 0) + int(sched.split_rows.shape[0] > 0) + int(
+    Probe.launches += int(sched.num_units > 0) + int(sched.num_packs > 0) + int(
+        sched.split_rows.shape[0] > 0) + int(
         fin is not None)
     if Probe.timing:
         ev1.record()
@@ -442,7 +519,8 @@ def spmm_csr(view: CsrView, x: torch.Tensor, w=None, w_index=None, heads: int = 
                                                    x.element_size()),
                               compulsory_bytes(view.n_rows, view.n_cols, view.num_edges, f,
                                                heads if w is not None else 0,
-                                               x.element_size())))
+                                               x.element_size()),
+                              (view.cols, view.num_edges, x, f) if Probe.keep else None))
     return out
 
 

@@ -108,6 +108,89 @@ def test_schedule_matches_restatement(cuda, cap):
     assert s.num_slots == slots
 
 
+def _short_row_graph(seed, n):
+    """Mostly short and empty rows (packs) with a few long and split rows."""
+    rng = np.random.default_rng(seed)
+    deg = rng.choice([0, 0, 0, 1, 2, 3, 5, 9, 17, 32], size=n)
+    deg[n // 3: n // 3 + min(n // 3, 1000)] = 0   # a run of empty rows (empty-only packs)
+    deg[rng.integers(0, n, 6)] = [33, 100, 600, 2000, 40, 5000]
+    rows = np.repeat(np.arange(n), deg)
+    return O.canonical_edges(n, rows, rng.integers(0, n, rows.size))
+
+
+@pytest.mark.parametrize("n", [16, 1001, 40000])
+def test_schedule_packs_match_restatement(cuda, n):
+    from paper_2411_01109_b200 import device as D
+
+    r, c = _short_row_graph(n, n)
+    off = O.csr_offsets(n, r)
+    s = D.build_schedule(_t(off, cuda), 512, 16, 32)
+    units, split_rows, slots, packs = O.schedule_units(off, 512, 16, 32)
+    np.testing.assert_array_equal(s.units.cpu().numpy(), units)
+    np.testing.assert_array_equal(s.split_rows.cpu().numpy(), split_rows)
+    np.testing.assert_array_equal(s.packs.cpu().numpy(), packs)
+    assert s.num_slots == slots
+    # every row is covered exactly once by units or packs
+    cover = np.zeros(n, np.int64)
+    np.add.at(cover, units[:, 0][units[:, 3] < 0], 1)
+    np.add.at(cover, split_rows[:, 0], 1)
+    for r0, _, _, cnt in packs:
+        cover[r0:r0 + cnt] += 1
+    assert (cover == 1).all()
+
+
+@pytest.mark.parametrize("pack_deg", [0, 32])
+@pytest.mark.parametrize("f", [8, 48, 64, 128, 512])
+@pytest.mark.parametrize("mode", ["plain", "weighted", "perm", "sumw"])
+def test_spmm_packed_rows_bitwise_equal_units(cuda, f, mode, pack_deg):
+    """Packed short rows (one team walking a run of rows as one edge stream)
+    give bit-identical output to the same rows as separate units, for every
+    team width, weights direct / through perm, output factors, ReLU and the
+    summed second weight block."""
+    from paper_2411_01109_b200 import device as D
+
+    n = 30000
+    r, c = _short_row_graph(f, n)
+    dg = _dg(n, r, c, cuda)
+    heads = 4 if f % 32 == 0 else 1
+    if mode == "sumw" and f > 256:
+        pytest.skip("summed weights need F/8 <= 32")
+    x = torch.randn(n, f, device=cuda, dtype=torch.float16)
+    fout = torch.rand(n, device=cuda, dtype=torch.float16)
+    view = dg.view(mode in ("perm", "sumw"))
+    e = r.size
+    w = widx = w2 = out2 = None
+    kw = {}
+    if mode == "weighted":
+        w = torch.randn(e, heads, device=cuda, dtype=torch.float16)
+    elif mode in ("perm", "sumw"):
+        ae = torch.randn(e, 2 * heads, device=cuda, dtype=torch.float16)
+        w, widx = ae[:, :heads], view.perm
+        if mode == "sumw":
+            kw = dict(w2_off=heads)
+    outs = []
+    saved = (D.PACK_DEG_WIDE, D.PACK_DEG_NARROW)
+    D.PACK_DEG_WIDE = D.PACK_DEG_NARROW = pack_deg
+    for packing in (False, True):
+        D.PACKING = packing
+        try:
+            extra = {}
+            if mode == "sumw":
+                extra["out2"] = torch.empty(n, heads, device=cuda, dtype=torch.float16)
+            y = D.spmm_csr(view, x, w, widx, heads if w is not None else 1, "discretized",
+                           fout=fout, relu=(mode == "plain"), **kw, **extra)
+            outs.append((y, extra.get("out2")))
+        finally:
+            D.PACKING = True
+    D.PACK_DEG_WIDE, D.PACK_DEG_NARROW = saved
+    if pack_deg > 0 or mode in ("plain", "weighted"):  # (the empty run is in CSR rows)
+        assert view.schedule(pack_deg=pack_deg).num_packs > 0
+    np.testing.assert_array_equal(bits(outs[0][0].cpu().numpy()), bits(outs[1][0].cpu().numpy()))
+    if mode == "sumw":
+        np.testing.assert_array_equal(bits(outs[0][1].cpu().numpy()),
+                                      bits(outs[1][1].cpu().numpy()))
+
+
 # ── reference-order SpMM (bit-exact) ─────────────────────────────────────
 
 
@@ -829,6 +912,29 @@ def test_gather_rows(cuda, shape):
     idx = rng.permutation(shape[0]).astype(np.int32)
     got = D.gather_rows(_t(src, cuda), _t(idx, cuda)).cpu().numpy()
     np.testing.assert_array_equal(bits(got), bits(src[idx]))
+
+
+@pytest.mark.parametrize("f", [8, 48, 64, 128, 256])
+def test_gather_probe_runs_and_times_below_spmm(cuda, f):
+    """hg_gather_probe (bench's gather floor) runs for every team width, leaves
+    its sink alone, and the Probe ceiling path returns a time."""
+    from paper_2411_01109_b200 import device as D
+
+    n = 20000
+    r, c = _hub_graph(f, n)
+    dg = _dg(n, r, c, cuda)
+    x = torch.randn(n, f, device=cuda, dtype=torch.float16)
+    view = dg.view(False)
+    D.gather_probe(view.cols, view.num_edges, x, f * 2)
+    D.gather_probe(view.cols, 0, x, f * 2)
+    with pytest.raises(Exception):
+        D.gather_probe(view.cols, view.num_edges, x, 1024)
+    D.Probe.reset(timing=True, keep=True)
+    D.spmm_csr(view, x, None, None, 1, "post")
+    ceil = D.Probe.gather_ceiling()
+    D.Probe.reset()
+    torch.cuda.synchronize()
+    assert ceil is not None and ceil > 0
 
 
 @pytest.mark.parametrize("heads,fh", [(4, 32), (4, 16), (2, 64), (1, 128), (8, 8)])

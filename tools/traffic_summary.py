@@ -1,15 +1,18 @@
 """Per-launch DRAM traffic of the dominant kernel from an ncu CSV taken with
 --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum.
-Writes the JSON bench.py reads for roofline.traffic."""
+Merges one workload's entry into the JSON bench.py reads for roofline.traffic.
+
+usage: traffic_summary.py CSV OUT.json WORKLOAD LAUNCHES_PER_EPOCH [source words...]"""
 from __future__ import annotations
 
 import collections
 import csv
 import json
 import sys
+from pathlib import Path
 
 
-def main(path, out, pattern="k_spmm_fast<", last=4, source=""):
+def main(path, out, workload, last, pattern="k_spmm_fast<", source=""):
     rows = list(csv.reader(open(path)))
     h = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     hdr = rows[h]
@@ -24,12 +27,14 @@ def main(path, out, pattern="k_spmm_fast<", last=4, source=""):
     ids = [i for i in sorted(per) if pattern in names[i]][-last:]
     bytes_ = [per[i]["dram__bytes_read.sum"] + per[i]["dram__bytes_write.sum"] for i in ids]
     ns = [per[i]["gpu__time_duration.sum"] for i in ids]
-    d = {"gcn_epoch": sum(bytes_) / len(bytes_), "gcn_epoch_per_launch_bytes": bytes_,
-         "gcn_epoch_per_launch_ns": ns, "kernels": [names[i][:80] for i in ids],
-         "source": source}
-    json.dump(d, open(out, "w"), indent=1)
-    print(json.dumps(d))
+    entry = {"bytes_per_launch": sum(bytes_) / len(bytes_), "per_launch_bytes": bytes_,
+             "per_launch_ns": ns, "kernels": [names[i][:80] for i in ids], "source": source}
+    p = Path(out)
+    d = json.loads(p.read_text()) if p.exists() else {}
+    d[workload] = entry
+    p.write_text(json.dumps(d, indent=1))
+    print(json.dumps(entry))
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], source=" ".join(sys.argv[3:]))
+    main(sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4]), source=" ".join(sys.argv[5:]))
