@@ -158,7 +158,7 @@ __device__ __forceinline__ float chunk_dot_f32(const typename RawV<V * sizeof(T)
 }
 
 template <typename T, int V, int TEAM, int G>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
 k_sddmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __restrict__ cols,
              const T* __restrict__ x, const T* __restrict__ y, T* __restrict__ out, int F,
              int heads) {
@@ -169,26 +169,43 @@ k_sddmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* _
   const int tl = lane & (TEAM - 1);
   const unsigned tmask =
       TEAM == 32 ? 0xffffffffu : (((1u << TEAM) - 1u) << (lane & ~(TEAM - 1)));
-  const int64_t team = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TEAM;
-  if (team >= num_units) return;
-  const int4 un = units[team];
-  const int row = un.x, beg = un.y, end = un.z;
   const int nvec = F / V;
   const bool cval = tl < nvec;
   const int hd = tl / G, gp = tl & (G - 1);  // head, position inside the head's lane group
+  // Persistent teams walk the unit list with stride nteams; the next unit's
+  // descriptor is fetched before the current one is processed.
+  const int64_t nteams = ((int64_t)gridDim.x * blockDim.x) / TEAM;
+  int64_t team = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TEAM;
+  if (team >= num_units) return;
+  int4 un = units[team];
+  for (;;) {
+  const int64_t nxt_team = team + nteams;
+  const int4 nxt = nxt_team < num_units ? units[nxt_team] : make_int4(0, 0, 0, 0);
+  const int row = un.x, beg = un.y, end = un.z;
   Raw xr;
   if (cval) xr = *reinterpret_cast<const Raw*>(x + (int64_t)row * F + tl * V);
-  int cj[EB];
+  // column ids spread over the team: lane tl holds edges base + tl + q*TEAM
+  constexpr int IDS = (EB + TEAM - 1) / TEAM;
+  const int tb = lane & ~(TEAM - 1);
+  int cq[IDS];
 #pragma unroll
-  for (int j = 0; j < EB; ++j) cj[j] = beg + j < end ? __ldg(cols + beg + j) : 0;
+  for (int q = 0; q < IDS; ++q) {
+    const int j = tl + q * TEAM;
+    cq[q] = (j < EB && beg + j < end) ? __ldcs(cols + beg + j) : 0;
+  }
   for (int base = beg; base < end; base += EB) {
-    int nj[EB];
+    int nq[IDS];
 #pragma unroll
-    for (int j = 0; j < EB; ++j) nj[j] = base + EB + j < end ? __ldg(cols + base + EB + j) : 0;
+    for (int q = 0; q < IDS; ++q) {
+      const int j = tl + q * TEAM;
+      nq[q] = (j < EB && base + EB + j < end) ? __ldcs(cols + base + EB + j) : 0;
+    }
     Raw yr[EB];
 #pragma unroll
-    for (int j = 0; j < EB; ++j)
-      if (base + j < end && cval) yr[j] = __ldg(reinterpret_cast<const Raw*>(y + (int64_t)cj[j] * F + tl * V));
+    for (int j = 0; j < EB; ++j) {
+      const int c = __shfl_sync(tmask, cq[j / TEAM], tb + j % TEAM);
+      if (base + j < end && cval) yr[j] = __ldg(reinterpret_cast<const Raw*>(y + (int64_t)c * F + tl * V));
+    }
     float v[EB];
 #pragma unroll
     for (int j = 0; j < EB; ++j) v[j] = (base + j < end && cval) ? chunk_dot_f32<T, V>(xr, yr[j]) : 0.0f;
@@ -219,7 +236,11 @@ k_sddmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* _
       }
     }
 #pragma unroll
-    for (int j = 0; j < EB; ++j) cj[j] = nj[j];
+    for (int q = 0; q < IDS; ++q) cq[q] = nq[q];
+  }
+  if (nxt_team >= num_units) break;
+  team = nxt_team;
+  un = nxt;
   }
 }
 
@@ -232,7 +253,13 @@ static int launch_sddmm_fast(const int4* units, int64_t nu, const int32_t* cols,
                              const void* y, void* out, int F, int heads, cudaStream_t st) {
   constexpr int tpb = 256 / TEAM;
   if (nu == 0) return HG_OK;
-  k_sddmm_fast<T, V, TEAM, G><<<(unsigned)((nu + tpb - 1) / tpb), 256, 0, st>>>(
+  int sms = 148, dev = 0, occ = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sddmm_fast<T, V, TEAM, G>, 256, 0);
+  const int64_t need = (nu + tpb - 1) / tpb;
+  const int64_t cap = (int64_t)sms * (occ > 0 ? occ : 4);
+  k_sddmm_fast<T, V, TEAM, G><<<(unsigned)(need < cap ? need : cap), 256, 0, st>>>(
       units, nu, cols, (const T*)x, (const T*)y, (T*)out, F, heads);
   HG_LAUNCHED();
   return HG_OK;

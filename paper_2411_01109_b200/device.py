@@ -613,8 +613,8 @@ def sddmm(dg: DeviceGraph, x, y, heads=1, transpose=False, fast=False):
     if x.shape[1] != y.shape[1]:
         raise ValueError("operand feature lengths differ")
     f = x.shape[1]
-    sched = view.schedule()
     out = torch.empty((view.num_edges, heads), dtype=x.dtype, device=x.device)
+    sched = view.schedule()
     nat.call("hg_sddmm_fast" if fast else "hg_sddmm", _p(view.offsets), _p(view.cols),
              view.n_rows, view.num_edges, _p(sched.units), sched.num_units, _p(x), _p(y),
              _p(out), f, heads, _dtype_code(x), _stream())
