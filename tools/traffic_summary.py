@@ -2,7 +2,9 @@
 --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum.
 Merges one workload's entry into the JSON bench.py reads for roofline.traffic.
 
-usage: traffic_summary.py CSV OUT.json WORKLOAD LAUNCHES_PER_EPOCH [source words...]"""
+usage: traffic_summary.py CSV OUT.json WORKLOAD KERNELS CALLS [source words...]
+(the last KERNELS launches matching k_spmm_fast -- unit, packed and follow-up
+kernels -- summed and divided by the CALLS hg_spmm calls they belong to)."""
 from __future__ import annotations
 
 import collections
@@ -12,7 +14,7 @@ import sys
 from pathlib import Path
 
 
-def main(path, out, workload, last, pattern="k_spmm_fast<", source=""):
+def main(path, out, workload, last, calls, pattern="k_spmm_fast", source=""):
     rows = list(csv.reader(open(path)))
     h = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     hdr = rows[h]
@@ -27,7 +29,7 @@ def main(path, out, workload, last, pattern="k_spmm_fast<", source=""):
     ids = [i for i in sorted(per) if pattern in names[i]][-last:]
     bytes_ = [per[i]["dram__bytes_read.sum"] + per[i]["dram__bytes_write.sum"] for i in ids]
     ns = [per[i]["gpu__time_duration.sum"] for i in ids]
-    entry = {"bytes_per_launch": sum(bytes_) / len(bytes_), "per_launch_bytes": bytes_,
+    entry = {"bytes_per_launch": sum(bytes_) / calls, "calls": calls, "per_launch_bytes": bytes_,
              "per_launch_ns": ns, "kernels": [names[i][:80] for i in ids], "source": source}
     p = Path(out)
     d = json.loads(p.read_text()) if p.exists() else {}
@@ -37,4 +39,5 @@ def main(path, out, workload, last, pattern="k_spmm_fast<", source=""):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4]), source=" ".join(sys.argv[5:]))
+    main(sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4]), int(sys.argv[5]),
+         source=" ".join(sys.argv[6:]))
