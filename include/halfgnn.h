@@ -79,9 +79,9 @@ int hg_degree_factors(const int64_t* offsets, int64_t n, int kind, int dtype, vo
  * Units are ordered by descending length class floor(log2(len))+1, rows
  * ascending inside a class (stable).  split_rows receives {row, first_slot,
  * nparts, 0} for every row with nparts > 1, rows ascending.
- * Packing (pack_rows > 0: a power of two in [2, 16], pack_rows * pack_deg <=
- * split_cap): every aligned block of pack_rows rows [k*pack_rows, ...) whose
- * rows all have degree <= pack_deg becomes one pack {first_row, begin, end,
+ * Packing (pack_rows > 0: a power of two in [2, 16], 0 <= pack_edges <=
+ * split_cap): every aligned block of pack_rows rows [k*pack_rows, ...) holding
+ * at most pack_edges edges in total becomes one pack {first_row, begin, end,
  * rows} (int32 x4, rows ascending) instead of per-row units -- short rows
  * walked as one edge stream by hg_spmm, so a run of near-empty rows costs one
  * team, not one dependent load chain per row.  pack_rows = 0: no packs.
@@ -91,7 +91,7 @@ int hg_degree_factors(const int64_t* offsets, int64_t n, int kind, int dtype, vo
  * Synchronises `stream`. */
 int hg_schedule_workspace(int64_t n, int64_t num_edges, int32_t split_cap, size_t* bytes);
 int hg_schedule_build(const int64_t* offsets, int64_t n, int32_t split_cap, int32_t pack_rows,
-                      int32_t pack_deg, int32_t* units, int64_t max_units, int32_t* split_rows,
+                      int32_t pack_edges, int32_t* units, int64_t max_units, int32_t* split_rows,
                       int64_t max_split, int32_t* packs, int64_t max_packs,
                       int64_t* counts_out, void* ws, size_t ws_bytes, void* stream);
 

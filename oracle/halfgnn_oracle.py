@@ -412,13 +412,13 @@ def edge_softmax_bwd(offsets, alpha, g):
 # ── scheduler and partitioner restatements (build-specified integer maps) ─
 
 
-def schedule_units(offsets, cap, pack_rows=0, pack_deg=0):
+def schedule_units(offsets, cap, pack_rows=0, pack_edges=0):
     """Restatement of hg_schedule_build (include/halfgnn.h): the degree-bucketed
     work units that replace simt.plan_edge_parallel / plan_vertex_grouped
     (simt.py:158-201) for the fp32-guarded kernels.  Returns (units (U,4) int32,
     split_rows (S,4) int32, num_slots), plus packs (P,4) int32 {first_row,
-    begin, end, rows} when pack_rows > 0 (aligned blocks of pack_rows rows all
-    of degree <= pack_deg; their rows get no units)."""
+    begin, end, rows} when pack_rows > 0 (aligned blocks of pack_rows rows with
+    at most pack_edges edges in total; their rows get no units)."""
     offsets = np.asarray(offsets, np.int64)
     n = offsets.size - 1
     deg = np.diff(offsets)
@@ -426,9 +426,8 @@ def schedule_units(offsets, cap, pack_rows=0, pack_deg=0):
     packs = np.zeros((0, 4), np.int32)
     if pack_rows:
         nb = -(-n // pack_rows)
-        short = np.ones(nb * pack_rows, bool)
-        short[:n] = deg <= pack_deg
-        blk = short.reshape(nb, pack_rows).all(axis=1)
+        r0 = np.arange(nb) * pack_rows
+        blk = offsets[np.minimum(r0 + pack_rows, n)] - offsets[r0] <= pack_edges
         nparts = np.where(np.repeat(blk, pack_rows)[:n], 0, nparts)
         r0 = np.flatnonzero(blk) * pack_rows
         cnt = np.minimum(pack_rows, n - r0)

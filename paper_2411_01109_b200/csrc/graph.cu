@@ -298,11 +298,12 @@ namespace hg {
 static constexpr int kNumClasses = 33;  // len 0 -> class 0, else floor(log2(len)) + 1
 
 // Per row: unit count, carry slots, split flag; with packing (pack_rows > 0, a
-// power of two <= 32) a row inside an aligned block of pack_rows rows that all
-// have degree <= pack_deg gets no unit -- the block becomes one pack, flagged
-// at its first row.  Blocks are whole half/quarter warps (blockDim % 32 == 0).
+// power of two <= 32) a row inside an aligned block of pack_rows rows holding
+// at most pack_edges edges in total gets no unit -- the block becomes one pack,
+// flagged at its first row.  Blocks are whole half/quarter warps
+// (blockDim % 32 == 0).
 __global__ void k_unit_counts(const int64_t* __restrict__ offsets, int64_t n, int64_t cap,
-                              int pack_rows, int64_t pack_deg,
+                              int pack_rows, int64_t pack_edges,
                               int64_t* __restrict__ nparts, int64_t* __restrict__ split_parts,
                               int64_t* __restrict__ split_flag, int64_t* __restrict__ pack_flag) {
   const int lane = threadIdx.x & 31;
@@ -312,11 +313,10 @@ __global__ void k_unit_counts(const int64_t* __restrict__ offsets, int64_t n, in
     const bool in = r < n;
     const int64_t d = in ? offsets[r + 1] - offsets[r] : 0;
     bool packed = false;
-    if (pack_rows > 0) {
-      const unsigned bal = __ballot_sync(0xffffffffu, !in || d <= pack_deg);
-      const unsigned grp = (pack_rows == 32 ? 0xffffffffu : ((1u << pack_rows) - 1u))
-                           << (lane & ~(pack_rows - 1));
-      packed = (bal & grp) == grp;
+    if (pack_rows > 0 && in) {
+      const int64_t r0 = r & ~(int64_t)(pack_rows - 1);
+      const int64_t r1 = r0 + pack_rows < n ? r0 + pack_rows : n;
+      packed = offsets[r1] - offsets[r0] <= pack_edges;
     }
     if (in) {
       const int64_t p = packed ? 0 : (d == 0 ? 1 : (d + cap - 1) / cap);
@@ -418,17 +418,17 @@ extern "C" int hg_schedule_workspace(int64_t n, int64_t m, int32_t cap, size_t* 
 }
 
 extern "C" int hg_schedule_build(const int64_t* offsets, int64_t n, int32_t cap,
-                                 int32_t pack_rows, int32_t pack_deg, int32_t* units,
+                                 int32_t pack_rows, int32_t pack_edges, int32_t* units,
                                  int64_t max_units, int32_t* split_rows, int64_t max_split,
                                  int32_t* packs, int64_t max_packs, int64_t* counts_out, void* ws,
                                  size_t ws_bytes, void* stream) {
   HG_REQUIRE(n > 0 && cap > 0 && counts_out, "hg_schedule_build: bad arguments");
   HG_REQUIRE(pack_rows == 0 || (pack_rows >= 2 && pack_rows <= kPackRows &&
-                                (pack_rows & (pack_rows - 1)) == 0 && pack_deg >= 0 &&
-                                (int64_t)pack_rows * pack_deg <= cap && packs &&
+                                (pack_rows & (pack_rows - 1)) == 0 && pack_edges >= 0 &&
+                                pack_edges <= cap && packs &&
                                 max_packs >= (n + pack_rows - 1) / pack_rows),
              "hg_schedule_build: pack_rows must be a power of two in [2, %d] with "
-             "pack_rows * pack_deg <= split_cap and room for ceil(n / pack_rows) packs",
+             "0 <= pack_edges <= split_cap and room for ceil(n / pack_rows) packs",
              kPackRows);
   HG_REQUIRE(n <= (int64_t)INT32_MAX, "hg_schedule_build: too many rows");
   cudaStream_t st = as_stream(stream);
@@ -447,7 +447,7 @@ extern "C" int hg_schedule_build(const int64_t* offsets, int64_t n, int32_t cap,
   HG_REQUIRE(cv.fits(), "hg_schedule_build: workspace too small");
 
   int g = grid_for(n, 256, 148 * 16);
-  k_unit_counts<<<g, 256, 0, st>>>(offsets, n, cap, pack_rows, pack_deg, p.nparts,
+  k_unit_counts<<<g, 256, 0, st>>>(offsets, n, cap, pack_rows, pack_edges, p.nparts,
                                    p.split_parts, p.split_flag, p.pack_flag);
   HG_LAUNCHED();
   // exclusive scans as inclusive scans shifted by one slot (base[0] = 0)

@@ -200,10 +200,13 @@ struct TeamShape {
   static constexpr int TPW = 32 / TEAM;  // teams per warp
 };
 
-template <typename T, int V, int TEAM, int NCH, bool WEIGHTED, bool SUMW = false>
+template <typename T, int V, int TEAM, int NCH, bool WEIGHTED, bool SUMW = false,
+          bool PK = false>
 struct FastTeam {
   static constexpr bool P2 = TeamShape<TEAM>::P2;
-  static constexpr int EB = NCH >= 4 ? 4 : 8;             // edges gathered per batch
+  // edges gathered per batch (packed teams: 4, the rolled accumulate shifts
+  // the batch registers once per edge)
+  static constexpr int EB = (NCH >= 4 || PK) ? 4 : 8;
   static constexpr int CPL = P2 ? (TEAM >= EB ? 1 : EB / TEAM) : (EB + TEAM - 1) / TEAM;
   using Raw = typename RawVec<V * sizeof(T)>::type;
 
@@ -352,8 +355,7 @@ struct FastTeam {
 // stream crosses its end.
 template <typename T, int V, int TEAM, int NCH, bool WEIGHTED, bool SUMW = false,
           bool PACKED = false>
-__global__ void __launch_bounds__(256, PACKED ? FastOcc<TEAM, NCH, true>::value
-                                             : FastOcc<TEAM, NCH, WEIGHTED>::value)
+__global__ void __launch_bounds__(256, (PACKED && NCH == 1) ? 4 : FastOcc<TEAM, NCH, WEIGHTED>::value)
 k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __restrict__ cols,
             int64_t num_edges, const T* __restrict__ w, const int32_t* __restrict__ widx,
             int heads, int fh, const T* __restrict__ x, T* __restrict__ y,
@@ -361,7 +363,7 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
             const T* __restrict__ fout, int wld, int w2off, T* __restrict__ out2,
             float* __restrict__ carry2, const int64_t* __restrict__ offsets,
             const int32_t* __restrict__ rowid) {
-  using Team = FastTeam<T, V, TEAM, NCH, WEIGHTED, SUMW>;
+  using Team = FastTeam<T, V, TEAM, NCH, WEIGHTED, SUMW, PACKED>;
   constexpr int EB = Team::EB;
   constexpr int CPL = Team::CPL;
   constexpr bool P2 = Team::P2;

@@ -28,14 +28,15 @@ from . import _native as nat
 DTYPE_CODE = {torch.float16: nat.HG_F16, torch.float32: nat.HG_F32}
 MIRROR = {"none": "none", "left": "right", "right": "left", "both": "both"}
 DEFAULT_SPLIT_CAP = 512
-# hg_spmm packs: aligned blocks of PACK_ROWS rows of degree <= PACK_DEG walked
+# hg_spmm packs: aligned blocks of PACK_ROWS rows with few edges in total, walked
 # by one team as one edge stream (hg_schedule_build)
 PACK_ROWS = 16
 PACKING = os.environ.get("HG_SPMM_PACKS", "1") != "0"  # A/B switch for measurement
-# row-degree bound of a pack by output row width: wide rows (>= 256 bytes, lane
-# teams of 16+) pack short rows; narrower teams pack only all-empty blocks
-PACK_DEG_WIDE = int(os.environ.get("HG_PACK_DEG_WIDE", "32"))
-PACK_DEG_NARROW = int(os.environ.get("HG_PACK_DEG_NARROW", "0"))
+# edge budget of a pack (all PACK_ROWS rows together) by output row width
+# (>= 256 bytes: wide); 0 packs only all-empty blocks.  A pack is walked by
+# one team, so the budget bounds its serial chain (profiles/r01/rowshape)
+PACK_EDGES_WIDE = int(os.environ.get("HG_PACK_EDGES_WIDE", "64"))
+PACK_EDGES_NARROW = int(os.environ.get("HG_PACK_EDGES_NARROW", "64"))
 LONG_ROW = 4096   # rows longer than this get a whole CTA in the row-owned softmax/sum kernels
 SHORT_ROW = 32    # fast GAT kernels: rows up to this many edges get one thread per head
 
@@ -291,9 +292,10 @@ class WorkSchedule:
 
 
 def build_schedule(offsets: torch.Tensor, split_cap: int = DEFAULT_SPLIT_CAP,
-                   pack_rows: int = 0, pack_deg: int = 0) -> WorkSchedule:
-    """pack_rows > 0: aligned blocks of pack_rows rows of degree <= pack_deg
-    become packs (hg_spmm only; the other unit consumers take pack_rows = 0)."""
+                   pack_rows: int = 0, pack_edges: int = 0) -> WorkSchedule:
+    """pack_rows > 0: aligned blocks of pack_rows rows holding at most
+    pack_edges edges become packs (hg_spmm only; the other unit consumers take
+    pack_rows = 0)."""
     n = offsets.numel() - 1
     m = int(offsets[-1].item())
     dev = offsets.device
@@ -305,7 +307,7 @@ def build_schedule(offsets: torch.Tensor, split_cap: int = DEFAULT_SPLIT_CAP,
     packs = torch.empty((max(max_packs, 1), 4), dtype=torch.int32, device=dev)
     ws = workspace(nat.size_query("hg_schedule_workspace", n, m, split_cap), dev)
     counts = (ctypes.c_int64 * 4)()
-    nat.call("hg_schedule_build", _p(offsets), n, split_cap, pack_rows, pack_deg, _p(units),
+    nat.call("hg_schedule_build", _p(offsets), n, split_cap, pack_rows, pack_edges, _p(units),
              max_units, _p(split), max_split, _p(packs), max_packs, counts, _p(ws),
              0 if ws is None else ws.numel(), _stream())
     return WorkSchedule(units[: counts[0]], split[: counts[1]], int(counts[2]), split_cap,
@@ -328,15 +330,15 @@ class CsrView:
     def num_edges(self):
         return self.cols.numel()
 
-    def schedule(self, split_cap: int = DEFAULT_SPLIT_CAP, pack_deg: int = -1) -> WorkSchedule:
-        """Work units (cached); pack_deg >= 0: aligned blocks of PACK_ROWS rows
-        of degree <= pack_deg become packs (hg_spmm only)."""
-        key = (split_cap, pack_deg)
+    def schedule(self, split_cap: int = DEFAULT_SPLIT_CAP, pack_edges: int = -1) -> WorkSchedule:
+        """Work units (cached); pack_edges >= 0: aligned blocks of PACK_ROWS rows
+        holding at most pack_edges edges become packs (hg_spmm only)."""
+        key = (split_cap, pack_edges)
         s = self._sched.get(key)
         if s is None:
-            if pack_deg >= 0:
+            if pack_edges >= 0:
                 s = build_schedule(self.offsets, split_cap, PACK_ROWS,
-                                   min(pack_deg, split_cap // PACK_ROWS))
+                                   min(pack_edges, split_cap))
             else:
                 s = build_schedule(self.offsets, split_cap)
             self._sched[key] = s
@@ -479,10 +481,10 @@ def spmm_csr(view: CsrView, x: torch.Tensor, w=None, w_index=None, heads: int = 
         raise ValueError(f"feature tensor has {x.shape[0]} rows for {view.n_cols} columns")
     f = x.shape[1]
     dt = _dtype_code(x)
-    pack_deg = -1
+    pack_edges = -1
     if PACKING:
-        pack_deg = PACK_DEG_WIDE if f * x.element_size() >= 256 else PACK_DEG_NARROW
-    sched = view.schedule(split_cap, pack_deg)
+        pack_edges = PACK_EDGES_WIDE if f * x.element_size() >= 256 else PACK_EDGES_NARROW
+    sched = view.schedule(split_cap, pack_edges)
     if out is None:
         out = torch.empty((view.n_rows, f), dtype=x.dtype, device=x.device)
     elif not _row_strided(out) or out.shape != (view.n_rows, f) or out.dtype != x.dtype:

@@ -124,8 +124,8 @@ def test_schedule_packs_match_restatement(cuda, n):
 
     r, c = _short_row_graph(n, n)
     off = O.csr_offsets(n, r)
-    s = D.build_schedule(_t(off, cuda), 512, 16, 32)
-    units, split_rows, slots, packs = O.schedule_units(off, 512, 16, 32)
+    s = D.build_schedule(_t(off, cuda), 512, 16, 64)
+    units, split_rows, slots, packs = O.schedule_units(off, 512, 16, 64)
     np.testing.assert_array_equal(s.units.cpu().numpy(), units)
     np.testing.assert_array_equal(s.split_rows.cpu().numpy(), split_rows)
     np.testing.assert_array_equal(s.packs.cpu().numpy(), packs)
@@ -139,10 +139,10 @@ def test_schedule_packs_match_restatement(cuda, n):
     assert (cover == 1).all()
 
 
-@pytest.mark.parametrize("pack_deg", [0, 32])
+@pytest.mark.parametrize("pack_edges", [0, 64, 512])
 @pytest.mark.parametrize("f", [8, 48, 64, 128, 512])
 @pytest.mark.parametrize("mode", ["plain", "weighted", "perm", "sumw"])
-def test_spmm_packed_rows_bitwise_equal_units(cuda, f, mode, pack_deg):
+def test_spmm_packed_rows_bitwise_equal_units(cuda, f, mode, pack_edges):
     """Packed short rows (one team walking a run of rows as one edge stream)
     give bit-identical output to the same rows as separate units, for every
     team width, weights direct / through perm, output factors, ReLU and the
@@ -169,8 +169,8 @@ def test_spmm_packed_rows_bitwise_equal_units(cuda, f, mode, pack_deg):
         if mode == "sumw":
             kw = dict(w2_off=heads)
     outs = []
-    saved = (D.PACK_DEG_WIDE, D.PACK_DEG_NARROW)
-    D.PACK_DEG_WIDE = D.PACK_DEG_NARROW = pack_deg
+    saved = (D.PACK_EDGES_WIDE, D.PACK_EDGES_NARROW)
+    D.PACK_EDGES_WIDE = D.PACK_EDGES_NARROW = pack_edges
     for packing in (False, True):
         D.PACKING = packing
         try:
@@ -182,9 +182,9 @@ def test_spmm_packed_rows_bitwise_equal_units(cuda, f, mode, pack_deg):
             outs.append((y, extra.get("out2")))
         finally:
             D.PACKING = True
-    D.PACK_DEG_WIDE, D.PACK_DEG_NARROW = saved
-    if pack_deg > 0 or mode in ("plain", "weighted"):  # (the empty run is in CSR rows)
-        assert view.schedule(pack_deg=pack_deg).num_packs > 0
+    D.PACK_EDGES_WIDE, D.PACK_EDGES_NARROW = saved
+    if mode in ("plain", "weighted"):  # (the empty run is in CSR rows)
+        assert view.schedule(pack_edges=pack_edges).num_packs > 0
     np.testing.assert_array_equal(bits(outs[0][0].cpu().numpy()), bits(outs[1][0].cpu().numpy()))
     if mode == "sumw":
         np.testing.assert_array_equal(bits(outs[0][1].cpu().numpy()),

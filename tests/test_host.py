@@ -168,3 +168,28 @@ def test_resolve_grad_scale():
     for bad in (0.5, 3.0, -2.0):
         with pytest.raises(ValueError, match="power of two"):
             resolve_grad_scale(bad, 100)
+
+
+@pytest.mark.parametrize("pack_edges", [0, 7, 64, 512])
+def test_schedule_pack_restatement_covers_rows_once(pack_edges):
+    """The oracle's hg_schedule_build restatement with packs: every row is in
+    exactly one whole-row unit, split row or pack; packs are aligned blocks of
+    16 rows within the edge budget; units never name a packed row."""
+    import numpy as np
+
+    import oracle as O
+
+    rng = np.random.default_rng(pack_edges)
+    n = 1003
+    deg = rng.choice([0, 0, 1, 2, 5, 40, 700], size=n)
+    off = np.r_[0, np.cumsum(deg)].astype(np.int64)
+    units, split_rows, slots, packs = O.schedule_units(off, 512, 16, pack_edges)
+    cover = np.zeros(n, np.int64)
+    np.add.at(cover, units[:, 0][units[:, 3] < 0], 1)
+    np.add.at(cover, split_rows[:, 0], 1)
+    for r0, beg, end, cnt in packs:
+        assert r0 % 16 == 0 and cnt == min(16, n - r0)
+        assert beg == off[r0] and end == off[r0 + cnt] and end - beg <= pack_edges
+        cover[r0:r0 + cnt] += 1
+    assert (cover == 1).all()
+    assert slots == sum(-(-d // 512) for d in deg if d > 512)
