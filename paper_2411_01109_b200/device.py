@@ -37,6 +37,9 @@ PACKING = os.environ.get("HG_SPMM_PACKS", "1") != "0"  # A/B switch for measurem
 # one team, so the budget bounds its serial chain (profiles/r01/rowshape)
 PACK_EDGES_WIDE = int(os.environ.get("HG_PACK_EDGES_WIDE", "64"))
 PACK_EDGES_NARROW = int(os.environ.get("HG_PACK_EDGES_NARROW", "64"))
+# packs trade parallelism for shorter dependent chains: only worth it when the
+# rows far outnumber the resident teams (Cora / Pubmed-sized graphs lost 3x)
+PACK_MIN_ROWS = int(os.environ.get("HG_PACK_MIN_ROWS", str(1 << 20)))
 LONG_ROW = 4096   # rows longer than this get a whole CTA in the row-owned softmax/sum kernels
 SHORT_ROW = 32    # fast GAT kernels: rows up to this many edges get one thread per head
 
@@ -482,7 +485,7 @@ def spmm_csr(view: CsrView, x: torch.Tensor, w=None, w_index=None, heads: int = 
     f = x.shape[1]
     dt = _dtype_code(x)
     pack_edges = -1
-    if PACKING:
+    if PACKING and view.n_rows >= PACK_MIN_ROWS:
         pack_edges = PACK_EDGES_WIDE if f * x.element_size() >= 256 else PACK_EDGES_NARROW
     sched = view.schedule(split_cap, pack_edges)
     if out is None:

@@ -169,8 +169,9 @@ def test_spmm_packed_rows_bitwise_equal_units(cuda, f, mode, pack_edges):
         if mode == "sumw":
             kw = dict(w2_off=heads)
     outs = []
-    saved = (D.PACK_EDGES_WIDE, D.PACK_EDGES_NARROW)
+    saved = (D.PACK_EDGES_WIDE, D.PACK_EDGES_NARROW, D.PACK_MIN_ROWS)
     D.PACK_EDGES_WIDE = D.PACK_EDGES_NARROW = pack_edges
+    D.PACK_MIN_ROWS = 0
     for packing in (False, True):
         D.PACKING = packing
         try:
@@ -182,7 +183,7 @@ def test_spmm_packed_rows_bitwise_equal_units(cuda, f, mode, pack_edges):
             outs.append((y, extra.get("out2")))
         finally:
             D.PACKING = True
-    D.PACK_EDGES_WIDE, D.PACK_EDGES_NARROW = saved
+    D.PACK_EDGES_WIDE, D.PACK_EDGES_NARROW, D.PACK_MIN_ROWS = saved
     if mode in ("plain", "weighted"):  # (the empty run is in CSR rows)
         assert view.schedule(pack_edges=pack_edges).num_packs > 0
     np.testing.assert_array_equal(bits(outs[0][0].cpu().numpy()), bits(outs[1][0].cpu().numpy()))
