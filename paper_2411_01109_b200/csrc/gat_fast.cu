@@ -190,6 +190,33 @@ d_gat_fwd_thread(int64_t blk, int64_t nblk, const int64_t* __restrict__ offsets,
   const int64_t beg = offsets[r], end = offsets[r + 1];
   if (end == beg || end - beg > short_max) return;
   const float a = Num<T>::to_f(sl[t]) * kLog2e;  // log2 domain
+  if (end - beg <= U) {
+    // one chunk (most rows of a power-law graph): the logits and their
+    // exponentials stay in registers between the two passes -- the same
+    // operations in the same order as fwd_pass1 + fwd_pass2, so bitwise equal
+    int c[U];
+    float v[U], p[U];
+    float mu = -INFINITY;
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = beg + u < end ? __ldg(cols + beg + u) : -1;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      v[u] = c[u] >= 0 ? leaky_f(fmaf(Num<T>::to_f(sr[(size_t)(unsigned)c[u] * H + h]), kLog2e, a), slope)
+                       : -INFINITY;
+      mu = fmaxf(mu, v[u]);
+    }
+    float s1 = 0.0f;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      p[u] = c[u] >= 0 ? exp2f(v[u] - mu) : 0.0f;
+      if (c[u] >= 0) s1 += p[u];
+    }
+    const float inv = 1.0f / s1;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (c[u] >= 0) alpha[(beg + u) * ald + h] = Num<T>::from_f(p[u] * inv);
+    return;
+  }
   float m = -INFINITY, s = 0.0f;
   fwd_pass1<T, H>(cols, sr, beg, end, 1, h, a, slope, m, s);
   fwd_pass2<T, H>(cols, sr, beg, end, 1, h, a, slope, m, 1.0f / s, alpha, ald);
@@ -251,8 +278,38 @@ d_gat_bwd_thread(int64_t blk, int64_t nblk, const int64_t* __restrict__ offsets,
   const int h = (int)(t - r * H);
   const int64_t beg = offsets[r], end = offsets[r + 1];
   if (end - beg > short_max) return;
-  const float d = bwd_pass1<T, H>(alpha, dalpha, beg, end, 1, h, ald);
   const float a = Num<T>::to_f(sl[t]);
+  if (end - beg <= U) {
+    // one chunk: alpha / dalpha / s_r read once (bwd_pass1 + bwd_pass2 in the
+    // same order, bitwise equal)
+    int c[U];
+    float sv[U], x[U], y[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = beg + u < end ? __ldg(cols + beg + u) : -1;
+    float d = 0.0f;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = beg + u;
+      x[u] = c[u] >= 0 ? Num<T>::to_f(alpha[e * ald + h]) : 0.0f;
+      y[u] = c[u] >= 0 ? Num<T>::to_f(dalpha[e * H + h]) : 0.0f;
+      sv[u] = c[u] >= 0 ? Num<T>::to_f(sr[(size_t)(unsigned)c[u] * H + h]) : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) d = fmaf(x[u], y[u], d);
+    float acc = 0.0f;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (c[u] >= 0) {
+        float g = x[u] * (y[u] - d);
+        g = a + sv[u] > 0.0f ? g : g * slope;
+        de[(beg + u) * ald + h] = Num<T>::from_f(g);
+        acc += g;
+      }
+    }
+    dsl[t] = Num<T>::from_f(acc);
+    return;
+  }
+  const float d = bwd_pass1<T, H>(alpha, dalpha, beg, end, 1, h, ald);
   dsl[t] = Num<T>::from_f(bwd_pass2<T, H>(cols, sr, alpha, dalpha, beg, end, 1, h, a, slope, d, de, ald));
 }
 
@@ -377,7 +434,7 @@ k_gat_fwd_all(const int64_t* __restrict__ offsets, const int32_t* __restrict__ c
 }
 
 template <typename T, int H>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 5)
 k_gat_bwd_all(const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
               int64_t n_rows, const int32_t* __restrict__ medium, int64_t n_medium,
               const int32_t* __restrict__ longr, int64_t n_long, int64_t b_med,
