@@ -232,9 +232,15 @@ int hg_softmax_xent(const void* logits, int logits_dtype, int64_t ld, const int6
 
 /* fp32-guarded SDDMM (numerics="fast"): out[e*heads+h] = rnd(sum over the head's
  * fh features of X[row(e)] * Y[cols[e]]), exact f16 products accumulated in
- * fp32, one rounding; same arguments as hg_sddmm. */
+ * fp32, one rounding; arguments as hg_sddmm plus optional packs (the
+ * hg_schedule_build packs of the same CSR, with pack_rowid = int32 row id per
+ * edge; NULL / 0 / NULL for none).  Packed rows give bitwise the unit result.
+ * Packs need a butterfly layout (F / V <= 32, power-of-two head widths in
+ * V-element vectors); other layouts fall back to the exact kernel and reject
+ * packs. */
 int hg_sddmm_fast(const int64_t* offsets, const int32_t* cols, int64_t n_rows, int64_t num_edges,
-                  const int32_t* units, int64_t num_units, const void* x, const void* y,
+                  const int32_t* units, int64_t num_units, const int32_t* packs,
+                  int64_t num_packs, const int32_t* pack_rowid, const void* x, const void* y,
                   void* out, int32_t F, int32_t heads, int dtype, void* stream);
 
 /* GAT attention projections (models.py:503-506, s_l = z a_l, s_r = z a_r) for all

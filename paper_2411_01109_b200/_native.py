@@ -50,7 +50,8 @@ SIGNATURES = {
                            _P, c_size_t, _P],
     "hg_gather_probe": [_P, _I64, _P, _I32, _I64, _P, _P],
     "hg_sddmm": [_P, _P, _I64, _I64, _P, _I64, _P, _P, _P, _I32, _I32, c_int, _P],
-    "hg_sddmm_fast": [_P, _P, _I64, _I64, _P, _I64, _P, _P, _P, _I32, _I32, c_int, _P],
+    "hg_sddmm_fast": [_P, _P, _I64, _I64, _P, _I64, _P, _I64, _P, _P, _P, _P, _I32, _I32, c_int,
+                      _P],
     "hg_attn_scores": [_P, _P, _I64, _I64, _P, _P, _I32, c_double, _P, c_int, _P],
     "hg_edge_softmax_fwd": [_P, _I64, _I64, _P, _P, _I32, _P, _I64, _I64, c_int, _P],
     "hg_edge_softmax_bwd": [_P, _I64, _I64, _P, _P, _P, _I32, _P, _I64, _I64, c_int, _P],

@@ -244,14 +244,114 @@ k_sddmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* _
   }
 }
 
+// Packs (hg_schedule_build): an aligned block of short rows walked as one edge
+// stream in 4-edge batches, each edge's X row picked by its row id (reused
+// from the previous edge of the batch when the row repeats).  Per-edge
+// arithmetic and the butterfly grouping are k_sddmm_fast's: bitwise equal.
+template <typename T, int V, int TEAM, int G>
+__global__ void __launch_bounds__(256, 4)
+k_sddmm_packed(const int4* __restrict__ packs, int64_t num_packs, const int32_t* __restrict__ rowid,
+               const int32_t* __restrict__ cols, const T* __restrict__ x,
+               const T* __restrict__ y, T* __restrict__ out, int F, int heads) {
+  using Raw = typename RawV<V * sizeof(T)>::type;
+  constexpr int EB = 4;
+  constexpr int LV = (G < EB ? G : EB);
+  constexpr int IDS = (EB + TEAM - 1) / TEAM;
+  const int lane = threadIdx.x & 31;
+  const int tl = lane & (TEAM - 1);
+  const int tb = lane & ~(TEAM - 1);
+  const unsigned tmask = TEAM == 32 ? 0xffffffffu : (((1u << TEAM) - 1u) << tb);
+  const int nvec = F / V;
+  const bool cval = tl < nvec;
+  const int hd = tl / G, gp = tl & (G - 1);
+  const int64_t team = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TEAM;
+  if (team >= num_packs) return;
+  const int4 pk = packs[team];
+  const int beg = pk.y, end = pk.z;
+  int cq[IDS], rq[IDS];
+#pragma unroll
+  for (int q = 0; q < IDS; ++q) {
+    const int j = tl + q * TEAM;
+    const bool in = j < EB && beg + j < end;
+    cq[q] = in ? __ldcs(cols + beg + j) : 0;
+    rq[q] = in ? __ldcs(rowid + beg + j) : -1;
+  }
+  for (int base = beg; base < end; base += EB) {
+    int nc[IDS], nr[IDS];
+#pragma unroll
+    for (int q = 0; q < IDS; ++q) {
+      const int j = tl + q * TEAM;
+      const bool in = j < EB && base + EB + j < end;
+      nc[q] = in ? __ldcs(cols + base + EB + j) : 0;
+      nr[q] = in ? __ldcs(rowid + base + EB + j) : -1;
+    }
+    Raw xr[EB], yr[EB];
+    int rj[EB];
+#pragma unroll
+    for (int j = 0; j < EB; ++j) {
+      const int c = __shfl_sync(tmask, cq[j / TEAM], tb + j % TEAM);
+      rj[j] = __shfl_sync(tmask, rq[j / TEAM], tb + j % TEAM);
+      if (rj[j] >= 0 && cval) {
+        yr[j] = __ldg(reinterpret_cast<const Raw*>(y + (int64_t)c * F + tl * V));
+        if (j == 0 || rj[j] != rj[j - 1])
+          xr[j] = __ldg(reinterpret_cast<const Raw*>(x + (int64_t)rj[j] * F + tl * V));
+      }
+    }
+#pragma unroll
+    for (int j = 1; j < EB; ++j)
+      if (rj[j] == rj[j - 1]) xr[j] = xr[j - 1];
+    float v[EB];
+#pragma unroll
+    for (int j = 0; j < EB; ++j) v[j] = (rj[j] >= 0 && cval) ? chunk_dot_f32<T, V>(xr[j], yr[j]) : 0.0f;
+    int eoff = 0;
+#pragma unroll
+    for (int s = G / 2, cnt = EB; s >= 1 && cnt > 1; s >>= 1, cnt >>= 1) {
+      const bool up = (gp & s) != 0;
+#pragma unroll
+      for (int i = 0; i < cnt / 2; ++i) {
+        const float send = up ? v[i] : v[i + cnt / 2];
+        const float keep = up ? v[i + cnt / 2] : v[i];
+        v[i] = keep + __shfl_xor_sync(tmask, send, s);
+      }
+      if (up) eoff += cnt / 2;
+    }
+#pragma unroll
+    for (int s = G / (2 * LV) > 0 ? (G / LV) / 2 : 0; s >= 1; s >>= 1)
+      v[0] += __shfl_xor_sync(tmask, v[0], s);
+    constexpr int KEEP = EB / LV;
+    const bool writer = G <= EB || (gp & (G / LV - 1)) == 0;
+    if (cval && writer) {
+#pragma unroll
+      for (int i = 0; i < KEEP; ++i) {
+        const int e = base + eoff + i;
+        if (e < end) out[(int64_t)e * heads + hd] = Num<T>::from_f(v[i]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < IDS; ++q) { cq[q] = nc[q]; rq[q] = nr[q]; }
+  }
+}
+
 }  // namespace hg
 
 using namespace hg;
 
+struct SdPacks {
+  const int4* packs;
+  int64_t np;
+  const int32_t* rowid;
+};
+
 template <typename T, int V, int TEAM, int G>
-static int launch_sddmm_fast(const int4* units, int64_t nu, const int32_t* cols, const void* x,
-                             const void* y, void* out, int F, int heads, cudaStream_t st) {
+static int launch_sddmm_fast(const int4* units, int64_t nu, const SdPacks& pk, const int32_t* cols,
+                             const void* x, const void* y, void* out, int F, int heads,
+                             cudaStream_t st) {
   constexpr int tpb = 256 / TEAM;
+  if (pk.np > 0) {
+    k_sddmm_packed<T, V, TEAM, G><<<(unsigned)((pk.np + tpb - 1) / tpb), 256, 0, st>>>(
+        pk.packs, pk.np, pk.rowid, cols, (const T*)x, (const T*)y, (T*)out, F, heads);
+    HG_LAUNCHED();
+  }
   if (nu == 0) return HG_OK;
   int sms = 148, dev = 0, occ = 0;
   if (cudaGetDevice(&dev) == cudaSuccess)
@@ -266,16 +366,16 @@ static int launch_sddmm_fast(const int4* units, int64_t nu, const int32_t* cols,
 }
 
 template <typename T, int V, int TEAM>
-static int dispatch_sddmm_fast_g(const int4* units, int64_t nu, const int32_t* cols,
-                                 const void* x, const void* y, void* out, int F, int heads,
-                                 int g, cudaStream_t st) {
+static int dispatch_sddmm_fast_g(const int4* units, int64_t nu, const SdPacks& pk,
+                                 const int32_t* cols, const void* x, const void* y, void* out,
+                                 int F, int heads, int g, cudaStream_t st) {
   switch (g) {
-    case 1: return launch_sddmm_fast<T, V, TEAM, 1>(units, nu, cols, x, y, out, F, heads, st);
-    case 2: if constexpr (TEAM >= 2) return launch_sddmm_fast<T, V, TEAM, 2>(units, nu, cols, x, y, out, F, heads, st); break;
-    case 4: if constexpr (TEAM >= 4) return launch_sddmm_fast<T, V, TEAM, 4>(units, nu, cols, x, y, out, F, heads, st); break;
-    case 8: if constexpr (TEAM >= 8) return launch_sddmm_fast<T, V, TEAM, 8>(units, nu, cols, x, y, out, F, heads, st); break;
-    case 16: if constexpr (TEAM >= 16) return launch_sddmm_fast<T, V, TEAM, 16>(units, nu, cols, x, y, out, F, heads, st); break;
-    case 32: if constexpr (TEAM >= 32) return launch_sddmm_fast<T, V, TEAM, 32>(units, nu, cols, x, y, out, F, heads, st); break;
+    case 1: return launch_sddmm_fast<T, V, TEAM, 1>(units, nu, pk, cols, x, y, out, F, heads, st);
+    case 2: if constexpr (TEAM >= 2) return launch_sddmm_fast<T, V, TEAM, 2>(units, nu, pk, cols, x, y, out, F, heads, st); break;
+    case 4: if constexpr (TEAM >= 4) return launch_sddmm_fast<T, V, TEAM, 4>(units, nu, pk, cols, x, y, out, F, heads, st); break;
+    case 8: if constexpr (TEAM >= 8) return launch_sddmm_fast<T, V, TEAM, 8>(units, nu, pk, cols, x, y, out, F, heads, st); break;
+    case 16: if constexpr (TEAM >= 16) return launch_sddmm_fast<T, V, TEAM, 16>(units, nu, pk, cols, x, y, out, F, heads, st); break;
+    case 32: if constexpr (TEAM >= 32) return launch_sddmm_fast<T, V, TEAM, 32>(units, nu, pk, cols, x, y, out, F, heads, st); break;
     default: break;
   }
   HG_REQUIRE(false, "hg_sddmm_fast: head group %d unsupported", g);
@@ -283,18 +383,19 @@ static int dispatch_sddmm_fast_g(const int4* units, int64_t nu, const int32_t* c
 
 // Returns -1 when the layout is not covered (caller falls back to the exact kernel).
 template <typename T, int V>
-static int dispatch_sddmm_fast(const int4* units, int64_t nu, const int32_t* cols, const void* x,
-                               const void* y, void* out, int F, int heads, cudaStream_t st) {
+static int dispatch_sddmm_fast(const int4* units, int64_t nu, const SdPacks& pk,
+                               const int32_t* cols, const void* x, const void* y, void* out,
+                               int F, int heads, cudaStream_t st) {
   const int nvec = F / V, g = F / heads / V;
   if (nvec > 32 || g < 1 || (g & (g - 1)) != 0 || nvec % g != 0) return -1;
   const int team = nvec <= 1 ? 1 : nvec <= 2 ? 2 : nvec <= 4 ? 4 : nvec <= 8 ? 8 : nvec <= 16 ? 16 : 32;
   switch (team) {
-    case 1: return dispatch_sddmm_fast_g<T, V, 1>(units, nu, cols, x, y, out, F, heads, g, st);
-    case 2: return dispatch_sddmm_fast_g<T, V, 2>(units, nu, cols, x, y, out, F, heads, g, st);
-    case 4: return dispatch_sddmm_fast_g<T, V, 4>(units, nu, cols, x, y, out, F, heads, g, st);
-    case 8: return dispatch_sddmm_fast_g<T, V, 8>(units, nu, cols, x, y, out, F, heads, g, st);
-    case 16: return dispatch_sddmm_fast_g<T, V, 16>(units, nu, cols, x, y, out, F, heads, g, st);
-    default: return dispatch_sddmm_fast_g<T, V, 32>(units, nu, cols, x, y, out, F, heads, g, st);
+    case 1: return dispatch_sddmm_fast_g<T, V, 1>(units, nu, pk, cols, x, y, out, F, heads, g, st);
+    case 2: return dispatch_sddmm_fast_g<T, V, 2>(units, nu, pk, cols, x, y, out, F, heads, g, st);
+    case 4: return dispatch_sddmm_fast_g<T, V, 4>(units, nu, pk, cols, x, y, out, F, heads, g, st);
+    case 8: return dispatch_sddmm_fast_g<T, V, 8>(units, nu, pk, cols, x, y, out, F, heads, g, st);
+    case 16: return dispatch_sddmm_fast_g<T, V, 16>(units, nu, pk, cols, x, y, out, F, heads, g, st);
+    default: return dispatch_sddmm_fast_g<T, V, 32>(units, nu, pk, cols, x, y, out, F, heads, g, st);
   }
 }
 
@@ -332,6 +433,7 @@ static int dispatch_sddmm(const int4* units, int64_t nu, const int32_t* cols, co
 
 extern "C" int hg_sddmm_fast(const int64_t* offsets, const int32_t* cols, int64_t n_rows,
                              int64_t num_edges, const int32_t* units, int64_t num_units,
+                             const int32_t* packs, int64_t num_packs, const int32_t* pack_rowid,
                              const void* x, const void* y, void* out, int32_t F, int32_t heads,
                              int dtype, void* stream) {
   HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
@@ -342,16 +444,21 @@ extern "C" int hg_sddmm_fast(const int64_t* offsets, const int32_t* cols, int64_
   const int fh = F / heads;
   const int4* u = reinterpret_cast<const int4*>(units);
   const bool aligned = reinterpret_cast<uintptr_t>(x) % 16 == 0 && reinterpret_cast<uintptr_t>(y) % 16 == 0;
+  SdPacks pk{reinterpret_cast<const int4*>(packs), packs && num_edges > 0 ? num_packs : 0,
+             pack_rowid};
+  HG_REQUIRE(pk.np == 0 || pack_rowid, "hg_sddmm_fast: packs need pack_rowid");
   int rc = -1;
   if (dtype == HG_F16 && aligned && fh % 8 == 0)
-    rc = dispatch_sddmm_fast<__half, 8>(u, num_units, cols, x, y, out, F, heads, st);
+    rc = dispatch_sddmm_fast<__half, 8>(u, num_units, pk, cols, x, y, out, F, heads, st);
   else if (dtype == HG_F16)
-    rc = dispatch_sddmm_fast<__half, 2>(u, num_units, cols, x, y, out, F, heads, st);
+    rc = dispatch_sddmm_fast<__half, 2>(u, num_units, pk, cols, x, y, out, F, heads, st);
   else if (aligned && fh % 4 == 0)
-    rc = dispatch_sddmm_fast<float, 4>(u, num_units, cols, x, y, out, F, heads, st);
+    rc = dispatch_sddmm_fast<float, 4>(u, num_units, pk, cols, x, y, out, F, heads, st);
   else
-    rc = dispatch_sddmm_fast<float, 2>(u, num_units, cols, x, y, out, F, heads, st);
+    rc = dispatch_sddmm_fast<float, 2>(u, num_units, pk, cols, x, y, out, F, heads, st);
   if (rc >= 0) return rc;
+  HG_REQUIRE(pk.np == 0, "hg_sddmm_fast: layout F=%d heads=%d is outside the butterfly kernel; "
+             "build the schedule without packs", F, heads);
   // layouts outside the butterfly kernel (F/V > 32, non-power-of-two heads):
   // the exact kernel (its result is within the fast tolerance by definition)
   return hg_sddmm(offsets, cols, n_rows, num_edges, units, num_units, x, y, out, F, heads,

@@ -606,6 +606,19 @@ def spmm_vertex_ref(dg: DeviceGraph, x, scaling="post", norm="none", staging=Fal
 # ── SDDMM, attention, softmax ────────────────────────────────────────────
 
 
+def _butterfly_layout(x, y, f, heads):
+    """Layouts hg_sddmm_fast runs on its butterfly kernels (and accepts packs
+    for): F / V <= 32 with power-of-two head widths in V-element vectors."""
+    fh = f // heads
+    aligned = x.data_ptr() % 16 == 0 and y.data_ptr() % 16 == 0
+    if x.dtype == torch.float16:
+        v = 8 if aligned and fh % 8 == 0 else 2
+    else:
+        v = 4 if aligned and fh % 4 == 0 else 2
+    g = fh // v
+    return f // v <= 32 and g >= 1 and g & (g - 1) == 0 and (f // v) % g == 0
+
+
 def sddmm(dg: DeviceGraph, x, y, heads=1, transpose=False, fast=False):
     """Per-edge (per-head) tree dot products, bit-exact with kernels.sddmm
     (fast=True: fp32 accumulation, one rounding -- hg_sddmm_fast).
@@ -619,11 +632,20 @@ def sddmm(dg: DeviceGraph, x, y, heads=1, transpose=False, fast=False):
         raise ValueError("operand feature lengths differ")
     f = x.shape[1]
     out = torch.empty((view.num_edges, heads), dtype=x.dtype, device=x.device)
-    sched = view.schedule()
-    nat.call("hg_sddmm_fast" if fast else "hg_sddmm", _p(view.offsets), _p(view.cols),
-             view.n_rows, view.num_edges, _p(sched.units), sched.num_units, _p(x), _p(y),
-             _p(out), f, heads, _dtype_code(x), _stream())
-    Probe.launches += 1
+    if fast:
+        packed = PACKING and view.n_rows >= PACK_MIN_ROWS and _butterfly_layout(x, y, f, heads)
+        sched = view.schedule(DEFAULT_SPLIT_CAP, PACK_EDGES_WIDE if packed else -1)
+        nat.call("hg_sddmm_fast", _p(view.offsets), _p(view.cols), view.n_rows, view.num_edges,
+                 _p(sched.units), sched.num_units, _p(sched.packs), sched.num_packs,
+                 _p(view.row_ids() if sched.num_packs else None), _p(x), _p(y), _p(out), f,
+                 heads, _dtype_code(x), _stream())
+        Probe.launches += 1 + int(sched.num_packs > 0)
+    else:
+        sched = view.schedule()
+        nat.call("hg_sddmm", _p(view.offsets), _p(view.cols), view.n_rows, view.num_edges,
+                 _p(sched.units), sched.num_units, _p(x), _p(y), _p(out), f, heads,
+                 _dtype_code(x), _stream())
+        Probe.launches += 1
     return out[:, 0] if heads == 1 else out
 
 

@@ -785,6 +785,35 @@ def test_sddmm_fast_vs_f64(cuda, heads, fh):
     assert np.all(np.abs(got - want) <= bound)
 
 
+@pytest.mark.parametrize("heads,fh", [(1, 8), (4, 32), (4, 16), (2, 64), (8, 8), (1, 2), (4, 6),
+                                     (1, 256), (3, 4)])
+@pytest.mark.parametrize("dtype", [torch.float16, torch.float32])
+def test_sddmm_packed_bitwise_equal_units(cuda, heads, fh, dtype):
+    """hg_sddmm_fast with short-row packs (one team per 16-row block, X row per
+    edge) is bitwise the per-row unit kernel, on empty / short / long / split
+    rows; layouts outside the butterfly kernel run unpacked."""
+    from paper_2411_01109_b200 import device as D
+
+    n = 20000
+    r, c = _short_row_graph(fh * heads + 1, n)
+    dg = _dg(n, r, c, cuda)
+    f = heads * fh
+    x = torch.randn(n, f, device=cuda).to(dtype)
+    y = torch.randn(n, f, device=cuda).to(dtype)
+    saved = D.PACK_MIN_ROWS
+    try:
+        D.PACK_MIN_ROWS = 1 << 40
+        want = D.sddmm(dg, x, y, heads=heads, fast=True)
+        D.PACK_MIN_ROWS = 0
+        got = D.sddmm(dg, x, y, heads=heads, fast=True)
+    finally:
+        D.PACK_MIN_ROWS = saved
+    it = torch.int16 if dtype == torch.float16 else torch.int32
+    assert torch.equal(got.contiguous().view(it), want.contiguous().view(it))
+    if D._butterfly_layout(x, y, f, heads):
+        assert dg.view(False).schedule(D.DEFAULT_SPLIT_CAP, D.PACK_EDGES_WIDE).num_packs > 0
+
+
 # ── tcgen05 GEMM with the GCN epilogue (hg_gemm_tc) ──────────────────────
 
 

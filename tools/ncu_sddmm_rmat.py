@@ -17,6 +17,6 @@ x = torch.randn(dg.n, f, device="cuda", dtype=torch.float16)
 y = torch.randn(dg.n, f, device="cuda", dtype=torch.float16)
 out = torch.empty((view.num_edges, 4), dtype=torch.float16, device="cuda")
 D.nat.call("hg_sddmm_fast", D._p(view.offsets), D._p(view.cols), view.n_rows, view.num_edges,
-           D._p(sched.units), sched.num_units, D._p(x), D._p(y), D._p(out), f, 4,
+           D._p(sched.units), sched.num_units, None, 0, None, D._p(x), D._p(y), D._p(out), f, 4,
            D._dtype_code(x), D._stream())
 torch.cuda.synchronize()

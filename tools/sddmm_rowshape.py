@@ -1,5 +1,6 @@
-"""hg_sddmm_fast on the C5 RMAT graph, F = 128 / 64 over 4 heads, against the
-gather probe of the same column stream.  Timing only."""
+"""hg_sddmm_fast on the C5 RMAT graph, F = 128 / 64 over 4 heads: per-row
+units only vs with short-row packs (device.sddmm), against the gather probe of
+the same column stream.  Timing only."""
 import json
 import sys
 from pathlib import Path
@@ -22,10 +23,11 @@ for f in (128, 64):
 
     def units():
         D.nat.call("hg_sddmm_fast", D._p(view.offsets), D._p(view.cols), view.n_rows,
-                   view.num_edges, D._p(sched.units), sched.num_units, D._p(x), D._p(y),
+                   view.num_edges, D._p(sched.units), sched.num_units, None, 0, None, D._p(x), D._p(y),
                    D._p(out), f, 4, D._dtype_code(x), D._stream())
 
     res[f] = {"units": round(t_ms(units), 3),
+              "packed": round(t_ms(lambda: D.sddmm(dg, x, y, heads=4, fast=True)), 3),
               "probe": round(t_ms(lambda: D.gather_probe(view.cols, view.num_edges, y, f * 2)), 3)}
     print(json.dumps({f: res[f]}), flush=True)
 print(json.dumps(res))
