@@ -1,3 +1,3 @@
-python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; tail -1 gpurun_out/pytest_gpu.log
-python bench.py --workload gat-rmat --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_gat.json 2>gpurun_out/bench_gat.err
-python bench.py --workload gat-pubmed --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/bench_gatp.json 2>gpurun_out/bench_gatp.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 2 --warmup 3 --no-sweep --no-small --no-cpu-baseline > /dev/null 2>&1
+python tools/launch_summary.py gpurun_out/launches_bench.csv > gpurun_out/launches_bench_gcn_v5.txt
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/gcn_epoch.csv python tools/ncu_target.py --epochs 2 > /dev/null 2>&1
