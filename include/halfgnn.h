@@ -168,8 +168,9 @@ int hg_spmm_vertex_ref(const int64_t* offsets, const int32_t* cols, int64_t n_ro
 
 /* Measurement only (no reference counterpart): the gather pattern of one SpMM
  * with the arithmetic removed -- cols[0..num_edges) streamed once and, per
- * edge, row_bytes (multiple of 16, <= 512) of x at cols[e] * ld_bytes fetched
- * with the k_spmm_fast team shape.  Its time is the floor of any gather SpMM of
+ * edge, row_bytes (multiple of 16, <= 512; <= 1024 for whole 32-byte chunks)
+ * of x at cols[e] * ld_bytes fetched with the k_spmm_fast team shape and lane
+ * width (32-byte lanes for rows of >= 96 bytes in whole 32-byte chunks).  Its time is the floor of any gather SpMM of
  * that graph and width; bench.py reports hg_spmm against it.  *out is written
  * only on a hash collision (keeps the loads live). */
 int hg_gather_probe(const int32_t* cols, int64_t num_edges, const void* x, int32_t row_bytes,

@@ -8,14 +8,35 @@
 //  * k_spmm_edge_ref   bit-exact replica of halfsparse's edge-parallel order
 //                      (kernels.py:328-391 / _ref_spmm_edge 603-688).
 //  * k_spmm_vertex_ref bit-exact replica of spmm_vertex_grouped (463-559).
+#include <cstdlib>
+
 #include "hg_common.cuh"
 
 namespace hg {
 
 template <int BYTES> struct RawVec;
+// 32 bytes per lane: one LDG.256 (ld.global.nc.v8.b32, sm_100) per neighbour
+// chunk -- half the load instructions of 16-byte lanes for the same bytes
+struct alignas(32) U32x8 { uint32_t a[8]; };
+template <> struct RawVec<32> { using type = U32x8; };
 template <> struct RawVec<16> { using type = uint4; };
 template <> struct RawVec<8> { using type = uint2; };
 template <> struct RawVec<4> { using type = uint32_t; };
+
+// Read-only gather of one lane chunk.
+template <typename R>
+__device__ __forceinline__ R ldg_raw(const R* p) {
+  if constexpr (sizeof(R) == 32) {
+    R v;
+    asm("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v.a[0]), "=r"(v.a[1]), "=r"(v.a[2]), "=r"(v.a[3]), "=r"(v.a[4]),
+                   "=r"(v.a[5]), "=r"(v.a[6]), "=r"(v.a[7])
+                 : "l"(p));
+    return v;
+  } else {
+    return __ldg(p);
+  }
+}
 
 // Convert a raw 16/8/4-byte vector of V elements of T to floats.
 template <typename T, int V>
@@ -146,9 +167,10 @@ __device__ __forceinline__ void acc_fma(float (&acc)[V], T w,
 // Minimum resident blocks per SM: caps registers so that 256-thread blocks of
 // single-chunk teams run 3-4 deep (24-32 warps/SM) for memory-level
 // parallelism, without spilling (ptxas -v: 64 regs unweighted TEAM >= 8).
-template <int TEAM, int NCH, bool WT>
+template <int TEAM, int NCH, bool WT, int VB = 16>
 struct FastOcc {
-  static constexpr int value = NCH == 1 ? ((!WT && TEAM >= 8 && TEAM <= 16) ? 4 : 3) : (NCH == 2 ? 2 : 1);
+  static constexpr int value =
+      NCH == 1 ? ((!WT && VB == 16 && TEAM >= 8 && TEAM <= 16) ? 4 : 3) : (NCH == 2 ? 2 : 1);
 };
 
 // Column ids of one batch for a non-power-of-two team: lane tl holds the ids
@@ -206,7 +228,7 @@ struct FastTeam {
   static constexpr bool P2 = TeamShape<TEAM>::P2;
   // edges gathered per batch (packed teams: 4, the rolled accumulate shifts
   // the batch registers once per edge)
-  static constexpr int EB = (NCH >= 4 || PK) ? 4 : 8;
+  static constexpr int EB = (NCH >= 4 || PK || V * sizeof(T) == 32) ? 4 : 8;
   static constexpr int CPL = P2 ? (TEAM >= EB ? 1 : EB / TEAM) : (EB + TEAM - 1) / TEAM;
   using Raw = typename RawVec<V * sizeof(T)>::type;
 
@@ -292,7 +314,7 @@ struct FastTeam {
 #pragma unroll
       for (int k = 0; k < NCH; ++k) {
         if (ok && cval[k]) {
-          raw[j][k] = __ldg(reinterpret_cast<const Raw*>(xl[k] + roff));
+          raw[j][k] = ldg_raw(reinterpret_cast<const Raw*>(xl[k] + roff));
           if (WEIGHTED) wv[j][k] = w[(size_t)(unsigned)wi * wld + chead[k]];
         }
       }
@@ -355,7 +377,9 @@ struct FastTeam {
 // stream crosses its end.
 template <typename T, int V, int TEAM, int NCH, bool WEIGHTED, bool SUMW = false,
           bool PACKED = false>
-__global__ void __launch_bounds__(256, (PACKED && NCH == 1) ? 4 : FastOcc<TEAM, NCH, WEIGHTED>::value)
+__global__ void __launch_bounds__(256, (PACKED && NCH == 1 && V * sizeof(T) <= 16)
+                                           ? 4
+                                           : FastOcc<TEAM, NCH, WEIGHTED, V * sizeof(T)>::value)
 k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __restrict__ cols,
             int64_t num_edges, const T* __restrict__ w, const int32_t* __restrict__ widx,
             int heads, int fh, const T* __restrict__ x, T* __restrict__ y,
@@ -618,6 +642,15 @@ static int launch_fast(const FastArgs& a) {
 
 // Weighted aggregation that also sums a second per-edge value block (w2off)
 // per head: one team size per power-of-two chunk count, single chunk per lane.
+// 32-byte lanes for binary16 rows of 48..512 elements, multiples of 16 (C3
+// sweep: F=64 1.11 -> 1.07 ms, 128: 2.12 -> 2.03, 256: 4.57 -> 4.27, 512: 9.18 ->
+// 8.60; F=16/32 got slower with 1-2 lane teams).  A/B switch for measurement:
+// HG_SPMM_LANE32=0 in the environment of the first call.
+static const bool kLane32 = [] {
+  const char* e = getenv("HG_SPMM_LANE32");
+  return !(e && e[0] == '0');
+}();
+
 template <typename T, int V>
 static int dispatch_sumw(const FastArgs& a) {
   const int nvec = a.F / V;
@@ -650,12 +683,33 @@ static int dispatch_layout(const FastArgs& a) {
   HG_REQUIRE(false, "hg_spmm: feature length %d too large", a.F);
 }
 
+// 32-byte lanes (binary16 x 16), single chunk per lane: F <= 512.
+template <typename T, bool WT>
+static int dispatch_layout32(const FastArgs& a) {
+  const int nvec = a.F / 16;
+  if (nvec <= 1) return launch_fast<T, 16, 1, 1, WT>(a);
+  if (nvec <= 2) return launch_fast<T, 16, 2, 1, WT>(a);
+  if (nvec <= 4) return launch_fast<T, 16, 4, 1, WT>(a);
+  if (nvec <= 8) return launch_fast<T, 16, 8, 1, WT>(a);
+  if (nvec <= 16) return launch_fast<T, 16, 16, 1, WT>(a);
+  return launch_fast<T, 16, 32, 1, WT>(a);
+}
+
 template <typename T>
 static int dispatch_fast(const FastArgs& a) {
   constexpr int VB = 16 / sizeof(T);
   const bool aligned = (reinterpret_cast<uintptr_t>(a.x) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(a.y) % 16 == 0);
   const bool big = aligned && (a.fh % VB == 0) && a.ldx % VB == 0 && a.ldy % VB == 0;
+  if constexpr (sizeof(T) == 2) {
+    const bool a32 = (reinterpret_cast<uintptr_t>(a.x) % 32 == 0) &&
+                     (reinterpret_cast<uintptr_t>(a.y) % 32 == 0) && a.fh % 16 == 0 &&
+                     a.ldx % 16 == 0 && a.ldy % 16 == 0 && a.F >= 48 && a.F <= 512;
+    if (a32 && kLane32) {
+      if (a.out2) return dispatch_sumw<T, 16>(a);
+      return a.w ? dispatch_layout32<T, true>(a) : dispatch_layout32<T, false>(a);
+    }
+  }
   if (a.out2) return big ? dispatch_sumw<T, VB>(a) : dispatch_sumw<T, 2>(a);
   if (a.w) return big ? dispatch_layout<T, VB, true>(a) : dispatch_layout<T, 2, true>(a);
   return big ? dispatch_layout<T, VB, false>(a) : dispatch_layout<T, 2, false>(a);
@@ -1108,9 +1162,9 @@ extern "C" int hg_spmm_vertex_ref(const int64_t* offsets, const int32_t* cols, i
 // team (the k_spmm_fast team shape).  Its time is the floor any gather SpMM on
 // that graph and width can reach; bench.py reports hg_spmm's time against it.
 namespace hg {
-template <int TEAM>
+template <int TEAM, typename R = uint4>
 __global__ void __launch_bounds__(256) k_gather_probe(const int* __restrict__ cols, int64_t E,
-                                                      const int4* __restrict__ x, int64_t ldv,
+                                                      const R* __restrict__ x, int64_t ldv,
                                                       int lanes, unsigned* __restrict__ out) {
   constexpr int RPL = 32 / TEAM;  // rows fetched per warp load
   const int lane = threadIdx.x & 31;
@@ -1120,14 +1174,19 @@ __global__ void __launch_bounds__(256) k_gather_probe(const int* __restrict__ co
   unsigned acc = 0;
   for (int64_t base = warp * 32; base < E; base += nwarps * 32) {
     const int c = base + lane < E ? __ldg(cols + base + lane) : -1;
-    int4 v[TEAM];
+    R v[TEAM];
 #pragma unroll
     for (int k = 0; k < TEAM; ++k) {
       const int r = __shfl_sync(0xffffffffu, c, k * RPL + slot);
-      v[k] = (r >= 0 && sub < lanes) ? __ldg(x + (int64_t)r * ldv + sub) : make_int4(0, 0, 0, 0);
+      if (r >= 0 && sub < lanes) v[k] = ldg_raw(x + (int64_t)r * ldv + sub);
+      else memset(&v[k], 0, sizeof(R));
     }
 #pragma unroll
-    for (int k = 0; k < TEAM; ++k) acc ^= (unsigned)(v[k].x ^ v[k].y ^ v[k].z ^ v[k].w);
+    for (int k = 0; k < TEAM; ++k) {
+      const unsigned* w = reinterpret_cast<const unsigned*>(&v[k]);
+#pragma unroll
+      for (int i = 0; i < (int)(sizeof(R) / 4); ++i) acc ^= w[i];
+    }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) acc ^= __shfl_xor_sync(0xffffffffu, acc, o);
@@ -1137,13 +1196,33 @@ __global__ void __launch_bounds__(256) k_gather_probe(const int* __restrict__ co
 
 extern "C" int hg_gather_probe(const int32_t* cols, int64_t num_edges, const void* x,
                                int32_t row_bytes, int64_t ld_bytes, uint32_t* out, void* stream) {
-  HG_REQUIRE(row_bytes > 0 && row_bytes % 16 == 0 && row_bytes <= 512,
-             "hg_gather_probe: row_bytes %d must be a multiple of 16 in [16, 512]", row_bytes);
+  HG_REQUIRE(row_bytes > 0 && row_bytes % 16 == 0 && row_bytes <= 1024,
+             "hg_gather_probe: row_bytes %d must be a multiple of 16 in [16, 1024]", row_bytes);
+  HG_REQUIRE(row_bytes <= 512 || (row_bytes % 32 == 0 && ld_bytes % 32 == 0 && kLane32),
+             "hg_gather_probe: rows over 512 bytes need 32-byte lanes");
   HG_REQUIRE(ld_bytes % 16 == 0 && ld_bytes >= row_bytes && num_edges >= 0,
              "hg_gather_probe: bad row stride");
   HG_REQUIRE(reinterpret_cast<uintptr_t>(x) % 16 == 0, "hg_gather_probe: x must be 16-byte aligned");
   if (num_edges == 0) return HG_OK;
   cudaStream_t st = as_stream(stream);
+  // the SpMM's lane width: 32 bytes for rows of 96..1024 bytes that are whole
+  // 32-byte chunks (k_spmm_fast's binary16 rule), else 16
+  if (kLane32 && row_bytes % 32 == 0 && ld_bytes % 32 == 0 && row_bytes >= 96 &&
+      reinterpret_cast<uintptr_t>(x) % 32 == 0) {
+    const int lanes = row_bytes / 32;
+    const int64_t ldv = ld_bytes / 32;
+    int sms = 148, dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned g = (unsigned)sms * 8;
+    const U32x8* xv = (const U32x8*)x;
+    unsigned* o = (unsigned*)out;
+    if (lanes <= 4) k_gather_probe<4, U32x8><<<g, 256, 0, st>>>(cols, num_edges, xv, ldv, lanes, o);
+    else if (lanes <= 8) k_gather_probe<8, U32x8><<<g, 256, 0, st>>>(cols, num_edges, xv, ldv, lanes, o);
+    else k_gather_probe<16, U32x8><<<g, 256, 0, st>>>(cols, num_edges, xv, ldv, lanes, o);
+    HG_LAUNCHED();
+    return HG_OK;
+  }
   const int lanes = row_bytes / 16;
   const int64_t ldv = ld_bytes / 16;
   int sms = 148;

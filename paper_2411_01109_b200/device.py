@@ -98,13 +98,13 @@ class Probe:
         """Seconds the timed spmm calls' gathers alone take (hg_gather_probe on
         the same column ids, feature buffer and width, X warm in L2 as after
         the producing kernel): the floor those calls could reach.  None when a
-        call's row exceeds the probe's 512 bytes."""
+        call's row exceeds the probe's 1024 bytes."""
         total = 0.0
         for r in cls.records:
             cols, ne, x, f = r[4]
             row_bytes = -(-f * x.element_size() // 16) * 16
             ld = x.stride(0) * x.element_size()
-            if row_bytes > 512 or ld < row_bytes or ld % 16 or x.data_ptr() % 16:
+            if row_bytes > 1024 or ld < row_bytes or ld % 16 or x.data_ptr() % 16:
                 return None
             gather_probe(cols, ne, x, row_bytes)
             ev0 = torch.cuda.Event(enable_timing=True)
