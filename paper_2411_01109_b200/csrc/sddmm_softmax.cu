@@ -7,12 +7,31 @@
 // implicit binary tree over power-of-two aligned index ranges; warps evaluate it
 // with predicated shuffle-down levels and combine 32-element block roots with a
 // binary-counter stack, so any row length reproduces the same tree.
+#include <cstdlib>
+
 #include "hg_common.cuh"
 
 namespace hg {
 
 template <int BYTES> struct RawV;
+struct alignas(32) SdU32x8 { uint32_t a[8]; };
+template <> struct RawV<32> { using type = SdU32x8; };
 template <> struct RawV<16> { using type = uint4; };
+
+// Read-only gather of one lane chunk (32 bytes: one LDG.256).
+template <typename R>
+__device__ __forceinline__ R ldg_chunk(const R* p) {
+  if constexpr (sizeof(R) == 32) {
+    R v;
+    asm("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(v.a[0]), "=r"(v.a[1]), "=r"(v.a[2]), "=r"(v.a[3]), "=r"(v.a[4]), "=r"(v.a[5]),
+          "=r"(v.a[6]), "=r"(v.a[7])
+        : "l"(p));
+    return v;
+  } else {
+    return __ldg(p);
+  }
+}
 template <> struct RawV<4> { using type = uint32_t; };
 template <> struct RawV<8> { using type = uint2; };
 
@@ -163,7 +182,7 @@ k_sddmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* _
              const T* __restrict__ x, const T* __restrict__ y, T* __restrict__ out, int F,
              int heads) {
   using Raw = typename RawV<V * sizeof(T)>::type;
-  constexpr int EB = 8;
+  constexpr int EB = V * sizeof(T) == 32 ? 4 : 8;
   constexpr int LV = (G < EB ? G : EB);  // butterfly levels that halve the batch: log2(LV)
   const int lane = threadIdx.x & 31;
   const int tl = lane & (TEAM - 1);
@@ -204,7 +223,7 @@ k_sddmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* _
 #pragma unroll
     for (int j = 0; j < EB; ++j) {
       const int c = __shfl_sync(tmask, cq[j / TEAM], tb + j % TEAM);
-      if (base + j < end && cval) yr[j] = __ldg(reinterpret_cast<const Raw*>(y + (int64_t)c * F + tl * V));
+      if (base + j < end && cval) yr[j] = ldg_chunk(reinterpret_cast<const Raw*>(y + (int64_t)c * F + tl * V));
     }
     float v[EB];
 #pragma unroll
@@ -249,7 +268,7 @@ k_sddmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* _
 // from the previous edge of the batch when the row repeats).  Per-edge
 // arithmetic and the butterfly grouping are k_sddmm_fast's: bitwise equal.
 template <typename T, int V, int TEAM, int G>
-__global__ void __launch_bounds__(256, 4)
+__global__ void __launch_bounds__(256, V * sizeof(T) == 32 ? 2 : 4)
 k_sddmm_packed(const int4* __restrict__ packs, int64_t num_packs, const int32_t* __restrict__ rowid,
                const int32_t* __restrict__ cols, const T* __restrict__ x,
                const T* __restrict__ y, T* __restrict__ out, int F, int heads) {
@@ -292,9 +311,9 @@ k_sddmm_packed(const int4* __restrict__ packs, int64_t num_packs, const int32_t*
       const int c = __shfl_sync(tmask, cq[j / TEAM], tb + j % TEAM);
       rj[j] = __shfl_sync(tmask, rq[j / TEAM], tb + j % TEAM);
       if (rj[j] >= 0 && cval) {
-        yr[j] = __ldg(reinterpret_cast<const Raw*>(y + (int64_t)c * F + tl * V));
+        yr[j] = ldg_chunk(reinterpret_cast<const Raw*>(y + (int64_t)c * F + tl * V));
         if (j == 0 || rj[j] != rj[j - 1])
-          xr[j] = __ldg(reinterpret_cast<const Raw*>(x + (int64_t)rj[j] * F + tl * V));
+          xr[j] = ldg_chunk(reinterpret_cast<const Raw*>(x + (int64_t)rj[j] * F + tl * V));
       }
     }
 #pragma unroll
@@ -431,6 +450,16 @@ static int dispatch_sddmm(const int4* units, int64_t nu, const int32_t* cols, co
   HG_REQUIRE(false, "hg_sddmm: feature length %d too large", F);
 }
 
+// 32-byte lanes for binary16 rows of 64..512 elements with 16-element heads
+// (A/B switch for measurement: HG_SPMM_LANE32=0, as for hg_spmm).
+static bool sd_lane32() {
+  static const bool on = [] {
+    const char* e = getenv("HG_SPMM_LANE32");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 extern "C" int hg_sddmm_fast(const int64_t* offsets, const int32_t* cols, int64_t n_rows,
                              int64_t num_edges, const int32_t* units, int64_t num_units,
                              const int32_t* packs, int64_t num_packs, const int32_t* pack_rowid,
@@ -448,7 +477,10 @@ extern "C" int hg_sddmm_fast(const int64_t* offsets, const int32_t* cols, int64_
              pack_rowid};
   HG_REQUIRE(pk.np == 0 || pack_rowid, "hg_sddmm_fast: packs need pack_rowid");
   int rc = -1;
-  if (dtype == HG_F16 && aligned && fh % 8 == 0)
+  const bool aligned32 = reinterpret_cast<uintptr_t>(x) % 32 == 0 && reinterpret_cast<uintptr_t>(y) % 32 == 0;
+  if (dtype == HG_F16 && aligned32 && fh % 16 == 0 && F >= 64 && F <= 512 && sd_lane32())
+    rc = dispatch_sddmm_fast<__half, 16>(u, num_units, pk, cols, x, y, out, F, heads, st);
+  else if (dtype == HG_F16 && aligned && fh % 8 == 0)
     rc = dispatch_sddmm_fast<__half, 8>(u, num_units, pk, cols, x, y, out, F, heads, st);
   else if (dtype == HG_F16)
     rc = dispatch_sddmm_fast<__half, 2>(u, num_units, pk, cols, x, y, out, F, heads, st);

@@ -619,6 +619,16 @@ def _butterfly_layout(x, y, f, heads):
     return f // v <= 32 and g >= 1 and g & (g - 1) == 0 and (f // v) % g == 0
 
 
+LANE32 = os.environ.get("HG_SPMM_LANE32", "1") != "0"
+
+
+def _sddmm_lane32(x, y, f, heads):
+    """hg_sddmm_fast's 32-byte-lane rule (binary16, 64..512 features, heads of
+    16-element multiples, 32-byte aligned operands)."""
+    return (LANE32 and x.dtype == torch.float16 and x.data_ptr() % 32 == 0
+            and y.data_ptr() % 32 == 0 and (f // heads) % 16 == 0 and 64 <= f <= 512)
+
+
 def sddmm(dg: DeviceGraph, x, y, heads=1, transpose=False, fast=False):
     """Per-edge (per-head) tree dot products, bit-exact with kernels.sddmm
     (fast=True: fp32 accumulation, one rounding -- hg_sddmm_fast).
@@ -633,7 +643,10 @@ def sddmm(dg: DeviceGraph, x, y, heads=1, transpose=False, fast=False):
     f = x.shape[1]
     out = torch.empty((view.num_edges, heads), dtype=x.dtype, device=x.device)
     if fast:
-        packed = PACKING and view.n_rows >= PACK_MIN_ROWS and _butterfly_layout(x, y, f, heads)
+        # packs only for the 16-byte-lane kernels: with 32-byte lanes the unit
+        # kernel alone was faster on RMAT-24 (F=128: 11.56 vs 11.78 ms)
+        packed = (PACKING and view.n_rows >= PACK_MIN_ROWS and _butterfly_layout(x, y, f, heads)
+                  and not _sddmm_lane32(x, y, f, heads))
         sched = view.schedule(DEFAULT_SPLIT_CAP, PACK_EDGES_WIDE if packed else -1)
         nat.call("hg_sddmm_fast", _p(view.offsets), _p(view.cols), view.n_rows, view.num_edges,
                  _p(sched.units), sched.num_units, _p(sched.packs), sched.num_packs,

@@ -800,14 +800,15 @@ def test_sddmm_packed_bitwise_equal_units(cuda, heads, fh, dtype):
     f = heads * fh
     x = torch.randn(n, f, device=cuda).to(dtype)
     y = torch.randn(n, f, device=cuda).to(dtype)
-    saved = D.PACK_MIN_ROWS
+    saved = (D.PACK_MIN_ROWS, D.LANE32)
     try:
+        D.LANE32 = False   # packs run with the 16-byte-lane kernels only
         D.PACK_MIN_ROWS = 1 << 40
         want = D.sddmm(dg, x, y, heads=heads, fast=True)
         D.PACK_MIN_ROWS = 0
         got = D.sddmm(dg, x, y, heads=heads, fast=True)
     finally:
-        D.PACK_MIN_ROWS = saved
+        D.PACK_MIN_ROWS, D.LANE32 = saved
     it = torch.int16 if dtype == torch.float16 else torch.int32
     assert torch.equal(got.contiguous().view(it), want.contiguous().view(it))
     if D._butterfly_layout(x, y, f, heads):
