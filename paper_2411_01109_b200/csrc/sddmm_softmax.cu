@@ -1487,24 +1487,43 @@ k_head_dots_bwd_v8(const __half* __restrict__ z, const __half* __restrict__ al,
   if (act) {
     *reinterpret_cast<uint4*>(a1) = *reinterpret_cast<const uint4*>(al + c * 8);
     *reinterpret_cast<uint4*>(a2) = *reinterpret_cast<const uint4*>(ar + c * 8);
-    for (int64_t r = (int64_t)blockIdx.x * rpi + rr; r < n; r += (int64_t)gridDim.x * rpi) {
-      const __half g1 = gl[r * heads + h], g2 = gr[r * heads + h];
-      const float g1f = __half2float(g1), g2f = __half2float(g2);
-      const uint4 zv = *reinterpret_cast<const uint4*>(z + r * F + c * 8);
-      const __half* ze = reinterpret_cast<const __half*>(&zv);
-      __align__(16) __half o[8];
-      uint4 prev = make_uint4(0, 0, 0, 0);
-      if (gz_in) prev = *reinterpret_cast<const uint4*>(gz_in + r * F + c * 8);
-      const __half* pe = reinterpret_cast<const __half*>(&prev);
+    // RU rows per step, all their loads issued before any use (the row loop
+    // was latency-bound with one 16-byte load in flight); rows still fold
+    // into sl / sr in the same order, so the result is unchanged.
+    constexpr int RU = 4;
+    const int64_t stride = (int64_t)gridDim.x * rpi;
+    for (int64_t r0 = (int64_t)blockIdx.x * rpi + rr; r0 < n; r0 += stride * RU) {
+      __half g1[RU], g2[RU];
+      uint4 zv[RU], prev[RU];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        o[i] = __hadd_rn(__hmul_rn(g1, a1[i]), __hmul_rn(g2, a2[i]));
-        if (gz_in) o[i] = __hadd_rn(pe[i], o[i]);
-        const float zf = __half2float(ze[i]);
-        sl[i] = fmaf(zf, g1f, sl[i]);
-        sr[i] = fmaf(zf, g2f, sr[i]);
+      for (int u = 0; u < RU; ++u) {
+        const int64_t r = r0 + u * stride;
+        prev[u] = make_uint4(0, 0, 0, 0);
+        if (r < n) {
+          g1[u] = gl[r * heads + h];
+          g2[u] = gr[r * heads + h];
+          zv[u] = *reinterpret_cast<const uint4*>(z + r * F + c * 8);
+          if (gz_in) prev[u] = *reinterpret_cast<const uint4*>(gz_in + r * F + c * 8);
+        }
       }
-      *reinterpret_cast<uint4*>(gz + r * F + c * 8) = *reinterpret_cast<const uint4*>(o);
+#pragma unroll
+      for (int u = 0; u < RU; ++u) {
+        const int64_t r = r0 + u * stride;
+        if (r >= n) break;
+        const float g1f = __half2float(g1[u]), g2f = __half2float(g2[u]);
+        const __half* ze = reinterpret_cast<const __half*>(&zv[u]);
+        const __half* pe = reinterpret_cast<const __half*>(&prev[u]);
+        __align__(16) __half o[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          o[i] = __hadd_rn(__hmul_rn(g1[u], a1[i]), __hmul_rn(g2[u], a2[i]));
+          if (gz_in) o[i] = __hadd_rn(pe[i], o[i]);
+          const float zf = __half2float(ze[i]);
+          sl[i] = fmaf(zf, g1f, sl[i]);
+          sr[i] = fmaf(zf, g2f, sr[i]);
+        }
+        *reinterpret_cast<uint4*>(gz + r * F + c * 8) = *reinterpret_cast<const uint4*>(o);
+      }
     }
   }
   float* bl = hdb_sh;
