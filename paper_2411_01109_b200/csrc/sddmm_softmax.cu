@@ -1369,14 +1369,17 @@ k_head_dots(const T* __restrict__ z, const T* __restrict__ al, const T* __restri
   const int64_t items = n * heads;
   const int64_t stride = (int64_t)gridDim.x * (blockDim.x / TEAM);
   const int nchunk = fh / V;
-  // grid-stride, two (node, head) items in flight per team
+  // grid-stride, IU (node, head) items in flight per team
+  constexpr int IU = 4;
   for (int64_t it0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TEAM; it0 < items;
-       it0 += 2 * stride) {
-    float pl[2] = {0.0f, 0.0f}, pr[2] = {0.0f, 0.0f};
-    for (int c = tl; c < nchunk; c += TEAM) {
-      Raw zr[2];
+       it0 += IU * stride) {
+    float pl[IU], pr[IU];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < IU; ++u) pl[u] = pr[u] = 0.0f;
+    for (int c = tl; c < nchunk; c += TEAM) {
+      Raw zr[IU];
+#pragma unroll
+      for (int u = 0; u < IU; ++u) {
         const int64_t item = it0 + u * stride;
         if (item < items) {
           const int64_t node = item / heads;
@@ -1385,7 +1388,7 @@ k_head_dots(const T* __restrict__ z, const T* __restrict__ al, const T* __restri
         }
       }
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < IU; ++u) {
         const int64_t item = it0 + u * stride;
         if (item >= items) continue;
         const int h = (int)(item % heads);
@@ -1404,7 +1407,7 @@ k_head_dots(const T* __restrict__ z, const T* __restrict__ al, const T* __restri
       }
     }
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < IU; ++u) {
 #pragma unroll
       for (int o = TEAM / 2; o >= 1; o >>= 1) {
         pl[u] += __shfl_xor_sync(tmask, pl[u], o, TEAM);
