@@ -513,15 +513,27 @@ __global__ void k_head_mean_v8(const __half* __restrict__ y, int64_t n, int head
     double s[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) s[k] = 0.0;
-    for (int h = 0; h < heads; ++h) {
-      const uint4 v = *reinterpret_cast<const uint4*>(y + (r * heads + h) * f + c * 8);
-      const __half* e = reinterpret_cast<const __half*>(&v);
+    // up to 8 heads loaded before any add (the head loop was one dependent
+    // load per step); sums in head order as before
+    for (int h0 = 0; h0 < heads; h0 += 8) {
+      uint4 v[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) s[k] += (double)__half2float(e[k]);
+      for (int u = 0; u < 8; ++u)
+        if (h0 + u < heads) v[u] = *reinterpret_cast<const uint4*>(y + (r * heads + h0 + u) * f + c * 8);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (h0 + u >= heads) break;
+        const __half* e = reinterpret_cast<const __half*>(&v[u]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) s[k] += (double)__half2float(e[k]);
+      }
     }
     __align__(16) __half o[8];
+    // power-of-two head counts: the quotient is an exact scaling
+    const bool p2 = (heads & (heads - 1)) == 0;
+    const double inv = 1.0 / heads;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) o[k] = __double2half(s[k] / heads);
+    for (int k = 0; k < 8; ++k) o[k] = __double2half(p2 ? s[k] * inv : s[k] / heads);
     *reinterpret_cast<uint4*>(out + r * f + c * 8) = *reinterpret_cast<const uint4*>(o);
   }
 }
