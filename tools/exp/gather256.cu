@@ -5,8 +5,16 @@
 
 struct V8 { uint32_t a[8]; };
 
+template <int MODE>
 __device__ __forceinline__ V8 ld256(const void* p) {
   V8 v;
+  if constexpr (MODE == 1) {
+    asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v.a[0]), "=r"(v.a[1]), "=r"(v.a[2]), "=r"(v.a[3]), "=r"(v.a[4]),
+                   "=r"(v.a[5]), "=r"(v.a[6]), "=r"(v.a[7])
+                 : "l"(p));
+    return v;
+  }
   asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(v.a[0]), "=r"(v.a[1]), "=r"(v.a[2]), "=r"(v.a[3]), "=r"(v.a[4]),
                  "=r"(v.a[5]), "=r"(v.a[6]), "=r"(v.a[7])
@@ -14,7 +22,7 @@ __device__ __forceinline__ V8 ld256(const void* p) {
   return v;
 }
 
-template <int TEAM, int BYTES>
+template <int TEAM, int BYTES, int MODE = 0>
 __global__ void __launch_bounds__(256) k_probe(const int* __restrict__ cols, int64_t E,
                                                const char* __restrict__ x, int64_t ld,
                                                unsigned* out) {
@@ -30,7 +38,7 @@ __global__ void __launch_bounds__(256) k_probe(const int* __restrict__ cols, int
 #pragma unroll
       for (int k = 0; k < TEAM; ++k) {
         const int r = __shfl_sync(0xffffffffu, c, k * RPL + slot);
-        if (r >= 0) v[k] = ld256(x + (int64_t)r * ld + sub * 32);
+        if (r >= 0) v[k] = ld256<MODE>(x + (int64_t)r * ld + sub * 32);
         else for (int i = 0; i < 8; ++i) v[k].a[i] = 0;
       }
 #pragma unroll
@@ -57,7 +65,14 @@ extern "C" int probe(const int* cols, int64_t E, const void* x, int64_t ld, int 
                      int lane_bytes, unsigned* out, int blocks, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const char* xb = (const char*)x;
-  if (lane_bytes == 32) {
+  if (lane_bytes == 33) {
+    switch (row_bytes / 32) {
+      case 2: k_probe<2, 32, 1><<<blocks, 256, 0, st>>>(cols, E, xb, ld, out); break;
+      case 4: k_probe<4, 32, 1><<<blocks, 256, 0, st>>>(cols, E, xb, ld, out); break;
+      case 8: k_probe<8, 32, 1><<<blocks, 256, 0, st>>>(cols, E, xb, ld, out); break;
+      default: return 1;
+    }
+  } else if (lane_bytes == 32) {
     switch (row_bytes / 32) {
       case 2: k_probe<2, 32><<<blocks, 256, 0, st>>>(cols, E, xb, ld, out); break;
       case 4: k_probe<4, 32><<<blocks, 256, 0, st>>>(cols, E, xb, ld, out); break;
