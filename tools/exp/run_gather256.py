@@ -1,4 +1,5 @@
-"""Random-row gather: 16-byte vs 32-byte lane loads on the C3 column stream."""
+"""Random-row gather: 16-byte vs 32-byte lane loads (and 32-byte with
+L1::no_allocate, lane code 33) on the C3 column stream.  Experiment only."""
 import ctypes
 import json
 import subprocess
@@ -12,7 +13,7 @@ sys.path.insert(0, str(HERE.parents[1]))
 import bench  # noqa: E402
 
 so = HERE / "gather256.so"
-if True:
+if not so.exists() or so.stat().st_mtime < (HERE / "gather256.cu").stat().st_mtime:
     subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-shared",
                     "-Xcompiler", "-fPIC", str(HERE / "gather256.cu"), "-o", str(so)], check=True)
 lib = ctypes.CDLL(str(so))
