@@ -27,6 +27,10 @@ import subprocess
 import sys
 import tempfile
 import time
+
+# stdout carries exactly one JSON line: NCCL's debug log goes to stderr unless
+# the caller chose a file (its version banner: see the process-group setup)
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
@@ -119,13 +123,14 @@ def dist_env():
     return ws, rank, local
 
 
-def max_over_ranks(dist, v):
-    """Max of a host float over ranks (device tensor for NCCL, host for gloo)."""
+def max_over_ranks(dist, v, op="max"):
+    """Max (or sum) of a host float over ranks (device tensor for NCCL, host
+    for gloo)."""
     import torch
 
     dev = "cpu" if dist.get_backend() == "gloo" else "cuda"
     tt = torch.tensor([v], device=dev, dtype=torch.float64)
-    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
     return float(tt.item())
 
 
@@ -367,7 +372,20 @@ def b200_arm(args, ws, rank, local):
 
         backend = os.environ.get("HG_DIST_BACKEND", "nccl")
         if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            # NCCL prints its version banner on stdout (NCCL_DEBUG=VERSION);
+            # stdout must carry only the JSON line, so the communicator is
+            # created (eagerly, device_id + a barrier) with fd 1 on stderr
+            sys.stdout.flush()
+            saved = os.dup(1)
+            os.dup2(2, 1)
+            try:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+                dist.barrier()
+                torch.cuda.synchronize()
+            finally:
+                sys.stdout.flush()
+                os.dup2(saved, 1)
+                os.close(saved)
         else:
             dist.init_process_group(backend)
     peak, peak_kind = peaks()
@@ -449,23 +467,46 @@ def b200_arm(args, ws, rank, local):
     lo, hi = (tr.part.lo, tr.part.hi) if use_dist else (0, dg.n)
     host_x = inner.host_features(x[lo:hi].cpu())
     h2d = host_x.numel() * host_x.element_size()
+    if dist is not None:  # whole-job bytes: every rank copies its own rows
+        h2d = int(max_over_ranks(dist, float(h2d), op="sum"))
+    def dist_feed(k):
+        """k partitioned steps fed from pinned host memory: the next step's
+        host->device copy runs on a side stream into a staging buffer while the
+        current step computes (as Trainer.run_epochs does on one GPU); a
+        device-to-device copy moves it into the captured graph's input."""
+        cur_s, side = torch.cuda.current_stream(), torch.cuda.Stream()
+        stage = [torch.empty_like(inner.x), torch.empty_like(inner.x)]
+        copied = [torch.cuda.Event(), torch.cuda.Event()]
+        used = [torch.cuda.Event(), torch.cuda.Event()]
+        side.wait_stream(cur_s)
+        with torch.cuda.stream(side):
+            stage[0].copy_(host_x, non_blocking=True)
+            copied[0].record()
+        for i in range(k):
+            cur, nxt = i % 2, 1 - i % 2
+            if i + 1 < k:
+                with torch.cuda.stream(side):
+                    if i >= 1:
+                        side.wait_event(used[nxt])
+                    stage[nxt].copy_(host_x, non_blocking=True)
+                    copied[nxt].record()
+            cur_s.wait_event(copied[cur])
+            inner.x.copy_(stage[cur])
+            used[cur].record()
+            loss, _ = tr.step()
+            float(loss)
+
     # untimed warm-up of the same path (first copies out of the fresh pinned
     # buffer, the feed's side stream and events)
     if use_dist:
-        for _ in range(min(2, args.warmup)):
-            inner.x.copy_(host_x, non_blocking=True)
-            loss, _ = tr.step()
-            float(loss)
+        dist_feed(min(2, args.warmup))
     else:
         tr.run_epochs(host_x, min(2, args.warmup))
     barrier()
     torch.cuda.synchronize()
     e0 = time.perf_counter()
     if use_dist:
-        for _ in range(args.steps):
-            inner.x.copy_(host_x, non_blocking=True)
-            loss, _ = tr.step()
-            float(loss)
+        dist_feed(args.steps)
     else:
         tr.run_epochs(host_x, args.steps)
     torch.cuda.synchronize()
@@ -487,7 +528,7 @@ def b200_arm(args, ws, rank, local):
             "config": workload_config(dg.n, dg.num_edges, parallelism, args.workload),
             "clocks": clocks.summary(),
             "e2e": {"value": round(e2e_ms, 4), "unit": "ms/epoch", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": 4},
+                    "d2h_bytes_per_step": 4 * ws},
             "gpu_launches": int(launches),
             "ms_per_step_eager": round(eager_ms, 4), "cuda_graph": graphed,
             "roofline": {"bound": "hbm", "achieved": round(achieved / 1e9, 1),
