@@ -44,8 +44,21 @@ LONG_ROW = 4096   # rows longer than this get a whole CTA in the row-owned softm
 SHORT_ROW = 32    # fast GAT kernels: rows up to this many edges get one thread per head
 
 
+class _Ptr(ctypes.c_void_p):
+    """A device pointer argument that keeps its tensor alive until the C call
+    has returned (the kernel is then enqueued), so inline temporaries such as
+    `_p(t.contiguous())` cannot be freed and their block handed to the next
+    argument's temporary before the launch."""
+
+    __slots__ = ("_keep",)
+
+
 def _p(t):
-    return None if t is None else ctypes.c_void_p(t.data_ptr())
+    if t is None:
+        return None
+    ptr = _Ptr(t.data_ptr())
+    ptr._keep = t
+    return ptr
 
 
 def _stream():

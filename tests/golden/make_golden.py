@@ -335,6 +335,21 @@ def gen_training():
     save("training.npz", **d)
 
 
+def gen_c2(mode="half"):
+    """C2 (Pubmed-shaped synth_sbm, 3-layer x 4-head x 16 GAT, classes 3 -> 4):
+    200 epochs of the reference harness (models.py:633-684 composed from
+    GATLayer, models.py:492-509).  About 40 min per mode on the build host;
+    run as `make_golden.py c2 half` / `c2 float32` (one file per mode)."""
+    g, x, labels = sp.synth_sbm(19717, 3, 0.00057, 5.71e-5, 500, 0)
+    cfg = M.TrainConfig(kind="gat", mode=mode, epochs=200, seed=0, hidden=16)
+    losses, accs, sec = harness_train(g, x.data, labels, cfg, 4, heads=4, layers=3)
+    save(f"c2_{mode}.npz", num_edges=np.int64(g.num_edges), loss=losses, acc=accs,
+         sec_per_epoch=np.float64(sec), config=np.str_(
+             "synth_sbm(19717,3,0.00057,5.71e-5,500,0); GAT 3 layers x 4 heads x 16, "
+             "concat + relu between layers, mean at the output; TrainConfig(seed=0, "
+             f"mode={mode}, epochs=200); classes padded 3 -> 4"))
+
+
 INGEST_CASES = [
     # (text, num_vertices, symmetrize)
     (b"# a comment\n0 1\n% another\n1 2\n\n2 0\n", None, False),    # test_sparse.py:127-131
@@ -411,5 +426,8 @@ def gen_ingest():
 if __name__ == "__main__":
     which = sys.argv[1:] or ["graph", "factors", "spmm", "vertex", "sddmm", "attention", "training",
                              "ingest"]
+    if which[0] == "c2":
+        gen_c2(*which[1:])
+        sys.exit(0)
     for w in which:
         globals()[f"gen_{w}" if w != "graph" else "gen_graph_build"]()
