@@ -28,9 +28,6 @@ import sys
 import tempfile
 import time
 
-# stdout carries exactly one JSON line: NCCL's debug log goes to stderr unless
-# the caller chose a file (its version banner: see the process-group setup)
-os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
@@ -134,92 +131,96 @@ def max_over_ranks(dist, v, op="max"):
     return float(tt.item())
 
 
-def load_traffic_profile(workload):
-    """ncu dram bytes per k_spmm_fast launch of this workload's epoch, from the
-    committed profile summary (None when that workload was not captured)."""
-    p = ROOT / "profiles" / "r01" / "ncu_spmm_summary.json"
-    try:
-        d = json.loads(p.read_text()).get(workload)
-        return d["bytes_per_launch"] if d else None
-    except Exception:
-        return None
+def load_traffic_profile(workload, ws):
+    """ncu DRAM bytes per hg_spmm call of this workload's epoch from the newest
+    committed `ncu --set full` summary (profiles/r*/ncu_spmm_summary.json), with
+    its source; (None, None) when that workload was not captured at this world
+    size (per-rank captures exist only for one GPU)."""
+    if ws != 1:
+        return None, None
+    for rnd in ("r02", "r01"):
+        p = ROOT / "profiles" / rnd / "ncu_spmm_summary.json"
+        try:
+            d = json.loads(p.read_text()).get(workload)
+        except Exception:
+            continue
+        if d:
+            return d["bytes_per_launch"], f"profiles/{rnd}/ncu_spmm_summary.json"
+    return None, None
 
 
-# ── CPU baseline (oracle restatement of the reference, row-panel sample) ──
+# ── CPU legs: the reference on the host cores (tools/refarm.py) ──
 
 
-def cpu_baseline_gcn(offsets, cols, x16, labels, budget_edges, kind="gcn", hidden=HIDDEN,
-                     heads=1, layers=2):
-    """Time one reference GCN epoch (oracle.train_epochs) on the first rows of the
-    graph holding ~budget_edges edges (all N vertices, all features), then
-    extrapolate: t = dense + sparse * E / E_sample.  Returns (ms, sample text, cores)."""
-    import numpy as np
+def cpu_leg_impl(cfg):
+    """('reference', halfsparse) when the unmodified reference is installed
+    under baseline/_ref and its Model covers the workload (2-layer, 1 head);
+    else ('port', None): the numpy restatement in oracle/."""
+    from tools import refarm as R
 
-    import oracle as O
+    H = R.load_reference()
+    if H is not None and cfg.get("heads", 1) == 1 and cfg.get("layers", 2) == 2:
+        return "reference", H
+    return "port", None
 
-    n = offsets.size - 1
-    e_total = int(offsets[-1])
-    r_end = int(np.searchsorted(offsets, budget_edges, side="left"))
-    r_end = max(1, min(r_end, n))
-    e_s = int(offsets[r_end])
-    rows = np.repeat(np.arange(r_end, dtype=np.int64), np.diff(offsets[: r_end + 1]))
-    g = O.OracleGraph(n, rows, cols[:e_s].astype(np.int64))
-    timer = O.Timer()
-    t0 = time.perf_counter()
-    O.train_epochs(g, x16.astype(np.float32), labels, kind=kind, mode="half", epochs=1,
-                   hidden=hidden, heads=heads, layers=layers, timer=timer)
-    wall = time.perf_counter() - t0
-    other = max(0.0, wall - timer.dense - timer.sparse)
-    ms = (timer.dense + other + timer.sparse * e_total / max(e_s, 1)) * 1e3
-    sample = (f"rows [0,{r_end}) = {e_s:,} of {e_total:,} edges, all {n:,} vertices; "
-              f"sparse {timer.sparse:.2f}s x{e_total / max(e_s, 1):.1f} + dense {timer.dense:.2f}s"
-              f" + other {other:.2f}s (numpy oracle: sparse kernels single-threaded, dense "
-              f"BLAS on all cores)")
-    try:
-        cores = len(os.sched_getaffinity(0))
-    except AttributeError:
-        cores = os.cpu_count() or 1
-    return ms, sample, cores
+
+def cpu_baseline(name, seed, budget_edges, torch_comparator=True):
+    """cpu_baseline object of the B200 arm: one reference epoch on a random
+    row-panel sample (after a small calibration epoch), extrapolated to the
+    full graph; plus the torch-CPU fp32 comparator for GCN."""
+    from tools import refarm as R
+
+    w = WORKLOADS[name]
+    hw = R.HostWorkload(name, seed, w["feat"], w["classes"])
+    impl, H = cpu_leg_impl(w["cfg"])
+    leg = R.CpuLeg(hw, impl, w["cfg"], H)
+    ms = leg.step(budget_edges, sample_seed=seed + 17)
+    cc = R.core_counts()
+    out = {"value": round(ms, 1), "unit": "ms/epoch", "cores": cc["sched_affinity"],
+           "kind": impl, "extrapolated": budget_edges < hw.num_edges,
+           "sample": leg.describe(budget_edges), "core_counts": cc,
+           "threads_note": "sparse operators single-threaded numpy; dense BLAS on all cores"}
+    if torch_comparator and w["cfg"]["kind"] == "gcn":
+        tl = R.CpuLeg(hw, "torch", w["cfg"])
+        tms = tl.step(min(4 * budget_edges, hw.num_edges), sample_seed=seed + 18)
+        out["torch_cpu_fp32"] = {"value": round(tms, 1), "unit": "ms/epoch",
+                                 "cores": cc["torch_threads"], "sample": tl.describe(
+                                     min(4 * budget_edges, hw.num_edges))}
+    return out
 
 
 def reference_arm(args, ws, rank):
-    """--impl reference: the reference's CPU path (oracle port) on this host, rank 0 only."""
+    """--impl reference: the reference's own CPU path on this host's cores,
+    rank 0 only (other ranks exit without work).  No GPU, no libhalfgnn.so:
+    the graph rows are regenerated on the host (synth.py)."""
     if rank != 0:
         return
-    import numpy as np
-    import torch
+    from tools import refarm as R
 
-    from paper_2411_01109_b200 import graphgen
-
-    if not torch.cuda.is_available():
-        raise SystemExit("reference arm needs the graph generator (GPU)")
-    dg, x, labels = build_workload(args.workload, args.seed)
-    offsets = dg.offsets.cpu().numpy()
-    cols = dg.cols.cpu().numpy()
-    x16, lab = x.cpu().numpy(), labels.cpu().numpy()
-    del dg
-    steps = args.steps + args.warmup
-    # the same row-panel sample every step (the per-edge cost of the reference's
-    # Python loops is only linear once fixed costs are amortised, so a fixed
-    # ~400K-edge sample keeps the extrapolation consistent with cpu_baseline);
-    # shrink it only for long runs so the arm still ends within a few minutes
-    budget = args.ref_budget_edges if steps <= 30 else max(100_000, args.ref_budget_edges * 30 // steps)
-    vals = []
-    sample = cores = None
-    for i in range(steps):
-        ms, sample, cores = cpu_baseline_gcn(offsets, cols, x16, lab, budget,
-                                             **WORKLOADS[args.workload]["cfg"])
-        if i >= args.warmup:
-            vals.append(ms)
-    v = statistics.median(vals) if vals else ms
+    w = WORKLOADS[args.workload]
+    hw = R.HostWorkload(args.workload, args.seed, w["feat"], w["classes"])
+    impl, H = cpu_leg_impl(w["cfg"])
+    leg = R.CpuLeg(hw, impl, w["cfg"], H)
+    # per-step sample: >= 1M edges sampled over the timed steps in total, and
+    # the whole run bounded to a few minutes (the dense part is full size)
+    budget = args.ref_budget_edges or max(100_000, 2_000_000 // max(args.steps, 1))
+    for i in range(args.warmup):
+        leg.step(min(budget, 20_000), sample_seed=10_000 + i, warm=True)
+    vals = [leg.step(budget, sample_seed=args.seed * 1000 + i) for i in range(args.steps)]
+    v = round(statistics.median(vals), 1)
+    cc = R.core_counts()
     line = {"metric": METRIC, "value": v, "unit": "ms/epoch", "impl": "reference",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": v,
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f16", "data": "synthetic",
-            "config": workload_config(int(offsets.size - 1), int(offsets[-1]),
-                                      name=args.workload),
-            "cpu_baseline": {"value": v, "unit": "ms/epoch", "cores": cores, "kind": "port",
-                             "sample": sample},
+            "dtype": "f16", "data": "synthetic (the B200 arm's graph rows, regenerated on the "
+                                    "host by synth.py)",
+            "config": workload_config(hw.n, hw.num_edges, name=args.workload),
+            "extrapolated": budget < hw.num_edges,
+            "scale_factor": round(hw.num_edges * leg.steps / max(leg.sampled_edges, 1), 1),
+            "per_step_ms": [round(x, 1) for x in vals],
+            "cpu_baseline": {"value": v, "unit": "ms/epoch", "cores": cc["sched_affinity"],
+                             "kind": impl, "sample": leg.describe(budget),
+                             "extrapolated": budget < hw.num_edges, "core_counts": cc},
             "e2e": {"value": v, "unit": "ms/epoch", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -340,12 +341,18 @@ def small_configs(args, peak):
         rec = {"ms_per_epoch": timed(), "ms_per_epoch_eager": eager, "cuda_graph": True,
                "nodes": n, "edges": int(rows.size)}
         if not args.no_cpu_baseline:
-            import oracle as O
+            from tools import refarm as R
 
-            g = O.OracleGraph(n, rows, cols)
-            t0 = time.perf_counter()
-            O.train_epochs(g, feats, labels, epochs=1, **kw)
-            rec["cpu_oracle_ms_per_epoch"] = round((time.perf_counter() - t0) * 1e3, 1)
+            impl, H = cpu_leg_impl(kw)
+            r64, c64 = rows.astype(np.int64), cols.astype(np.int64)
+            x16 = feats.astype(np.float16)
+            if impl == "reference":
+                s_, o_ = R.reference_epoch(H, n, r64, c64, x16, labels, kw["kind"], kw["hidden"])
+            else:
+                s_, o_ = R.port_epoch(n, r64, c64, x16, labels, kw["kind"], kw["hidden"],
+                                      kw.get("heads", 1), kw.get("layers", 2))
+            rec["cpu_ms_per_epoch"] = round((s_ + o_) * 1e3, 1)
+            rec["cpu_kind"] = impl
         out[name] = rec
     return out
 
@@ -431,7 +438,12 @@ def b200_arm(args, ws, rank, local):
 
     # ---- eager pass: SpMM roofline (CUDA events around every hg_spmm) ----
     D.Probe.reset(timing=True)
+    rb0 = tr.bundle.ex.recv_bytes if use_dist else 0
     eager_ms, _ = timed_steps(args.steps)
+    recv_per_step = (tr.bundle.ex.recv_bytes - rb0) / args.steps if use_dist else 0.0
+    if dist is not None:
+        recv_max = max_over_ranks(dist, recv_per_step)
+        recv_sum = max_over_ranks(dist, recv_per_step, op="sum")
     launches = D.Probe.launches
     spmm_b, spmm_s, spmm_n = D.Probe.summary()
     compulsory = D.Probe.compulsory_per_launch()
@@ -444,6 +456,16 @@ def b200_arm(args, ws, rank, local):
     ceil = D.Probe.gather_ceiling()
     if ceil:
         ceiling_s = (ceil, probe_s)
+    # the L2 random-gather roof (live), and the eager pass's calls priced at it
+    from tools import l2_gather_peak
+
+    l2_peak = l2_gather_peak.measure() if rank == 0 else None
+    D.Probe.reset(timing=True)
+    timed_steps(1)
+    _, _, _ = D.Probe.summary()
+    l2_ideal = D.Probe.l2_ideal_seconds(l2_peak) if l2_peak else None
+    if l2_ideal is not None:   # scale to the eager pass's per-step SpMM time
+        l2_ideal *= args.steps
     D.Probe.reset(timing=False)
 
     # ---- device-resident timing (value): the step replayed as a CUDA graph ----
@@ -518,7 +540,17 @@ def b200_arm(args, ws, rank, local):
     result = None
     if rank == 0:
         achieved = spmm_b / spmm_s if spmm_s > 0 else 0.0
-        traffic = load_traffic_profile(args.workload)
+        traffic, traffic_src = load_traffic_profile(args.workload, ws)
+        dram_gbs = traffic * spmm_n / spmm_s / 1e9 if traffic and spmm_s > 0 else None
+        l2 = None
+        if l2_peak:
+            ideal = l2_ideal
+            l2 = {"peak_GBps_by_row_bytes": {str(k): round(v, 1) for k, v in l2_peak.items()},
+                  "frac": round(ideal / spmm_s, 4) if ideal and spmm_s > 0 else None,
+                  "what": "tools/l2_gather_peak.py, run live: hg_gather_probe on uniform random "
+                          "ids over a 32 MB L2-resident table (same gather-model bytes); frac = "
+                          "time the step's hg_spmm calls would take at that rate for their row "
+                          "widths / their measured time"}
         result = {
             "metric": METRIC, "value": round(t_ms, 4), "unit": "ms/epoch", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_ms, 4),
@@ -537,10 +569,18 @@ def b200_arm(args, ws, rank, local):
                          "kernel": "k_spmm_fast (hg_spmm)", "launches": spmm_n,
                          "peak_source": peak_kind,
                          "bytes_model": "4E+8(N+1)+2FE+2FN per SpMM launch, F = stored width",
+                         "frac_note": ("achieved counts every gathered row (SURVEY 8(d) gather "
+                                       "model); above 1 the rows are served from L2, not HBM -- "
+                                       "read hbm_dram_frac for DRAM and l2.frac for the L2 "
+                                       "gather roof" if achieved > peak else None),
+                         "hbm_dram_frac": (round(dram_gbs * 1e9 / peak, 4)
+                                           if dram_gbs else None),
+                         "traffic_source": traffic_src,
                          "compulsory_bytes": round(compulsory),
                          "traffic_over_compulsory": (round(traffic / compulsory, 3)
                                                      if traffic and compulsory else None),
                          "compulsory_model": "4E+8(N+1)+2F(N_cols+N_rows): ids, X once, Y once",
+                         "l2": l2,
                          "gather_ceiling": (None if ceiling_s is None else {
                              "spmm_ms_per_step": round(ceiling_s[1] * 1e3, 4),
                              "probe_ms_per_step": round(ceiling_s[0] * 1e3, 4),
@@ -548,6 +588,13 @@ def b200_arm(args, ws, rank, local):
                              "what": "hg_gather_probe: the same column ids, feature buffers and "
                                      "widths as the step's hg_spmm calls, loads only (X warm in "
                                      "L2); frac = probe time / hg_spmm time"})},
+            "exchange": (None if not use_dist else {
+                "recv_bytes_per_rank_per_step_max": int(recv_max),
+                "recv_bytes_per_step_total": int(recv_sum),
+                "n_rows_max_over_mean": round(tr.part.n_max * ws / dg.n, 4),
+                "what": "bytes each rank receives per epoch over the fabric: exact-count "
+                        "feature / gradient all-gathers ((N - n_local) rows each) and the GAT "
+                        "edge-value all-to-all; the static GIN input gathered once at load"}),
             "final_loss": round(final_loss, 5),
             "grad_scale": (tr.inner if use_dist else tr).grad_scale,
             "setup_s": round(setup_s, 1),
@@ -557,17 +604,25 @@ def b200_arm(args, ws, rank, local):
     if rank == 0 and ws == 1 and not args.no_small and args.workload == "gcn-reddit":
         result["small_configs"] = small_configs(args, peak)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        offsets = dg.offsets.cpu().numpy()
-        cols = dg.cols.cpu().numpy()
-        ms, sample, cores = cpu_baseline_gcn(offsets, cols, x.cpu().numpy(),
-                                             labels.cpu().numpy(), args.cpu_budget_edges,
-                                             **WORKLOADS[args.workload]["cfg"])
-        result["cpu_baseline"] = {"value": round(ms, 1), "unit": "ms/epoch", "cores": cores,
-                                  "kind": "port", "sample": sample}
+        result["cpu_baseline"] = cpu_baseline(args.workload, args.seed, args.cpu_budget_edges)
     if rank == 0:
         print(json.dumps(result), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def spawn_ranks(n):
+    """`bench.py --gpus N` without torchrun: relaunch this command under
+    torch.distributed.run with N ranks on this node (rank 0 prints the line)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -582,10 +637,17 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-small", action="store_true", help="skip the C1/C2 epoch timings")
     ap.add_argument("--no-graph", action="store_true", help="time eager steps, no CUDA graph")
-    ap.add_argument("--cpu-budget-edges", type=int, default=400_000)
-    ap.add_argument("--ref-budget-edges", type=int, default=400_000)
+    ap.add_argument("--cpu-budget-edges", type=int, default=500_000,
+                    help="edges in the B200 arm's cpu_baseline sample")
+    ap.add_argument("--ref-budget-edges", type=int, default=0,
+                    help="edges per --impl reference step (0: max(100K, 2M / steps))")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
     ws, rank, local = dist_env()
+    if ws != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; launch with "
+                         f"torchrun --nproc-per-node {args.gpus} or without torchrun")
     if args.impl == "reference":
         reference_arm(args, ws, rank)
         return

@@ -107,6 +107,20 @@ class Probe:
         return sum(r[3] for r in cls.records) / max(len(cls.records), 1)
 
     @classmethod
+    def l2_ideal_seconds(cls, peak_gbs_by_row_bytes):
+        """Seconds the timed spmm calls would take at the measured L2 random-gather
+        peak for their row width (tools/l2_gather_peak.py), counting the same
+        gather-model bytes; None if a width was not measured."""
+        total = 0.0
+        for r in cls.records:
+            rb, _ = r[5]
+            fits = [w for w in peak_gbs_by_row_bytes if w >= rb]
+            if not fits:
+                return None
+            total += r[2] / (peak_gbs_by_row_bytes[min(fits)] * 1e9)
+        return total
+
+    @classmethod
     def gather_ceiling(cls, reps=3):
         """Seconds the timed spmm calls' gathers alone take (hg_gather_probe on
         the same column ids, feature buffer and width, X warm in L2 as after
@@ -538,7 +552,8 @@ def spmm_csr(view: CsrView, x: torch.Tensor, w=None, w_index=None, heads: int = 
                               compulsory_bytes(view.n_rows, view.n_cols, view.num_edges, f,
                                                heads if w is not None else 0,
                                                x.element_size()),
-                              (view.cols, view.num_edges, x, f) if Probe.keep else None))
+                              (view.cols, view.num_edges, x, f) if Probe.keep else None,
+                              (-(-f * x.element_size() // 16) * 16, view.num_edges)))
     return out
 
 

@@ -18,10 +18,11 @@ import math
 import numpy as np
 import torch
 
+from . import synth as S
 from .device import DeviceGraph, build_csr
 
-REDDIT_N, REDDIT_E = 232_965, 114_848_857
-PRODUCTS_N, PRODUCTS_UNDIRECTED_E = 2_449_029, 61_859_140
+REDDIT_N, REDDIT_E = S.REDDIT_N, S.REDDIT_E
+PRODUCTS_N, PRODUCTS_UNDIRECTED_E = S.PRODUCTS_N, S.PRODUCTS_UNDIRECTED_E
 
 
 def synth_sbm(n, classes, p_in, p_out, feat_dim, seed, chunk=1 << 24):
@@ -84,101 +85,141 @@ def _gen(seed, device):
     return g
 
 
-def _exact_degree_graph(n, deg, gen, device, max_rounds=8):
-    """Rows with exactly deg[r] distinct uniform columns: draw, canonicalise on
-    the GPU, top up each row's shortfall, repeat."""
-    deg = deg.to(device)
-    rows = torch.repeat_interleave(torch.arange(n, device=device), deg)
-    cols = torch.randint(0, n, (rows.numel(),), generator=gen, device=device)
-    for _ in range(max_rounds):
-        offsets, c32, r64 = build_csr(n, rows, cols, want_rows=True)
-        have = offsets[1:] - offsets[:-1]
-        short = deg - have
-        if int(short.sum().item()) == 0:
-            return offsets, c32
-        extra_r = torch.repeat_interleave(torch.arange(n, device=device), short.clamp_min(0))
-        extra_c = torch.randint(0, n, (extra_r.numel(),), generator=gen, device=device)
-        rows = torch.cat([r64, extra_r])
-        cols = torch.cat([c32.to(torch.int64), extra_c])
-        del offsets, c32, r64
-    offsets, c32, _ = build_csr(n, rows, cols)
-    return offsets, c32
+# ── counter-based draws on the device, bit-identical to synth.h (numpy) ──
+
+def _s64(c):
+    return c - (1 << 64) if c >= 1 << 63 else c
+
+
+def _srl(z, k):
+    """Logical right shift of int64 tensors holding uint64 bit patterns."""
+    return (z >> k) & ((1 << (64 - k)) - 1)
+
+
+def _h(seed, stream, idx):
+    """synth.h(seed, stream, idx) on int64 tensors (wrapping arithmetic)."""
+    z = idx + _s64(S.key_base(seed, stream))
+    z = z ^ _srl(z, 30)
+    z = z * _s64(S.MIX1)
+    z = z ^ _srl(z, 27)
+    z = z * _s64(S.MIX2)
+    return z ^ _srl(z, 31)
+
+
+def _mulhi32(hv, n):
+    return (_srl(hv, 32) * n) >> 32
+
+
+def _unit53(hv):
+    return _srl(hv, 11).to(torch.float64) * (1.0 / (1 << 53))
 
 
 def reddit_like(seed=0, device="cuda", n=REDDIT_N, e=REDDIT_E):
-    """C3: lognormal row degrees (mean 493, clipped [1, 2e4]) rescaled
-    to sum to E exactly, uniform columns, exactly E unique edges."""
-    gen = _gen(seed, device)
-    mean = e / n
-    sigma = 1.0
-    mu = math.log(mean) - sigma * sigma / 2
-    raw = torch.empty(n, device=device, dtype=torch.float64).log_normal_(mu, sigma, generator=gen)
-    raw = raw.clamp(1.0, 2.0e4)
-    deg = torch.floor(raw * (e / raw.sum())).clamp(1, min(20000, n)).to(torch.int64)
-    rem = e - int(deg.sum().item())
-    # hand out the remainder one edge at a time to the rows with headroom
-    while rem != 0:
-        step = 1 if rem > 0 else -1
-        room = (deg < min(20000, n)) if step > 0 else (deg > 1)
-        idx = torch.nonzero(room).flatten()[: abs(rem)]
-        deg[idx] += step
-        rem -= step * idx.numel()
-    offsets, cols = _exact_degree_graph(n, deg, gen, device)
-    return DeviceGraph(n, offsets, cols)
+    """C3 (synth.reddit_rows): lognormal row degrees (host numpy,
+    mean 493, clipped [1, 2e4], rescaled to sum to E), each row's columns the
+    first deg distinct counter-based uniform draws; exactly E unique edges.
+    Bit-identical to synth.reddit_graph."""
+    deg = torch.from_numpy(S.reddit_degrees(seed, n, e)).to(device)
+    ar = torch.arange(n, device=device)
+    nxt = torch.zeros(n, dtype=torch.int64, device=device)
+    need = deg
+    rows = torch.zeros(0, dtype=torch.int64, device=device)
+    cols = torch.zeros(0, dtype=torch.int64, device=device)
+    while True:
+        cnt = need.clamp_min(0)
+        total = int(cnt.sum().item())
+        if total == 0:
+            break
+        rid = torch.repeat_interleave(ar, cnt)
+        start = torch.cumsum(cnt, 0) - cnt
+        k = torch.arange(total, device=device) - start[rid] + nxt[rid]
+        nxt = nxt + cnt
+        c = _mulhi32(_h(seed, S.S_REDDIT, (rid << 32) | k), n)
+        offsets, c32, r64 = build_csr(n, torch.cat([rows, rid]), torch.cat([cols, c]),
+                                      want_rows=True)
+        rows, cols = r64, c32.to(torch.int64)
+        del rid, k, c
+        need = deg - (offsets[1:] - offsets[:-1])
+    return DeviceGraph(n, offsets, c32)
 
 
 def products_like(seed=0, device="cuda", n=PRODUCTS_N, undirected=PRODUCTS_UNDIRECTED_E,
                   exponent=2.1, max_degree=17_000):
-    """C4: Chung-Lu power-law graph with exactly `undirected` distinct undirected
-    edges (no self loops), symmetrised.  Expected degrees follow
-    rank^(-1/(exponent-1)) scaled to the target mean and clipped to
-    [1, max_degree] (ogbn-products' maximum degree is ~17K); endpoints are
-    drawn proportionally, duplicates are topped up until the count is exact."""
-    gen = _gen(seed, device)
-    ranks = torch.arange(1, n + 1, device=device, dtype=torch.float64)
-    w = ranks.pow(-1.0 / (exponent - 1.0))
-    mean = 2.0 * undirected / n
-    for _ in range(20):  # rescale so the clipped weights keep the target mean
-        w = (w * (mean * n / w.clamp(1.0, max_degree).sum())).clamp(min=1e-9)
-    w = w.clamp(1.0, max_degree)
-    prob = (w / w.sum()).float()
-    perm = torch.randperm(n, generator=gen, device=device)
-    keys = torch.empty(0, dtype=torch.int64, device=device)
-    need = undirected
-    for _ in range(16):
-        m = int(need * 1.15) + 1024
-        a = perm[torch.multinomial(prob, m, replacement=True, generator=gen)]
-        b = perm[torch.multinomial(prob, m, replacement=True, generator=gen)]
-        keep = a != b
-        lo, hi = torch.minimum(a, b)[keep], torch.maximum(a, b)[keep]
-        keys = torch.unique(torch.cat([keys, lo * n + hi]))
-        need = undirected - keys.numel()
-        if need <= 0:
-            break
-    if keys.numel() > undirected:  # drop a random surplus
-        pick = torch.randperm(keys.numel(), generator=gen, device=device)[:undirected]
-        keys = keys[pick]
+    """C4 (synth.products_graph): Chung-Lu power-law graph with exactly
+    `undirected` distinct undirected edges (no self loops), symmetrised.
+    Expected degrees follow rank^(-1/(exponent-1)) scaled to the target mean and
+    clipped to [1, max_degree] (ogbn-products' maximum degree is ~17K);
+    endpoints by inverse CDF of counter-based uniforms, vertex ids permuted;
+    the first `undirected` distinct pairs in draw order are kept.
+    Bit-identical to synth.products_graph."""
+    cdf_h, total = S.products_cdf(n, undirected, exponent, max_degree)
+    cdf = torch.from_numpy(cdf_h).to(device)
+    perm = torch.from_numpy(S.products_perm(seed, n)).to(device)
+    keys = torch.zeros(0, dtype=torch.int64, device=device)
+    first = torch.zeros(0, dtype=torch.int64, device=device)
+    t0 = 0
+    while keys.numel() < undirected:
+        m = S.products_batch(undirected - keys.numel())
+        t = torch.arange(t0, t0 + m, device=device)
+        ia = torch.searchsorted(cdf, _unit53(_h(seed, S.S_PROD_A, t)) * total, right=True)
+        ib = torch.searchsorted(cdf, _unit53(_h(seed, S.S_PROD_B, t)) * total, right=True)
+        a, b = perm[ia.clamp_max(n - 1)], perm[ib.clamp_max(n - 1)]
+        del ia, ib
+        ok = a != b
+        k = torch.minimum(a, b)[ok] * n + torch.maximum(a, b)[ok]
+        tt = t[ok]
+        del a, b, ok, t
+        allk, allt = torch.cat([keys, k]), torch.cat([first, tt])
+        del k, tt
+        sk, order = torch.sort(allk, stable=True)
+        st = allt[order]
+        del allk, allt, order
+        head = torch.ones_like(sk, dtype=torch.bool)
+        head[1:] = sk[1:] != sk[:-1]
+        keys, first = sk[head], st[head]
+        del sk, st, head
+        t0 += m
+    if keys.numel() > undirected:
+        keep = torch.argsort(first)[:undirected].sort().values
+        keys = keys[keep]
     src, dst = keys // n, keys % n
+    del keys, first
     offsets, c32, _ = build_csr(n, torch.cat([src, dst]), torch.cat([dst, src]))
     return DeviceGraph(n, offsets, c32)
 
 
-def rmat(scale=24, edge_factor=16, seed=0, device="cuda", abc=(0.57, 0.19, 0.19)):
-    """C5: Graph500 RMAT, deduplicated (self loops kept as generated)."""
-    gen = _gen(seed, device)
+def rmat(scale=24, edge_factor=16, seed=0, device="cuda", abc=S.RMAT_ABC, scrambled=True):
+    """C5: Graph500 RMAT, deduplicated (self loops kept as generated), vertex
+    ids scrambled by a seeded bijection as Graph500 does (hubs spread over the
+    id range, so row partitions balance).  Bit-identical to synth.rmat_graph."""
     n = 1 << scale
     m = edge_factor * n
-    a, b, c = abc
+    ta, tab, tabc = S.rmat_thresholds(abc)
+    t = torch.arange(m, device=device)
     rows = torch.zeros(m, dtype=torch.int64, device=device)
     cols = torch.zeros(m, dtype=torch.int64, device=device)
     for bit in range(scale):
-        u = torch.rand(m, generator=gen, device=device)
-        right = ((u >= a) & (u < a + b)) | (u >= a + b + c)
-        down = u >= a + b
-        rows |= down.to(torch.int64) << bit
-        cols |= right.to(torch.int64) << bit
+        u = _srl(_h(seed, S.S_RMAT + bit, t), 40)
+        rows |= (u >= tab).to(torch.int64) << bit
+        cols |= (((u >= ta) & (u < tab)) | (u >= tabc)).to(torch.int64) << bit
+        del u
+    del t
+    if scrambled:
+        rows, cols = _scramble(rows, seed, scale), _scramble(cols, seed, scale)
     offsets, c32, _ = build_csr(n, rows, cols)
     return DeviceGraph(n, offsets, c32)
+
+
+def _scramble(v, seed, scale):
+    """synth.scramble on the device."""
+    mask = (1 << scale) - 1
+    k1, k2, k3 = S.scramble_consts(seed, scale)
+    s1, s2 = max(1, scale // 2), max(1, scale // 2 + 1)
+    x = (v * k1) & mask
+    x = x ^ (x >> s1)
+    x = (x * k2) & mask
+    x = x ^ (x >> s2)
+    return x ^ k3
 
 
 def planted_features(n, feat, classes, seed=0, device="cuda", dtype=torch.float16):

@@ -502,21 +502,13 @@ class _ScaleCombineFn(torch.autograd.Function):
     def forward(ctx, x, a, ope, lam):
         ctx.lam = lam
         ctx.save_for_backward(x, ope)
-        if x.is_cuda:
-            return D.scale_combine(x, a, ope, lam)
-        return x * ope + D.scale_f64(a, lam)
+        return D.scale_combine(x, a, ope, lam)
 
     @staticmethod
     def backward(ctx, g):
         x, ope = ctx.saved_tensors
         g = g.contiguous()
-        if g.is_cuda:
-            gx, ga, gope = D.scale_combine_bwd(x, g, ope, ctx.lam, *ctx.needs_input_grad[:3])
-            return gx, ga, gope, None
-        gx = g * ope if ctx.needs_input_grad[0] else None
-        ga = D.scale_f64(g, ctx.lam) if ctx.needs_input_grad[1] else None
-        gope = (x.double() * g.double()).sum().to(ope.dtype).reshape(ope.shape) \
-            if ctx.needs_input_grad[2] else None
+        gx, ga, gope = D.scale_combine_bwd(x, g, ope, ctx.lam, *ctx.needs_input_grad[:3])
         return gx, ga, gope, None
 
 

@@ -5,12 +5,15 @@ with s_p = searchsorted(offsets, (p*E)//P, 'left') (nnz-balanced, bit-exact
 with oracle.partition_splits): its CSR rows (global column ids), the CSC rows
 of the same vertices (for the backward pass), its feature rows and labels.
 
-Exchange: before each aggregation the rank's feature rows are all-gathered
-(NCCL over NVLink) into a [P * n_max, F] buffer -- rank q's rows at
-q*n_max.. -- and the local column ids are pre-remapped into that padded
-layout once, so the SpMM reads the gathered buffer in place (no compaction).
-Backward all-gathers the output gradient the same way and aggregates over the
-local CSC rows.  GAT additionally sends per-edge values (alpha, d_e) to the
+Exchange: before each aggregation the ranks' feature rows are all-gathered
+with exact per-rank counts (NCCL over NVLink: one group of P broadcasts, the
+all-gather-v idiom) into an [N, F] buffer in global row order, so the local
+CSR keeps its global column ids and the SpMM reads the gathered buffer in
+place; each rank receives exactly (N - n_local) * F * 2 bytes per gather, no
+padding to the largest partition.  Backward all-gathers the output gradient
+the same way and aggregates over the local CSC rows.  A static input (GIN's
+first aggregation reads the raw features) is gathered once when it is loaded
+(`DistTrainer.refresh_inputs`), not every epoch.  GAT additionally sends per-edge values (alpha, d_e) to the
 owner of each edge's column with one all-to-all (each edge travels once,
 E/P per rank instead of the E an all-gather would deliver).
 Weight gradients and the loss are all-reduced (the data-parallel sum).
@@ -43,6 +46,12 @@ def split_points(offsets, parts: int) -> np.ndarray:
 
 
 def remap_to_padded(ids: torch.Tensor, splits: np.ndarray, stride: int) -> torch.Tensor:
+    """(The round-1 padded all-gather layout; kept for the exchange-layout
+    tests.)"""
+    return _remap_to_padded(ids, splits, stride)
+
+
+def _remap_to_padded(ids: torch.Tensor, splits: np.ndarray, stride: int) -> torch.Tensor:
     """Global id -> q*stride + (id - splits[q]) where q owns id."""
     bounds = torch.as_tensor(splits[1:-1], dtype=torch.int64, device=ids.device)
     ids64 = ids.to(torch.int64)
@@ -57,10 +66,10 @@ class LocalPart:
     parts: int
     splits: np.ndarray        # vertex split points [P+1]
     edge_splits: np.ndarray   # CSR edge offsets of the split points [P+1]
-    n_max: int                # padded rows per rank in gathered feature buffers
+    n_max: int                # rows of the largest partition (balance diagnostic)
     e_max: int                # largest per-rank edge count
-    fwd: CsrView              # local CSR rows, columns in the padded feature layout
-    bwd: CsrView              # local CSC rows, columns padded, perm -> received edge buffer
+    fwd: CsrView              # local CSR rows, global column ids
+    bwd: CsrView              # local CSC rows, global column ids, perm -> received edge buffer
     send_index: torch.Tensor  # local CSR edges grouped by the rank owning their column
     send_counts: list         # edges sent to each rank
     recv_counts: list         # edges received from each rank (this rank's CSC edges)
@@ -79,17 +88,19 @@ class LocalPart:
 
 
 def make_local_part(offsets, cols, t_offsets, t_cols, perm, rank, parts) -> LocalPart:
-    """Slice rank `rank`'s CSR/CSC rows out of the global arrays and remap ids."""
+    """Slice rank `rank`'s CSR/CSC rows out of the global arrays (column ids
+    stay global: the gathered buffers are in global row order)."""
     splits = split_points(offsets, parts)
     eoff = offsets[torch.as_tensor(splits, device=offsets.device)].cpu().numpy()
     n_max = int(np.diff(splits).max())
     e_max = int(np.diff(eoff).max()) if parts > 0 else 0
     lo, hi = int(splits[rank]), int(splits[rank + 1])
     f_off = (offsets[lo:hi + 1] - offsets[lo]).contiguous()
-    f_cols = remap_to_padded(cols[int(offsets[lo]):int(offsets[hi])], splits, n_max)
+    n = int(splits[-1])
+    f_cols = cols[int(offsets[lo]):int(offsets[hi])].contiguous()
     t_lo, t_hi = int(t_offsets[lo]), int(t_offsets[hi])
     b_off = (t_offsets[lo:hi + 1] - t_offsets[lo]).contiguous()
-    b_cols = remap_to_padded(t_cols[t_lo:t_hi], splits, n_max)
+    b_cols = t_cols[t_lo:t_hi].contiguous()
     # Edge values for the column owner travel by all-to-all (SURVEY 8(e)
     # option A): rank q sends rank p the values of its edges whose column p
     # owns, in ascending global edge id; concatenated over q that is p's CSC
@@ -108,38 +119,50 @@ def make_local_part(offsets, cols, t_offsets, t_cols, perm, rank, parts) -> Loca
                                my_cols, right=True)
     send_index = torch.argsort(owner, stable=True)
     send_counts = torch.bincount(owner, minlength=parts).cpu().tolist()
-    fwd = CsrView(f_off, f_cols, hi - lo, parts * n_max)
-    bwd = CsrView(b_off, b_cols, hi - lo, parts * n_max, perm=recv_pos.to(torch.int32))
+    fwd = CsrView(f_off, f_cols, hi - lo, n)
+    bwd = CsrView(b_off, b_cols, hi - lo, n, perm=recv_pos.to(torch.int32))
     return LocalPart(rank, parts, splits, eoff, n_max, e_max, fwd, bwd, send_index,
                      send_counts, recv_counts)
 
 
 class Exchange:
-    """Padded all-gathers over a torch.distributed process group.  NCCL moves
-    device tensors over NVLink; a gloo group (CPU tests, or several ranks
-    sharing one GPU for validation) stages device tensors through the host."""
+    """Exact-count all-gathers over a torch.distributed process group.  NCCL
+    moves device tensors over NVLink (all_gather into per-rank views of
+    different sizes = one NCCL group of broadcasts); a gloo group (CPU tests,
+    or several ranks sharing one GPU for validation) stages through the host,
+    padding to the largest partition there only.  `recv_bytes` counts the
+    bytes this rank received (feature rows and edge values)."""
 
     def __init__(self, dist, part: LocalPart):
         self.dist = dist
         self.part = part
         self.staged = dist.get_backend() == "gloo"
+        self.recv_bytes = 0
+        self.gathers = 0
 
-    def _all_gather(self, out, send):
-        if self.staged and out.is_cuda:
-            host = out.cpu()
-            self.dist.all_gather_into_tensor(host, send.cpu())
-            out.copy_(host)
-        else:
-            self.dist.all_gather_into_tensor(out, send)
+    def _views(self, out):
+        s = self.part.splits
+        return [out[int(s[q]):int(s[q + 1])] for q in range(self.part.parts)]
 
     def gather_rows(self, x_local: torch.Tensor) -> torch.Tensor:
+        """[n_local, ...] -> [N, ...] in global row order."""
         p = self.part
-        send = x_local
-        if x_local.shape[0] != p.n_max:
-            send = x_local.new_zeros((p.n_max,) + tuple(x_local.shape[1:]))
-            send[: x_local.shape[0]] = x_local
-        out = x_local.new_empty((p.parts * p.n_max,) + tuple(x_local.shape[1:]))
-        self._all_gather(out, send.contiguous())
+        x_local = x_local.contiguous()
+        tail = tuple(x_local.shape[1:])
+        n = int(p.splits[-1])
+        out = x_local.new_empty((n,) + tail)
+        row = x_local[0].numel() * x_local.element_size() if x_local.shape[0] else 0
+        self.recv_bytes += (n - p.n_local) * row
+        self.gathers += 1
+        if self.staged:
+            send = x_local.new_zeros((p.n_max,) + tail, device="cpu")
+            send[: p.n_local] = x_local.cpu()
+            host = send.new_empty((p.parts * p.n_max,) + tail)
+            self.dist.all_gather_into_tensor(host, send)
+            for q, v in enumerate(self._views(out)):
+                v.copy_(host[q * p.n_max: q * p.n_max + v.shape[0]])
+        else:
+            self.dist.all_gather(self._views(out), x_local)
         return out
 
     def gather_edges(self, v_local: torch.Tensor) -> torch.Tensor:
@@ -149,6 +172,8 @@ class Exchange:
         p = self.part
         send = v_local.index_select(0, p.send_index).contiguous()
         out = v_local.new_empty((sum(p.recv_counts),) + tuple(v_local.shape[1:]))
+        row = v_local[0].numel() * v_local.element_size() if v_local.shape[0] else 0
+        self.recv_bytes += (sum(p.recv_counts) - p.recv_counts[p.rank]) * row
         if self.staged and out.is_cuda:
             host = out.cpu()
             self.dist.all_to_all_single(host, send.cpu(), p.recv_counts, p.send_counts)
@@ -239,6 +264,18 @@ class DistBundle:
         self.ops = ops
         self._tables = tables  # callable (kind, side, dtype) -> global table [N]
         self._cache = {}
+        self._static = None    # (local input tensor, its gathered [N, F] copy)
+
+    def set_static(self, x_local, x_full):
+        """Register a gathered copy of a static input (GIN's raw features):
+        aggregations of x_local read x_full instead of gathering again."""
+        self._static = (x_local, x_full)
+
+    def _gathered(self, x):
+        st = self._static
+        if st is not None and x.data_ptr() == st[0].data_ptr() and x.shape == st[0].shape:
+            return st[1]
+        return self.ex.gather_rows(x.contiguous())
 
     @property
     def n(self):
@@ -248,22 +285,13 @@ class DistBundle:
     def num_edges(self):
         return self.part.fwd.num_edges
 
-    def _padded(self, table):
-        p = self.part
-        out = table.new_zeros(p.parts * p.n_max)
-        for q in range(p.parts):
-            a, b = int(p.splits[q]), int(p.splits[q + 1])
-            out[q * p.n_max: q * p.n_max + (b - a)] = table[a:b]
-        return out
-
     def norm_tables(self, norm, transpose, dtype):
         key = (norm, transpose, dtype)
         t = self._cache.get(key)
         if t is None:
             kind = "inv_sqrt" if norm == "both" else "inv"
             row_side, col_side = ("col", "row") if transpose else ("row", "col")
-            fin = self._padded(self._tables(kind, col_side, dtype)) \
-                if norm in ("left", "both") else None
+            fin = self._tables(kind, col_side, dtype) if norm in ("left", "both") else None
             fout = self._tables(kind, row_side, dtype)[self.part.lo:self.part.hi].contiguous() \
                 if norm in ("right", "both") else None
             t = (fin, fout)
@@ -307,7 +335,8 @@ class DistBundle:
 
     def gat_attention_bwd(self, s_l, s_r, alpha, g, slope):
         """(ds_l, ds_r): row sums locally; the column owner sums d_e over its CSC
-        rows after the padded all-gather of every rank's edge values."""
+        rows after the all-to-all that sends each edge value to its column's
+        owner."""
         de, ds_l = D.gat_attention_bwd(self.part.fwd, s_l.contiguous(),
                                        self.ex.gather_rows(s_r.contiguous()), alpha, g, slope)
         bwd = self.part.bwd
@@ -342,7 +371,7 @@ class DistBundle:
                 widx = view.perm
             return self._gather_scaled(row_scale(x.contiguous(), fin_local), scaling, norm,
                                        transpose, heads, w, widx)
-        x_full = self.ex.gather_rows(x.contiguous())
+        x_full = self._gathered(x)
         fin, fout = self.norm_tables(norm, transpose, x.dtype)
         widx = None
         if w is not None and weight_via_perm:
@@ -400,14 +429,24 @@ class DistTrainer:
         self.n_total = dg.n
         self._graph = None
         self._graph_out = None
+        self.refresh_inputs()
 
     @property
     def x(self):
         return self.inner.x
 
+    def refresh_inputs(self):
+        """Gather the static input once (after features are loaded or replaced):
+        GIN's first aggregation reads the raw features, which do not change
+        between epochs; other models need nothing."""
+        if self.inner.cfg.kind == "gin":
+            self.bundle.set_static(self.inner.x, self.bundle.ex.gather_rows(self.inner.x))
+
     def load_features(self, feats, out=None):
         lo, hi = self.part.lo, self.part.hi
-        return self.inner.load_features(feats[lo:hi], out=self.inner.x)
+        out = self.inner.load_features(feats[lo:hi], out=self.inner.x)
+        self.refresh_inputs()
+        return out
 
     def step(self, overflow=None):
         if self._graph is not None and overflow is None:

@@ -180,12 +180,19 @@ def _run(rank, world, port, out_q, kind="gcn"):
         tr = DistTrainer(g, torch.from_numpy(x), labels, cfg, dist, ops=HostOps)
         losses = []
         first = None
+        if kind == "gin":   # the static raw input was gathered once at load time
+            g0 = tr.bundle.ex.gathers
+            assert tr.bundle._gathered(tr.inner.x) is tr.bundle._static[1]
+            assert tr.bundle.ex.gathers == g0
+        ex = tr.bundle.ex
+        b0 = ex.recv_bytes
         for _ in range(3):
             loss, logits = tr.step()
             losses.append(float(loss))
             first = logits.numpy() if first is None else first
         parts = [None] * world
-        dist.all_gather_object(parts, (tr.part.lo, tr.part.hi, first, logits.numpy()))
+        dist.all_gather_object(parts, (tr.part.lo, tr.part.hi, first, logits.numpy(),
+                                       ex.recv_bytes - b0))
         if rank == 0:
             out_q.put((losses, parts, [p.master.numpy() for p in tr.inner.opt.params]))
     finally:
@@ -207,15 +214,17 @@ def _run_world(world, kind="gcn"):
 
 
 @pytest.mark.timeout(400)
-@pytest.mark.parametrize("kind", ["gcn", "gat"])
-def test_two_rank_step_matches_single_rank(kind):
+@pytest.mark.parametrize("kind,world", [("gcn", 2), ("gat", 2), ("gcn", 3)])
+def test_multi_rank_step_matches_single_rank(kind, world):
     l1, parts1, w1 = _run_world(1, kind)
-    l2, parts2, w2 = _run_world(2, kind)
+    l2, parts2, w2 = _run_world(world, kind)
+    assert parts1[0][4] == 0            # one rank receives nothing
+    assert all(p[4] > 0 for p in parts2)
     n = _graph()[0]
     # nnz-balanced split points (bit-exact rule)
     offsets = O.csr_offsets(n, _graph()[1])
-    s = O.partition_splits(offsets, 2)
-    assert [(p[0], p[1]) for p in parts2] == [(int(s[0]), int(s[1])), (int(s[1]), int(s[2]))]
+    s = O.partition_splits(offsets, world)
+    assert [(p[0], p[1]) for p in parts2] == [(int(s[q]), int(s[q + 1])) for q in range(world)]
     # step 1 (same weights): row-owned aggregation + global tables give
     # identical logits, rank by rank
     np.testing.assert_array_equal(parts1[0][2], np.concatenate([p[2] for p in parts2], axis=0))
@@ -226,3 +235,29 @@ def test_two_rank_step_matches_single_rank(kind):
     np.testing.assert_allclose(l1, l2, rtol=1e-6, atol=1e-7)
     for a, b in zip(w1, w2):
         np.testing.assert_allclose(a, b, rtol=1e-5, atol=1e-6)
+
+
+def test_static_input_gathered_once():
+    """GIN's raw features are static: DistBundle reads the copy gathered at load
+    time instead of gathering again every epoch."""
+    from paper_2411_01109_b200.partition import DistBundle
+
+    class _Ex:
+        gathers = 0
+
+        def gather_rows(self, x):
+            self.gathers += 1
+            return torch.cat([x, x])
+
+    class _Part:
+        rank, parts = 0, 1
+
+    ex = _Ex()
+    b = DistBundle(_Part(), ex, None)
+    x = torch.ones(3, 4)
+    full = ex.gather_rows(x)
+    b.set_static(x, full)
+    assert b._gathered(x) is full and ex.gathers == 1
+    y = torch.ones(3, 4)
+    assert b._gathered(y).shape == (6, 4) and ex.gathers == 2
+    assert b._gathered(x[:2]) is not full           # a different view is not the input

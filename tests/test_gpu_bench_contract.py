@@ -38,3 +38,25 @@ def test_bench_json_line_contract(cuda):
         assert key in r, key
     assert r["bound"] in ("hbm", "tensor") and r["peak"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+
+
+@pytest.mark.timeout(900)
+def test_bench_spawns_ranks_for_gpus_flag(cuda):
+    """`bench.py --gpus 2` without torchrun launches two ranks itself and reports
+    n_gpus 2 (validated with both ranks on this one GPU over gloo)."""
+    import os
+
+    env = dict(os.environ, HG_DIST_SHARED_GPU="1", HG_DIST_BACKEND="gloo")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run(
+        [sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--workload", "gat-pubmed",
+         "--steps", "3", "--warmup", "3", "--no-cpu-baseline"],
+        capture_output=True, text=True, cwd=ROOT, timeout=850, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2
+    ex = d["exchange"]
+    assert ex["recv_bytes_per_rank_per_step_max"] > 0
+    assert ex["n_rows_max_over_mean"] <= 1.5
