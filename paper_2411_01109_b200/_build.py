@@ -91,5 +91,29 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     return LIB
 
 
+def build_variant(name: str, defines, srcs=("spmm.cu",)) -> Path:
+    """A/B build: the library with `srcs` recompiled under extra -D defines,
+    linked with the regular objects, at tools/exp/variants/<name>/libhalfgnn.so
+    (load it with HG_LIB=<path>).  Measurement only."""
+    build()
+    out_dir = ROOT / "tools" / "exp" / "variants" / name
+    out_dir.mkdir(parents=True, exist_ok=True)
+    nvcc = _nvcc()
+    objs = []
+    for src in sources():
+        if src.name in srcs:
+            obj = out_dir / (src.stem + ".o")
+            cmd = [nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", str(src), "-o", str(obj)]
+            res = subprocess.run(cmd, capture_output=True, text=True)
+            if res.returncode != 0:
+                raise RuntimeError(res.stderr)
+            objs.append(obj)
+        else:
+            objs.append(BUILD / (src.stem + ".o"))
+    lib = out_dir / "libhalfgnn.so"
+    subprocess.run([nvcc, *ARCH, "-shared", "-o", str(lib), *map(str, objs)], check=True)
+    return lib
+
+
 if __name__ == "__main__":
     print(build(verbose=True, force="--force" in sys.argv))

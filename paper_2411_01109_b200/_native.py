@@ -8,11 +8,14 @@ HG_ECUDA -> RuntimeError.
 from __future__ import annotations
 
 import ctypes
+import os
 from ctypes import (POINTER, c_char_p, c_double, c_float, c_int, c_int32, c_int64, c_size_t,
                     c_void_p)
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().with_name("libhalfgnn.so")
+# HG_LIB: an alternative build of the same library (A/B measurements of
+# compile-time kernel variants, tools/exp/variants); default the in-tree build
+LIB_PATH = Path(os.environ.get("HG_LIB") or Path(__file__).resolve().with_name("libhalfgnn.so"))
 
 HG_OK, HG_EINVAL, HG_ECUDA = 0, 1, 2
 ABI_VERSION = 3

@@ -167,10 +167,18 @@ __device__ __forceinline__ void acc_fma(float (&acc)[V], T w,
 // Minimum resident blocks per SM: caps registers so that 256-thread blocks of
 // single-chunk teams run 3-4 deep (24-32 warps/SM) for memory-level
 // parallelism, without spilling (ptxas -v: 64 regs unweighted TEAM >= 8).
+#ifndef HG_SPMM_EB32
+#define HG_SPMM_EB32 4   // edges per batch of 32-byte-lane unit teams
+#endif
+#ifndef HG_SPMM_OCC32
+#define HG_SPMM_OCC32 3  // 32-byte-lane unweighted teams (A/B builds: tools/exp/variants)
+#endif
 template <int TEAM, int NCH, bool WT, int VB = 16>
 struct FastOcc {
   static constexpr int value =
-      NCH == 1 ? ((!WT && VB == 16 && TEAM >= 8 && TEAM <= 16) ? 4 : 3) : (NCH == 2 ? 2 : 1);
+      NCH == 1 ? ((!WT && VB == 16 && TEAM >= 8 && TEAM <= 16) ? 4
+                  : (!WT && VB == 32) ? HG_SPMM_OCC32 : 3)
+               : (NCH == 2 ? 2 : 1);
 };
 
 // Column ids of one batch for a non-power-of-two team: lane tl holds the ids
@@ -228,7 +236,7 @@ struct FastTeam {
   static constexpr bool P2 = TeamShape<TEAM>::P2;
   // edges gathered per batch (packed teams: 4, the rolled accumulate shifts
   // the batch registers once per edge)
-  static constexpr int EB = (NCH >= 4 || PK || V * sizeof(T) == 32) ? 4 : 8;
+  static constexpr int EB = V * sizeof(T) == 32 ? (PK ? 4 : HG_SPMM_EB32) : (NCH >= 4 || PK) ? 4 : 8;
   static constexpr int CPL = P2 ? (TEAM >= EB ? 1 : EB / TEAM) : (EB + TEAM - 1) / TEAM;
   using Raw = typename RawVec<V * sizeof(T)>::type;
 
@@ -791,6 +799,14 @@ extern "C" int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_ro
              (long long)w_ld, heads);
   HG_REQUIRE(!out2 || (w && w2_off >= heads && w2_off + heads <= w_ld),
              "hg_spmm: summed second weight block needs w and heads <= w2_off <= w_ld - heads");
+  // id batches are aligned to the address of cols and loaded as vectors from
+  // cols, w_index and pack_rowid alike: the three must share their 16-byte phase
+  HG_REQUIRE(reinterpret_cast<uintptr_t>(cols) % 4 == 0 &&
+                 (!w_index || ((reinterpret_cast<uintptr_t>(cols) ^
+                                reinterpret_cast<uintptr_t>(w_index)) & 15) == 0) &&
+                 (!pack_rowid || ((reinterpret_cast<uintptr_t>(cols) ^
+                                   reinterpret_cast<uintptr_t>(pack_rowid)) & 15) == 0),
+             "hg_spmm: cols, w_index and pack_rowid must have the same address modulo 16");
   cudaStream_t st = as_stream(stream);
   if (n_rows == 0) return HG_OK;
   Carver cv(ws, ws_bytes);

@@ -97,10 +97,12 @@ def make_local_part(offsets, cols, t_offsets, t_cols, perm, rank, parts) -> Loca
     lo, hi = int(splits[rank]), int(splits[rank + 1])
     f_off = (offsets[lo:hi + 1] - offsets[lo]).contiguous()
     n = int(splits[-1])
-    f_cols = cols[int(offsets[lo]):int(offsets[hi])].contiguous()
+    # fresh allocations (not views at an edge offset): the kernels vector-load
+    # column ids from 16-byte-aligned bases
+    f_cols = cols[int(offsets[lo]):int(offsets[hi])].clone()
     t_lo, t_hi = int(t_offsets[lo]), int(t_offsets[hi])
     b_off = (t_offsets[lo:hi + 1] - t_offsets[lo]).contiguous()
-    b_cols = t_cols[t_lo:t_hi].contiguous()
+    b_cols = t_cols[t_lo:t_hi].clone()
     # Edge values for the column owner travel by all-to-all (SURVEY 8(e)
     # option A): rank q sends rank p the values of its edges whose column p
     # owns, in ascending global edge id; concatenated over q that is p's CSC
