@@ -344,6 +344,29 @@ def test_c1_gcn_accuracy_parity(cuda):
         assert all(row[5] == 0 for row in res.trace)
 
 
+@pytest.mark.timeout(900)
+def test_c2_gat_accuracy_parity(cuda):
+    """C2 (Pubmed-shaped synth_sbm, 3-layer x 4-head x 16 GAT, classes 3 -> 4)
+    200 epochs: final train / val accuracy within 0.5 pt of the reference
+    harness's 200-epoch run (tests/golden/c2_half.npz, make_golden.py c2 half:
+    reference GATLayers composed with concat / mean, models.py:492-509,
+    633-684), in both numerics; the loss trace follows the reference's."""
+    from paper_2411_01109_b200 import graphgen, models as M, sparse as sp
+
+    d = load_golden("c2_half.npz")
+    rows, cols, feats, labels = graphgen.pubmed_like(0)
+    assert rows.size == int(d["num_edges"])
+    g = sp.CooGraph(19717, rows, cols)
+    want_train, want_val = d["acc"][-1]
+    for numerics, atol in (("reference", 5e-3), ("fast", 1e-2)):
+        res = M.train(g, feats, labels, M.TrainConfig(kind="gat", hidden=16, heads=4, layers=3,
+                                                      epochs=200, seed=0, numerics=numerics))
+        assert abs(res.train_acc - want_train) <= 0.005, (numerics, res.train_acc, want_train)
+        assert abs(res.val_acc - want_val) <= 0.005, (numerics, res.val_acc, want_val)
+        np.testing.assert_allclose(res.losses, d["loss"], atol=atol, rtol=0)
+        assert all(row[5] == 0 for row in res.trace)
+
+
 def test_conversions_and_nan_abort(cuda):
     from paper_2411_01109_b200 import graphgen, models as M, sparse as sp
 

@@ -152,6 +152,20 @@ def test_oracle_c1_gcn_first_epochs():
     np.testing.assert_allclose(res["losses"], d["c1_gcn_half_loss"][:10], atol=1e-4)
 
 
+def test_oracle_c2_gat_first_epochs():
+    """C2 (Pubmed-shaped, 3-layer x 4-head GAT): the oracle's first 2 epochs
+    against the reference's 200-epoch golden trace (make_golden.py c2 half)."""
+    from paper_2411_01109_b200.graphgen import pubmed_like
+
+    d = load_golden("c2_half.npz")
+    rows, cols, feats, labels = pubmed_like(0)
+    assert rows.size == int(d["num_edges"])
+    g = O.OracleGraph(19717, rows, cols)
+    res = O.train_epochs(g, feats, labels, kind="gat", mode="half", epochs=2, seed=0,
+                         hidden=16, heads=4, layers=3)
+    np.testing.assert_allclose(res["losses"], d["loss"][:2], atol=1e-4)
+
+
 def test_partition_splits_rule():
     rng = np.random.default_rng(4)
     for _ in range(20):
