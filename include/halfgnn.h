@@ -281,11 +281,27 @@ int hg_adam_step(float* master, float* m, float* v, const void* grad, int grad_d
  * binary16 operands, fp32 accumulation in TMEM (tcgen05.mma kind::f16, M=128
  * tiles, TMA-fed 4-stage ring), one rounding per step; bias / row_scale may be
  * NULL.  a: [m, k] pitch lda; bt: [n, k] pitch ldb (B transposed, K-major);
- * out: [m, n] pitch ldo.  n: multiple of 16 in [16, 256]; pitches multiples
- * of 8 elements; 16-byte aligned pointers. */
+ * out: [m, n] pitch ldo.  n: multiple of 8 in [8, 256] (8 mod 16 runs as the
+ * next multiple of 16, the padding neither read from bt nor stored); pitches
+ * multiples of 8 elements; 16-byte aligned pointers.  Also the backward's
+ * dx = g W^T (matmul backward, models.py:151-153): a = g, bt = W. */
 int hg_gemm_tc(const void* a, int64_t m, int64_t k, int64_t lda, const void* bt, int32_t n,
                int64_t ldb, const void* bias, const void* row_scale, int32_t relu, void* out,
                int64_t ldo, void* stream);
+
+/* matmul backward's weight gradient (models.py:154-155, b._accumulate(mm(a.T,
+ * g))): out[m, n] = rnd(sum_k a[k, m] b[k, n]) -- fp32 accumulation, one
+ * rounding -- with accumulate != 0: out = rnd(out + that) (Tensor._accumulate,
+ * models.py:107-109).  a: [k, m] pitch lda (the layer input x), b: [k, n] pitch
+ * ldb (the output gradient); the contraction over the k vertices is split
+ * across the SMs (tcgen05, fp32 TMEM partials), partials summed in a fixed
+ * order.  bias_out (may be NULL): [n] = rnd(sum_k b[k, n]), the bias gradient
+ * (add_bias backward, models.py:168-170), same accumulate rule, computed from
+ * the same read of b.  m, n: multiples of 8, n <= 256; 16-byte aligned a / b. */
+int hg_gemm_wgrad_workspace(int64_t k, int64_t m, int32_t n, size_t* bytes);
+int hg_gemm_wgrad(const void* a, int64_t k, int64_t m, int64_t lda, const void* b, int32_t n,
+                  int64_t ldb, void* out, int64_t ldo, void* bias_out, int32_t accumulate,
+                  void* ws, size_t ws_bytes, void* stream);
 
 /* ----------------------------------------------------------------- ingest */
 

@@ -24,6 +24,8 @@
 // (HBM), which is what the GCN layer-1 GEMM (233K x 608 x 64) costs.
 #include <cuda.h>
 
+#include <algorithm>
+
 #include "hg_common.cuh"
 
 namespace hg {
@@ -129,7 +131,9 @@ struct TcCfg {
   static constexpr bool kTmaStore = N % 64 == 0;
   static constexpr uint32_t kPitch = N * 2 + 16;  // padded staging row pitch (bytes)
   static constexpr uint32_t kBufs = (kTmaStore && N <= 128) ? 2 : 1;
-  static constexpr uint32_t kStage = kTmaStore ? kBufs * kTcBM * N * 2 : kTcBM * kPitch;
+  // (a width n_out < N, i.e. N padded up from 8 mod 16, takes the padded tile)
+  static constexpr uint32_t kStageT = kTmaStore ? kBufs * kTcBM * N * 2 : 0;
+  static constexpr uint32_t kStage = kStageT > kTcBM * kPitch ? kStageT : kTcBM * kPitch;
   static constexpr int kStages0 = (int)((200u * 1024u - kStage - kRes) / kSlot);
   static constexpr int kStages = kStages0 > 8 ? 8 : kStages0;
   static constexpr uint32_t kCols = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 2 * N <= 128 ? 128 : 2 * N <= 256 ? 256 : 512;
@@ -153,7 +157,8 @@ template <int N, bool RESB>
 __global__ void __launch_bounds__(192, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
           const __grid_constant__ CUtensorMap map_o, int64_t m, int num_kb, const __half* __restrict__ bias,
-          const __half* __restrict__ row_scale, __half* __restrict__ out, int64_t ldo, int relu) {
+          const __half* __restrict__ row_scale, __half* __restrict__ out, int64_t ldo, int relu,
+          int n_out) {
   using C = TcCfg<N, RESB>;
   constexpr int S = C::kStages;
   // instruction descriptor: f16 x f16 -> f32, both K-major, M = 128, N
@@ -174,6 +179,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t num_tiles = (m + kTcBM - 1) / kTcBM;
+  // TMA-store epilogue only when every one of the N columns is stored
+  const bool tstore = C::kTmaStore && n_out == N;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -256,8 +263,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
       const __half sv = (live && row_scale) ? row_scale[row] : __float2half_rn(1.0f);
       mbar_wait(&tfull[a], (tc >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      unsigned char* sbuf = stage + (C::kTmaStore ? (tc % C::kBufs) * (kTcBM * N * 2) : 0);
-      if constexpr (C::kTmaStore) {
+      unsigned char* sbuf = stage + (tstore ? (tc % C::kBufs) * (kTcBM * N * 2) : 0);
+      if (tstore) {
         // the TMA store issued from this buffer kBufs tiles ago has read it
         if (et == 0) {
           if constexpr (C::kBufs == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
@@ -265,7 +272,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
         }
         epi_bar();
       }
-      unsigned char* srow = sbuf + r * (C::kTmaStore ? 128 : C::kPitch);
+      unsigned char* srow = sbuf + r * (tstore ? 128 : C::kPitch);
       // TMEM loads batched 32 columns per wait (two x16 loads in flight)
       constexpr int kLdB = N % 32 == 0 ? 32 : 16;
 #pragma unroll
@@ -283,12 +290,12 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           __half t = __float2half_rn(__uint_as_float(v[j]));
-          if (bias) t = __hadd_rn(t, bias[c0 + j]);
+          if (bias && c0 + j < n_out) t = __hadd_rn(t, bias[c0 + j]);
           if (row_scale) t = __hmul_rn(t, sv);
           if (relu && !(__hgt(t, __float2half_rn(0.0f)))) t = __float2half_rn(0.0f);
           h[j] = t;
         }
-        if constexpr (C::kTmaStore) {
+        if (tstore) {
           // 64-column boxes of 128 rows x 128 B, 16-byte chunk c of row r at c ^ (r & 7)
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
@@ -304,7 +311,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&tempty[a]);  // accumulator drained: the MMA warp may reuse it
-      if constexpr (C::kTmaStore) {
+      if (tstore) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> TMA
         epi_bar();
         if (et == 0) {
@@ -317,7 +324,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
         epi_bar();
         // coalesced write-back of the live rows: 16-byte chunks, row-major
         const int rows = (int)((m - m0) < kTcBM ? (m - m0) : kTcBM);
-        constexpr int CPR = N / 8;
+        const int CPR = n_out / 8;  // n_out <= N: columns past n_out are padding
         for (int ch = et; ch < rows * CPR; ch += 128) {
           const int rr = ch / CPR, c8 = ch - rr * CPR;
           *reinterpret_cast<uint4*>(out + (m0 + rr) * ldo + c8 * 8) =
@@ -326,7 +333,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
         epi_bar();
       }
     }
-    if (C::kTmaStore && et == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (tstore && et == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -353,8 +360,8 @@ static EncodeTiledFn encode_tiled() {
 
 // 2-D fp16 tensor [rows, cols] with row pitch ld (elements), box {64 cols, box_rows}.
 static int g_tma_err = 0;
-static bool make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld,
-                     uint32_t box_rows) {
+static bool make_map_box(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld,
+                         uint32_t box_cols, uint32_t box_rows) {
   EncodeTiledFn fn = encode_tiled();
   if (!fn) {
     g_tma_err = -1;
@@ -362,7 +369,7 @@ static bool make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t co
   }
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-  cuuint32_t box[2] = {(cuuint32_t)kTcBK, box_rows};
+  cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
   const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptr), dims,
                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -372,10 +379,15 @@ static bool make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t co
   return r == CUDA_SUCCESS;
 }
 
+static bool make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld,
+                     uint32_t box_rows) {
+  return make_map_box(map, ptr, rows, cols, ld, (uint32_t)kTcBK, box_rows);
+}
+
 template <int N, bool RESB>
 static int launch_gemm_tc_v(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
                             int64_t m, int num_kb, const void* bias, const void* row_scale,
-                            void* out, int64_t ldo, int relu, cudaStream_t st) {
+                            void* out, int64_t ldo, int relu, int n_out, cudaStream_t st) {
   constexpr size_t smem = TcCfg<N, RESB>::kSmem;
   static_assert(smem <= 227 * 1024, "gemm_tc shared memory budget");
   static_assert(TcCfg<N, RESB>::kStages >= 2, "gemm_tc ring too shallow");
@@ -387,7 +399,8 @@ static int launch_gemm_tc_v(const CUtensorMap& ma, const CUtensorMap& mb, const 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const unsigned grid = (unsigned)(tiles < sms ? tiles : sms);
   k_gemm_tc<N, RESB><<<grid, 192, smem, st>>>(
-      ma, mb, mo, m, num_kb, (const __half*)bias, (const __half*)row_scale, (__half*)out, ldo, relu);
+      ma, mb, mo, m, num_kb, (const __half*)bias, (const __half*)row_scale, (__half*)out, ldo, relu,
+      n_out);
   HG_LAUNCHED();
   return HG_OK;
 }
@@ -395,11 +408,267 @@ static int launch_gemm_tc_v(const CUtensorMap& ma, const CUtensorMap& mb, const 
 template <int N>
 static int launch_gemm_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
                           int64_t m, int64_t k, const void* bias, const void* row_scale, void* out,
-                          int64_t ldo, int relu, cudaStream_t st) {
+                          int64_t ldo, int relu, int n_out, cudaStream_t st) {
   const int num_kb = (int)((k + kTcBK - 1) / kTcBK);
   if (num_kb <= TcCfg<N, true>::kMaxResKb)
-    return launch_gemm_tc_v<N, true>(ma, mb, mo, m, num_kb, bias, row_scale, out, ldo, relu, st);
-  return launch_gemm_tc_v<N, false>(ma, mb, mo, m, num_kb, bias, row_scale, out, ldo, relu, st);
+    return launch_gemm_tc_v<N, true>(ma, mb, mo, m, num_kb, bias, row_scale, out, ldo, relu,
+                                     n_out, st);
+  return launch_gemm_tc_v<N, false>(ma, mb, mo, m, num_kb, bias, row_scale, out, ldo, relu,
+                                    n_out, st);
+}
+
+
+// ---------------------------------------------------------------------------
+// Weight gradient of the per-layer GEMM (matmul's backward, models.py:151-155):
+//
+//   out[m, n] = rnd(sum_k A[k, m] B[k, n])        A = x [K, M], B = g [K, N]
+//
+// The contraction runs over the vertices (K = 233K .. 16.7M rows) while the
+// output is tiny (M, N <= a few hundred), so the kernel splits K across the
+// SMs: CTA (group, split) streams its slab range of A and B once through a
+// TMA ring and keeps one fp32 TMEM accumulator per 128-row tile of M (up to
+// 512 TMEM columns), then writes its fp32 partial tile; hg_wgrad_reduce sums
+// the partials in split order (deterministic) and rounds once.  The bias
+// gradient (add_bias backward, models.py:168-170: column sums of g) rides
+// along as one more accumulator fed by a constant all-ones A tile, so g is
+// read once for both.  Both operands
+// are row-major in HBM, i.e. MN-major for the MMA: 64-element-wide x 32-row
+// TMA boxes with 128-byte swizzle are exactly the canonical MN-major SW128
+// atoms (8 K-rows of 128 B, 1024 B apart; the next 64 MN elements one box on).
+// Bound by reading A and B once from HBM.
+constexpr int kWgBK = 32;                         // K rows per slab
+constexpr uint32_t kWgBox = 64 * kWgBK * 2;       // one 64 (MN) x 32 (K) fp16 box
+constexpr int kWgMaxMT = 8;                       // 128-row M tiles per CTA
+
+// MN-major, 128-byte-swizzled operand: LBO = next 64-element MN block,
+// SBO = next 8-row K group.
+__device__ __forceinline__ uint64_t sw128_mnmajor_desc(const void* tile, uint32_t lbo) {
+  const uint64_t addr = smem_u32(tile);
+  uint64_t d = (addr >> 4) & 0x3FFFull;
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= 1ull << 46;
+  d |= 2ull << 61;
+  return d;
+}
+
+template <int NB>
+__global__ void __launch_bounds__(192, 1)
+k_gemm_wgrad(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+             int64_t m, int n, int mt_total, int mt_group, int64_t slabs, int64_t slabs_per_split,
+             int splits, int stages, uint32_t tmem_cols, int with_bias, float* __restrict__ part) {
+  constexpr int UN = 64 * NB;  // UMMA N
+  // f16 x f16 -> f32, A and B MN-major, M = 128, N = UN
+  constexpr uint32_t kIdesc = (1u << 4) | (1u << 15) | (1u << 16) | ((uint32_t)(UN >> 3) << 17) |
+                              ((uint32_t)(kTcBM >> 4) << 24);
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int group = blockIdx.x / splits, split = blockIdx.x - group * splits;
+  const int t0 = group * mt_group;
+  const int mt = min(mt_group, mt_total - t0);
+  const uint32_t stage_bytes = (uint32_t)(2 * mt_group + NB) * kWgBox;
+  unsigned char* ones = base + (size_t)stages * stage_bytes;  // [2][kWgBox] of 1.0
+  uint64_t* full = reinterpret_cast<uint64_t*>(ones + 2 * kWgBox);
+  uint64_t* empty = full + stages;
+  uint64_t* tfull = empty + stages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  const int64_t kb0 = (int64_t)split * slabs_per_split;
+  const int64_t nkb = min(slabs_per_split, slabs - kb0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // the bias accumulator: rows of the all-ones tile times B = column sums of B
+  const bool bias_acc = with_bias && group == 0;
+  if (bias_acc) {
+    for (int i = threadIdx.x; i < (int)(2 * kWgBox / 16); i += blockDim.x)
+      reinterpret_cast<uint4*>(ones)[i] = make_uint4(0x3C003C00u, 0x3C003C00u, 0x3C003C00u, 0x3C003C00u);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
+  }
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer: per slab, mt tiles x 2 boxes of A and NB boxes of B
+      for (int64_t it = 0; it < nkb; ++it) {
+        const int s = (int)(it % stages);
+        mbar_wait(&empty[s], (uint32_t)((it / stages) & 1) ^ 1);
+        mbar_expect_tx(&full[s], (uint32_t)(2 * mt + NB) * kWgBox);
+        unsigned char* st = base + (size_t)s * stage_bytes;
+        const int krow = (int)((kb0 + it) * kWgBK);
+        for (int t = 0; t < mt; ++t)
+          for (int h = 0; h < 2; ++h)
+            tma_load_2d(st + (2 * t + h) * kWgBox, &map_a, &full[s], (t0 + t) * kTcBM + 64 * h, krow);
+        for (int b = 0; b < NB; ++b)
+          tma_load_2d(st + (2 * mt_group + b) * kWgBox, &map_b, &full[s], 64 * b, krow);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      for (int64_t it = 0; it < nkb; ++it) {
+        const int s = (int)(it % stages);
+        mbar_wait(&full[s], (uint32_t)(it / stages) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        unsigned char* st = base + (size_t)s * stage_bytes;
+        for (int t = 0; t < mt; ++t) {
+#pragma unroll
+          for (int k = 0; k < kWgBK / 16; ++k) {  // 16 K rows = 2 swizzle atoms = 2048 B
+            const uint64_t da = sw128_mnmajor_desc(st + 2 * t * kWgBox + k * 2048, kWgBox);
+            const uint64_t db = sw128_mnmajor_desc(st + 2 * mt_group * kWgBox + k * 2048, kWgBox);
+            umma_f16_f32(tmem + (uint32_t)(t * UN), da, db, kIdesc, (it | k) != 0);
+          }
+        }
+        if (bias_acc) {
+#pragma unroll
+          for (int k = 0; k < kWgBK / 16; ++k) {
+            const uint64_t da = sw128_mnmajor_desc(ones + k * 2048, kWgBox);
+            const uint64_t db = sw128_mnmajor_desc(st + 2 * mt_group * kWgBox + k * 2048, kWgBox);
+            umma_f16_f32(tmem + (uint32_t)(mt * UN), da, db, kIdesc, (it | k) != 0);
+          }
+        }
+        umma_commit(&empty[s]);
+      }
+      umma_commit(tfull);
+    }
+    __syncwarp();
+  } else {  // epilogue warps 2..5: TMEM lane quarter q = rows 32q..32q+31 of each tile
+    const int q = warp & 3;
+    if (nkb > 0) {
+      mbar_wait(tfull, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    // tile mt (bias_acc only): any one TMEM lane holds the column sums; lane 0 -> row m
+    const int tiles = mt + (bias_acc && q == 0 ? 1 : 0);
+    for (int t = 0; t < tiles; ++t) {
+      const bool brow = t == mt;
+      const int64_t row = brow ? (lane == 0 ? m : m + 1) : (int64_t)(t0 + t) * kTcBM + q * 32 + lane;
+      float* dst = part + ((int64_t)split * (m + 1) + row) * n;
+#pragma unroll 1
+      for (int cb = 0; cb < UN; cb += 32) {
+        uint32_t v[32];
+        if (nkb > 0) {
+          tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + t * UN + cb, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+          tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + t * UN + cb + 16,
+                    *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = 0u;
+        }
+        if (row < m || (brow && lane == 0)) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            if (cb + j < n)  // n is a multiple of 8 (and so of 4)
+              *reinterpret_cast<float4*>(dst + cb + j) =
+                  make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
+                              __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols));
+}
+
+// out[m, n] = rnd(sum_s part[s, m, n]) in split order; with accumulate,
+// out = rnd(out + that) (autograd's in-place gradient accumulation).
+// Partials are [splits][m + 1][n]; row m holds the bias column sums (written
+// to bias_out when it is non-null).
+__global__ void k_wgrad_reduce(const float* __restrict__ part, int splits, int64_t m, int n,
+                               __half* __restrict__ out, int64_t ldo, __half* __restrict__ bias_out,
+                               int accumulate) {
+  const int64_t n4 = n / 4;
+  const int64_t total = (m + (bias_out ? 1 : 0)) * n4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / n4, c = (i - r * n4) * 4;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < splits; ++s) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(part + ((int64_t)s * (m + 1) + r) * n + c));
+      acc.x = __fadd_rn(acc.x, v.x);
+      acc.y = __fadd_rn(acc.y, v.y);
+      acc.z = __fadd_rn(acc.z, v.z);
+      acc.w = __fadd_rn(acc.w, v.w);
+    }
+    __half h[4] = {__float2half_rn(acc.x), __float2half_rn(acc.y), __float2half_rn(acc.z),
+                   __float2half_rn(acc.w)};
+    __half* o = r < m ? out + r * ldo + c : bias_out + c;
+    if (accumulate) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) h[j] = __hadd_rn(o[j], h[j]);
+    }
+    *reinterpret_cast<uint2*>(o) = *reinterpret_cast<const uint2*>(h);
+  }
+}
+
+struct WgradPlan {
+  int nb, mt_total, mt_group, groups, splits, stages;
+  int64_t slabs, sps;
+  uint32_t tmem_cols;
+  size_t smem, part_bytes;
+};
+
+static WgradPlan wgrad_plan(int64_t k, int64_t m, int n, int sms) {
+  WgradPlan p{};
+  p.nb = (n + 63) / 64;
+  p.mt_total = (int)((m + kTcBM - 1) / kTcBM);
+  // TMEM: one 64*nb-column accumulator per tile, plus the bias accumulator
+  const int mt_cap = std::min(kWgMaxMT, 512 / (64 * p.nb) - 1);
+  p.groups = (p.mt_total + mt_cap - 1) / mt_cap;
+  p.mt_group = (p.mt_total + p.groups - 1) / p.groups;
+  const uint32_t cols = (uint32_t)((p.mt_group + 1) * 64 * p.nb);
+  p.tmem_cols = 32;
+  while (p.tmem_cols < cols) p.tmem_cols <<= 1;
+  p.slabs = (k + kWgBK - 1) / kWgBK;
+  // >= 16 slabs (512 rows) per split keeps the partials small next to A
+  int64_t want = std::max<int64_t>(1, std::min<int64_t>(sms / p.groups, (p.slabs + 15) / 16));
+  p.sps = (p.slabs + want - 1) / want;
+  p.splits = (int)((p.slabs + p.sps - 1) / p.sps);
+  if (p.splits < 1) p.splits = 1;
+  const uint32_t stage = (uint32_t)(2 * p.mt_group + p.nb) * kWgBox;
+  p.stages = (int)std::min<uint32_t>(8, (200u * 1024u) / stage);
+  p.smem = 1024 + (size_t)p.stages * stage + 2 * kWgBox + (2 * p.stages + 1) * 8 + 16;
+  p.part_bytes = align_up((size_t)p.splits * (size_t)(m + 1) * (size_t)n * sizeof(float));
+  return p;
+}
+
+static int device_sms() {
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+template <int NB>
+static int launch_wgrad(const CUtensorMap& ma, const CUtensorMap& mb, const WgradPlan& p, int64_t m,
+                        int n, int with_bias, float* part, cudaStream_t st) {
+  HG_CUDA(cudaFuncSetAttribute(k_gemm_wgrad<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)p.smem));
+  k_gemm_wgrad<NB><<<p.groups * p.splits, 192, p.smem, st>>>(
+      ma, mb, m, n, p.mt_total, p.mt_group, p.slabs, p.sps, p.splits, p.stages, p.tmem_cols,
+      with_bias, part);
+  HG_LAUNCHED();
+  return HG_OK;
 }
 
 }  // namespace hg
@@ -412,7 +681,10 @@ extern "C" int hg_gemm_tc(const void* a, int64_t m, int64_t k, int64_t lda, cons
   HG_REQUIRE(m >= 0 && k > 0, "hg_gemm_tc: bad arguments");
   if (m == 0) return HG_OK;
   HG_REQUIRE(a && bt && out, "hg_gemm_tc: null operand");
-  HG_REQUIRE(n >= 16 && n <= 256 && n % 16 == 0, "hg_gemm_tc: N=%d must be a multiple of 16 in [16, 256]", n);
+  HG_REQUIRE(n >= 8 && n <= 256 && n % 8 == 0, "hg_gemm_tc: N=%d must be a multiple of 8 in [8, 256]", n);
+  // UMMA N is a multiple of 16: a width of 8 (mod 16) runs as the next
+  // multiple, its extra Bt rows zero-filled by TMA and its columns not stored
+  const int n16 = (n + 15) / 16 * 16;
   HG_REQUIRE(lda >= k && ldb >= k && ldo >= n && lda % 8 == 0 && ldb % 8 == 0 && ldo % 8 == 0,
              "hg_gemm_tc: row pitches must cover K / N and be multiples of 8 elements");
   HG_REQUIRE(((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(bt) |
@@ -428,7 +700,7 @@ extern "C" int hg_gemm_tc(const void* a, int64_t m, int64_t k, int64_t lda, cons
   HG_REQUIRE(make_map(&ma, a, m, k, lda, kTcBM),
              "hg_gemm_tc: cuTensorMapEncodeTiled(A [%lld x %lld], pitch %lld, ptr %p) failed: %d",
              (long long)m, (long long)k, (long long)lda, a, g_tma_err);
-  HG_REQUIRE(make_map(&mb, bt, n, k, ldb, (uint32_t)n),
+  HG_REQUIRE(make_map(&mb, bt, n, k, ldb, (uint32_t)n16),
              "hg_gemm_tc: cuTensorMapEncodeTiled(Bt [%d x %lld], pitch %lld, ptr %p) failed: %d",
              n, (long long)k, (long long)ldb, bt, g_tma_err);
   CUtensorMap mo = ma;  // TMA-store epilogue (N % 64 == 0): 64-column boxes of the output
@@ -437,12 +709,68 @@ extern "C" int hg_gemm_tc(const void* a, int64_t m, int64_t k, int64_t lda, cons
                "hg_gemm_tc: cuTensorMapEncodeTiled(out [%lld x %d], pitch %lld) failed: %d",
                (long long)m, n, (long long)ldo, g_tma_err);
   cudaStream_t st = as_stream(stream);
-  switch (n) {
-#define HG_TC(NN) case NN: return launch_gemm_tc<NN>(ma, mb, mo, m, k, bias, row_scale, out, ldo, relu, st);
+  switch (n16) {
+#define HG_TC(NN) case NN: return launch_gemm_tc<NN>(ma, mb, mo, m, k, bias, row_scale, out, ldo, relu, n, st);
     HG_TC(16) HG_TC(32) HG_TC(48) HG_TC(64) HG_TC(80) HG_TC(96) HG_TC(112) HG_TC(128)
     HG_TC(144) HG_TC(160) HG_TC(176) HG_TC(192) HG_TC(208) HG_TC(224) HG_TC(240) HG_TC(256)
 #undef HG_TC
     default: break;
   }
   HG_REQUIRE(false, "hg_gemm_tc: unsupported N=%d", n);
+}
+
+extern "C" int hg_gemm_wgrad_workspace(int64_t k, int64_t m, int32_t n, size_t* bytes) {
+  HG_REQUIRE(bytes && k >= 0 && m >= 0 && n >= 8 && n <= 256 && n % 8 == 0,
+             "hg_gemm_wgrad_workspace: bad arguments (N=%d must be a multiple of 8 in [8, 256])", n);
+  *bytes = (k == 0 || m == 0) ? 0 : wgrad_plan(k, m, n, device_sms()).part_bytes;
+  return HG_OK;
+}
+
+extern "C" int hg_gemm_wgrad(const void* a, int64_t k, int64_t m, int64_t lda, const void* b,
+                             int32_t n, int64_t ldb, void* out, int64_t ldo, void* bias_out,
+                             int32_t accumulate, void* ws, size_t ws_bytes, void* stream) {
+  HG_REQUIRE(k >= 0 && m >= 0, "hg_gemm_wgrad: bad arguments");
+  HG_REQUIRE(n >= 8 && n <= 256 && n % 8 == 0, "hg_gemm_wgrad: N=%d must be a multiple of 8 in [8, 256]", n);
+  if (m == 0) return HG_OK;
+  HG_REQUIRE(out, "hg_gemm_wgrad: null output");
+  HG_REQUIRE(m % 8 == 0 && lda >= m && ldb >= n && ldo >= n && lda % 8 == 0 && ldb % 8 == 0 && ldo % 4 == 0,
+             "hg_gemm_wgrad: M must be a multiple of 8 and pitches cover M / N (multiples of 8)");
+  cudaStream_t st = as_stream(stream);
+  if (k == 0) {  // empty sum: zeros (or out unchanged when accumulating)
+    k_wgrad_reduce<<<grid_for((m + 1) * (n / 4), 256, 4096), 256, 0, st>>>(
+        nullptr, 0, m, n, (__half*)out, ldo, (__half*)bias_out, accumulate);
+    HG_LAUNCHED();
+    return HG_OK;
+  }
+  HG_REQUIRE(a && b, "hg_gemm_wgrad: null operand");
+  HG_REQUIRE(((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0 &&
+                 ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(bias_out)) & 7) == 0,
+             "hg_gemm_wgrad: operands must be 16-byte aligned, out 8-byte aligned");
+  const WgradPlan p = wgrad_plan(k, m, n, device_sms());
+  HG_REQUIRE(ws && ws_bytes >= p.part_bytes, "hg_gemm_wgrad: workspace too small (%zu < %zu)",
+             ws_bytes, p.part_bytes);
+  int dev = 0;
+  HG_CUDA(cudaGetDevice(&dev));
+  HG_CUDA(cudaSetDevice(dev));
+  CUtensorMap ma, mb;
+  // A = x [k rows, m cols]: boxes of 64 columns x 32 rows; B = g [k, n] likewise
+  HG_REQUIRE(make_map_box(&ma, a, k, m, lda, 64, kWgBK),
+             "hg_gemm_wgrad: cuTensorMapEncodeTiled(A [%lld x %lld]) failed: %d", (long long)k,
+             (long long)m, g_tma_err);
+  HG_REQUIRE(make_map_box(&mb, b, k, n, ldb, 64, kWgBK),
+             "hg_gemm_wgrad: cuTensorMapEncodeTiled(B [%lld x %d]) failed: %d", (long long)k, n,
+             g_tma_err);
+  float* part = static_cast<float*>(ws);
+  int rc = HG_OK;
+  switch (p.nb) {
+    case 1: rc = launch_wgrad<1>(ma, mb, p, m, n, bias_out != nullptr, part, st); break;
+    case 2: rc = launch_wgrad<2>(ma, mb, p, m, n, bias_out != nullptr, part, st); break;
+    case 3: rc = launch_wgrad<3>(ma, mb, p, m, n, bias_out != nullptr, part, st); break;
+    default: rc = launch_wgrad<4>(ma, mb, p, m, n, bias_out != nullptr, part, st); break;
+  }
+  if (rc != HG_OK) return rc;
+  k_wgrad_reduce<<<grid_for((m + 1) * (n / 4), 256, 4096), 256, 0, st>>>(
+      part, p.splits, m, n, (__half*)out, ldo, (__half*)bias_out, accumulate);
+  HG_LAUNCHED();
+  return HG_OK;
 }

@@ -829,7 +829,7 @@ def edge_rowsum(dg: DeviceGraph, v, transpose=False):
 def gemm_tc(a, bt, bias=None, row_scale=None, out=None, relu=False):
     """rnd(rnd(rnd(a @ bt.T) + bias) * row_scale[:, None]) (then max(., 0) with
     relu) on the tcgen05 tensor cores (hg_gemm_tc): a [M, K] fp16, bt [N, K]
-    fp16 (N % 16 == 0)."""
+    fp16 (N % 8 == 0)."""
     _require_cuda(a, bt)
     if a.dtype != torch.float16 or bt.dtype != torch.float16:
         raise ValueError("hg_gemm_tc takes binary16 operands")
@@ -850,6 +850,41 @@ def gemm_tc(a, bt, bias=None, row_scale=None, out=None, relu=False):
              out.stride(0), _stream())
     Probe.launches += 1
     return out
+
+
+def gemm_wgrad(a, b, out=None, bias_out=None, accumulate=False, bias=False):
+    """rnd(a.T @ b) -- fp32 accumulation, one rounding -- on the tcgen05 tensor
+    cores with the vertex dimension split across the SMs (hg_gemm_wgrad):
+    a [K, M] fp16 (layer input), b [K, N] fp16 (output gradient), M and N
+    multiples of 8, N <= 256.  With bias (or a bias_out buffer) the column sums
+    rnd(sum_k b[k, :]) come out of the same pass; returns (dW, db) then.  With
+    accumulate, out = rnd(out + a.T @ b) (and likewise bias_out): autograd's
+    gradient accumulation into a leaf, done in the kernel."""
+    _require_cuda(a, b)
+    if a.dtype != torch.float16 or b.dtype != torch.float16:
+        raise ValueError("hg_gemm_wgrad takes binary16 operands")
+    a, b = a.contiguous(), b.contiguous()
+    if a.data_ptr() % 16:
+        a = a.clone()
+    if b.data_ptr() % 16:
+        b = b.clone()
+    k, m = a.shape
+    k2, n = b.shape
+    if k2 != k:
+        raise ValueError(f"row counts differ: {k} vs {k2}")
+    if accumulate and (out is None or ((bias or bias_out is not None) and bias_out is None)):
+        raise ValueError("accumulate needs the output buffers")
+    if out is None:
+        out = torch.empty((m, n), dtype=torch.float16, device=a.device)
+    if bias and bias_out is None:
+        bias_out = torch.empty(n, dtype=torch.float16, device=a.device)
+    nbytes = nat.size_query("hg_gemm_wgrad_workspace", k, m, n)
+    ws = workspace(nbytes, a.device)
+    nat.call("hg_gemm_wgrad", _p(a), k, m, a.stride(0), _p(b), n, b.stride(0), _p(out),
+             out.stride(0), _p(bias_out), int(accumulate), _p(ws),
+             0 if ws is None else ws.numel(), _stream())
+    Probe.launches += 2 if k else 1
+    return out if bias_out is None else (out, bias_out)
 
 
 def bias_scale_rows(x, bias=None, row_scale=None, out=None):

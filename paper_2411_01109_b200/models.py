@@ -281,12 +281,14 @@ class _GCNLayerFn(torch.autograd.Function):
     """GCNLayer (models.py:456-468) = spmm_agg(add_bias(matmul(x, W), b)) with
     the GEMM, the bias add and the aggregation's left-norm input scale in one
     tcgen05 kernel (hg_gemm_tc), then the gather SpMM.  Backward: transposed
-    SpMM, bias gradient = its column sums, dW = x^T dh and dx = dh W^T on
-    cuBLAS (fp32 accumulation, one rounding: matmul's backward, 150-155)."""
+    SpMM, then dW = x^T dh with the bias gradient (column sums of dh) in the
+    same tcgen05 pass (hg_gemm_wgrad) and dx = dh W^T (hg_gemm_tc): fp32
+    accumulation, one rounding (matmul's backward, 150-155)."""
 
     @staticmethod
     def forward(ctx, x, w, b, bundle, reduction, relu=False):
         ctx.bundle, ctx.reduction, ctx.relu = bundle, reduction, relu
+        ctx.leaves = (w, b)
         y = bundle.gcn_agg_tc(x, w, b, reduction, relu=True) if relu else \
             bundle.gcn_agg_tc(x, w, b, reduction)
         ctx.save_for_backward(x, w, y if relu else None)
@@ -300,8 +302,9 @@ class _GCNLayerFn(torch.autograd.Function):
         if ctx.relu:
             g = D.relu_grad(y, g)
         gh = ctx.bundle.spmm(g, None, r.scaling, _MIRROR[r.norm], transpose=True)
-        gx = gh @ w.t() if ctx.needs_input_grad[0] else None
-        return gx, x.t() @ gh, D.col_sums(gh), None, None, None
+        gx = D.gemm_tc(gh, w) if ctx.needs_input_grad[0] else None
+        gw, gb = _weight_grads(x, gh, *ctx.leaves)
+        return gx, gw, gb, None, None, None
 
 
 def spmm_agg(bundle, x, reduction, width="half2", overflow=None, tag="agg"):
@@ -446,8 +449,58 @@ def shadow_div(num, den, overflow=None, tag="div"):
 # ── dense / elementwise ops ──────────────────────────────────────────────
 
 
+def _tc_shapes(x, w):
+    """x @ w fits the tcgen05 kernels (hg_gemm_tc forward / dx, hg_gemm_wgrad
+    dW): binary16 CUDA operands, widths multiples of 8 up to 256 (the input
+    width only bounds dx, and only when x needs a gradient)."""
+    return (x.is_cuda and x.dtype == torch.float16 and w.dtype == torch.float16
+            and x.dim() == 2 and w.dim() == 2 and x.shape[1] == w.shape[0]
+            and x.shape[1] % 8 == 0 and w.shape[1] % 8 == 0 and w.shape[1] <= 256
+            and (not x.requires_grad or x.shape[1] <= 256))
+
+
+def _weight_grads(x, g, w, b=None):
+    """(dW, db) of y = x w (+ b): one hg_gemm_wgrad pass over x and g (fp32
+    accumulation, one rounding each; matmul / add_bias backward, models.py:
+    151-155, 168-170).  When the leaves own persistent gradient buffers (a
+    ParamGroup), the kernel accumulates into them in place and autograd gets
+    None -- no separate accumulate kernel."""
+    if (w.is_leaf and w.grad is not None and w.grad.is_contiguous()
+            and (b is None or (b.is_leaf and b.grad is not None))):
+        D.gemm_wgrad(x, g, out=w.grad, bias_out=None if b is None else b.grad,
+                     accumulate=True)
+        return None, None
+    if b is None:
+        return D.gemm_wgrad(x, g), None
+    return D.gemm_wgrad(x, g, bias=True)
+
+
+class _MatmulTCFn(torch.autograd.Function):
+    """matmul (models.py:141-158) on the tcgen05 tensor cores: y = x w with fp32
+    accumulation and one rounding (hg_gemm_tc); backward dx = g w^T
+    (hg_gemm_tc) and dW = x^T g (hg_gemm_wgrad, split over the vertices)."""
+
+    @staticmethod
+    def forward(ctx, x, w):
+        ctx.w_leaf = w
+        ctx.save_for_backward(x, w)
+        return D.gemm_tc(x, w.t().contiguous())
+
+    @staticmethod
+    def backward(ctx, g):
+        x, w = ctx.saved_tensors
+        g = g.contiguous()
+        gx = D.gemm_tc(g, w) if ctx.needs_input_grad[0] else None
+        gw = _weight_grads(x, g, ctx.w_leaf)[0] if ctx.needs_input_grad[1] else None
+        return gx, gw
+
+
 def matmul(a, b):
-    """Tensor-core GEMM, fp32 accumulation, one rounding to the input dtype."""
+    """Tensor-core GEMM, fp32 accumulation, one rounding to the input dtype:
+    the hand-written tcgen05 kernels for binary16 CUDA operands, torch for the
+    float32 mode and host tensors."""
+    if _tc_shapes(a, b):
+        return _MatmulTCFn.apply(a, b)
     return a @ b
 
 
@@ -632,8 +685,7 @@ class Linear:
         """tc: run on the tcgen05 GEMM with the bias (and, with relu_out, the
         following ReLU) fused into its epilogue when the shapes allow."""
         w = self.w.publish(mode)
-        if (tc and mode == "half" and x.is_cuda and self.b is not None and w.shape[1] % 16 == 0
-                and x.shape[1] % 8 == 0):
+        if tc and mode == "half" and self.b is not None and _tc_shapes(x, w):
             return _LinearTCFn.apply(x, w, self.b.publish(mode), relu_out)
         out = matmul(x, w)
         if self.b is not None:
@@ -643,13 +695,16 @@ class Linear:
 
 class _LinearTCFn(torch.autograd.Function):
     """[relu](add_bias(matmul(x, W), b)) (models.py:141-185) as one tcgen05 GEMM
-    with the epilogue fused; backward on cuBLAS (fp32 accumulation, one
-    rounding), the ReLU mask taken from the output (y > 0 iff pre-activation > 0)."""
+    with the epilogue fused; backward on the tensor cores too: dx = g W^T
+    (hg_gemm_tc), dW = x^T g and db = column sums of g from one hg_gemm_wgrad
+    pass (fp32 accumulation, one rounding each), the ReLU mask taken from the
+    output (y > 0 iff pre-activation > 0)."""
 
     @staticmethod
     def forward(ctx, x, w, b, relu_out):
         y = D.gemm_tc(x, w.t().contiguous(), b, None, relu=relu_out)
         ctx.relu_out = relu_out
+        ctx.leaves = (w, b)
         ctx.save_for_backward(x, w, y if relu_out else None)
         return y
 
@@ -659,11 +714,10 @@ class _LinearTCFn(torch.autograd.Function):
         g = g.contiguous()
         if ctx.relu_out:
             g = D.relu_grad(y, g)
-        gx = None
-        if ctx.needs_input_grad[0]:
-            # dx = g W^T: W is already the [K, N] "B transposed" operand of hg_gemm_tc
-            gx = D.gemm_tc(g, w) if w.shape[0] % 16 == 0 else g @ w.t()
-        return gx, x.t() @ g, D.col_sums(g), None
+        # dx = g W^T: W is already the [K, N] "B transposed" operand of hg_gemm_tc
+        gx = D.gemm_tc(g, w) if ctx.needs_input_grad[0] else None
+        gw, gb = _weight_grads(x, g, *ctx.leaves)
+        return gx, gw, gb, None
 
 
 class GCNLayer:
@@ -684,7 +738,7 @@ class GCNLayer:
         fuse = relu_out and overflow is None and getattr(bundle, "fused_relu", False)
         if getattr(bundle, "fused_bias_agg", False) and self.lin.b is not None:
             w, b = self.lin.w.publish(mode), self.lin.b.publish(mode)
-            if mode == "half" and w.shape[1] % 16 == 0 and x.shape[1] % 8 == 0:
+            if mode == "half" and _tc_shapes(x, w):
                 # tensor-core GEMM with the bias / input-scale epilogue fused
                 y = _GCNLayerFn.apply(x, w, b, bundle, self.reduction, fuse)
             else:

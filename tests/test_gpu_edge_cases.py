@@ -66,9 +66,9 @@ def test_gemm_tc_degenerate_shapes(cuda):
         if m:
             want = (a.float() @ bt.float().t())
             assert torch.allclose(got.float(), want, atol=5e-2, rtol=1e-2)
-    with pytest.raises(ValueError, match="multiple of 16"):
+    with pytest.raises(ValueError, match="multiple of 8"):
         D.gemm_tc(torch.randn(4, 8, device=cuda, dtype=torch.float16),
-                  torch.randn(24, 8, device=cuda, dtype=torch.float16))
+                  torch.randn(12, 8, device=cuda, dtype=torch.float16))
 
 
 def test_softmax_xent_single_class_and_padding(cuda):

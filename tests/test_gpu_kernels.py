@@ -934,6 +934,111 @@ def test_gemm_tc_from_autograd_worker_thread(cuda):
     assert torch.allclose(x.grad.float(), g @ w.detach().float().t(), atol=2e-2, rtol=1e-2)
 
 
+def _wgrad_check(got, a, b):
+    """got = rnd(a^T b) up to the fp32 summation order: within one fp16 step
+    of the float64 value rounded once, plus an fp32-accumulation slack."""
+    acc = a.astype(np.float64).T @ b.astype(np.float64)
+    h = acc.astype(np.float16).astype(np.float64)
+    slack = 2.0 ** -10 * np.abs(h) + 1e-6 * (np.abs(a.astype(np.float64)).T
+                                              @ np.abs(b.astype(np.float64))) + 2.0 ** -24
+    bad = np.abs(got.astype(np.float64) - h) > slack
+    assert not bad.any(), f"{bad.sum()} of {bad.size} outside; max |d| {np.abs(got - h).max()}"
+
+
+@pytest.mark.parametrize("k,m,n", [(233, 608, 64), (5000, 64, 48), (100_000, 608, 64),
+                                   (7, 24, 8), (3000, 128, 128), (4097, 1032, 256),
+                                   (70_001, 112, 48), (19_717, 512, 64), (40, 8, 200)])
+def test_gemm_wgrad_vs_f64(cuda, k, m, n):
+    """hg_gemm_wgrad (dW = x^T g, split over the vertices, MN-major tcgen05
+    operands) and its fused bias gradient (column sums of g) vs float64:
+    ragged K, M and N, several M-tile groups, N from 8 to 256."""
+    from paper_2411_01109_b200 import device as D
+
+    rng = np.random.default_rng(k + m + n)
+    a = rng.normal(0, 1, (k, m)).astype(np.float16)
+    b = rng.normal(0, 1, (k, n)).astype(np.float16)
+    dw, db = D.gemm_wgrad(_t(a, cuda), _t(b, cuda), bias=True)
+    _wgrad_check(dw.cpu().numpy(), a, b)
+    _wgrad_check(db.cpu().numpy()[None, :], np.ones((k, 1), np.float16), b)
+    # deterministic: same bits on a second call
+    dw2 = D.gemm_wgrad(_t(a, cuda), _t(b, cuda))
+    assert torch.equal(dw, dw2)
+
+
+def test_gemm_wgrad_accumulate_and_empty(cuda):
+    """accumulate: out = rnd(out + rnd(a^T b)) (Tensor._accumulate); K = 0 gives
+    zeros, or leaves an accumulated output unchanged; strided (sliced) operands."""
+    from paper_2411_01109_b200 import device as D
+
+    rng = np.random.default_rng(5)
+    a = rng.normal(0, 1, (3000, 64)).astype(np.float16)
+    b = rng.normal(0, 1, (3000, 32)).astype(np.float16)
+    prev = rng.normal(0, 4, (64, 32)).astype(np.float16)
+    prevb = rng.normal(0, 4, 32).astype(np.float16)
+    out, outb = _t(prev, cuda), _t(prevb, cuda)
+    fresh, freshb = D.gemm_wgrad(_t(a, cuda), _t(b, cuda), bias=True)
+    D.gemm_wgrad(_t(a, cuda), _t(b, cuda), out=out, bias_out=outb, accumulate=True)
+    assert torch.equal(out, (prev_t := _t(prev, cuda)) + fresh)
+    assert torch.equal(outb, _t(prevb, cuda) + freshb)
+    z = D.gemm_wgrad(torch.empty(0, 16, device=cuda, dtype=torch.float16),
+                     torch.empty(0, 8, device=cuda, dtype=torch.float16))
+    assert z.shape == (16, 8) and not z.any()
+    keep = prev_t.clone()
+    D.gemm_wgrad(torch.empty(0, 64, device=cuda, dtype=torch.float16),
+                 torch.empty(0, 32, device=cuda, dtype=torch.float16), out=keep, accumulate=True)
+    assert torch.equal(keep, prev_t)
+    wide = _t(rng.normal(0, 1, (3000, 96)).astype(np.float16), cuda)
+    got = D.gemm_wgrad(wide[:, 16:80], _t(b, cuda))   # pitch 96, 16-byte aligned start
+    _wgrad_check(got.cpu().numpy(), wide[:, 16:80].cpu().numpy(), b)
+    with pytest.raises(ValueError, match="multiple of 8"):
+        D.gemm_wgrad(torch.zeros(8, 16, device=cuda, dtype=torch.float16),
+                     torch.zeros(8, 12, device=cuda, dtype=torch.float16))
+
+
+@pytest.mark.parametrize("n", [8, 24, 40, 56, 200])
+def test_gemm_tc_widths_8_mod_16(cuda, n):
+    """hg_gemm_tc with N = 8 (mod 16): runs as the next multiple of 16 and
+    stores only N columns (bias read only for those)."""
+    from paper_2411_01109_b200 import device as D
+
+    rng = np.random.default_rng(n)
+    a = rng.normal(0, 1, (1000, 72)).astype(np.float16)
+    wt = rng.normal(0, 0.2, (n, 72)).astype(np.float16)
+    bias = rng.normal(0, 1, n).astype(np.float16)
+    got = D.gemm_tc(_t(a, cuda), _t(wt, cuda), _t(bias, cuda)).cpu().numpy().astype(np.float64)
+    acc = a.astype(np.float64) @ wt.astype(np.float64).T
+    h = (acc.astype(np.float16).astype(np.float64) + bias).astype(np.float16).astype(np.float64)
+    assert got.shape == (1000, n)
+    assert np.all(np.abs(got - h) <= 2.0 ** -9 * np.abs(h) + 1e-3)
+
+
+def test_linear_tc_backward_on_tensor_cores(cuda):
+    """_LinearTCFn / _MatmulTCFn backward: dx, dW, db all from the tcgen05
+    kernels; with ParamGroup-style leaves (persistent .grad) the weight and
+    bias gradients accumulate in place and match a fresh computation."""
+    from paper_2411_01109_b200 import models as M
+
+    rng = np.random.default_rng(9)
+    x = _t(rng.normal(0, 1, (4000, 64)).astype(np.float16), cuda).requires_grad_(True)
+    w = _t((rng.normal(0, 0.1, (64, 40))).astype(np.float16), cuda).requires_grad_(True)
+    b = _t(rng.normal(0, 1, 40).astype(np.float16), cuda).requires_grad_(True)
+    g = _t(rng.normal(0, 1, (4000, 40)).astype(np.float16), cuda)
+    y = M._LinearTCFn.apply(x, w, b, False)
+    y.backward(g)
+    gw, gb, gx = w.grad.clone(), b.grad.clone(), x.grad.clone()
+    xf, wf, gf = x.detach().double(), w.detach().double(), g.double()
+    assert torch.allclose(gx.double(), gf @ wf.t(), atol=2e-2, rtol=1e-2)
+    assert torch.allclose(gw.double(), xf.t() @ gf, atol=0.5, rtol=2e-3)
+    assert torch.allclose(gb.double(), gf.sum(0), atol=0.5, rtol=2e-3)
+    # in place: pre-existing grads accumulate, autograd's own add not needed
+    y = M._LinearTCFn.apply(x, w, b, False)
+    y.backward(g)
+    assert torch.equal(w.grad, gw + gw) and torch.equal(b.grad, gb + gb)
+    # plain matmul (GAT projection, no bias) takes the same kernels
+    z = M.matmul(x, w)
+    assert z.grad_fn is not None and "MatmulTC" in type(z.grad_fn).__name__
+
+
 @pytest.mark.parametrize("shape", [(1000,), (1000, 4), (999, 3), (500, 8)])
 def test_gather_rows(cuda, shape):
     from paper_2411_01109_b200 import device as D

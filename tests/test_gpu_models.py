@@ -412,6 +412,38 @@ def test_cuda_graph_step_matches_eager(cuda):
         np.testing.assert_allclose(la, lb, rtol=0, atol=1e-6, err_msg=kind)
 
 
+@pytest.mark.parametrize("kind,kw", [("gcn", {}), ("gin", {}), ("gat", {"heads": 4, "layers": 3})])
+def test_training_step_dense_math_on_own_kernels(cuda, kind, kw):
+    """A fast-numerics half training step (the benched path) launches no
+    cuBLAS / library GEMM: forward, dx and dW GEMMs all run on hg_gemm_tc /
+    hg_gemm_wgrad (tcgen05).  The kernel list goes to HG_KERNEL_LIST if set."""
+    import os
+
+    from torch.profiler import ProfilerActivity, profile
+
+    from paper_2411_01109_b200 import graphgen, models as M
+    from paper_2411_01109_b200.device import DeviceGraph
+
+    rows, cols, feats, labels = graphgen.synth_sbm(3000, 3, 0.01, 0.001, 100, 1)
+    dg = DeviceGraph.from_edges(3000, rows, cols)
+    cfg = M.TrainConfig(kind=kind, hidden=16, numerics="fast", grad_scale="auto", **kw)
+    tr = M.Trainer(M.GraphBundle.build(dg, numerics="fast"), feats, labels, cfg)
+    for _ in range(2):
+        tr.step()
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        tr.step()
+        torch.cuda.synchronize()
+    names = sorted({e.name for e in prof.events() if e.device_type.name == "CUDA"})
+    if os.environ.get("HG_KERNEL_LIST"):
+        with open(os.environ["HG_KERNEL_LIST"], "a") as f:
+            f.write(f"== {kind}\n" + "\n".join(names) + "\n")
+    lib = [n for n in names if any(t in n.lower() for t in ("nvjet", "cublas", "cutlass", "sgemm",
+                                                            "hgemm", "gemv", "gemmk"))]
+    assert not lib, lib
+    assert any("k_gemm_wgrad" in n for n in names) and any("k_gemm_tc" in n for n in names)
+
+
 def test_run_epochs_host_feed_matches_steps(cuda):
     """Double-buffered host feeding (e2e path) trains exactly like step()."""
     from paper_2411_01109_b200 import graphgen, models as M
