@@ -7,7 +7,7 @@
 // add_bias (161-166) -> the aggregation's left-norm input scaling
 // (kernels.py:358-361), each rounding exactly where the reference rounds.
 //
-// Persistent, one CTA (192 threads) per SM over 128-row tiles:
+// Persistent, one CTA (320 threads) per SM over 128-row tiles:
 //   warp 0 / lane 0   TMA producer: 64-wide K slabs of A (128 x 64) and Bt
 //                     (N x 64) into a 3-8 deep shared-memory ring
 //                     (cp.async.bulk.tensor, SWIZZLE_128B, OOB -> zeros),
@@ -16,8 +16,9 @@
 //                     (M=128, N, K=16) per slab into one of two fp32 TMEM
 //                     accumulators; tcgen05.commit frees the slab / hands the
 //                     accumulator to the epilogue;
-//   warps 2-5         epilogue: tcgen05.ld 32x32b (warp w owns TMEM lanes
-//                     32(w%4)..+31 = rows), fp16 rounding, bias, row scale,
+//   warps 2-9         epilogue: tcgen05.ld 32x32b (warp w owns TMEM lanes
+//                     32(w%4)..+31 = rows; the two warps of a quarter split
+//                     the 16-column chunks), fp16x2 rounding, bias, row scale,
 //                     staged in shared memory, coalesced 16-byte stores; it
 //                     overlaps the next tile's MMAs.
 // Fed by TMA and drained from TMEM, the kernel is bound by reading A once
@@ -25,6 +26,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "hg_common.cuh"
 
@@ -112,8 +114,8 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 
-__device__ __forceinline__ void epi_bar() {  // named barrier over the 4 epilogue warps
-  asm volatile("bar.sync 1, 128;" ::: "memory");
+__device__ __forceinline__ void epi_bar_n(int threads) {  // named barrier over the epilogue warps
+  asm volatile("bar.sync 1, %0;" ::"r"(threads) : "memory");
 }
 
 // smem ring depth for a given N (the ring plus the output staging tile fit ~200 KB)
@@ -138,8 +140,13 @@ struct TcCfg {
   static constexpr int kStages = kStages0 > 8 ? 8 : kStages0;
   static constexpr uint32_t kCols = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 2 * N <= 128 ? 128 : 2 * N <= 256 ? 256 : 512;
   static constexpr size_t kSmem = 1024 + (size_t)kStages * kSlot + kRes + kStage +
-                                  (2 * kStages + 5) * 8 + 16;
+                                  (2 * kStages + 5) * 8 + 16 + N * 2;
 };
+
+// Epilogue: kEpiWarps warps, two per TMEM lane quarter (warp w reads lanes
+// 32 (w % 4) ..); the pair splits the tile's 16-column chunks between them.
+constexpr int kEpiWarps = 8;
+constexpr int kTcThreads = 64 + 32 * kEpiWarps;
 
 // Persistent: one CTA per SM loops over 128-row tiles.  Warp 0 = TMA producer
 // (runs ahead across tile boundaries through the ring), warp 1 = MMA issuer,
@@ -154,13 +161,14 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
 }
 
 template <int N, bool RESB>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kTcThreads, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
           const __grid_constant__ CUtensorMap map_o, int64_t m, int num_kb, const __half* __restrict__ bias,
           const __half* __restrict__ row_scale, __half* __restrict__ out, int64_t ldo, int relu,
           int n_out) {
   using C = TcCfg<N, RESB>;
   constexpr int S = C::kStages;
+  constexpr int kEpiThreads = 32 * kEpiWarps;
   // instruction descriptor: f16 x f16 -> f32, both K-major, M = 128, N
   constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kTcBM >> 4) << 24);
 
@@ -176,6 +184,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
   uint64_t* tempty = tfull + 2;                      // [2]
   uint64_t* bfull = tempty + 2;                      // resident B landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
+  __half* sbias = reinterpret_cast<__half*>(tmem_slot + 4);  // [N], zero past n_out
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t num_tiles = (m + kTcBM - 1) / kTcBM;
@@ -189,13 +198,15 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], kEpiThreads);
     }
     mbar_init(bfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
   }
+  for (int j = threadIdx.x; j < N; j += blockDim.x)
+    sbias[j] = (bias && j < n_out) ? bias[j] : __ushort_as_half(0);
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
@@ -250,17 +261,21 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
       }
     }
     __syncwarp();
-  } else {  // epilogue warps 2..5: TMEM lane quarter = warp % 4
+  } else {  // epilogue warps 2..: TMEM lane quarter = warp % 4, chunk parity = pair member
     const int q = warp & 3;
-    const int r = q * 32 + lane;  // tile row = TMEM lane
-    const int et = threadIdx.x - 64;  // 0..127
+    const int half = (warp - 2) >> 2;  // 0 / 1: 16-column chunks of this parity
+    const int r = q * 32 + lane;       // tile row = TMEM lane
+    const int et = threadIdx.x - 64;   // 0 .. kEpiThreads - 1
+    const __half2 z2 = __half2half2(__ushort_as_half(0));
+    const __half2* bias2 = reinterpret_cast<const __half2*>(sbias);
+    constexpr int kChunks = N / 16;
     uint32_t tc = 0;
     for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tc) {
       const uint32_t a = tc & 1;
       const int64_t m0 = tile * kTcBM;
       const int64_t row = m0 + r;
       const bool live = row < m;
-      const __half sv = (live && row_scale) ? row_scale[row] : __float2half_rn(1.0f);
+      const __half2 sv2 = __half2half2((live && row_scale) ? row_scale[row] : __float2half_rn(1.0f));
       mbar_wait(&tfull[a], (tc >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       unsigned char* sbuf = stage + (tstore ? (tc % C::kBufs) * (kTcBM * N * 2) : 0);
@@ -270,50 +285,60 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
           if constexpr (C::kBufs == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
           else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         }
-        epi_bar();
+        epi_bar_n(kEpiThreads);
       }
       unsigned char* srow = sbuf + r * (tstore ? 128 : C::kPitch);
-      // TMEM loads batched 32 columns per wait (two x16 loads in flight)
-      constexpr int kLdB = N % 32 == 0 ? 32 : 16;
+      // this warp's chunks: half, half + 2, ... ; TMEM loads two chunks per wait
 #pragma unroll
-      for (int cb = 0; cb < N; cb += kLdB) {
-        uint32_t vv[kLdB];
-#pragma unroll
-        for (int u = 0; u < kLdB / 16; ++u)
-          tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + a * N + cb + 16 * u,
-                    *reinterpret_cast<uint32_t(*)[16]>(&vv[16 * u]));
+      for (int ch0 = half; ch0 < kChunks; ch0 += 4) {
+        uint32_t vv[2][16];
+        const bool two = ch0 + 2 < kChunks;
+        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + a * N + ch0 * 16, vv[0]);
+        if (two) tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + a * N + (ch0 + 2) * 16, vv[1]);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-      for (int c0 = cb; c0 < cb + kLdB; c0 += 16) {
-        const uint32_t* v = &vv[c0 - cb];
-        __align__(16) __half h[16];
+        for (int u = 0; u < 2; ++u) {
+          if (u == 1 && !two) break;
+          const int c0 = (ch0 + 2 * u) * 16;
+          __align__(16) __half2 h[8];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          __half t = __float2half_rn(__uint_as_float(v[j]));
-          if (bias && c0 + j < n_out) t = __hadd_rn(t, bias[c0 + j]);
-          if (row_scale) t = __hmul_rn(t, sv);
-          if (relu && !(__hgt(t, __float2half_rn(0.0f)))) t = __float2half_rn(0.0f);
-          h[j] = t;
-        }
-        if (tstore) {
-          // 64-column boxes of 128 rows x 128 B, 16-byte chunk c of row r at c ^ (r & 7)
+          for (int j = 0; j < 8; ++j)
+            h[j] = __floats2half2_rn(__uint_as_float(vv[u][2 * j]), __uint_as_float(vv[u][2 * j + 1]));
+          if (bias) {
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            const int c = c0 / 8 + hh;
-            unsigned char* dst = sbuf + (c / 8) * (kTcBM * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4);
-            *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(&h[8 * hh]);
+            for (int j = 0; j < 8; ++j) h[j] = __hadd2_rn(h[j], bias2[c0 / 2 + j]);
           }
-        } else {
-          reinterpret_cast<uint4*>(srow + c0 * 2)[0] = *reinterpret_cast<const uint4*>(&h[0]);
-          reinterpret_cast<uint4*>(srow + c0 * 2)[1] = *reinterpret_cast<const uint4*>(&h[8]);
+          if (row_scale) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) h[j] = __hmul2_rn(h[j], sv2);
+          }
+          if (relu) {  // models.relu: x > 0 ? x : +0 (NaN -> 0)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const unsigned mk = __hgt2_mask(h[j], z2);
+              h[j] = __halves2half2(__ushort_as_half((unsigned short)(__half_as_ushort(__low2half(h[j])) & mk)),
+                                    __ushort_as_half((unsigned short)(__half_as_ushort(__high2half(h[j])) & (mk >> 16))));
+            }
+          }
+          if (tstore) {
+            // 64-column boxes of 128 rows x 128 B, 16-byte chunk c of row r at c ^ (r & 7)
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              const int c = c0 / 8 + hh;
+              unsigned char* dst = sbuf + (c / 8) * (kTcBM * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4);
+              *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(&h[4 * hh]);
+            }
+          } else {
+            reinterpret_cast<uint4*>(srow + c0 * 2)[0] = *reinterpret_cast<const uint4*>(&h[0]);
+            reinterpret_cast<uint4*>(srow + c0 * 2)[1] = *reinterpret_cast<const uint4*>(&h[4]);
+          }
         }
-      }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&tempty[a]);  // accumulator drained: the MMA warp may reuse it
       if (tstore) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> TMA
-        epi_bar();
+        epi_bar_n(kEpiThreads);
         if (et == 0) {
 #pragma unroll
           for (int bx = 0; bx < N / 64; ++bx)
@@ -321,16 +346,16 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
       } else {
-        epi_bar();
+        epi_bar_n(kEpiThreads);
         // coalesced write-back of the live rows: 16-byte chunks, row-major
         const int rows = (int)((m - m0) < kTcBM ? (m - m0) : kTcBM);
         const int CPR = n_out / 8;  // n_out <= N: columns past n_out are padding
-        for (int ch = et; ch < rows * CPR; ch += 128) {
+        for (int ch = et; ch < rows * CPR; ch += kEpiThreads) {
           const int rr = ch / CPR, c8 = ch - rr * CPR;
           *reinterpret_cast<uint4*>(out + (m0 + rr) * ldo + c8 * 8) =
               *reinterpret_cast<const uint4*>(sbuf + rr * C::kPitch + c8 * 16);
         }
-        epi_bar();
+        epi_bar_n(kEpiThreads);
       }
     }
     if (tstore && et == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -398,7 +423,7 @@ static int launch_gemm_tc_v(const CUtensorMap& ma, const CUtensorMap& mb, const 
   if (cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const unsigned grid = (unsigned)(tiles < sms ? tiles : sms);
-  k_gemm_tc<N, RESB><<<grid, 192, smem, st>>>(
+  k_gemm_tc<N, RESB><<<grid, kTcThreads, smem, st>>>(
       ma, mb, mo, m, num_kb, (const __half*)bias, (const __half*)row_scale, (__half*)out, ldo, relu,
       n_out);
   HG_LAUNCHED();
@@ -436,8 +461,9 @@ static int launch_gemm_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CU
 // TMA boxes with 128-byte swizzle are exactly the canonical MN-major SW128
 // atoms (8 K-rows of 128 B, 1024 B apart; the next 64 MN elements one box on).
 // Bound by reading A and B once from HBM.
-constexpr int kWgBK = 32;                         // K rows per slab
-constexpr uint32_t kWgBox = 64 * kWgBK * 2;       // one 64 (MN) x 32 (K) fp16 box
+// K rows per slab: 32, 64 or 128 (the deepest that leaves >= 3 ring stages);
+// one TMA box = 64 (MN) x bk (K) fp16 = 128 * bk bytes
+constexpr uint32_t kWgOnes = 4096;                // all-ones A tile: 2 x 16 K-rows x 128 B
 constexpr int kWgMaxMT = 8;                       // 128-row M tiles per CTA
 
 // MN-major, 128-byte-swizzled operand: LBO = next 64-element MN block,
@@ -456,7 +482,8 @@ template <int NB>
 __global__ void __launch_bounds__(192, 1)
 k_gemm_wgrad(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
              int64_t m, int n, int mt_total, int mt_group, int64_t slabs, int64_t slabs_per_split,
-             int splits, int stages, uint32_t tmem_cols, int with_bias, float* __restrict__ part) {
+             int splits, int stages, int bk, int a_boxes, uint32_t tmem_cols, int with_bias,
+             float* __restrict__ part) {
   constexpr int UN = 64 * NB;  // UMMA N
   // f16 x f16 -> f32, A and B MN-major, M = 128, N = UN
   constexpr uint32_t kIdesc = (1u << 4) | (1u << 15) | (1u << 16) | ((uint32_t)(UN >> 3) << 17) |
@@ -467,22 +494,29 @@ k_gemm_wgrad(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ 
   const int group = blockIdx.x / splits, split = blockIdx.x - group * splits;
   const int t0 = group * mt_group;
   const int mt = min(mt_group, mt_total - t0);
-  const uint32_t stage_bytes = (uint32_t)(2 * mt_group + NB) * kWgBox;
-  unsigned char* ones = base + (size_t)stages * stage_bytes;  // [2][kWgBox] of 1.0
-  uint64_t* full = reinterpret_cast<uint64_t*>(ones + 2 * kWgBox);
+  const uint32_t box = 128u * (uint32_t)bk;
+  // a stage: a_boxes A half-tiles (64 M columns each; halves wholly past M are
+  // neither loaded nor stored: their MMA rows only feed output rows >= M,
+  // which are dropped) then NB boxes of B
+  const uint32_t stage_bytes = (uint32_t)(a_boxes + NB) * box;
+  unsigned char* ones = base + (size_t)stages * stage_bytes;  // kWgOnes bytes of 1.0
+  uint64_t* full = reinterpret_cast<uint64_t*>(ones + kWgOnes);
   uint64_t* empty = full + stages;
   uint64_t* tfull = empty + stages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
-  const int64_t kb0 = (int64_t)split * slabs_per_split;
-  const int64_t nkb = min(slabs_per_split, slabs - kb0);
+  // slabs split, split + splits, ...: the CTAs sweep A and B together, front
+  // to back (one moving window of DRAM pages instead of a stream per CTA)
+  const int64_t nkb = split < slabs ? (slabs - split + splits - 1) / splits : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // the bias accumulator: rows of the all-ones tile times B = column sums of B
   const bool bias_acc = with_bias && group == 0;
   if (bias_acc) {
-    for (int i = threadIdx.x; i < (int)(2 * kWgBox / 16); i += blockDim.x)
+    for (int i = threadIdx.x; i < (int)(kWgOnes / 16); i += blockDim.x)
       reinterpret_cast<uint4*>(ones)[i] = make_uint4(0x3C003C00u, 0x3C003C00u, 0x3C003C00u, 0x3C003C00u);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
   }
+  const int64_t lh = (m - (int64_t)t0 * kTcBM + 63) / 64;
+  const int live_halves = lh < 2 * mt ? (int)lh : 2 * mt;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // ones tile -> tensor core
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
@@ -506,45 +540,42 @@ k_gemm_wgrad(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ 
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {  // TMA producer: per slab, mt tiles x 2 boxes of A and NB boxes of B
+    if (lane == 0) {  // TMA producer: per slab, the live A half-tiles and NB boxes of B
+      int s = 0;
+      uint32_t ph = 0;
       for (int64_t it = 0; it < nkb; ++it) {
-        const int s = (int)(it % stages);
-        mbar_wait(&empty[s], (uint32_t)((it / stages) & 1) ^ 1);
-        mbar_expect_tx(&full[s], (uint32_t)(2 * mt + NB) * kWgBox);
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_expect_tx(&full[s], (uint32_t)(live_halves + NB) * box);
         unsigned char* st = base + (size_t)s * stage_bytes;
-        const int krow = (int)((kb0 + it) * kWgBK);
-        for (int t = 0; t < mt; ++t)
-          for (int h = 0; h < 2; ++h)
-            tma_load_2d(st + (2 * t + h) * kWgBox, &map_a, &full[s], (t0 + t) * kTcBM + 64 * h, krow);
+        const int krow = (int)((split + it * splits) * bk);
+        for (int hb = 0; hb < live_halves; ++hb)
+          tma_load_2d(st + hb * box, &map_a, &full[s], t0 * kTcBM + 64 * hb, krow);
         for (int b = 0; b < NB; ++b)
-          tma_load_2d(st + (2 * mt_group + b) * kWgBox, &map_b, &full[s], 64 * b, krow);
+          tma_load_2d(st + (a_boxes + b) * box, &map_b, &full[s], 64 * b, krow);
+        if (++s == stages) { s = 0; ph ^= 1; }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
+      int s = 0;
+      uint32_t ph = 0;
       for (int64_t it = 0; it < nkb; ++it) {
-        const int s = (int)(it % stages);
-        mbar_wait(&full[s], (uint32_t)(it / stages) & 1);
+        mbar_wait(&full[s], ph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         unsigned char* st = base + (size_t)s * stage_bytes;
-        for (int t = 0; t < mt; ++t) {
-#pragma unroll
-          for (int k = 0; k < kWgBK / 16; ++k) {  // 16 K rows = 2 swizzle atoms = 2048 B
-            const uint64_t da = sw128_mnmajor_desc(st + 2 * t * kWgBox + k * 2048, kWgBox);
-            const uint64_t db = sw128_mnmajor_desc(st + 2 * mt_group * kWgBox + k * 2048, kWgBox);
-            umma_f16_f32(tmem + (uint32_t)(t * UN), da, db, kIdesc, (it | k) != 0);
-          }
-        }
-        if (bias_acc) {
-#pragma unroll
-          for (int k = 0; k < kWgBK / 16; ++k) {
-            const uint64_t da = sw128_mnmajor_desc(ones + k * 2048, kWgBox);
-            const uint64_t db = sw128_mnmajor_desc(st + 2 * mt_group * kWgBox + k * 2048, kWgBox);
-            umma_f16_f32(tmem + (uint32_t)(mt * UN), da, db, kIdesc, (it | k) != 0);
-          }
+        unsigned char* sbt = st + a_boxes * box;
+        for (int k = 0; k < bk / 16; ++k) {  // 16 K rows = 2 swizzle atoms = 2048 B
+          const uint64_t db = sw128_mnmajor_desc(sbt + k * 2048, box);
+          const uint32_t accum = (it | k) != 0;
+          for (int t = 0; t < mt; ++t)
+            umma_f16_f32(tmem + (uint32_t)(t * UN), sw128_mnmajor_desc(st + 2 * t * box + k * 2048, box),
+                         db, kIdesc, accum);
+          if (bias_acc)
+            umma_f16_f32(tmem + (uint32_t)(mt * UN), sw128_mnmajor_desc(ones, 2048), db, kIdesc, accum);
         }
         umma_commit(&empty[s]);
+        if (++s == stages) { s = 0; ph ^= 1; }
       }
       umma_commit(tfull);
     }
@@ -590,39 +621,65 @@ k_gemm_wgrad(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ 
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols));
 }
 
-// out[m, n] = rnd(sum_s part[s, m, n]) in split order; with accumulate,
+// out[m, n] = rnd(sum_s part[s, m, n]) in a fixed order; with accumulate,
 // out = rnd(out + that) (autograd's in-place gradient accumulation).
 // Partials are [splits][m + 1][n]; row m holds the bias column sums (written
-// to bias_out when it is non-null).
-__global__ void k_wgrad_reduce(const float* __restrict__ part, int splits, int64_t m, int n,
-                               __half* __restrict__ out, int64_t ldo, __half* __restrict__ bias_out,
-                               int accumulate) {
+// to bias_out when it is non-null).  Block = 32 float4 columns x kRedY split
+// lanes: lane y folds splits y, y + kRedY, ... in order, then the kRedY
+// partial sums are added in y order through shared memory (deterministic).
+constexpr int kRedY = 16;
+__global__ void __launch_bounds__(32 * kRedY)
+k_wgrad_reduce(const float* __restrict__ part, int splits, int64_t m, int n,
+               __half* __restrict__ out, int64_t ldo, __half* __restrict__ bias_out,
+               int accumulate) {
+  __shared__ float4 sh[kRedY][32];
   const int64_t n4 = n / 4;
   const int64_t total = (m + (bias_out ? 1 : 0)) * n4;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / n4, c = (i - r * n4) * 4;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int s = 0; s < splits; ++s) {
+  const int64_t i = (int64_t)blockIdx.x * 32 + threadIdx.x;
+  const int y = threadIdx.y;
+  const int64_t r = i / n4, c = (i - r * n4) * 4;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (i < total) {
+    for (int s = y; s < splits; s += kRedY) {
       const float4 v = __ldg(reinterpret_cast<const float4*>(part + ((int64_t)s * (m + 1) + r) * n + c));
       acc.x = __fadd_rn(acc.x, v.x);
       acc.y = __fadd_rn(acc.y, v.y);
       acc.z = __fadd_rn(acc.z, v.z);
       acc.w = __fadd_rn(acc.w, v.w);
     }
-    __half h[4] = {__float2half_rn(acc.x), __float2half_rn(acc.y), __float2half_rn(acc.z),
-                   __float2half_rn(acc.w)};
-    __half* o = r < m ? out + r * ldo + c : bias_out + c;
-    if (accumulate) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) h[j] = __hadd_rn(o[j], h[j]);
-    }
-    *reinterpret_cast<uint2*>(o) = *reinterpret_cast<const uint2*>(h);
   }
+  sh[y][threadIdx.x] = acc;
+  __syncthreads();
+  if (y != 0 || i >= total) return;
+#pragma unroll
+  for (int k = 1; k < kRedY; ++k) {
+    const float4 v = sh[k][threadIdx.x];
+    acc.x = __fadd_rn(acc.x, v.x);
+    acc.y = __fadd_rn(acc.y, v.y);
+    acc.z = __fadd_rn(acc.z, v.z);
+    acc.w = __fadd_rn(acc.w, v.w);
+  }
+  __half h[4] = {__float2half_rn(acc.x), __float2half_rn(acc.y), __float2half_rn(acc.z),
+                 __float2half_rn(acc.w)};
+  __half* o = r < m ? out + r * ldo + c : bias_out + c;
+  if (accumulate) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) h[j] = __hadd_rn(o[j], h[j]);
+  }
+  *reinterpret_cast<uint2*>(o) = *reinterpret_cast<const uint2*>(h);
+}
+
+static int launch_wgrad_reduce(const float* part, int splits, int64_t m, int n, void* out,
+                               int64_t ldo, void* bias_out, int accumulate, cudaStream_t st) {
+  const int64_t total = (m + (bias_out ? 1 : 0)) * (n / 4);
+  k_wgrad_reduce<<<(unsigned)((total + 31) / 32), dim3(32, kRedY), 0, st>>>(
+      part, splits, m, n, (__half*)out, ldo, (__half*)bias_out, accumulate);
+  HG_LAUNCHED();
+  return HG_OK;
 }
 
 struct WgradPlan {
-  int nb, mt_total, mt_group, groups, splits, stages;
+  int nb, mt_total, mt_group, groups, splits, stages, bk, a_boxes;
   int64_t slabs, sps;
   uint32_t tmem_cols;
   size_t smem, part_bytes;
@@ -630,6 +687,7 @@ struct WgradPlan {
 
 static WgradPlan wgrad_plan(int64_t k, int64_t m, int n, int sms) {
   WgradPlan p{};
+
   p.nb = (n + 63) / 64;
   p.mt_total = (int)((m + kTcBM - 1) / kTcBM);
   // TMEM: one 64*nb-column accumulator per tile, plus the bias accumulator
@@ -639,15 +697,30 @@ static WgradPlan wgrad_plan(int64_t k, int64_t m, int n, int sms) {
   const uint32_t cols = (uint32_t)((p.mt_group + 1) * 64 * p.nb);
   p.tmem_cols = 32;
   while (p.tmem_cols < cols) p.tmem_cols <<= 1;
-  p.slabs = (k + kWgBK - 1) / kWgBK;
-  // >= 16 slabs (512 rows) per split keeps the partials small next to A
-  int64_t want = std::max<int64_t>(1, std::min<int64_t>(sms / p.groups, (p.slabs + 15) / 16));
+  p.a_boxes = (int)std::min<int64_t>(2 * p.mt_group, (m + 63) / 64);
+  // narrow operands (<= 3 boxes per slab): two CTAs per SM -- one CTA's ring
+  // streams ~25 GB/s whatever its depth (C4 GIN dW: 171 -> 132 us); wide ones
+  // need the whole shared memory for depth.  HG_WG_CTAS overrides (A/B runs).
+  int cps = p.a_boxes + p.nb <= 3 ? 2 : 1;
+  if (const char* e = getenv("HG_WG_CTAS")) cps = std::max(1, atoi(e));
+  const uint32_t budget = (200u * 1024u) / (uint32_t)cps;
+  // deepest slab that keeps >= 3 stages in ~200 KB of shared memory
+  p.bk = 32;
+  for (int cand : {128, 64})
+    if ((uint32_t)(p.a_boxes + p.nb) * 128u * cand * 3 <= budget) { p.bk = cand; break; }
+  // measurement knobs (A/B runs only): HG_WG_BK = slab rows, HG_WG_STAGES = ring depth
+  if (const char* e = getenv("HG_WG_BK")) p.bk = atoi(e);
+  p.slabs = (k + p.bk - 1) / p.bk;
+  // >= 512 rows per split keeps the partials small next to A
+  const int64_t min_slabs = 512 / p.bk;
+  int64_t want = std::max<int64_t>(1, std::min<int64_t>(cps * sms / p.groups, (p.slabs + min_slabs - 1) / min_slabs));
   p.sps = (p.slabs + want - 1) / want;
   p.splits = (int)((p.slabs + p.sps - 1) / p.sps);
   if (p.splits < 1) p.splits = 1;
-  const uint32_t stage = (uint32_t)(2 * p.mt_group + p.nb) * kWgBox;
-  p.stages = (int)std::min<uint32_t>(8, (200u * 1024u) / stage);
-  p.smem = 1024 + (size_t)p.stages * stage + 2 * kWgBox + (2 * p.stages + 1) * 8 + 16;
+  const uint32_t stage = (uint32_t)(p.a_boxes + p.nb) * 128u * (uint32_t)p.bk;
+  p.stages = (int)std::min<uint32_t>(16, budget / stage);
+  if (const char* e = getenv("HG_WG_STAGES")) p.stages = std::min(p.stages, atoi(e));
+  p.smem = 1024 + (size_t)p.stages * stage + kWgOnes + (2 * p.stages + 1) * 8 + 16;
   p.part_bytes = align_up((size_t)p.splits * (size_t)(m + 1) * (size_t)n * sizeof(float));
   return p;
 }
@@ -665,7 +738,7 @@ static int launch_wgrad(const CUtensorMap& ma, const CUtensorMap& mb, const Wgra
   HG_CUDA(cudaFuncSetAttribute(k_gemm_wgrad<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)p.smem));
   k_gemm_wgrad<NB><<<p.groups * p.splits, 192, p.smem, st>>>(
-      ma, mb, m, n, p.mt_total, p.mt_group, p.slabs, p.sps, p.splits, p.stages, p.tmem_cols,
+      ma, mb, m, n, p.mt_total, p.mt_group, p.slabs, p.sps, p.splits, p.stages, p.bk, p.a_boxes, p.tmem_cols,
       with_bias, part);
   HG_LAUNCHED();
   return HG_OK;
@@ -737,10 +810,7 @@ extern "C" int hg_gemm_wgrad(const void* a, int64_t k, int64_t m, int64_t lda, c
              "hg_gemm_wgrad: M must be a multiple of 8 and pitches cover M / N (multiples of 8)");
   cudaStream_t st = as_stream(stream);
   if (k == 0) {  // empty sum: zeros (or out unchanged when accumulating)
-    k_wgrad_reduce<<<grid_for((m + 1) * (n / 4), 256, 4096), 256, 0, st>>>(
-        nullptr, 0, m, n, (__half*)out, ldo, (__half*)bias_out, accumulate);
-    HG_LAUNCHED();
-    return HG_OK;
+    return launch_wgrad_reduce(nullptr, 0, m, n, out, ldo, bias_out, accumulate, st);
   }
   HG_REQUIRE(a && b, "hg_gemm_wgrad: null operand");
   HG_REQUIRE(((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0 &&
@@ -754,10 +824,10 @@ extern "C" int hg_gemm_wgrad(const void* a, int64_t k, int64_t m, int64_t lda, c
   HG_CUDA(cudaSetDevice(dev));
   CUtensorMap ma, mb;
   // A = x [k rows, m cols]: boxes of 64 columns x 32 rows; B = g [k, n] likewise
-  HG_REQUIRE(make_map_box(&ma, a, k, m, lda, 64, kWgBK),
+  HG_REQUIRE(make_map_box(&ma, a, k, m, lda, 64, (uint32_t)p.bk),
              "hg_gemm_wgrad: cuTensorMapEncodeTiled(A [%lld x %lld]) failed: %d", (long long)k,
              (long long)m, g_tma_err);
-  HG_REQUIRE(make_map_box(&mb, b, k, n, ldb, 64, kWgBK),
+  HG_REQUIRE(make_map_box(&mb, b, k, n, ldb, 64, (uint32_t)p.bk),
              "hg_gemm_wgrad: cuTensorMapEncodeTiled(B [%lld x %d]) failed: %d", (long long)k, n,
              g_tma_err);
   float* part = static_cast<float*>(ws);
@@ -769,8 +839,5 @@ extern "C" int hg_gemm_wgrad(const void* a, int64_t k, int64_t m, int64_t lda, c
     default: rc = launch_wgrad<4>(ma, mb, p, m, n, bias_out != nullptr, part, st); break;
   }
   if (rc != HG_OK) return rc;
-  k_wgrad_reduce<<<grid_for((m + 1) * (n / 4), 256, 4096), 256, 0, st>>>(
-      part, p.splits, m, n, (__half*)out, ldo, (__half*)bias_out, accumulate);
-  HG_LAUNCHED();
-  return HG_OK;
+  return launch_wgrad_reduce(part, p.splits, m, n, out, ldo, bias_out, accumulate, st);
 }
