@@ -340,6 +340,33 @@ int hg_gat_attention_fwd(const int64_t* offsets, const int32_t* cols, int64_t n_
                          int64_t n_medium, const int32_t* long_rows, int64_t n_long,
                          int32_t short_max, int dtype, void* stream);
 
+/* The first pass of hg_gat_attention_fwd alone: stats[(r, h)] = (m, 1/s), the
+ * log2-domain row max and reciprocal exp-sum of leaky(s_l[r] + s_r[c]) (float
+ * pairs, 8-byte aligned, [n_rows, heads]) -- what hg_gat_aggregate needs to
+ * form alpha = rnd(exp2(l - m) * (1/s)) bit for bit as hg_gat_attention_fwd. */
+int hg_gat_attention_stats(const int64_t* offsets, const int32_t* cols, int64_t n_rows,
+                           const void* s_l, const void* s_r, int32_t heads, float slope,
+                           float* stats, const int32_t* medium_rows, int64_t n_medium,
+                           const int32_t* long_rows, int64_t n_long, int32_t short_max,
+                           int dtype, void* stream);
+
+/* Fused GAT layer core, forward (attention_scores -> leaky_relu -> edge_softmax
+ * -> spmm_weighted, models.py:317-412 + 293-314, in one row-owned pass over
+ * the hg_spmm schedule): y[r] = sum_e alpha_e * x[c_e] per head (fp32,
+ * [relu]), alpha_e computed in the gather loop from s_l[r], s_r[c_e] and
+ * stats (hg_gat_attention_stats) and written to alpha_out [E, heads] for the
+ * backward.  Bit-identical to hg_gat_attention_fwd + hg_spmm(w = alpha) on
+ * the same schedule; no E x heads array is read.  Workspace: as hg_spmm with
+ * in_scale = 0 and no second values. */
+int hg_gat_aggregate(const int64_t* offsets, const int32_t* cols, int64_t n_rows, int64_t n_cols,
+                     int64_t num_edges, const int32_t* units, int64_t num_units,
+                     const int32_t* split_rows, int64_t num_split_rows, int64_t num_slots,
+                     const int32_t* packs, int64_t num_packs, const int32_t* pack_rowid,
+                     const void* s_l, const void* s_r, const float* stats, float slope,
+                     void* alpha_out, int32_t heads, const void* x, void* y, int32_t F,
+                     int64_t ldx, int64_t ldy, int32_t relu, int dtype, void* ws,
+                     size_t ws_bytes, void* stream);
+
 /* Backward of the above (models.py:188-200, 329-333, 403-410): per row,
  * D = sum alpha*dalpha (fp32); de[e, h] = rnd(alpha (dalpha - D) * leaky'(l_e));
  * ds_l[r, h] = rnd(sum_e of the unrounded de).  alpha and de rows are ae_ld

@@ -101,7 +101,7 @@ __device__ __forceinline__ void fwd_pass2(const int32_t* __restrict__ cols, cons
                        : 0.0f;
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (c[u] >= 0) alpha[(e0 + u * step) * ald + h] = Num<T>::from_f(exp2f(v[u] - m) * inv);
+      if (c[u] >= 0) alpha[(e0 + u * step) * ald + h] = Num<T>::from_f(ex2_neg(v[u] - m) * inv);
   }
 }
 
@@ -182,7 +182,7 @@ template <typename T, int H>
 __device__ __forceinline__ void
 d_gat_fwd_thread(int64_t blk, int64_t nblk, const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
                  int64_t n_rows, const T* __restrict__ sl, const T* __restrict__ sr, float slope,
-                 T* __restrict__ alpha, int short_max, int ald) {
+                 T* __restrict__ alpha, int short_max, int ald, float2* __restrict__ stats) {
   const int64_t t = blk * (int64_t)blockDim.x + threadIdx.x;
   if (t >= n_rows * H) return;
   const int64_t r = t / H;
@@ -208,10 +208,14 @@ d_gat_fwd_thread(int64_t blk, int64_t nblk, const int64_t* __restrict__ offsets,
     float s1 = 0.0f;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      p[u] = c[u] >= 0 ? exp2f(v[u] - mu) : 0.0f;
+      p[u] = c[u] >= 0 ? ex2_neg(v[u] - mu) : 0.0f;
       if (c[u] >= 0) s1 += p[u];
     }
     const float inv = 1.0f / s1;
+    if (stats) {  // hg_gat_attention_stats: alpha = rnd(exp2(l - m) * inv) later, in hg_gat_aggregate
+      stats[t] = make_float2(mu, inv);
+      return;
+    }
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (c[u] >= 0) alpha[(beg + u) * ald + h] = Num<T>::from_f(p[u] * inv);
@@ -219,6 +223,10 @@ d_gat_fwd_thread(int64_t blk, int64_t nblk, const int64_t* __restrict__ offsets,
   }
   float m = -INFINITY, s = 0.0f;
   fwd_pass1<T, H>(cols, sr, beg, end, 1, h, a, slope, m, s);
+  if (stats) {
+    stats[t] = make_float2(m, 1.0f / s);
+    return;
+  }
   fwd_pass2<T, H>(cols, sr, beg, end, 1, h, a, slope, m, 1.0f / s, alpha, ald);
 }
 
@@ -226,7 +234,8 @@ template <typename T, int H>
 __device__ __forceinline__ void
 d_gat_fwd_warp(int64_t blk, int64_t nblk, const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
                const int32_t* __restrict__ rows, int64_t n_list, const T* __restrict__ sl,
-               const T* __restrict__ sr, float slope, T* __restrict__ alpha, int ald) {
+               const T* __restrict__ sr, float slope, T* __restrict__ alpha, int ald,
+               float2* __restrict__ stats) {
   constexpr int EPB = 32 / H;
   const int lane = threadIdx.x & 31, j = lane / H, h = lane % H;
   const int64_t nwarps = (int64_t)nblk * (blockDim.x >> 5);
@@ -238,6 +247,10 @@ d_gat_fwd_warp(int64_t blk, int64_t nblk, const int64_t* __restrict__ offsets, c
     float m = -INFINITY, s = 0.0f;
     fwd_pass1<T, H>(cols, sr, beg + j, end, EPB, h, a, slope, m, s);
     ms_warp<H>(m, s);
+    if (stats) {
+      if (j == 0) stats[r * H + h] = make_float2(m, 1.0f / s);
+      continue;
+    }
     fwd_pass2<T, H>(cols, sr, beg + j, end, EPB, h, a, slope, m, 1.0f / s, alpha, ald);
   }
 }
@@ -246,7 +259,8 @@ template <typename T, int H>
 __device__ __forceinline__ void
 d_gat_fwd_cta(int64_t blk, int64_t nblk, const int64_t* __restrict__ offsets, const int32_t* __restrict__ cols,
               const int32_t* __restrict__ rows, const T* __restrict__ sl,
-              const T* __restrict__ sr, float slope, T* __restrict__ alpha, int ald) {
+              const T* __restrict__ sr, float slope, T* __restrict__ alpha, int ald,
+              float2* __restrict__ stats) {
   constexpr int EPB = 256 / H;
   __shared__ float sm[8][H], ss[8][H];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, j = tid / H, h = tid % H;
@@ -261,6 +275,10 @@ d_gat_fwd_cta(int64_t blk, int64_t nblk, const int64_t* __restrict__ offsets, co
   float mt = sm[0][h], st = ss[0][h];
 #pragma unroll
   for (int k = 1; k < 8; ++k) ms_merge(mt, st, sm[k][h], ss[k][h]);
+  if (stats) {
+    if (j == 0) stats[r * H + h] = make_float2(mt, 1.0f / st);
+    return;
+  }
   fwd_pass2<T, H>(cols, sr, beg + j, end, EPB, h, a, slope, mt, 1.0f / st, alpha, ald);
 }
 
@@ -421,16 +439,16 @@ k_gat_fwd_all(const int64_t* __restrict__ offsets, const int32_t* __restrict__ c
               int64_t n_rows, const int32_t* __restrict__ medium, int64_t n_medium,
               const int32_t* __restrict__ longr, int64_t n_long, int64_t b_med,
               const T* __restrict__ sl, const T* __restrict__ sr, float slope,
-              T* __restrict__ alpha, int short_max, int ald) {
+              T* __restrict__ alpha, int short_max, int ald, float2* __restrict__ stats) {
   int64_t b = blockIdx.x;
   if (b < n_long)
-    return d_gat_fwd_cta<T, H>(b, n_long, offsets, cols, longr, sl, sr, slope, alpha, ald);
+    return d_gat_fwd_cta<T, H>(b, n_long, offsets, cols, longr, sl, sr, slope, alpha, ald, stats);
   b -= n_long;
   if (b < b_med)
     return d_gat_fwd_warp<T, H>(b, b_med, offsets, cols, medium, n_medium, sl, sr, slope, alpha,
-                                ald);
+                                ald, stats);
   b -= b_med;
-  d_gat_fwd_thread<T, H>(b, 0, offsets, cols, n_rows, sl, sr, slope, alpha, short_max, ald);
+  d_gat_fwd_thread<T, H>(b, 0, offsets, cols, n_rows, sl, sr, slope, alpha, short_max, ald, stats);
 }
 
 template <typename T, int H>
@@ -578,10 +596,11 @@ static inline unsigned all_blocks(const GatRows& g, int H) {
 }
 
 template <typename T, int H>
-static void gat_fwd(const GatRows& g, const void* sl, const void* sr, float slope, void* alpha) {
+static void gat_fwd(const GatRows& g, const void* sl, const void* sr, float slope, void* alpha,
+                    float2* stats) {
   k_gat_fwd_all<T, H><<<all_blocks(g, H), 256, 0, g.st>>>(
       g.offsets, g.cols, g.n_rows, g.medium, g.n_medium, g.longr, g.n_long, med_blocks(g),
-      (const T*)sl, (const T*)sr, slope, (T*)alpha, g.short_max, g.ald);
+      (const T*)sl, (const T*)sr, slope, (T*)alpha, g.short_max, g.ald, stats);
 }
 
 template <typename T, int H>
@@ -635,8 +654,26 @@ extern "C" int hg_gat_attention_fwd(const int64_t* offsets, const int32_t* cols,
   if (n_rows == 0) return HG_OK;
   GatRows g{offsets, cols, n_rows, medium_rows, n_medium, long_rows, n_long, short_max,
             as_stream(stream), (int)(alpha_ld ? alpha_ld : heads)};
-  if (dtype == HG_F16) { HG_GAT_HEADS(gat_fwd, __half, g, s_l, s_r, slope, alpha) }
-  else { HG_GAT_HEADS(gat_fwd, float, g, s_l, s_r, slope, alpha) }
+  if (dtype == HG_F16) { HG_GAT_HEADS(gat_fwd, __half, g, s_l, s_r, slope, alpha, nullptr) }
+  else { HG_GAT_HEADS(gat_fwd, float, g, s_l, s_r, slope, alpha, nullptr) }
+  HG_LAUNCHED();
+  return HG_OK;
+}
+
+extern "C" int hg_gat_attention_stats(const int64_t* offsets, const int32_t* cols, int64_t n_rows,
+                                      const void* s_l, const void* s_r, int32_t heads, float slope,
+                                      float* stats, const int32_t* medium_rows, int64_t n_medium,
+                                      const int32_t* long_rows, int64_t n_long, int32_t short_max,
+                                      int dtype, void* stream) {
+  int rc = gat_rows_check(heads, dtype, n_medium, medium_rows, n_long, long_rows, short_max);
+  if (rc) return rc;
+  if (n_rows == 0) return HG_OK;
+  HG_REQUIRE(stats && (reinterpret_cast<uintptr_t>(stats) & 7) == 0, "hg_gat_attention_stats: stats must be 8-byte aligned");
+  GatRows g{offsets, cols, n_rows, medium_rows, n_medium, long_rows, n_long, short_max,
+            as_stream(stream), heads};
+  float2* st = reinterpret_cast<float2*>(stats);
+  if (dtype == HG_F16) { HG_GAT_HEADS(gat_fwd, __half, g, s_l, s_r, slope, nullptr, st) }
+  else { HG_GAT_HEADS(gat_fwd, float, g, s_l, s_r, slope, nullptr, st) }
   HG_LAUNCHED();
   return HG_OK;
 }

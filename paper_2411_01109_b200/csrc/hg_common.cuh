@@ -123,6 +123,15 @@ struct Num<float> {
   static __device__ __forceinline__ float hi(float2 v) { return v.y; }
 };
 
+// 2^x for x <= 0 as one MUFU.EX2 (flush-to-zero).  Equal to exp2f for every
+// x >= -126; below, both are < 2^-126 and every use (alpha = 2^(l - m) / s with
+// s >= 1, rounded to binary16) rounds them to zero alike.
+__device__ __forceinline__ float ex2_neg(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // Largest r with offsets[r] <= e (offsets non-decreasing, n+1 entries, e < offsets[n]).
 __device__ __forceinline__ int64_t row_of_edge(const int64_t* __restrict__ offsets, int64_t n,
                                                int64_t e) {

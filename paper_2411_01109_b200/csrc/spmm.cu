@@ -230,8 +230,14 @@ struct TeamShape {
   static constexpr int TPW = 32 / TEAM;  // teams per warp
 };
 
+// ATT: the edge weight is the GAT attention coefficient, computed in the
+// gather loop from the column's s_r (loaded through the weight path with the
+// column id as index) and the row's (s_l, m, 1/sum) -- bit for bit the alpha
+// hg_gat_attention_fwd writes -- and stored by one lane per head.
+constexpr float kAttLog2e = 1.4426950408889634f;  // = gat_fast.cu kLog2e
+
 template <typename T, int V, int TEAM, int NCH, bool WEIGHTED, bool SUMW = false,
-          bool PK = false>
+          bool PK = false, bool ATT = false>
 struct FastTeam {
   static constexpr bool P2 = TeamShape<TEAM>::P2;
   // edges gathered per batch (packed teams: 4, the rolled accumulate shifts
@@ -266,6 +272,35 @@ struct FastTeam {
   T* pout2;
   int pldy, pfmode;
   bool plead;
+  // ATT state: the row's log2-domain s_l, running max and 1/sum per chunk
+  const T* asl;
+  const float2* astats;
+  T* aout;
+  float aslope;
+  float aa[NCH], am[NCH], ainv[NCH];
+  bool alead[NCH];
+
+  __device__ __forceinline__ void load_att(int r) {
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) {
+      if (cval[k]) {
+        const int64_t i = (int64_t)r * heads + chead[k];
+        aa[k] = Num<T>::to_f(asl[i]) * kAttLog2e;
+        const float2 st = astats[i];
+        am[k] = st.x;
+        ainv[k] = st.y;
+      }
+    }
+  }
+
+  // alpha of edge e for chunk k from its column's s_r (gat_fast.cu fwd_pass2)
+  __device__ __forceinline__ T att_weight(int k, T srv, int e) const {
+    float v = fmaf(Num<T>::to_f(srv), kAttLog2e, aa[k]);
+    v = v > 0.0f ? v : v * aslope;
+    const T a = Num<T>::from_f(ex2_neg(v - am[k]) * ainv[k]);
+    if (alead[k]) aout[(int64_t)e * heads + chead[k]] = a;
+    return a;
+  }
 
   __device__ __forceinline__ void store_row() {
 #pragma unroll
@@ -286,6 +321,7 @@ struct FastTeam {
       if (prow >= 0) store_row();
       prow = r;
       pfo = pfout ? pfout[r] : Num<T>::zero();
+      if (ATT) load_att(r);
     }
   }
 
@@ -318,6 +354,7 @@ struct FastTeam {
       const int c = shfl_id(ids, j);
       int wi = b + j;
       if (WEIGHTED && use_widx) wi = shfl_id(wids, j);
+      if (ATT) wi = c;  // s_r[c, head]
       const size_t roff = (size_t)(unsigned)c * (unsigned)ldx;
 #pragma unroll
       for (int k = 0; k < NCH; ++k) {
@@ -343,7 +380,7 @@ struct FastTeam {
 #pragma unroll
           for (int k = 0; k < NCH; ++k) {
             if (cval[k]) {
-              if (WEIGHTED) acc_fma<T, V>(acc[k], wv[0][k], raw[0][k]);
+              if (WEIGHTED) acc_fma<T, V>(acc[k], ATT ? att_weight(k, wv[0][k], b + j) : wv[0][k], raw[0][k]);
               else acc_add<T, V>(acc[k], raw[0][k]);
             }
           }
@@ -371,7 +408,7 @@ struct FastTeam {
 #pragma unroll
       for (int k = 0; k < NCH; ++k) {
         if (ok && cval[k]) {
-          if (WEIGHTED) acc_fma<T, V>(acc[k], wv[j][k], raw[j][k]);
+          if (WEIGHTED) acc_fma<T, V>(acc[k], ATT ? att_weight(k, wv[j][k], b + j) : wv[j][k], raw[j][k]);
           else acc_add<T, V>(acc[k], raw[j][k]);
         }
       }
@@ -384,7 +421,7 @@ struct FastTeam {
 // of consecutive short rows (hg_schedule_build), each row stored as the edge
 // stream crosses its end.
 template <typename T, int V, int TEAM, int NCH, bool WEIGHTED, bool SUMW = false,
-          bool PACKED = false>
+          bool PACKED = false, bool ATT = false>
 __global__ void __launch_bounds__(256, (PACKED && NCH == 1 && V * sizeof(T) <= 16)
                                            ? 4
                                            : FastOcc<TEAM, NCH, WEIGHTED, V * sizeof(T)>::value)
@@ -394,8 +431,9 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
             float* __restrict__ carry, int F, int ldx, int ldy, int fmode,
             const T* __restrict__ fout, int wld, int w2off, T* __restrict__ out2,
             float* __restrict__ carry2, const int64_t* __restrict__ offsets,
-            const int32_t* __restrict__ rowid) {
-  using Team = FastTeam<T, V, TEAM, NCH, WEIGHTED, SUMW, PACKED>;
+            const int32_t* __restrict__ rowid, const T* __restrict__ att_sl,
+            const float2* __restrict__ att_stats, T* __restrict__ att_out, float att_slope) {
+  using Team = FastTeam<T, V, TEAM, NCH, WEIGHTED, SUMW, PACKED, ATT>;
   constexpr int EB = Team::EB;
   constexpr int CPL = Team::CPL;
   constexpr bool P2 = Team::P2;
@@ -436,6 +474,15 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
     for (int i = 0; i < V; ++i) t.acc[k][i] = 0.0f;
   }
   const bool lead = t.cval[0] && (tl * V) % fh == 0;  // SUMW: first lane of its head
+  if constexpr (ATT) {
+    t.asl = att_sl;
+    t.astats = att_stats;
+    t.aout = att_out;
+    t.aslope = att_slope;
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) t.alead[k] = t.cval[k] && ((tl + k * TEAM) * V) % fh == 0;
+    if (!PACKED) t.load_att(row);
+  }
   if constexpr (PACKED) {
     t.prow = -1;
     t.pfo = Num<T>::zero();
@@ -611,31 +658,37 @@ struct FastArgs {
   int wld, w2off;
   void* out2;
   float* carry2;
+  const void* att_sl;      // ATT (hg_gat_aggregate): s_l, per-row (m, 1/sum), alpha out
+  const float2* att_stats;
+  void* att_out;
+  float att_slope;
   cudaStream_t st;
 };
 
 template <int X> struct Pow2Up { static constexpr int value = X <= 1 ? 1 : 2 * Pow2Up<(X + 1) / 2>::value; };
 template <> struct Pow2Up<1> { static constexpr int value = 1; };
 
-template <typename T, int V, int TEAM, int NCH, bool WT, bool SUMW = false>
+template <typename T, int V, int TEAM, int NCH, bool WT, bool SUMW = false, bool ATT = false>
 static int launch_fast(const FastArgs& a) {
   constexpr int kThreads = 256;
   constexpr int teams_per_block = (kThreads / 32) * TeamShape<TEAM>::TPW;
   constexpr int TEAMF = Pow2Up<TEAM>::value;  // follow-up pass: power-of-two teams
   if (a.num_units > 0) {
     int64_t blocks = (a.num_units + teams_per_block - 1) / teams_per_block;
-    k_spmm_fast<T, V, TEAM, NCH, WT, SUMW><<<(unsigned)blocks, kThreads, 0, a.st>>>(
+    k_spmm_fast<T, V, TEAM, NCH, WT, SUMW, false, ATT><<<(unsigned)blocks, kThreads, 0, a.st>>>(
         a.units, a.num_units, a.cols, a.num_edges, (const T*)a.w, a.widx, a.heads, a.fh,
         (const T*)a.x, (T*)a.y, a.carry, a.F, a.ldx, a.ldy, a.fmode, (const T*)a.fout,
-        a.wld, a.w2off, (T*)a.out2, a.carry2, a.offsets, nullptr);
+        a.wld, a.w2off, (T*)a.out2, a.carry2, a.offsets, nullptr, (const T*)a.att_sl,
+        a.att_stats, (T*)a.att_out, a.att_slope);
     HG_LAUNCHED();
   }
   if (a.num_packs > 0) {
     int64_t blocks = (a.num_packs + teams_per_block - 1) / teams_per_block;
-    k_spmm_fast<T, V, TEAM, NCH, WT, SUMW, true><<<(unsigned)blocks, kThreads, 0, a.st>>>(
+    k_spmm_fast<T, V, TEAM, NCH, WT, SUMW, true, ATT><<<(unsigned)blocks, kThreads, 0, a.st>>>(
         a.packs, a.num_packs, a.cols, a.num_edges, (const T*)a.w, a.widx, a.heads, a.fh,
         (const T*)a.x, (T*)a.y, nullptr, a.F, a.ldx, a.ldy, a.fmode, (const T*)a.fout,
-        a.wld, a.w2off, (T*)a.out2, nullptr, a.offsets, a.rowid);
+        a.wld, a.w2off, (T*)a.out2, nullptr, a.offsets, a.rowid, (const T*)a.att_sl,
+        a.att_stats, (T*)a.att_out, a.att_slope);
     HG_LAUNCHED();
   }
   if (a.num_split > 0) {
@@ -671,7 +724,7 @@ static int dispatch_sumw(const FastArgs& a) {
   return launch_fast<T, V, 32, 1, true, true>(a);
 }
 
-template <typename T, int V, bool WT>
+template <typename T, int V, bool WT, bool ATT = false>
 static int dispatch_layout(const FastArgs& a) {
   const int nvec = a.F / V;
   // Teams stay power-of-two lane groups even when some lanes idle (F=48: 6 of
@@ -679,28 +732,28 @@ static int dispatch_layout(const FastArgs& a) {
   // wavefronts, and a team straddling two quarters doubles the L1 data-pipe
   // wavefronts (ncu, profiles/r01: 7-lane teams ran 27% slower than 8-lane
   // teams at the same L2 sector count).
-  if (nvec <= 1) return launch_fast<T, V, 1, 1, WT>(a);
-  if (nvec <= 2) return launch_fast<T, V, 2, 1, WT>(a);
-  if (nvec <= 4) return launch_fast<T, V, 4, 1, WT>(a);
-  if (nvec <= 8) return launch_fast<T, V, 8, 1, WT>(a);
-  if (nvec <= 16) return launch_fast<T, V, 16, 1, WT>(a);
-  if (nvec <= 32) return launch_fast<T, V, 32, 1, WT>(a);
-  if (nvec <= 64) return launch_fast<T, V, 32, 2, WT>(a);
-  if (nvec <= 128) return launch_fast<T, V, 32, 4, WT>(a);
-  if (nvec <= 256) return launch_fast<T, V, 32, 8, WT>(a);
+  if (nvec <= 1) return launch_fast<T, V, 1, 1, WT, false, ATT>(a);
+  if (nvec <= 2) return launch_fast<T, V, 2, 1, WT, false, ATT>(a);
+  if (nvec <= 4) return launch_fast<T, V, 4, 1, WT, false, ATT>(a);
+  if (nvec <= 8) return launch_fast<T, V, 8, 1, WT, false, ATT>(a);
+  if (nvec <= 16) return launch_fast<T, V, 16, 1, WT, false, ATT>(a);
+  if (nvec <= 32) return launch_fast<T, V, 32, 1, WT, false, ATT>(a);
+  if (nvec <= 64) return launch_fast<T, V, 32, 2, WT, false, ATT>(a);
+  if (nvec <= 128) return launch_fast<T, V, 32, 4, WT, false, ATT>(a);
+  if (nvec <= 256) return launch_fast<T, V, 32, 8, WT, false, ATT>(a);
   HG_REQUIRE(false, "hg_spmm: feature length %d too large", a.F);
 }
 
 // 32-byte lanes (binary16 x 16), single chunk per lane: F <= 512.
-template <typename T, bool WT>
+template <typename T, bool WT, bool ATT = false>
 static int dispatch_layout32(const FastArgs& a) {
   const int nvec = a.F / 16;
-  if (nvec <= 1) return launch_fast<T, 16, 1, 1, WT>(a);
-  if (nvec <= 2) return launch_fast<T, 16, 2, 1, WT>(a);
-  if (nvec <= 4) return launch_fast<T, 16, 4, 1, WT>(a);
-  if (nvec <= 8) return launch_fast<T, 16, 8, 1, WT>(a);
-  if (nvec <= 16) return launch_fast<T, 16, 16, 1, WT>(a);
-  return launch_fast<T, 16, 32, 1, WT>(a);
+  if (nvec <= 1) return launch_fast<T, 16, 1, 1, WT, false, ATT>(a);
+  if (nvec <= 2) return launch_fast<T, 16, 2, 1, WT, false, ATT>(a);
+  if (nvec <= 4) return launch_fast<T, 16, 4, 1, WT, false, ATT>(a);
+  if (nvec <= 8) return launch_fast<T, 16, 8, 1, WT, false, ATT>(a);
+  if (nvec <= 16) return launch_fast<T, 16, 16, 1, WT, false, ATT>(a);
+  return launch_fast<T, 16, 32, 1, WT, false, ATT>(a);
 }
 
 template <typename T>
@@ -709,15 +762,18 @@ static int dispatch_fast(const FastArgs& a) {
   const bool aligned = (reinterpret_cast<uintptr_t>(a.x) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(a.y) % 16 == 0);
   const bool big = aligned && (a.fh % VB == 0) && a.ldx % VB == 0 && a.ldy % VB == 0;
+  const bool att = a.att_stats != nullptr;
   if constexpr (sizeof(T) == 2) {
     const bool a32 = (reinterpret_cast<uintptr_t>(a.x) % 32 == 0) &&
                      (reinterpret_cast<uintptr_t>(a.y) % 32 == 0) && a.fh % 16 == 0 &&
                      a.ldx % 16 == 0 && a.ldy % 16 == 0 && a.F >= 48 && a.F <= 512;
     if (a32 && kLane32) {
+      if (att) return dispatch_layout32<T, true, true>(a);
       if (a.out2) return dispatch_sumw<T, 16>(a);
       return a.w ? dispatch_layout32<T, true>(a) : dispatch_layout32<T, false>(a);
     }
   }
+  if (att) return big ? dispatch_layout<T, VB, true, true>(a) : dispatch_layout<T, 2, true, true>(a);
   if (a.out2) return big ? dispatch_sumw<T, VB>(a) : dispatch_sumw<T, 2>(a);
   if (a.w) return big ? dispatch_layout<T, VB, true>(a) : dispatch_layout<T, 2, true>(a);
   return big ? dispatch_layout<T, VB, false>(a) : dispatch_layout<T, 2, false>(a);
@@ -820,7 +876,7 @@ extern "C" int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_ro
     if (rc) return rc;
     x = xs;
   }
-  FastArgs a;
+  FastArgs a{};
   a.offsets = offsets; a.cols = cols; a.n_rows = n_rows; a.n_cols = n_cols;
   a.num_edges = num_edges;
   a.units = reinterpret_cast<const int4*>(units); a.num_units = num_units;
@@ -847,6 +903,54 @@ extern "C" int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_ro
     if (rc) return rc;
   }
   return HG_OK;
+}
+
+// Fused GAT layer core, forward (fast numerics): the weighted aggregation of
+// hg_spmm with each edge's attention coefficient computed in the gather loop
+// from s_l, s_r and the per-row softmax statistics of hg_gat_attention_stats,
+// and written to alpha_out (needed by the backward) by one lane per head.
+extern "C" int hg_gat_aggregate(const int64_t* offsets, const int32_t* cols, int64_t n_rows,
+                                int64_t n_cols, int64_t num_edges, const int32_t* units,
+                                int64_t num_units, const int32_t* split_rows,
+                                int64_t num_split_rows, int64_t num_slots, const int32_t* packs,
+                                int64_t num_packs, const int32_t* pack_rowid, const void* s_l,
+                                const void* s_r, const float* stats, float slope,
+                                void* alpha_out, int32_t heads, const void* x, void* y, int32_t F,
+                                int64_t ldx, int64_t ldy, int32_t relu, int dtype, void* ws,
+                                size_t ws_bytes, void* stream) {
+  HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "hg_gat_aggregate: unknown dtype %d", dtype);
+  HG_REQUIRE(heads >= 1 && F >= 2 && F % heads == 0 && (F / heads) % 2 == 0,
+             "hg_gat_aggregate: F=%d must split into %d heads of even width", F, heads);
+  HG_REQUIRE(n_rows >= 0 && n_cols >= 0 && num_edges >= 0 && num_edges <= (int64_t)INT32_MAX,
+             "hg_gat_aggregate: bad sizes");
+  if (ldx == 0) ldx = F;
+  if (ldy == 0) ldy = F;
+  HG_REQUIRE(ldx >= F && ldy >= F && ldx <= INT32_MAX && ldy <= INT32_MAX,
+             "hg_gat_aggregate: row strides must be >= F");
+  HG_REQUIRE(reinterpret_cast<uintptr_t>(cols) % 4 == 0 &&
+                 (!pack_rowid || ((reinterpret_cast<uintptr_t>(cols) ^
+                                   reinterpret_cast<uintptr_t>(pack_rowid)) & 15) == 0),
+             "hg_gat_aggregate: cols and pack_rowid must have the same address modulo 16");
+  if (n_rows == 0) return HG_OK;
+  HG_REQUIRE(s_l && s_r && stats && alpha_out && x && y, "hg_gat_aggregate: null operand");
+  Carver cv(ws, ws_bytes);
+  float* carry = cv.take<float>((size_t)num_slots * F);
+  HG_REQUIRE(cv.fits(), "hg_gat_aggregate: workspace too small (%zu < %zu)", ws_bytes, cv.used);
+  FastArgs a{};
+  a.offsets = offsets; a.cols = cols; a.n_rows = n_rows; a.n_cols = n_cols;
+  a.num_edges = num_edges;
+  a.units = reinterpret_cast<const int4*>(units); a.num_units = num_units;
+  a.split_rows = reinterpret_cast<const int4*>(split_rows); a.num_split = num_split_rows;
+  a.packs = reinterpret_cast<const int4*>(packs); a.num_packs = packs ? num_packs : 0;
+  a.rowid = pack_rowid;
+  HG_REQUIRE(a.num_packs == 0 || num_edges == 0 || pack_rowid, "hg_gat_aggregate: packs need pack_rowid");
+  a.w = s_r; a.widx = nullptr; a.heads = heads; a.fh = F / heads; a.wld = heads;
+  a.x = x; a.y = y; a.carry = carry; a.F = F; a.ldx = (int)ldx; a.ldy = (int)ldy;
+  a.fmode = relu ? 4 : 0;
+  a.att_sl = s_l; a.att_stats = reinterpret_cast<const float2*>(stats); a.att_out = alpha_out;
+  a.att_slope = slope;
+  a.st = as_stream(stream);
+  return dtype == HG_F16 ? dispatch_fast<__half>(a) : dispatch_fast<float>(a);
 }
 
 // ------------------------------------------------------ reference edge order

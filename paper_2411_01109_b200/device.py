@@ -757,6 +757,65 @@ def gat_attention_fwd(view: CsrView, s_l, s_r, slope=0.2, out=None):
     return alpha
 
 
+def gat_attention_stats(view: CsrView, s_l, s_r, slope=0.2):
+    """Per-row softmax statistics of leaky(s_l[r] + s_r[c]): float32 [N, H, 2]
+    = (log2-domain max, 1 / exp-sum) (hg_gat_attention_stats)."""
+    _require_cuda(s_l, s_r)
+    s_l, s_r = s_l.contiguous(), s_r.contiguous()
+    h = _heads_of(s_l)
+    stats = torch.empty((view.n_rows, h, 2), dtype=torch.float32, device=s_l.device)
+    med, lng = view.row_classes()
+    nat.call("hg_gat_attention_stats", _p(view.offsets), _p(view.cols), view.n_rows, _p(s_l),
+             _p(s_r), h, float(slope), _p(stats), _p(med), med.numel(), _p(lng), lng.numel(),
+             SHORT_ROW, _dtype_code(s_l), _stream())
+    Probe.launches += 1
+    return stats
+
+
+def gat_aggregate(view: CsrView, z, s_l, s_r, stats, heads, slope=0.2, relu=False,
+                  split_cap: int = DEFAULT_SPLIT_CAP):
+    """Fused GAT forward core: (y [N, F], alpha [E, H]) with y[r] = sum_e alpha_e
+    z[c_e] per head and alpha formed in the gather loop from s_l, s_r and
+    `stats` (hg_gat_aggregate) -- bitwise equal to gat_attention_fwd followed
+    by spmm_csr(view, z, alpha, heads=heads) on the same schedule."""
+    _require_cuda(z, s_l, s_r, stats)
+    z = z.contiguous()
+    s_l, s_r = s_l.contiguous(), s_r.contiguous()
+    if z.dim() != 2 or z.shape[0] != view.n_cols:
+        raise ValueError(f"feature tensor has {z.shape[0]} rows for {view.n_cols} columns")
+    f = z.shape[1]
+    dt = _dtype_code(z)
+    pack_edges = -1
+    if PACKING and view.n_rows >= PACK_MIN_ROWS:
+        pack_edges = PACK_EDGES_WIDE if f * z.element_size() >= 256 else PACK_EDGES_NARROW
+    sched = view.schedule(split_cap, pack_edges)
+    out = torch.empty((view.n_rows, f), dtype=z.dtype, device=z.device)
+    alpha = torch.empty((view.num_edges, heads), dtype=z.dtype, device=z.device)
+    nbytes = nat.size_query("hg_spmm_workspace", view.n_cols, f, sched.num_slots, 0, 0, dt)
+    ws = workspace(nbytes, z.device)
+    if Probe.timing:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+    nat.call("hg_gat_aggregate", _p(view.offsets), _p(view.cols), view.n_rows, view.n_cols,
+             view.num_edges, _p(sched.units), sched.num_units, _p(sched.split_rows),
+             sched.split_rows.shape[0], sched.num_slots, _p(sched.packs), sched.num_packs,
+             _p(view.row_ids() if sched.num_packs else None), _p(s_l), _p(s_r), _p(stats),
+             float(slope), _p(alpha), heads, _p(z), _p(out), f, z.stride(0), out.stride(0),
+             int(relu), dt, _p(ws), 0 if ws is None else ws.numel(), _stream())
+    Probe.launches += int(sched.num_units > 0) + int(sched.num_packs > 0) + int(
+        sched.split_rows.shape[0] > 0)
+    if Probe.timing:
+        ev1.record()
+        Probe.records.append((ev0, ev1, spmm_bytes(view.n_rows, view.n_cols, view.num_edges, f,
+                                                   heads, z.element_size()),
+                              compulsory_bytes(view.n_rows, view.n_cols, view.num_edges, f,
+                                               heads, z.element_size()),
+                              (view.cols, view.num_edges, z, f) if Probe.keep else None,
+                              (-(-f * z.element_size() // 16) * 16, view.num_edges)))
+    return out, alpha
+
+
 def gat_attention_bwd(view: CsrView, s_l, s_r, alpha, dalpha, slope=0.2, de_out=None):
     """(de [E, H], ds_l [N, H]) of gat_attention_fwd.  With de_out (the d_e half
     of interleaved [E, 2H] rows, alpha its other half) the two share one row

@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import csv
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -837,6 +838,14 @@ class GATLayer:
         return relu(out) if relu_out and not fuse else out
 
 
+# GAT forward core as hg_gat_attention_stats + hg_gat_aggregate (SURVEY 8(f)1,
+# bitwise the same result as hg_gat_attention_fwd + hg_spmm on alpha).  Off by
+# default: measured on C5 (RMAT-24, 4 heads) the alpha math inside the gather
+# loop lengthens each batch more than the saved alpha pass returns (119.6 ->
+# 122.8 ms/epoch); equal on C2.  HG_FUSED_GAT=1 selects it.
+FUSED_GAT_FWD = os.environ.get("HG_FUSED_GAT", "0") == "1"
+
+
 class _GATCoreFn(torch.autograd.Function):
     """The multi-head GAT layer core (models.py:492-509) after z = x W as one
     autograd node, for single-GPU fast numerics: head dots s = z a -> fused
@@ -849,8 +858,15 @@ class _GATCoreFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, z, a_l, a_r, bundle, heads, relu):
         s_l, s_r = bundle.head_dots(z, a_l, a_r, heads)
-        alpha = D.gat_attention_fwd(bundle.dg.view(False), s_l, s_r, 0.2)
-        out = D.spmm_csr(bundle.dg.view(False), z, alpha, None, heads, "post", relu=relu)
+        view = bundle.dg.view(False)
+        if FUSED_GAT_FWD:
+            # row statistics, then scores -> alpha -> weighted aggregation in
+            # one gather pass (alpha written once for the backward, never re-read)
+            stats = D.gat_attention_stats(view, s_l, s_r, 0.2)
+            out, alpha = D.gat_aggregate(view, z, s_l, s_r, stats, heads, 0.2, relu=relu)
+        else:
+            alpha = D.gat_attention_fwd(view, s_l, s_r, 0.2)
+            out = D.spmm_csr(view, z, alpha, None, heads, "post", relu=relu)
         ctx.bundle, ctx.heads, ctx.relu = bundle, heads, relu
         ctx.save_for_backward(z, a_l, a_r, s_l, s_r, alpha, out if relu else None)
         return out

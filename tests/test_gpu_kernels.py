@@ -666,6 +666,39 @@ def test_gat_attention_fast_vs_f64(cuda, heads):
     assert np.all(np.abs(got_r.astype(np.float64) - want_r) <= 2e-3 * np.maximum(1, np.abs(want_r)))
 
 
+@pytest.mark.parametrize("heads,fh", [(1, 64), (4, 32), (4, 16), (8, 8), (2, 6), (4, 128)])
+@pytest.mark.parametrize("packs", [False, True])
+def test_gat_fused_forward_bitwise_equals_composed(cuda, heads, fh, packs):
+    """hg_gat_attention_stats + hg_gat_aggregate (alpha formed in the gather
+    loop) == hg_gat_attention_fwd + hg_spmm(w = alpha), bit for bit: alpha,
+    the aggregation (all three row classes, split hub rows with carries, packed
+    short rows) and the fused ReLU."""
+    from paper_2411_01109_b200 import device as D
+
+    n = 6000
+    r, c = _hub_graph(heads + fh, n)
+    dg = _dg(n, r, c, cuda)
+    rng = np.random.default_rng(fh)
+    sl = _t(rng.normal(0, 3, (n, heads)).astype(np.float16), cuda)
+    sr = _t(rng.normal(0, 3, (n, heads)).astype(np.float16), cuda)
+    z = _t(rng.normal(0, 1, (n, heads * fh)).astype(np.float16), cuda)
+    saved = D.PACK_MIN_ROWS
+    D.PACK_MIN_ROWS = 0 if packs else 1 << 40
+    try:
+        view = dg.view(False)
+        for relu in (False, True):
+            alpha = D.gat_attention_fwd(view, sl, sr, 0.2)
+            want = D.spmm_csr(view, z, alpha, None, heads, "post", relu=relu)
+            stats = D.gat_attention_stats(view, sl, sr, 0.2)
+            got, galpha = D.gat_aggregate(view, z, sl, sr, stats, heads, 0.2, relu=relu)
+            assert torch.equal(galpha.view(torch.int16), alpha.view(torch.int16))
+            assert torch.equal(got.view(torch.int16), want.view(torch.int16))
+        if packs and fh * heads * 2 < 256:
+            assert view.schedule(pack_edges=D.PACK_EDGES_NARROW).num_packs > 0
+    finally:
+        D.PACK_MIN_ROWS = saved
+
+
 @pytest.mark.parametrize("heads,f", [(4, 16), (2, 3), (8, 8), (4, 24), (3, 40)])
 def test_head_mean_bits(cuda, heads, f):
     from paper_2411_01109_b200 import device as D
