@@ -134,6 +134,25 @@ int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_rows, int64_t
             const void* in_scale, const void* out_factor, int64_t w_ld, int32_t w2_off,
             void* out2, int dtype, void* ws, size_t ws_bytes, void* stream);
 
+/* hg_spmm in fp32 partial mode, for column-blocked aggregation
+ * (a row's edges split by the rank owning their column, block q run as soon as
+ * rank q's feature rows have landed; partition.py): each row starts from
+ * acc_in[r] (NULL: 0) and, with acc_out != NULL, ends unrounded in acc_out[r]
+ * ([n_rows, F] fp32, 16-byte aligned, may alias acc_in); with acc_out NULL the
+ * row is finished into y like hg_spmm (scaling / out_factor / relu).  Chaining
+ * the blocks in ascending column order reproduces hg_spmm's fp32 sum bit for
+ * bit on every row that is one unit in each block; split rows regroup their
+ * carries.  Weights as hg_spmm (w / w_index / heads / w_ld; a block's
+ * w_index maps its edges back to the unblocked edge order).  F: a multiple of 4. */
+int hg_spmm_acc(const int64_t* offsets, const int32_t* cols, int64_t n_rows, int64_t n_cols,
+                int64_t num_edges, const int32_t* units, int64_t num_units,
+                const int32_t* split_rows, int64_t num_split_rows, int64_t num_slots,
+                const int32_t* packs, int64_t num_packs, const int32_t* pack_rowid,
+                const void* w, const int32_t* w_index, int32_t heads, int64_t w_ld,
+                const void* x, void* y, int32_t F, int64_t ldx, int64_t ldy, int32_t scaling,
+                int32_t relu, const void* out_factor, const float* acc_in, float* acc_out,
+                int dtype, void* ws, size_t ws_bytes, void* stream);
+
 /* Reference-order SpMM, bit-exact with halfsparse _spmm_edge_parallel
  * (kernels.py:328-391; order spelled out in _ref_spmm_edge, kernels.py:603-688):
  * warp w owns edges [w*warp_chunk, ...), CTA c owns warps [c*warps_per_cta, ...);

@@ -74,6 +74,9 @@ SIGNATURES = {
     "hg_parse_edges": [_P, _I64, _I64, _P, _P, _PI64, _P, c_size_t, _P],
     "hg_gat_attention_fwd": [_P, _P, _I64, _P, _P, _I32, c_float, _P, _I64, _P, _I64, _P, _I64,
                              _I32, c_int, _P],
+    "hg_spmm_acc": [_P, _P, _I64, _I64, _I64, _P, _I64, _P, _I64, _I64, _P, _I64, _P, _P, _P,
+                    _I32, _I64, _P, _P, _I32, _I64, _I64, _I32, _I32, _P, _P, _P, c_int, _P,
+                    c_size_t, _P],
     "hg_gat_attention_stats": [_P, _P, _I64, _P, _P, _I32, c_float, _P, _P, _I64, _P, _I64,
                                _I32, c_int, _P],
     "hg_gat_aggregate": [_P, _P, _I64, _I64, _I64, _P, _I64, _P, _I64, _I64, _P, _I64, _P,

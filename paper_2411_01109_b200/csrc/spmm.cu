@@ -86,6 +86,23 @@ __device__ __forceinline__ void store_out(T* dst, const float (&acc)[V], int fmo
 }
 
 template <int V>
+__device__ __forceinline__ void load_carry(const float* src, float (&acc)[V]) {
+  if constexpr (V % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < V; i += 4) {
+      const float4 v = *reinterpret_cast<const float4*>(src + i);
+      acc[i] = v.x; acc[i + 1] = v.y; acc[i + 2] = v.z; acc[i + 3] = v.w;
+    }
+  } else if constexpr (V == 2) {
+    const float2 v = *reinterpret_cast<const float2*>(src);
+    acc[0] = v.x; acc[1] = v.y;
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc[i] = src[i];
+  }
+}
+
+template <int V>
 __device__ __forceinline__ void store_carry(float* dst, const float (&acc)[V]) {
   if constexpr (V % 4 == 0) {
 #pragma unroll
@@ -272,6 +289,18 @@ struct FastTeam {
   T* pout2;
   int pldy, pfmode;
   bool plead;
+  // fp32 partial-output mode (column-blocked aggregation, partition.py):
+  // rows start from acc_in[r] and end in acc_out[r] unrounded (NULL: 0 / rnd)
+  const float* accin;
+  float* accout;
+  int accld;
+
+  __device__ __forceinline__ void load_acc(int r) {
+#pragma unroll
+    for (int k = 0; k < NCH; ++k)
+      if (cval[k]) load_carry<V>(accin + (int64_t)r * accld + (xl[k] - px), acc[k]);
+  }
+
   // ATT state: the row's log2-domain s_l, running max and 1/sum per chunk
   const T* asl;
   const float2* astats;
@@ -305,7 +334,10 @@ struct FastTeam {
   __device__ __forceinline__ void store_row() {
 #pragma unroll
     for (int k = 0; k < NCH; ++k) {
-      if (cval[k]) store_out<T, V>(py + (int64_t)prow * pldy + (xl[k] - px), acc[k], pfmode, pfo);
+      if (cval[k]) {
+        if (accout) store_carry<V>(accout + (int64_t)prow * accld + (xl[k] - px), acc[k]);
+        else store_out<T, V>(py + (int64_t)prow * pldy + (xl[k] - px), acc[k], pfmode, pfo);
+      }
 #pragma unroll
       for (int i = 0; i < V; ++i) acc[k][i] = 0.0f;
     }
@@ -322,6 +354,7 @@ struct FastTeam {
       prow = r;
       pfo = pfout ? pfout[r] : Num<T>::zero();
       if (ATT) load_att(r);
+      if (accin) load_acc(r);
     }
   }
 
@@ -432,7 +465,8 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
             const T* __restrict__ fout, int wld, int w2off, T* __restrict__ out2,
             float* __restrict__ carry2, const int64_t* __restrict__ offsets,
             const int32_t* __restrict__ rowid, const T* __restrict__ att_sl,
-            const float2* __restrict__ att_stats, T* __restrict__ att_out, float att_slope) {
+            const float2* __restrict__ att_stats, T* __restrict__ att_out, float att_slope,
+            const float* __restrict__ acc_in, float* __restrict__ acc_out, int acc_ld) {
   using Team = FastTeam<T, V, TEAM, NCH, WEIGHTED, SUMW, PACKED, ATT>;
   constexpr int EB = Team::EB;
   constexpr int CPL = Team::CPL;
@@ -474,6 +508,10 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
     for (int i = 0; i < V; ++i) t.acc[k][i] = 0.0f;
   }
   const bool lead = t.cval[0] && (tl * V) % fh == 0;  // SUMW: first lane of its head
+  t.accin = acc_in;
+  t.accout = acc_out;
+  t.accld = acc_ld;
+  t.px = x;
   if constexpr (ATT) {
     t.asl = att_sl;
     t.astats = att_stats;
@@ -508,11 +546,14 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
       empty &= empty - 1;
       t.prow = row + i;
       t.pfo = fout ? fout[row + i] : Num<T>::zero();
+      if (acc_in) t.load_acc(row + i);
       t.store_row();
     }
     t.prow = -1;
   }
   const int beg = t.beg, end = t.end;
+  // fp32 partial mode: the row's first unit starts from acc_in
+  if (!PACKED && acc_in && (slot < 0 || (int64_t)beg == __ldg(offsets + row))) t.load_acc(row);
 
   // Batches aligned to the absolute address of cols (vector id loads).
   const int mis = (int)((reinterpret_cast<uintptr_t>(cols) >> 2) & (EB - 1));
@@ -569,7 +610,11 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
     t.template batch<false>(b, ids, wids, rids);
   }
 
-  if (slot < 0) {
+  if (slot < 0 && acc_out) {
+#pragma unroll
+    for (int k = 0; k < NCH; ++k)
+      if (t.cval[k]) store_carry<V>(acc_out + (int64_t)row * acc_ld + (t.xl[k] - x), t.acc[k]);
+  } else if (slot < 0) {
     const T fo = fout ? fout[row] : Num<T>::zero();
 #pragma unroll
     for (int k = 0; k < NCH; ++k)
@@ -591,7 +636,8 @@ __global__ void __launch_bounds__(256)
 k_spmm_fast_followup(const int4* __restrict__ split_rows, int64_t num_split,
                      const float* __restrict__ carry, T* __restrict__ y, int F, int ldy,
                      int fmode, const T* __restrict__ fout, int heads2,
-                     const float* __restrict__ carry2, T* __restrict__ out2) {
+                     const float* __restrict__ carry2, T* __restrict__ out2,
+                     float* __restrict__ acc_out, int acc_ld) {
   const int lane = threadIdx.x & 31;
   const int tl = lane & (TEAM - 1);
   const int64_t team = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TEAM;
@@ -632,7 +678,8 @@ k_spmm_fast_followup(const int4* __restrict__ split_rows, int64_t num_split,
           for (int i = 0; i < V; ++i) acc[i] += buf[q][i];
         }
     }
-    store_out<T, V>(y + (int64_t)sr.x * ldy + c * V, acc, fmode, fo);
+    if (acc_out) store_carry<V>(acc_out + (int64_t)sr.x * acc_ld + c * V, acc);
+    else store_out<T, V>(y + (int64_t)sr.x * ldy + c * V, acc, fmode, fo);
   }
 }
 
@@ -662,6 +709,9 @@ struct FastArgs {
   const float2* att_stats;
   void* att_out;
   float att_slope;
+  const float* acc_in;     // fp32 partial mode (hg_spmm_acc)
+  float* acc_out;
+  int acc_ld;
   cudaStream_t st;
 };
 
@@ -679,7 +729,7 @@ static int launch_fast(const FastArgs& a) {
         a.units, a.num_units, a.cols, a.num_edges, (const T*)a.w, a.widx, a.heads, a.fh,
         (const T*)a.x, (T*)a.y, a.carry, a.F, a.ldx, a.ldy, a.fmode, (const T*)a.fout,
         a.wld, a.w2off, (T*)a.out2, a.carry2, a.offsets, nullptr, (const T*)a.att_sl,
-        a.att_stats, (T*)a.att_out, a.att_slope);
+        a.att_stats, (T*)a.att_out, a.att_slope, a.acc_in, a.acc_out, a.acc_ld);
     HG_LAUNCHED();
   }
   if (a.num_packs > 0) {
@@ -688,14 +738,14 @@ static int launch_fast(const FastArgs& a) {
         a.packs, a.num_packs, a.cols, a.num_edges, (const T*)a.w, a.widx, a.heads, a.fh,
         (const T*)a.x, (T*)a.y, nullptr, a.F, a.ldx, a.ldy, a.fmode, (const T*)a.fout,
         a.wld, a.w2off, (T*)a.out2, nullptr, a.offsets, a.rowid, (const T*)a.att_sl,
-        a.att_stats, (T*)a.att_out, a.att_slope);
+        a.att_stats, (T*)a.att_out, a.att_slope, a.acc_in, a.acc_out, a.acc_ld);
     HG_LAUNCHED();
   }
   if (a.num_split > 0) {
     int64_t blocks = (a.num_split + kThreads / TEAMF - 1) / (kThreads / TEAMF);
     k_spmm_fast_followup<T, V, TEAMF, NCH><<<(unsigned)blocks, kThreads, 0, a.st>>>(
         a.split_rows, a.num_split, a.carry, (T*)a.y, a.F, a.ldy, a.fmode, (const T*)a.fout,
-        SUMW ? a.heads : 0, a.carry2, SUMW ? (T*)a.out2 : nullptr);
+        SUMW ? a.heads : 0, a.carry2, SUMW ? (T*)a.out2 : nullptr, a.acc_out, a.acc_ld);
     HG_LAUNCHED();
   }
   return HG_OK;
@@ -828,15 +878,15 @@ extern "C" int hg_spmm_workspace(int64_t n_cols, int32_t F, int64_t num_slots, i
   return HG_OK;
 }
 
-extern "C" int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_rows,
-                       int64_t n_cols, int64_t num_edges, const int32_t* units, int64_t num_units,
-                       const int32_t* split_rows, int64_t num_split_rows, int64_t num_slots,
-                       const int32_t* packs, int64_t num_packs, const int32_t* pack_rowid,
-                       const void* w, const int32_t* w_index, int32_t heads, const void* x,
-                       void* y, int32_t F, int64_t ldx, int64_t ldy, int32_t scaling,
-                       int32_t relu, const void* in_scale, const void* out_factor,
-                       int64_t w_ld, int32_t w2_off, void* out2, int dtype, void* ws,
-                       size_t ws_bytes, void* stream) {
+static int spmm_impl(const int64_t* offsets, const int32_t* cols, int64_t n_rows,
+                     int64_t n_cols, int64_t num_edges, const int32_t* units, int64_t num_units,
+                     const int32_t* split_rows, int64_t num_split_rows, int64_t num_slots,
+                     const int32_t* packs, int64_t num_packs, const int32_t* pack_rowid,
+                     const void* w, const int32_t* w_index, int32_t heads, const void* x,
+                     void* y, int32_t F, int64_t ldx, int64_t ldy, int32_t scaling,
+                     int32_t relu, const void* in_scale, const void* out_factor,
+                     int64_t w_ld, int32_t w2_off, void* out2, int dtype, void* ws,
+                     size_t ws_bytes, void* stream, const float* acc_in, float* acc_out) {
   HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
   HG_REQUIRE(F > 0 && F % 2 == 0, "feature length %d must be even and positive", F);
   HG_REQUIRE(heads >= 1 && F % heads == 0 && (F / heads) % 2 == 0,
@@ -889,6 +939,7 @@ extern "C" int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_ro
   a.fmode = (out_factor == nullptr ? 0 : (scaling == HG_SCALING_POST ? 1 : 2)) | (relu ? 4 : 0);
   a.fout = out_factor; a.st = st;
   a.wld = (int)w_ld; a.w2off = w2_off; a.out2 = out2; a.carry2 = carry2;
+  a.acc_in = acc_in; a.acc_out = acc_out; a.acc_ld = F;
   // Column slabs: when X (n_cols x F) overflows the L2 budget but a slab of
   // >= 32 columns fits, aggregate slab by slab so the random row gathers of
   // each pass hit L2 (the column stream is re-read once per slab, sequentially).
@@ -899,10 +950,46 @@ extern "C" int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_ro
     if (heads == 1) s.fh = s.F;
     s.x = static_cast<const char*>(x) + (size_t)j * elem_size(dtype);
     s.y = static_cast<char*>(y) + (size_t)j * elem_size(dtype);
+    if (acc_in) s.acc_in = acc_in + j;
+    if (acc_out) s.acc_out = acc_out + j;
     const int rc = dtype == HG_F16 ? dispatch_fast<__half>(s) : dispatch_fast<float>(s);
     if (rc) return rc;
   }
   return HG_OK;
+}
+
+extern "C" int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_rows,
+                       int64_t n_cols, int64_t num_edges, const int32_t* units, int64_t num_units,
+                       const int32_t* split_rows, int64_t num_split_rows, int64_t num_slots,
+                       const int32_t* packs, int64_t num_packs, const int32_t* pack_rowid,
+                       const void* w, const int32_t* w_index, int32_t heads, const void* x,
+                       void* y, int32_t F, int64_t ldx, int64_t ldy, int32_t scaling,
+                       int32_t relu, const void* in_scale, const void* out_factor,
+                       int64_t w_ld, int32_t w2_off, void* out2, int dtype, void* ws,
+                       size_t ws_bytes, void* stream) {
+  return spmm_impl(offsets, cols, n_rows, n_cols, num_edges, units, num_units, split_rows,
+                   num_split_rows, num_slots, packs, num_packs, pack_rowid, w, w_index, heads, x, y,
+                   F, ldx, ldy, scaling, relu, in_scale, out_factor, w_ld, w2_off, out2, dtype, ws,
+                   ws_bytes, stream, nullptr, nullptr);
+}
+
+extern "C" int hg_spmm_acc(const int64_t* offsets, const int32_t* cols, int64_t n_rows,
+                           int64_t n_cols, int64_t num_edges, const int32_t* units,
+                           int64_t num_units, const int32_t* split_rows, int64_t num_split_rows,
+                           int64_t num_slots, const int32_t* packs, int64_t num_packs,
+                           const int32_t* pack_rowid, const void* w, const int32_t* w_index,
+                           int32_t heads, int64_t w_ld, const void* x, void* y, int32_t F,
+                           int64_t ldx, int64_t ldy, int32_t scaling, int32_t relu,
+                           const void* out_factor, const float* acc_in, float* acc_out, int dtype,
+                           void* ws, size_t ws_bytes, void* stream) {
+  HG_REQUIRE(F % 4 == 0, "hg_spmm_acc: F=%d must be a multiple of 4 (fp32 row vectors)", F);
+  HG_REQUIRE(((reinterpret_cast<uintptr_t>(acc_in) | reinterpret_cast<uintptr_t>(acc_out)) & 15) == 0,
+             "hg_spmm_acc: accumulators must be 16-byte aligned");
+  HG_REQUIRE(acc_out || y, "hg_spmm_acc: no output");
+  return spmm_impl(offsets, cols, n_rows, n_cols, num_edges, units, num_units, split_rows,
+                   num_split_rows, num_slots, packs, num_packs, pack_rowid, w, w_index, heads, x,
+                   acc_out ? nullptr : y, F, ldx, ldy, scaling, relu, nullptr, out_factor, w_ld, 0,
+                   nullptr, dtype, ws, ws_bytes, stream, acc_in, acc_out);
 }
 
 // Fused GAT layer core, forward (fast numerics): the weighted aggregation of

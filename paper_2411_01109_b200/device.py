@@ -557,6 +557,53 @@ def spmm_csr(view: CsrView, x: torch.Tensor, w=None, w_index=None, heads: int = 
     return out
 
 
+def spmm_csr_acc(view: CsrView, x: torch.Tensor, acc_in=None, acc_out=None, scaling="post",
+                 fout=None, out=None, relu=False, split_cap: int = DEFAULT_SPLIT_CAP,
+                 w=None, w_index=None, heads: int = 1):
+    """One column block of a blocked aggregation (hg_spmm_acc): rows start from
+    the fp32 acc_in (None: 0); with acc_out the unrounded fp32 sums go there
+    (may be acc_in), else the rows are finished into `out` (returned).  w /
+    w_index / heads: edge weights as spmm_csr (w_index maps the block's edges
+    to rows of w)."""
+    _require_cuda(x)
+    if not _row_strided(x):
+        x = x.contiguous()
+    if x.dim() != 2 or x.shape[0] != view.n_cols:
+        raise ValueError(f"feature tensor has {x.shape[0]} rows for {view.n_cols} columns")
+    f = x.shape[1]
+    dt = _dtype_code(x)
+    for a in (acc_in, acc_out):
+        if a is not None and (a.dtype != torch.float32 or a.shape != (view.n_rows, f)
+                              or not a.is_contiguous()):
+            raise ValueError("accumulators must be contiguous float32 [n_rows, F]")
+    pack_edges = -1
+    if PACKING and view.n_rows >= PACK_MIN_ROWS:
+        pack_edges = PACK_EDGES_WIDE if f * x.element_size() >= 256 else PACK_EDGES_NARROW
+    sched = view.schedule(split_cap, pack_edges)
+    if acc_out is None and out is None:
+        out = torch.empty((view.n_rows, f), dtype=x.dtype, device=x.device)
+    nbytes = nat.size_query("hg_spmm_workspace", view.n_cols, f, sched.num_slots, 0, 0, dt)
+    ws = workspace(nbytes, x.device)
+    w_ld = 0
+    if w is not None:
+        if w.dim() == 2 and w.stride(1) == 1:
+            w_ld = w.stride(0)
+        else:
+            w = w.contiguous()
+        if w.dtype != x.dtype:
+            raise ValueError("edge weights must match the feature dtype")
+    nat.call("hg_spmm_acc", _p(view.offsets), _p(view.cols), view.n_rows, view.n_cols,
+             view.num_edges, _p(sched.units), sched.num_units, _p(sched.split_rows),
+             sched.split_rows.shape[0], sched.num_slots, _p(sched.packs), sched.num_packs,
+             _p(view.row_ids() if sched.num_packs else None), _p(w), _p(w_index), heads, w_ld,
+             _p(x), _p(out), f, x.stride(0),
+             f if out is None else out.stride(0), nat.SCALING_CODES[scaling], int(relu), _p(fout),
+             _p(acc_in), _p(acc_out), dt, _p(ws), 0 if ws is None else ws.numel(), _stream())
+    Probe.launches += int(sched.num_units > 0) + int(sched.num_packs > 0) + int(
+        sched.split_rows.shape[0] > 0)
+    return acc_out if acc_out is not None else out
+
+
 def spmm(dg: DeviceGraph, x, w=None, scaling="post", norm="none", transpose=False, heads=1,
          out=None, weight_via_perm=False, relu=False):
     """SpMMv / SpMMve on the graph (or its transpose), fp32-guarded.

@@ -17,6 +17,17 @@ first aggregation reads the raw features) is gathered once when it is loaded
 owner of each edge's column with one all-to-all (each edge travels once,
 E/P per rank instead of the E an all-gather would deliver).
 Weight gradients and the loss are all-reduced (the data-parallel sum).
+
+Comm/compute overlap (`overlap=True`, the default on CUDA): each
+rank's CSR (and CSC) rows are also split into P column blocks by the rank that
+owns each column (`column_blocks`).  An unweighted aggregation then receives
+the P feature slabs as P ordered NCCL broadcasts (async) and runs block q as
+soon as slab q has landed, carrying the rows' fp32 sums from block to block
+(hg_spmm_acc) and rounding once after the last block: the SpMM of the first
+slabs overlaps the transfer of the later ones.  The blocks run in ascending
+column order, so every row that is a single work unit in each block sums in
+exactly the unblocked order (bitwise equal); split hub rows regroup their
+fp32 carries (within the fast-path tolerance).
 Degree-factor tables are global (computed once from the full graph), which
 makes the concatenated rank outputs bit-identical to the 1-GPU result.
 
@@ -25,6 +36,7 @@ tests drive the same exchange logic with a host implementation.
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -127,6 +139,37 @@ def make_local_part(offsets, cols, t_offsets, t_cols, perm, rank, parts) -> Loca
                      send_counts, recv_counts)
 
 
+def column_blocks(view: CsrView, splits: np.ndarray) -> list:
+    """Split a CSR whose rows hold sorted global column ids into P CSRs by the
+    rank owning each column: block q keeps, row by row and in order, the edges
+    with a column in [s_q, s_{q+1}), column ids rebased to s_q (they index rank
+    q's feature slab).  Concatenating the blocks' rows in q order gives back
+    each original row."""
+    off, cols = view.offsets, view.cols
+    dev = cols.device
+    n, e = view.n_rows, cols.numel()
+    parts = len(splits) - 1
+    c64 = cols.to(torch.int64)
+    owner = torch.searchsorted(torch.as_tensor(splits[1:-1], dtype=torch.int64, device=dev), c64,
+                               right=True)
+    rows = torch.repeat_interleave(torch.arange(n, device=dev), (off[1:] - off[:-1]).to(torch.int64),
+                                   output_size=e)
+    counts = torch.bincount(owner * n + rows, minlength=parts * n).view(parts, n)
+    order = torch.argsort(owner, stable=True)          # grouped by owner, CSR order inside
+    per_block = counts.sum(1).cpu().tolist()
+    out, start = [], 0
+    for q in range(parts):
+        seg = order[start:start + per_block[q]]
+        start += per_block[q]
+        o_q = torch.zeros(n + 1, dtype=off.dtype, device=dev)
+        o_q[1:] = torch.cumsum(counts[q], 0)
+        c_q = (c64[seg] - int(splits[q])).to(torch.int32).clone()
+        # perm: block slot -> edge of the unblocked view (edge weights follow it)
+        out.append(CsrView(o_q, c_q, n, int(splits[q + 1] - splits[q]),
+                           perm=seg.to(torch.int32).clone()))
+    return out
+
+
 class Exchange:
     """Exact-count all-gathers over a torch.distributed process group.  NCCL
     moves device tensors over NVLink (all_gather into per-rank views of
@@ -166,6 +209,38 @@ class Exchange:
         else:
             self.dist.all_gather(self._views(out), x_local)
         return out
+
+    def gather_slabs(self, x_local: torch.Tensor):
+        """(slabs, waits): rank q's rows as slab q (slab `rank` is x_local
+        itself), for a column-blocked aggregation.  NCCL: P async broadcasts
+        issued in rank order on the process group's stream; waits[q]() makes
+        the current stream wait for slab q only, so the SpMM of the slabs that
+        have landed overlaps the transfer of the rest.  gloo: one staged
+        all-gather, no waits."""
+        p = self.part
+        x_local = x_local.contiguous()
+        tail = tuple(x_local.shape[1:])
+        row = x_local[0].numel() * x_local.element_size() if x_local.shape[0] else 0
+        n = int(p.splits[-1])
+        self.recv_bytes += (n - p.n_local) * row
+        self.gathers += 1
+        if self.staged:
+            full = x_local.new_empty((n,) + tail)
+            send = x_local.new_zeros((p.n_max,) + tail, device="cpu")
+            send[: p.n_local] = x_local.cpu()
+            host = send.new_empty((p.parts * p.n_max,) + tail)
+            self.dist.all_gather_into_tensor(host, send)
+            for q, v in enumerate(self._views(full)):
+                v.copy_(host[q * p.n_max: q * p.n_max + v.shape[0]])
+            return self._views(full), [None] * p.parts
+        slabs, waits = [], []
+        for q in range(p.parts):
+            buf = x_local if q == p.rank else x_local.new_empty(
+                (int(p.splits[q + 1] - p.splits[q]),) + tail)
+            work = self.dist.broadcast(buf, src=q, async_op=True)
+            slabs.append(buf)
+            waits.append(None if q == p.rank else work.wait)
+        return slabs, waits
 
     def gather_edges(self, v_local: torch.Tensor) -> torch.Tensor:
         """Per-edge values ([E_local, ...], CSR order) -> the values of this
@@ -260,13 +335,65 @@ class DistBundle:
 
     numerics = "fast"
 
-    def __init__(self, part: LocalPart, exchange: Exchange, tables, ops=CudaOps):
+    def __init__(self, part: LocalPart, exchange: Exchange, tables, ops=CudaOps, overlap=None):
         self.part = part
         self.ex = exchange
         self.ops = ops
         self._tables = tables  # callable (kind, side, dtype) -> global table [N]
         self._cache = {}
         self._static = None    # (local input tensor, its gathered [N, F] copy)
+        # column-blocked, transfer-overlapped unweighted aggregation (CUDA ops, P > 1)
+        if overlap is None:
+            overlap = os.environ.get("HG_DIST_OVERLAP", "1") != "0"
+        self.overlap = bool(overlap) and ops is CudaOps and part.parts > 1
+        self._blocks = {}
+
+    def blocks(self, transpose):
+        """The P column blocks of the local CSR (forward) or CSC (backward)."""
+        b = self._blocks.get(transpose)
+        if b is None:
+            b = column_blocks(self.part.bwd if transpose else self.part.fwd, self.part.splits)
+            self._blocks[transpose] = b
+        return b
+
+    def _block_windex(self, transpose, via_perm):
+        """Per block: the row of the weight array each block edge reads -- the
+        unblocked edge (block perm) or, for weights received in CSC order, that
+        edge's slot in the receive buffer (view.perm after the block perm)."""
+        key = ("widx", transpose, via_perm)
+        w = self._blocks.get(key)
+        if w is None:
+            view = self.part.bwd if transpose else self.part.fwd
+            w = [(view.perm.long()[b.perm.long()].to(torch.int32).clone() if via_perm
+                  else b.perm) for b in self.blocks(transpose)]
+            self._blocks[key] = w
+        return w
+
+    def _blocked_agg(self, xs_local, scaling, fout, transpose, full=None, w=None,
+                     via_perm=False, heads=1):
+        """Aggregation of the gathered rows block by block: block q as soon as
+        slab q has landed, rows' fp32 sums carried from block to block
+        (hg_spmm_acc), rounded (scaling, out factor) after the last.  Edge
+        weights (GAT's alpha) follow each block edge to its unblocked slot."""
+        blocks = self.blocks(transpose)
+        widx = self._block_windex(transpose, via_perm) if w is not None else None
+        if full is not None:      # a static input gathered earlier: slabs are views
+            slabs, waits = self.ex._views(full), [None] * self.part.parts
+        else:
+            slabs, waits = self.ex.gather_slabs(xs_local)
+        f = slabs[0].shape[1]
+        n = self.part.n_local
+        acc = torch.empty((n, f), dtype=torch.float32, device=slabs[0].device)
+        out = None
+        last = len(blocks) - 1
+        for q, (view, slab) in enumerate(zip(blocks, slabs)):
+            if waits[q] is not None:
+                waits[q]()
+            out = D.spmm_csr_acc(view, slab, acc_in=None if q == 0 else acc,
+                                 acc_out=None if q == last else acc, scaling=scaling,
+                                 fout=fout if q == last else None, w=w,
+                                 w_index=None if widx is None else widx[q], heads=heads)
+        return out
 
     def set_static(self, x_local, x_full):
         """Register a gathered copy of a static input (GIN's raw features):
@@ -321,6 +448,8 @@ class DistBundle:
     def _gather_scaled(self, xs, scaling, norm, transpose, heads=1, w=None, widx=None):
         view = self.part.bwd if transpose else self.part.fwd
         _, fout = self.norm_tables(norm, transpose, xs.dtype)
+        if self.overlap and w is None and xs.shape[1] % 4 == 0:
+            return self._blocked_agg(xs, scaling, fout, transpose)
         return self.ops.spmm(view, self.ex.gather_rows(xs.contiguous()), w, widx, heads,
                              scaling, None, fout)
 
@@ -373,8 +502,16 @@ class DistBundle:
                 widx = view.perm
             return self._gather_scaled(row_scale(x.contiguous(), fin_local), scaling, norm,
                                        transpose, heads, w, widx)
-        x_full = self._gathered(x)
         fin, fout = self.norm_tables(norm, transpose, x.dtype)
+        if self.overlap and fin is None and x.shape[1] % 4 == 0:
+            st = self._static
+            static = (st[1] if st is not None and x.data_ptr() == st[0].data_ptr()
+                      and x.shape == st[0].shape else None)
+            if w is not None:
+                w = self.ex.gather_edges(w.contiguous()) if weight_via_perm else w.contiguous()
+            return self._blocked_agg(x, scaling, fout, transpose, full=static, w=w,
+                                     via_perm=weight_via_perm, heads=heads)
+        x_full = self._gathered(x)
         widx = None
         if w is not None and weight_via_perm:
             w = self.ex.gather_edges(w.contiguous())

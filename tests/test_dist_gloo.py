@@ -261,3 +261,40 @@ def test_static_input_gathered_once():
     y = torch.ones(3, 4)
     assert b._gathered(y).shape == (6, 4) and ex.gathers == 2
     assert b._gathered(x[:2]) is not full           # a different view is not the input
+
+
+def test_column_blocks_restore_rows():
+    """partition.column_blocks (CPU tensors): block q holds each row's edges
+    whose column rank q owns, rebased to s_q; concatenating the blocks' rows in
+    q order restores every CSR row."""
+    import numpy as np
+    import torch
+
+    from paper_2411_01109_b200.device import CsrView
+    from paper_2411_01109_b200.partition import column_blocks, split_points
+
+    rng = np.random.default_rng(3)
+    n = 500
+    deg = rng.integers(0, 40, n)
+    rows = np.repeat(np.arange(n), deg)
+    cols = rng.integers(0, n, rows.size)
+    key = np.unique(rows * n + cols)
+    rows, cols = key // n, key % n
+    off = np.zeros(n + 1, np.int64)
+    np.add.at(off, rows + 1, 1)
+    off = np.cumsum(off)
+    view = CsrView(torch.from_numpy(off), torch.from_numpy(cols.astype(np.int32)), n, n)
+    for parts in (1, 2, 5):
+        splits = split_points(torch.from_numpy(off), parts)
+        blocks = column_blocks(view, splits)
+        assert len(blocks) == parts
+        assert sum(b.num_edges for b in blocks) == cols.size
+        for q, b in enumerate(blocks):
+            assert b.n_rows == n and b.n_cols == splits[q + 1] - splits[q]
+            bc = b.cols.numpy()
+            assert bc.size == 0 or (bc.min() >= 0 and bc.max() < b.n_cols)
+        for r in range(n):
+            cat = np.concatenate([blocks[q].cols.numpy()[int(blocks[q].offsets[r]):
+                                                        int(blocks[q].offsets[r + 1])]
+                                  + splits[q] for q in range(parts)])
+            np.testing.assert_array_equal(cat, cols[off[r]:off[r + 1]])

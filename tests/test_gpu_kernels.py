@@ -666,6 +666,55 @@ def test_gat_attention_fast_vs_f64(cuda, heads):
     assert np.all(np.abs(got_r.astype(np.float64) - want_r) <= 2e-3 * np.maximum(1, np.abs(want_r)))
 
 
+@pytest.mark.parametrize("f", [16, 48, 64, 128])
+@pytest.mark.parametrize("parts,packs", [(2, False), (3, True), (8, False), (8, True)])
+def test_spmm_acc_column_blocks_chain(cuda, f, parts, packs):
+    """hg_spmm_acc chained over the column blocks of a CSR (partition.column_blocks)
+    == hg_spmm on the whole CSR: bitwise on every row that is one work unit in
+    each block (short rows, packed or not), within the Appendix-A bound of
+    float64 on split hub rows; block concatenation restores every row."""
+    from paper_2411_01109_b200 import device as D
+    from paper_2411_01109_b200.partition import column_blocks
+
+    n = 6000
+    r, c = _hub_graph(parts + f, n)
+    dg = _dg(n, r, c, cuda)
+    view = dg.view(False)
+    splits = np.linspace(0, n, parts + 1).astype(np.int64)
+    blocks = column_blocks(view, splits)
+    # structure: rows of the blocks concatenated in q order = the original rows
+    off = view.offsets.cpu().numpy()
+    cols = view.cols.cpu().numpy()
+    bo = [b.offsets.cpu().numpy() for b in blocks]
+    bc = [b.cols.cpu().numpy() for b in blocks]
+    for row in (0, 1, 2, 3, 7, 100, 5999):
+        cat = np.concatenate([bc[q][bo[q][row]:bo[q][row + 1]] + splits[q] for q in range(parts)])
+        np.testing.assert_array_equal(cat, cols[off[row]:off[row + 1]])
+    x = torch.randn(n, f, device=cuda, dtype=torch.float16)
+    fout = torch.rand(n, device=cuda, dtype=torch.float16)
+    saved = D.PACK_MIN_ROWS
+    D.PACK_MIN_ROWS = 0 if packs else 1 << 40
+    try:
+        want = D.spmm_csr(view, x, None, None, 1, "discretized", fout=fout)
+        acc = torch.empty(n, f, device=cuda, dtype=torch.float32)
+        got = None
+        for q, b in enumerate(blocks):
+            got = D.spmm_csr_acc(b, x[int(splits[q]):int(splits[q + 1])],
+                                 acc_in=None if q == 0 else acc,
+                                 acc_out=None if q == parts - 1 else acc, scaling="discretized",
+                                 fout=fout if q == parts - 1 else None)
+    finally:
+        D.PACK_MIN_ROWS = saved
+    deg = np.diff(off)
+    single = deg <= D.DEFAULT_SPLIT_CAP
+    g, w = got.cpu().numpy(), want.cpu().numpy()
+    np.testing.assert_array_equal(bits(g[single]), bits(w[single]))
+    fo = fout.cpu().numpy().astype(np.float64)
+    f64 = O.spmm_f64(n, r, c, x.cpu().numpy(), None, None, fo)
+    gg, ww = g.astype(np.float64), w.astype(np.float64)
+    assert np.all(np.abs(gg - f64) <= 1e-2 * np.maximum(1.0, np.abs(f64)) + np.abs(ww - f64))
+
+
 @pytest.mark.parametrize("heads,fh", [(1, 64), (4, 32), (4, 16), (8, 8), (2, 6), (4, 128)])
 @pytest.mark.parametrize("packs", [False, True])
 def test_gat_fused_forward_bitwise_equals_composed(cuda, heads, fh, packs):
