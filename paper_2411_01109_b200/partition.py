@@ -19,12 +19,13 @@ E/P per rank instead of the E an all-gather would deliver).
 Weight gradients and the loss are all-reduced (the data-parallel sum).
 
 Comm/compute overlap (`overlap=True`, the default on CUDA): each
-rank's CSR (and CSC) rows are also split into P column blocks by the rank that
-owns each column (`column_blocks`).  An unweighted aggregation then receives
-the P feature slabs as P ordered NCCL broadcasts (async) and runs block q as
-soon as slab q has landed, carrying the rows' fp32 sums from block to block
-(hg_spmm_acc) and rounding once after the last block: the SpMM of the first
-slabs overlaps the transfer of the later ones.  The blocks run in ascending
+rank's CSR (and CSC) rows are also split into G column blocks, runs of
+consecutive ranks' columns (`column_blocks`, G from the rows' degree:
+`block_groups`).  An aggregation then receives the feature rows as P ordered
+async NCCL broadcasts and runs block g as soon as its ranks' rows have landed,
+carrying the rows' fp32 sums from block to block (hg_spmm_acc) and rounding
+once after the last: the SpMM of the first blocks overlaps the transfer of
+the later ones.  The blocks run in ascending
 column order, so every row that is a single work unit in each block sums in
 exactly the unblocked order (bitwise equal); split hub rows regroup their
 fp32 carries (within the fast-path tolerance).
@@ -139,12 +140,32 @@ def make_local_part(offsets, cols, t_offsets, t_cols, perm, rank, parts) -> Loca
                      send_counts, recv_counts)
 
 
+def block_bounds(splits: np.ndarray, groups: int) -> np.ndarray:
+    """Column-block boundaries: `groups` runs of consecutive ranks (as equal in
+    rank count as possible), given as vertex ids (a subset of the splits)."""
+    parts = len(splits) - 1
+    g = max(1, min(groups, parts))
+    idx = np.round(np.linspace(0, parts, g + 1)).astype(np.int64)
+    return np.asarray(splits)[idx]
+
+
+def block_groups(view: CsrView, parts: int) -> int:
+    """Column blocks worth running for a rank's rows: each block re-reads and
+    re-writes the rows' fp32 sums and walks every row once (C5 rank 0 at P = 8,
+    F = 128: 1.57 ms unblocked, +0.77 ms per extra block), so blocks pay only
+    while they keep ~4 edges per row.  Measured per-block SpMM times with the
+    transfer modelled at 900 GB/s (tools/overlap_timeline.py, profiles/r02):
+    C5 (15.6 edges per row) 5.61 ms serial -> 5.17 ms at 4 blocks, 7.20 ms at 8."""
+    deg = view.num_edges / max(1, view.n_rows)
+    return max(1, min(parts, int(deg // 4)))
+
+
 def column_blocks(view: CsrView, splits: np.ndarray) -> list:
-    """Split a CSR whose rows hold sorted global column ids into P CSRs by the
-    rank owning each column: block q keeps, row by row and in order, the edges
-    with a column in [s_q, s_{q+1}), column ids rebased to s_q (they index rank
-    q's feature slab).  Concatenating the blocks' rows in q order gives back
-    each original row."""
+    """Split a CSR whose rows hold sorted global column ids into CSRs by column
+    range: block q keeps, row by row and in order, the edges with a column in
+    [splits[q], splits[q+1]) (a rank's range, or a run of ranks'), column ids
+    rebased to splits[q] (they index that range of the gathered rows).
+    Concatenating the blocks' rows in q order gives back each original row."""
     off, cols = view.offsets, view.cols
     dev = cols.device
     n, e = view.n_rows, cols.numel()
@@ -210,37 +231,30 @@ class Exchange:
             self.dist.all_gather(self._views(out), x_local)
         return out
 
-    def gather_slabs(self, x_local: torch.Tensor):
-        """(slabs, waits): rank q's rows as slab q (slab `rank` is x_local
-        itself), for a column-blocked aggregation.  NCCL: P async broadcasts
-        issued in rank order on the process group's stream; waits[q]() makes
-        the current stream wait for slab q only, so the SpMM of the slabs that
-        have landed overlaps the transfer of the rest.  gloo: one staged
+    def gather_async(self, x_local: torch.Tensor):
+        """(full, waits): the all-gathered [N, ...] rows in global order, filled
+        by P async NCCL broadcasts issued in rank order on the process group's
+        stream (this rank's rows copied in place); waits[q]() makes the current
+        stream wait until ranks 0..q have landed, so an aggregation over the
+        rows already there overlaps the transfer of the rest.  gloo: one staged
         all-gather, no waits."""
         p = self.part
         x_local = x_local.contiguous()
+        if self.staged:
+            return self.gather_rows(x_local), [None] * p.parts
         tail = tuple(x_local.shape[1:])
         row = x_local[0].numel() * x_local.element_size() if x_local.shape[0] else 0
         n = int(p.splits[-1])
         self.recv_bytes += (n - p.n_local) * row
         self.gathers += 1
-        if self.staged:
-            full = x_local.new_empty((n,) + tail)
-            send = x_local.new_zeros((p.n_max,) + tail, device="cpu")
-            send[: p.n_local] = x_local.cpu()
-            host = send.new_empty((p.parts * p.n_max,) + tail)
-            self.dist.all_gather_into_tensor(host, send)
-            for q, v in enumerate(self._views(full)):
-                v.copy_(host[q * p.n_max: q * p.n_max + v.shape[0]])
-            return self._views(full), [None] * p.parts
-        slabs, waits = [], []
+        full = x_local.new_empty((n,) + tail)
+        views = self._views(full)
+        views[p.rank].copy_(x_local)
+        waits = []
         for q in range(p.parts):
-            buf = x_local if q == p.rank else x_local.new_empty(
-                (int(p.splits[q + 1] - p.splits[q]),) + tail)
-            work = self.dist.broadcast(buf, src=q, async_op=True)
-            slabs.append(buf)
+            work = self.dist.broadcast(views[q], src=q, async_op=True)
             waits.append(None if q == p.rank else work.wait)
-        return slabs, waits
+        return full, waits
 
     def gather_edges(self, v_local: torch.Tensor) -> torch.Tensor:
         """Per-edge values ([E_local, ...], CSR order) -> the values of this
@@ -349,10 +363,13 @@ class DistBundle:
         self._blocks = {}
 
     def blocks(self, transpose):
-        """The P column blocks of the local CSR (forward) or CSC (backward)."""
+        """(bounds, column blocks) of the local CSR (forward) or CSC (backward):
+        block_groups() runs of consecutive ranks' columns."""
         b = self._blocks.get(transpose)
         if b is None:
-            b = column_blocks(self.part.bwd if transpose else self.part.fwd, self.part.splits)
+            view = self.part.bwd if transpose else self.part.fwd
+            bounds = block_bounds(self.part.splits, block_groups(view, self.part.parts))
+            b = (bounds, column_blocks(view, bounds))
             self._blocks[transpose] = b
         return b
 
@@ -365,7 +382,7 @@ class DistBundle:
         if w is None:
             view = self.part.bwd if transpose else self.part.fwd
             w = [(view.perm.long()[b.perm.long()].to(torch.int32).clone() if via_perm
-                  else b.perm) for b in self.blocks(transpose)]
+                  else b.perm) for b in self.blocks(transpose)[1]]
             self._blocks[key] = w
         return w
 
@@ -375,21 +392,24 @@ class DistBundle:
         slab q has landed, rows' fp32 sums carried from block to block
         (hg_spmm_acc), rounded (scaling, out factor) after the last.  Edge
         weights (GAT's alpha) follow each block edge to its unblocked slot."""
-        blocks = self.blocks(transpose)
+        bounds, blocks = self.blocks(transpose)
         widx = self._block_windex(transpose, via_perm) if w is not None else None
-        if full is not None:      # a static input gathered earlier: slabs are views
-            slabs, waits = self.ex._views(full), [None] * self.part.parts
-        else:
-            slabs, waits = self.ex.gather_slabs(xs_local)
-        f = slabs[0].shape[1]
+        waits = [None] * self.part.parts
+        if full is None:          # (a static input was gathered earlier)
+            full, waits = self.ex.gather_async(xs_local)
+        f = full.shape[1]
         n = self.part.n_local
-        acc = torch.empty((n, f), dtype=torch.float32, device=slabs[0].device)
+        acc = torch.empty((n, f), dtype=torch.float32, device=full.device) if len(blocks) > 1 \
+            else None
+        splits = [int(v) for v in self.part.splits]
         out = None
         last = len(blocks) - 1
-        for q, (view, slab) in enumerate(zip(blocks, slabs)):
-            if waits[q] is not None:
-                waits[q]()
-            out = D.spmm_csr_acc(view, slab, acc_in=None if q == 0 else acc,
+        for q, view in enumerate(blocks):
+            lo, hi = int(bounds[q]), int(bounds[q + 1])
+            for r in range(splits.index(lo), splits.index(hi)):   # the block's ranks landed
+                if waits[r] is not None:
+                    waits[r]()
+            out = D.spmm_csr_acc(view, full[lo:hi], acc_in=None if q == 0 else acc,
                                  acc_out=None if q == last else acc, scaling=scaling,
                                  fout=fout if q == last else None, w=w,
                                  w_index=None if widx is None else widx[q], heads=heads)
