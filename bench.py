@@ -305,6 +305,39 @@ def spmm_sweep(dg, peak, feats=(16, 32, 64, 128, 256, 512), reps=3):
     return out
 
 
+def parity_block(dg, f=64, n_random=2000, n_hubs=20, seed=0):
+    """Parity of the benched aggregation on the benched graph: the fp32-guarded
+    SpMM (discretized / both norm, F = 64, as the first GCN aggregation) on
+    the top-degree hub rows (the split rows with fp32 carries) plus random rows,
+    against a float64 segment sum computed here with torch (the Appendix-A
+    rule |y - y64| <= 1e-2 max(1, |y64|))."""
+    import torch
+
+    from paper_2411_01109_b200 import device as D
+
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    x = torch.randn(dg.n, f, device="cuda", dtype=torch.float16, generator=g)
+    y = D.spmm(dg, x, None, "discretized", "both")
+    fin, fout = dg.norm_tables("both", False, torch.float16)
+    deg = dg.offsets[1:] - dg.offsets[:-1]
+    hubs = torch.topk(deg, min(n_hubs, dg.n)).indices
+    rnd = torch.randint(0, dg.n, (n_random,), device="cuda", generator=g)
+    rows = torch.unique(torch.cat([hubs, rnd]))
+    lo, cnt = dg.offsets[rows], deg[rows]
+    seg = torch.repeat_interleave(torch.arange(rows.numel(), device="cuda"), cnt)
+    starts = torch.cumsum(cnt, 0) - cnt
+    eidx = lo[seg] + (torch.arange(seg.numel(), device="cuda") - starts[seg])
+    c = dg.cols[eidx].long()
+    contrib = x[c].double() * fin[c].double()[:, None]
+    s64 = torch.zeros(rows.numel(), f, dtype=torch.float64, device="cuda").index_add_(0, seg, contrib)
+    y64 = s64 * fout[rows].double()[:, None]
+    err = ((y[rows].double() - y64).abs() / y64.abs().clamp(min=1.0)).max().item()
+    return {"kernel": "hg_spmm (fast, discretized/both, F=64)", "rows_checked": int(rows.numel()),
+            "hub_rows": int(hubs.numel()), "edges_checked": int(seg.numel()),
+            "max_mixed_err": float(err), "bound": 1e-2, "ok": bool(err <= 1e-2),
+            "reference": "float64 segment sum (torch, in this run)"}
+
+
 def small_configs(args, peak):
     """C1 (Cora-shaped 2-layer GCN) and C2 (Pubmed-shaped 3-layer 4-head GAT):
     device-timed ms/epoch, plus the oracle port's epoch on the same graph."""
@@ -599,6 +632,8 @@ def b200_arm(args, ws, rank, local):
             "grad_scale": (tr.inner if use_dist else tr).grad_scale,
             "setup_s": round(setup_s, 1),
         }
+    if rank == 0 and ws == 1 and args.workload in ("gcn-reddit", "gin-products", "gat-rmat"):
+        result["parity"] = parity_block(dg)
     if not args.no_sweep and ws == 1 and args.workload == "gcn-reddit":
         result["spmm_sweep_reddit"] = spmm_sweep(dg, peak)
     if rank == 0 and ws == 1 and not args.no_small and args.workload == "gcn-reddit":

@@ -286,10 +286,14 @@ int hg_head_dots_bwd(const void* z, const void* a_l, const void* a_r, const void
  *   c1 = fp32(1 - b1^t), c2 = fp32(1 - b2^t) with t = *step (device fp64).
  * omb1/omb2 are fp32(1 - b1) / fp32(1 - b2) formed in double by the caller.
  * g is read from `grad` (dtype), widened and multiplied by grad_unscale (1 for
- * the reference; 2^-k undoes a static power-of-two loss scale exactly). */
+ * the reference; 2^-k undoes a static power-of-two loss scale exactly).
+ * pub_out (may be NULL): the next step's published copy, rnd(p) in pub_dtype
+ * (Param.publish, models.py:418-433); grad_zero (may be NULL): a pub_dtype
+ * gradient buffer zeroed after use (the next step's accumulation target). */
 int hg_adam_step(float* master, float* m, float* v, const void* grad, int grad_dtype,
                  int64_t count, float lr, float omb1, float omb2, double b1, double b2,
-                 float eps, const double* step, float grad_unscale, void* stream);
+                 float eps, const double* step, float grad_unscale, void* pub_out,
+                 void* grad_zero, int pub_dtype, void* stream);
 
 /* ------------------------------------------------------ dense GEMM (tcgen05) */
 

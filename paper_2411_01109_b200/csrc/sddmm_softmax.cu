@@ -1565,11 +1565,12 @@ __global__ void k_head_dots_bwd_fold(const float* __restrict__ part, int nblk, i
   }
 }
 
-template <typename G>
+template <typename G, typename PT>
 __global__ void k_adam(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
                        const G* __restrict__ grad, int64_t count, float lr, float omb1,
                        float omb2, double b1, double b2, float eps,
-                       const double* __restrict__ step, float unscale) {
+                       const double* __restrict__ step, float unscale, PT* __restrict__ pub,
+                       PT* __restrict__ gzero) {
   const double t = *step;
   const float c1 = (float)(1.0 - pow(b1, t)), c2 = (float)(1.0 - pow(b2, t));
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
@@ -1582,7 +1583,12 @@ __global__ void k_adam(float* __restrict__ p, float* __restrict__ m, float* __re
     v[i] = vi;
     const float num = __fmul_rn(lr, __fdiv_rn(mi, c1));
     const float den = __fadd_rn(__fsqrt_rn(__fdiv_rn(vi, c2)), eps);
-    p[i] = __fsub_rn(p[i], __fdiv_rn(num, den));
+    const float pn = __fsub_rn(p[i], __fdiv_rn(num, den));
+    p[i] = pn;
+    // the next step's published copy (ParamGroup.publish: RN cast of the
+    // master) and its zeroed gradient, fused here instead of two more passes
+    if (pub) pub[i] = Num<PT>::from_f(pn);
+    if (gzero) gzero[i] = Num<PT>::zero();
   }
 }
 
@@ -1624,17 +1630,27 @@ extern "C" int hg_head_dots(const void* z, const void* a_l, const void* a_r, int
 extern "C" int hg_adam_step(float* master, float* m, float* v, const void* grad, int grad_dtype,
                             int64_t count, float lr, float omb1, float omb2, double b1, double b2,
                             float eps, const double* step, float grad_unscale,
-                            void* stream) {
+                            void* pub_out, void* grad_zero, int pub_dtype, void* stream) {
   HG_REQUIRE(grad_dtype == HG_F16 || grad_dtype == HG_F32, "unknown dtype %d", grad_dtype);
+  HG_REQUIRE(pub_dtype == HG_F16 || pub_dtype == HG_F32, "unknown dtype %d", pub_dtype);
+  HG_REQUIRE(!(grad_zero == grad && grad_dtype != pub_dtype), "hg_adam_step: grad_zero aliases grad of another dtype");
   if (count == 0) return HG_OK;
   cudaStream_t st = as_stream(stream);
   const int g = grid_for(count, 256, 148 * 8);
-  if (grad_dtype == HG_F16)
-    k_adam<__half><<<g, 256, 0, st>>>(master, m, v, (const __half*)grad, count, lr, omb1, omb2,
-                                      b1, b2, eps, step, grad_unscale);
+  if (grad_dtype == HG_F16 && pub_dtype == HG_F16)
+    k_adam<__half, __half><<<g, 256, 0, st>>>(master, m, v, (const __half*)grad, count, lr, omb1,
+                                              omb2, b1, b2, eps, step, grad_unscale,
+                                              (__half*)pub_out, (__half*)grad_zero);
+  else if (grad_dtype == HG_F32 && pub_dtype == HG_F16)
+    k_adam<float, __half><<<g, 256, 0, st>>>(master, m, v, (const float*)grad, count, lr, omb1,
+                                             omb2, b1, b2, eps, step, grad_unscale,
+                                             (__half*)pub_out, (__half*)grad_zero);
+  else if (grad_dtype == HG_F32)
+    k_adam<float, float><<<g, 256, 0, st>>>(master, m, v, (const float*)grad, count, lr, omb1,
+                                            omb2, b1, b2, eps, step, grad_unscale,
+                                            (float*)pub_out, (float*)grad_zero);
   else
-    k_adam<float><<<g, 256, 0, st>>>(master, m, v, (const float*)grad, count, lr, omb1, omb2,
-                                     b1, b2, eps, step, grad_unscale);
+    HG_REQUIRE(false, "hg_adam_step: fp16 gradients with an fp32 published copy");
   HG_LAUNCHED();
   return HG_OK;
 }

@@ -1108,13 +1108,17 @@ def head_dots(z, a_l, a_r, heads):
     return s_l, s_r
 
 
-def adam_step(master, m, v, grad, lr, b1, b2, eps, step, grad_unscale=1.0):
+def adam_step(master, m, v, grad, lr, b1, b2, eps, step, grad_unscale=1.0, pub=None,
+              grad_zero=None):
     """One fused Adam update over flat fp32 arrays (hg_adam_step); `step` is the
     device fp64 step count (already incremented); the gradient is multiplied by
-    grad_unscale (exact for a power of two) before use."""
+    grad_unscale (exact for a power of two) before use.  pub: also write the
+    next step's published copy rnd(master); grad_zero: a gradient buffer of
+    pub's dtype to clear for the next step's accumulation."""
+    pdt = _dtype_code(pub if pub is not None else (grad_zero if grad_zero is not None else grad))
     nat.call("hg_adam_step", _p(master), _p(m), _p(v), _p(grad), _dtype_code(grad),
              master.numel(), float(lr), float(1 - b1), float(1 - b2), float(b1), float(b2),
-             float(eps), _p(step), float(grad_unscale), _stream())
+             float(eps), _p(step), float(grad_unscale), _p(pub), _p(grad_zero), pdt, _stream())
     Probe.launches += 1
 
 

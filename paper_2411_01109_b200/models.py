@@ -631,11 +631,20 @@ class ParamGroup:
             p.published = leaf
             p.group = self
         self._ptrs = [p.published.grad.data_ptr() for p in self.params]
+        self.fresh = False   # True: pub / grad already prepared by the fused Adam step
 
     @torch.no_grad()
     def publish(self):
         self.pub.copy_(self.master)
         self.grad.zero_()
+        self.fresh = False
+
+    def publish_if_stale(self):
+        """publish() unless the last fused Adam step already wrote the published
+        copy and cleared the gradient; either way the state is consumed."""
+        if not self.fresh:
+            self.publish()
+        self.fresh = False
 
     def check_grads(self):
         """True if autograd accumulated in place into the flat gradient."""
@@ -1045,8 +1054,11 @@ class Adam:
         g = self.group
         if g is not None and g.master.is_cuda and (flat_grad is not None or g.check_grads()):
             grad = g.grad if flat_grad is None else flat_grad
+            # the kernel also publishes the next step's weights and clears the
+            # gradient (ParamGroup.publish fused away: g.fresh)
             D.adam_step(g.master, self.m, self.v, grad, self.lr, b1, b2, self.eps, self._t,
-                        self.grad_unscale)
+                        self.grad_unscale, pub=g.pub, grad_zero=g.grad)
+            g.fresh = True
             return
         if flat_grad is not None:
             for o, p in zip(_offsets(self.params), self.params):
@@ -1195,7 +1207,7 @@ class Trainer:
 
     def _step_eager(self, overflow=None):
         cfg = self.cfg
-        self.group.publish()
+        self.group.publish_if_stale()
         logits = self.model.forward(self.bundle, self.x, cfg.mode, cfg.width, overflow)
         loss = self.loss_backward(logits, D.softmax_xent, logits.shape[0])
         self.opt.step()

@@ -628,7 +628,7 @@ class DistTrainer:
     def _step_eager(self, overflow=None):
         tr = self.inner
         cfg = tr.cfg
-        tr.group.publish()
+        tr.group.publish_if_stale()
         logits = tr.model.forward(self.bundle, tr.x, cfg.mode, cfg.width, overflow)
         loss = tr.loss_backward(logits, self.bundle.ops.xent, self.n_total)
         if not tr.group.check_grads():
