@@ -122,7 +122,13 @@ int hg_schedule_build(const int64_t* offsets, int64_t n, int32_t split_cap, int3
  * packs / num_packs: the hg_schedule_build packs of the same CSR (NULL / 0 when
  * the schedule was built without packing), pack_rowid: int32 row id per edge
  * (needed with packs); a packed row's result is bitwise the one it gets as its
- * own unit. */
+ * own unit.
+ * split_counters / slot_split (both NULL: a separate follow-up launch folds
+ * the split rows' carries): int32 [num_split_rows] arrival counters, all zero
+ * (and left zero), and int32 [num_slots] = the split_rows index owning each
+ * slot; then the last unit of each split row to finish folds its carries in
+ * slot order inside the same launch (bitwise the follow-up's result).  Calls
+ * sharing the counters must be stream-ordered. */
 int hg_spmm_workspace(int64_t n_cols, int32_t F, int64_t num_slots, int has_in_scale,
                       int32_t sum_heads, int dtype, size_t* bytes);
 int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_rows, int64_t n_cols,
@@ -132,7 +138,8 @@ int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_rows, int64_t
             const void* w, const int32_t* w_index, int32_t heads, const void* x, void* y,
             int32_t F, int64_t ldx, int64_t ldy, int32_t scaling, int32_t relu,
             const void* in_scale, const void* out_factor, int64_t w_ld, int32_t w2_off,
-            void* out2, int dtype, void* ws, size_t ws_bytes, void* stream);
+            void* out2, int dtype, void* ws, size_t ws_bytes, void* stream,
+            int32_t* split_counters, const int32_t* slot_split);
 
 /* hg_spmm in fp32 partial mode, for column-blocked aggregation
  * (a row's edges split by the rank owning their column, block q run as soon as

@@ -44,7 +44,8 @@ SIGNATURES = {
     "hg_spmm_workspace": [_I64, _I32, _I64, c_int, _I32, c_int, _PSZ],
     "hg_spmm": [_P, _P, _I64, _I64, _I64, _P, _I64, _P, _I64, _I64, _P, _I64, _P, _P, _P, _I32,
                 _P, _P,
-                _I32, _I64, _I64, _I32, _I32, _P, _P, _I64, _I32, _P, c_int, _P, c_size_t, _P],
+                _I32, _I64, _I64, _I32, _I32, _P, _P, _I64, _I32, _P, c_int, _P, c_size_t, _P,
+                _P, _P],
     "hg_spmm_edge_ref_workspace": [_I64, _I64, _I32, _I32, _I32, c_int, c_int, _PSZ],
     "hg_spmm_edge_ref": [_P, _P, _I64, _I64, _I64, _I32, _I32, _P, _P, _P, _I32, _I32, _P, _P,
                          _P, _P, c_int, _P, c_size_t, _P],

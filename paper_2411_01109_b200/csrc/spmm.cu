@@ -466,7 +466,9 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
             float* __restrict__ carry2, const int64_t* __restrict__ offsets,
             const int32_t* __restrict__ rowid, const T* __restrict__ att_sl,
             const float2* __restrict__ att_stats, T* __restrict__ att_out, float att_slope,
-            const float* __restrict__ acc_in, float* __restrict__ acc_out, int acc_ld) {
+            const float* __restrict__ acc_in, float* __restrict__ acc_out, int acc_ld,
+            int* __restrict__ split_cnt, const int32_t* __restrict__ slot_split,
+            const int4* __restrict__ split_info) {
   using Team = FastTeam<T, V, TEAM, NCH, WEIGHTED, SUMW, PACKED, ATT>;
   constexpr int EB = Team::EB;
   constexpr int CPL = Team::CPL;
@@ -628,6 +630,59 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
     if (slot < 0) out2[(int64_t)row * heads + t.chead[0]] = Num<T>::from_f(t.acc2);
     else carry2[(int64_t)slot * heads + t.chead[0]] = t.acc2;
   }
+  if (slot >= 0 && split_cnt != nullptr) {
+    // Fused follow-up: the split row's last unit to finish (a per-row arrival
+    // counter) folds the fp32 carries in slot order -- the arithmetic of
+    // k_spmm_fast_followup, so bitwise the same -- and re-arms the counter.
+    __threadfence();
+    __syncwarp(t.tmask);
+    int si = 0, last = 0;
+    if (tl == 0) {
+      si = __ldg(slot_split + slot);
+      last = atomicAdd(split_cnt + si, 1) == __ldg(&split_info[si].z) - 1;
+    }
+    si = __shfl_sync(t.tmask, si, t.tbase);
+    last = __shfl_sync(t.tmask, last, t.tbase);
+    if (last) {
+      __threadfence();
+      const int4 sr = split_info[si];
+      const T fo = fout ? fout[sr.x] : Num<T>::zero();
+#pragma unroll
+      for (int k = 0; k < NCH; ++k) {
+        if (!t.cval[k]) continue;
+        const int64_t col = t.xl[k] - x;
+        float a2[V];
+#pragma unroll
+        for (int i = 0; i < V; ++i) a2[i] = 0.0f;
+        for (int q = 0; q < sr.z; ++q) {
+          const float* src = carry + (int64_t)(sr.y + q) * F + col;
+          float b2[V];
+          if constexpr (V % 4 == 0) {
+#pragma unroll
+            for (int i = 0; i < V; i += 4) {
+              const float4 v = __ldcg(reinterpret_cast<const float4*>(src + i));
+              b2[i] = v.x; b2[i + 1] = v.y; b2[i + 2] = v.z; b2[i + 3] = v.w;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < V; ++i) b2[i] = __ldcg(src + i);
+          }
+#pragma unroll
+          for (int i = 0; i < V; ++i) a2[i] += b2[i];
+        }
+        if (acc_out) store_carry<V>(acc_out + (int64_t)sr.x * acc_ld + col, a2);
+        else store_out<T, V>(y + (int64_t)sr.x * ldy + col, a2, fmode, fo);
+      }
+      if (SUMW) {
+        for (int hh = tl; hh < heads; hh += TEAM) {
+          float sum = 0.0f;
+          for (int q = 0; q < sr.z; ++q) sum += __ldcg(carry2 + (int64_t)(sr.y + q) * heads + hh);
+          out2[(int64_t)sr.x * heads + hh] = Num<T>::from_f(sum);
+        }
+      }
+      if (tl == 0) split_cnt[si] = 0;
+    }
+  }
 }
 
 // One team per split row: fp32 carries folded in slot (edge) order.
@@ -712,6 +767,8 @@ struct FastArgs {
   const float* acc_in;     // fp32 partial mode (hg_spmm_acc)
   float* acc_out;
   int acc_ld;
+  int* split_cnt;          // fused follow-up (hg_spmm split_counters / slot_split)
+  const int32_t* slot_split;
   cudaStream_t st;
 };
 
@@ -729,7 +786,8 @@ static int launch_fast(const FastArgs& a) {
         a.units, a.num_units, a.cols, a.num_edges, (const T*)a.w, a.widx, a.heads, a.fh,
         (const T*)a.x, (T*)a.y, a.carry, a.F, a.ldx, a.ldy, a.fmode, (const T*)a.fout,
         a.wld, a.w2off, (T*)a.out2, a.carry2, a.offsets, nullptr, (const T*)a.att_sl,
-        a.att_stats, (T*)a.att_out, a.att_slope, a.acc_in, a.acc_out, a.acc_ld);
+        a.att_stats, (T*)a.att_out, a.att_slope, a.acc_in, a.acc_out, a.acc_ld, a.split_cnt,
+        a.slot_split, a.split_rows);
     HG_LAUNCHED();
   }
   if (a.num_packs > 0) {
@@ -738,10 +796,11 @@ static int launch_fast(const FastArgs& a) {
         a.packs, a.num_packs, a.cols, a.num_edges, (const T*)a.w, a.widx, a.heads, a.fh,
         (const T*)a.x, (T*)a.y, nullptr, a.F, a.ldx, a.ldy, a.fmode, (const T*)a.fout,
         a.wld, a.w2off, (T*)a.out2, nullptr, a.offsets, a.rowid, (const T*)a.att_sl,
-        a.att_stats, (T*)a.att_out, a.att_slope, a.acc_in, a.acc_out, a.acc_ld);
+        a.att_stats, (T*)a.att_out, a.att_slope, a.acc_in, a.acc_out, a.acc_ld, nullptr,
+        nullptr, nullptr);
     HG_LAUNCHED();
   }
-  if (a.num_split > 0) {
+  if (a.num_split > 0 && a.split_cnt == nullptr) {
     int64_t blocks = (a.num_split + kThreads / TEAMF - 1) / (kThreads / TEAMF);
     k_spmm_fast_followup<T, V, TEAMF, NCH><<<(unsigned)blocks, kThreads, 0, a.st>>>(
         a.split_rows, a.num_split, a.carry, (T*)a.y, a.F, a.ldy, a.fmode, (const T*)a.fout,
@@ -886,7 +945,8 @@ static int spmm_impl(const int64_t* offsets, const int32_t* cols, int64_t n_rows
                      void* y, int32_t F, int64_t ldx, int64_t ldy, int32_t scaling,
                      int32_t relu, const void* in_scale, const void* out_factor,
                      int64_t w_ld, int32_t w2_off, void* out2, int dtype, void* ws,
-                     size_t ws_bytes, void* stream, const float* acc_in, float* acc_out) {
+                     size_t ws_bytes, void* stream, const float* acc_in, float* acc_out,
+                     int32_t* split_counters = nullptr, const int32_t* slot_split = nullptr) {
   HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
   HG_REQUIRE(F > 0 && F % 2 == 0, "feature length %d must be even and positive", F);
   HG_REQUIRE(heads >= 1 && F % heads == 0 && (F / heads) % 2 == 0,
@@ -940,6 +1000,10 @@ static int spmm_impl(const int64_t* offsets, const int32_t* cols, int64_t n_rows
   a.fout = out_factor; a.st = st;
   a.wld = (int)w_ld; a.w2off = w2_off; a.out2 = out2; a.carry2 = carry2;
   a.acc_in = acc_in; a.acc_out = acc_out; a.acc_ld = F;
+  if (split_counters && slot_split && num_split_rows > 0) {
+    a.split_cnt = split_counters;
+    a.slot_split = slot_split;
+  }
   // Column slabs: when X (n_cols x F) overflows the L2 budget but a slab of
   // >= 32 columns fits, aggregate slab by slab so the random row gathers of
   // each pass hit L2 (the column stream is re-read once per slab, sequentially).
@@ -966,11 +1030,12 @@ extern "C" int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_ro
                        void* y, int32_t F, int64_t ldx, int64_t ldy, int32_t scaling,
                        int32_t relu, const void* in_scale, const void* out_factor,
                        int64_t w_ld, int32_t w2_off, void* out2, int dtype, void* ws,
-                       size_t ws_bytes, void* stream) {
+                       size_t ws_bytes, void* stream, int32_t* split_counters,
+                       const int32_t* slot_split) {
   return spmm_impl(offsets, cols, n_rows, n_cols, num_edges, units, num_units, split_rows,
                    num_split_rows, num_slots, packs, num_packs, pack_rowid, w, w_index, heads, x, y,
                    F, ldx, ldy, scaling, relu, in_scale, out_factor, w_ld, w2_off, out2, dtype, ws,
-                   ws_bytes, stream, nullptr, nullptr);
+                   ws_bytes, stream, nullptr, nullptr, split_counters, slot_split);
 }
 
 extern "C" int hg_spmm_acc(const int64_t* offsets, const int32_t* cols, int64_t n_rows,

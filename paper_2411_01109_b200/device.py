@@ -28,6 +28,11 @@ from . import _native as nat
 DTYPE_CODE = {torch.float16: nat.HG_F16, torch.float32: nat.HG_F32}
 MIRROR = {"none": "none", "left": "right", "right": "left", "both": "both"}
 DEFAULT_SPLIT_CAP = 512
+# HG_FUSED_FOLLOWUP=1: hg_spmm folds split rows' carries in the launch itself
+# (last-arriving unit, arrival counters).  Off by default: bitwise the same,
+# but measured no faster (C3 4.419 -> 4.438 ms, GIN 12.83 -> 12.94 ms: the
+# hub rows' last units serialise the fold at the tail of the launch).
+FUSED_FOLLOWUP = os.environ.get("HG_FUSED_FOLLOWUP", "0") == "1"
 # hg_spmm packs: aligned blocks of PACK_ROWS rows with few edges in total, walked
 # by one team as one edge stream (hg_schedule_build)
 PACK_ROWS = 16
@@ -320,6 +325,25 @@ class WorkSchedule:
     def num_units(self):
         return self.units.shape[0]
 
+    def finish_state(self):
+        """(arrival counters, slot -> split row) for hg_spmm's fused follow-up
+        (None, None without split rows).  The counters start zero and every
+        launch leaves them zero; launches sharing them must be stream-ordered."""
+        st = getattr(self, "_finish", None)
+        if st is None:
+            ns = self.split_rows.shape[0]
+            if ns == 0:
+                st = (None, None)
+            else:
+                dev = self.split_rows.device
+                cnt = torch.zeros(ns, dtype=torch.int32, device=dev)
+                slot_split = torch.repeat_interleave(
+                    torch.arange(ns, dtype=torch.int32, device=dev),
+                    self.split_rows[:, 2].long(), output_size=self.num_slots)
+                st = (cnt, slot_split)
+            self._finish = st
+        return st
+
 
 def build_schedule(offsets: torch.Tensor, split_cap: int = DEFAULT_SPLIT_CAP,
                    pack_rows: int = 0, pack_edges: int = 0) -> WorkSchedule:
@@ -519,6 +543,7 @@ def spmm_csr(view: CsrView, x: torch.Tensor, w=None, w_index=None, heads: int = 
         out = torch.empty((view.n_rows, f), dtype=x.dtype, device=x.device)
     elif not _row_strided(out) or out.shape != (view.n_rows, f) or out.dtype != x.dtype:
         raise ValueError("out must be [n_rows, F] with unit column stride")
+    fin_state = sched.finish_state() if FUSED_FOLLOWUP else (None, None)
     nbytes = nat.size_query("hg_spmm_workspace", view.n_cols, f, sched.num_slots,
                             int(fin is not None), heads if out2 is not None else 0, dt)
     ws = workspace(nbytes, x.device)
@@ -540,10 +565,9 @@ def spmm_csr(view: CsrView, x: torch.Tensor, w=None, w_index=None, heads: int = 
              _p(view.row_ids() if sched.num_packs else None), _p(w), _p(w_index), heads, _p(x),
              _p(out), f, x.stride(0), out.stride(0), nat.SCALING_CODES[scaling], int(relu),
              _p(fin), _p(fout), w_ld, int(w2_off), _p(out2), dt, _p(ws),
-             0 if ws is None else ws.numel(), _stream())
+             0 if ws is None else ws.numel(), _stream(), *map(_p, fin_state))
     Probe.launches += int(sched.num_units > 0) + int(sched.num_packs > 0) + int(
-        sched.split_rows.shape[0] > 0) + int(
-        fin is not None)
+        sched.split_rows.shape[0] > 0 and fin_state[0] is None) + int(fin is not None)
     if Probe.timing:
         ev1.record()
         Probe.records.append((ev0, ev1, spmm_bytes(view.n_rows, view.n_cols, view.num_edges, f,

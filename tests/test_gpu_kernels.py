@@ -666,6 +666,51 @@ def test_gat_attention_fast_vs_f64(cuda, heads):
     assert np.all(np.abs(got_r.astype(np.float64) - want_r) <= 2e-3 * np.maximum(1, np.abs(want_r)))
 
 
+@pytest.mark.parametrize("f", [8, 48, 64, 256])
+@pytest.mark.parametrize("mode", ["plain", "sumw"])
+def test_spmm_fused_followup_bitwise(cuda, f, mode):
+    """hg_spmm with split_counters / slot_split (the last unit of each split
+    row folds the carries) == the separate follow-up launch, bit for bit, and
+    the counters are left zero (graph replays reuse them)."""
+    from paper_2411_01109_b200 import device as D
+
+    n = 6000
+    r, c = _hub_graph(f, n)
+    dg = _dg(n, r, c, cuda)
+    view = dg.view(mode == "sumw")
+    heads = 4 if f % 64 == 0 else 1
+    x = torch.randn(n, f, device=cuda, dtype=torch.float16)
+    fout = torch.rand(n, device=cuda, dtype=torch.float16)
+    kw, extra = {}, {}
+    w = widx = None
+    if mode == "sumw":
+        if f > 256:
+            pytest.skip("summed weights need F/8 <= 32")
+        ae = torch.randn(r.size, 2 * heads, device=cuda, dtype=torch.float16)
+        w, widx = ae[:, :heads], view.perm
+        kw = dict(w2_off=heads)
+    outs = []
+    saved = D.FUSED_FOLLOWUP
+    try:
+        for fused in (False, True):
+            D.FUSED_FOLLOWUP = fused
+            if mode == "sumw":
+                extra = {"out2": torch.empty(n, heads, device=cuda, dtype=torch.float16)}
+            for _ in range(2):   # second call reuses the (re-armed) counters
+                y = D.spmm_csr(view, x, w, widx, heads if w is not None else 1, "discretized",
+                               fout=fout, **kw, **extra)
+            outs.append((y, extra.get("out2")))
+    finally:
+        D.FUSED_FOLLOWUP = saved
+    sched = view.schedule(D.DEFAULT_SPLIT_CAP, -1)
+    assert sched.split_rows.shape[0] > 0
+    cnt, _ = sched.finish_state()
+    assert int(cnt.abs().sum()) == 0
+    assert torch.equal(outs[0][0].view(torch.int16), outs[1][0].view(torch.int16))
+    if mode == "sumw":
+        assert torch.equal(outs[0][1].view(torch.int16), outs[1][1].view(torch.int16))
+
+
 @pytest.mark.parametrize("f", [16, 48, 64, 128])
 @pytest.mark.parametrize("parts,packs", [(2, False), (3, True), (8, False), (8, True)])
 def test_spmm_acc_column_blocks_chain(cuda, f, parts, packs):
