@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define HG_ABI_VERSION 3
+#define HG_ABI_VERSION 4
 
 enum { HG_OK = 0, HG_EINVAL = 1, HG_ECUDA = 2 };
 enum { HG_F16 = 0, HG_F32 = 1 };
@@ -332,6 +332,25 @@ int hg_gemm_wgrad_workspace(int64_t k, int64_t m, int32_t n, size_t* bytes);
 int hg_gemm_wgrad(const void* a, int64_t k, int64_t m, int64_t lda, const void* b, int32_t n,
                   int64_t ldb, void* out, int64_t ldo, void* bias_out, int32_t accumulate,
                   void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------- multi-GPU exchange */
+
+/* The row-partitioned feature exchange (SURVEY 8(b) hg_allgather_features,
+ * 8(e); Python: partition.Exchange over torch.distributed) for callers that
+ * hold their own NCCL communicator.  libnccl.so.2 is bound at run time
+ * (hg_nccl_available() = 0 when it cannot be loaded).  comm is an ncclComm_t.
+ *   hg_nccl_unique_id:     128-byte ncclUniqueId (rank 0 shares it out of band)
+ *   hg_nccl_comm_init:     ncclCommInitRank (the CUDA device current at the call)
+ *   hg_allgather_features: x_full[s_q .. s_{q+1}) = rank q's x_local for every q
+ *     (row_bytes bytes per row; splits: HOST int64[parts + 1], s_0 = 0, the
+ *     nnz-balanced split points); one NCCL group of exact-count broadcasts on
+ *     `stream`, no padding to the largest partition. */
+int hg_nccl_available(void);
+int hg_nccl_unique_id(void* id_out);
+int hg_nccl_comm_init(void** comm_out, int32_t nranks, const void* id, int32_t rank);
+int hg_nccl_comm_destroy(void* comm);
+int hg_allgather_features(void* comm, const void* x_local, void* x_full, const int64_t* splits,
+                          int32_t parts, int32_t rank, int64_t row_bytes, void* stream);
 
 /* ----------------------------------------------------------------- ingest */
 

@@ -18,7 +18,7 @@ from pathlib import Path
 LIB_PATH = Path(os.environ.get("HG_LIB") or Path(__file__).resolve().with_name("libhalfgnn.so"))
 
 HG_OK, HG_EINVAL, HG_ECUDA = 0, 1, 2
-ABI_VERSION = 3
+ABI_VERSION = 4
 HG_F16, HG_F32 = 0, 1
 SCALING_CODES = {"post": 0, "pre": 1, "discretized": 2}
 FACTOR_INV, FACTOR_INV_SQRT = 1, 2
@@ -75,6 +75,11 @@ SIGNATURES = {
     "hg_parse_edges": [_P, _I64, _I64, _P, _P, _PI64, _P, c_size_t, _P],
     "hg_gat_attention_fwd": [_P, _P, _I64, _P, _P, _I32, c_float, _P, _I64, _P, _I64, _P, _I64,
                              _I32, c_int, _P],
+    "hg_nccl_available": [],
+    "hg_nccl_unique_id": [_P],
+    "hg_nccl_comm_init": [_P, _I32, _P, _I32],
+    "hg_nccl_comm_destroy": [_P],
+    "hg_allgather_features": [_P, _P, _P, _P, _I32, _I32, _I64, _P],
     "hg_spmm_acc": [_P, _P, _I64, _I64, _I64, _P, _I64, _P, _I64, _I64, _P, _I64, _P, _P, _P,
                     _I32, _I64, _P, _P, _I32, _I64, _I64, _I32, _I32, _P, _P, _P, c_int, _P,
                     c_size_t, _P],

@@ -1161,3 +1161,54 @@ def head_dots_bwd(z, a_l, a_r, g_l, g_r, heads, gz_acc=None):
              _p(ga_r), _p(gz_acc), _dtype_code(z), _p(ws), ws.numel(), _stream())
     Probe.launches += 2
     return gz, ga_l, ga_r
+
+
+# ── multi-GPU exchange through the C ABI (callers with their own NCCL comm) ──
+
+
+class NcclComm:
+    """An NCCL communicator owned through the C ABI (hg_nccl_comm_init) -- the
+    path a non-Python host uses for the row-partitioned exchange.  Rank 0
+    makes the id (`unique_id()`) and shares it out of band."""
+
+    def __init__(self, nranks: int, rank: int, uid: bytes):
+        if len(uid) != 128:
+            raise ValueError("an ncclUniqueId is 128 bytes")
+        self.nranks, self.rank = nranks, rank
+        self._uid = ctypes.create_string_buffer(uid, 128)
+        self.handle = ctypes.c_void_p()
+        nat.call("hg_nccl_comm_init", ctypes.byref(self.handle), nranks, self._uid, rank)
+
+    @staticmethod
+    def available() -> bool:
+        return bool(nat.lib().hg_nccl_available())
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        nat.call("hg_nccl_unique_id", buf)
+        return buf.raw
+
+    def close(self):
+        if self.handle:
+            nat.call("hg_nccl_comm_destroy", self.handle)
+            self.handle = ctypes.c_void_p()
+
+
+def allgather_features(comm: NcclComm, x_local: torch.Tensor, splits, out=None):
+    """hg_allgather_features: [N, ...] rows in global order from every rank's
+    x_local (rows [splits[q], splits[q+1]) of rank q), exact counts."""
+    _require_cuda(x_local)
+    x_local = x_local.contiguous()
+    sp = [int(v) for v in splits]
+    n = sp[-1]
+    tail = tuple(x_local.shape[1:])
+    if out is None:
+        out = x_local.new_empty((n,) + tail)
+    row = x_local.element_size()
+    for d in tail:
+        row *= int(d)
+    arr = (ctypes.c_int64 * len(sp))(*sp)
+    nat.call("hg_allgather_features", comm.handle, _p(x_local), _p(out), arr, len(sp) - 1,
+             comm.rank, row, _stream())
+    return out

@@ -676,6 +676,8 @@ def test_spmm_fused_followup_bitwise(cuda, f, mode):
 
     n = 6000
     r, c = _hub_graph(f, n)
+    if mode == "sumw":   # hubs on the CSC side (the transposed view this mode reads)
+        r, c = O.canonical_edges(n, c, r)
     dg = _dg(n, r, c, cuda)
     view = dg.view(mode == "sumw")
     heads = 4 if f % 64 == 0 else 1
@@ -1220,3 +1222,23 @@ def test_spmm_interleaved_weights_and_second_sums(cuda, heads, fh):
     assert torch.equal(got, want)
     want2 = D.edge_sums_fast(bwd, ae[:, heads:].contiguous(), bwd.perm)
     assert torch.allclose(s2.float(), want2.float(), atol=2e-2, rtol=2e-3)
+
+
+def test_allgather_features_c_abi_one_rank(cuda):
+    """hg_allgather_features through the C ABI with a communicator made by
+    hg_nccl_comm_init (libnccl bound at run time): one rank (this box has one
+    GPU) -- the group of exact-count broadcasts copies the rank's rows into
+    place; bad splits are rejected."""
+    from paper_2411_01109_b200 import device as D
+
+    assert D.NcclComm.available()
+    comm = D.NcclComm(1, 0, D.NcclComm.unique_id())
+    try:
+        x = torch.randn(1000, 48, device=cuda, dtype=torch.float16)
+        full = D.allgather_features(comm, x, [0, 1000])
+        torch.cuda.synchronize()
+        assert torch.equal(full, x)
+        with pytest.raises(ValueError, match="splits"):
+            D.allgather_features(comm, x, [5, 1000])
+    finally:
+        comm.close()
