@@ -1,4 +1,5 @@
 # round-2 profiling pass (one B200): launch lists, per-call DRAM traffic, --set full captures
+# usage: gpurun -- bash tools/profile_r02.sh   (outputs in gpurun_out/r02/prof, copied to profiles/r02)
 P=gpurun_out/r02/prof; mkdir -p $P; T=/tmp/hgprof; mkdir -p $T
 for w in gcn-reddit gin-products gat-rmat; do
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $P/launch_$w.csv python tools/ncu_target.py --workload $w --epochs 3 > /dev/null 2>&1; echo launch_$w=$?
