@@ -27,7 +27,7 @@ from . import _native as nat
 
 DTYPE_CODE = {torch.float16: nat.HG_F16, torch.float32: nat.HG_F32}
 MIRROR = {"none": "none", "left": "right", "right": "left", "both": "both"}
-DEFAULT_SPLIT_CAP = 512
+DEFAULT_SPLIT_CAP = int(os.environ.get("HG_SPLIT_CAP", "512"))  # edges per work unit (A/B knob)
 # HG_FUSED_FOLLOWUP=1: hg_spmm folds split rows' carries in the launch itself
 # (last-arriving unit, arrival counters).  Off by default: bitwise the same,
 # but measured no faster (C3 4.419 -> 4.438 ms, GIN 12.83 -> 12.94 ms: the
