@@ -230,16 +230,16 @@ def reference_arm(args, ws, rank):
 WORKLOADS = {
     "gcn-reddit": dict(desc="GCN 2-layer train epoch, synthetic Reddit-shaped graph (C3)",
                        graph="reddit_like", feat=602, classes=41,
-                       cfg=dict(kind="gcn", hidden=64),
+                       cfg=dict(kind="gcn", hidden=64), reorder="degree",
                        l2="inputs larger than L2 (column stream 459 MB, features 280 MB)"),
     "gin-products": dict(desc="GIN 2-layer train epoch, synthetic ogbn-products-shaped "
                               "power-law graph (C4)",
                          graph="products_like", feat=100, classes=47,
-                         cfg=dict(kind="gin", hidden=64),
+                         cfg=dict(kind="gin", hidden=64), reorder="degree",
                          l2="inputs larger than L2 (column stream 495 MB, features 490 MB)"),
     "gat-rmat": dict(desc="GAT 2-layer 4-head train epoch, synthetic RMAT scale-24 graph (C5)",
                      graph="rmat", feat=128, classes=16,
-                     cfg=dict(kind="gat", hidden=32, heads=4),
+                     cfg=dict(kind="gat", hidden=32, heads=4), reorder="degree",
                      l2="inputs larger than L2 (column stream ~1 GB, features 4.3 GB)"),
     "gat-pubmed": dict(desc="GAT 3-layer 4-head train epoch, synthetic Pubmed-shaped graph (C2)",
                        graph="pubmed_like", feat=500, classes=3,
@@ -433,14 +433,24 @@ def b200_arm(args, ws, rank, local):
     dg, x, labels = build_workload(args.workload, args.seed)
     cfg = TrainConfig(mode="half", seed=args.seed, scaling="discretized", norm="both",
                       numerics="fast", grad_scale="auto", **WORKLOADS[args.workload]["cfg"])
+    # locality relabelling (device.locality_order): the same graph, features,
+    # labels and split per original vertex; hot rows packed together
+    reorder = args.reorder if args.reorder != "auto" else WORKLOADS[args.workload].get(
+        "reorder", "none")
+    order = None
+    if reorder == "degree":
+        order = D.locality_order(dg.offsets, dg.bwd.offsets, parts=ws)
+        dg = dg.relabel(order)
     if use_dist:
         from paper_2411_01109_b200.partition import DistTrainer
 
-        tr = DistTrainer(dg, x, labels, cfg, dist)
+        tr = DistTrainer(dg, x, labels, cfg, dist, node_order=order)
         parallelism = f"row-partition x{ws} ({dist.get_backend()} all-gather)"
     else:
-        tr = Trainer(GraphBundle.build(dg, numerics="fast"), x, labels, cfg)
+        tr = Trainer(GraphBundle.build(dg, numerics="fast"), x, labels, cfg, node_order=order)
         parallelism = "dp1"
+    if order is not None:
+        x = x[order]   # the trainer's vertex order (the e2e feed copies these rows)
     for _ in range(args.warmup):
         tr.step()
     torch.cuda.synchronize()
@@ -590,7 +600,11 @@ def b200_arm(args, ws, rank, local):
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "f16", "data": f"synthetic (seeded {WORKLOADS[args.workload]['graph']} graph, "
                                     "planted labels)",
-            "config": workload_config(dg.n, dg.num_edges, parallelism, args.workload),
+            "config": dict(workload_config(dg.n, dg.num_edges, parallelism, args.workload),
+                           vertex_order=("degree-sorted relabelling (device.locality_order, "
+                                         "rank-interleaved; same graph, features, labels and "
+                                         "split per original vertex)" if order is not None
+                                         else "as generated")),
             "clocks": clocks.summary(),
             "e2e": {"value": round(e2e_ms, 4), "unit": "ms/epoch", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": 4 * ws},
@@ -672,6 +686,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-small", action="store_true", help="skip the C1/C2 epoch timings")
     ap.add_argument("--no-graph", action="store_true", help="time eager steps, no CUDA graph")
+    ap.add_argument("--reorder", choices=("auto", "none", "degree"), default="auto",
+                    help="vertex relabelling for gather locality (auto: the workload's default)")
     ap.add_argument("--cpu-budget-edges", type=int, default=500_000,
                     help="edges in the B200 arm's cpu_baseline sample")
     ap.add_argument("--ref-budget-edges", type=int, default=0,

@@ -513,6 +513,41 @@ class DeviceGraph:
             raise ValueError("graph was built without its transpose")
         return self.bwd if transpose else self.fwd
 
+    def relabel(self, order: torch.Tensor) -> "DeviceGraph":
+        """The same graph with vertex order[i] renamed i (order: new -> old id,
+        a permutation); edges, degrees and every per-vertex quantity follow
+        their vertex, CSR / CSC rebuilt canonical on the GPU."""
+        order = order.to(self.device, torch.int64)
+        if order.numel() != self.n:
+            raise ValueError("order must be a permutation of the vertices")
+        new_of_old = torch.empty_like(order)
+        new_of_old[order] = torch.arange(self.n, device=self.device)
+        return DeviceGraph.from_edges(self.n, new_of_old[self.rows()],
+                                      new_of_old[self.cols.long()], device=self.device,
+                                      build_transpose=self.bwd is not None)
+
+
+def locality_order(offsets, t_offsets=None, parts: int = 1) -> torch.Tensor:
+    """Vertex relabelling for gather locality (new -> old id): vertices by
+    descending total degree, so the rows that the aggregations gather most
+    share L2 lines and DRAM pages (random ids spread each hot 100-256-byte row
+    over lines shared with cold rows).  With parts > 1 the sorted vertices are
+    dealt round-robin to the parts' contiguous id ranges (each rank of a row
+    partition gets an equal share of the hubs, ids degree-sorted inside it).
+    Stable, deterministic.  Measured on one B200 (tools/exp/reorder_probe.py):
+    C4 F=112 SpMM 4.95 -> 4.32 ms, C5 F=128 13.7 -> 11.2 ms."""
+    deg = offsets[1:] - offsets[:-1]
+    if t_offsets is not None:
+        deg = deg + (t_offsets[1:] - t_offsets[:-1])
+    by_deg = torch.argsort(deg, descending=True, stable=True)
+    if parts <= 1:
+        return by_deg
+    n = by_deg.numel()
+    k = torch.arange(n, device=by_deg.device)
+    # rank p takes sorted positions p, p + parts, ...; ranks laid out in id order
+    key = (k % parts) * n + k // parts
+    return by_deg[torch.argsort(key, stable=True)]
+
 
 # ── SpMM ─────────────────────────────────────────────────────────────────
 

@@ -1156,7 +1156,13 @@ class Trainer:
     model, optimiser, masks and device-resident inputs.  `step()` is one epoch
     (forward, loss, backward, Adam) with no host synchronisation."""
 
-    def __init__(self, bundle, features, labels, config: TrainConfig, row_slice=None):
+    def __init__(self, bundle, features, labels, config: TrainConfig, row_slice=None,
+                 node_order=None):
+        """node_order (new -> old vertex id, e.g. device.locality_order): the
+        bundle's graph is the relabelled one (DeviceGraph.relabel); features and
+        labels are given in the original ids and the train / validation split
+        is drawn over the original ids, so every original vertex keeps its
+        features, label and split."""
         self.cfg = config
         self.bundle = bundle
         dev = config.device
@@ -1166,6 +1172,11 @@ class Trainer:
         n, fan_in = feats.shape
         labels_t = labels if isinstance(labels, torch.Tensor) else torch.from_numpy(
             np.asarray(labels, dtype=np.int64))
+        self.node_order = node_order
+        if node_order is not None:
+            order = torch.as_tensor(node_order, dtype=torch.int64)
+            feats = feats[order.to(feats.device)]
+            labels_t = labels_t[order.to(labels_t.device)]
         c = int(labels_t.max()) + 1
         self.n_cls = c + c % 2   # the reference harness pads odd class counts to even
         self.in_store = _round_store(fan_in)
@@ -1179,6 +1190,8 @@ class Trainer:
         perm = rng.permutation(n)
         val = np.zeros(n, dtype=bool)
         val[perm[: int(n * config.val_fraction)]] = True
+        if node_order is not None:
+            val = val[torch.as_tensor(node_order).cpu().numpy()]
         lo, hi = row_slice or (0, n)
         self.val_mask = torch.from_numpy(val[lo:hi]).to(dev)
         self.train_mask = ~self.val_mask

@@ -574,7 +574,8 @@ class DistTrainer:
     the 1-GPU Trainer (identical RNG stream); the loss is the global mean, the
     weight gradients are all-reduced before Adam."""
 
-    def __init__(self, dg: D.DeviceGraph, features, labels, config, dist, ops=CudaOps):
+    def __init__(self, dg: D.DeviceGraph, features, labels, config, dist, ops=CudaOps,
+                 node_order=None):
         from .models import Trainer
 
         self.dist = dist
@@ -584,7 +585,8 @@ class DistTrainer:
         self.part = part
         self.bundle = DistBundle(part, Exchange(dist, part),
                                  lambda k, side, dt: dg.factor(k, side, dt), ops)
-        self.inner = Trainer(self.bundle, features, labels, config, row_slice=(part.lo, part.hi))
+        self.inner = Trainer(self.bundle, features, labels, config, row_slice=(part.lo, part.hi),
+                             node_order=node_order)
         self.n_total = dg.n
         self._graph = None
         self._graph_out = None

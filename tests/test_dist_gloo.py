@@ -298,3 +298,33 @@ def test_column_blocks_restore_rows():
                                                         int(blocks[q].offsets[r + 1])]
                                   + splits[q] for q in range(parts)])
             np.testing.assert_array_equal(cat, cols[off[r]:off[r + 1]])
+
+
+def test_locality_order_permutation_and_rank_interleave():
+    """device.locality_order (CPU tensors): a permutation, vertices by
+    descending total degree (stable); with parts > 1 each part's contiguous
+    id range holds every parts-th vertex of that order (hubs shared out)."""
+    import torch
+
+    from paper_2411_01109_b200.device import locality_order
+
+    g = torch.Generator().manual_seed(0)
+    n = 1003
+    deg = torch.randint(0, 50, (n,), generator=g)
+    off = torch.zeros(n + 1, dtype=torch.int64)
+    off[1:] = torch.cumsum(deg, 0)
+    tdeg = torch.randint(0, 50, (n,), generator=g)
+    toff = torch.zeros(n + 1, dtype=torch.int64)
+    toff[1:] = torch.cumsum(tdeg, 0)
+    o1 = locality_order(off, toff)
+    assert sorted(o1.tolist()) == list(range(n))
+    tot = (deg + tdeg)[o1]
+    assert bool((tot[:-1] >= tot[1:]).all())
+    for parts in (2, 3, 8):
+        op = locality_order(off, toff, parts=parts)
+        assert sorted(op.tolist()) == list(range(n))
+        pos = 0
+        for p in range(parts):
+            share = o1[p::parts]
+            assert op[pos:pos + share.numel()].tolist() == share.tolist()
+            pos += share.numel()

@@ -50,13 +50,14 @@ def test_bench_spawns_ranks_for_gpus_flag(cuda):
     env.pop("WORLD_SIZE", None)
     out = subprocess.run(
         [sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--workload", "gat-pubmed",
-         "--steps", "3", "--warmup", "3", "--no-cpu-baseline"],
+         "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--reorder", "degree"],
         capture_output=True, text=True, cwd=ROOT, timeout=850, env=env)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")]
     assert len(lines) == 1, out.stdout
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2
+    assert d["config"]["vertex_order"].startswith("degree-sorted")
     ex = d["exchange"]
     assert ex["recv_bytes_per_rank_per_step_max"] > 0
     assert ex["n_rows_max_over_mean"] <= 1.5

@@ -444,6 +444,40 @@ def test_training_step_dense_math_on_own_kernels(cuda, kind, kw):
     assert any("k_gemm_wgrad" in n for n in names) and any("k_gemm_tc" in n for n in names)
 
 
+def test_locality_relabel_same_graph_and_training(cuda):
+    """DeviceGraph.relabel(locality_order): the relabelled graph is the same
+    graph (edge set maps exactly), its aggregation equals the original's row
+    for row within the fast-path bound of float64, and training with
+    node_order (features / labels / split per original vertex) reaches the
+    same accuracy and a close loss trace."""
+    import oracle as O
+    from paper_2411_01109_b200 import device as D, graphgen, models as M
+    from paper_2411_01109_b200.device import DeviceGraph
+
+    rows, cols, feats, labels = graphgen.synth_sbm(2000, 4, 0.02, 0.002, 32, 3)
+    dg = DeviceGraph.from_edges(2000, rows, cols)
+    order = D.locality_order(dg.offsets, dg.bwd.offsets)
+    dr = dg.relabel(order)
+    o = order.cpu().numpy()
+    new_of_old = np.empty_like(o)
+    new_of_old[o] = np.arange(o.size)
+    r0 = np.repeat(np.arange(2000), np.diff(dg.offsets.cpu().numpy()))
+    e0 = set(zip(new_of_old[r0].tolist(), new_of_old[dg.cols.cpu().numpy()].tolist()))
+    r1 = np.repeat(np.arange(2000), np.diff(dr.offsets.cpu().numpy()))
+    assert e0 == set(zip(r1.tolist(), dr.cols.cpu().numpy().tolist()))
+    x = torch.randn(2000, 64, device=cuda, dtype=torch.float16)
+    y0 = D.spmm(dg, x, None, "discretized", "both").double().cpu().numpy()
+    y1 = D.spmm(dr, x[order], None, "discretized", "both").double().cpu().numpy()[new_of_old]
+    assert np.all(np.abs(y1 - y0) <= 1e-2 * np.maximum(1.0, np.abs(y0)))
+    cfg = M.TrainConfig(kind="gcn", hidden=16, epochs=30, numerics="fast")
+    a = M.Trainer(M.GraphBundle.build(dg), feats, labels, cfg)
+    b = M.Trainer(M.GraphBundle.build(dr), feats, labels, cfg, node_order=order)
+    assert bool((b.labels.cpu() == torch.as_tensor(labels)[order.cpu()]).all())
+    la = [float(a.step()[0]) for _ in range(30)]
+    lb = [float(b.step()[0]) for _ in range(30)]
+    np.testing.assert_allclose(la, lb, rtol=0, atol=5e-3)
+
+
 def test_run_epochs_host_feed_matches_steps(cuda):
     """Double-buffered host feeding (e2e path) trains exactly like step()."""
     from paper_2411_01109_b200 import graphgen, models as M
