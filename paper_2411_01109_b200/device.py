@@ -28,11 +28,12 @@ from . import _native as nat
 DTYPE_CODE = {torch.float16: nat.HG_F16, torch.float32: nat.HG_F32}
 MIRROR = {"none": "none", "left": "right", "right": "left", "both": "both"}
 DEFAULT_SPLIT_CAP = int(os.environ.get("HG_SPLIT_CAP", "512"))  # edges per work unit (A/B knob)
-# HG_FUSED_FOLLOWUP=1: hg_spmm folds split rows' carries in the launch itself
-# (last-arriving unit, arrival counters).  Off by default: bitwise the same,
-# but measured no faster (C3 4.419 -> 4.438 ms, GIN 12.83 -> 12.94 ms: the
-# hub rows' last units serialise the fold at the tail of the launch).
-FUSED_FOLLOWUP = os.environ.get("HG_FUSED_FOLLOWUP", "0") == "1"
+# hg_spmm folds split rows' carries in the launch itself (last-arriving unit,
+# arrival counters; bitwise the follow-up kernel's result).  On the
+# degree-sorted graphs (locality_order) it is faster (C3 4.279 -> 4.244 ms,
+# C4 11.51 -> 11.45, C5 93.15 -> 92.55); on generated ids it was not (4.419 ->
+# 4.438 ms).  HG_FUSED_FOLLOWUP=0 selects the separate follow-up launch.
+FUSED_FOLLOWUP = os.environ.get("HG_FUSED_FOLLOWUP", "1") != "0"
 # hg_spmm packs: aligned blocks of PACK_ROWS rows with few edges in total, walked
 # by one team as one edge stream (hg_schedule_build)
 PACK_ROWS = 16

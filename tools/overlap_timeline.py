@@ -62,12 +62,16 @@ def main():
     ap.add_argument("--rank", type=int, default=0)
     ap.add_argument("--heads", type=int, default=4)
     ap.add_argument("--bw", default="450,700,900", help="modelled NVLink GB/s per rank")
+    ap.add_argument("--no-reorder", action="store_true", help="keep the generated vertex ids")
     args = ap.parse_args()
     dg = graphgen.rmat(scale=args.scale, seed=0)
+    if not args.no_reorder:   # as bench.py: degree-sorted, rank-interleaved relabelling
+        dg = dg.relabel(D.locality_order(dg.offsets, dg.bwd.offsets, parts=args.parts))
     part = make_local_part(dg.offsets, dg.cols, dg.bwd.offsets, dg.bwd.cols, dg.bwd.perm,
                            args.rank, args.parts)
     n, h = dg.n, args.heads
     out = {"graph": f"RMAT scale {args.scale}, {dg.num_edges} edges", "parts": args.parts,
+           "vertex_order": "as generated" if args.no_reorder else "degree-sorted, rank-interleaved",
            "rank": args.rank, "rank_rows": part.n_local, "rank_edges": part.fwd.num_edges,
            "transfer_model": "slab bytes / B, P broadcasts in rank order (not measured: 1 GPU)",
            "layers": []}
