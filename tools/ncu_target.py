@@ -21,11 +21,16 @@ def main():
     ap.add_argument("--workload", default="gcn-reddit", choices=sorted(bench.WORKLOADS))
     ap.add_argument("--epochs", type=int, default=1)
     ap.add_argument("--feats", default="")
+    ap.add_argument("--no-reorder", action="store_true")
     args = ap.parse_args()
     dg, x, labels = bench.build_workload(args.workload, 0)
+    order = None
+    if bench.WORKLOADS[args.workload].get("reorder") == "degree" and not args.no_reorder:
+        order = D.locality_order(dg.offsets, dg.bwd.offsets)   # as bench.py
+        dg = dg.relabel(order)
     cfg = TrainConfig(mode="half", seed=0, scaling="discretized", norm="both", numerics="fast",
                       grad_scale="auto", **bench.WORKLOADS[args.workload]["cfg"])
-    tr = Trainer(GraphBundle.build(dg), x, labels, cfg)
+    tr = Trainer(GraphBundle.build(dg), x, labels, cfg, node_order=order)
     for _ in range(args.epochs):
         tr.step()
     for f in [int(v) for v in args.feats.split(",") if v]:
