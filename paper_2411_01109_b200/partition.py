@@ -358,8 +358,12 @@ class DistBundle:
         self._static = None    # (local input tensor, its gathered [N, F] copy)
         # column-blocked, transfer-overlapped unweighted aggregation (CUDA ops, P > 1)
         if overlap is None:
-            overlap = os.environ.get("HG_DIST_OVERLAP", "1") != "0"
-        self.overlap = bool(overlap) and ops is CudaOps and part.parts > 1
+            env = os.environ.get("HG_DIST_OVERLAP", "1")
+            # "force": the blocked path even for one part (a one-rank NCCL group
+            # then exercises the async-broadcast exchange, e.g. under graph capture)
+            overlap = "force" if env == "force" else env != "0"
+        self.overlap = (bool(overlap) and ops is CudaOps
+                        and (part.parts > 1 or overlap == "force"))
         self._blocks = {}
 
     def blocks(self, transpose):

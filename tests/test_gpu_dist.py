@@ -103,8 +103,8 @@ def test_partitioned_cuda_step_matches_one_rank(cuda, kind):
         np.testing.assert_allclose(l1, lw, rtol=1e-4, err_msg=kind)
 
 
-def _run_nccl_graph(port, out_q):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+def _run_nccl_graph(port, out_q, overlap="1"):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), HG_DIST_OVERLAP=overlap)
     torch.cuda.set_device(0)
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     try:
@@ -131,13 +131,16 @@ def _run_nccl_graph(port, out_q):
 
 
 @pytest.mark.timeout(600)
-def test_partitioned_step_cuda_graph_with_nccl(cuda):
+@pytest.mark.parametrize("overlap", ["1", "force"])
+def test_partitioned_step_cuda_graph_with_nccl(cuda, overlap):
     """The partitioned step (NCCL all-gathers / all-reduces inside) captured as
     a CUDA graph replays to the same losses as eager steps (one-rank NCCL
-    group: the capture path bench.py takes at N > 1)."""
+    group: the capture path bench.py takes at N > 1).  overlap="force" runs the
+    column-blocked aggregation with its async NCCL broadcasts and per-rank
+    waits inside the captured graph."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    p = ctx.Process(target=_run_nccl_graph, args=(_free_port(), q))
+    p = ctx.Process(target=_run_nccl_graph, args=(_free_port(), q, overlap))
     p.start()
     res = q.get(timeout=500)
     p.join(timeout=120)
