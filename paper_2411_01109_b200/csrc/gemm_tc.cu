@@ -693,6 +693,8 @@ static WgradPlan wgrad_plan(int64_t k, int64_t m, int n, int sms) {
   // TMEM: one 64*nb-column accumulator per tile, plus the bias accumulator
   const int mt_cap = std::min(kWgMaxMT, 512 / (64 * p.nb) - 1);
   p.groups = (p.mt_total + mt_cap - 1) / mt_cap;
+  if (const char* e = getenv("HG_WG_GROUPS"))  // measurement knob (A/B runs only)
+    p.groups = std::max(p.groups, std::min(p.mt_total, atoi(e)));
   p.mt_group = (p.mt_total + p.groups - 1) / p.groups;
   const uint32_t cols = (uint32_t)((p.mt_group + 1) * 64 * p.nb);
   p.tmem_cols = 32;
