@@ -177,7 +177,10 @@ __device__ __forceinline__ float chunk_dot_f32(const typename RawV<V * sizeof(T)
 }
 
 template <typename T, int V, int TEAM, int G>
-__global__ void __launch_bounds__(256, 3)
+#ifndef HG_SDDMM_OCC
+#define HG_SDDMM_OCC 3   // resident 256-thread blocks per SM (A/B builds)
+#endif
+__global__ void __launch_bounds__(256, HG_SDDMM_OCC)
 k_sddmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __restrict__ cols,
              const T* __restrict__ x, const T* __restrict__ y, T* __restrict__ out, int F,
              int heads) {
