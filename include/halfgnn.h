@@ -296,11 +296,25 @@ int hg_head_dots_bwd(const void* z, const void* a_l, const void* a_r, const void
  * the reference; 2^-k undoes a static power-of-two loss scale exactly).
  * pub_out (may be NULL): the next step's published copy, rnd(p) in pub_dtype
  * (Param.publish, models.py:418-433); grad_zero (may be NULL): a pub_dtype
- * gradient buffer zeroed after use (the next step's accumulation target). */
+ * gradient buffer zeroed after use (the next step's accumulation target).
+ * step_done (may be NULL): an int32 counter, zero, left zero; then the step
+ * used is *step + 1 and is written back to *step by the kernel (the device step
+ * count advances with no extra launch).  t_desc (HOST int64[4 * nt], nt <= 8,
+ * needs pub_out and pub_t): {flat offset, rows K, cols N, offset in pub_t} of
+ * 2-D weights whose transposed published copy [N, K] is also written. */
 int hg_adam_step(float* master, float* m, float* v, const void* grad, int grad_dtype,
                  int64_t count, float lr, float omb1, float omb2, double b1, double b2,
-                 float eps, const double* step, float grad_unscale, void* pub_out,
-                 void* grad_zero, int pub_dtype, void* stream);
+                 float eps, double* step, float grad_unscale, void* pub_out,
+                 void* grad_zero, int pub_dtype, int32_t* step_done, const int64_t* t_desc,
+                 int32_t nt, void* pub_t, void* stream);
+
+/* cross_entropy's mean (models.py:552-572): *loss_out = fp32(sum(nll) / denom),
+ * fp64 sums in a fixed order (block chunks, then the block partials in block
+ * order by the last block).  ws: hg_loss_mean_workspace bytes, 8-byte aligned,
+ * its trailing counter zero (left zero) -- a dedicated buffer per stream. */
+int hg_loss_mean_workspace(size_t* bytes);
+int hg_loss_mean(const double* nll, int64_t n, double denom, float* loss_out, void* ws,
+                 size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------ dense GEMM (tcgen05) */
 

@@ -102,7 +102,9 @@ SIGNATURES = {
     "hg_col_sums_workspace": [_I64, _I32, _PSZ],
     "hg_col_sums": [_P, _I64, _I32, _P, c_int, _P, c_size_t, _P],
     "hg_adam_step": [_P, _P, _P, _P, c_int, _I64, c_float, c_float, c_float, c_double, c_double,
-                     c_float, _P, c_float, _P, _P, c_int, _P],
+                     c_float, _P, c_float, _P, _P, c_int, _P, _P, _I32, _P, _P],
+    "hg_loss_mean_workspace": [_PSZ],
+    "hg_loss_mean": [_P, _I64, c_double, _P, _P, c_size_t, _P],
 }
 _RESTYPES = {"hg_last_error": c_char_p}
 

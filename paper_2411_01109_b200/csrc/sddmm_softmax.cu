@@ -1568,13 +1568,26 @@ __global__ void k_head_dots_bwd_fold(const float* __restrict__ part, int nblk, i
   }
 }
 
+// Extras of the fused Adam step: the next step's published copy (and the
+// transposed copies of up to kAdamMaxT 2-D weights, the forward GEMMs' B^T
+// operands), the cleared gradient, and the step counter advanced in-kernel.
+constexpr int kAdamMaxT = 8;
+template <typename PT>
+struct AdamExtra {
+  PT* pub;
+  PT* gzero;
+  PT* pub_t;
+  int* done;                 // non-null: t = *step + 1, written back by the last block
+  int nt;
+  int64_t t_off[kAdamMaxT], t_rows[kAdamMaxT], t_cols[kAdamMaxT], t_dst[kAdamMaxT];
+};
+
 template <typename G, typename PT>
 __global__ void k_adam(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
                        const G* __restrict__ grad, int64_t count, float lr, float omb1,
                        float omb2, double b1, double b2, float eps,
-                       const double* __restrict__ step, float unscale, PT* __restrict__ pub,
-                       PT* __restrict__ gzero) {
-  const double t = *step;
+                       double* __restrict__ step, float unscale, const AdamExtra<PT> ex) {
+  const double t = ex.done ? *step + 1.0 : *step;
   const float c1 = (float)(1.0 - pow(b1, t)), c2 = (float)(1.0 - pow(b2, t));
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -1589,9 +1602,62 @@ __global__ void k_adam(float* __restrict__ p, float* __restrict__ m, float* __re
     const float pn = __fsub_rn(p[i], __fdiv_rn(num, den));
     p[i] = pn;
     // the next step's published copy (ParamGroup.publish: RN cast of the
-    // master) and its zeroed gradient, fused here instead of two more passes
-    if (pub) pub[i] = Num<PT>::from_f(pn);
-    if (gzero) gzero[i] = Num<PT>::zero();
+    // master), its transposed copy for 2-D weights, and the zeroed gradient,
+    // fused here instead of separate passes
+    if (ex.pub) {
+      const PT h = Num<PT>::from_f(pn);
+      ex.pub[i] = h;
+      for (int j = 0; j < ex.nt; ++j) {
+        const int64_t o = i - ex.t_off[j];
+        if (o >= 0 && o < ex.t_rows[j] * ex.t_cols[j]) {
+          const int64_t r = o / ex.t_cols[j], c = o - r * ex.t_cols[j];
+          ex.pub_t[ex.t_dst[j] + c * ex.t_rows[j] + r] = h;
+        }
+      }
+    }
+    if (ex.gzero) ex.gzero[i] = Num<PT>::zero();
+  }
+  if (ex.done) {  // the last block to finish advances the device step count
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(ex.done, 1) == (int)gridDim.x - 1) {
+        *step = t;
+        *ex.done = 0;
+      }
+    }
+  }
+}
+
+// loss = fp32(sum(nll) / denom): kLossBlocks blocks each sum a contiguous
+// chunk (strided over the block's threads, then a fixed tree), the last block
+// to finish (arrival counter, re-armed) adds the block partials in block order.
+constexpr int kLossBlocks = 148;
+__global__ void __launch_bounds__(512) k_loss_mean(const double* __restrict__ nll, int64_t n,
+                                                   double denom, float* __restrict__ out,
+                                                   double* __restrict__ part, int* __restrict__ done) {
+  __shared__ double sh[512];
+  const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = (int64_t)blockIdx.x * chunk;
+  const int64_t hi = lo + chunk < n ? lo + chunk : n;
+  double s = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) s += nll[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = sh[0];
+    __threadfence();
+    if (atomicAdd(done, 1) == (int)gridDim.x - 1) {
+      __threadfence();
+      double t = 0.0;
+      for (int b = 0; b < (int)gridDim.x; ++b) t += __ldcg(part + b);
+      *out = (float)(t / denom);
+      *done = 0;
+    }
   }
 }
 
@@ -1630,30 +1696,70 @@ extern "C" int hg_head_dots(const void* z, const void* a_l, const void* a_r, int
   return HG_OK;
 }
 
+template <typename PT>
+static AdamExtra<PT> adam_extra(void* pub_out, void* grad_zero, int* step_done,
+                                const int64_t* t_desc, int nt, void* pub_t) {
+  AdamExtra<PT> ex{};
+  ex.pub = (PT*)pub_out;
+  ex.gzero = (PT*)grad_zero;
+  ex.pub_t = (PT*)pub_t;
+  ex.done = step_done;
+  ex.nt = pub_t ? nt : 0;
+  for (int j = 0; j < ex.nt; ++j) {
+    ex.t_off[j] = t_desc[4 * j];
+    ex.t_rows[j] = t_desc[4 * j + 1];
+    ex.t_cols[j] = t_desc[4 * j + 2];
+    ex.t_dst[j] = t_desc[4 * j + 3];
+  }
+  return ex;
+}
+
 extern "C" int hg_adam_step(float* master, float* m, float* v, const void* grad, int grad_dtype,
                             int64_t count, float lr, float omb1, float omb2, double b1, double b2,
-                            float eps, const double* step, float grad_unscale,
-                            void* pub_out, void* grad_zero, int pub_dtype, void* stream) {
+                            float eps, double* step, float grad_unscale, void* pub_out,
+                            void* grad_zero, int pub_dtype, int32_t* step_done,
+                            const int64_t* t_desc, int32_t nt, void* pub_t, void* stream) {
   HG_REQUIRE(grad_dtype == HG_F16 || grad_dtype == HG_F32, "unknown dtype %d", grad_dtype);
   HG_REQUIRE(pub_dtype == HG_F16 || pub_dtype == HG_F32, "unknown dtype %d", pub_dtype);
   HG_REQUIRE(!(grad_zero == grad && grad_dtype != pub_dtype), "hg_adam_step: grad_zero aliases grad of another dtype");
+  HG_REQUIRE(nt >= 0 && nt <= kAdamMaxT && (nt == 0 || (t_desc && pub_t && pub_out)),
+             "hg_adam_step: at most %d transposed copies, with their descriptors", kAdamMaxT);
   if (count == 0) return HG_OK;
   cudaStream_t st = as_stream(stream);
   const int g = grid_for(count, 256, 148 * 8);
   if (grad_dtype == HG_F16 && pub_dtype == HG_F16)
     k_adam<__half, __half><<<g, 256, 0, st>>>(master, m, v, (const __half*)grad, count, lr, omb1,
                                               omb2, b1, b2, eps, step, grad_unscale,
-                                              (__half*)pub_out, (__half*)grad_zero);
+                                              adam_extra<__half>(pub_out, grad_zero, step_done, t_desc, nt, pub_t));
   else if (grad_dtype == HG_F32 && pub_dtype == HG_F16)
     k_adam<float, __half><<<g, 256, 0, st>>>(master, m, v, (const float*)grad, count, lr, omb1,
                                              omb2, b1, b2, eps, step, grad_unscale,
-                                             (__half*)pub_out, (__half*)grad_zero);
+                                             adam_extra<__half>(pub_out, grad_zero, step_done, t_desc, nt, pub_t));
   else if (grad_dtype == HG_F32)
     k_adam<float, float><<<g, 256, 0, st>>>(master, m, v, (const float*)grad, count, lr, omb1,
                                             omb2, b1, b2, eps, step, grad_unscale,
-                                            (float*)pub_out, (float*)grad_zero);
+                                            adam_extra<float>(pub_out, grad_zero, step_done, t_desc, nt, pub_t));
   else
     HG_REQUIRE(false, "hg_adam_step: fp16 gradients with an fp32 published copy");
+  HG_LAUNCHED();
+  return HG_OK;
+}
+
+extern "C" int hg_loss_mean_workspace(size_t* bytes) {
+  HG_REQUIRE(bytes, "hg_loss_mean_workspace: null output");
+  *bytes = kLossBlocks * sizeof(double) + 16;
+  return HG_OK;
+}
+
+extern "C" int hg_loss_mean(const double* nll, int64_t n, double denom, float* loss_out,
+                            void* ws, size_t ws_bytes, void* stream) {
+  HG_REQUIRE(n >= 0 && loss_out && (n == 0 || nll), "hg_loss_mean: bad arguments");
+  HG_REQUIRE(ws && ws_bytes >= kLossBlocks * sizeof(double) + 16 &&
+                 (reinterpret_cast<uintptr_t>(ws) & 7) == 0,
+             "hg_loss_mean: workspace too small");
+  double* part = static_cast<double*>(ws);
+  int* done = reinterpret_cast<int*>(part + kLossBlocks);
+  k_loss_mean<<<kLossBlocks, 512, 0, as_stream(stream)>>>(nll, n, denom, loss_out, part, done);
   HG_LAUNCHED();
   return HG_OK;
 }

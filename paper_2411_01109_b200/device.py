@@ -1169,16 +1169,41 @@ def head_dots(z, a_l, a_r, heads):
 
 
 def adam_step(master, m, v, grad, lr, b1, b2, eps, step, grad_unscale=1.0, pub=None,
-              grad_zero=None):
+              grad_zero=None, step_done=None, transposed=None, pub_t=None):
     """One fused Adam update over flat fp32 arrays (hg_adam_step); `step` is the
-    device fp64 step count (already incremented); the gradient is multiplied by
-    grad_unscale (exact for a power of two) before use.  pub: also write the
-    next step's published copy rnd(master); grad_zero: a gradient buffer of
-    pub's dtype to clear for the next step's accumulation."""
+    device fp64 step count (already incremented -- or, with step_done (an int32
+    zero counter), advanced by the kernel itself); the gradient is multiplied
+    by grad_unscale (exact for a power of two) before use.  pub: also write the
+    next step's published copy rnd(master); transposed [(offset, K, N,
+    offset_in_pub_t)] + pub_t: and the transposed copies of those 2-D weights;
+    grad_zero: a gradient buffer of pub's dtype to clear for the next step."""
     pdt = _dtype_code(pub if pub is not None else (grad_zero if grad_zero is not None else grad))
+    tl = list(transposed or []) if pub_t is not None else []
+    desc = (ctypes.c_int64 * max(1, 4 * len(tl)))(*[int(v) for t in tl for v in t])
     nat.call("hg_adam_step", _p(master), _p(m), _p(v), _p(grad), _dtype_code(grad),
              master.numel(), float(lr), float(1 - b1), float(1 - b2), float(b1), float(b2),
-             float(eps), _p(step), float(grad_unscale), _p(pub), _p(grad_zero), pdt, _stream())
+             float(eps), _p(step), float(grad_unscale), _p(pub), _p(grad_zero), pdt,
+             _p(step_done), desc, len(tl), _p(pub_t if tl else None), _stream())
+
+
+_LOSS_WS = {}
+
+
+def loss_mean(nll, denom):
+    """fp32(sum(nll) / denom) as a device scalar (hg_loss_mean, fixed-order fp64
+    sums; a dedicated zero-initialised scratch per (device, stream) holds the
+    block partials and the arrival counter the kernel re-arms)."""
+    key = (nll.device, torch.cuda.current_stream(nll.device).cuda_stream)
+    ws = _LOSS_WS.get(key)
+    if ws is None:
+        ws = torch.zeros(nat.size_query("hg_loss_mean_workspace"), dtype=torch.uint8,
+                         device=nll.device)
+        _LOSS_WS[key] = ws
+    out = torch.empty((), dtype=torch.float32, device=nll.device)
+    nat.call("hg_loss_mean", _p(nll.contiguous()), nll.numel(), float(denom), _p(out), _p(ws),
+             ws.numel(), _stream())
+    Probe.launches += 1
+    return out
     Probe.launches += 1
 
 

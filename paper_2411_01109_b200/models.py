@@ -171,7 +171,7 @@ class GraphBundle:
         """GCN layer forward: tcgen05 GEMM with bias + input scale fused, then
         the gather SpMM (optionally with the next ReLU in its epilogue)."""
         fin, fout = self.dg.norm_tables(reduction.norm, False, x.dtype)
-        xs = D.gemm_tc(x, w.t().contiguous(), b, fin)
+        xs = D.gemm_tc(x, _wt(w), b, fin)
         return D.spmm_csr(self.dg.view(False), xs, None, None, 1, reduction.scaling, None, fout,
                           relu=relu)
 
@@ -450,6 +450,14 @@ def shadow_div(num, den, overflow=None, tag="div"):
 # ── dense / elementwise ops ──────────────────────────────────────────────
 
 
+def _wt(w):
+    """W^T [N, K] contiguous: the published transposed copy a ParamGroup keeps
+    for its 2-D weights (written with the weights, no per-step transpose),
+    else a copy."""
+    t = getattr(w, "_hg_t", None)
+    return t if t is not None else w.t().contiguous()
+
+
 def _tc_shapes(x, w):
     """x @ w fits the tcgen05 kernels (hg_gemm_tc forward / dx, hg_gemm_wgrad
     dW): binary16 CUDA operands, widths multiples of 8 up to 256 (the input
@@ -485,7 +493,7 @@ class _MatmulTCFn(torch.autograd.Function):
     def forward(ctx, x, w):
         ctx.w_leaf = w
         ctx.save_for_backward(x, w)
-        return D.gemm_tc(x, w.t().contiguous())
+        return D.gemm_tc(x, _wt(w))
 
     @staticmethod
     def backward(ctx, g):
@@ -632,11 +640,28 @@ class ParamGroup:
             p.group = self
         self._ptrs = [p.published.grad.data_ptr() for p in self.params]
         self.fresh = False   # True: pub / grad already prepared by the fused Adam step
+        # transposed published copies of the 2-D weights (the forward GEMMs' B^T
+        # operand; written with the published copy, no per-step transpose)
+        self.transposed = []
+        toff = 0
+        for p, off in zip(self.params, offs):
+            if p.master.dim() == 2 and len(self.transposed) < 8:
+                k, n = p.master.shape
+                self.transposed.append((off, k, n, toff))
+                toff += (k * n + 7) // 8 * 8
+        self.pub_t = torch.empty(max(toff, 1), dtype=self.dtype, device=dev)
+        for p, (off, k, n, t0) in zip([p for p in self.params if p.master.dim() == 2],
+                                      self.transposed):
+            p.published._hg_t = self.pub_t[t0:t0 + k * n].view(n, k)
 
     @torch.no_grad()
     def publish(self):
         self.pub.copy_(self.master)
         self.grad.zero_()
+        for p in self.params:
+            t = getattr(p.published, "_hg_t", None)
+            if t is not None:
+                t.copy_(p.published.t())
         self.fresh = False
 
     def publish_if_stale(self):
@@ -712,7 +737,7 @@ class _LinearTCFn(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, x, w, b, relu_out):
-        y = D.gemm_tc(x, w.t().contiguous(), b, None, relu=relu_out)
+        y = D.gemm_tc(x, _wt(w), b, None, relu=relu_out)
         ctx.relu_out = relu_out
         ctx.leaves = (w, b)
         ctx.save_for_backward(x, w, y if relu_out else None)
@@ -1043,6 +1068,7 @@ class Adam:
             self.v = [torch.zeros_like(p.master) for p in self.params]
         dev = self.params[0].master.device if self.params else "cpu"
         self._t = torch.zeros((), dtype=torch.float64, device=dev)
+        self._done = None
         self.t = 0
 
     @torch.no_grad()
@@ -1050,16 +1076,20 @@ class Adam:
         """flat_grad: optional gradient for the whole group (e.g. all-reduced fp32)."""
         self.t += 1
         b1, b2 = self.betas
-        self._t.add_(1.0)
         g = self.group
         if g is not None and g.master.is_cuda and (flat_grad is not None or g.check_grads()):
             grad = g.grad if flat_grad is None else flat_grad
-            # the kernel also publishes the next step's weights and clears the
+            # the kernel also advances the device step count, publishes the next
+            # step's weights (and their transposed copies) and clears the
             # gradient (ParamGroup.publish fused away: g.fresh)
+            if self._done is None:
+                self._done = torch.zeros(1, dtype=torch.int32, device=g.master.device)
             D.adam_step(g.master, self.m, self.v, grad, self.lr, b1, b2, self.eps, self._t,
-                        self.grad_unscale, pub=g.pub, grad_zero=g.grad)
+                        self.grad_unscale, pub=g.pub, grad_zero=g.grad, step_done=self._done,
+                        transposed=g.transposed, pub_t=g.pub_t)
             g.fresh = True
             return
+        self._t.add_(1.0)
         if flat_grad is not None:
             for o, p in zip(_offsets(self.params), self.params):
                 p.published.grad = flat_grad[o:o + p.master.numel()].view(p.master.shape)
@@ -1237,7 +1267,7 @@ class Trainer:
         if self.cfg.mode == "half":
             self.conversions.forward += 1
             self.conversions.backward += 1
-        loss = (nll.sum() / denom).float()
+        loss = D.loss_mean(nll, denom) if nll.is_cuda else (nll.sum() / denom).float()
         torch.autograd.backward(logits, grad)
         return loss
 

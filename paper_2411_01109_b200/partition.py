@@ -508,7 +508,8 @@ class DistBundle:
         """GCN layer forward: tcgen05 GEMM + bias + input scale on the local rows,
         all-gather of the scaled rows, SpMM over the local CSR rows."""
         fin = self.local_in_scale(reduction.norm, False, x.dtype)
-        xs = D.gemm_tc(x, w.t().contiguous(), b, fin)
+        wt = getattr(w, "_hg_t", None)   # ParamGroup's transposed published copy
+        xs = D.gemm_tc(x, wt if wt is not None else w.t().contiguous(), b, fin)
         return self._gather_scaled(xs, reduction.scaling, reduction.norm, False)
 
     def spmm(self, x, w=None, scaling="post", norm="none", transpose=False, heads=1,
