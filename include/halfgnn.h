@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define HG_ABI_VERSION 4
+#define HG_ABI_VERSION 5
 
 enum { HG_OK = 0, HG_EINVAL = 1, HG_ECUDA = 2 };
 enum { HG_F16 = 0, HG_F32 = 1 };
@@ -128,7 +128,13 @@ int hg_schedule_build(const int64_t* offsets, int64_t n, int32_t split_cap, int3
  * (and left zero), and int32 [num_slots] = the split_rows index owning each
  * slot; then the last unit of each split row to finish folds its carries in
  * slot order inside the same launch (bitwise the follow-up's result).  Calls
- * sharing the counters must be stream-ordered. */
+ * sharing the counters must be stream-ordered.
+ * comb_res (NULL: off; [n_rows, F] pitch comb_ldr, 16-byte aligned rows): the
+ * GIN combine in the row store, y = rnd(rnd(res * ope) + rnd(h * lam)) with h
+ * the finished aggregate, fp64 products (models.py:220-240 scale_combine);
+ * comb_ope: device scalar of the element type (NULL: 1); with ope = NULL and
+ * lam = 1 a rounded residual add (a gradient accumulated into the output).
+ * Not with relu. */
 int hg_spmm_workspace(int64_t n_cols, int32_t F, int64_t num_slots, int has_in_scale,
                       int32_t sum_heads, int dtype, size_t* bytes);
 int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_rows, int64_t n_cols,
@@ -139,7 +145,8 @@ int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_rows, int64_t
             int32_t F, int64_t ldx, int64_t ldy, int32_t scaling, int32_t relu,
             const void* in_scale, const void* out_factor, int64_t w_ld, int32_t w2_off,
             void* out2, int dtype, void* ws, size_t ws_bytes, void* stream,
-            int32_t* split_counters, const int32_t* slot_split);
+            int32_t* split_counters, const int32_t* slot_split, const void* comb_res,
+            int64_t comb_ldr, const void* comb_ope, double comb_lam);
 
 /* hg_spmm in fp32 partial mode, for column-blocked aggregation
  * (a row's edges split by the rank owning their column, block q run as soon as

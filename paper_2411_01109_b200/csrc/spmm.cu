@@ -85,6 +85,44 @@ __device__ __forceinline__ void store_out(T* dst, const float (&acc)[V], int fmo
   *reinterpret_cast<Raw*>(dst) = r;
 }
 
+// GIN's combine in the epilogue (models.py:220-240, scale_combine; hg_scale_combine):
+// out = rnd(rnd(res * o) + rnd(h * lam)), h = the finished aggregate, products
+// in fp64 -- the same roundings as the separate pass; o = lam = 1 is a plain
+// rounded add (a residual gradient accumulated in the same store).
+struct Combine {
+  const void* res;   // NULL: off
+  int64_t ldr;
+  const void* ope;   // device scalar of the element type (NULL: 1)
+  double lam;
+};
+
+template <typename T, int V>
+__device__ __forceinline__ void store_out_comb(T* dst, const float (&acc)[V], int fmode, T fo,
+                                               const T* res, double o, double lam) {
+  using Raw = typename RawVec<V * sizeof(T)>::type;
+  const Raw rr = *reinterpret_cast<const Raw*>(res);
+  const T* re = reinterpret_cast<const T*>(&rr);
+  Raw r;
+  T* p = reinterpret_cast<T*>(&r);
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const T h = finalize<T>(acc[i], fmode, fo);
+    const T u = Num<T>::from_d(Num<T>::to_d(re[i]) * o);
+    const T v = Num<T>::from_d(Num<T>::to_d(h) * lam);
+    p[i] = Num<T>::add(u, v);
+  }
+  *reinterpret_cast<Raw*>(dst) = r;
+}
+
+template <typename T, int V>
+__device__ __forceinline__ void store_fin(T* dst, const float (&acc)[V], int fmode, T fo,
+                                          const Combine& cb, int64_t row, int64_t col) {
+  if (cb.res) store_out_comb<T, V>(dst, acc, fmode, fo,
+                                   static_cast<const T*>(cb.res) + row * cb.ldr + col,
+                                   cb.ope ? Num<T>::to_d(*static_cast<const T*>(cb.ope)) : 1.0, cb.lam);
+  else store_out<T, V>(dst, acc, fmode, fo);
+}
+
 template <int V>
 __device__ __forceinline__ void load_carry(const float* src, float (&acc)[V]) {
   if constexpr (V % 4 == 0) {
@@ -289,6 +327,7 @@ struct FastTeam {
   T* pout2;
   int pldy, pfmode;
   bool plead;
+  Combine comb;   // GIN combine / residual add in the row store
   // fp32 partial-output mode (column-blocked aggregation, partition.py):
   // rows start from acc_in[r] and end in acc_out[r] unrounded (NULL: 0 / rnd)
   const float* accin;
@@ -336,7 +375,8 @@ struct FastTeam {
     for (int k = 0; k < NCH; ++k) {
       if (cval[k]) {
         if (accout) store_carry<V>(accout + (int64_t)prow * accld + (xl[k] - px), acc[k]);
-        else store_out<T, V>(py + (int64_t)prow * pldy + (xl[k] - px), acc[k], pfmode, pfo);
+        else store_fin<T, V>(py + (int64_t)prow * pldy + (xl[k] - px), acc[k], pfmode, pfo, comb,
+                             prow, xl[k] - px);
       }
 #pragma unroll
       for (int i = 0; i < V; ++i) acc[k][i] = 0.0f;
@@ -468,7 +508,7 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
             const float2* __restrict__ att_stats, T* __restrict__ att_out, float att_slope,
             const float* __restrict__ acc_in, float* __restrict__ acc_out, int acc_ld,
             int* __restrict__ split_cnt, const int32_t* __restrict__ slot_split,
-            const int4* __restrict__ split_info) {
+            const int4* __restrict__ split_info, const Combine comb) {
   using Team = FastTeam<T, V, TEAM, NCH, WEIGHTED, SUMW, PACKED, ATT>;
   constexpr int EB = Team::EB;
   constexpr int CPL = Team::CPL;
@@ -513,6 +553,7 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
   t.accin = acc_in;
   t.accout = acc_out;
   t.accld = acc_ld;
+  t.comb = comb;
   t.px = x;
   if constexpr (ATT) {
     t.asl = att_sl;
@@ -620,7 +661,8 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
     const T fo = fout ? fout[row] : Num<T>::zero();
 #pragma unroll
     for (int k = 0; k < NCH; ++k)
-      if (t.cval[k]) store_out<T, V>(y + (int64_t)row * ldy + (t.xl[k] - x), t.acc[k], fmode, fo);
+      if (t.cval[k]) store_fin<T, V>(y + (int64_t)row * ldy + (t.xl[k] - x), t.acc[k], fmode, fo, comb,
+                                     row, t.xl[k] - x);
   } else {
 #pragma unroll
     for (int k = 0; k < NCH; ++k)
@@ -671,7 +713,7 @@ k_spmm_fast(const int4* __restrict__ units, int64_t num_units, const int32_t* __
           for (int i = 0; i < V; ++i) a2[i] += b2[i];
         }
         if (acc_out) store_carry<V>(acc_out + (int64_t)sr.x * acc_ld + col, a2);
-        else store_out<T, V>(y + (int64_t)sr.x * ldy + col, a2, fmode, fo);
+        else store_fin<T, V>(y + (int64_t)sr.x * ldy + col, a2, fmode, fo, comb, sr.x, col);
       }
       if (SUMW) {
         for (int hh = tl; hh < heads; hh += TEAM) {
@@ -692,7 +734,7 @@ k_spmm_fast_followup(const int4* __restrict__ split_rows, int64_t num_split,
                      const float* __restrict__ carry, T* __restrict__ y, int F, int ldy,
                      int fmode, const T* __restrict__ fout, int heads2,
                      const float* __restrict__ carry2, T* __restrict__ out2,
-                     float* __restrict__ acc_out, int acc_ld) {
+                     float* __restrict__ acc_out, int acc_ld, const Combine comb) {
   const int lane = threadIdx.x & 31;
   const int tl = lane & (TEAM - 1);
   const int64_t team = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TEAM;
@@ -734,7 +776,7 @@ k_spmm_fast_followup(const int4* __restrict__ split_rows, int64_t num_split,
         }
     }
     if (acc_out) store_carry<V>(acc_out + (int64_t)sr.x * acc_ld + c * V, acc);
-    else store_out<T, V>(y + (int64_t)sr.x * ldy + c * V, acc, fmode, fo);
+    else store_fin<T, V>(y + (int64_t)sr.x * ldy + c * V, acc, fmode, fo, comb, sr.x, c * V);
   }
 }
 
@@ -769,6 +811,7 @@ struct FastArgs {
   int acc_ld;
   int* split_cnt;          // fused follow-up (hg_spmm split_counters / slot_split)
   const int32_t* slot_split;
+  Combine comb;            // GIN combine / residual add in the store (res NULL: off)
   cudaStream_t st;
 };
 
@@ -787,7 +830,7 @@ static int launch_fast(const FastArgs& a) {
         (const T*)a.x, (T*)a.y, a.carry, a.F, a.ldx, a.ldy, a.fmode, (const T*)a.fout,
         a.wld, a.w2off, (T*)a.out2, a.carry2, a.offsets, nullptr, (const T*)a.att_sl,
         a.att_stats, (T*)a.att_out, a.att_slope, a.acc_in, a.acc_out, a.acc_ld, a.split_cnt,
-        a.slot_split, a.split_rows);
+        a.slot_split, a.split_rows, a.comb);
     HG_LAUNCHED();
   }
   if (a.num_packs > 0) {
@@ -797,14 +840,14 @@ static int launch_fast(const FastArgs& a) {
         (const T*)a.x, (T*)a.y, nullptr, a.F, a.ldx, a.ldy, a.fmode, (const T*)a.fout,
         a.wld, a.w2off, (T*)a.out2, nullptr, a.offsets, a.rowid, (const T*)a.att_sl,
         a.att_stats, (T*)a.att_out, a.att_slope, a.acc_in, a.acc_out, a.acc_ld, nullptr,
-        nullptr, nullptr);
+        nullptr, nullptr, a.comb);
     HG_LAUNCHED();
   }
   if (a.num_split > 0 && a.split_cnt == nullptr) {
     int64_t blocks = (a.num_split + kThreads / TEAMF - 1) / (kThreads / TEAMF);
     k_spmm_fast_followup<T, V, TEAMF, NCH><<<(unsigned)blocks, kThreads, 0, a.st>>>(
         a.split_rows, a.num_split, a.carry, (T*)a.y, a.F, a.ldy, a.fmode, (const T*)a.fout,
-        SUMW ? a.heads : 0, a.carry2, SUMW ? (T*)a.out2 : nullptr, a.acc_out, a.acc_ld);
+        SUMW ? a.heads : 0, a.carry2, SUMW ? (T*)a.out2 : nullptr, a.acc_out, a.acc_ld, a.comb);
     HG_LAUNCHED();
   }
   return HG_OK;
@@ -946,7 +989,8 @@ static int spmm_impl(const int64_t* offsets, const int32_t* cols, int64_t n_rows
                      int32_t relu, const void* in_scale, const void* out_factor,
                      int64_t w_ld, int32_t w2_off, void* out2, int dtype, void* ws,
                      size_t ws_bytes, void* stream, const float* acc_in, float* acc_out,
-                     int32_t* split_counters = nullptr, const int32_t* slot_split = nullptr) {
+                     int32_t* split_counters = nullptr, const int32_t* slot_split = nullptr,
+                     Combine comb = Combine{}) {
   HG_REQUIRE(dtype == HG_F16 || dtype == HG_F32, "unknown dtype %d", dtype);
   HG_REQUIRE(F > 0 && F % 2 == 0, "feature length %d must be even and positive", F);
   HG_REQUIRE(heads >= 1 && F % heads == 0 && (F / heads) % 2 == 0,
@@ -1000,6 +1044,10 @@ static int spmm_impl(const int64_t* offsets, const int32_t* cols, int64_t n_rows
   a.fout = out_factor; a.st = st;
   a.wld = (int)w_ld; a.w2off = w2_off; a.out2 = out2; a.carry2 = carry2;
   a.acc_in = acc_in; a.acc_out = acc_out; a.acc_ld = F;
+  HG_REQUIRE(!comb.res || (!acc_out && !(relu) && comb.ldr >= F &&
+                           ((reinterpret_cast<uintptr_t>(comb.res) | (uintptr_t)(comb.ldr * elem_size(dtype))) & 15) == 0),
+             "hg_spmm: combine needs a 16-byte aligned residual with rows >= F, no ReLU, no fp32 output");
+  a.comb = comb;
   if (split_counters && slot_split && num_split_rows > 0) {
     a.split_cnt = split_counters;
     a.slot_split = slot_split;
@@ -1016,6 +1064,7 @@ static int spmm_impl(const int64_t* offsets, const int32_t* cols, int64_t n_rows
     s.y = static_cast<char*>(y) + (size_t)j * elem_size(dtype);
     if (acc_in) s.acc_in = acc_in + j;
     if (acc_out) s.acc_out = acc_out + j;
+    if (comb.res) s.comb.res = static_cast<const char*>(comb.res) + (size_t)j * elem_size(dtype);
     const int rc = dtype == HG_F16 ? dispatch_fast<__half>(s) : dispatch_fast<float>(s);
     if (rc) return rc;
   }
@@ -1031,11 +1080,13 @@ extern "C" int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_ro
                        int32_t relu, const void* in_scale, const void* out_factor,
                        int64_t w_ld, int32_t w2_off, void* out2, int dtype, void* ws,
                        size_t ws_bytes, void* stream, int32_t* split_counters,
-                       const int32_t* slot_split) {
+                       const int32_t* slot_split, const void* comb_res, int64_t comb_ldr,
+                       const void* comb_ope, double comb_lam) {
   return spmm_impl(offsets, cols, n_rows, n_cols, num_edges, units, num_units, split_rows,
                    num_split_rows, num_slots, packs, num_packs, pack_rowid, w, w_index, heads, x, y,
                    F, ldx, ldy, scaling, relu, in_scale, out_factor, w_ld, w2_off, out2, dtype, ws,
-                   ws_bytes, stream, nullptr, nullptr, split_counters, slot_split);
+                   ws_bytes, stream, nullptr, nullptr, split_counters, slot_split,
+                   Combine{comb_res, comb_ldr, comb_ope, comb_lam});
 }
 
 extern "C" int hg_spmm_acc(const int64_t* offsets, const int32_t* cols, int64_t n_rows,

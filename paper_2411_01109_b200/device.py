@@ -561,9 +561,12 @@ def _row_strided(t):
 def spmm_csr(view: CsrView, x: torch.Tensor, w=None, w_index=None, heads: int = 1,
              scaling: str = "post", fin=None, fout=None, out=None,
              split_cap: int = DEFAULT_SPLIT_CAP, relu: bool = False, w2_off: int = 0,
-             out2=None) -> torch.Tensor:
+             out2=None, combine=None) -> torch.Tensor:
     """fp32-guarded row-owned SpMM over one CSR view (hg_spmm).  x and out may
-    be column slices of wider row-major storage (row strides passed through)."""
+    be column slices of wider row-major storage (row strides passed through).
+    combine = (res [n_rows, F], ope (device scalar or None), lam): the row store
+    writes rnd(rnd(res * ope) + rnd(y * lam)) (GIN's combine; ope None and
+    lam 1: a rounded residual add)."""
     _require_cuda(x)
     if not _row_strided(x) or fin is not None:
         x = x.contiguous()
@@ -595,13 +598,22 @@ def spmm_csr(view: CsrView, x: torch.Tensor, w=None, w_index=None, heads: int = 
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record()
+    c_res = c_ope = None
+    c_lam = 1.0
+    if combine is not None:
+        c_res, c_ope, c_lam = combine
+        if c_res.shape != (view.n_rows, f) or c_res.dtype != x.dtype or c_res.stride(1) != 1:
+            raise ValueError("combine residual must be [n_rows, F] of the feature dtype")
+        if c_ope is not None:
+            c_ope = c_ope.reshape(-1)[:1].contiguous()
     nat.call("hg_spmm", _p(view.offsets), _p(view.cols), view.n_rows, view.n_cols,
              view.num_edges, _p(sched.units), sched.num_units, _p(sched.split_rows),
              sched.split_rows.shape[0], sched.num_slots, _p(sched.packs), sched.num_packs,
              _p(view.row_ids() if sched.num_packs else None), _p(w), _p(w_index), heads, _p(x),
              _p(out), f, x.stride(0), out.stride(0), nat.SCALING_CODES[scaling], int(relu),
              _p(fin), _p(fout), w_ld, int(w2_off), _p(out2), dt, _p(ws),
-             0 if ws is None else ws.numel(), _stream(), *map(_p, fin_state))
+             0 if ws is None else ws.numel(), _stream(), *map(_p, fin_state), _p(c_res),
+             0 if c_res is None else c_res.stride(0), _p(c_ope), float(c_lam))
     Probe.launches += int(sched.num_units > 0) + int(sched.num_packs > 0) + int(
         sched.split_rows.shape[0] > 0 and fin_state[0] is None) + int(fin is not None)
     if Probe.timing:
@@ -665,14 +677,15 @@ def spmm_csr_acc(view: CsrView, x: torch.Tensor, acc_in=None, acc_out=None, scal
 
 
 def spmm(dg: DeviceGraph, x, w=None, scaling="post", norm="none", transpose=False, heads=1,
-         out=None, weight_via_perm=False, relu=False):
+         out=None, weight_via_perm=False, relu=False, combine=None):
     """SpMMv / SpMMve on the graph (or its transpose), fp32-guarded.
     weight_via_perm: w is indexed by forward edge id and read through perm
     (spmm_weighted backward, models.py:309-311) without materialising w[perm]."""
     view = dg.view(transpose)
     fin, fout = dg.norm_tables(norm, transpose, x.dtype)
     widx = view.perm if (w is not None and weight_via_perm) else None
-    return spmm_csr(view, x, w, widx, heads, scaling, fin, fout, out, relu=relu)
+    return spmm_csr(view, x, w, widx, heads, scaling, fin, fout, out, relu=relu,
+                    combine=combine)
 
 
 def spmm_edge_ref(dg: DeviceGraph, x, w=None, scaling="post", norm="none", transpose=False,

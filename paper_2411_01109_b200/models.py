@@ -143,10 +143,12 @@ class GraphBundle:
         return self.numerics == "fast"
 
     def spmm(self, x, w=None, scaling="post", norm="none", transpose=False, heads=1,
-             weight_via_perm=False, relu=False):
+             weight_via_perm=False, relu=False, combine=None):
         if self.numerics == "fast":
             return D.spmm(self.dg, x, w, scaling, norm, transpose, heads,
-                          weight_via_perm=weight_via_perm, relu=relu)
+                          weight_via_perm=weight_via_perm, relu=relu, combine=combine)
+        if combine is not None:
+            raise ValueError("the combine epilogue needs numerics='fast'")
         if relu:
             raise ValueError("fused ReLU needs numerics='fast'")
         # reference order: one head at a time, weights materialised in CSC order
@@ -579,6 +581,33 @@ def scale_combine(x, a, one_plus_eps, lam):
     return _ScaleCombineFn.apply(x, a, one_plus_eps, float(lam))
 
 
+class _AggCombineFn(torch.autograd.Function):
+    """GIN's scale_combine(x, spmm_agg(x)) (models.py:220-240, 274-290, 487) as
+    one aggregation whose row store applies the combine (hg_spmm combine):
+    the aggregate never goes to HBM.  Backward: the combine's backward (dx
+    direct, d agg, d(1+eps)), the transposed aggregation of d agg with the
+    direct dx added in its row store (the sum autograd would form)."""
+
+    @staticmethod
+    def forward(ctx, x, ope, bundle, reduction, lam):
+        ctx.bundle, ctx.reduction, ctx.lam = bundle, reduction, lam
+        ctx.save_for_backward(x, ope)
+        return bundle.spmm(x, None, reduction.scaling, reduction.norm, combine=(x, ope, lam))
+
+    @staticmethod
+    def backward(ctx, g):
+        x, ope = ctx.saved_tensors
+        need_x, need_ope = ctx.needs_input_grad[0], ctx.needs_input_grad[1]
+        g = g.contiguous()
+        gx_d, ga, gope = D.scale_combine_bwd(x, g, ope, ctx.lam, need_x, need_x, need_ope)
+        gx = None
+        if need_x:
+            r = ctx.reduction
+            gx = ctx.bundle.spmm(ga, None, r.scaling, _MIRROR[r.norm], transpose=True,
+                                 combine=(gx_d, None, 1.0))
+        return gx, gope, None, None, None
+
+
 # ── parameters and layers ────────────────────────────────────────────────
 
 
@@ -806,8 +835,13 @@ class GINLayer:
     fuses_relu_out = True
 
     def __call__(self, bundle, x, mode, width, overflow, tag, relu_out=False):
-        agg = spmm_agg(bundle, x, self.reduction, width, overflow, tag)
-        mixed = scale_combine(x, agg, self.one_plus_eps.publish(mode), self.lam)
+        ope = self.one_plus_eps.publish(mode)
+        if (overflow is None and isinstance(bundle, GraphBundle) and bundle.numerics == "fast"
+                and x.is_cuda and FUSED_GIN_COMBINE):
+            mixed = _AggCombineFn.apply(x, ope, bundle, self.reduction, self.lam)
+        else:
+            agg = spmm_agg(bundle, x, self.reduction, width, overflow, tag)
+            mixed = scale_combine(x, agg, ope, self.lam)
         tc = getattr(bundle, "fused_bias_agg", False)
         return self.phi2(self.phi1(mixed, mode, tc=tc, relu_out=True), mode, tc=tc,
                          relu_out=relu_out)
@@ -871,6 +905,10 @@ class GATLayer:
             out = _HeadMeanFn.apply(out, h)
         return relu(out) if relu_out and not fuse else out
 
+
+# GIN's combine folded into the aggregation's row store (and the backward's
+# residual add into the transposed aggregation's); HG_FUSED_GIN=0: separate passes.
+FUSED_GIN_COMBINE = os.environ.get("HG_FUSED_GIN", "1") != "0"
 
 # GAT forward core as hg_gat_attention_stats + hg_gat_aggregate (SURVEY 8(f)1,
 # bitwise the same result as hg_gat_attention_fwd + hg_spmm on alpha).  Off by

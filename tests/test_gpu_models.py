@@ -478,6 +478,35 @@ def test_locality_relabel_same_graph_and_training(cuda):
     np.testing.assert_allclose(la, lb, rtol=0, atol=5e-3)
 
 
+def test_gin_combine_epilogue_bitwise(cuda):
+    """GIN's scale_combine folded into the aggregation's row store (forward)
+    and the residual gradient add into the transposed aggregation's store
+    (backward) train bit for bit like the separate passes (packs and split
+    rows included)."""
+    from paper_2411_01109_b200 import device as D, graphgen, models as M
+    from paper_2411_01109_b200.device import DeviceGraph
+
+    rows, cols, feats, labels = graphgen.synth_sbm(3000, 3, 0.05, 0.003, 40, 6)
+    hub = np.repeat(np.arange(3), 900)
+    rows = np.concatenate([rows, hub]).astype(np.int64)
+    cols = np.concatenate([cols, np.random.default_rng(0).integers(0, 3000, hub.size)])
+    dg = DeviceGraph.from_edges(3000, rows, cols)
+    cfg = M.TrainConfig(kind="gin", hidden=16, numerics="fast")
+    saved = (M.FUSED_GIN_COMBINE, D.PACK_MIN_ROWS)
+    out = []
+    try:
+        D.PACK_MIN_ROWS = 0
+        for fused in (False, True):
+            M.FUSED_GIN_COMBINE = fused
+            tr = M.Trainer(M.GraphBundle.build(dg), feats, labels, cfg)
+            losses = [float(tr.step()[0]) for _ in range(4)]
+            out.append((losses, tr.group.master.clone()))
+    finally:
+        M.FUSED_GIN_COMBINE, D.PACK_MIN_ROWS = saved
+    assert out[0][0] == out[1][0]
+    assert torch.equal(out[0][1], out[1][1])
+
+
 def test_run_epochs_host_feed_matches_steps(cuda):
     """Double-buffered host feeding (e2e path) trains exactly like step()."""
     from paper_2411_01109_b200 import graphgen, models as M
