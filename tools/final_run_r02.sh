@@ -1,3 +1,6 @@
+# Round-2 consolidated run on one B200 (smoke, GPU tests, every bench line,
+# the reference arm, launch lists, per-call traffic, one --set full SpMM capture).
+# usage: gpurun -- bash tools/final_run_r02.sh   (outputs under gpurun_out/r02/)
 P=gpurun_out/r02/final4; mkdir -p $P
 ( time timeout 300 python -c "import __graft_entry__ as g; g.smoke()" ) > $P/smoke.log 2>&1; echo smoke=$?
 timeout 1800 python -m pytest tests -m gpu -q > $P/pytest_gpu.log 2>&1; echo tests=$?; tail -1 $P/pytest_gpu.log
