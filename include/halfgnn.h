@@ -340,6 +340,20 @@ int hg_gemm_tc(const void* a, int64_t m, int64_t k, int64_t lda, const void* bt,
                int64_t ldb, const void* bias, const void* row_scale, int32_t relu, void* out,
                int64_t ldo, void* stream);
 
+/* The GAT projection with its head dots in one pass (GATLayer, models.py:492-509: z =
+ * matmul(x, W), then s_l = matmul(z_h, a_l[h]), s_r likewise, per head):
+ * out = rnd(a @ bt^T) as hg_gemm_tc (no bias / row_scale / relu), and
+ * dot_out_a[m, h] = rnd(sum_f out[m, h*fh + f] * dot_a[h*fh + f]) (dot_out_b
+ * from dot_b) -- exact products of the rounded z, fp32 sums, one rounding --
+ * formed from the TMEM accumulator tile in the epilogue instead of a second
+ * read of z (hg_head_dots); each epilogue thread owns whole heads, so no
+ * cross-thread sum.  heads <= 8, fh = n / heads a multiple of 16, heads even
+ * unless fh == 16;
+ * dot_a / dot_b: [heads * fh] binary16; dot_out_*: [m, heads]. */
+int hg_gemm_tc_dots(const void* a, int64_t m, int64_t k, int64_t lda, const void* bt, int32_t n,
+                    int64_t ldb, void* out, int64_t ldo, const void* dot_a, const void* dot_b,
+                    int32_t heads, void* dot_out_a, void* dot_out_b, void* stream);
+
 /* matmul backward's weight gradient (models.py:154-155, b._accumulate(mm(a.T,
  * g))): out[m, n] = rnd(sum_k a[k, m] b[k, n]) -- fp32 accumulation, one
  * rounding -- with accumulate != 0: out = rnd(out + that) (Tensor._accumulate,

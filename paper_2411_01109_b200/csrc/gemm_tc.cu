@@ -118,6 +118,18 @@ __device__ __forceinline__ void epi_bar_n(int threads) {  // named barrier over 
   asm volatile("bar.sync 1, %0;" ::"r"(threads) : "memory");
 }
 
+// packed fp32 FMA (FFMA2): d = a * b + c on both lanes, each lane one IEEE fma
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long x, y, z, d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a.x), "f"(a.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(y) : "f"(b.x), "f"(b.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(z) : "f"(c.x), "f"(c.y));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(x), "l"(y), "l"(z));
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(d));
+  return r;
+}
+
 // smem ring depth for a given N (the ring plus the output staging tile fit ~200 KB)
 template <int N, bool RESB>
 struct TcCfg {
@@ -140,7 +152,7 @@ struct TcCfg {
   static constexpr int kStages = kStages0 > 8 ? 8 : kStages0;
   static constexpr uint32_t kCols = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 2 * N <= 128 ? 128 : 2 * N <= 256 ? 256 : 512;
   static constexpr size_t kSmem = 1024 + (size_t)kStages * kSlot + kRes + kStage +
-                                  (2 * kStages + 5) * 8 + 16 + N * 2;
+                                  (2 * kStages + 5) * 8 + 16 + N * 2 + N * 8;
 };
 
 // Epilogue: kEpiWarps warps, two per TMEM lane quarter (warp w reads lanes
@@ -165,7 +177,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
           const __grid_constant__ CUtensorMap map_o, int64_t m, int num_kb, const __half* __restrict__ bias,
           const __half* __restrict__ row_scale, __half* __restrict__ out, int64_t ldo, int relu,
-          int n_out) {
+          int n_out, const __half* __restrict__ dot_a, const __half* __restrict__ dot_b,
+          int dot_heads, int dot_fh, __half* __restrict__ dot_out_a, __half* __restrict__ dot_out_b) {
   using C = TcCfg<N, RESB>;
   constexpr int S = C::kStages;
   constexpr int kEpiThreads = 32 * kEpiWarps;
@@ -173,12 +186,16 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
   constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kTcBM >> 4) << 24);
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* base = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-aligned, offset from smem_raw so the compiler keeps the shared state
+  // space (LDS / STS, not generic LD / ST)
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   unsigned char* sa = base;                          // [S][128 x 128 B]
   unsigned char* sb = base + S * C::kABytes;         // ring: [S][N x 128 B]; RESB: [kb][N x 128 B]
   unsigned char* stage = sb + (RESB ? C::kRes : S * C::kBBytes);  // output staging
-  uint64_t* full = reinterpret_cast<uint64_t*>(stage + C::kStage);
+  // head vectors for the epilogue's dots: [N / 2] column pairs as fp32
+  // (a_l[2p], a_l[2p + 1], a_r[2p], a_r[2p + 1])
+  float4* svec = reinterpret_cast<float4*>(stage + C::kStage);
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage + C::kStage + N * 8);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;                       // [2]
   uint64_t* tempty = tfull + 2;                      // [2]
@@ -207,6 +224,11 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
   }
   for (int j = threadIdx.x; j < N; j += blockDim.x)
     sbias[j] = (bias && j < n_out) ? bias[j] : __ushort_as_half(0);
+  if (dot_out_a) {  // head vectors by column pair, fp32, for the epilogue's dots
+    for (int p = threadIdx.x; p < N / 2; p += blockDim.x)
+      svec[p] = make_float4(__half2float(dot_a[2 * p]), __half2float(dot_a[2 * p + 1]),
+                            __half2float(dot_b[2 * p]), __half2float(dot_b[2 * p + 1]));
+  }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
@@ -269,6 +291,19 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
     const __half2 z2 = __half2half2(__ushort_as_half(0));
     const __half2* bias2 = reinterpret_cast<const __half2*>(sbias);
     constexpr int kChunks = N / 16;
+    constexpr int kPer = (kChunks + 1) / 2;  // chunks per warp half (the last may be absent)
+    // this warp half's 16-column chunks, in column order: whole groups of G
+    // chunks alternate between the halves -- G = 1 (chunk parity) normally, a
+    // head's width with the head dots so each thread owns whole heads
+    const int G = dot_out_a ? dot_fh >> 4 : 1;
+    int mych[kPer], myhd[kPer];
+    unsigned last = 0;  // bit k: chunk k completes its head (for this thread)
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      mych[k] = (2 * (k / G) + half) * G + k % G;
+      myhd[k] = 2 * (k / G) + half;
+      if (k % G == G - 1 || k == kPer - 1) last |= 1u << k;
+    }
     uint32_t tc = 0;
     for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tc) {
       const uint32_t a = tc & 1;
@@ -288,18 +323,25 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
         epi_bar_n(kEpiThreads);
       }
       unsigned char* srow = sbuf + r * (tstore ? 128 : C::kPitch);
-      // this warp's chunks: half, half + 2, ... ; TMEM loads two chunks per wait
+      // head dots (GAT s_l / s_r): this thread owns whole heads and meets their
+      // chunks in column order -- one running register pair (even / odd column
+      // lanes) per head, rounded and stored when the head is complete
+      float2 run_l = make_float2(0.0f, 0.0f), run_r = run_l;
+      // TMEM loads two chunks per wait
 #pragma unroll
-      for (int ch0 = half; ch0 < kChunks; ch0 += 4) {
+      for (int k0 = 0; k0 < kPer; k0 += 2) {
+        if constexpr (kChunks % 2 == 1) {  // warp-uniform: half 1 has one chunk fewer
+          if (mych[k0] >= kChunks) break;
+        }
         uint32_t vv[2][16];
-        const bool two = ch0 + 2 < kChunks;
-        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + a * N + ch0 * 16, vv[0]);
-        if (two) tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + a * N + (ch0 + 2) * 16, vv[1]);
+        const bool two = k0 + 1 < kPer && (kChunks % 2 == 0 || mych[k0 + 1] < kChunks);
+        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + a * N + mych[k0] * 16, vv[0]);
+        if (two) tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + a * N + mych[k0 + 1] * 16, vv[1]);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           if (u == 1 && !two) break;
-          const int c0 = (ch0 + 2 * u) * 16;
+          const int c0 = mych[k0 + u] * 16;
           __align__(16) __half2 h[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j)
@@ -311,6 +353,23 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
           if (row_scale) {
 #pragma unroll
             for (int j = 0; j < 8; ++j) h[j] = __hmul2_rn(h[j], sv2);
+          }
+          if (dot_out_a) {  // z . a over this chunk's 16 columns (exact products, fp32 sum)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 v = svec[c0 / 2 + j];
+              const float2 zf = __half22float2(h[j]);
+              run_l = ffma2(zf, make_float2(v.x, v.y), run_l);
+              run_r = ffma2(zf, make_float2(v.z, v.w), run_r);
+            }
+            if ((last >> (k0 + u)) & 1) {  // head complete: one rounding, then restart
+              if (live) {
+                const int hd = myhd[k0 + u];
+                dot_out_a[row * dot_heads + hd] = __float2half_rn(run_l.x + run_l.y);
+                dot_out_b[row * dot_heads + hd] = __float2half_rn(run_r.x + run_r.y);
+              }
+              run_l = run_r = make_float2(0.0f, 0.0f);
+            }
           }
           if (relu) {  // models.relu: x > 0 ? x : +0 (NaN -> 0)
 #pragma unroll
@@ -409,10 +468,19 @@ static bool make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t co
   return make_map_box(map, ptr, rows, cols, ld, (uint32_t)kTcBK, box_rows);
 }
 
+struct Dots {  // GAT head dots fused into the epilogue (NULL out_a: off)
+  const void* a;
+  const void* b;
+  int heads, fh;
+  void* out_a;
+  void* out_b;
+};
+
 template <int N, bool RESB>
 static int launch_gemm_tc_v(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
                             int64_t m, int num_kb, const void* bias, const void* row_scale,
-                            void* out, int64_t ldo, int relu, int n_out, cudaStream_t st) {
+                            void* out, int64_t ldo, int relu, int n_out, const Dots& dt,
+                            cudaStream_t st) {
   constexpr size_t smem = TcCfg<N, RESB>::kSmem;
   static_assert(smem <= 227 * 1024, "gemm_tc shared memory budget");
   static_assert(TcCfg<N, RESB>::kStages >= 2, "gemm_tc ring too shallow");
@@ -425,7 +493,8 @@ static int launch_gemm_tc_v(const CUtensorMap& ma, const CUtensorMap& mb, const 
   const unsigned grid = (unsigned)(tiles < sms ? tiles : sms);
   k_gemm_tc<N, RESB><<<grid, kTcThreads, smem, st>>>(
       ma, mb, mo, m, num_kb, (const __half*)bias, (const __half*)row_scale, (__half*)out, ldo, relu,
-      n_out);
+      n_out, (const __half*)dt.a, (const __half*)dt.b, dt.heads, dt.fh, (__half*)dt.out_a,
+      (__half*)dt.out_b);
   HG_LAUNCHED();
   return HG_OK;
 }
@@ -433,13 +502,13 @@ static int launch_gemm_tc_v(const CUtensorMap& ma, const CUtensorMap& mb, const 
 template <int N>
 static int launch_gemm_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
                           int64_t m, int64_t k, const void* bias, const void* row_scale, void* out,
-                          int64_t ldo, int relu, int n_out, cudaStream_t st) {
+                          int64_t ldo, int relu, int n_out, const Dots& dt, cudaStream_t st) {
   const int num_kb = (int)((k + kTcBK - 1) / kTcBK);
   if (num_kb <= TcCfg<N, true>::kMaxResKb)
     return launch_gemm_tc_v<N, true>(ma, mb, mo, m, num_kb, bias, row_scale, out, ldo, relu,
-                                     n_out, st);
+                                     n_out, dt, st);
   return launch_gemm_tc_v<N, false>(ma, mb, mo, m, num_kb, bias, row_scale, out, ldo, relu,
-                                    n_out, st);
+                                    n_out, dt, st);
 }
 
 
@@ -489,8 +558,9 @@ k_gemm_wgrad(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ 
   constexpr uint32_t kIdesc = (1u << 4) | (1u << 15) | (1u << 16) | ((uint32_t)(UN >> 3) << 17) |
                               ((uint32_t)(kTcBM >> 4) << 24);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* base = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-aligned, offset from smem_raw so the compiler keeps the shared state
+  // space (LDS / STS, not generic LD / ST)
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int group = blockIdx.x / splits, split = blockIdx.x - group * splits;
   const int t0 = group * mt_group;
   const int mt = min(mt_group, mt_total - t0);
@@ -750,9 +820,36 @@ static int launch_wgrad(const CUtensorMap& ma, const CUtensorMap& mb, const Wgra
 
 using namespace hg;
 
+static int gemm_tc_impl(const void* a, int64_t m, int64_t k, int64_t lda, const void* bt,
+                        int32_t n, int64_t ldb, const void* bias, const void* row_scale,
+                        int32_t relu, void* out, int64_t ldo, void* stream, const Dots& dots);
+
 extern "C" int hg_gemm_tc(const void* a, int64_t m, int64_t k, int64_t lda, const void* bt,
                           int32_t n, int64_t ldb, const void* bias, const void* row_scale,
                           int32_t relu, void* out, int64_t ldo, void* stream) {
+  return gemm_tc_impl(a, m, k, lda, bt, n, ldb, bias, row_scale, relu, out, ldo, stream, Dots{});
+}
+
+extern "C" int hg_gemm_tc_dots(const void* a, int64_t m, int64_t k, int64_t lda, const void* bt,
+                               int32_t n, int64_t ldb, void* out, int64_t ldo, const void* dot_a,
+                               const void* dot_b, int32_t heads, void* dot_out_a, void* dot_out_b,
+                               void* stream) {
+  HG_REQUIRE(heads >= 1 && heads <= 8 && n % heads == 0 && (n / heads) % 16 == 0,
+             "hg_gemm_tc_dots: heads=%d must split N=%d into multiples of 16 (<= 8 heads)", heads, n);
+  // each epilogue thread owns whole heads: an even head count, or 16-wide heads
+  HG_REQUIRE(heads % 2 == 0 || n / heads == 16,
+             "hg_gemm_tc_dots: %d heads of width %d: odd head counts need 16-wide heads", heads,
+             n / heads);
+  HG_REQUIRE(dot_a && dot_b && dot_out_a && dot_out_b &&
+                 ((reinterpret_cast<uintptr_t>(dot_a) | reinterpret_cast<uintptr_t>(dot_b)) & 3) == 0,
+             "hg_gemm_tc_dots: null or misaligned head vectors / outputs");
+  return gemm_tc_impl(a, m, k, lda, bt, n, ldb, nullptr, nullptr, 0, out, ldo, stream,
+                      Dots{dot_a, dot_b, heads, n / heads, dot_out_a, dot_out_b});
+}
+
+static int gemm_tc_impl(const void* a, int64_t m, int64_t k, int64_t lda, const void* bt,
+                        int32_t n, int64_t ldb, const void* bias, const void* row_scale,
+                        int32_t relu, void* out, int64_t ldo, void* stream, const Dots& dots) {
   HG_REQUIRE(m >= 0 && k > 0, "hg_gemm_tc: bad arguments");
   if (m == 0) return HG_OK;
   HG_REQUIRE(a && bt && out, "hg_gemm_tc: null operand");
@@ -785,7 +882,7 @@ extern "C" int hg_gemm_tc(const void* a, int64_t m, int64_t k, int64_t lda, cons
                (long long)m, n, (long long)ldo, g_tma_err);
   cudaStream_t st = as_stream(stream);
   switch (n16) {
-#define HG_TC(NN) case NN: return launch_gemm_tc<NN>(ma, mb, mo, m, k, bias, row_scale, out, ldo, relu, n, st);
+#define HG_TC(NN) case NN: return launch_gemm_tc<NN>(ma, mb, mo, m, k, bias, row_scale, out, ldo, relu, n, dots, st);
     HG_TC(16) HG_TC(32) HG_TC(48) HG_TC(64) HG_TC(80) HG_TC(96) HG_TC(112) HG_TC(128)
     HG_TC(144) HG_TC(160) HG_TC(176) HG_TC(192) HG_TC(208) HG_TC(224) HG_TC(240) HG_TC(256)
 #undef HG_TC

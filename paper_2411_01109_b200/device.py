@@ -1031,6 +1031,36 @@ def gemm_tc(a, bt, bias=None, row_scale=None, out=None, relu=False):
     return out
 
 
+def gemm_tc_dots(a, bt, a_l, a_r, heads):
+    """(z, s_l, s_r): z = rnd(a @ bt.T) on the tcgen05 tensor cores with the GAT
+    head dots s_l[n, h] = rnd(sum_f z[n, h, f] a_l[h, f]) (s_r likewise, fp32
+    sums of exact products of the rounded z) formed in the same epilogue
+    (hg_gemm_tc_dots): N / heads a multiple of 16, heads <= 8."""
+    _require_cuda(a, bt)
+    if a.dtype != torch.float16 or bt.dtype != torch.float16:
+        raise ValueError("hg_gemm_tc_dots takes binary16 operands")
+    a, bt = a.contiguous(), bt.contiguous()
+    if a.data_ptr() % 16:
+        a = a.clone()
+    if bt.data_ptr() % 16:
+        bt = bt.clone()
+    m, k = a.shape
+    n, k2 = bt.shape
+    if k2 != k:
+        raise ValueError(f"inner dimensions differ: {k} vs {k2}")
+    a_l = a_l.to(torch.float16).contiguous()
+    a_r = a_r.to(torch.float16).contiguous()
+    if a_l.numel() != n or a_r.numel() != n:
+        raise ValueError("head vectors must hold heads x (N / heads) values")
+    out = torch.empty((m, n), dtype=torch.float16, device=a.device)
+    s_l = torch.empty((m, heads), dtype=torch.float16, device=a.device)
+    s_r = torch.empty_like(s_l)
+    nat.call("hg_gemm_tc_dots", _p(a), m, k, a.stride(0), _p(bt), n, bt.stride(0), _p(out),
+             out.stride(0), _p(a_l), _p(a_r), heads, _p(s_l), _p(s_r), _stream())
+    Probe.launches += 1
+    return out, s_l, s_r
+
+
 def gemm_wgrad(a, b, out=None, bias_out=None, accumulate=False, bias=False):
     """rnd(a.T @ b) -- fp32 accumulation, one rounding -- on the tcgen05 tensor
     cores with the vertex dimension split across the SMs (hg_gemm_wgrad):

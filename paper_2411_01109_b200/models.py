@@ -878,15 +878,21 @@ class GATLayer:
 
     def __call__(self, bundle, x, mode, width, overflow, tag, relu_out=False):
         h, so = self.heads, self.store_out
-        z = matmul(x, self.w.publish(mode))                       # [N, H*so]
+        w = self.w.publish(mode)
         a_l, a_r = self.a_l.publish(mode), self.a_r.publish(mode)
         mean = self.reduce == "mean" and h > 1
         if (overflow is None and isinstance(bundle, GraphBundle) and bundle.fused_gat):
             fuse = relu_out and not mean
-            out = _GATCoreFn.apply(z, a_l, a_r, bundle, h, fuse)
+            if _dots_shapes(x, w, h) and a_l.dtype == torch.float16:
+                z, s_l, s_r = _GATProjFn.apply(x, w, a_l, a_r, h)      # [N, H*so], [N, H] x 2
+                out = _GATCoreFn.apply(z, a_l, a_r, bundle, h, fuse, s_l, s_r)
+            else:
+                z = matmul(x, w)                                      # [N, H*so]
+                out = _GATCoreFn.apply(z, a_l, a_r, bundle, h, fuse)
             if mean:
                 out = _HeadMeanFn.apply(out, h)
             return relu(out) if relu_out and not fuse else out
+        z = matmul(x, w)                                          # [N, H*so]
         # s = z_h . a_h for every head (models.matmul semantics: fp32
         # accumulation of exact products, one rounding), one kernel
         s_l, s_r = _HeadDotsFn.apply(z, a_l, a_r, h, bundle)
@@ -918,6 +924,44 @@ FUSED_GIN_COMBINE = os.environ.get("HG_FUSED_GIN", "1") != "0"
 FUSED_GAT_FWD = os.environ.get("HG_FUSED_GAT", "0") == "1"
 
 
+# The GAT projection's head dots formed in the GEMM epilogue (hg_gemm_tc_dots)
+# instead of a second read of z; HG_FUSED_GAT_DOTS=0: separate hg_head_dots.
+FUSED_GAT_DOTS = os.environ.get("HG_FUSED_GAT_DOTS", "1") != "0"
+
+
+def _dots_shapes(x, w, heads):
+    """hg_gemm_tc_dots takes the layer: <= 8 heads of a width that is a multiple
+    of 16, an even head count unless the heads are 16 wide."""
+    fh = w.shape[1] // heads
+    return (FUSED_GAT_DOTS and _tc_shapes(x, w) and heads <= 8 and w.shape[1] % heads == 0
+            and fh % 16 == 0 and (heads % 2 == 0 or fh == 16))
+
+
+class _GATProjFn(torch.autograd.Function):
+    """z = x W with the head dots s_l = z_h . a_l[h], s_r = z_h . a_r[h]
+    (GATLayer, models.py:492-509) from one tcgen05 GEMM whose epilogue forms the
+    dots from the accumulator tile (hg_gemm_tc_dots).  Backward: the head-dot
+    gradient accumulates into dz in place (hg_head_dots_bwd, gz_acc), then
+    dx = dz W^T (hg_gemm_tc) and dW = x^T dz (hg_gemm_wgrad)."""
+
+    @staticmethod
+    def forward(ctx, x, w, a_l, a_r, heads):
+        ctx.w_leaf, ctx.heads = w, heads
+        z, s_l, s_r = D.gemm_tc_dots(x, _wt(w), a_l, a_r, heads)
+        ctx.save_for_backward(x, w, z, a_l, a_r)
+        return z, s_l, s_r
+
+    @staticmethod
+    def backward(ctx, gz, ds_l, ds_r):
+        x, w, z, a_l, a_r = ctx.saved_tensors
+        gz = gz.contiguous()
+        gz, ga_l, ga_r = D.head_dots_bwd(z, a_l, a_r, ds_l.contiguous(), ds_r.contiguous(),
+                                         ctx.heads, gz_acc=gz)
+        gx = D.gemm_tc(gz, w) if ctx.needs_input_grad[0] else None
+        gw = _weight_grads(x, gz, ctx.w_leaf)[0] if ctx.needs_input_grad[1] else None
+        return gx, gw, ga_l, ga_r, None
+
+
 class _GATCoreFn(torch.autograd.Function):
     """The multi-head GAT layer core (models.py:492-509) after z = x W as one
     autograd node, for single-GPU fast numerics: head dots s = z a -> fused
@@ -928,8 +972,12 @@ class _GATCoreFn(torch.autograd.Function):
     (no separate add of the two N x H*F gradients)."""
 
     @staticmethod
-    def forward(ctx, z, a_l, a_r, bundle, heads, relu):
-        s_l, s_r = bundle.head_dots(z, a_l, a_r, heads)
+    def forward(ctx, z, a_l, a_r, bundle, heads, relu, s_l=None, s_r=None):
+        # s_l / s_r given: formed by the projection (_GATProjFn), whose backward
+        # takes their gradients and the head-dot backward
+        ctx.dots_in = s_l is not None
+        if not ctx.dots_in:
+            s_l, s_r = bundle.head_dots(z, a_l, a_r, heads)
         view = bundle.dg.view(False)
         if FUSED_GAT_FWD:
             # row statistics, then scores -> alpha -> weighted aggregation in
@@ -959,8 +1007,10 @@ class _GATCoreFn(torch.autograd.Function):
         # RMAT-24: +14.7 ms in the aggregation and +3 ms in the strided
         # attention kernels against the 10.6 ms sum pass it replaces)
         ds_r = D.edge_sums_fast(bwd, de, bwd.perm)
+        if ctx.dots_in:
+            return gz, None, None, None, None, None, ds_l, ds_r
         gz, ga_l, ga_r = D.head_dots_bwd(z, a_l, a_r, ds_l, ds_r, h, gz_acc=gz)
-        return gz, ga_l, ga_r, None, None, None
+        return gz, ga_l, ga_r, None, None, None, None, None
 
 
 class _HeadDotsFn(torch.autograd.Function):

@@ -1047,6 +1047,38 @@ def test_relu_grad(cuda):
     np.testing.assert_array_equal(bits(got), bits(np.where(pre > 0, g, np.float16(0))))
 
 
+@pytest.mark.parametrize("m,k,heads,fh", [(1, 8, 1, 16), (300, 128, 4, 32), (5000, 64, 8, 16),
+                                          (1031, 608, 2, 64), (2000, 128, 2, 128),
+                                          (700, 64, 3, 16), (129, 72, 1, 16)])
+def test_gemm_tc_dots_vs_f64(cuda, m, k, heads, fh):
+    """hg_gemm_tc_dots: z equals hg_gemm_tc bit for bit, and the epilogue's head
+    dots are rnd(sum_f z_h[f] a[h, f]) over the ROUNDED z -- exact products, fp32
+    sums -- within one fp16 step of the float64 value (and of hg_head_dots)."""
+    from paper_2411_01109_b200 import device as D
+
+    rng = np.random.default_rng(m + k + heads)
+    n = heads * fh
+    a = _t(rng.normal(0, 1, (m, k)).astype(np.float16), cuda)
+    bt = _t(rng.normal(0, 0.2, (n, k)).astype(np.float16), cuda)
+    al = _t(rng.normal(0, 0.3, (heads, fh)).astype(np.float16), cuda)
+    ar = _t(rng.normal(0, 0.3, (heads, fh)).astype(np.float16), cuda)
+    z, sl, sr = D.gemm_tc_dots(a, bt, al, ar, heads)
+    assert torch.equal(z.view(torch.int16), D.gemm_tc(a, bt).view(torch.int16))
+    zh = z.double().reshape(m, heads, fh)
+    hl, hr = D.head_dots(z, al, ar, heads)
+    for got, vec, other in ((sl, al, hl), (sr, ar, hr)):
+        want = (zh * vec.double()[None]).sum(-1)
+        mag = (zh.abs() * vec.double().abs()[None]).sum(-1)
+        h = want.half().double()
+        slack = 2.0 ** -10 * h.abs() + 1e-6 * mag + 2.0 ** -24
+        assert bool(((got.double() - h).abs() <= slack).all())
+        assert bool(((got.double() - other.double()).abs() <= 2 * slack).all())
+    with pytest.raises(ValueError, match="multiples of 16"):
+        D.gemm_tc_dots(a, bt.new_zeros(24, k), al.new_zeros(24), ar.new_zeros(24), 2)
+    with pytest.raises(ValueError, match="odd head counts"):
+        D.gemm_tc_dots(a, bt.new_zeros(96, k), al.new_zeros(96), ar.new_zeros(96), 3)
+
+
 def test_gemm_tc_from_autograd_worker_thread(cuda):
     """hg_gemm_tc encodes its TMA descriptors through the driver API; it must
     work from autograd's backward worker thread (no context bound there)."""

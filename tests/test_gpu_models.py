@@ -614,10 +614,12 @@ def test_gcn_large_graph_tracks_torch_fp32_with_grad_scale(cuda):
     assert abs(l1[1] - want[1]) > abs(got[1] - want[1])
 
 
-def test_gat_core_fused_matches_composed(cuda):
+@pytest.mark.parametrize("fh", [8, 16])
+def test_gat_core_fused_matches_composed(cuda, fh):
     """The single-node GAT core (_GATCoreFn, ReLU fused) against the composed
     ops (taken when overflow counters watch): same outputs and gradients up to
-    fp16 rounding order."""
+    fp16 rounding order.  fh=16: the projection also forms the head dots in its
+    GEMM epilogue (_GATProjFn, hg_gemm_tc_dots)."""
     from paper_2411_01109_b200 import graphgen, models as M
     from paper_2411_01109_b200.device import DeviceGraph
 
@@ -625,8 +627,9 @@ def test_gat_core_fused_matches_composed(cuda):
     dg = DeviceGraph.from_edges(400, rows, cols)
     b = M.GraphBundle.build(dg)
     rng = np.random.default_rng(0)
-    layer = M.GATLayer(rng, 24, 8, heads=4, store_in=24, store_out=8)
+    layer = M.GATLayer(rng, 24, fh, heads=4, store_in=24, store_out=fh)
     x = torch.from_numpy(feats).cuda().half()
+    assert M._dots_shapes(x, layer.w.publish("half"), 4) == (fh == 16)
     outs, grads = [], []
     for ov in (None, M.OverflowCounters()):
         for p in layer.params():
