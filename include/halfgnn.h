@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define HG_ABI_VERSION 5
+#define HG_ABI_VERSION 6
 
 enum { HG_OK = 0, HG_EINVAL = 1, HG_ECUDA = 2 };
 enum { HG_F16 = 0, HG_F32 = 1 };
@@ -134,7 +134,12 @@ int hg_schedule_build(const int64_t* offsets, int64_t n, int32_t split_cap, int3
  * the finished aggregate, fp64 products (models.py:220-240 scale_combine);
  * comb_ope: device scalar of the element type (NULL: 1); with ope = NULL and
  * lam = 1 a rounded residual add (a gradient accumulated into the output).
- * Not with relu. */
+ * Not with relu.
+ * hd_gl (NULL: off) with hd_gr, hd_al, hd_ar: the GAT head-dot backward's dz
+ * term in the same store (GATLayer, models.py:492-509; hg_head_dots_bwd with
+ * gz_in): y[r, c] = rnd(h + rnd(rnd(hd_gl[r, c / fh] * hd_al[c]) +
+ * rnd(hd_gr[r, c / fh] * hd_ar[c]))), fh = F / heads; hd_gl / hd_gr:
+ * [n_rows, heads], hd_al / hd_ar: [F].  Not with comb_res, out2 or relu. */
 int hg_spmm_workspace(int64_t n_cols, int32_t F, int64_t num_slots, int has_in_scale,
                       int32_t sum_heads, int dtype, size_t* bytes);
 int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_rows, int64_t n_cols,
@@ -146,7 +151,8 @@ int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_rows, int64_t
             const void* in_scale, const void* out_factor, int64_t w_ld, int32_t w2_off,
             void* out2, int dtype, void* ws, size_t ws_bytes, void* stream,
             int32_t* split_counters, const int32_t* slot_split, const void* comb_res,
-            int64_t comb_ldr, const void* comb_ope, double comb_lam);
+            int64_t comb_ldr, const void* comb_ope, double comb_lam, const void* hd_gl,
+            const void* hd_gr, const void* hd_al, const void* hd_ar);
 
 /* hg_spmm in fp32 partial mode, for column-blocked aggregation
  * (a row's edges split by the rank owning their column, block q run as soon as
@@ -287,7 +293,9 @@ int hg_head_dots(const void* z, const void* a_l, const void* a_r, int64_t n, int
  * ga_{l,r}[h, f] = rnd(sum_n z[n, h*fh+f] g_{l,r}[n, h]) with a deterministic
  * two-pass fp32 reduction (workspace: hg_head_dots_bwd_workspace).  With gz_in
  * (may alias gz) the result is accumulated: gz = rnd(gz_in + that value) -- the
- * two gradient contributions z receives in a GAT layer, summed in one pass. */
+ * two gradient contributions z receives in a GAT layer, summed in one pass.
+ * gz NULL: only ga_l / ga_r (the dz term already folded into the transposed
+ * aggregation's store, hg_spmm hd_gl). */
 int hg_head_dots_bwd_workspace(int32_t heads, int32_t fh, size_t* bytes);
 int hg_head_dots_bwd(const void* z, const void* a_l, const void* a_r, const void* g_l,
                      const void* g_r, int64_t n, int32_t heads, int32_t fh, void* gz,

@@ -18,7 +18,7 @@ from pathlib import Path
 LIB_PATH = Path(os.environ.get("HG_LIB") or Path(__file__).resolve().with_name("libhalfgnn.so"))
 
 HG_OK, HG_EINVAL, HG_ECUDA = 0, 1, 2
-ABI_VERSION = 5
+ABI_VERSION = 6
 HG_F16, HG_F32 = 0, 1
 SCALING_CODES = {"post": 0, "pre": 1, "discretized": 2}
 FACTOR_INV, FACTOR_INV_SQRT = 1, 2
@@ -45,7 +45,7 @@ SIGNATURES = {
     "hg_spmm": [_P, _P, _I64, _I64, _I64, _P, _I64, _P, _I64, _I64, _P, _I64, _P, _P, _P, _I32,
                 _P, _P,
                 _I32, _I64, _I64, _I32, _I32, _P, _P, _I64, _I32, _P, c_int, _P, c_size_t, _P,
-                _P, _P, _P, _I64, _P, c_double],
+                _P, _P, _P, _I64, _P, c_double, _P, _P, _P, _P],
     "hg_spmm_edge_ref_workspace": [_I64, _I64, _I32, _I32, _I32, c_int, c_int, _PSZ],
     "hg_spmm_edge_ref": [_P, _P, _I64, _I64, _I64, _I32, _I32, _P, _P, _P, _I32, _I32, _P, _P,
                          _P, _P, c_int, _P, c_size_t, _P],

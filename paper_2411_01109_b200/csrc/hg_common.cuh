@@ -91,6 +91,7 @@ struct Num<__half> {
   static __device__ __forceinline__ __half2 add2(__half2 a, __half2 b) { return __hadd2_rn(a, b); }
   static __device__ __forceinline__ __half2 mul2(__half2 a, __half2 b) { return __hmul2_rn(a, b); }
   static __device__ __forceinline__ __half2 bcast(__half a) { return __half2half2(a); }
+  static __device__ __forceinline__ __half2 pack2(__half a, __half b) { return __halves2half2(a, b); }
   static __device__ __forceinline__ __half2 zero2() { return __halves2half2(zero(), zero()); }
   static __device__ __forceinline__ __half lo(__half2 v) { return __low2half(v); }
   static __device__ __forceinline__ __half hi(__half2 v) { return __high2half(v); }
@@ -118,6 +119,7 @@ struct Num<float> {
     return make_float2(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y));
   }
   static __device__ __forceinline__ float2 bcast(float a) { return make_float2(a, a); }
+  static __device__ __forceinline__ float2 pack2(float a, float b) { return make_float2(a, b); }
   static __device__ __forceinline__ float2 zero2() { return make_float2(0.0f, 0.0f); }
   static __device__ __forceinline__ float lo(float2 v) { return v.x; }
   static __device__ __forceinline__ float hi(float2 v) { return v.y; }

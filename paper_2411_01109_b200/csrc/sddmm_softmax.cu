@@ -1449,7 +1449,7 @@ k_head_dots_bwd(const T* __restrict__ z, const T* __restrict__ al, const T* __re
         const T g1 = gl[r * heads + h], g2 = gr[r * heads + h];
         const float zf = N::to_f(z[r * F + f]);
         const T v = N::add(N::mul(g1, a1), N::mul(g2, a2));
-        gz[r * F + f] = gz_in ? N::add(gz_in[r * F + f], v) : v;
+        if (gz) gz[r * F + f] = gz_in ? N::add(gz_in[r * F + f], v) : v;
         sl = fmaf(zf, N::to_f(g1), sl);
         sr = fmaf(zf, N::to_f(g2), sr);
       }
@@ -1509,7 +1509,7 @@ k_head_dots_bwd_v8(const __half* __restrict__ z, const __half* __restrict__ al,
           g1[u] = gl[r * heads + h];
           g2[u] = gr[r * heads + h];
           zv[u] = *reinterpret_cast<const uint4*>(z + r * F + c * 8);
-          if (gz_in) prev[u] = *reinterpret_cast<const uint4*>(gz_in + r * F + c * 8);
+          if (gz && gz_in) prev[u] = *reinterpret_cast<const uint4*>(gz_in + r * F + c * 8);
         }
       }
 #pragma unroll
@@ -1528,7 +1528,8 @@ k_head_dots_bwd_v8(const __half* __restrict__ z, const __half* __restrict__ al,
           sl[i] = fmaf(zf, g1f, sl[i]);
           sr[i] = fmaf(zf, g2f, sr[i]);
         }
-        *reinterpret_cast<uint4*>(gz + r * F + c * 8) = *reinterpret_cast<const uint4*>(o);
+        // gz NULL: the dz term went into the aggregation's store (hg_spmm head dots)
+        if (gz) *reinterpret_cast<uint4*>(gz + r * F + c * 8) = *reinterpret_cast<const uint4*>(o);
       }
     }
   }

@@ -94,6 +94,15 @@ struct Combine {
   int64_t ldr;
   const void* ope;   // device scalar of the element type (NULL: 1)
   double lam;
+  // GAT head-dot backward in the store (hg_head_dots_bwd's dz term): with
+  // hgl set, out = rnd(h + rnd(rnd(gl[row, hd] al[c]) + rnd(gr[row, hd] ar[c]))),
+  // hd = c / hfh -- the transposed aggregation's dz and the head dots' in one store
+  const void* hgl;
+  const void* hgr;
+  const void* hal;
+  const void* har;
+  int hheads, hfh;
+  int hcol0;  // the column slab's first column
 };
 
 template <typename T, int V>
@@ -115,9 +124,61 @@ __device__ __forceinline__ void store_out_comb(T* dst, const float (&acc)[V], in
 }
 
 template <typename T, int V>
+__device__ __forceinline__ void store_out_hdots(T* dst, const float (&acc)[V], int fmode, T fo,
+                                                const Combine& cb, int64_t row, int64_t col) {
+  using Raw = typename RawVec<V * sizeof(T)>::type;
+  const T* gl = static_cast<const T*>(cb.hgl) + row * cb.hheads;
+  const T* gr = static_cast<const T*>(cb.hgr) + row * cb.hheads;
+  const T* al = static_cast<const T*>(cb.hal);
+  const T* ar = static_cast<const T*>(cb.har);
+  Raw r;
+  T* p = reinterpret_cast<T*>(&r);
+  const int c0 = (int)col + cb.hcol0;
+  int hd = c0 / cb.hfh, next = (hd + 1) * cb.hfh;
+  T g1 = gl[hd], g2 = gr[hd];
+  if constexpr (V % 2 == 0) {
+    // the lane's columns inside one head (fh a multiple of V) and the head
+    // vectors Raw-aligned: vector loads of a_l / a_r, paired math (the same
+    // per-element IEEE roundings as the scalar path)
+    if (c0 + V <= next && ((reinterpret_cast<uintptr_t>(al + c0) |
+                            reinterpret_cast<uintptr_t>(ar + c0)) % sizeof(Raw)) == 0) {
+      using T2 = typename Num<T>::T2;
+      const Raw ra = *reinterpret_cast<const Raw*>(al + c0);
+      const Raw rb = *reinterpret_cast<const Raw*>(ar + c0);
+      const T2* a2 = reinterpret_cast<const T2*>(&ra);
+      const T2* b2 = reinterpret_cast<const T2*>(&rb);
+      const T2 g12 = Num<T>::bcast(g1), g22 = Num<T>::bcast(g2);
+      T2* p2 = reinterpret_cast<T2*>(&r);
+#pragma unroll
+      for (int i = 0; i < V / 2; ++i) {
+        const T2 hh = Num<T>::pack2(finalize<T>(acc[2 * i], fmode, fo),
+                                    finalize<T>(acc[2 * i + 1], fmode, fo));
+        p2[i] = Num<T>::add2(hh, Num<T>::add2(Num<T>::mul2(g12, a2[i]), Num<T>::mul2(g22, b2[i])));
+      }
+      *reinterpret_cast<Raw*>(dst) = r;
+      return;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int c = c0 + i;
+    if (c == next) {  // the lane's columns cross into the next head
+      ++hd;
+      next += cb.hfh;
+      g1 = gl[hd];
+      g2 = gr[hd];
+    }
+    const T h = finalize<T>(acc[i], fmode, fo);
+    p[i] = Num<T>::add(h, Num<T>::add(Num<T>::mul(g1, al[c]), Num<T>::mul(g2, ar[c])));
+  }
+  *reinterpret_cast<Raw*>(dst) = r;
+}
+
+template <typename T, int V>
 __device__ __forceinline__ void store_fin(T* dst, const float (&acc)[V], int fmode, T fo,
                                           const Combine& cb, int64_t row, int64_t col) {
-  if (cb.res) store_out_comb<T, V>(dst, acc, fmode, fo,
+  if (cb.hgl) store_out_hdots<T, V>(dst, acc, fmode, fo, cb, row, col);
+  else if (cb.res) store_out_comb<T, V>(dst, acc, fmode, fo,
                                    static_cast<const T*>(cb.res) + row * cb.ldr + col,
                                    cb.ope ? Num<T>::to_d(*static_cast<const T*>(cb.ope)) : 1.0, cb.lam);
   else store_out<T, V>(dst, acc, fmode, fo);
@@ -1065,6 +1126,7 @@ static int spmm_impl(const int64_t* offsets, const int32_t* cols, int64_t n_rows
     if (acc_in) s.acc_in = acc_in + j;
     if (acc_out) s.acc_out = acc_out + j;
     if (comb.res) s.comb.res = static_cast<const char*>(comb.res) + (size_t)j * elem_size(dtype);
+    s.comb.hcol0 = j;
     const int rc = dtype == HG_F16 ? dispatch_fast<__half>(s) : dispatch_fast<float>(s);
     if (rc) return rc;
   }
@@ -1081,12 +1143,18 @@ extern "C" int hg_spmm(const int64_t* offsets, const int32_t* cols, int64_t n_ro
                        int64_t w_ld, int32_t w2_off, void* out2, int dtype, void* ws,
                        size_t ws_bytes, void* stream, int32_t* split_counters,
                        const int32_t* slot_split, const void* comb_res, int64_t comb_ldr,
-                       const void* comb_ope, double comb_lam) {
+                       const void* comb_ope, double comb_lam, const void* hd_gl,
+                       const void* hd_gr, const void* hd_al, const void* hd_ar) {
+  HG_REQUIRE(!hd_gl || (hd_gr && hd_al && hd_ar && !comb_res && heads >= 1 && F % heads == 0 &&
+                        !out2 && !relu),
+             "hg_spmm: the head-dot store needs g_l, g_r, a_l, a_r, F = heads x fh, no residual "
+             "combine, second output or ReLU");
   return spmm_impl(offsets, cols, n_rows, n_cols, num_edges, units, num_units, split_rows,
                    num_split_rows, num_slots, packs, num_packs, pack_rowid, w, w_index, heads, x, y,
                    F, ldx, ldy, scaling, relu, in_scale, out_factor, w_ld, w2_off, out2, dtype, ws,
                    ws_bytes, stream, nullptr, nullptr, split_counters, slot_split,
-                   Combine{comb_res, comb_ldr, comb_ope, comb_lam});
+                   Combine{comb_res, comb_ldr, comb_ope, comb_lam, hd_gl, hd_gr, hd_al, hd_ar,
+                           heads, hd_gl ? F / heads : 1, 0});
 }
 
 extern "C" int hg_spmm_acc(const int64_t* offsets, const int32_t* cols, int64_t n_rows,

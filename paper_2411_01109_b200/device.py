@@ -561,12 +561,14 @@ def _row_strided(t):
 def spmm_csr(view: CsrView, x: torch.Tensor, w=None, w_index=None, heads: int = 1,
              scaling: str = "post", fin=None, fout=None, out=None,
              split_cap: int = DEFAULT_SPLIT_CAP, relu: bool = False, w2_off: int = 0,
-             out2=None, combine=None) -> torch.Tensor:
+             out2=None, combine=None, head_dots=None) -> torch.Tensor:
     """fp32-guarded row-owned SpMM over one CSR view (hg_spmm).  x and out may
     be column slices of wider row-major storage (row strides passed through).
     combine = (res [n_rows, F], ope (device scalar or None), lam): the row store
     writes rnd(rnd(res * ope) + rnd(y * lam)) (GIN's combine; ope None and
-    lam 1: a rounded residual add)."""
+    lam 1: a rounded residual add).  head_dots = (g_l, g_r [n_rows, heads],
+    a_l, a_r [F]): the row store adds the GAT head-dot backward's dz term,
+    rnd(y + rnd(rnd(g_l a_l) + rnd(g_r a_r))) per head (hg_head_dots_bwd's)."""
     _require_cuda(x)
     if not _row_strided(x) or fin is not None:
         x = x.contiguous()
@@ -606,6 +608,14 @@ def spmm_csr(view: CsrView, x: torch.Tensor, w=None, w_index=None, heads: int = 
             raise ValueError("combine residual must be [n_rows, F] of the feature dtype")
         if c_ope is not None:
             c_ope = c_ope.reshape(-1)[:1].contiguous()
+    hd = (None, None, None, None)
+    if head_dots is not None:
+        # (head vectors re-based to 32-byte alignment for the store's vector loads)
+        hd = tuple(t.to(x.dtype).contiguous() for t in head_dots)
+        hd = hd[:2] + tuple(t if t.data_ptr() % 32 == 0 else t.clone() for t in hd[2:])
+        if (hd[0].shape != (view.n_rows, heads) or hd[1].shape != (view.n_rows, heads)
+                or hd[2].numel() != f or hd[3].numel() != f):
+            raise ValueError("head_dots: g_l, g_r [n_rows, heads] and a_l, a_r [F]")
     nat.call("hg_spmm", _p(view.offsets), _p(view.cols), view.n_rows, view.n_cols,
              view.num_edges, _p(sched.units), sched.num_units, _p(sched.split_rows),
              sched.split_rows.shape[0], sched.num_slots, _p(sched.packs), sched.num_packs,
@@ -613,7 +623,7 @@ def spmm_csr(view: CsrView, x: torch.Tensor, w=None, w_index=None, heads: int = 
              _p(out), f, x.stride(0), out.stride(0), nat.SCALING_CODES[scaling], int(relu),
              _p(fin), _p(fout), w_ld, int(w2_off), _p(out2), dt, _p(ws),
              0 if ws is None else ws.numel(), _stream(), *map(_p, fin_state), _p(c_res),
-             0 if c_res is None else c_res.stride(0), _p(c_ope), float(c_lam))
+             0 if c_res is None else c_res.stride(0), _p(c_ope), float(c_lam), *map(_p, hd))
     Probe.launches += int(sched.num_units > 0) + int(sched.num_packs > 0) + int(
         sched.split_rows.shape[0] > 0 and fin_state[0] is None) + int(fin is not None)
     if Probe.timing:
@@ -1250,13 +1260,17 @@ def loss_mean(nll, denom):
     Probe.launches += 1
 
 
-def head_dots_bwd(z, a_l, a_r, g_l, g_r, heads, gz_acc=None):
+def head_dots_bwd(z, a_l, a_r, g_l, g_r, heads, gz_acc=None, dz=True):
     """Backward of head_dots: (gz, ga_l, ga_r), deterministic (hg_head_dots_bwd).
-    gz_acc: an existing gradient of z to accumulate into (in place)."""
+    gz_acc: an existing gradient of z to accumulate into (in place); dz=False:
+    only (None, ga_l, ga_r) -- the dz term went into an aggregation's store."""
     z = z.contiguous()
     n = z.shape[0]
     fh = z.shape[1] // heads
-    gz = torch.empty_like(z) if gz_acc is None else gz_acc
+    if not dz:
+        gz = gz_acc = None
+    else:
+        gz = torch.empty_like(z) if gz_acc is None else gz_acc
     ga_l = torch.empty_like(a_l)
     ga_r = torch.empty_like(a_r)
     ws = workspace(nat.size_query("hg_head_dots_bwd_workspace", heads, fh), z.device)

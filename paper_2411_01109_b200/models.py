@@ -929,6 +929,12 @@ FUSED_GAT_FWD = os.environ.get("HG_FUSED_GAT", "0") == "1"
 FUSED_GAT_DOTS = os.environ.get("HG_FUSED_GAT_DOTS", "1") != "0"
 
 
+# The head dots' dz term folded into the transposed aggregation's row store
+# (hg_spmm hd_gl) instead of a read-modify-write pass over dz in
+# hg_head_dots_bwd; HG_FUSED_GAT_DZ=0: the separate accumulate.
+FUSED_GAT_DZ = os.environ.get("HG_FUSED_GAT_DZ", "1") != "0"
+
+
 def _dots_shapes(x, w, heads):
     """hg_gemm_tc_dots takes the layer: <= 8 heads of a width that is a multiple
     of 16, an even head count unless the heads are 16 wide."""
@@ -946,6 +952,7 @@ class _GATProjFn(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, x, w, a_l, a_r, heads):
+        ctx.set_materialize_grads(False)
         ctx.w_leaf, ctx.heads = w, heads
         z, s_l, s_r = D.gemm_tc_dots(x, _wt(w), a_l, a_r, heads)
         ctx.save_for_backward(x, w, z, a_l, a_r)
@@ -955,8 +962,10 @@ class _GATProjFn(torch.autograd.Function):
     def backward(ctx, gz, ds_l, ds_r):
         x, w, z, a_l, a_r = ctx.saved_tensors
         gz = gz.contiguous()
-        gz, ga_l, ga_r = D.head_dots_bwd(z, a_l, a_r, ds_l.contiguous(), ds_r.contiguous(),
-                                         ctx.heads, gz_acc=gz)
+        ga_l = ga_r = None
+        if ds_l is not None:  # (None: the consumer folded the head-dot backward in)
+            gz, ga_l, ga_r = D.head_dots_bwd(z, a_l, a_r, ds_l.contiguous(), ds_r.contiguous(),
+                                             ctx.heads, gz_acc=gz)
         gx = D.gemm_tc(gz, w) if ctx.needs_input_grad[0] else None
         gw = _weight_grads(x, gz, ctx.w_leaf)[0] if ctx.needs_input_grad[1] else None
         return gx, gw, ga_l, ga_r, None
@@ -1000,13 +1009,20 @@ class _GATCoreFn(torch.autograd.Function):
             g = D.relu_grad(y, g)
         dalpha = b.sddmm(g, z, heads=h).reshape(-1, h)
         bwd = b.dg.view(True)
-        gz = D.spmm_csr(bwd, g, alpha, bwd.perm, h, "post")
         de, ds_l = D.gat_attention_bwd(b.dg.view(False), s_l, s_r, alpha, dalpha, 0.2)
         # (fusing these column sums into the transposed aggregation through
         # interleaved (alpha | d_e) rows -- hg_spmm out2 -- measured slower on
         # RMAT-24: +14.7 ms in the aggregation and +3 ms in the strided
         # attention kernels against the 10.6 ms sum pass it replaces)
         ds_r = D.edge_sums_fast(bwd, de, bwd.perm)
+        if FUSED_GAT_DZ:
+            # the head dots' dz term added in the transposed aggregation's row
+            # store (bitwise the separate accumulate), then only da = z^T ds
+            gz = D.spmm_csr(bwd, g, alpha, bwd.perm, h, "post",
+                            head_dots=(ds_l, ds_r, a_l, a_r))
+            _, ga_l, ga_r = D.head_dots_bwd(z, a_l, a_r, ds_l, ds_r, h, dz=False)
+            return gz, ga_l, ga_r, None, None, None, None, None
+        gz = D.spmm_csr(bwd, g, alpha, bwd.perm, h, "post")
         if ctx.dots_in:
             return gz, None, None, None, None, None, ds_l, ds_r
         gz, ga_l, ga_r = D.head_dots_bwd(z, a_l, a_r, ds_l, ds_r, h, gz_acc=gz)

@@ -713,6 +713,48 @@ def test_spmm_fused_followup_bitwise(cuda, f, mode):
         assert torch.equal(outs[0][1].view(torch.int16), outs[1][1].view(torch.int16))
 
 
+@pytest.mark.parametrize("heads,fh", [(1, 16), (4, 16), (4, 32), (2, 64), (3, 16), (1, 256)])
+@pytest.mark.parametrize("packs", [False, True])
+def test_spmm_head_dot_store_bitwise(cuda, heads, fh, packs):
+    """hg_spmm with the head-dot store (hd_gl..) == hg_spmm then hg_head_dots_bwd
+    accumulating into its output, bit for bit: every row class (split hub rows,
+    fused and separate follow-up, packs), multi-head weights through a perm;
+    and head_dots_bwd(dz=False) gives the same da."""
+    from paper_2411_01109_b200 import device as D
+
+    n, f = 6000, heads * fh
+    r, c = _hub_graph(heads + fh, n)
+    r, c = O.canonical_edges(n, c, r)   # hubs on the CSC side (the view aggregated)
+    dg = _dg(n, r, c, cuda)
+    view = dg.view(True)
+    rng = np.random.default_rng(heads * fh)
+    x = _t(rng.normal(0, 1, (n, f)).astype(np.float16), cuda)
+    z = _t(rng.normal(0, 1, (n, f)).astype(np.float16), cuda)
+    w = _t(rng.uniform(0, 1, (r.size, heads)).astype(np.float16), cuda)
+    gl = _t(rng.normal(0, 2, (n, heads)).astype(np.float16), cuda)
+    gr = _t(rng.normal(0, 2, (n, heads)).astype(np.float16), cuda)
+    al = _t(rng.normal(0, 0.5, f).astype(np.float16), cuda)
+    ar = _t(rng.normal(0, 0.5, f).astype(np.float16), cuda)
+    saved = D.PACK_MIN_ROWS, D.FUSED_FOLLOWUP
+    D.PACK_MIN_ROWS = 0 if packs else 1 << 40
+    try:
+        for fused in (False, True):
+            D.FUSED_FOLLOWUP = fused
+            want = D.spmm_csr(view, x, w, view.perm, heads, "post")
+            want, wl, wr = D.head_dots_bwd(z, al, ar, gl, gr, heads, gz_acc=want)
+            got = D.spmm_csr(view, x, w, view.perm, heads, "post", head_dots=(gl, gr, al, ar))
+            assert torch.equal(got.view(torch.int16), want.view(torch.int16))
+            none, gotl, gotr = D.head_dots_bwd(z, al, ar, gl, gr, heads, dz=False)
+            assert none is None
+            assert torch.equal(gotl.view(torch.int16), wl.view(torch.int16))
+            assert torch.equal(gotr.view(torch.int16), wr.view(torch.int16))
+    finally:
+        D.PACK_MIN_ROWS, D.FUSED_FOLLOWUP = saved
+    assert view.schedule(D.DEFAULT_SPLIT_CAP, -1).split_rows.shape[0] > 0
+    with pytest.raises(ValueError, match="head-dot store"):
+        D.spmm_csr(view, x, w, view.perm, heads, "post", relu=True, head_dots=(gl, gr, al, ar))
+
+
 @pytest.mark.parametrize("f", [16, 48, 64, 128])
 @pytest.mark.parametrize("parts,packs", [(2, False), (3, True), (8, False), (8, True)])
 def test_spmm_acc_column_blocks_chain(cuda, f, parts, packs):

@@ -614,6 +614,37 @@ def test_gcn_large_graph_tracks_torch_fp32_with_grad_scale(cuda):
     assert abs(l1[1] - want[1]) > abs(got[1] - want[1])
 
 
+@pytest.mark.parametrize("fh", [8, 16, 32])
+def test_gat_head_dot_folds_bitwise(cuda, fh):
+    """The GAT layer with the projection's head dots in the GEMM epilogue and
+    their dz term in the transposed aggregation's store (HG_FUSED_GAT_DZ) ==
+    the separate hg_head_dots_bwd accumulate: bitwise the same outputs and
+    gradients of every parameter."""
+    from paper_2411_01109_b200 import graphgen, models as M
+    from paper_2411_01109_b200.device import DeviceGraph
+
+    rows, cols, feats, labels = graphgen.synth_sbm(3000, 3, 0.01, 0.001, 32, 5)
+    dg = DeviceGraph.from_edges(3000, rows, cols)
+    b = M.GraphBundle.build(dg)
+    rng = np.random.default_rng(1)
+    layer = M.GATLayer(rng, 32, fh, heads=4, store_in=32, store_out=fh)
+    x = torch.from_numpy(feats).cuda().half()
+    res = []
+    saved = M.FUSED_GAT_DZ
+    try:
+        for dz in (False, True):
+            M.FUSED_GAT_DZ = dz
+            for p in layer.params():
+                p.published = None
+            y = layer(b, x, "half", "half2", None, "gat", relu_out=True)
+            (y.float() * torch.linspace(-1, 1, y.numel(), device=cuda).view_as(y)).sum().backward()
+            res.append([y.detach()] + [p.published.grad.clone() for p in layer.params()])
+    finally:
+        M.FUSED_GAT_DZ = saved
+    for a, c in zip(*res):
+        assert torch.equal(a.view(torch.int16), c.view(torch.int16))
+
+
 @pytest.mark.parametrize("fh", [8, 16])
 def test_gat_core_fused_matches_composed(cuda, fh):
     """The single-node GAT core (_GATCoreFn, ReLU fused) against the composed

@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert set(declared) == set(_native.SIGNATURES), "ctypes table out of sync with header"
-    assert lib.hg_abi_version() == 5
+    assert lib.hg_abi_version() == 6
 
 
 def test_library_workspace_queries_without_gpu():
