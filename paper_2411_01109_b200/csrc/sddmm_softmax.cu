@@ -1474,8 +1474,11 @@ k_head_dots_bwd(const T* __restrict__ z, const T* __restrict__ al, const T* __re
 
 // Vectorised pass 1 for binary16 with fh % 8 == 0: thread (rr, c) owns the
 // 8-feature chunk c of row slot rr (one head), 16-byte loads / stores, fp32
-// partials per feature folded over the row slots in slot order.
-__global__ void __launch_bounds__(256)
+// partials per feature folded over the row slots in slot order.  DZ = false
+// (gz NULL: da only): no gz traffic, so <= 64 registers and all kHdbBlocks
+// blocks resident at once -- the same rows in the same order, the same da bits.
+template <bool DZ>
+__global__ void __launch_bounds__(256, DZ ? 2 : 4)
 k_head_dots_bwd_v8(const __half* __restrict__ z, const __half* __restrict__ al,
                    const __half* __restrict__ ar, const __half* __restrict__ gl,
                    const __half* __restrict__ gr, int64_t n, int heads, int fh,
@@ -1509,7 +1512,7 @@ k_head_dots_bwd_v8(const __half* __restrict__ z, const __half* __restrict__ al,
           g1[u] = gl[r * heads + h];
           g2[u] = gr[r * heads + h];
           zv[u] = *reinterpret_cast<const uint4*>(z + r * F + c * 8);
-          if (gz && gz_in) prev[u] = *reinterpret_cast<const uint4*>(gz_in + r * F + c * 8);
+          if (DZ && gz_in) prev[u] = *reinterpret_cast<const uint4*>(gz_in + r * F + c * 8);
         }
       }
 #pragma unroll
@@ -1529,7 +1532,7 @@ k_head_dots_bwd_v8(const __half* __restrict__ z, const __half* __restrict__ al,
           sr[i] = fmaf(zf, g2f, sr[i]);
         }
         // gz NULL: the dz term went into the aggregation's store (hg_spmm head dots)
-        if (gz) *reinterpret_cast<uint4*>(gz + r * F + c * 8) = *reinterpret_cast<const uint4*>(o);
+        if (DZ) *reinterpret_cast<uint4*>(gz + r * F + c * 8) = *reinterpret_cast<const uint4*>(o);
       }
     }
   }
@@ -1788,8 +1791,9 @@ extern "C" int hg_head_dots_bwd(const void* z, const void* a_l, const void* a_r,
     if (vec) {
       const size_t sh = (size_t)2 * (256 / (F / 8)) * F * sizeof(float);
       if (sh > 48 * 1024)
-        HG_CUDA(cudaFuncSetAttribute(k_head_dots_bwd_v8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
-      k_head_dots_bwd_v8<<<kHdbBlocks, 256, sh, st>>>(
+        HG_CUDA(cudaFuncSetAttribute(gz ? k_head_dots_bwd_v8<true> : k_head_dots_bwd_v8<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+      (gz ? k_head_dots_bwd_v8<true> : k_head_dots_bwd_v8<false>)<<<kHdbBlocks, 256, sh, st>>>(
           (const __half*)z, (const __half*)a_l, (const __half*)a_r, (const __half*)g_l,
           (const __half*)g_r, n, heads, fh, (__half*)gz, (const __half*)gz_in, part);
     } else {
