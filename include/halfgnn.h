@@ -362,6 +362,15 @@ int hg_gemm_tc_dots(const void* a, int64_t m, int64_t k, int64_t lda, const void
                     int64_t ldb, void* out, int64_t ldo, const void* dot_a, const void* dot_b,
                     int32_t heads, void* dot_out_a, void* dot_out_b, void* stream);
 
+/* The ReLU backward folded into the next layer's dX GEMM (models.relu
+ * backward, models.py:176-185, on matmul's dx, 151-153): out = rnd(a @ bt^T)
+ * where mask > 0, else +0 (NaN mask -> 0) -- mask = the ReLU's output, [m, n]
+ * binary16 pitch ldm, read one tile ahead in the epilogue.  n % 16 == 0; the
+ * caller guarantees the dX is that ReLU's only gradient contribution. */
+int hg_gemm_tc_masked(const void* a, int64_t m, int64_t k, int64_t lda, const void* bt, int32_t n,
+                      int64_t ldb, void* out, int64_t ldo, const void* mask, int64_t ldm,
+                      void* stream);
+
 /* matmul backward's weight gradient (models.py:154-155, b._accumulate(mm(a.T,
  * g))): out[m, n] = rnd(sum_k a[k, m] b[k, n]) -- fp32 accumulation, one
  * rounding -- with accumulate != 0: out = rnd(out + that) (Tensor._accumulate,

@@ -69,6 +69,7 @@ SIGNATURES = {
     "hg_gemm_tc": [_P, _I64, _I64, _I64, _P, _I32, _I64, _P, _P, _I32, _P, _I64, _P],
     "hg_gemm_tc_dots": [_P, _I64, _I64, _I64, _P, _I32, _I64, _P, _I64, _P, _P, _I32, _P, _P,
                         _P],
+    "hg_gemm_tc_masked": [_P, _I64, _I64, _I64, _P, _I32, _I64, _P, _I64, _P, _I64, _P],
     "hg_gemm_wgrad_workspace": [_I64, _I64, _I32, _PSZ],
     "hg_gemm_wgrad": [_P, _I64, _I64, _I64, _P, _I32, _I64, _P, _I64, _P, _I32, _P, c_size_t, _P],
     "hg_count_lines_workspace": [_I64, _PSZ],

@@ -178,7 +178,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
           const __grid_constant__ CUtensorMap map_o, int64_t m, int num_kb, const __half* __restrict__ bias,
           const __half* __restrict__ row_scale, __half* __restrict__ out, int64_t ldo, int relu,
           int n_out, const __half* __restrict__ dot_a, const __half* __restrict__ dot_b,
-          int dot_heads, int dot_fh, __half* __restrict__ dot_out_a, __half* __restrict__ dot_out_b) {
+          int dot_heads, int dot_fh, __half* __restrict__ dot_out_a, __half* __restrict__ dot_out_b,
+          const __half* __restrict__ mask, int64_t ldm) {
   using C = TcCfg<N, RESB>;
   constexpr int S = C::kStages;
   constexpr int kEpiThreads = 32 * kEpiWarps;
@@ -304,6 +305,21 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
       myhd[k] = 2 * (k / G) + half;
       if (k % G == G - 1 || k == kPer - 1) last |= 1u << k;
     }
+    // ReLU backward folded in (mask != NULL): out = mask > 0 ? out : +0, the
+    // mask chunks of this thread's columns loaded one tile ahead into registers
+    uint4 ym[kPer][2];
+    auto load_mask = [&](int64_t t) {
+      const int64_t mr = t * kTcBM + r;
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        const bool ok = mask && t < num_tiles && mr < m && (kChunks % 2 == 0 || mych[k] < kChunks);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh)
+          ym[k][hh] = ok ? __ldg(reinterpret_cast<const uint4*>(mask + mr * ldm + mych[k] * 16 + hh * 8))
+                         : make_uint4(0, 0, 0, 0);
+      }
+    };
+    if (mask) load_mask(blockIdx.x);
     uint32_t tc = 0;
     for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tc) {
       const uint32_t a = tc & 1;
@@ -371,6 +387,15 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
               run_l = run_r = make_float2(0.0f, 0.0f);
             }
           }
+          if (mask) {  // relu backward: y > 0 ? g : +0 (NaN y -> 0), y = this chunk's mask
+            const __half2* y2 = reinterpret_cast<const __half2*>(&ym[k0 + u][0]);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const unsigned mk = __hgt2_mask(y2[j], z2);
+              h[j] = __halves2half2(__ushort_as_half((unsigned short)(__half_as_ushort(__low2half(h[j])) & mk)),
+                                    __ushort_as_half((unsigned short)(__half_as_ushort(__high2half(h[j])) & (mk >> 16))));
+            }
+          }
           if (relu) {  // models.relu: x > 0 ? x : +0 (NaN -> 0)
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
@@ -395,6 +420,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUt
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&tempty[a]);  // accumulator drained: the MMA warp may reuse it
+      if (mask) load_mask(tile + gridDim.x);  // in flight over the store and the next MMA
       if (tstore) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> TMA
         epi_bar_n(kEpiThreads);
@@ -468,12 +494,14 @@ static bool make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t co
   return make_map_box(map, ptr, rows, cols, ld, (uint32_t)kTcBK, box_rows);
 }
 
-struct Dots {  // GAT head dots fused into the epilogue (NULL out_a: off)
+struct Dots {  // epilogue extras: GAT head dots (NULL out_a: off), ReLU-backward mask (NULL: off)
   const void* a;
   const void* b;
   int heads, fh;
   void* out_a;
   void* out_b;
+  const void* mask;
+  int64_t ldm;
 };
 
 template <int N, bool RESB>
@@ -494,7 +522,7 @@ static int launch_gemm_tc_v(const CUtensorMap& ma, const CUtensorMap& mb, const 
   k_gemm_tc<N, RESB><<<grid, kTcThreads, smem, st>>>(
       ma, mb, mo, m, num_kb, (const __half*)bias, (const __half*)row_scale, (__half*)out, ldo, relu,
       n_out, (const __half*)dt.a, (const __half*)dt.b, dt.heads, dt.fh, (__half*)dt.out_a,
-      (__half*)dt.out_b);
+      (__half*)dt.out_b, (const __half*)dt.mask, dt.ldm);
   HG_LAUNCHED();
   return HG_OK;
 }
@@ -844,7 +872,17 @@ extern "C" int hg_gemm_tc_dots(const void* a, int64_t m, int64_t k, int64_t lda,
                  ((reinterpret_cast<uintptr_t>(dot_a) | reinterpret_cast<uintptr_t>(dot_b)) & 3) == 0,
              "hg_gemm_tc_dots: null or misaligned head vectors / outputs");
   return gemm_tc_impl(a, m, k, lda, bt, n, ldb, nullptr, nullptr, 0, out, ldo, stream,
-                      Dots{dot_a, dot_b, heads, n / heads, dot_out_a, dot_out_b});
+                      Dots{dot_a, dot_b, heads, n / heads, dot_out_a, dot_out_b, nullptr, 0});
+}
+
+extern "C" int hg_gemm_tc_masked(const void* a, int64_t m, int64_t k, int64_t lda, const void* bt,
+                                 int32_t n, int64_t ldb, void* out, int64_t ldo, const void* mask,
+                                 int64_t ldm, void* stream) {
+  HG_REQUIRE(mask && ldm >= n && ldm % 8 == 0 && (reinterpret_cast<uintptr_t>(mask) & 15) == 0 &&
+                 n % 16 == 0,
+             "hg_gemm_tc_masked: the mask must be [m, n] binary16, 16-byte aligned rows, n %% 16 == 0");
+  return gemm_tc_impl(a, m, k, lda, bt, n, ldb, nullptr, nullptr, 0, out, ldo, stream,
+                      Dots{nullptr, nullptr, 1, 16, nullptr, nullptr, mask, ldm});
 }
 
 static int gemm_tc_impl(const void* a, int64_t m, int64_t k, int64_t lda, const void* bt,

@@ -1071,6 +1071,32 @@ def gemm_tc_dots(a, bt, a_l, a_r, heads):
     return out, s_l, s_r
 
 
+def gemm_tc_masked(a, bt, mask):
+    """The ReLU backward folded into dX: y = rnd(a @ bt.T) where mask > 0,
+    else +0 (relu_grad(mask, a @ bt.T), models.py:176-185) on the tcgen05
+    tensor cores (hg_gemm_tc_masked): a [M, K], bt [N, K], mask [M, N] fp16,
+    N a multiple of 16."""
+    _require_cuda(a, bt)
+    if a.dtype != torch.float16 or bt.dtype != torch.float16 or mask.dtype != torch.float16:
+        raise ValueError("hg_gemm_tc_masked takes binary16 operands")
+    a, bt = a.contiguous(), bt.contiguous()
+    if a.data_ptr() % 16:
+        a = a.clone()
+    if bt.data_ptr() % 16:
+        bt = bt.clone()
+    m, k = a.shape
+    n, k2 = bt.shape
+    if k2 != k or mask.shape != (m, n):
+        raise ValueError("shapes: a [M, K], bt [N, K], mask [M, N]")
+    if mask.stride(1) != 1 or mask.stride(0) % 8 or mask.data_ptr() % 16:
+        mask = mask.contiguous().clone()
+    out = torch.empty((m, n), dtype=torch.float16, device=a.device)
+    nat.call("hg_gemm_tc_masked", _p(a), m, k, a.stride(0), _p(bt), n, bt.stride(0), _p(out),
+             out.stride(0), _p(mask), mask.stride(0), _stream())
+    Probe.launches += 1
+    return out
+
+
 def gemm_wgrad(a, b, out=None, bias_out=None, accumulate=False, bias=False):
     """rnd(a.T @ b) -- fp32 accumulation, one rounding -- on the tcgen05 tensor
     cores with the vertex dimension split across the SMs (hg_gemm_wgrad):

@@ -876,7 +876,10 @@ class GATLayer:
 
     fuses_relu_out = True
 
-    def __call__(self, bundle, x, mode, width, overflow, tag, relu_out=False):
+    def __call__(self, bundle, x, mode, width, overflow, tag, relu_out=False, link_out=None,
+                 link_in=None):
+        """link_out / link_in (_ReluLink, Model.forward): this layer's fused
+        ReLU output feeds only the next layer / x is such an output."""
         h, so = self.heads, self.store_out
         w = self.w.publish(mode)
         a_l, a_r = self.a_l.publish(mode), self.a_r.publish(mode)
@@ -884,11 +887,13 @@ class GATLayer:
         if (overflow is None and isinstance(bundle, GraphBundle) and bundle.fused_gat):
             fuse = relu_out and not mean
             if _dots_shapes(x, w, h) and a_l.dtype == torch.float16:
-                z, s_l, s_r = _GATProjFn.apply(x, w, a_l, a_r, h)      # [N, H*so], [N, H] x 2
-                out = _GATCoreFn.apply(z, a_l, a_r, bundle, h, fuse, s_l, s_r)
+                z, s_l, s_r = _GATProjFn.apply(x, w, a_l, a_r, h, link_in)  # [N, H*so], [N, H] x 2
+                out = _GATCoreFn.apply(z, a_l, a_r, bundle, h, fuse, s_l, s_r,
+                                       link_out if fuse else None)
             else:
                 z = matmul(x, w)                                      # [N, H*so]
-                out = _GATCoreFn.apply(z, a_l, a_r, bundle, h, fuse)
+                out = _GATCoreFn.apply(z, a_l, a_r, bundle, h, fuse, None, None,
+                                       link_out if fuse else None)
             if mean:
                 out = _HeadMeanFn.apply(out, h)
             return relu(out) if relu_out and not fuse else out
@@ -943,6 +948,22 @@ def _dots_shapes(x, w, heads):
             and fh % 16 == 0 and (heads % 2 == 0 or fh == 16))
 
 
+class _ReluLink:
+    """Between a layer whose epilogue applied the inter-layer ReLU and the
+    next layer, its ReLU output's only consumer (Model.forward): set when the
+    consumer's dX GEMM already masked the gradient (hg_gemm_tc_masked), so the
+    producer skips its relu_grad pass."""
+    __slots__ = ("premasked",)
+
+    def __init__(self):
+        self.premasked = False
+
+
+# The ReLU backward folded into the next GAT layer's dX GEMM (hg_gemm_tc_masked)
+# instead of a relu_grad pass; HG_FUSED_RELU_BWD=0: the separate pass.
+FUSED_RELU_BWD = os.environ.get("HG_FUSED_RELU_BWD", "1") != "0"
+
+
 class _GATProjFn(torch.autograd.Function):
     """z = x W with the head dots s_l = z_h . a_l[h], s_r = z_h . a_r[h]
     (GATLayer, models.py:492-509) from one tcgen05 GEMM whose epilogue forms the
@@ -951,9 +972,9 @@ class _GATProjFn(torch.autograd.Function):
     dx = dz W^T (hg_gemm_tc) and dW = x^T dz (hg_gemm_wgrad)."""
 
     @staticmethod
-    def forward(ctx, x, w, a_l, a_r, heads):
+    def forward(ctx, x, w, a_l, a_r, heads, link=None):
         ctx.set_materialize_grads(False)
-        ctx.w_leaf, ctx.heads = w, heads
+        ctx.w_leaf, ctx.heads, ctx.link = w, heads, link
         z, s_l, s_r = D.gemm_tc_dots(x, _wt(w), a_l, a_r, heads)
         ctx.save_for_backward(x, w, z, a_l, a_r)
         return z, s_l, s_r
@@ -966,9 +987,17 @@ class _GATProjFn(torch.autograd.Function):
         if ds_l is not None:  # (None: the consumer folded the head-dot backward in)
             gz, ga_l, ga_r = D.head_dots_bwd(z, a_l, a_r, ds_l.contiguous(), ds_r.contiguous(),
                                              ctx.heads, gz_acc=gz)
-        gx = D.gemm_tc(gz, w) if ctx.needs_input_grad[0] else None
+        gx = None
+        if ctx.needs_input_grad[0]:
+            if ctx.link is not None and FUSED_RELU_BWD and x.shape[1] % 16 == 0:
+                # x is the previous layer's ReLU output, consumed only here:
+                # mask dX by x > 0 in the GEMM epilogue (the ReLU's backward)
+                gx = D.gemm_tc_masked(gz, w, x)
+                ctx.link.premasked = True
+            else:
+                gx = D.gemm_tc(gz, w)
         gw = _weight_grads(x, gz, ctx.w_leaf)[0] if ctx.needs_input_grad[1] else None
-        return gx, gw, ga_l, ga_r, None
+        return gx, gw, ga_l, ga_r, None, None
 
 
 class _GATCoreFn(torch.autograd.Function):
@@ -981,7 +1010,7 @@ class _GATCoreFn(torch.autograd.Function):
     (no separate add of the two N x H*F gradients)."""
 
     @staticmethod
-    def forward(ctx, z, a_l, a_r, bundle, heads, relu, s_l=None, s_r=None):
+    def forward(ctx, z, a_l, a_r, bundle, heads, relu, s_l=None, s_r=None, link=None):
         # s_l / s_r given: formed by the projection (_GATProjFn), whose backward
         # takes their gradients and the head-dot backward
         ctx.dots_in = s_l is not None
@@ -996,7 +1025,7 @@ class _GATCoreFn(torch.autograd.Function):
         else:
             alpha = D.gat_attention_fwd(view, s_l, s_r, 0.2)
             out = D.spmm_csr(view, z, alpha, None, heads, "post", relu=relu)
-        ctx.bundle, ctx.heads, ctx.relu = bundle, heads, relu
+        ctx.bundle, ctx.heads, ctx.relu, ctx.link = bundle, heads, relu, link
         ctx.save_for_backward(z, a_l, a_r, s_l, s_r, alpha, out if relu else None)
         return out
 
@@ -1005,7 +1034,7 @@ class _GATCoreFn(torch.autograd.Function):
         z, a_l, a_r, s_l, s_r, alpha, y = ctx.saved_tensors
         b, h = ctx.bundle, ctx.heads
         g = g.contiguous()
-        if ctx.relu:
+        if ctx.relu and not (ctx.link is not None and ctx.link.premasked):
             g = D.relu_grad(y, g)
         dalpha = b.sddmm(g, z, heads=h).reshape(-1, h)
         bwd = b.dg.view(True)
@@ -1021,12 +1050,12 @@ class _GATCoreFn(torch.autograd.Function):
             gz = D.spmm_csr(bwd, g, alpha, bwd.perm, h, "post",
                             head_dots=(ds_l, ds_r, a_l, a_r))
             _, ga_l, ga_r = D.head_dots_bwd(z, a_l, a_r, ds_l, ds_r, h, dz=False)
-            return gz, ga_l, ga_r, None, None, None, None, None
+            return gz, ga_l, ga_r, None, None, None, None, None, None
         gz = D.spmm_csr(bwd, g, alpha, bwd.perm, h, "post")
         if ctx.dots_in:
-            return gz, None, None, None, None, None, ds_l, ds_r
+            return gz, None, None, None, None, None, ds_l, ds_r, None
         gz, ga_l, ga_r = D.head_dots_bwd(z, a_l, a_r, ds_l, ds_r, h, gz_acc=gz)
-        return gz, ga_l, ga_r, None, None, None, None, None
+        return gz, ga_l, ga_r, None, None, None, None, None, None
 
 
 class _HeadDotsFn(torch.autograd.Function):
@@ -1112,13 +1141,20 @@ class Model:
 
     def forward(self, bundle, x, mode, width="half2", overflow=None):
         h = x
+        link = None   # the previous GAT layer's fused ReLU output, consumed only by this layer
         for i, layer in enumerate(self.layers):
             inner = i + 1 < len(self.layers)
+            gat = isinstance(layer, GATLayer)
+            kw = {"link_in": link} if gat and link is not None else {}
+            link = None
             if inner and getattr(layer, "fuses_relu_out", False):
                 # the layer applies the inter-layer ReLU in its own epilogue
-                h = layer(bundle, h, mode, width, overflow, f"{self.kind}{i}", relu_out=True)
+                if gat and isinstance(self.layers[i + 1], GATLayer):
+                    link = kw["link_out"] = _ReluLink()
+                h = layer(bundle, h, mode, width, overflow, f"{self.kind}{i}", relu_out=True,
+                          **kw)
                 continue
-            h = layer(bundle, h, mode, width, overflow, f"{self.kind}{i}")
+            h = layer(bundle, h, mode, width, overflow, f"{self.kind}{i}", **kw)
             if inner:
                 h = relu(h)
         return h

@@ -1121,6 +1121,24 @@ def test_gemm_tc_dots_vs_f64(cuda, m, k, heads, fh):
         D.gemm_tc_dots(a, bt.new_zeros(96, k), al.new_zeros(96), ar.new_zeros(96), 3)
 
 
+@pytest.mark.parametrize("m,k,n", [(1, 16, 16), (300, 64, 128), (5000, 128, 64), (1031, 48, 256)])
+def test_gemm_tc_masked_bitwise(cuda, m, k, n):
+    """hg_gemm_tc_masked == relu_grad(mask, hg_gemm_tc(...)) bit for bit: the
+    ReLU backward folded into the dX epilogue (+0 where mask <= 0 or NaN)."""
+    from paper_2411_01109_b200 import device as D
+
+    rng = np.random.default_rng(m + n)
+    a = _t(rng.normal(0, 1, (m, k)).astype(np.float16), cuda)
+    bt = _t(rng.normal(0, 0.2, (n, k)).astype(np.float16), cuda)
+    y = rng.normal(0, 1, (m, n)).astype(np.float16)
+    y[rng.random((m, n)) < 0.05] = 0.0
+    y[rng.random((m, n)) < 0.01] = np.nan
+    y = _t(y, cuda)
+    want = D.relu_grad(y, D.gemm_tc(a, bt))
+    got = D.gemm_tc_masked(a, bt, y)
+    assert torch.equal(got.view(torch.int16), want.view(torch.int16))
+
+
 def test_gemm_tc_from_autograd_worker_thread(cuda):
     """hg_gemm_tc encodes its TMA descriptors through the driver API; it must
     work from autograd's backward worker thread (no context bound there)."""

@@ -645,6 +645,33 @@ def test_gat_head_dot_folds_bitwise(cuda, fh):
         assert torch.equal(a.view(torch.int16), c.view(torch.int16))
 
 
+@pytest.mark.parametrize("hidden,layers", [(16, 2), (16, 3), (8, 3)])
+def test_gat_relu_backward_fold_bitwise(cuda, hidden, layers):
+    """The inter-layer ReLU's backward folded into the next GAT layer's dX GEMM
+    (hg_gemm_tc_masked, relu_grad skipped by the producer) trains bit for bit
+    like the separate relu_grad pass: losses and every parameter."""
+    from paper_2411_01109_b200 import graphgen, models as M
+    from paper_2411_01109_b200.device import DeviceGraph
+
+    rows, cols, feats, labels = graphgen.synth_sbm(3000, 4, 0.01, 0.001, 32, 9)
+    dg = DeviceGraph.from_edges(3000, rows, cols)
+    runs = []
+    saved = M.FUSED_RELU_BWD
+    try:
+        for fold in (False, True):
+            M.FUSED_RELU_BWD = fold
+            tr = M.Trainer(M.GraphBundle.build(dg), feats, labels,
+                           M.TrainConfig(kind="gat", hidden=hidden, heads=4, layers=layers,
+                                         epochs=3, seed=3))
+            losses = [float(tr.step()[0]) for _ in range(3)]
+            runs.append((losses, [p.master.clone() for p in tr.model.params()]))
+    finally:
+        M.FUSED_RELU_BWD = saved
+    assert runs[0][0] == runs[1][0]
+    for p0, p1 in zip(runs[0][1], runs[1][1]):
+        assert torch.equal(p0, p1)
+
+
 @pytest.mark.parametrize("fh", [8, 16])
 def test_gat_core_fused_matches_composed(cuda, fh):
     """The single-node GAT core (_GATCoreFn, ReLU fused) against the composed
