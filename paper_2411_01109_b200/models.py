@@ -745,12 +745,16 @@ class Linear:
     def params(self):
         return [self.w] + ([self.b] if self.b is not None else [])
 
-    def __call__(self, x, mode, tc=False, relu_out=False):
+    def __call__(self, x, mode, tc=False, relu_out=False, link_out=None, link_in=None):
         """tc: run on the tcgen05 GEMM with the bias (and, with relu_out, the
-        following ReLU) fused into its epilogue when the shapes allow."""
+        following ReLU) fused into its epilogue when the shapes allow.
+        link_out / link_in (_ReluLink): this call's ReLU output feeds only the
+        next Linear / x is such an output (the ReLU backward then runs in the
+        consumer's dX GEMM)."""
         w = self.w.publish(mode)
         if tc and mode == "half" and self.b is not None and _tc_shapes(x, w):
-            return _LinearTCFn.apply(x, w, self.b.publish(mode), relu_out)
+            return _LinearTCFn.apply(x, w, self.b.publish(mode), relu_out,
+                                     link_out if relu_out else None, link_in)
         out = matmul(x, w)
         if self.b is not None:
             out = add_bias(out, self.b.publish(mode))
@@ -765,9 +769,10 @@ class _LinearTCFn(torch.autograd.Function):
     output (y > 0 iff pre-activation > 0)."""
 
     @staticmethod
-    def forward(ctx, x, w, b, relu_out):
+    def forward(ctx, x, w, b, relu_out, link_out=None, link_in=None):
         y = D.gemm_tc(x, _wt(w), b, None, relu=relu_out)
         ctx.relu_out = relu_out
+        ctx.links = (link_out, link_in)
         ctx.leaves = (w, b)
         ctx.save_for_backward(x, w, y if relu_out else None)
         return y
@@ -775,13 +780,20 @@ class _LinearTCFn(torch.autograd.Function):
     @staticmethod
     def backward(ctx, g):
         x, w, y = ctx.saved_tensors
+        link_out, link_in = ctx.links
         g = g.contiguous()
-        if ctx.relu_out:
+        if ctx.relu_out and not (link_out is not None and link_out.premasked):
             g = D.relu_grad(y, g)
         # dx = g W^T: W is already the [K, N] "B transposed" operand of hg_gemm_tc
-        gx = D.gemm_tc(g, w) if ctx.needs_input_grad[0] else None
+        gx = None
+        if ctx.needs_input_grad[0]:
+            if link_in is not None and FUSED_RELU_BWD and x.shape[1] % 16 == 0:
+                gx = D.gemm_tc_masked(g, w, x)   # x > 0: the producer's ReLU backward
+                link_in.premasked = True
+            else:
+                gx = D.gemm_tc(g, w)
         gw, gb = _weight_grads(x, g, *ctx.leaves)
-        return gx, gw, gb, None
+        return gx, gw, gb, None, None, None
 
 
 class GCNLayer:
@@ -843,8 +855,9 @@ class GINLayer:
             agg = spmm_agg(bundle, x, self.reduction, width, overflow, tag)
             mixed = scale_combine(x, agg, ope, self.lam)
         tc = getattr(bundle, "fused_bias_agg", False)
-        return self.phi2(self.phi1(mixed, mode, tc=tc, relu_out=True), mode, tc=tc,
-                         relu_out=relu_out)
+        link = _ReluLink()   # phi1's ReLU output is consumed by phi2 alone
+        return self.phi2(self.phi1(mixed, mode, tc=tc, relu_out=True, link_out=link), mode,
+                         tc=tc, relu_out=relu_out, link_in=link)
 
 
 class GATLayer:

@@ -645,11 +645,13 @@ def test_gat_head_dot_folds_bitwise(cuda, fh):
         assert torch.equal(a.view(torch.int16), c.view(torch.int16))
 
 
-@pytest.mark.parametrize("hidden,layers", [(16, 2), (16, 3), (8, 3)])
-def test_gat_relu_backward_fold_bitwise(cuda, hidden, layers):
-    """The inter-layer ReLU's backward folded into the next GAT layer's dX GEMM
-    (hg_gemm_tc_masked, relu_grad skipped by the producer) trains bit for bit
-    like the separate relu_grad pass: losses and every parameter."""
+@pytest.mark.parametrize("kind,hidden,layers", [("gat", 16, 2), ("gat", 16, 3), ("gat", 8, 3),
+                                                ("gin", 32, 2), ("gin", 16, 3)])
+def test_relu_backward_fold_bitwise(cuda, kind, hidden, layers):
+    """A ReLU's backward folded into its only consumer's dX GEMM
+    (hg_gemm_tc_masked, relu_grad skipped by the producer: between GAT layers,
+    and between GIN's two MLP linears) trains bit for bit like the separate
+    relu_grad pass: losses and every parameter."""
     from paper_2411_01109_b200 import graphgen, models as M
     from paper_2411_01109_b200.device import DeviceGraph
 
@@ -661,8 +663,8 @@ def test_gat_relu_backward_fold_bitwise(cuda, hidden, layers):
         for fold in (False, True):
             M.FUSED_RELU_BWD = fold
             tr = M.Trainer(M.GraphBundle.build(dg), feats, labels,
-                           M.TrainConfig(kind="gat", hidden=hidden, heads=4, layers=layers,
-                                         epochs=3, seed=3))
+                           M.TrainConfig(kind=kind, hidden=hidden, layers=layers, epochs=3,
+                                         seed=3, **({"heads": 4} if kind == "gat" else {})))
             losses = [float(tr.step()[0]) for _ in range(3)]
             runs.append((losses, [p.master.clone() for p in tr.model.params()]))
     finally:
