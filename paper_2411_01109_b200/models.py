@@ -289,8 +289,9 @@ class _GCNLayerFn(torch.autograd.Function):
     accumulation, one rounding (matmul's backward, 150-155)."""
 
     @staticmethod
-    def forward(ctx, x, w, b, bundle, reduction, relu=False):
+    def forward(ctx, x, w, b, bundle, reduction, relu=False, link_out=None, link_in=None):
         ctx.bundle, ctx.reduction, ctx.relu = bundle, reduction, relu
+        ctx.links = (link_out, link_in)
         ctx.leaves = (w, b)
         y = bundle.gcn_agg_tc(x, w, b, reduction, relu=True) if relu else \
             bundle.gcn_agg_tc(x, w, b, reduction)
@@ -301,13 +302,20 @@ class _GCNLayerFn(torch.autograd.Function):
     def backward(ctx, g):
         x, w, y = ctx.saved_tensors
         r = ctx.reduction
+        link_out, link_in = ctx.links
         g = g.contiguous()
-        if ctx.relu:
+        if ctx.relu and not (link_out is not None and link_out.premasked):
             g = D.relu_grad(y, g)
         gh = ctx.bundle.spmm(g, None, r.scaling, _MIRROR[r.norm], transpose=True)
-        gx = D.gemm_tc(gh, w) if ctx.needs_input_grad[0] else None
+        gx = None
+        if ctx.needs_input_grad[0]:
+            if link_in is not None and FUSED_RELU_BWD and x.shape[1] % 16 == 0:
+                gx = D.gemm_tc_masked(gh, w, x)   # x > 0: the previous layer's ReLU backward
+                link_in.premasked = True
+            else:
+                gx = D.gemm_tc(gh, w)
         gw, gb = _weight_grads(x, gh, *ctx.leaves)
-        return gx, gw, gb, None, None, None
+        return gx, gw, gb, None, None, None, None, None
 
 
 def spmm_agg(bundle, x, reduction, width="half2", overflow=None, tag="agg"):
@@ -808,15 +816,20 @@ class GCNLayer:
         return self.lin.params()
 
     fuses_relu_out = True
+    takes_relu_link = True
 
-    def __call__(self, bundle, x, mode, width, overflow, tag, relu_out=False):
+    def __call__(self, bundle, x, mode, width, overflow, tag, relu_out=False, link_out=None,
+                 link_in=None):
+        """link_out / link_in (_ReluLink, Model.forward): this layer's fused
+        ReLU output feeds only the next layer / x is such an output."""
         # fused ReLU only when no overflow counters watch the pre-activation
         fuse = relu_out and overflow is None and getattr(bundle, "fused_relu", False)
         if getattr(bundle, "fused_bias_agg", False) and self.lin.b is not None:
             w, b = self.lin.w.publish(mode), self.lin.b.publish(mode)
             if mode == "half" and _tc_shapes(x, w):
                 # tensor-core GEMM with the bias / input-scale epilogue fused
-                y = _GCNLayerFn.apply(x, w, b, bundle, self.reduction, fuse)
+                y = _GCNLayerFn.apply(x, w, b, bundle, self.reduction, fuse,
+                                      link_out if fuse else None, link_in)
             else:
                 y = _BiasAggFn.apply(matmul(x, w), b, bundle, self.reduction, fuse)
             if overflow is not None:
@@ -888,6 +901,7 @@ class GATLayer:
         return [self.w, self.a_l, self.a_r]
 
     fuses_relu_out = True
+    takes_relu_link = True
 
     def __call__(self, bundle, x, mode, width, overflow, tag, relu_out=False, link_out=None,
                  link_in=None):
@@ -1157,12 +1171,12 @@ class Model:
         link = None   # the previous GAT layer's fused ReLU output, consumed only by this layer
         for i, layer in enumerate(self.layers):
             inner = i + 1 < len(self.layers)
-            gat = isinstance(layer, GATLayer)
-            kw = {"link_in": link} if gat and link is not None else {}
+            linked = getattr(layer, "takes_relu_link", False)
+            kw = {"link_in": link} if linked and link is not None else {}
             link = None
             if inner and getattr(layer, "fuses_relu_out", False):
                 # the layer applies the inter-layer ReLU in its own epilogue
-                if gat and isinstance(self.layers[i + 1], GATLayer):
+                if linked and getattr(self.layers[i + 1], "takes_relu_link", False):
                     link = kw["link_out"] = _ReluLink()
                 h = layer(bundle, h, mode, width, overflow, f"{self.kind}{i}", relu_out=True,
                           **kw)

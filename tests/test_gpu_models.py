@@ -646,12 +646,13 @@ def test_gat_head_dot_folds_bitwise(cuda, fh):
 
 
 @pytest.mark.parametrize("kind,hidden,layers", [("gat", 16, 2), ("gat", 16, 3), ("gat", 8, 3),
-                                                ("gin", 32, 2), ("gin", 16, 3)])
+                                                ("gin", 32, 2), ("gin", 16, 3),
+                                                ("gcn", 16, 2), ("gcn", 64, 3)])
 def test_relu_backward_fold_bitwise(cuda, kind, hidden, layers):
     """A ReLU's backward folded into its only consumer's dX GEMM
     (hg_gemm_tc_masked, relu_grad skipped by the producer: between GAT layers,
-    and between GIN's two MLP linears) trains bit for bit like the separate
-    relu_grad pass: losses and every parameter."""
+    between GCN layers, and between GIN's two MLP linears) trains bit for bit
+    like the separate relu_grad pass: losses and every parameter."""
     from paper_2411_01109_b200 import graphgen, models as M
     from paper_2411_01109_b200.device import DeviceGraph
 
