@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -569,14 +570,17 @@ def b200_arm(args, ws, rank, local):
         tr.run_epochs(host_x, min(2, args.warmup))
     barrier()
     torch.cuda.synchronize()
+    # wall-clock e2e: at least ~0.25 s of steps so sub-millisecond epochs are
+    # not one host hiccup away from a different number (same on every rank)
+    e2e_steps = max(args.steps, min(500, int(math.ceil(250.0 / max(t_ms, 1e-3)))))
     e0 = time.perf_counter()
     if use_dist:
-        dist_feed(args.steps)
+        dist_feed(e2e_steps)
     else:
-        tr.run_epochs(host_x, args.steps)
+        tr.run_epochs(host_x, e2e_steps)
     torch.cuda.synchronize()
     barrier()
-    e2e_ms = (time.perf_counter() - e0) * 1e3 / args.steps
+    e2e_ms = (time.perf_counter() - e0) * 1e3 / e2e_steps
     if dist is not None:
         e2e_ms = max_over_ranks(dist, e2e_ms)
 
@@ -607,7 +611,7 @@ def b200_arm(args, ws, rank, local):
                                          else "as generated")),
             "clocks": clocks.summary(),
             "e2e": {"value": round(e2e_ms, 4), "unit": "ms/epoch", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": 4 * ws},
+                    "d2h_bytes_per_step": 4 * ws, "steps": e2e_steps},
             "gpu_launches": int(launches),
             "ms_per_step_eager": round(eager_ms, 4), "cuda_graph": graphed,
             "roofline": {"bound": "hbm", "achieved": round(achieved / 1e9, 1),
